@@ -1,0 +1,268 @@
+/*
+ * hfta.h -- C ABI of libhfta, the B200 (sm_100a) hot path of HFTA
+ * ("Horizontally Fused Training Array", arXiv 2102.02344).
+ *
+ * One horizontally fused training step of B same-architecture models that
+ * differ only in hyper-parameters (paper §3).  Every call below
+ * runs ONE set of kernel launches for all B models ("the horizontal fusion of
+ * many ... operators"); the model index b is folded into the
+ * launch grid / tile scheduler.  Citations: P:Lnnn = PAPER.md line nnn.
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions (apply to every entry point)
+ * ---------------------------------------------------------------------------
+ * Layout.  Model-major: element (b, i, j) of a per-model matrix lives at
+ *   ptr[b*bstride + i*ld + j]  (elements, not bytes).
+ *   This replaces the paper's channel-folded [N, B*C, ...] layout (App. B,
+ *   P:L1262-1293); the two are a bijection.  bstride == 0 on an INPUT means
+ *   "shared by all models" (the same data batch, reading R5).  Outputs must
+ *   have bstride > 0 (or B == 1) and must not alias inputs.
+ * Dtype.  HFTA_F32: every activation/operand is fp32 and contractions are
+ *   fp32-accurate.  HFTA_BF16 (bf16-AMP, reading R16): activations and GEMM
+ *   operands are bf16, accumulation fp32; weight gradients, BN statistics,
+ *   BN affine parameters, biases, losses and optimizer state are always fp32.
+ * Ownership.  The caller owns every buffer (allocated with cudaMalloc or by
+ *   PyTorch).  The library never allocates device memory, never frees, and
+ *   keeps no pointer beyond the stream-ordered completion of the call.
+ *   Scratch memory is passed as (ws, ws_bytes); query the size first with the
+ *   matching *_workspace() function.
+ * Streams.  `stream` is a cudaStream_t (NULL = legacy default stream).  All
+ *   calls only enqueue work and return; hyper-parameter vectors and the step
+ *   counter are DEVICE arrays so a whole step can be captured in a CUDA graph.
+ * Errors.  Arguments are validated before anything is enqueued; on error
+ *   nothing is launched and a status != HFTA_OK is returned;
+ *   hfta_last_error() (thread-local) names the argument and shapes.  Kernel
+ *   faults surface asynchronously; with env HFTA_SYNC=1 every call
+ *   synchronizes its stream and reports HFTA_ERR_CUDA.
+ * Device.  hfta_init() must succeed first; it requires compute capability
+ *   10.0 (B200, sm_100a).  There is no fallback for any other device and no
+ *   CPU path.
+ * Determinism.  For fixed inputs all outputs are bitwise reproducible
+ *   (fixed-order reductions, no floating-point atomics).
+ */
+#ifndef HFTA_H_
+#define HFTA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int hfta_status;
+enum {
+  HFTA_OK = 0,
+  HFTA_ERR_INVALID_VALUE = 1, /* null required pointer, B < 1, bad scalar   */
+  HFTA_ERR_SHAPE = 2,         /* inconsistent dims/strides                   */
+  HFTA_ERR_ALIGNMENT = 3,     /* pointer/stride not aligned as required      */
+  HFTA_ERR_UNSUPPORTED = 4,   /* dtype / configuration not implemented       */
+  HFTA_ERR_ARCH = 5,          /* device is not compute capability 10.0       */
+  HFTA_ERR_WORKSPACE = 6,     /* ws too small                                */
+  HFTA_ERR_CUDA = 7,          /* CUDA launch error (message has the string)  */
+  HFTA_ERR_NOT_INITIALIZED = 8
+};
+
+typedef enum { HFTA_F32 = 0, HFTA_BF16 = 1 } hfta_dtype;
+typedef enum { HFTA_ACT_NONE = 0, HFTA_ACT_RELU = 1, HFTA_ACT_LEAKY_RELU = 2 } hfta_act;
+
+typedef struct { const void* ptr; int64_t bstride; int64_t ld; } hfta_in;
+typedef struct { void* ptr; int64_t bstride; int64_t ld; } hfta_out;
+typedef void* hfta_stream; /* cudaStream_t */
+
+/* ---------------------------------------------------------------- setup -- */
+
+/* Select `device`, check CC 10.0, cache SM count.  HFTA_ERR_ARCH otherwise. */
+hfta_status hfta_init(int device);
+/* Thread-local message of the last failing call ("" if none). */
+const char* hfta_last_error(void);
+/* Library version string. */
+const char* hfta_version(void);
+/* Number of kernels this library launched (process-wide counter). */
+uint64_t hfta_launch_count(void);
+
+/* ------------------------------------------------ fused Linear / Conv1d -- */
+/*
+ * Fused Linear and Conv1d(kernel=1): App. B rows "Linear -> baddbmm"
+ * and "Conv1d", grouped with G = B.
+ * For each b in [0, B):
+ *   Y_b[M,N] = X_b[M,K] * W_b[N,K]^T + bias_b       (Linear, PyTorch [out,in])
+ * X: [B][M][K] (bstride 0 = shared input), W: [B][N][K], Y: [B][M][N],
+ * all of dtype dt; bias fp32 or NULL.  The bias is a 2-D table:
+ *   bias element for (b, m, n) = bias[b*bias_bstride + (m / bias_row_div)*bias_ld + n]
+ * (bias_row_div = 0 or bias_ld = 0 means a plain per-model [N] bias).  The
+ * row-grouped form is the exact split-weight rewrite of PointNet-seg's
+ * concat(global, point) layer.
+ * Alignment: for the tensor-core path, X/W/Y pointers 16-B aligned and
+ * ld*sizeof(dt), bstride*sizeof(dt) multiples of 16; other shapes run a SIMT
+ * kernel (no alignment requirement).  M, N, K >= 1.
+ */
+hfta_status hfta_fused_linear_fwd(int B, int64_t M, int64_t N, int64_t K, hfta_dtype dt,
+                                  hfta_in X, hfta_in W,
+                                  const float* bias, int64_t bias_bstride, int64_t bias_ld,
+                                  int64_t bias_row_div, hfta_out Y, hfta_stream stream);
+
+/* Scratch bytes for hfta_fused_linear_bwd with these sizes. */
+size_t hfta_fused_linear_bwd_workspace(int B, int64_t M, int64_t N, int64_t K, hfta_dtype dt);
+
+/*
+ * Backward of hfta_fused_linear_fwd (same dims).  For each b:
+ *   dX_b[M,K] = dY_b[M,N] * W_b[N,K]           (dX.ptr == NULL: skipped)
+ *   dW_b[N,K] (+)= dY_b^T * X_b   fp32, [B][N][K] at dW + b*dW_bstride, ld K
+ *   dbias_b[N] (+)= sum_m dY_b[m,:]   fp32 (dbias == NULL: skipped)
+ * accumulate != 0 adds into dW/dbias instead of overwriting (D(real)+D(fake)
+ * accumulation of the DCGAN step).  The reduction over M is split in a fixed
+ * number of chunks reduced in fixed order (deterministic).
+ */
+hfta_status hfta_fused_linear_bwd(int B, int64_t M, int64_t N, int64_t K, hfta_dtype dt,
+                                  hfta_in dY, hfta_in X, hfta_in W, hfta_out dX,
+                                  float* dW, int64_t dW_bstride,
+                                  float* dbias, int64_t dbias_bstride, int accumulate,
+                                  void* ws, size_t ws_bytes, hfta_stream stream);
+
+/* ------------------------------------------------------- fused BatchNorm -- */
+/*
+ * Fused BatchNorm1d/2d (App. B rows P:L1274-1278): statistics per (model b,
+ * channel c) over the R rows of model b (reading R13); PyTorch training-mode
+ * semantics (reading R6): biased variance normalises, unbiased variance
+ * (R/(R-1)) enters running_var; running <- (1-momentum)*running + momentum*stat.
+ * X: [B][R][C] dtype dt (R = rows, e.g. N*L points or N*H*W pixels, C contiguous).
+ * gamma, beta: fp32, element (b,c) at gamma[b*gb_bstride + c].
+ * running_mean/var, save_mean/save_invstd: fp32 [B][C] contiguous.
+ * Y = act(gamma * (X - mean) * invstd + beta), act in {none, ReLU,
+ * LeakyReLU(act_alpha)}; Y.ptr == NULL computes statistics only (the max-over-
+ * points path applies BN inside hfta_bn_max_fwd).  running_* may be NULL.
+ * R >= 2.
+ */
+size_t hfta_fused_bn_workspace(int B, int64_t R, int64_t C);
+hfta_status hfta_fused_bn_fwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_in X,
+                              const float* gamma, const float* beta, int64_t gb_bstride,
+                              float* running_mean, float* running_var, float momentum, float eps,
+                              hfta_act act, float act_alpha, hfta_out Y,
+                              float* save_mean, float* save_invstd,
+                              void* ws, size_t ws_bytes, hfta_stream stream);
+/*
+ * Backward: dY is the gradient w.r.t. the activation output; act' is
+ * recomputed from X and the saved statistics.  With z = act input:
+ *   dbeta = sum_r dz, dgamma = sum_r dz*xhat,
+ *   dX = gamma*invstd/R * (R*dz - dbeta - xhat*dgamma).
+ * dgamma/dbeta fp32 at [b*gb_bstride + c] (accumulate != 0 adds).
+ */
+hfta_status hfta_fused_bn_bwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_in dY, hfta_in X,
+                              const float* gamma, const float* beta, int64_t gb_bstride,
+                              const float* save_mean, const float* save_invstd,
+                              hfta_act act, float act_alpha, hfta_out dX,
+                              float* dgamma, float* dbeta, int accumulate,
+                              void* ws, size_t ws_bytes, hfta_stream stream);
+
+/* ------------------------------------------------- PointNet glue (K8) -- */
+/*
+ * BN-apply + activation + max over points, fused (the max-pool of PointNet,
+ * App. B row MaxPool family P:L1286-1287 as used by the cited model):
+ *   out[b][n][c] = max_l act(gamma*(X[b][n*L+l][c]-mean)*invstd + beta)
+ *   argmax[b][n][c] = first l attaining it (reading R15), int32.
+ * X [B][N*L][C] dtype dt; out [B][N][C] dtype dt (ld = out.ld).
+ */
+hfta_status hfta_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C, hfta_dtype dt, hfta_in X,
+                            const float* gamma, const float* beta, int64_t gb_bstride,
+                            const float* save_mean, const float* save_invstd,
+                            hfta_act act, float act_alpha, hfta_out out, int32_t* argmax,
+                            hfta_stream stream);
+/*
+ * Backward of hfta_bn_max_fwd followed by the BN backward: dG [B][N][C]
+ * (dtype dt) is scattered to the argmax rows, passed through act' and BN
+ * backward; writes dX [B][N*L][C] (dtype dt) and dgamma/dbeta.
+ * Workspace: hfta_bn_max_bwd_workspace().
+ */
+size_t hfta_bn_max_bwd_workspace(int B, int64_t N, int64_t C);
+hfta_status hfta_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C, hfta_dtype dt,
+                            hfta_in dG, hfta_in X, const int32_t* argmax,
+                            const float* gamma, const float* beta, int64_t gb_bstride,
+                            const float* save_mean, const float* save_invstd,
+                            hfta_act act, float act_alpha, hfta_out dX,
+                            float* dgamma, float* dbeta, void* ws, size_t ws_bytes,
+                            hfta_stream stream);
+/*
+ * PointNet input transform (STN): T_b,n = F_b[n] viewed as 3x3 row-major
+ * (+ I3 if add_identity), x'_b[n*L+l][:] = x[n*L+l][:] * T_b,n.
+ * X fp32 [B][N*L][3] (bstride 0 = shared), F dtype dt [B][N][9] (ld >= 9),
+ * Xout dtype dt [B][N*L][3] (ld >= 3).
+ */
+hfta_status hfta_transform_points_fwd(int B, int64_t N, int64_t L, hfta_dtype dt, hfta_in X,
+                                      hfta_in F, int add_identity, hfta_out Xout,
+                                      hfta_stream stream);
+/* dF_b[n] = sum_l x[n*L+l]^T dXout_b[n*L+l]   (dtype dt [B][N][9]; dX not needed). */
+hfta_status hfta_transform_points_bwd(int B, int64_t N, int64_t L, hfta_dtype dt, hfta_in X,
+                                      hfta_in dXout, hfta_out dF, hfta_stream stream);
+/*
+ * Dropout (App. B row Dropout) with a counter-based mask
+ * (reading R14): element i of model b is kept iff
+ * Philox4x32-10(ctr=(i/4, b, step, layer), key=(seed lo, seed hi))[i%4]
+ * >= floor(p*2^32); kept values are scaled by 1/(1-p).  i = row*cols + col.
+ * X/Y [B][rows][cols] dtype dt.  bwd: same mask applied to dY.
+ */
+hfta_status hfta_dropout_fwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in X,
+                             hfta_out Y, uint64_t seed, int64_t step, int32_t layer, float p,
+                             hfta_stream stream);
+hfta_status hfta_dropout_bwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in dY,
+                             hfta_out dX, uint64_t seed, int64_t step, int32_t layer, float p,
+                             hfta_stream stream);
+/*
+ * Segmented column sums: S[b][g][c] = sum_{r in group g} X[b][r][c] with
+ * groups of `group` consecutive rows (group = rows: plain column sum).
+ * S fp32 at S + b*S_bstride + g*C + c.  accumulate != 0 adds.
+ */
+size_t hfta_colsum_workspace(int B, int64_t rows, int64_t C, int64_t group);
+hfta_status hfta_colsum(int B, int64_t rows, int64_t C, int64_t group, hfta_dtype dt, hfta_in X,
+                        float* S, int64_t S_bstride, int accumulate, void* ws, size_t ws_bytes,
+                        hfta_stream stream);
+
+/* ---------------------------------------------------- fused loss (K8d) -- */
+/*
+ * Per-model losses l_b and d l_b / d logits (App. C: the per-model gradients
+ * equal B * dL/d(theta_b) for the mean-reduced fused loss L = (1/B) sum_b l_b,
+ * Eq. 1-3; computed analytically, reading R9).
+ * NLL: logits [B][rows][K] dtype dt, labels int32 [rows] (labels_bstride 0 =
+ * shared) ; l_b = -(1/rows) sum_r log_softmax(z_r)[y_r]; dlogits dtype dt.
+ * loss: fp32 [B]; mean_loss (nullable) fp32 scalar = (1/B) sum_b l_b.
+ */
+size_t hfta_loss_workspace(int B, int64_t rows);
+hfta_status hfta_loss_nll(int B, int64_t rows, int64_t K, hfta_dtype dt, hfta_in logits,
+                          const int32_t* labels, int64_t labels_bstride, float* loss,
+                          float* mean_loss, hfta_out dlogits, void* ws, size_t ws_bytes,
+                          hfta_stream stream);
+/* MSE (mean over rows*C): A [B][rows][C] dtype dt vs T fp32 [rows][C] (T_bstride 0 = shared). */
+hfta_status hfta_loss_mse(int B, int64_t rows, int64_t C, hfta_dtype dt, hfta_in A,
+                          const float* T, int64_t T_bstride, int64_t T_ld, float* loss,
+                          float* mean_loss, hfta_out dA, void* ws, size_t ws_bytes,
+                          hfta_stream stream);
+
+/* ------------------------------------------------------ fused Adam (K7) -- */
+/*
+ * Fused Adam ("scalar-vector operations ... replaced by
+ * broadcasted vector-vector operations"), PyTorch-1.6 form (reading R7).
+ * For every element j of model b (param/grad/exp_avg/exp_avg_sq fp32 at
+ * [b*bstride + j], j < P):
+ *   g = grad + wd[b]*p ; m = beta1[b]*m + (1-beta1[b])*g ;
+ *   v = beta2[b]*v + (1-beta2[b])*g^2 ;
+ *   p -= lr[b]/(1-beta1[b]^t) * m / (sqrt(v)/sqrt(1-beta2[b]^t) + eps[b])
+ * lr, beta1, beta2, eps, wd: device fp32 [B]; step: device int64 scalar t>=1
+ * (shared, read at kernel time so graphs can replay).  param_bf16 (nullable):
+ * bf16 shadow [b*bf16_bstride + j] written with round-to-nearest-even.
+ */
+hfta_status hfta_fused_adam(int B, int64_t P, float* param, const float* grad,
+                            float* exp_avg, float* exp_avg_sq, int64_t bstride,
+                            const float* lr, const float* beta1, const float* beta2,
+                            const float* eps, const float* weight_decay, const int64_t* step,
+                            void* param_bf16, int64_t bf16_bstride, hfta_stream stream);
+
+/* ------------------------------------------------------------- utility -- */
+/* n fp32 -> bf16 (RNE); used to initialise the bf16 weight shadow. */
+hfta_status hfta_cast_f32_bf16(int64_t n, const float* src, void* dst, hfta_stream stream);
+/* *step += 1 on device (graph-capturable step counter). */
+hfta_status hfta_step_increment(int64_t* step, hfta_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HFTA_H_ */

@@ -1,0 +1,104 @@
+// api_common.cu -- init, error reporting, launch accounting, small utilities.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace hfta {
+
+static thread_local std::string g_err;
+static std::atomic<int> g_sms{0};
+static std::atomic<int> g_init{0};
+static std::atomic<uint64_t> g_launches{0};
+static int g_sync = -1;
+
+hfta_status fail(hfta_status code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+hfta_status check_init() {
+  if (!g_init.load()) return fail(HFTA_ERR_NOT_INITIALIZED, "hfta_init() has not succeeded");
+  return HFTA_OK;
+}
+
+int num_sms() { return g_sms.load(); }
+void count_launches(uint64_t n) { g_launches += n; }
+
+hfta_status post_launch(cudaStream_t s, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(HFTA_ERR_CUDA, "%s: launch failed: %s", what, cudaGetErrorString(e));
+  if (g_sync < 0) {
+    const char* v = getenv("HFTA_SYNC");
+    g_sync = (v && v[0] == '1') ? 1 : 0;
+  }
+  if (g_sync) {
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(HFTA_ERR_CUDA, "%s: kernel failed: %s", what, cudaGetErrorString(e));
+  }
+  return HFTA_OK;
+}
+
+__global__ void k_cast_f32_bf16(int64_t n, const float* __restrict__ s, __nv_bfloat16* __restrict__ d) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = __float2bfloat16_rn(s[i]);
+}
+
+__global__ void k_step_inc(int64_t* step) { *step += 1; }
+
+}  // namespace hfta
+
+using namespace hfta;
+
+extern "C" {
+
+hfta_status hfta_init(int device) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(HFTA_ERR_ARCH, "hfta_init: no CUDA device (%s)", e == cudaSuccess ? "count 0" : cudaGetErrorString(e));
+  if (device < 0 || device >= n) return fail(HFTA_ERR_INVALID_VALUE, "hfta_init: device %d of %d", device, n);
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return fail(HFTA_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess)
+    return fail(HFTA_ERR_CUDA, "cudaGetDeviceProperties: %s", cudaGetErrorString(e));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(HFTA_ERR_ARCH, "hfta_init: device %d is %s (CC %d.%d); libhfta requires CC 10.0 (B200, sm_100a)",
+                device, prop.name, prop.major, prop.minor);
+  g_sms = prop.multiProcessorCount;
+  g_init = 1;
+  return HFTA_OK;
+}
+
+const char* hfta_last_error(void) { return g_err.c_str(); }
+const char* hfta_version(void) { return "libhfta 0.1 (sm_100a)"; }
+uint64_t hfta_launch_count(void) { return g_launches.load(); }
+
+hfta_status hfta_cast_f32_bf16(int64_t n, const float* src, void* dst, hfta_stream stream) {
+  if (hfta_status s = check_init()) return s;
+  HFTA_REQUIRE(n >= 0 && (n == 0 || (src && dst)), HFTA_ERR_INVALID_VALUE, "hfta_cast_f32_bf16: bad args");
+  if (n == 0) return HFTA_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int grid = (int)std::min<int64_t>(cdiv(n, 256), (int64_t)num_sms() * 8);
+  k_cast_f32_bf16<<<grid, 256, 0, st>>>(n, src, (__nv_bfloat16*)dst);
+  count_launches(1);
+  return post_launch(st, "hfta_cast_f32_bf16");
+}
+
+hfta_status hfta_step_increment(int64_t* step, hfta_stream stream) {
+  if (hfta_status s = check_init()) return s;
+  HFTA_REQUIRE(step, HFTA_ERR_INVALID_VALUE, "hfta_step_increment: step is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  k_step_inc<<<1, 1, 0, st>>>(step);
+  count_launches(1);
+  return post_launch(st, "hfta_step_increment");
+}
+
+}  // extern "C"

@@ -1,0 +1,557 @@
+// bn.cu -- fused BatchNorm forward/backward with per-model statistics (K6)
+// and the PointNet BN-apply + max-over-points fusion (K8a).
+// App. B rows BatchNorm1d/BatchNorm2d: the fused BN runs over
+// B*C channels, i.e. statistics per (model b, channel c) (reading R13).
+// HBM-bound: 128-bit loads along C (4 fp32 / 8 bf16 per access), one CTA row
+// of threads per row slice, fixed-order partial merges in fp64.
+#include <initializer_list>
+#include <tuple>
+
+#include "common.cuh"
+
+namespace hfta {
+namespace {
+
+constexpr int NT = 256;
+
+struct Geo {
+  int vec, tpr, cb, rpb, colgroups, chunks;
+  int64_t rows_per_chunk;
+};
+
+int pow2ceil(int64_t x) { int p = 1; while (p < x) p <<= 1; return p; }
+
+bool vec_ok(const void* p, int64_t ld, int64_t bs, int64_t C, int vec) {
+  return p == nullptr || (aligned16(p) && ld % vec == 0 && bs % vec == 0 && C % vec == 0);
+}
+
+Geo make_geo(int B, int64_t R, int64_t C, int vec) {
+  Geo g;
+  g.vec = vec;
+  g.tpr = (int)std::min<int64_t>(32, pow2ceil(cdiv(C, vec)));
+  g.cb = g.tpr * vec;
+  g.rpb = NT / g.tpr;
+  g.colgroups = (int)cdiv(C, g.cb);
+  int64_t target = 4 * (int64_t)std::max(num_sms(), 148);
+  int64_t chunks = std::max<int64_t>(1, target / ((int64_t)g.colgroups * B));
+  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, cdiv(R, (int64_t)g.rpb * 8)));
+  g.rows_per_chunk = cdiv(cdiv(R, chunks), g.rpb) * g.rpb;
+  g.chunks = (int)cdiv(R, g.rows_per_chunk);
+  return g;
+}
+
+// Welford-free stable stats: per-thread fp32 sums of (x - shift) and (x - shift)^2
+// with shift = x[row 0] of the column; merged across row lanes in fixed order.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(NT) k_bn_stats(int64_t R, int64_t C, const T* __restrict__ X,
+                                                 int64_t xbs, int64_t ld, Geo g,
+                                                 float* __restrict__ p1, float* __restrict__ p2) {
+  __shared__ float s1[NT * VEC], s2[NT * VEC];
+  const int b = blockIdx.z, chunk = blockIdx.y;
+  const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
+  const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
+  const T* Xb = X + (int64_t)b * xbs;
+  float a1[VEC], a2[VEC], sh[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) { a1[v] = 0.f; a2[v] = 0.f; sh[v] = 0.f; }
+  if (c0 < C) {
+    ld_vec<T, VEC>(Xb + c0, sh);
+    const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
+    const int64_t r1 = min(R, r0 + g.rows_per_chunk);
+    for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
+      float x[VEC];
+      ld_vec<T, VEC>(Xb + r * ld + c0, x);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        float d = x[v] - sh[v];
+        a1[v] += d;
+        a2[v] = fmaf(d, d, a2[v]);
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    s1[rl * g.cb + lane * VEC + v] = a1[v];
+    s2[rl * g.cb + lane * VEC + v] = a2[v];
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < g.cb; col += NT) {
+    int64_t c = (int64_t)blockIdx.x * g.cb + col;
+    if (c >= C) continue;
+    float t1 = 0.f, t2 = 0.f;
+    for (int r = 0; r < g.rpb; ++r) { t1 += s1[r * g.cb + col]; t2 += s2[r * g.cb + col]; }
+    int64_t o = ((int64_t)b * g.chunks + chunk) * C + c;
+    p1[o] = t1;
+    p2[o] = t2;
+  }
+}
+
+template <typename T>
+__global__ void k_bn_finalize(int B, int64_t R, int64_t C, const T* __restrict__ X, int64_t xbs, int chunks,
+                              const float* __restrict__ p1, const float* __restrict__ p2, float eps,
+                              float momentum, float* __restrict__ rmean, float* __restrict__ rvar,
+                              float* __restrict__ smean, float* __restrict__ sinv) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * C) return;
+  int64_t b = i / C, c = i % C;
+  double s1 = 0.0, s2 = 0.0;
+  for (int k = 0; k < chunks; ++k) {
+    s1 += p1[(b * chunks + k) * C + c];
+    s2 += p2[(b * chunks + k) * C + c];
+  }
+  double shift = (double)ldf(X + b * xbs + c);
+  double md = s1 / (double)R;
+  double var = s2 / (double)R - md * md;
+  if (var < 0.0) var = 0.0;
+  double mean = shift + md;
+  smean[i] = (float)mean;
+  sinv[i] = (float)(1.0 / sqrt(var + (double)eps));
+  if (rmean) rmean[i] = (float)((1.0 - momentum) * (double)rmean[i] + momentum * mean);
+  if (rvar) rvar[i] = (float)((1.0 - momentum) * (double)rvar[i] + momentum * var * (double)R / (double)(R - 1));
+}
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(NT) k_bn_apply(int64_t R, int64_t C, const T* __restrict__ X, int64_t xbs,
+                                                 int64_t xld, T* __restrict__ Y, int64_t ybs, int64_t yld,
+                                                 const float* __restrict__ gamma, const float* __restrict__ beta,
+                                                 int64_t gbs, const float* __restrict__ smean,
+                                                 const float* __restrict__ sinv, int act, float alpha, Geo g) {
+  const int b = blockIdx.z, chunk = blockIdx.y;
+  const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
+  const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
+  if (c0 >= C) return;
+  float sc[VEC], sf[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    float m = smean[(int64_t)b * C + c0 + v], is = sinv[(int64_t)b * C + c0 + v];
+    float ga = gamma[(int64_t)b * gbs + c0 + v], be = beta[(int64_t)b * gbs + c0 + v];
+    sc[v] = ga * is;
+    sf[v] = be - m * ga * is;
+  }
+  const T* Xb = X + (int64_t)b * xbs;
+  T* Yb = Y + (int64_t)b * ybs;
+  const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
+  const int64_t r1 = min(R, r0 + g.rows_per_chunk);
+  for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
+    float x[VEC];
+    ld_vec<T, VEC>(Xb + r * xld + c0, x);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) x[v] = act_fwd(fmaf(x[v], sc[v], sf[v]), act, alpha);
+    st_vec<T, VEC>(Yb + r * yld + c0, x);
+  }
+}
+
+// ------------------------------------------------------------- backward --
+template <typename T, int VEC>
+__global__ void __launch_bounds__(NT) k_bn_bwd_reduce(int64_t R, int64_t C, const T* __restrict__ dY, int64_t dbs,
+                                                      int64_t dld, const T* __restrict__ X, int64_t xbs, int64_t xld,
+                                                      const float* __restrict__ gamma, const float* __restrict__ beta,
+                                                      int64_t gbs, const float* __restrict__ smean,
+                                                      const float* __restrict__ sinv, int act, float alpha, Geo g,
+                                                      float* __restrict__ p1, float* __restrict__ p2) {
+  __shared__ float s1[NT * VEC], s2[NT * VEC];
+  const int b = blockIdx.z, chunk = blockIdx.y;
+  const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
+  const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
+  float a1[VEC], a2[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) { a1[v] = 0.f; a2[v] = 0.f; }
+  if (c0 < C) {
+    float m[VEC], is[VEC], ga[VEC], be[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      m[v] = smean[(int64_t)b * C + c0 + v]; is[v] = sinv[(int64_t)b * C + c0 + v];
+      ga[v] = gamma[(int64_t)b * gbs + c0 + v]; be[v] = beta[(int64_t)b * gbs + c0 + v];
+    }
+    const T* Xb = X + (int64_t)b * xbs;
+    const T* Db = dY + (int64_t)b * dbs;
+    const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
+    const int64_t r1 = min(R, r0 + g.rows_per_chunk);
+    for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
+      float x[VEC], d[VEC];
+      ld_vec<T, VEC>(Xb + r * xld + c0, x);
+      ld_vec<T, VEC>(Db + r * dld + c0, d);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        float xh = (x[v] - m[v]) * is[v];
+        float dz = d[v] * act_grad(fmaf(ga[v], xh, be[v]), act, alpha);
+        a1[v] += dz;
+        a2[v] = fmaf(dz, xh, a2[v]);
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    s1[rl * g.cb + lane * VEC + v] = a1[v];
+    s2[rl * g.cb + lane * VEC + v] = a2[v];
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < g.cb; col += NT) {
+    int64_t c = (int64_t)blockIdx.x * g.cb + col;
+    if (c >= C) continue;
+    float t1 = 0.f, t2 = 0.f;
+    for (int r = 0; r < g.rpb; ++r) { t1 += s1[r * g.cb + col]; t2 += s2[r * g.cb + col]; }
+    int64_t o = ((int64_t)b * g.chunks + chunk) * C + c;
+    p1[o] = t1;
+    p2[o] = t2;
+  }
+}
+
+// dbeta, dgamma (fp32, written to the gradient arena) and the per-(b,c)
+// coefficients of the apply pass stored in ws: k1 = gamma*invstd, k2 = dbeta/R, k3 = dgamma/R.
+__global__ void k_bn_bwd_finalize(int B, int64_t R, int64_t C, int chunks, const float* __restrict__ p1,
+                                  const float* __restrict__ p2, const float* __restrict__ gamma, int64_t gbs,
+                                  const float* __restrict__ sinv, float* __restrict__ dgamma,
+                                  float* __restrict__ dbeta, int accumulate, float* __restrict__ coef) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * C) return;
+  int64_t b = i / C, c = i % C;
+  double s1 = 0.0, s2 = 0.0;
+  for (int k = 0; k < chunks; ++k) {
+    s1 += p1[(b * chunks + k) * C + c];
+    s2 += p2[(b * chunks + k) * C + c];
+  }
+  float db = (float)s1, dg = (float)s2;
+  if (dbeta) dbeta[b * gbs + c] = accumulate ? dbeta[b * gbs + c] + db : db;
+  if (dgamma) dgamma[b * gbs + c] = accumulate ? dgamma[b * gbs + c] + dg : dg;
+  coef[i] = gamma[b * gbs + c] * sinv[i];
+  coef[(int64_t)B * C + i] = (float)(s1 / (double)R);
+  coef[2 * (int64_t)B * C + i] = (float)(s2 / (double)R);
+}
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(NT) k_bn_bwd_apply(int B, int64_t R, int64_t C, const T* __restrict__ dY,
+                                                     int64_t dbs, int64_t dld, const T* __restrict__ X, int64_t xbs,
+                                                     int64_t xld, T* __restrict__ dX, int64_t obs, int64_t old,
+                                                     const float* __restrict__ gamma, const float* __restrict__ beta,
+                                                     int64_t gbs, const float* __restrict__ smean,
+                                                     const float* __restrict__ sinv, int act, float alpha, Geo g,
+                                                     const float* __restrict__ coef) {
+  const int b = blockIdx.z, chunk = blockIdx.y;
+  const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
+  const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
+  if (c0 >= C) return;
+  const int64_t BC = (int64_t)B * C;
+  float m[VEC], is[VEC], ga[VEC], be[VEC], k1[VEC], k2[VEC], k3[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    int64_t i = (int64_t)b * C + c0 + v;
+    m[v] = smean[i]; is[v] = sinv[i];
+    ga[v] = gamma[(int64_t)b * gbs + c0 + v]; be[v] = beta[(int64_t)b * gbs + c0 + v];
+    k1[v] = coef[i]; k2[v] = coef[BC + i]; k3[v] = coef[2 * BC + i];
+  }
+  const T* Xb = X + (int64_t)b * xbs;
+  const T* Db = dY + (int64_t)b * dbs;
+  T* Ob = dX + (int64_t)b * obs;
+  const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
+  const int64_t r1 = min(R, r0 + g.rows_per_chunk);
+  for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
+    float x[VEC], d[VEC];
+    ld_vec<T, VEC>(Xb + r * xld + c0, x);
+    ld_vec<T, VEC>(Db + r * dld + c0, d);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      float xh = (x[v] - m[v]) * is[v];
+      float dz = d[v] * act_grad(fmaf(ga[v], xh, be[v]), act, alpha);
+      x[v] = k1[v] * (dz - k2[v] - xh * k3[v]);
+    }
+    st_vec<T, VEC>(Ob + r * old + c0, x);
+  }
+}
+
+// --------------------------------------------------- BN + act + max (K8a) --
+// grid (colgroups, N, B); block reduces max/argmax over the L rows of sample n.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(NT) k_bn_max_fwd(int64_t L, int64_t C, const T* __restrict__ X, int64_t xbs,
+                                                   int64_t xld, const float* __restrict__ gamma,
+                                                   const float* __restrict__ beta, int64_t gbs,
+                                                   const float* __restrict__ smean, const float* __restrict__ sinv,
+                                                   int act, float alpha, T* __restrict__ out, int64_t obs,
+                                                   int64_t old, int32_t* __restrict__ amax, int64_t N, Geo g) {
+  __shared__ float sv[NT * VEC];
+  __shared__ int si[NT * VEC];
+  const int b = blockIdx.z;
+  const int64_t n = blockIdx.y;
+  const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
+  const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
+  float best[VEC];
+  int bi[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) { best[v] = -INFINITY; bi[v] = 0x7fffffff; }
+  if (c0 < C) {
+    float sc[VEC], sf[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      float m = smean[(int64_t)b * C + c0 + v], is = sinv[(int64_t)b * C + c0 + v];
+      float ga = gamma[(int64_t)b * gbs + c0 + v], be = beta[(int64_t)b * gbs + c0 + v];
+      sc[v] = ga * is;
+      sf[v] = be - m * ga * is;
+    }
+    const T* Xb = X + (int64_t)b * xbs + n * L * xld;
+    for (int64_t l = rl; l < L; l += g.rpb) {
+      float x[VEC];
+      ld_vec<T, VEC>(Xb + l * xld + c0, x);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        float z = act_fwd(fmaf(x[v], sc[v], sf[v]), act, alpha);
+        if (z > best[v]) { best[v] = z; bi[v] = (int)l; }   // rows visited in increasing l per lane
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    sv[rl * g.cb + lane * VEC + v] = best[v];
+    si[rl * g.cb + lane * VEC + v] = bi[v];
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < g.cb; col += NT) {
+    int64_t c = (int64_t)blockIdx.x * g.cb + col;
+    if (c >= C) continue;
+    float bv = -INFINITY;
+    int bidx = 0x7fffffff;
+    for (int r = 0; r < g.rpb; ++r) {
+      float v = sv[r * g.cb + col];
+      int ix = si[r * g.cb + col];
+      if (v > bv || (v == bv && ix < bidx)) { bv = v; bidx = ix; }   // first index on ties (R15)
+    }
+    stf(out + (int64_t)b * obs + n * old + c, bv);
+    amax[((int64_t)b * N + n) * C + c] = bidx;
+  }
+}
+
+// step 1 of the max backward: per (b, c) loop over samples n: dz at the argmax
+// row, dbeta = sum dz, dgamma = sum dz*xhat; writes coef (k1,k2,k3) and dz [B][N][C].
+template <typename T>
+__global__ void k_bn_max_bwd_small(int B, int64_t N, int64_t L, int64_t C, const T* __restrict__ dG, int64_t gbs_,
+                                   int64_t gld, const T* __restrict__ X, int64_t xbs, int64_t xld,
+                                   const int32_t* __restrict__ amax, const float* __restrict__ gamma,
+                                   const float* __restrict__ beta, int64_t gbs, const float* __restrict__ smean,
+                                   const float* __restrict__ sinv, int act, float alpha, float* __restrict__ dgamma,
+                                   float* __restrict__ dbeta, float* __restrict__ coef, float* __restrict__ dz_out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * C) return;
+  int64_t b = i / C, c = i % C;
+  float m = smean[i], is = sinv[i], ga = gamma[b * gbs + c], be = beta[b * gbs + c];
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t n = 0; n < N; ++n) {
+    int64_t l = amax[(b * N + n) * C + c];
+    float x = ldf(X + b * xbs + (n * L + l) * xld + c);
+    float xh = (x - m) * is;
+    float dz = ldf(dG + b * gbs_ + n * gld + c) * act_grad(fmaf(ga, xh, be), act, alpha);
+    dz_out[(b * N + n) * C + c] = dz;
+    s1 += dz;
+    s2 += (double)dz * xh;
+  }
+  float db = (float)s1, dg = (float)s2;
+  dbeta[b * gbs + c] = db;
+  dgamma[b * gbs + c] = dg;
+  const double R = (double)(N * L);
+  coef[i] = ga * is;
+  coef[(int64_t)B * C + i] = (float)(s1 / R);
+  coef[2 * (int64_t)B * C + i] = (float)(s2 / R);
+}
+
+// step 2: dense dX = k1 * (dz_sparse - k2 - xhat*k3), grid (colgroups, chunks, B)
+template <typename T, int VEC>
+__global__ void __launch_bounds__(NT) k_bn_max_bwd_apply(int B, int64_t N, int64_t L, int64_t C,
+                                                         const T* __restrict__ X, int64_t xbs, int64_t xld,
+                                                         const int32_t* __restrict__ amax,
+                                                         const float* __restrict__ dz, T* __restrict__ dX,
+                                                         int64_t obs, int64_t old, const float* __restrict__ smean,
+                                                         const float* __restrict__ sinv,
+                                                         const float* __restrict__ coef, Geo g) {
+  const int b = blockIdx.z, chunk = blockIdx.y;
+  const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
+  const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
+  if (c0 >= C) return;
+  const int64_t BC = (int64_t)B * C;
+  float m[VEC], is[VEC], k1[VEC], k2[VEC], k3[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    int64_t i = (int64_t)b * C + c0 + v;
+    m[v] = smean[i]; is[v] = sinv[i];
+    k1[v] = coef[i]; k2[v] = coef[BC + i]; k3[v] = coef[2 * BC + i];
+  }
+  const int64_t R = N * L;
+  const T* Xb = X + (int64_t)b * xbs;
+  T* Ob = dX + (int64_t)b * obs;
+  const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
+  const int64_t r1 = min(R, r0 + g.rows_per_chunk);
+  for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
+    const int64_t n = r / L, l = r % L;
+    float x[VEC];
+    ld_vec<T, VEC>(Xb + r * xld + c0, x);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      int64_t j = ((int64_t)b * N + n) * C + c0 + v;
+      float d = (amax[j] == (int32_t)l) ? dz[j] : 0.f;
+      float xh = (x[v] - m[v]) * is[v];
+      x[v] = k1[v] * (d - k2[v] - xh * k3[v]);
+    }
+    st_vec<T, VEC>(Ob + r * old + c0, x);
+  }
+}
+
+int pick_vec(hfta_dtype dt, int64_t C, std::initializer_list<std::tuple<const void*, int64_t, int64_t>> ts) {
+  int vec = dt == HFTA_BF16 ? 8 : 4;
+  for (auto& t : ts)
+    if (!vec_ok(std::get<0>(t), std::get<1>(t), std::get<2>(t), C, vec)) return 1;
+  return vec;
+}
+
+size_t bn_parts_bytes(int B, int64_t R, int64_t C) {
+  Geo g1 = make_geo(B, R, C, 1), g4 = make_geo(B, R, C, 4), g8 = make_geo(B, R, C, 8);
+  int ch = std::max(g1.chunks, std::max(g4.chunks, g8.chunks));
+  return align_up(2 * (size_t)B * ch * C * sizeof(float), 256);
+}
+
+}  // namespace
+}  // namespace hfta
+
+using namespace hfta;
+
+#define LAUNCH_VEC(T, vec, KERNEL, GRID, ...)                                                   \
+  do {                                                                                        \
+    if (vec == 1) KERNEL<T, 1><<<GRID, NT, 0, s>>>(__VA_ARGS__);                               \
+    else if (vec == 4) KERNEL<T, 4><<<GRID, NT, 0, s>>>(__VA_ARGS__);                          \
+    else KERNEL<T, 8><<<GRID, NT, 0, s>>>(__VA_ARGS__);                                        \
+  } while (0)
+
+#define DT_DISPATCH(dt, ...)                                                                   \
+  do {                                                                                        \
+    if (dt == HFTA_F32) { using T = float; __VA_ARGS__; }                                     \
+    else { using T = __nv_bfloat16; __VA_ARGS__; }                                            \
+  } while (0)
+
+extern "C" {
+
+size_t hfta_fused_bn_workspace(int B, int64_t R, int64_t C) {
+  if (B < 1 || R < 1 || C < 1) return 0;
+  return bn_parts_bytes(B, R, C) + align_up(3 * (size_t)B * C * sizeof(float), 256);
+}
+
+hfta_status hfta_fused_bn_fwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_in X, const float* gamma,
+                              const float* beta, int64_t gb_bstride, float* running_mean, float* running_var,
+                              float momentum, float eps, hfta_act act, float act_alpha, hfta_out Y,
+                              float* save_mean, float* save_invstd, void* ws, size_t ws_bytes,
+                              hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(R >= 2 && C >= 1, HFTA_ERR_SHAPE, "bn_fwd: R=%lld (needs >= 2), C=%lld", (long long)R, (long long)C);
+  HFTA_REQUIRE(X.ptr && gamma && beta && save_mean && save_invstd, HFTA_ERR_INVALID_VALUE,
+               "bn_fwd: X, gamma, beta, save_mean, save_invstd are required");
+  HFTA_REQUIRE(X.ld >= C && (!Y.ptr || Y.ld >= C), HFTA_ERR_SHAPE, "bn_fwd: ld < C");
+  HFTA_REQUIRE(!Y.ptr || Y.bstride > 0 || B == 1, HFTA_ERR_SHAPE, "bn_fwd: Y.bstride must be > 0");
+  size_t need = hfta_fused_bn_workspace(B, R, C);
+  HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "bn_fwd: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  int vec = pick_vec(dt, C, {{X.ptr, X.ld, X.bstride}, {Y.ptr, Y.ld, Y.bstride}});
+  Geo g = make_geo(B, R, C, vec);
+  float* p1 = reinterpret_cast<float*>(ws);
+  float* p2 = p1 + (size_t)B * g.chunks * C;
+  dim3 grid(g.colgroups, g.chunks, B);
+  DT_DISPATCH(dt, {
+    LAUNCH_VEC(T, vec, k_bn_stats, grid, R, C, (const T*)X.ptr, X.bstride, X.ld, g, p1, p2);
+    k_bn_finalize<T><<<(unsigned)cdiv((int64_t)B * C, 256), 256, 0, s>>>(
+        B, R, C, (const T*)X.ptr, X.bstride, g.chunks, p1, p2, eps, momentum, running_mean, running_var,
+        save_mean, save_invstd);
+    if (Y.ptr)
+      LAUNCH_VEC(T, vec, k_bn_apply, grid, R, C, (const T*)X.ptr, X.bstride, X.ld, (T*)Y.ptr, Y.bstride, Y.ld,
+                 gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, g);
+  });
+  count_launches(Y.ptr ? 3 : 2);
+  return post_launch(s, "hfta_fused_bn_fwd");
+}
+
+hfta_status hfta_fused_bn_bwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_in dY, hfta_in X,
+                              const float* gamma, const float* beta, int64_t gb_bstride, const float* save_mean,
+                              const float* save_invstd, hfta_act act, float act_alpha, hfta_out dX,
+                              float* dgamma, float* dbeta, int accumulate, void* ws, size_t ws_bytes,
+                              hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(R >= 2 && C >= 1, HFTA_ERR_SHAPE, "bn_bwd: R=%lld, C=%lld", (long long)R, (long long)C);
+  HFTA_REQUIRE(dY.ptr && X.ptr && gamma && beta && save_mean && save_invstd && dX.ptr, HFTA_ERR_INVALID_VALUE,
+               "bn_bwd: dY, X, gamma, beta, save_mean, save_invstd, dX are required");
+  HFTA_REQUIRE(dX.bstride > 0 || B == 1, HFTA_ERR_SHAPE, "bn_bwd: dX.bstride must be > 0");
+  size_t need = hfta_fused_bn_workspace(B, R, C);
+  HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "bn_bwd: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  int vec = pick_vec(dt, C, {{X.ptr, X.ld, X.bstride}, {dY.ptr, dY.ld, dY.bstride}, {dX.ptr, dX.ld, dX.bstride}});
+  Geo g = make_geo(B, R, C, vec);
+  float* p1 = reinterpret_cast<float*>(ws);
+  float* p2 = p1 + (size_t)B * g.chunks * C;
+  size_t parts_bytes = bn_parts_bytes(B, R, C);
+  float* coef = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + parts_bytes);
+  dim3 grid(g.colgroups, g.chunks, B);
+  DT_DISPATCH(dt, {
+    LAUNCH_VEC(T, vec, k_bn_bwd_reduce, grid, R, C, (const T*)dY.ptr, dY.bstride, dY.ld, (const T*)X.ptr,
+               X.bstride, X.ld, gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, g, p1, p2);
+    k_bn_bwd_finalize<<<(unsigned)cdiv((int64_t)B * C, 256), 256, 0, s>>>(
+        B, R, C, g.chunks, p1, p2, gamma, gb_bstride, save_invstd, dgamma, dbeta, accumulate, coef);
+    LAUNCH_VEC(T, vec, k_bn_bwd_apply, grid, B, R, C, (const T*)dY.ptr, dY.bstride, dY.ld, (const T*)X.ptr,
+               X.bstride, X.ld, (T*)dX.ptr, dX.bstride, dX.ld, gamma, beta, gb_bstride, save_mean, save_invstd,
+               (int)act, act_alpha, g, coef);
+  });
+  count_launches(3);
+  return post_launch(s, "hfta_fused_bn_bwd");
+}
+
+hfta_status hfta_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C, hfta_dtype dt, hfta_in X, const float* gamma,
+                            const float* beta, int64_t gb_bstride, const float* save_mean,
+                            const float* save_invstd, hfta_act act, float act_alpha, hfta_out out,
+                            int32_t* argmax, hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(N >= 1 && L >= 1 && C >= 1, HFTA_ERR_SHAPE, "bn_max_fwd: N,L,C = %lld,%lld,%lld", (long long)N,
+               (long long)L, (long long)C);
+  HFTA_REQUIRE(X.ptr && gamma && beta && save_mean && save_invstd && out.ptr && argmax, HFTA_ERR_INVALID_VALUE,
+               "bn_max_fwd: null argument");
+  HFTA_REQUIRE(out.ld >= C && (out.bstride > 0 || B == 1), HFTA_ERR_SHAPE, "bn_max_fwd: out stride");
+  cudaStream_t s = (cudaStream_t)stream;
+  int vec = pick_vec(dt, C, {{X.ptr, X.ld, X.bstride}});
+  Geo g = make_geo(B, N * L, C, vec);
+  dim3 grid(g.colgroups, (unsigned)N, B);
+  DT_DISPATCH(dt, {
+    LAUNCH_VEC(T, vec, k_bn_max_fwd, grid, L, C, (const T*)X.ptr, X.bstride, X.ld, gamma, beta, gb_bstride,
+               save_mean, save_invstd, (int)act, act_alpha, (T*)out.ptr, out.bstride, out.ld, argmax, N, g);
+  });
+  count_launches(1);
+  return post_launch(s, "hfta_bn_max_fwd");
+}
+
+size_t hfta_bn_max_bwd_workspace(int B, int64_t N, int64_t C) {
+  if (B < 1 || N < 1 || C < 1) return 0;
+  return align_up(3 * (size_t)B * C * sizeof(float), 256) + align_up((size_t)B * N * C * sizeof(float), 256);
+}
+
+hfta_status hfta_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C, hfta_dtype dt, hfta_in dG, hfta_in X,
+                            const int32_t* argmax, const float* gamma, const float* beta, int64_t gb_bstride,
+                            const float* save_mean, const float* save_invstd, hfta_act act, float act_alpha,
+                            hfta_out dX, float* dgamma, float* dbeta, void* ws, size_t ws_bytes,
+                            hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(N >= 1 && L >= 1 && C >= 1 && N * L >= 2, HFTA_ERR_SHAPE, "bn_max_bwd: bad N,L,C");
+  HFTA_REQUIRE(dG.ptr && X.ptr && argmax && gamma && beta && save_mean && save_invstd && dX.ptr && dgamma && dbeta,
+               HFTA_ERR_INVALID_VALUE, "bn_max_bwd: null argument");
+  size_t need = hfta_bn_max_bwd_workspace(B, N, C);
+  HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "bn_max_bwd: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  float* coef = reinterpret_cast<float*>(ws);
+  float* dz = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align_up(3 * (size_t)B * C * sizeof(float), 256));
+  int vec = pick_vec(dt, C, {{X.ptr, X.ld, X.bstride}, {dX.ptr, dX.ld, dX.bstride}});
+  Geo g = make_geo(B, N * L, C, vec);
+  dim3 grid(g.colgroups, g.chunks, B);
+  DT_DISPATCH(dt, {
+    k_bn_max_bwd_small<T><<<(unsigned)cdiv((int64_t)B * C, 128), 128, 0, s>>>(
+        B, N, L, C, (const T*)dG.ptr, dG.bstride, dG.ld, (const T*)X.ptr, X.bstride, X.ld, argmax, gamma, beta,
+        gb_bstride, save_mean, save_invstd, (int)act, act_alpha, dgamma, dbeta, coef, dz);
+    LAUNCH_VEC(T, vec, k_bn_max_bwd_apply, grid, B, N, L, C, (const T*)X.ptr, X.bstride, X.ld, argmax, dz,
+               (T*)dX.ptr, dX.bstride, dX.ld, save_mean, save_invstd, coef, g);
+  });
+  count_launches(2);
+  return post_launch(s, "hfta_bn_max_bwd");
+}
+
+}  // extern "C"

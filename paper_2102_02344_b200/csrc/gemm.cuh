@@ -1,0 +1,36 @@
+// gemm.cuh -- the model-batched contraction engine behind the fused Linear /
+// Conv1d(k=1) layers (App. B rows Linear->baddbmm P:L1271-1272 and Conv1d
+// P:L1265-1266).  One launch computes, for every model b in [0, B):
+//   C_b[m][n] (+)= sum_k A_b(m,k) * B_b(n,k)  (+ bias_b(m,n))
+// A_b(m,k) = A[b*a_bs + m*a_ld + k]   (a_kmajor)   or  A[b*a_bs + k*a_ld + m]
+// B_b(n,k) = B[b*b_bs + n*b_ld + k]   (b_kmajor)   or  B[b*b_bs + k*b_ld + n]
+// fwd: A = X (K-major), B = W (K-major); dgrad: A = dY (K-major), B = W
+// (MN-major); wgrad: A = dY (MN-major), B = X (MN-major), fp32 out, split-K.
+#pragma once
+#include "common.cuh"
+
+namespace hfta {
+
+struct GemmP {
+  int B;
+  int64_t M, N, K;
+  const void* A; int64_t a_bs, a_ld; int a_kmajor;
+  const void* Bm; int64_t b_bs, b_ld; int b_kmajor;
+  void* C; int64_t c_bs, c_ld;
+  const float* bias; int64_t bias_bs, bias_ld, bias_div;  // bias(b,m,n) = bias[b*bs + (m/div)*ld + n]
+  int accumulate;   // C += result (fp32 output only)
+  int splits;       // split-K chunks (>= 1); > 1 needs `part`
+  int64_t k_chunk;  // reduction rows per split (multiple of the K tile)
+  float* part;      // [splits][B][M][N] fp32 partials
+};
+
+// dt_in: operand dtype; out_f32: C is fp32 (else dt_in).
+hfta_status gemm_simt(const GemmP& p, hfta_dtype dt_in, bool out_f32, cudaStream_t s);
+hfta_status splitk_reduce(const GemmP& p, cudaStream_t s);   // C (+)= sum_s part[s]
+
+// tcgen05 / TMA path; returns HFTA_ERR_UNSUPPORTED if the shape/alignment
+// does not qualify (caller then uses gemm_simt).
+hfta_status gemm_tc(const GemmP& p, hfta_dtype dt_in, bool out_f32, cudaStream_t s);
+bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32);
+
+}  // namespace hfta

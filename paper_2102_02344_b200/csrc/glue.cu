@@ -1,0 +1,267 @@
+// glue.cu -- PointNet glue kernels (K8b/K8c) and segmented column sums.
+//  * input transform x' = x * T (STN, the cited PointNet model; reading R1)
+//  * dropout with a Philox4x32-10 counter-based mask (App. B row Dropout,
+//    P:L1295-1296; reading R14)
+//  * segmented column sums (dbias, and the per-sample sums of the seg
+//    split-weight rewrite)
+#include "common.cuh"
+
+namespace hfta {
+namespace {
+
+// ---------------------------------------------------- transform points --
+template <typename T>
+__global__ void k_transform_fwd(int64_t N, int64_t L, const float* __restrict__ X, int64_t xbs, int64_t xld,
+                                const T* __restrict__ F, int64_t fbs, int64_t fld, int add_id, T* __restrict__ Y,
+                                int64_t ybs, int64_t yld) {
+  const int b = blockIdx.y;
+  const int64_t R = N * L;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = r / L;
+    const T* t = F + (int64_t)b * fbs + n * fld;
+    const float* x = X + (int64_t)b * xbs + r * xld;
+    float x0 = x[0], x1 = x[1], x2 = x[2];
+    T* y = Y + (int64_t)b * ybs + r * yld;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      float t0 = ldf(t + 0 * 3 + j) + (add_id && j == 0 ? 1.f : 0.f);
+      float t1 = ldf(t + 1 * 3 + j) + (add_id && j == 1 ? 1.f : 0.f);
+      float t2 = ldf(t + 2 * 3 + j) + (add_id && j == 2 ? 1.f : 0.f);
+      stf(y + j, fmaf(x0, t0, fmaf(x1, t1, x2 * t2)));
+    }
+  }
+}
+
+// dF[b][n][i*3+j] = sum_l x[n*L+l][i] * dY[b][n*L+l][j]; one block per (n, b).
+template <typename T>
+__global__ void k_transform_bwd(int64_t N, int64_t L, const float* __restrict__ X, int64_t xbs, int64_t xld,
+                                const T* __restrict__ dY, int64_t dbs, int64_t dld, T* __restrict__ dF,
+                                int64_t fbs, int64_t fld) {
+  __shared__ float red[9][256];
+  const int b = blockIdx.y;
+  const int64_t n = blockIdx.x;
+  float acc[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] = 0.f;
+  for (int64_t l = threadIdx.x; l < L; l += blockDim.x) {
+    const int64_t r = n * L + l;
+    const float* x = X + (int64_t)b * xbs + r * xld;
+    const T* d = dY + (int64_t)b * dbs + r * dld;
+    float dj[3] = {ldf(d), ldf(d + 1), ldf(d + 2)};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) acc[i * 3 + j] = fmaf(x[i], dj[j], acc[i * 3 + j]);
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q) red[q][threadIdx.x] = acc[q];
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w)
+#pragma unroll
+      for (int q = 0; q < 9; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x < 9) stf(dF + (int64_t)b * fbs + n * fld + threadIdx.x, red[threadIdx.x][0]);
+}
+
+// ------------------------------------------------------------- Philox --
+struct U4 { uint32_t x, y, z, w; };
+
+__device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+  }
+  return c;
+}
+
+template <typename T>
+__global__ void k_dropout(int64_t rows, int64_t cols, const T* __restrict__ X, int64_t xbs, int64_t xld,
+                          T* __restrict__ Y, int64_t ybs, int64_t yld, uint32_t k0, uint32_t k1, uint32_t step,
+                          uint32_t layer, uint32_t thr, float scale) {
+  const int b = blockIdx.y;
+  const int64_t n = rows * cols;
+  const int64_t groups = (n + 3) / 4;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < groups; q += (int64_t)gridDim.x * blockDim.x) {
+    U4 w = philox4x32_10(U4{(uint32_t)q, (uint32_t)b, step, layer}, k0, k1);
+    uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int64_t i = q * 4 + e;
+      if (i >= n) break;
+      int64_t r = i / cols, c = i % cols;
+      float v = ldf(X + (int64_t)b * xbs + r * xld + c);
+      stf(Y + (int64_t)b * ybs + r * yld + c, ws[e] >= thr ? v * scale : 0.f);
+    }
+  }
+}
+
+// ------------------------------------------------------------- colsum --
+// grid (cdiv(C,32), ngroups*cpg, B), block (32, 8): partial sums per chunk.
+template <typename T>
+__global__ void k_colsum_part(int64_t C, int64_t group, int cpg, int64_t rpc, const T* __restrict__ X, int64_t xbs,
+                              int64_t xld, float* __restrict__ part) {
+  __shared__ float red[8][33];
+  const int b = blockIdx.z;
+  const int64_t chunk = blockIdx.y;
+  const int64_t g = chunk / cpg, j = chunk % cpg;
+  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int64_t r0 = g * group + j * rpc;
+  const int64_t r1 = min((g + 1) * group, r0 + rpc);
+  float acc = 0.f;
+  if (c < C)
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) acc += ldf(X + (int64_t)b * xbs + r * xld + c);
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < C) {
+    float s = 0.f;
+    for (int y = 0; y < 8; ++y) s += red[y][threadIdx.x];
+    part[((int64_t)b * gridDim.y + chunk) * C + c] = s;
+  }
+}
+
+__global__ void k_colsum_fin(int B, int64_t C, int64_t ngroups, int cpg, const float* __restrict__ part,
+                             float* __restrict__ S, int64_t sbs, int accumulate) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * ngroups * C) return;
+  int64_t b = i / (ngroups * C), rem = i % (ngroups * C), g = rem / C, c = rem % C;
+  double s = 0.0;
+  for (int j = 0; j < cpg; ++j) s += part[((b * ngroups + g) * cpg + j) * C + c];
+  float* o = S + b * sbs + g * C + c;
+  *o = accumulate ? *o + (float)s : (float)s;
+}
+
+struct ColsumGeo { int64_t ngroups; int cpg; int64_t rpc; };
+ColsumGeo colsum_geo(int B, int64_t rows, int64_t C, int64_t group) {
+  ColsumGeo g;
+  g.ngroups = cdiv(rows, group);
+  int64_t blocks_per = cdiv(C, 32) * (int64_t)B * g.ngroups;
+  int64_t target = 4 * (int64_t)std::max(num_sms(), 148);
+  int64_t cpg = std::max<int64_t>(1, std::min<int64_t>(cdiv(target, blocks_per), cdiv(group, 256)));
+  g.rpc = cdiv(group, cpg);
+  g.cpg = (int)cdiv(group, g.rpc);
+  return g;
+}
+
+}  // namespace
+
+size_t colsum_ws(int B, int64_t rows, int64_t C, int64_t group) {
+  if (B < 1 || rows < 1 || C < 1 || group < 1) return 0;
+  ColsumGeo g = colsum_geo(B, rows, C, group);
+  return align_up((size_t)B * g.ngroups * g.cpg * C * sizeof(float), 256);
+}
+
+hfta_status colsum_impl(int B, int64_t rows, int64_t C, int64_t group, hfta_dtype dt, hfta_in X, float* S,
+                        int64_t S_bstride, int accumulate, void* ws, size_t ws_bytes, cudaStream_t s) {
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(rows >= 1 && C >= 1 && group >= 1 && X.ptr && S, HFTA_ERR_INVALID_VALUE, "colsum: bad args");
+  size_t need = colsum_ws(B, rows, C, group);
+  HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "colsum: workspace %zu < %zu", ws_bytes, need);
+  ColsumGeo g = colsum_geo(B, rows, C, group);
+  float* part = reinterpret_cast<float*>(ws);
+  dim3 grid((unsigned)cdiv(C, 32), (unsigned)(g.ngroups * g.cpg), B);
+  if (dt == HFTA_F32)
+    k_colsum_part<float><<<grid, dim3(32, 8), 0, s>>>(C, group, g.cpg, g.rpc, (const float*)X.ptr, X.bstride, X.ld, part);
+  else
+    k_colsum_part<__nv_bfloat16><<<grid, dim3(32, 8), 0, s>>>(C, group, g.cpg, g.rpc, (const __nv_bfloat16*)X.ptr,
+                                                               X.bstride, X.ld, part);
+  int64_t tot = (int64_t)B * g.ngroups * C;
+  k_colsum_fin<<<(unsigned)cdiv(tot, 256), 256, 0, s>>>(B, C, g.ngroups, g.cpg, part, S, S_bstride, accumulate);
+  count_launches(2);
+  return post_launch(s, "colsum");
+}
+
+}  // namespace hfta
+
+using namespace hfta;
+
+extern "C" {
+
+hfta_status hfta_transform_points_fwd(int B, int64_t N, int64_t L, hfta_dtype dt, hfta_in X, hfta_in F,
+                                      int add_identity, hfta_out Xout, hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(N >= 1 && L >= 1 && X.ptr && F.ptr && Xout.ptr, HFTA_ERR_INVALID_VALUE, "transform_fwd: bad args");
+  HFTA_REQUIRE(X.ld >= 3 && F.ld >= 9 && Xout.ld >= 3 && (Xout.bstride > 0 || B == 1), HFTA_ERR_SHAPE,
+               "transform_fwd: strides");
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid((unsigned)std::min<int64_t>(cdiv(N * L, 256), 1024), B);
+  if (dt == HFTA_F32)
+    k_transform_fwd<float><<<grid, 256, 0, s>>>(N, L, (const float*)X.ptr, X.bstride, X.ld, (const float*)F.ptr,
+                                               F.bstride, F.ld, add_identity, (float*)Xout.ptr, Xout.bstride, Xout.ld);
+  else
+    k_transform_fwd<__nv_bfloat16><<<grid, 256, 0, s>>>(N, L, (const float*)X.ptr, X.bstride, X.ld,
+                                                       (const __nv_bfloat16*)F.ptr, F.bstride, F.ld, add_identity,
+                                                       (__nv_bfloat16*)Xout.ptr, Xout.bstride, Xout.ld);
+  count_launches(1);
+  return post_launch(s, "hfta_transform_points_fwd");
+}
+
+hfta_status hfta_transform_points_bwd(int B, int64_t N, int64_t L, hfta_dtype dt, hfta_in X, hfta_in dXout,
+                                      hfta_out dF, hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(N >= 1 && L >= 1 && X.ptr && dXout.ptr && dF.ptr, HFTA_ERR_INVALID_VALUE, "transform_bwd: bad args");
+  HFTA_REQUIRE(dF.ld >= 9 && (dF.bstride > 0 || B == 1), HFTA_ERR_SHAPE, "transform_bwd: dF strides");
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid((unsigned)N, B);
+  if (dt == HFTA_F32)
+    k_transform_bwd<float><<<grid, 256, 0, s>>>(N, L, (const float*)X.ptr, X.bstride, X.ld, (const float*)dXout.ptr,
+                                               dXout.bstride, dXout.ld, (float*)dF.ptr, dF.bstride, dF.ld);
+  else
+    k_transform_bwd<__nv_bfloat16><<<grid, 256, 0, s>>>(N, L, (const float*)X.ptr, X.bstride, X.ld,
+                                                       (const __nv_bfloat16*)dXout.ptr, dXout.bstride, dXout.ld,
+                                                       (__nv_bfloat16*)dF.ptr, dF.bstride, dF.ld);
+  count_launches(1);
+  return post_launch(s, "hfta_transform_points_bwd");
+}
+
+static hfta_status dropout_common(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in X, hfta_out Y,
+                                  uint64_t seed, int64_t step, int32_t layer, float p, hfta_stream stream,
+                                  const char* what) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(rows >= 1 && cols >= 1 && X.ptr && Y.ptr, HFTA_ERR_INVALID_VALUE, "%s: bad args", what);
+  HFTA_REQUIRE(p >= 0.f && p < 1.f, HFTA_ERR_INVALID_VALUE, "%s: p=%g not in [0,1)", what, (double)p);
+  HFTA_REQUIRE(X.ld >= cols && Y.ld >= cols && (Y.bstride > 0 || B == 1), HFTA_ERR_SHAPE, "%s: strides", what);
+  cudaStream_t s = (cudaStream_t)stream;
+  double t = floor((double)p * 4294967296.0);
+  uint32_t thr = (uint32_t)(t > 4294967295.0 ? 4294967295.0 : t);
+  float scale = 1.0f / (1.0f - p);
+  int64_t groups = cdiv(rows * cols, 4);
+  dim3 grid((unsigned)std::min<int64_t>(cdiv(groups, 256), 2048), B);
+  uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
+  if (dt == HFTA_F32)
+    k_dropout<float><<<grid, 256, 0, s>>>(rows, cols, (const float*)X.ptr, X.bstride, X.ld, (float*)Y.ptr, Y.bstride,
+                                         Y.ld, k0, k1, (uint32_t)step, (uint32_t)layer, thr, scale);
+  else
+    k_dropout<__nv_bfloat16><<<grid, 256, 0, s>>>(rows, cols, (const __nv_bfloat16*)X.ptr, X.bstride, X.ld,
+                                                 (__nv_bfloat16*)Y.ptr, Y.bstride, Y.ld, k0, k1, (uint32_t)step,
+                                                 (uint32_t)layer, thr, scale);
+  count_launches(1);
+  return post_launch(s, what);
+}
+
+hfta_status hfta_dropout_fwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in X, hfta_out Y, uint64_t seed,
+                             int64_t step, int32_t layer, float p, hfta_stream stream) {
+  return dropout_common(B, rows, cols, dt, X, Y, seed, step, layer, p, stream, "hfta_dropout_fwd");
+}
+
+hfta_status hfta_dropout_bwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in dY, hfta_out dX,
+                             uint64_t seed, int64_t step, int32_t layer, float p, hfta_stream stream) {
+  return dropout_common(B, rows, cols, dt, dY, dX, seed, step, layer, p, stream, "hfta_dropout_bwd");
+}
+
+size_t hfta_colsum_workspace(int B, int64_t rows, int64_t C, int64_t group) { return colsum_ws(B, rows, C, group); }
+
+hfta_status hfta_colsum(int B, int64_t rows, int64_t C, int64_t group, hfta_dtype dt, hfta_in X, float* S,
+                        int64_t S_bstride, int accumulate, void* ws, size_t ws_bytes, hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  return colsum_impl(B, rows, C, group, dt, X, S, S_bstride, accumulate, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,145 @@
+// linear.cu -- C ABI of the fused Linear / Conv1d(k=1) layer (K1/K2).
+// App. B rows "Linear -> baddbmm(b[B,1,Fy], x[B,N,Fx], w[B,Fx,Fy])"
+// and "Conv1d ... G = B x g": one launch for
+// all B models, model index in the grid / tile scheduler.
+#include "gemm.cuh"
+
+namespace hfta {
+hfta_status colsum_impl(int B, int64_t rows, int64_t C, int64_t group, hfta_dtype dt, hfta_in X,
+                        float* S, int64_t S_bstride, int accumulate, void* ws, size_t ws_bytes,
+                        cudaStream_t s);
+size_t colsum_ws(int B, int64_t rows, int64_t C, int64_t group);
+
+namespace {
+// split-K policy of the weight-gradient contraction (reduction over M rows).
+struct Split { int splits; int64_t chunk; };
+Split wgrad_split(int B, int64_t M, int64_t N, int64_t K) {
+  int64_t tiles = cdiv(N, 128) * cdiv(K, 128) * (int64_t)B;
+  int64_t want = cdiv(2 * (int64_t)std::max(num_sms(), 148), tiles);
+  int64_t maxs = std::max<int64_t>(1, M / 1024);
+  int64_t splits = std::max<int64_t>(1, std::min(want, maxs));
+  int64_t chunk = cdiv(cdiv(M, splits), 128) * 128;
+  splits = cdiv(M, chunk);
+  return {(int)splits, chunk};
+}
+
+hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s) {
+  if (gemm_tc_supported(p, dt, out_f32)) return gemm_tc(p, dt, out_f32, s);
+  return gemm_simt(p, dt, out_f32, s);
+}
+
+hfta_status check_in(const hfta_in& t, const char* name, int B) {
+  HFTA_REQUIRE(t.ptr, HFTA_ERR_INVALID_VALUE, "%s.ptr is NULL", name);
+  HFTA_REQUIRE(t.bstride >= 0 && t.ld >= 1, HFTA_ERR_SHAPE, "%s: bstride %lld / ld %lld invalid", name,
+               (long long)t.bstride, (long long)t.ld);
+  (void)B;
+  return HFTA_OK;
+}
+hfta_status check_out(const hfta_out& t, const char* name, int B) {
+  HFTA_REQUIRE(t.ptr, HFTA_ERR_INVALID_VALUE, "%s.ptr is NULL", name);
+  HFTA_REQUIRE(t.ld >= 1 && (t.bstride > 0 || B == 1), HFTA_ERR_SHAPE,
+               "%s: output needs bstride > 0 (got %lld) and ld >= 1", name, (long long)t.bstride);
+  return HFTA_OK;
+}
+}  // namespace
+}  // namespace hfta
+
+using namespace hfta;
+
+extern "C" {
+
+hfta_status hfta_fused_linear_fwd(int B, int64_t M, int64_t N, int64_t K, hfta_dtype dt,
+                                  hfta_in X, hfta_in W, const float* bias, int64_t bias_bstride,
+                                  int64_t bias_ld, int64_t bias_row_div, hfta_out Y,
+                                  hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(M >= 1 && N >= 1 && K >= 1, HFTA_ERR_SHAPE, "linear_fwd: M,N,K = %lld,%lld,%lld",
+               (long long)M, (long long)N, (long long)K);
+  HFTA_REQUIRE(dt == HFTA_F32 || dt == HFTA_BF16, HFTA_ERR_UNSUPPORTED, "linear_fwd: dtype %d", (int)dt);
+  if (hfta_status st = check_in(X, "X", B)) return st;
+  if (hfta_status st = check_in(W, "W", B)) return st;
+  if (hfta_status st = check_out(Y, "Y", B)) return st;
+  HFTA_REQUIRE(X.ld >= K, HFTA_ERR_SHAPE, "linear_fwd: X [%lld x %lld] has ld %lld < K", (long long)M,
+               (long long)K, (long long)X.ld);
+  HFTA_REQUIRE(W.ld >= K, HFTA_ERR_SHAPE, "linear_fwd: W [%lld x %lld] has ld %lld < K", (long long)N,
+               (long long)K, (long long)W.ld);
+  HFTA_REQUIRE(Y.ld >= N, HFTA_ERR_SHAPE, "linear_fwd: Y [%lld x %lld] has ld %lld < N", (long long)M,
+               (long long)N, (long long)Y.ld);
+  GemmP p{};
+  p.B = B; p.M = M; p.N = N; p.K = K;
+  p.A = X.ptr; p.a_bs = X.bstride; p.a_ld = X.ld; p.a_kmajor = 1;
+  p.Bm = W.ptr; p.b_bs = W.bstride; p.b_ld = W.ld; p.b_kmajor = 1;
+  p.C = Y.ptr; p.c_bs = Y.bstride; p.c_ld = Y.ld;
+  p.bias = bias; p.bias_bs = bias_bstride; p.bias_ld = bias_ld;
+  p.bias_div = (bias_ld > 0 && bias_row_div > 0) ? bias_row_div : 0;
+  p.splits = 1; p.k_chunk = cdiv(K, 16) * 16;
+  return run_gemm(p, dt, false, (cudaStream_t)stream);
+}
+
+size_t hfta_fused_linear_bwd_workspace(int B, int64_t M, int64_t N, int64_t K, hfta_dtype dt) {
+  if (B < 1 || M < 1 || N < 1 || K < 1) return 0;
+  Split sp = wgrad_split(B, M, N, K);
+  size_t part = sp.splits > 1 ? (size_t)sp.splits * B * N * K * sizeof(float) : 0;
+  size_t cs = colsum_ws(B, M, N, M);
+  return align_up(part, 256) + align_up(cs, 256);
+  (void)dt;
+}
+
+hfta_status hfta_fused_linear_bwd(int B, int64_t M, int64_t N, int64_t K, hfta_dtype dt,
+                                  hfta_in dY, hfta_in X, hfta_in W, hfta_out dX, float* dW,
+                                  int64_t dW_bstride, float* dbias, int64_t dbias_bstride,
+                                  int accumulate, void* ws, size_t ws_bytes, hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(M >= 1 && N >= 1 && K >= 1, HFTA_ERR_SHAPE, "linear_bwd: M,N,K = %lld,%lld,%lld",
+               (long long)M, (long long)N, (long long)K);
+  HFTA_REQUIRE(dt == HFTA_F32 || dt == HFTA_BF16, HFTA_ERR_UNSUPPORTED, "linear_bwd: dtype %d", (int)dt);
+  if (hfta_status st = check_in(dY, "dY", B)) return st;
+  HFTA_REQUIRE(dY.ld >= N, HFTA_ERR_SHAPE, "linear_bwd: dY ld %lld < N %lld", (long long)dY.ld, (long long)N);
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t need = hfta_fused_linear_bwd_workspace(B, M, N, K, dt);
+  HFTA_REQUIRE(ws_bytes >= need && (need == 0 || ws), HFTA_ERR_WORKSPACE,
+               "linear_bwd: workspace %zu < required %zu bytes", ws_bytes, need);
+  if (dX.ptr) {
+    if (hfta_status st = check_in(W, "W", B)) return st;
+    if (hfta_status st = check_out(dX, "dX", B)) return st;
+    HFTA_REQUIRE(dX.ld >= K && W.ld >= K, HFTA_ERR_SHAPE, "linear_bwd: dX/W ld < K");
+    GemmP p{};
+    p.B = B; p.M = M; p.N = K; p.K = N;                         // dX[M,K] = dY[M,N] W[N,K]
+    p.A = dY.ptr; p.a_bs = dY.bstride; p.a_ld = dY.ld; p.a_kmajor = 1;
+    p.Bm = W.ptr; p.b_bs = W.bstride; p.b_ld = W.ld; p.b_kmajor = 0;
+    p.C = dX.ptr; p.c_bs = dX.bstride; p.c_ld = dX.ld;
+    p.splits = 1; p.k_chunk = cdiv(N, 16) * 16;
+    if (hfta_status st = run_gemm(p, dt, false, s)) return st;
+  }
+  if (dW) {
+    if (hfta_status st = check_in(X, "X", B)) return st;
+    HFTA_REQUIRE(X.ld >= K, HFTA_ERR_SHAPE, "linear_bwd: X ld %lld < K %lld", (long long)X.ld, (long long)K);
+    HFTA_REQUIRE(dW_bstride >= N * K || B == 1, HFTA_ERR_SHAPE, "linear_bwd: dW_bstride %lld < N*K",
+                 (long long)dW_bstride);
+    Split sp = wgrad_split(B, M, N, K);
+    GemmP p{};
+    p.B = B; p.M = N; p.N = K; p.K = M;                         // dW[N,K] = dY^T[N,M] X[M,K]
+    p.A = dY.ptr; p.a_bs = dY.bstride; p.a_ld = dY.ld; p.a_kmajor = 0;
+    p.Bm = X.ptr; p.b_bs = X.bstride; p.b_ld = X.ld; p.b_kmajor = 0;
+    p.C = dW; p.c_bs = dW_bstride; p.c_ld = K;
+    p.accumulate = accumulate;
+    p.splits = sp.splits; p.k_chunk = sp.chunk;
+    p.part = sp.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
+    if (hfta_status st = run_gemm(p, dt, true, s)) return st;
+    if (sp.splits > 1)
+      if (hfta_status st = splitk_reduce(p, s)) return st;
+  }
+  if (dbias) {
+    Split sp = wgrad_split(B, M, N, K);
+    size_t off = align_up(sp.splits > 1 ? (size_t)sp.splits * B * N * K * sizeof(float) : 0, 256);
+    char* cws = ws ? reinterpret_cast<char*>(ws) + off : nullptr;
+    if (hfta_status st = colsum_impl(B, M, N, M, dt, dY, dbias, dbias_bstride, accumulate, cws,
+                                     ws_bytes > off ? ws_bytes - off : 0, s))
+      return st;
+  }
+  return HFTA_OK;
+}
+
+}  // extern "C"

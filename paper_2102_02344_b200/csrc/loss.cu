@@ -1,0 +1,159 @@
+// loss.cu -- fused per-model losses (K8d).  App. C: the fused
+// loss L = (1/B) sum_b l_b (Eq. 1, sum over b = 0..B-1, reading R8) needs
+// scaling by B so that each model receives its serial gradient (Eq. 3).  The
+// kernels write d l_b / d logits directly -- analytically the same as
+// back-propagating B*L (reading R9) -- plus loss[B] and L.
+#include "common.cuh"
+
+namespace hfta {
+namespace {
+
+constexpr int NT = 256;
+constexpr int ROWS_PER_BLOCK = 64;
+
+// grid (chunks, B): one warp per row; lanes stride over the K classes.
+template <typename T>
+__global__ void __launch_bounds__(NT) k_nll(int64_t rows, int64_t K, const T* __restrict__ Z, int64_t zbs,
+                                            int64_t zld, const int32_t* __restrict__ y, int64_t ybs,
+                                            T* __restrict__ dZ, int64_t dbs, int64_t dld, float* __restrict__ part) {
+  __shared__ float wsum[NT / 32];
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const float inv_rows = 1.0f / (float)rows;
+  float lsum = 0.f;
+  const int64_t r0 = (int64_t)blockIdx.x * ROWS_PER_BLOCK;
+  const int64_t r1 = min(rows, r0 + ROWS_PER_BLOCK);
+  for (int64_t r = r0 + warp; r < r1; r += NT / 32) {
+    const T* z = Z + (int64_t)b * zbs + r * zld;
+    float m = -INFINITY;
+    for (int64_t k = lane; k < K; k += 32) m = fmaxf(m, ldf(z + k));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float se = 0.f;
+    for (int64_t k = lane; k < K; k += 32) se += expf(ldf(z + k) - m);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const float lse = m + logf(se);
+    const int32_t t = y[(int64_t)b * ybs + r];
+    if (lane == 0) lsum += lse - ldf(z + t);
+    T* d = dZ + (int64_t)b * dbs + r * dld;
+    for (int64_t k = lane; k < K; k += 32) {
+      float pk = expf(ldf(z + k) - lse);
+      stf(d + k, (pk - (k == t ? 1.f : 0.f)) * inv_rows);
+    }
+  }
+  if (lane == 0) wsum[warp] = lsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < NT / 32; ++w) s += wsum[w];
+    part[(int64_t)b * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT) k_mse(int64_t rows, int64_t C, const T* __restrict__ A, int64_t abs_,
+                                            int64_t ald, const float* __restrict__ Tg, int64_t tbs, int64_t tld,
+                                            T* __restrict__ dA, int64_t dbs, int64_t dld, float* __restrict__ part) {
+  __shared__ float red[NT];
+  const int b = blockIdx.y;
+  const float scale = 2.0f / ((float)rows * (float)C);
+  float s = 0.f;
+  const int64_t r0 = (int64_t)blockIdx.x * ROWS_PER_BLOCK;
+  const int64_t r1 = min(rows, r0 + ROWS_PER_BLOCK);
+  const int64_t n = (r1 - r0) * C;
+  for (int64_t e = threadIdx.x; e < n; e += NT) {
+    int64_t r = r0 + e / C, c = e % C;
+    float d = ldf(A + (int64_t)b * abs_ + r * ald + c) - Tg[(int64_t)b * tbs + r * tld + c];
+    s = fmaf(d, d, s);
+    stf(dA + (int64_t)b * dbs + r * dld + c, d * scale);
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = NT / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[(int64_t)b * gridDim.x + blockIdx.x] = red[0];
+}
+
+// loss[b] = scale * sum_chunks part (fixed order, fp64); mean over b.
+__global__ void k_loss_fin(int B, int chunks, const float* __restrict__ part, double scale, float* __restrict__ loss,
+                           float* __restrict__ mean_loss) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double tot = 0.0;
+  for (int b = 0; b < B; ++b) {
+    double s = 0.0;
+    for (int k = 0; k < chunks; ++k) s += part[(int64_t)b * chunks + k];
+    float l = (float)(s * scale);
+    loss[b] = l;
+    tot += l;
+  }
+  if (mean_loss) *mean_loss = (float)(tot / B);
+}
+
+}  // namespace
+}  // namespace hfta
+
+using namespace hfta;
+
+extern "C" {
+
+size_t hfta_loss_workspace(int B, int64_t rows) {
+  if (B < 1 || rows < 1) return 0;
+  return align_up((size_t)B * cdiv(rows, ROWS_PER_BLOCK) * sizeof(float), 256);
+}
+
+hfta_status hfta_loss_nll(int B, int64_t rows, int64_t K, hfta_dtype dt, hfta_in logits, const int32_t* labels,
+                          int64_t labels_bstride, float* loss, float* mean_loss, hfta_out dlogits, void* ws,
+                          size_t ws_bytes, hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(rows >= 1 && K >= 1 && logits.ptr && labels && loss && dlogits.ptr, HFTA_ERR_INVALID_VALUE,
+               "loss_nll: bad args");
+  HFTA_REQUIRE(logits.ld >= K && dlogits.ld >= K && (dlogits.bstride > 0 || B == 1), HFTA_ERR_SHAPE,
+               "loss_nll: strides");
+  size_t need = hfta_loss_workspace(B, rows);
+  HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "loss_nll: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  int chunks = (int)cdiv(rows, ROWS_PER_BLOCK);
+  float* part = reinterpret_cast<float*>(ws);
+  dim3 grid(chunks, B);
+  if (dt == HFTA_F32)
+    k_nll<float><<<grid, NT, 0, s>>>(rows, K, (const float*)logits.ptr, logits.bstride, logits.ld, labels,
+                                    labels_bstride, (float*)dlogits.ptr, dlogits.bstride, dlogits.ld, part);
+  else
+    k_nll<__nv_bfloat16><<<grid, NT, 0, s>>>(rows, K, (const __nv_bfloat16*)logits.ptr, logits.bstride, logits.ld,
+                                            labels, labels_bstride, (__nv_bfloat16*)dlogits.ptr, dlogits.bstride,
+                                            dlogits.ld, part);
+  k_loss_fin<<<1, 32, 0, s>>>(B, chunks, part, 1.0 / (double)rows, loss, mean_loss);
+  count_launches(2);
+  return post_launch(s, "hfta_loss_nll");
+}
+
+hfta_status hfta_loss_mse(int B, int64_t rows, int64_t C, hfta_dtype dt, hfta_in A, const float* T, int64_t T_bstride,
+                          int64_t T_ld, float* loss, float* mean_loss, hfta_out dA, void* ws, size_t ws_bytes,
+                          hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(rows >= 1 && C >= 1 && A.ptr && T && loss && dA.ptr, HFTA_ERR_INVALID_VALUE, "loss_mse: bad args");
+  HFTA_REQUIRE(A.ld >= C && T_ld >= C && dA.ld >= C && (dA.bstride > 0 || B == 1), HFTA_ERR_SHAPE,
+               "loss_mse: strides");
+  size_t need = hfta_loss_workspace(B, rows);
+  HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "loss_mse: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  int chunks = (int)cdiv(rows, ROWS_PER_BLOCK);
+  float* part = reinterpret_cast<float*>(ws);
+  dim3 grid(chunks, B);
+  if (dt == HFTA_F32)
+    k_mse<float><<<grid, NT, 0, s>>>(rows, C, (const float*)A.ptr, A.bstride, A.ld, T, T_bstride, T_ld,
+                                    (float*)dA.ptr, dA.bstride, dA.ld, part);
+  else
+    k_mse<__nv_bfloat16><<<grid, NT, 0, s>>>(rows, C, (const __nv_bfloat16*)A.ptr, A.bstride, A.ld, T, T_bstride,
+                                            T_ld, (__nv_bfloat16*)dA.ptr, dA.bstride, dA.ld, part);
+  k_loss_fin<<<1, 32, 0, s>>>(B, chunks, part, 1.0 / ((double)rows * (double)C), loss, mean_loss);
+  count_launches(2);
+  return post_launch(s, "hfta_loss_mse");
+}
+
+}  // extern "C"

@@ -1,0 +1,299 @@
+"""Per-kernel parity of libhfta (through the C ABI) against the oracle's layer
+definitions on the same seeded inputs.  Sizes span several tiles with a
+ragged tail; B in {1, 3}; shared inputs use bstride 0."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import layers as OL
+from oracle.adam import adam_step
+from oracle.philox import dropout_keep_mask
+from tests._cmp import assert_close, relerr
+
+pytestmark = pytest.mark.gpu
+
+H = None
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _init():
+    global H
+    import paper_2102_02344_b200.hfta as hfta
+    hfta.hfta_init(0)
+    H = hfta
+
+
+R = np.random.default_rng(2024)
+DT = {"f32": (0, torch.float32), "bf16": (1, torch.bfloat16)}
+
+
+def dev(a, tdt=torch.float32):
+    return torch.tensor(np.asarray(a), dtype=torch.float64).to(tdt).to(DEV).contiguous()
+
+
+def host(t):
+    return t.detach().float().cpu().numpy().astype(np.float64)
+
+
+def rounded(a, tdt):
+    """The value the device sees after storing a in tdt."""
+    return torch.tensor(a).to(tdt).double().numpy()
+
+
+def s():
+    return torch.cuda.current_stream().cuda_stream
+
+
+# ----------------------------------------------------------------- linear ----
+SHAPES = [(300, 64, 3), (1000, 128, 64), (257, 200, 136), (32, 9, 256), (37, 40, 256), (130, 3, 64)]
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("B,shared", [(1, False), (3, False), (3, True)])
+def test_linear_fwd_bwd(dt, M, N, K, B, shared):
+    code, tdt = DT[dt]
+    X = rounded(R.standard_normal((1 if shared else B, M, K)), tdt)
+    W = rounded(R.standard_normal((B, N, K)) / np.sqrt(K), tdt)
+    bias = R.standard_normal((B, N)).astype(np.float32).astype(np.float64)
+    dY = rounded(R.standard_normal((B, M, N)), tdt)
+    Xd, Wd, bd, dYd = dev(X, tdt), dev(W, tdt), dev(bias), dev(dY, tdt)
+    Y = torch.empty(B, M, N, dtype=tdt, device=DEV)
+    xbs = 0 if shared else M * K
+    H.hfta_fused_linear_fwd(B, M, N, K, code, H.tin(Xd, xbs, K), H.tin(Wd, N * K, K), H.ptr(bd), N, 0, 0,
+                            H.tout(Y, M * N, N), s())
+    dX = torch.empty(B, M, K, dtype=tdt, device=DEV)
+    dW = torch.empty(B, N, K, device=DEV)
+    db = torch.empty(B, N, device=DEV)
+    ws = torch.empty(max(H.hfta_fused_linear_bwd_workspace(B, M, N, K, code), 1), dtype=torch.uint8, device=DEV)
+    H.hfta_fused_linear_bwd(B, M, N, K, code, H.tin(dYd, M * N, N), H.tin(Xd, xbs, K), H.tin(Wd, N * K, K),
+                            H.tout(dX, M * K, K), H.ptr(dW), N * K, H.ptr(db), N, 0, H.ptr(ws), ws.numel(), s())
+    torch.cuda.synchronize()
+    tol = 1e-5 if dt == "f32" else 1e-2
+    for b in range(B):
+        xb = X[0 if shared else b]
+        y = OL.linear_fwd(xb, W[b], bias[b])
+        dx, dw, dbb = OL.linear_bwd(dY[b], xb, W[b])
+        assert_close(host(Y[b]), y, tol, "Y")
+        assert_close(host(dX[b]), dx, tol, "dX")
+        assert_close(host(dW[b]), dw, 1e-5 if dt == "f32" else 1e-4, "dW")
+        assert_close(host(db[b]), dbb, 1e-5, "dbias")
+
+
+def test_linear_bwd_accumulate_and_rowgroup_bias():
+    B, M, N, K, L = 2, 500, 48, 32, 125
+    X = R.standard_normal((B, M, K)).astype(np.float32).astype(np.float64)
+    W = R.standard_normal((B, N, K)).astype(np.float32).astype(np.float64)
+    tab = R.standard_normal((B, M // L, N)).astype(np.float32).astype(np.float64)
+    Y = torch.empty(B, M, N, device=DEV)
+    H.hfta_fused_linear_fwd(B, M, N, K, 0, H.tin(dev(X), M * K, K), H.tin(dev(W), N * K, K), H.ptr(dev(tab)),
+                            (M // L) * N, N, L, H.tout(Y, M * N, N), s())
+    dY = R.standard_normal((B, M, N)).astype(np.float32).astype(np.float64)
+    dW0 = R.standard_normal((B, N, K)).astype(np.float32).astype(np.float64)
+    dW = dev(dW0)
+    ws = torch.empty(max(H.hfta_fused_linear_bwd_workspace(B, M, N, K, 0), 1), dtype=torch.uint8, device=DEV)
+    H.hfta_fused_linear_bwd(B, M, N, K, 0, H.tin(dev(dY), M * N, N), H.tin(dev(X), M * K, K),
+                            H.tin(dev(W), N * K, K), H.tout(None, 0, 1), H.ptr(dW), N * K, None, 0, 1,
+                            H.ptr(ws), ws.numel(), s())
+    torch.cuda.synchronize()
+    for b in range(B):
+        ref = X[b] @ W[b].T + np.repeat(tab[b], L, axis=0)
+        assert_close(host(Y[b]), ref, 1e-5, "row-group bias")
+        assert_close(host(dW[b]), dW0[b] + dY[b].T @ X[b], 1e-5, "accumulate")
+
+
+def test_linear_errors():
+    with pytest.raises(H.HftaError) as e:
+        H.hfta_fused_linear_fwd(0, 4, 4, 4, 0, H.hfta_in(None, 0, 4), H.hfta_in(None, 0, 4), None, 0, 0, 0,
+                                H.hfta_out(None, 0, 4), s())
+    assert e.value.code == 1
+    x = torch.zeros(4, 4, device=DEV)
+    with pytest.raises(H.HftaError) as e:
+        H.hfta_fused_linear_fwd(1, 4, 4, 8, 0, H.tin(x, 0, 4), H.tin(x, 0, 4), None, 0, 0, 0, H.tout(x, 16, 4), s())
+    assert e.value.code == 2 and "ld" in str(e.value)
+
+
+# -------------------------------------------------------------------- BN ----
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("Rr,C,act", [(5000, 64, 1), (1000, 1024, 0), (32, 512, 1), (777, 48, 2), (300, 9, 1)])
+def test_bn_fwd_bwd(dt, Rr, C, act):
+    code, tdt = DT[dt]
+    B = 3
+    X = rounded(R.standard_normal((B, Rr, C)) * 2 + 3, tdt)
+    g = R.uniform(0.5, 1.5, (B, C)).astype(np.float32).astype(np.float64)
+    be = R.uniform(-0.5, 0.5, (B, C)).astype(np.float32).astype(np.float64)
+    dY = rounded(R.standard_normal((B, Rr, C)), tdt)
+    rm0, rv0 = R.standard_normal((B, C)).astype(np.float32), R.uniform(0.5, 2, (B, C)).astype(np.float32)
+    Xd, gd, bed = dev(X, tdt), dev(g), dev(be)
+    rm, rv = dev(rm0), dev(rv0)
+    Y = torch.empty(B, Rr, C, dtype=tdt, device=DEV)
+    sm, si = torch.empty(B, C, device=DEV), torch.empty(B, C, device=DEV)
+    ws = torch.empty(H.hfta_fused_bn_workspace(B, Rr, C), dtype=torch.uint8, device=DEV)
+    H.hfta_fused_bn_fwd(B, Rr, C, code, H.tin(Xd, Rr * C, C), H.ptr(gd), H.ptr(bed), C, H.ptr(rm), H.ptr(rv), 0.1,
+                        1e-5, act, 0.2, H.tout(Y, Rr * C, C), H.ptr(sm), H.ptr(si), H.ptr(ws), ws.numel(), s())
+    dX = torch.empty(B, Rr, C, dtype=tdt, device=DEV)
+    dg, db = torch.empty(B, C, device=DEV), torch.empty(B, C, device=DEV)
+    H.hfta_fused_bn_bwd(B, Rr, C, code, H.tin(dev(dY, tdt), Rr * C, C), H.tin(Xd, Rr * C, C), H.ptr(gd), H.ptr(bed),
+                        C, H.ptr(sm), H.ptr(si), act, 0.2, H.tout(dX, Rr * C, C), H.ptr(dg), H.ptr(db), 0, H.ptr(ws),
+                        ws.numel(), s())
+    torch.cuda.synchronize()
+    actf = {0: (lambda z: z, lambda d, z: d), 1: (OL.relu, OL.relu_bwd),
+            2: (lambda z: OL.leaky_relu(z, 0.2), lambda d, z: OL.leaky_relu_bwd(d, z, 0.2))}[act]
+    tol = 1e-5 if dt == "f32" else 1e-2
+    for b in range(B):
+        z, c = OL.bn_fwd(X[b], g[b], be[b])
+        assert_close(host(Y[b]), actf[0](z), tol, "Y")
+        rmr, rvr = OL.bn_running(rm0[b].astype(np.float64), rv0[b].astype(np.float64), c, Rr)
+        assert_close(host(rm[b]), rmr, 1e-6, "running_mean")
+        assert_close(host(rv[b]), rvr, 1e-6, "running_var")
+        assert_close(host(sm[b]), c["mean"], 1e-6, "save_mean")
+        assert_close(host(si[b]), c["invstd"], 1e-6, "save_invstd")
+        dx, dgr, dbr = OL.bn_bwd(actf[1](dY[b], z), c, g[b])
+        assert_close(host(dg[b]), dgr, 1e-5 if dt == "f32" else 1e-3, "dgamma")
+        assert_close(host(db[b]), dbr, 1e-5 if dt == "f32" else 1e-3, "dbeta")
+        assert_close(host(dX[b]), dx, 1e-4 if dt == "f32" else 2e-2, "dX")
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("act", [0, 1])
+def test_bn_max_fwd_bwd(dt, act):
+    code, tdt = DT[dt]
+    B, N, L, C = 2, 3, 700, 136
+    Rr = N * L
+    X = rounded(R.standard_normal((B, Rr, C)), tdt)
+    g = R.uniform(0.5, 1.5, (B, C)).astype(np.float32).astype(np.float64)
+    be = R.uniform(-0.5, 0.5, (B, C)).astype(np.float32).astype(np.float64)
+    Xd, gd, bed = dev(X, tdt), dev(g), dev(be)
+    sm, si = torch.empty(B, C, device=DEV), torch.empty(B, C, device=DEV)
+    ws = torch.empty(max(H.hfta_fused_bn_workspace(B, Rr, C), H.hfta_bn_max_bwd_workspace(B, N, C)),
+                     dtype=torch.uint8, device=DEV)
+    H.hfta_fused_bn_fwd(B, Rr, C, code, H.tin(Xd, Rr * C, C), H.ptr(gd), H.ptr(bed), C, None, None, 0.1, 1e-5, act,
+                        0.0, H.tout(None, 0, 1), H.ptr(sm), H.ptr(si), H.ptr(ws), ws.numel(), s())
+    G = torch.empty(B, N, C, dtype=tdt, device=DEV)
+    am = torch.empty(B, N, C, dtype=torch.int32, device=DEV)
+    H.hfta_bn_max_fwd(B, N, L, C, code, H.tin(Xd, Rr * C, C), H.ptr(gd), H.ptr(bed), C, H.ptr(sm), H.ptr(si), act,
+                      0.0, H.tout(G, N * C, C), H.ptr(am), s())
+    dG = rounded(R.standard_normal((B, N, C)), tdt)
+    dX = torch.empty(B, Rr, C, dtype=tdt, device=DEV)
+    dg, db = torch.empty(B, C, device=DEV), torch.empty(B, C, device=DEV)
+    H.hfta_bn_max_bwd(B, N, L, C, code, H.tin(dev(dG, tdt), N * C, C), H.tin(Xd, Rr * C, C), H.ptr(am), H.ptr(gd),
+                      H.ptr(bed), C, H.ptr(sm), H.ptr(si), act, 0.0, H.tout(dX, Rr * C, C), H.ptr(dg), H.ptr(db),
+                      H.ptr(ws), ws.numel(), s())
+    torch.cuda.synchronize()
+    for b in range(B):
+        z, c = OL.bn_fwd(X[b], g[b], be[b])
+        a = OL.relu(z) if act else z
+        gmax, idx = OL.max_over_points(a.reshape(N, L, C))
+        if dt == "f32":
+            assert np.array_equal(host(am[b]).astype(np.int64), idx)
+        assert_close(host(G[b]), gmax, 1e-5 if dt == "f32" else 1e-2, "max")
+        da = OL.max_over_points_bwd(dG[b], host(am[b]).astype(np.int64), L).reshape(Rr, C)
+        dz = OL.relu_bwd(da, z) if act else da
+        dx, dgr, dbr = OL.bn_bwd(dz, c, g[b])
+        assert_close(host(dX[b]), dx, 1e-4 if dt == "f32" else 2e-2, "dX")
+        assert_close(host(dg[b]), dgr, 1e-4 if dt == "f32" else 2e-2, "dgamma")
+        assert_close(host(db[b]), dbr, 1e-4 if dt == "f32" else 2e-2, "dbeta")
+
+
+# ------------------------------------------------------------------ glue ----
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_transform_points(dt):
+    code, tdt = DT[dt]
+    B, N, L = 3, 4, 333
+    x = R.standard_normal((N, L, 3)).astype(np.float32).astype(np.float64)
+    F = rounded(R.standard_normal((B, N, 9)) * 0.1, tdt)
+    Y = torch.empty(B, N * L, 3, dtype=tdt, device=DEV)
+    xd = dev(x.reshape(N * L, 3))
+    H.hfta_transform_points_fwd(B, N, L, code, H.tin(xd, 0, 3), H.tin(dev(F, tdt), N * 9, 9), 1,
+                                H.tout(Y, N * L * 3, 3), s())
+    dY = rounded(R.standard_normal((B, N * L, 3)), tdt)
+    dF = torch.empty(B, N, 9, dtype=tdt, device=DEV)
+    H.hfta_transform_points_bwd(B, N, L, code, H.tin(xd, 0, 3), H.tin(dev(dY, tdt), N * L * 3, 3),
+                                H.tout(dF, N * 9, 9), s())
+    torch.cuda.synchronize()
+    for b in range(B):
+        T = F[b].reshape(N, 3, 3) + np.eye(3)
+        assert_close(host(Y[b]).reshape(N, L, 3), OL.transform_points(x, T), 1e-6 if dt == "f32" else 1e-2, "x'")
+        _, dT = OL.transform_points_bwd(dY[b].reshape(N, L, 3), x, T)
+        assert_close(host(dF[b]).reshape(N, 3, 3), dT, 1e-5 if dt == "f32" else 1e-2, "dT")
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_dropout_mask_bit_exact(dt):
+    code, tdt = DT[dt]
+    B, rows, cols, p = 3, 32, 257, 0.3
+    X = rounded(R.standard_normal((B, rows, cols)), tdt)
+    Y = torch.empty(B, rows, cols, dtype=tdt, device=DEV)
+    H.hfta_dropout_fwd(B, rows, cols, code, H.tin(dev(X, tdt), rows * cols, cols), H.tout(Y, rows * cols, cols), 42,
+                       5, 0, p, s())
+    torch.cuda.synchronize()
+    for b in range(B):
+        keep = dropout_keep_mask(42, b, 5, 0, rows * cols, p).reshape(rows, cols)
+        got = host(Y[b])
+        assert np.array_equal(got != 0, keep & (X[b] != 0))
+        assert_close(got, OL.dropout(X[b], keep, np.float32(p)), 1e-6 if dt == "f32" else 1e-2, "dropout")
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_loss_nll_mse(dt):
+    code, tdt = DT[dt]
+    B, rows, K = 3, 300, 50
+    Z = rounded(R.standard_normal((B, rows, K)) * 3, tdt)
+    y = R.integers(0, K, rows)
+    loss, ml = torch.empty(B, device=DEV), torch.empty(1, device=DEV)
+    dZ = torch.empty(B, rows, K, dtype=tdt, device=DEV)
+    ws = torch.empty(H.hfta_loss_workspace(B, rows), dtype=torch.uint8, device=DEV)
+    H.hfta_loss_nll(B, rows, K, code, H.tin(dev(Z, tdt), rows * K, K), H.ptr(dev(y, torch.int32)), 0, H.ptr(loss),
+                    H.ptr(ml), H.tout(dZ, rows * K, K), H.ptr(ws), ws.numel(), s())
+    torch.cuda.synchronize()
+    refs = []
+    for b in range(B):
+        l, dz = OL.nll_mean(Z[b], y)
+        refs.append(l)
+        assert abs(host(loss)[b] - l) <= 1e-5 * abs(l)
+        assert_close(host(dZ[b]), dz, 1e-5 if dt == "f32" else 1e-2, "dlogits")
+    assert abs(host(ml)[0] - np.mean(refs)) <= 1e-5 * abs(np.mean(refs))      # App. C Eq. 1
+    A = rounded(R.standard_normal((B, rows, 64)), tdt)
+    T = R.standard_normal((rows, 64)).astype(np.float32).astype(np.float64)
+    dA = torch.empty(B, rows, 64, dtype=tdt, device=DEV)
+    H.hfta_loss_mse(B, rows, 64, code, H.tin(dev(A, tdt), rows * 64, 64), H.ptr(dev(T)), 0, 64, H.ptr(loss),
+                    H.ptr(ml), H.tout(dA, rows * 64, 64), H.ptr(ws), ws.numel(), s())
+    torch.cuda.synchronize()
+    for b in range(B):
+        l, da = OL.mse_mean(A[b], T)
+        assert abs(host(loss)[b] - l) <= 1e-5 * abs(l)
+        assert_close(host(dA[b]), da, 1e-5 if dt == "f32" else 1e-2, "dA")
+
+
+@pytest.mark.parametrize("P,shadow", [(4672, True), (1001, False)])
+def test_fused_adam(P, shadow):
+    B, T = 3, 4
+    hp = dict(lr=np.float32([1e-3, 3e-3, 1e-2]), beta1=np.float32([0.9, 0.8, 0.5]),
+              beta2=np.float32([0.999, 0.99, 0.9]), eps=np.float32([1e-8, 1e-6, 1e-4]),
+              wd=np.float32([0.0, 1e-2, 0.3]))
+    p0 = R.standard_normal((B, P)).astype(np.float32)
+    pd, gd = dev(p0), torch.empty(B, P, device=DEV)
+    md, vd = torch.zeros(B, P, device=DEV), torch.zeros(B, P, device=DEV)
+    sh = torch.empty(B, P, dtype=torch.bfloat16, device=DEV) if shadow else None
+    hv = {k: dev(v) for k, v in hp.items()}
+    step = torch.zeros(1, dtype=torch.int64, device=DEV)
+    ps = [p0[b].astype(np.float64) for b in range(B)]
+    ms = [np.zeros(P) for _ in range(B)]
+    vs = [np.zeros(P) for _ in range(B)]
+    for t in range(1, T + 1):
+        g = R.standard_normal((B, P)).astype(np.float32)
+        gd.copy_(torch.from_numpy(g))
+        H.hfta_step_increment(H.ptr(step), s())
+        H.hfta_fused_adam(B, P, H.ptr(pd), H.ptr(gd), H.ptr(md), H.ptr(vd), P, H.ptr(hv["lr"]), H.ptr(hv["beta1"]),
+                          H.ptr(hv["beta2"]), H.ptr(hv["eps"]), H.ptr(hv["wd"]), H.ptr(step), H.ptr(sh), P, s())
+        for b in range(B):
+            ps[b], ms[b], vs[b] = adam_step(ps[b], g[b].astype(np.float64), ms[b], vs[b], t,
+                                            *(float(hp[k][b]) for k in ("lr", "beta1", "beta2", "eps", "wd")))
+    torch.cuda.synchronize()
+    for b in range(B):
+        assert_close(host(pd[b]), ps[b], 1e-6, "param")
+        assert_close(host(md[b]), ms[b], 1e-6, "m")
+        assert_close(host(vd[b]), vs[b], 1e-6, "v")
+        if shadow:
+            assert np.array_equal(host(sh[b]), rounded(host(pd[b]), torch.bfloat16))
