@@ -161,7 +161,9 @@ hfta_status hfta_fused_bn_bwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_i
  * App. B row MaxPool family P:L1286-1287 as used by the cited model):
  *   out[b][n][c] = max_l act(gamma*(X[b][n*L+l][c]-mean)*invstd + beta)
  *   argmax[b][n][c] = first l attaining it (reading R15), int32.
- * X [B][N*L][C] dtype dt; out [B][N][C] dtype dt (ld = out.ld).
+ * X [B][N*L][C] dtype dt; out [B][N][C] fp32 (ld = out.ld).  Per-sample
+ * tensors ([N] rows: pooled features, the FC head, the 3x3 transform) are
+ * fp32 in both precision modes.
  */
 hfta_status hfta_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C, hfta_dtype dt, hfta_in X,
                             const float* gamma, const float* beta, int64_t gb_bstride,
@@ -170,7 +172,7 @@ hfta_status hfta_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C, hfta_dtype d
                             hfta_stream stream);
 /*
  * Backward of hfta_bn_max_fwd followed by the BN backward: dG [B][N][C]
- * (dtype dt) is scattered to the argmax rows, passed through act' and BN
+ * (fp32) is scattered to the argmax rows, passed through act' and BN
  * backward; writes dX [B][N*L][C] (dtype dt) and dgamma/dbeta.
  * Workspace: hfta_bn_max_bwd_workspace().
  */
@@ -185,13 +187,13 @@ hfta_status hfta_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C, hfta_dtype d
 /*
  * PointNet input transform (STN): T_b,n = F_b[n] viewed as 3x3 row-major
  * (+ I3 if add_identity), x'_b[n*L+l][:] = x[n*L+l][:] * T_b,n.
- * X fp32 [B][N*L][3] (bstride 0 = shared), F dtype dt [B][N][9] (ld >= 9),
+ * X fp32 [B][N*L][3] (bstride 0 = shared), F fp32 [B][N][9] (ld >= 9),
  * Xout dtype dt [B][N*L][3] (ld >= 3).
  */
 hfta_status hfta_transform_points_fwd(int B, int64_t N, int64_t L, hfta_dtype dt, hfta_in X,
                                       hfta_in F, int add_identity, hfta_out Xout,
                                       hfta_stream stream);
-/* dF_b[n] = sum_l x[n*L+l]^T dXout_b[n*L+l]   (dtype dt [B][N][9]; dX not needed). */
+/* dF_b[n] = sum_l x[n*L+l]^T dXout_b[n*L+l]   (fp32 [B][N][9]; dX not needed). */
 hfta_status hfta_transform_points_bwd(int B, int64_t N, int64_t L, hfta_dtype dt, hfta_in X,
                                       hfta_in dXout, hfta_out dF, hfta_stream stream);
 /*

@@ -23,6 +23,30 @@ from .philox import dropout_keep_mask
 
 
 # ------------------------------------------------------------- helpers ----
+# Decision margins (reading R15b).  ReLU'(z) and the argmax of a max-pool are
+# discontinuous decisions; an element whose decision is within rounding
+# distance of the threshold may legitimately be taken either way by a
+# lower-precision implementation.  When `MARGINS` is a list, every ReLU and
+# max-pool of a forward pass appends its smallest relative margin:
+#   ReLU: min_r,c |z| / rms(z)    max-pool: min_n,c (top1 - top2) / |top1|
+MARGINS = None
+
+
+def _note(kind, name, value):
+    if MARGINS is not None:
+        MARGINS.append((kind, name, float(value)))
+
+
+def _relu_margin(name, z):
+    if MARGINS is not None:
+        _note("relu", name, np.min(np.abs(z)) / max(np.sqrt(np.mean(z * z)), 1e-300))
+
+
+def _max_margin(name, x):
+    if MARGINS is not None:
+        s = np.sort(x, axis=1)
+        _note("max", name, np.min((s[:, -1] - s[:, -2]) / np.maximum(np.abs(s[:, -1]), 1e-300)))
+
 
 def _bn_state(state, name, C):
     return state.get(name + ".rm", np.zeros(C)), state.get(name + ".rv", np.ones(C))
@@ -34,6 +58,8 @@ def _conv_bn_act(P, S, newS, r, conv, bn, act):
     z, c = Lr.bn_fwd(y, P[bn + ".g"], P[bn + ".beta"])
     rm, rv = _bn_state(S, bn, y.shape[1])
     newS[bn + ".rm"], newS[bn + ".rv"] = Lr.bn_running(rm, rv, c, y.shape[0])
+    if act == "relu":
+        _relu_margin(bn, z)
     a = Lr.relu(z) if act == "relu" else z
     return a, dict(r=r, z=z, bn=c, conv=conv, bnn=bn, act=act)
 
@@ -67,6 +93,7 @@ def _stn_fwd(P, S, newS, x):
     a1, k1 = _conv_bn_act(P, S, newS, r, "stn.c1", "stn.bn1", "relu")
     a2, k2 = _conv_bn_act(P, S, newS, a1, "stn.c2", "stn.bn2", "relu")
     a3, k3 = _conv_bn_act(P, S, newS, a2, "stn.c3", "stn.bn3", "relu")
+    _max_margin("stn.max", a3.reshape(N, L, -1))
     g, idx = Lr.max_over_points(a3.reshape(N, L, -1))
     f1, k4 = _conv_bn_act(P, S, newS, g, "stn.fc1", "stn.bn4", "relu")
     f2, k5 = _conv_bn_act(P, S, newS, f1, "stn.fc2", "stn.bn5", "relu")
@@ -95,6 +122,7 @@ def _feat_fwd(P, S, newS, x):
     a1, k1 = _conv_bn_act(P, S, newS, r, "feat.c1", "feat.bn1", "relu")
     a2, k2 = _conv_bn_act(P, S, newS, a1, "feat.c2", "feat.bn2", "relu")
     z3, k3 = _conv_bn_act(P, S, newS, a2, "feat.c3", "feat.bn3", None)
+    _max_margin("feat.max", z3.reshape(N, L, -1))
     g, idx = Lr.max_over_points(z3.reshape(N, L, -1))
     return g, a1, dict(T=T, stn=stn_c, x=x, k=(k1, k2, k3), idx=idx, L=L)
 
@@ -122,6 +150,7 @@ def pointnet_cls_loss_grads(P, S, x, labels, keep, p_drop):
     z2, bn2 = Lr.bn_fwd(d2, P["head.bn2.g"], P["head.bn2.beta"])
     rm, rv = _bn_state(S, "head.bn2", d2.shape[1])
     newS["head.bn2.rm"], newS["head.bn2.rv"] = Lr.bn_running(rm, rv, bn2, d2.shape[0])
+    _relu_margin("head.bn2", z2)
     h2 = Lr.relu(z2)
     logits = Lr.linear_fwd(h2, P["head.fc3.W"], P["head.fc3.b"])
     loss, dlogits = Lr.nll_mean(logits, labels)
@@ -292,6 +321,17 @@ def train_step(arch, P, S, opt, batch, t, hp_b, b=0, dropout_seed=42, p_drop=0.3
         raise ValueError(arch)
     newP, newOpt = adam_model(P, G, opt, t, hp_b)
     return dict(loss=loss, grads=G, params=newP, opt=newOpt, stats=newS, out=out)
+
+
+def decision_margins(arch, P, batch, t=1, b=0, **kw):
+    """Smallest ReLU / max-pool margins of one model's forward (reading R15b)."""
+    global MARGINS
+    MARGINS = []
+    try:
+        train_step(arch, P, {}, {}, batch, t, dict(lr=0.0, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.0), b=b, **kw)
+        return list(MARGINS)
+    finally:
+        MARGINS = None
 
 
 def fused_step_oracle(arch, Ps, Ss, opts, batch, t, hp, **kw):

@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(NT) k_bn_max_fwd(int64_t L, int64_t C, const T
                                                    int64_t xld, const float* __restrict__ gamma,
                                                    const float* __restrict__ beta, int64_t gbs,
                                                    const float* __restrict__ smean, const float* __restrict__ sinv,
-                                                   int act, float alpha, T* __restrict__ out, int64_t obs,
+                                                   int act, float alpha, float* __restrict__ out, int64_t obs,
                                                    int64_t old, int32_t* __restrict__ amax, int64_t N, Geo g) {
   __shared__ float sv[NT * VEC];
   __shared__ int si[NT * VEC];
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(NT) k_bn_max_fwd(int64_t L, int64_t C, const T
       int ix = si[r * g.cb + col];
       if (v > bv || (v == bv && ix < bidx)) { bv = v; bidx = ix; }   // first index on ties (R15)
     }
-    stf(out + (int64_t)b * obs + n * old + c, bv);
+    out[(int64_t)b * obs + n * old + c] = bv;
     amax[((int64_t)b * N + n) * C + c] = bidx;
   }
 }
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(NT) k_bn_max_fwd(int64_t L, int64_t C, const T
 // step 1 of the max backward: per (b, c) loop over samples n: dz at the argmax
 // row, dbeta = sum dz, dgamma = sum dz*xhat; writes coef (k1,k2,k3) and dz [B][N][C].
 template <typename T>
-__global__ void k_bn_max_bwd_small(int B, int64_t N, int64_t L, int64_t C, const T* __restrict__ dG, int64_t gbs_,
+__global__ void k_bn_max_bwd_small(int B, int64_t N, int64_t L, int64_t C, const float* __restrict__ dG, int64_t gbs_,
                                    int64_t gld, const T* __restrict__ X, int64_t xbs, int64_t xld,
                                    const int32_t* __restrict__ amax, const float* __restrict__ gamma,
                                    const float* __restrict__ beta, int64_t gbs, const float* __restrict__ smean,
@@ -337,7 +337,7 @@ __global__ void k_bn_max_bwd_small(int B, int64_t N, int64_t L, int64_t C, const
     int64_t l = amax[(b * N + n) * C + c];
     float x = ldf(X + b * xbs + (n * L + l) * xld + c);
     float xh = (x - m) * is;
-    float dz = ldf(dG + b * gbs_ + n * gld + c) * act_grad(fmaf(ga, xh, be), act, alpha);
+    float dz = dG[b * gbs_ + n * gld + c] * act_grad(fmaf(ga, xh, be), act, alpha);
     dz_out[(b * N + n) * C + c] = dz;
     s1 += dz;
     s2 += (double)dz * xh;
@@ -514,7 +514,7 @@ hfta_status hfta_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C, hfta_dtype d
   dim3 grid(g.colgroups, (unsigned)N, B);
   DT_DISPATCH(dt, {
     LAUNCH_VEC(T, vec, k_bn_max_fwd, grid, L, C, (const T*)X.ptr, X.bstride, X.ld, gamma, beta, gb_bstride,
-               save_mean, save_invstd, (int)act, act_alpha, (T*)out.ptr, out.bstride, out.ld, argmax, N, g);
+               save_mean, save_invstd, (int)act, act_alpha, (float*)out.ptr, out.bstride, out.ld, argmax, N, g);
   });
   count_launches(1);
   return post_launch(s, "hfta_bn_max_fwd");
@@ -545,7 +545,7 @@ hfta_status hfta_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C, hfta_dtype d
   dim3 grid(g.colgroups, g.chunks, B);
   DT_DISPATCH(dt, {
     k_bn_max_bwd_small<T><<<(unsigned)cdiv((int64_t)B * C, 128), 128, 0, s>>>(
-        B, N, L, C, (const T*)dG.ptr, dG.bstride, dG.ld, (const T*)X.ptr, X.bstride, X.ld, argmax, gamma, beta,
+        B, N, L, C, (const float*)dG.ptr, dG.bstride, dG.ld, (const T*)X.ptr, X.bstride, X.ld, argmax, gamma, beta,
         gb_bstride, save_mean, save_invstd, (int)act, act_alpha, dgamma, dbeta, coef, dz);
     LAUNCH_VEC(T, vec, k_bn_max_bwd_apply, grid, B, N, L, C, (const T*)X.ptr, X.bstride, X.ld, argmax, dz,
                (T*)dX.ptr, dX.bstride, dX.ld, save_mean, save_invstd, coef, g);

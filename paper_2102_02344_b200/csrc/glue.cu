@@ -12,13 +12,13 @@ namespace {
 // ---------------------------------------------------- transform points --
 template <typename T>
 __global__ void k_transform_fwd(int64_t N, int64_t L, const float* __restrict__ X, int64_t xbs, int64_t xld,
-                                const T* __restrict__ F, int64_t fbs, int64_t fld, int add_id, T* __restrict__ Y,
+                                const float* __restrict__ F, int64_t fbs, int64_t fld, int add_id, T* __restrict__ Y,
                                 int64_t ybs, int64_t yld) {
   const int b = blockIdx.y;
   const int64_t R = N * L;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = r / L;
-    const T* t = F + (int64_t)b * fbs + n * fld;
+    const float* t = F + (int64_t)b * fbs + n * fld;
     const float* x = X + (int64_t)b * xbs + r * xld;
     float x0 = x[0], x1 = x[1], x2 = x[2];
     T* y = Y + (int64_t)b * ybs + r * yld;
@@ -35,7 +35,7 @@ __global__ void k_transform_fwd(int64_t N, int64_t L, const float* __restrict__ 
 // dF[b][n][i*3+j] = sum_l x[n*L+l][i] * dY[b][n*L+l][j]; one block per (n, b).
 template <typename T>
 __global__ void k_transform_bwd(int64_t N, int64_t L, const float* __restrict__ X, int64_t xbs, int64_t xld,
-                                const T* __restrict__ dY, int64_t dbs, int64_t dld, T* __restrict__ dF,
+                                const T* __restrict__ dY, int64_t dbs, int64_t dld, float* __restrict__ dF,
                                 int64_t fbs, int64_t fld) {
   __shared__ float red[9][256];
   const int b = blockIdx.y;
@@ -62,7 +62,7 @@ __global__ void k_transform_bwd(int64_t N, int64_t L, const float* __restrict__ 
       for (int q = 0; q < 9; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x < 9) stf(dF + (int64_t)b * fbs + n * fld + threadIdx.x, red[threadIdx.x][0]);
+  if (threadIdx.x < 9) dF[(int64_t)b * fbs + n * fld + threadIdx.x] = red[threadIdx.x][0];
 }
 
 // ------------------------------------------------------------- Philox --
@@ -195,7 +195,7 @@ hfta_status hfta_transform_points_fwd(int B, int64_t N, int64_t L, hfta_dtype dt
                                                F.bstride, F.ld, add_identity, (float*)Xout.ptr, Xout.bstride, Xout.ld);
   else
     k_transform_fwd<__nv_bfloat16><<<grid, 256, 0, s>>>(N, L, (const float*)X.ptr, X.bstride, X.ld,
-                                                       (const __nv_bfloat16*)F.ptr, F.bstride, F.ld, add_identity,
+                                                       (const float*)F.ptr, F.bstride, F.ld, add_identity,
                                                        (__nv_bfloat16*)Xout.ptr, Xout.bstride, Xout.ld);
   count_launches(1);
   return post_launch(s, "hfta_transform_points_fwd");
@@ -215,7 +215,7 @@ hfta_status hfta_transform_points_bwd(int B, int64_t N, int64_t L, hfta_dtype dt
   else
     k_transform_bwd<__nv_bfloat16><<<grid, 256, 0, s>>>(N, L, (const float*)X.ptr, X.bstride, X.ld,
                                                        (const __nv_bfloat16*)dXout.ptr, dXout.bstride, dXout.ld,
-                                                       (__nv_bfloat16*)dF.ptr, dF.bstride, dF.ld);
+                                                       (float*)dF.ptr, dF.bstride, dF.ld);
   count_launches(1);
   return post_launch(s, "hfta_transform_points_bwd");
 }

@@ -67,34 +67,35 @@ class FusedPointNet:
     def _alloc(self):
         B, N, R = self.B, self.N, self.R
         c1, c2, c3, f1, f2 = self.c1, self.c2, self.c3, self.f1, self.f2
-        a = _Acts(B, self.tdt, self.device)
+        a = _Acts(B, self.tdt, self.device)          # per-point tensors: dt
+        f = _Acts(B, torch.float32, self.device)     # per-sample tensors: fp32 in both modes
         self.x_dt = torch.empty(R, 3, dtype=self.tdt, device=self.device)
         S = {}
         for p in ("stn", "feat"):
             S[p + ".y1"], S[p + ".a1"] = a(R, c1), a(R, c1)
             S[p + ".y2"], S[p + ".a2"] = a(R, c2), a(R, c2)
             S[p + ".y3"] = a(R, c3)
-            S[p + ".g"] = a(N, c3)
+            S[p + ".g"] = f(N, c3)
             S[p + ".amax"] = torch.empty(B, N, c3, dtype=torch.int32, device=self.device)
-        S["stn.f1"], S["stn.h4"] = a(N, f1), a(N, f1)
-        S["stn.f2"], S["stn.h5"] = a(N, f2), a(N, f2)
-        S["stn.f3"] = a(N, 9)
+        S["stn.f1"], S["stn.h4"] = f(N, f1), f(N, f1)
+        S["stn.f2"], S["stn.h5"] = f(N, f2), f(N, f2)
+        S["stn.f3"] = f(N, 9)
         S["feat.xt"] = a(R, 3)
         if self.task == "cls":
-            S["head.y1"], S["head.h1"] = a(N, f1), a(N, f1)
-            S["head.y2"], S["head.d2"], S["head.h2"] = a(N, f2), a(N, f2), a(N, f2)
-            S["head.logits"] = a(N, self.k)
-            S["d.logits"] = a(N, self.k)
-            S["d.f2a"], S["d.f2b"] = a(N, f2), a(N, f2)
-            S["d.f1a"], S["d.f1b"] = a(N, f1), a(N, f1)
+            S["head.y1"], S["head.h1"] = f(N, f1), f(N, f1)
+            S["head.y2"], S["head.d2"], S["head.h2"] = f(N, f2), f(N, f2), f(N, f2)
+            S["head.logits"] = f(N, self.k)
+            S["d.logits"] = f(N, self.k)
+            S["d.f2a"], S["d.f2b"] = f(N, f2), f(N, f2)
+            S["d.f1a"], S["d.f1b"] = f(N, f1), f(N, f1)
         S["d.big"] = a(R, c3)
         S["d.c2a"], S["d.c2b"] = a(R, c2), a(R, c2)
         S["d.c1a"], S["d.c1b"] = a(R, c1), a(R, c1)
-        S["d.g"] = a(N, c3)
+        S["d.g"] = f(N, c3)
         S["d.xt"] = a(R, 3)
-        S["d.f3"] = a(N, 9)
-        S["d.sf1a"], S["d.sf1b"] = a(N, f1), a(N, f1)
-        S["d.sf2a"], S["d.sf2b"] = a(N, f2), a(N, f2)
+        S["d.f3"] = f(N, 9)
+        S["d.sf1a"], S["d.sf1b"] = f(N, f1), f(N, f1)
+        S["d.sf2a"], S["d.sf2b"] = f(N, f2), f(N, f2)
         self.S = S
         self.loss = torch.zeros(B, device=self.device)
         self.mean_loss = torch.zeros(1, device=self.device)
@@ -102,7 +103,8 @@ class FusedPointNet:
         ws = Workspace(self.device)
         for (M, Nn, K) in [(R, c1, 3), (R, c2, c1), (R, c3, c2), (N, f1, c3), (N, f2, f1), (N, 9, f2),
                            (N, self.k, f2)]:
-            ws.reserve(H.hfta_fused_linear_bwd_workspace(B, M, Nn, K, self.dt))
+            for dt in (self.dt, H.HFTA_F32):
+                ws.reserve(H.hfta_fused_linear_bwd_workspace(B, M, Nn, K, dt))
         for (Rr, Cc) in [(R, c1), (R, c2), (R, c3), (N, f1), (N, f2)]:
             ws.reserve(H.hfta_fused_bn_workspace(B, Rr, Cc))
         ws.reserve(H.hfta_bn_max_bwd_workspace(B, N, c3))
@@ -111,14 +113,19 @@ class FusedPointNet:
         self.ws = ws
 
     # ----------------------------------------------------------- wrappers --
+    def _dt(self, t):
+        return H.HFTA_F32 if t.dtype == torch.float32 else H.HFTA_BF16
+
     def _lin_fwd(self, X, M, name, Y, s):
         Nn, K = self.arena.shape[name + ".W"]
-        H.hfta_fused_linear_fwd(self.B, M, Nn, K, self.dt, X, self.arena.w_in(name + ".W", self.dt),
+        dt = self._dt(Y)
+        H.hfta_fused_linear_fwd(self.B, M, Nn, K, dt, X, self.arena.w_in(name + ".W", dt),
                                 self.arena.fptr("p", name + ".b"), self.arena.P, 0, 0, _out(Y), s)
 
     def _lin_bwd(self, dY, X, M, name, dX, s, accumulate=0):
         Nn, K = self.arena.shape[name + ".W"]
-        H.hfta_fused_linear_bwd(self.B, M, Nn, K, self.dt, _in(dY), X, self.arena.w_in(name + ".W", self.dt),
+        dt = self._dt(dY)
+        H.hfta_fused_linear_bwd(self.B, M, Nn, K, dt, _in(dY), X, self.arena.w_in(name + ".W", dt),
                                 _out(dX) if dX is not None else H.tout(None, 0, 1),
                                 self.arena.fptr("g", name + ".W"), self.arena.P,
                                 self.arena.fptr("g", name + ".b"), self.arena.P, accumulate,
@@ -128,7 +135,7 @@ class FusedPointNet:
         R, C = X.shape[1], X.shape[2]
         rm, rv = self.running[name]
         sm, si = self.saved[name]
-        H.hfta_fused_bn_fwd(self.B, R, C, self.dt, _in(X), self.arena.fptr("p", name + ".g"),
+        H.hfta_fused_bn_fwd(self.B, R, C, self._dt(X), _in(X), self.arena.fptr("p", name + ".g"),
                             self.arena.fptr("p", name + ".beta"), self.arena.P, H.ptr(rm), H.ptr(rv), 0.1, 1e-5,
                             act, 0.0, _out(Y) if Y is not None else H.tout(None, 0, 1), H.ptr(sm), H.ptr(si),
                             self.ws.ptr, self.ws.nbytes, s)
@@ -136,7 +143,7 @@ class FusedPointNet:
     def _bn_bwd(self, dY, X, name, act, dX, s):
         R, C = X.shape[1], X.shape[2]
         sm, si = self.saved[name]
-        H.hfta_fused_bn_bwd(self.B, R, C, self.dt, _in(dY), _in(X), self.arena.fptr("p", name + ".g"),
+        H.hfta_fused_bn_bwd(self.B, R, C, self._dt(X), _in(dY), _in(X), self.arena.fptr("p", name + ".g"),
                             self.arena.fptr("p", name + ".beta"), self.arena.P, H.ptr(sm), H.ptr(si), act, 0.0,
                             _out(dX), self.arena.fptr("g", name + ".g"), self.arena.fptr("g", name + ".beta"), 0,
                             self.ws.ptr, self.ws.nbytes, s)
@@ -210,15 +217,15 @@ class FusedPointNet:
         self._lin_fwd(_in(S["feat.g"]), N, "head.fc1", S["head.y1"], s)
         self._bn_fwd(S["head.y1"], "head.bn1", A_RELU, S["head.h1"], s)
         self._lin_fwd(_in(S["head.h1"]), N, "head.fc2", S["head.y2"], s)
-        H.hfta_dropout_fwd(self.B, N, self.f2, self.dt, _in(S["head.y2"]), _out(S["head.d2"]), self.dropout_seed,
+        H.hfta_dropout_fwd(self.B, N, self.f2, H.HFTA_F32, _in(S["head.y2"]), _out(S["head.d2"]), self.dropout_seed,
                            self.t, 0, self.p_drop, s)
         self._bn_fwd(S["head.d2"], "head.bn2", A_RELU, S["head.h2"], s)
         self._lin_fwd(_in(S["head.h2"]), N, "head.fc3", S["head.logits"], s)
-        H.hfta_loss_nll(self.B, N, self.k, self.dt, _in(S["head.logits"]), H.ptr(self.labels), 0, H.ptr(self.loss),
+        H.hfta_loss_nll(self.B, N, self.k, H.HFTA_F32, _in(S["head.logits"]), H.ptr(self.labels), 0, H.ptr(self.loss),
                         H.ptr(self.mean_loss), _out(S["d.logits"]), self.ws.ptr, self.ws.nbytes, s)
         self._lin_bwd(S["d.logits"], _in(S["head.h2"]), N, "head.fc3", S["d.f2a"], s)
         self._bn_bwd(S["d.f2a"], S["head.d2"], "head.bn2", A_RELU, S["d.f2b"], s)
-        H.hfta_dropout_bwd(self.B, N, self.f2, self.dt, _in(S["d.f2b"]), _out(S["d.f2a"]), self.dropout_seed,
+        H.hfta_dropout_bwd(self.B, N, self.f2, H.HFTA_F32, _in(S["d.f2b"]), _out(S["d.f2a"]), self.dropout_seed,
                            self.t, 0, self.p_drop, s)
         self._lin_bwd(S["d.f2a"], _in(S["head.h1"]), N, "head.fc2", S["d.f1a"], s)
         self._bn_bwd(S["d.f1a"], S["head.y1"], "head.bn1", A_RELU, S["d.f1b"], s)

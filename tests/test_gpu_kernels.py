@@ -87,14 +87,15 @@ def test_linear_bwd_accumulate_and_rowgroup_bias():
     W = R.standard_normal((B, N, K)).astype(np.float32).astype(np.float64)
     tab = R.standard_normal((B, M // L, N)).astype(np.float32).astype(np.float64)
     Y = torch.empty(B, M, N, device=DEV)
-    H.hfta_fused_linear_fwd(B, M, N, K, 0, H.tin(dev(X), M * K, K), H.tin(dev(W), N * K, K), H.ptr(dev(tab)),
+    Xd, Wd, tabd = dev(X), dev(W), dev(tab)      # keep references: the launch is asynchronous
+    H.hfta_fused_linear_fwd(B, M, N, K, 0, H.tin(Xd, M * K, K), H.tin(Wd, N * K, K), H.ptr(tabd),
                             (M // L) * N, N, L, H.tout(Y, M * N, N), s())
     dY = R.standard_normal((B, M, N)).astype(np.float32).astype(np.float64)
     dW0 = R.standard_normal((B, N, K)).astype(np.float32).astype(np.float64)
-    dW = dev(dW0)
+    dW, dYd = dev(dW0), dev(dY)
     ws = torch.empty(max(H.hfta_fused_linear_bwd_workspace(B, M, N, K, 0), 1), dtype=torch.uint8, device=DEV)
-    H.hfta_fused_linear_bwd(B, M, N, K, 0, H.tin(dev(dY), M * N, N), H.tin(dev(X), M * K, K),
-                            H.tin(dev(W), N * K, K), H.tout(None, 0, 1), H.ptr(dW), N * K, None, 0, 1,
+    H.hfta_fused_linear_bwd(B, M, N, K, 0, H.tin(dYd, M * N, N), H.tin(Xd, M * K, K),
+                            H.tin(Wd, N * K, K), H.tout(None, 0, 1), H.ptr(dW), N * K, None, 0, 1,
                             H.ptr(ws), ws.numel(), s())
     torch.cuda.synchronize()
     for b in range(B):
@@ -170,14 +171,15 @@ def test_bn_max_fwd_bwd(dt, act):
                      dtype=torch.uint8, device=DEV)
     H.hfta_fused_bn_fwd(B, Rr, C, code, H.tin(Xd, Rr * C, C), H.ptr(gd), H.ptr(bed), C, None, None, 0.1, 1e-5, act,
                         0.0, H.tout(None, 0, 1), H.ptr(sm), H.ptr(si), H.ptr(ws), ws.numel(), s())
-    G = torch.empty(B, N, C, dtype=tdt, device=DEV)
+    G = torch.empty(B, N, C, device=DEV)                   # per-sample tensors are fp32
     am = torch.empty(B, N, C, dtype=torch.int32, device=DEV)
     H.hfta_bn_max_fwd(B, N, L, C, code, H.tin(Xd, Rr * C, C), H.ptr(gd), H.ptr(bed), C, H.ptr(sm), H.ptr(si), act,
                       0.0, H.tout(G, N * C, C), H.ptr(am), s())
-    dG = rounded(R.standard_normal((B, N, C)), tdt)
+    dG = R.standard_normal((B, N, C)).astype(np.float32).astype(np.float64)
+    dGd = dev(dG)
     dX = torch.empty(B, Rr, C, dtype=tdt, device=DEV)
     dg, db = torch.empty(B, C, device=DEV), torch.empty(B, C, device=DEV)
-    H.hfta_bn_max_bwd(B, N, L, C, code, H.tin(dev(dG, tdt), N * C, C), H.tin(Xd, Rr * C, C), H.ptr(am), H.ptr(gd),
+    H.hfta_bn_max_bwd(B, N, L, C, code, H.tin(dGd, N * C, C), H.tin(Xd, Rr * C, C), H.ptr(am), H.ptr(gd),
                       H.ptr(bed), C, H.ptr(sm), H.ptr(si), act, 0.0, H.tout(dX, Rr * C, C), H.ptr(dg), H.ptr(db),
                       H.ptr(ws), ws.numel(), s())
     torch.cuda.synchronize()
@@ -187,7 +189,7 @@ def test_bn_max_fwd_bwd(dt, act):
         gmax, idx = OL.max_over_points(a.reshape(N, L, C))
         if dt == "f32":
             assert np.array_equal(host(am[b]).astype(np.int64), idx)
-        assert_close(host(G[b]), gmax, 1e-5 if dt == "f32" else 1e-2, "max")
+        assert_close(host(G[b]), gmax, 1e-5 if dt == "f32" else 1e-3, "max")
         da = OL.max_over_points_bwd(dG[b], host(am[b]).astype(np.int64), L).reshape(Rr, C)
         dz = OL.relu_bwd(da, z) if act else da
         dx, dgr, dbr = OL.bn_bwd(dz, c, g[b])
@@ -202,13 +204,13 @@ def test_transform_points(dt):
     code, tdt = DT[dt]
     B, N, L = 3, 4, 333
     x = R.standard_normal((N, L, 3)).astype(np.float32).astype(np.float64)
-    F = rounded(R.standard_normal((B, N, 9)) * 0.1, tdt)
+    F = R.standard_normal((B, N, 9)).astype(np.float32).astype(np.float64) * 0.1
     Y = torch.empty(B, N * L, 3, dtype=tdt, device=DEV)
-    xd = dev(x.reshape(N * L, 3))
-    H.hfta_transform_points_fwd(B, N, L, code, H.tin(xd, 0, 3), H.tin(dev(F, tdt), N * 9, 9), 1,
+    xd, Fd = dev(x.reshape(N * L, 3)), dev(F)
+    H.hfta_transform_points_fwd(B, N, L, code, H.tin(xd, 0, 3), H.tin(Fd, N * 9, 9), 1,
                                 H.tout(Y, N * L * 3, 3), s())
     dY = rounded(R.standard_normal((B, N * L, 3)), tdt)
-    dF = torch.empty(B, N, 9, dtype=tdt, device=DEV)
+    dF = torch.empty(B, N, 9, device=DEV)
     H.hfta_transform_points_bwd(B, N, L, code, H.tin(xd, 0, 3), H.tin(dev(dY, tdt), N * L * 3, 3),
                                 H.tout(dF, N * 9, 9), s())
     torch.cuda.synchronize()
@@ -216,7 +218,7 @@ def test_transform_points(dt):
         T = F[b].reshape(N, 3, 3) + np.eye(3)
         assert_close(host(Y[b]).reshape(N, L, 3), OL.transform_points(x, T), 1e-6 if dt == "f32" else 1e-2, "x'")
         _, dT = OL.transform_points_bwd(dY[b].reshape(N, L, 3), x, T)
-        assert_close(host(dF[b]).reshape(N, 3, 3), dT, 1e-5 if dt == "f32" else 1e-2, "dT")
+        assert_close(host(dF[b]).reshape(N, 3, 3), dT, 1e-5, "dT")
 
 
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
@@ -244,7 +246,8 @@ def test_loss_nll_mse(dt):
     loss, ml = torch.empty(B, device=DEV), torch.empty(1, device=DEV)
     dZ = torch.empty(B, rows, K, dtype=tdt, device=DEV)
     ws = torch.empty(H.hfta_loss_workspace(B, rows), dtype=torch.uint8, device=DEV)
-    H.hfta_loss_nll(B, rows, K, code, H.tin(dev(Z, tdt), rows * K, K), H.ptr(dev(y, torch.int32)), 0, H.ptr(loss),
+    Zd, yd = dev(Z, tdt), dev(y, torch.int32)
+    H.hfta_loss_nll(B, rows, K, code, H.tin(Zd, rows * K, K), H.ptr(yd), 0, H.ptr(loss),
                     H.ptr(ml), H.tout(dZ, rows * K, K), H.ptr(ws), ws.numel(), s())
     torch.cuda.synchronize()
     refs = []
@@ -257,7 +260,8 @@ def test_loss_nll_mse(dt):
     A = rounded(R.standard_normal((B, rows, 64)), tdt)
     T = R.standard_normal((rows, 64)).astype(np.float32).astype(np.float64)
     dA = torch.empty(B, rows, 64, dtype=tdt, device=DEV)
-    H.hfta_loss_mse(B, rows, 64, code, H.tin(dev(A, tdt), rows * 64, 64), H.ptr(dev(T)), 0, 64, H.ptr(loss),
+    Ad, Td = dev(A, tdt), dev(T)
+    H.hfta_loss_mse(B, rows, 64, code, H.tin(Ad, rows * 64, 64), H.ptr(Td), 0, 64, H.ptr(loss),
                     H.ptr(ml), H.tout(dA, rows * 64, 64), H.ptr(ws), ws.numel(), s())
     torch.cuda.synchronize()
     for b in range(B):
