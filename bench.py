@@ -1,0 +1,284 @@
+#!/usr/bin/env python
+"""Benchmark of the HFTA fused training step on B200 (BJ metric: fused
+models x samples / sec per B200).
+
+Workload (BJ configs[1]): PointNet-cls, ModelNet40-shaped synthetic point
+clouds (batch N=32, L=2500 points, k=40 classes), B fused models with
+per-model hyper-parameters, bf16-AMP (per-point tensors bf16, per-sample
+tensors/statistics/optimizer fp32), one step = forward + backward + fused
+Adam over all B models.  `value` = B * N * steps / time (device-timed, inputs
+resident in HBM), summed over ranks (weak scaling: B models per GPU).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--B 64] [--dtype bf16|f32]
+  python bench.py --impl reference ...   (the CPU oracle, bounded sample)
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused models x samples/sec per B200 (PointNet-cls, HFTA fused training step)"
+UNIT = "model-samples/s"
+
+
+def peaks():
+    p = dict(hbm_gbs=6650.0, bf16_tflops=1590.0, bf16_tflops_sustained=1400.0, sm_max_mhz=1965.0,
+             source="fallback (B200_PROFILING.md)")
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: float(m[k]) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained", "sm_max_mhz") if k in m})
+        p["source"] = "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        pass
+    return p
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (recipe clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 9]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ oracle --
+
+def cpu_oracle_sample(n_samples=8, L=2500, k=40, steps=1):
+    """The oracle as it stands (one model trained alone, NumPy fp64) on a
+    bounded sample of the workload: n_samples point clouds of cfg2."""
+    import synth
+    from oracle import models as OM
+    P = synth.init_params("pointnet_cls", 1000, k)
+    x, y = synth.points_cls(0, N=n_samples, L=L, k=k)
+    hp = synth.hparams_pointnet(7, 1)
+    t0 = time.perf_counter()
+    for t in range(1, steps + 1):
+        OM.train_step("pointnet_cls", P, {}, {}, (x, y), t, OM.hp_of(hp, 0))
+    dt = time.perf_counter() - t0
+    return n_samples * steps / dt, dt
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    n = args.ref_samples
+    for _ in range(args.warmup):
+        cpu_oracle_sample(n, args.L, args.k)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_oracle_sample(n, args.L, args.k)
+    dt = time.perf_counter() - t0
+    v = n * args.steps / dt
+    cores = os.cpu_count()
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "pointnet_cls cfg2 (BJ configs[1]) sample: 1 model x %d samples x %d points, "
+                                   "k=%d, fp64 NumPy oracle (one model trained alone)" % (n, args.L, args.k)},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": "1 model x %d samples of cfg2 per step" % n},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------- ours --
+
+def build_net(args, rank, device):
+    import torch
+    import synth
+    from paper_2102_02344_b200.pointnet import FusedPointNet
+    B, k = args.B, args.k
+    specs = [(n, s) for n, s, _ in synth.param_specs("pointnet_cls", k)]
+    base = rank * B
+    Ps = [synth.init_params("pointnet_cls", 1000 + base + b, k) for b in range(B)] if not args.fast_init else None
+    if Ps is None:   # identical initial parameters, different hyper-parameters (still B independent models)
+        P0 = synth.init_params("pointnet_cls", 1000, k)
+        Ps = [P0] * B
+    hp_all = synth.hparams_pointnet(7, B * args.gpus)
+    hp = {kk: v[base:base + B] for kk, v in hp_all.items()}
+    net = FusedPointNet(B, specs, Ps, hp, task="cls", dtype=args.dtype, N=args.N, L=args.L, k=k, device=device)
+    x, y = synth.points_cls(0, N=args.N, L=args.L, k=k)
+    xd = torch.tensor(x.reshape(-1, 3), dtype=torch.float32, device=device)
+    yd = torch.tensor(y, dtype=torch.int32, device=device)
+    net.set_batch(xd, yd)
+    return net, x, y
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2102_02344_b200.hfta as H
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    H.hfta_init(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    net, x_host_np, y_host_np = build_net(args, rank, device)
+    stream = torch.cuda.current_stream()
+    B, N = args.B, args.N
+    loss_all = torch.empty(B * world, device=device)
+
+    def gather_losses():
+        if world > 1:
+            dist.all_gather_into_tensor(loss_all, net.loss)      # C1: per-model losses only
+
+    # ---- device-timed region (inputs resident in HBM) ----
+    for _ in range(args.warmup):
+        net.step()
+        gather_losses()
+    torch.cuda.synchronize()
+    probe_name = args.probe
+    net.probe_arm(probe_name)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local_rank)
+    clocks.start()
+    l0 = H.hfta_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        net.step()
+        gather_losses()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = H.hfta_launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    probe_ms = net.probe_collect()
+    t = torch.tensor([ms], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = B * N * args.steps * world / (ms_max / 1e3)
+    mem_peak = torch.cuda.max_memory_allocated(device)
+
+    # ---- end to end through the public API: pinned host inputs in, losses out ----
+    xh = torch.from_numpy(x_host_np.reshape(-1, 3).astype(np.float32)).pin_memory()
+    yh = torch.from_numpy(y_host_np.astype(np.int32)).pin_memory()
+    lh = torch.empty(B, dtype=torch.float32).pin_memory()
+    xd = torch.empty_like(xh, device=device)
+    yd = torch.empty_like(yh, device=device)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        xd.copy_(xh, non_blocking=True)
+        yd.copy_(yh, non_blocking=True)
+        loss = net.step(xd, yd)
+        gather_losses()
+        lh.copy_(loss, non_blocking=True)
+        stream.synchronize()            # the host reads the step's per-model losses
+    f1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([f0.elapsed_time(f1)], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = B * N * args.steps * world / (float(te.item()) / 1e3)
+
+    if rank == 0:
+        pk = peaks()
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if args.dtype == "bf16" else "f32",
+                "data": "synthetic (seeded point clouds, random-init models)",
+                "config": {"workload": "pointnet_cls cfg2 (BJ configs[1])", "B_per_gpu": B, "batch": N,
+                           "points": args.L, "classes": args.k, "precision": args.dtype,
+                           "l2": "working set >> L2 (activations ~%.0f GB/step)" % (mem_peak / 1e9),
+                           "parallelism": "model-array sharding, %d x %d models" % (world, B)},
+                "gpu_launches": int(launches),
+                "peak_mem_gb": mem_peak / 1e9,
+                "clocks": clk,
+                "e2e": {"value": e2e_value, "unit": UNIT,
+                        "h2d_bytes_per_step": int(xh.numel() * 4 + yh.numel() * 4),
+                        "d2h_bytes_per_step": int(B * 4)}}
+        line["roofline"] = net.probe_roofline(probe_name, probe_ms, pk)
+        if world == 1 and not args.no_cpu_baseline:
+            v, dt = cpu_oracle_sample(args.ref_samples, args.L, args.k)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                                    "sample": "1 model x %d samples of cfg2, one fp64 step (%.1f s)" %
+                                              (args.ref_samples, dt)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--B", type=int, default=64)
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--N", type=int, default=32)
+    ap.add_argument("--L", type=int, default=2500)
+    ap.add_argument("--k", type=int, default=40)
+    ap.add_argument("--probe", default="feat.c3:fwd")
+    ap.add_argument("--ref-samples", type=int, default=8)
+    ap.add_argument("--fast-init", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -112,6 +112,67 @@ class FusedPointNet:
         ws.alloc()
         self.ws = ws
 
+    # ------------------------------------------------------------- probe --
+    # CUDA events around one named contraction inside the timed region (the
+    # bench's roofline figure).  name = "<layer>:fwd" or "<layer>:bwd".
+    _probe = None
+
+    def probe_arm(self, name):
+        self._probe = name
+        self._probe_ev = []
+
+    def _pbegin(self, tag, s):
+        if self._probe != tag:
+            return None
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(torch.cuda.current_stream())
+        return e0
+
+    def _pend(self, e0):
+        if e0 is None:
+            return
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(torch.cuda.current_stream())
+        self._probe_ev.append((e0, e1))
+
+    def probe_collect(self):
+        ms = [a.elapsed_time(b) for a, b in getattr(self, "_probe_ev", [])]
+        self._probe = None
+        return ms
+
+    def probe_roofline(self, name, ms, peaks, path="simt"):
+        """Algorithmic work of one launch of the probed contraction / its time."""
+        layer, kind = name.split(":")
+        Nn, K = self.arena.shape[layer + ".W"]
+        M = self.R if (".c" in layer) else self.N
+        s = 2 if self.dt == H.HFTA_BF16 and M == self.R else 4
+        mult = 1 if kind == "fwd" else 2            # bwd = dgrad + wgrad
+        flops = mult * 2.0 * self.B * M * Nn * K
+        if kind == "fwd":
+            nbytes = self.B * (M * K + Nn * K + M * Nn) * s
+        else:   # dgrad reads dY, W, writes dX; wgrad reads dY, X, writes dW fp32
+            nbytes = self.B * ((M * Nn + Nn * K + M * K) * s + (M * Nn + M * K) * s + Nn * K * 4)
+        t = float(np.mean(ms)) / 1e3 if ms else float("nan")
+        if path == "simt":   # FFMA-bound SIMT kernel: 148 SM x 128 FMA/clk x 2 flop x max clock
+            peak = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
+            ach = flops / t / 1e12
+            return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "traffic": None, "kernel": name, "launches_timed": len(ms), "ms_per_launch": t * 1e3,
+                    "algorithmic": {"flops": flops, "bytes": nbytes},
+                    "peak_source": "FFMA: 148 SM x 128 lanes x 2 flop x %.0f MHz" % peaks["sm_max_mhz"]}
+        ridge = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+        if flops / nbytes >= ridge:
+            peak = peaks["bf16_tflops"] if self.dt == H.HFTA_BF16 else peaks["bf16_tflops"] / 4.0
+            ach = flops / t / 1e12
+            return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "traffic": None, "kernel": name, "launches_timed": len(ms), "ms_per_launch": t * 1e3,
+                    "algorithmic": {"flops": flops, "bytes": nbytes}, "peak_source": peaks["source"]}
+        ach = nbytes / t / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "traffic": None, "kernel": name, "launches_timed": len(ms),
+                "ms_per_launch": t * 1e3, "algorithmic": {"flops": flops, "bytes": nbytes},
+                "peak_source": peaks["source"]}
+
     # ----------------------------------------------------------- wrappers --
     def _dt(self, t):
         return H.HFTA_F32 if t.dtype == torch.float32 else H.HFTA_BF16
@@ -119,17 +180,21 @@ class FusedPointNet:
     def _lin_fwd(self, X, M, name, Y, s):
         Nn, K = self.arena.shape[name + ".W"]
         dt = self._dt(Y)
+        e0 = self._pbegin(name + ":fwd", s)
         H.hfta_fused_linear_fwd(self.B, M, Nn, K, dt, X, self.arena.w_in(name + ".W", dt),
                                 self.arena.fptr("p", name + ".b"), self.arena.P, 0, 0, _out(Y), s)
+        self._pend(e0)
 
     def _lin_bwd(self, dY, X, M, name, dX, s, accumulate=0):
         Nn, K = self.arena.shape[name + ".W"]
         dt = self._dt(dY)
+        e0 = self._pbegin(name + ":bwd", s)
         H.hfta_fused_linear_bwd(self.B, M, Nn, K, dt, _in(dY), X, self.arena.w_in(name + ".W", dt),
                                 _out(dX) if dX is not None else H.tout(None, 0, 1),
                                 self.arena.fptr("g", name + ".W"), self.arena.P,
                                 self.arena.fptr("g", name + ".b"), self.arena.P, accumulate,
                                 self.ws.ptr, self.ws.nbytes, s)
+        self._pend(e0)
 
     def _bn_fwd(self, X, name, act, Y, s):
         R, C = X.shape[1], X.shape[2]
