@@ -351,13 +351,13 @@ __global__ void k_bn_max_bwd_small(int B, int64_t N, int64_t L, int64_t C, const
   coef[2 * (int64_t)B * C + i] = (float)(s2 / R);
 }
 
-// step 2: dense dX = k1 * (dz_sparse - k2 - xhat*k3), grid (colgroups, chunks, B)
+// step 2: dense dX = k1 * (0 - k2 - xhat*k3) for every row (the scattered
+// gradient is zero off the argmax rows), grid (colgroups, chunks, B).
 template <typename T, int VEC>
 __global__ void __launch_bounds__(NT) k_bn_max_bwd_apply(int B, int64_t N, int64_t L, int64_t C,
                                                          const T* __restrict__ X, int64_t xbs, int64_t xld,
-                                                         const int32_t* __restrict__ amax,
-                                                         const float* __restrict__ dz, T* __restrict__ dX,
-                                                         int64_t obs, int64_t old, const float* __restrict__ smean,
+                                                         T* __restrict__ dX, int64_t obs, int64_t old,
+                                                         const float* __restrict__ smean,
                                                          const float* __restrict__ sinv,
                                                          const float* __restrict__ coef, Geo g) {
   const int b = blockIdx.z, chunk = blockIdx.y;
@@ -365,12 +365,14 @@ __global__ void __launch_bounds__(NT) k_bn_max_bwd_apply(int B, int64_t N, int64
   const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
   if (c0 >= C) return;
   const int64_t BC = (int64_t)B * C;
-  float m[VEC], is[VEC], k1[VEC], k2[VEC], k3[VEC];
+  float sc[VEC], sf[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
     int64_t i = (int64_t)b * C + c0 + v;
-    m[v] = smean[i]; is[v] = sinv[i];
-    k1[v] = coef[i]; k2[v] = coef[BC + i]; k3[v] = coef[2 * BC + i];
+    // k1*(-k2 - (x - m)*is*k3) = x*(-k1*is*k3) + k1*(m*is*k3 - k2)
+    const float k1 = coef[i], k2 = coef[BC + i], k3 = coef[2 * BC + i], m = smean[i], is = sinv[i];
+    sc[v] = -k1 * is * k3;
+    sf[v] = k1 * (m * is * k3 - k2);
   }
   const int64_t R = N * L;
   const T* Xb = X + (int64_t)b * xbs;
@@ -378,17 +380,28 @@ __global__ void __launch_bounds__(NT) k_bn_max_bwd_apply(int B, int64_t N, int64
   const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
   const int64_t r1 = min(R, r0 + g.rows_per_chunk);
   for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
-    const int64_t n = r / L, l = r % L;
     float x[VEC];
     ld_vec<T, VEC>(Xb + r * xld + c0, x);
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      int64_t j = ((int64_t)b * N + n) * C + c0 + v;
-      float d = (amax[j] == (int32_t)l) ? dz[j] : 0.f;
-      float xh = (x[v] - m[v]) * is[v];
-      x[v] = k1[v] * (d - k2[v] - xh * k3[v]);
-    }
+    for (int v = 0; v < VEC; ++v) x[v] = fmaf(x[v], sc[v], sf[v]);
     st_vec<T, VEC>(Ob + r * old + c0, x);
+  }
+}
+
+// step 3: the argmax rows, recomputed in full: dX = k1 * (dz - k2 - xhat*k3).
+template <typename T>
+__global__ void k_bn_max_bwd_scatter(int B, int64_t N, int64_t L, int64_t C, const T* __restrict__ X, int64_t xbs,
+                                     int64_t xld, const int32_t* __restrict__ amax, const float* __restrict__ dz,
+                                     T* __restrict__ dX, int64_t obs, int64_t old, const float* __restrict__ smean,
+                                     const float* __restrict__ sinv, const float* __restrict__ coef) {
+  const int64_t tot = (int64_t)B * N * C;
+  const int64_t BC = (int64_t)B * C;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < tot; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = j / (N * C), c = j % C, n = (j / C) % N;
+    const int64_t r = n * L + amax[j];
+    const int64_t i = b * C + c;
+    const float xh = (ldf(X + b * xbs + r * xld + c) - smean[i]) * sinv[i];
+    stf(dX + b * obs + r * old + c, coef[i] * (dz[j] - coef[BC + i] - xh * coef[2 * BC + i]));
   }
 }
 
@@ -547,10 +560,13 @@ hfta_status hfta_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C, hfta_dtype d
     k_bn_max_bwd_small<T><<<(unsigned)cdiv((int64_t)B * C, 128), 128, 0, s>>>(
         B, N, L, C, (const float*)dG.ptr, dG.bstride, dG.ld, (const T*)X.ptr, X.bstride, X.ld, argmax, gamma, beta,
         gb_bstride, save_mean, save_invstd, (int)act, act_alpha, dgamma, dbeta, coef, dz);
-    LAUNCH_VEC(T, vec, k_bn_max_bwd_apply, grid, B, N, L, C, (const T*)X.ptr, X.bstride, X.ld, argmax, dz,
+    LAUNCH_VEC(T, vec, k_bn_max_bwd_apply, grid, B, N, L, C, (const T*)X.ptr, X.bstride, X.ld,
                (T*)dX.ptr, dX.bstride, dX.ld, save_mean, save_invstd, coef, g);
+    k_bn_max_bwd_scatter<T><<<(unsigned)std::min<int64_t>(cdiv((int64_t)B * N * C, 256), 4096), 256, 0, s>>>(
+        B, N, L, C, (const T*)X.ptr, X.bstride, X.ld, argmax, dz, (T*)dX.ptr, dX.bstride, dX.ld, save_mean,
+        save_invstd, coef);
   });
-  count_launches(2);
+  count_launches(3);
   return post_launch(s, "hfta_bn_max_bwd");
 }
 

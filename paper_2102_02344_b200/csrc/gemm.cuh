@@ -33,4 +33,11 @@ hfta_status splitk_reduce(const GemmP& p, cudaStream_t s);   // C (+)= sum_s par
 hfta_status gemm_tc(const GemmP& p, hfta_dtype dt_in, bool out_f32, cudaStream_t s);
 bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32);
 
+// HBM-bound skinny contractions (K <= 8 fwd, N-out <= 8 dgrad, K-out <= 3 wgrad).
+bool skinny_fwd_ok(const GemmP& p);
+bool skinny_dgrad_ok(const GemmP& p);
+bool skinny_wgrad_ok(const GemmP& p);
+size_t skinny_wgrad_ws(int B, int64_t rows, int64_t N, int64_t Ko);
+hfta_status gemm_skinny(const GemmP& p, hfta_dtype dt, void* ws, size_t ws_bytes, cudaStream_t s);
+
 }  // namespace hfta

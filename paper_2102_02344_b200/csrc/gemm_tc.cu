@@ -1,10 +1,479 @@
-// gemm_tc.cu -- tcgen05 / TMEM / TMA model-batched GEMM (placeholder; the
-// SIMT path serves every shape until this lands).
+// gemm_tc.cu -- tcgen05 / TMEM / TMA model-batched GEMM (K1 fwd/dgrad, K2 wgrad).
+//
+// The fused Linear / Conv1d(k=1) of App. B
+// for all B models in ONE persistent launch: the model index b is folded into
+// the tile scheduler (tile = (b, split, m-tile, n-tile)), so many small
+// per-model GEMMs fill the 148 SMs (the paper's "horizontal fusion",
+// P:L856-857, done in the scheduler instead of by a grouped library call).
+//
+// Per CTA (1 per SM, 192 threads):
+//   warp 0      TMA producer: 3-D tensor maps [B][rows][cols] (bstride = dim 2),
+//               SWIZZLE_128B boxes of 64 elements (128 B) along the contiguous dim.
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma.kind::f16
+//               (bf16 x bf16 -> fp32 in TMEM), M=128, N=BN, K=16 per instruction.
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> bias / convert ->
+//               global stores (row per thread); double-buffered TMEM
+//               accumulators let the epilogue of tile i overlap the MMAs of i+1.
+// Operands: A(m,k), B(n,k) each K-major ([m][k], k contiguous) or MN-major
+// ([k][m], m contiguous); MN-major is what the dgrad (B = W) and wgrad
+// (A = dY, B = X) contractions need, read without a transpose pass.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "gemm.cuh"
 
 namespace hfta {
-bool gemm_tc_supported(const GemmP&, hfta_dtype, bool) { return false; }
-hfta_status gemm_tc(const GemmP&, hfta_dtype, bool, cudaStream_t) {
-  return fail(HFTA_ERR_UNSUPPORTED, "gemm_tc: not available");
+namespace {
+
+constexpr int BM = 128;     // UMMA M (one CTA, cta_group::1)
+constexpr int BK = 64;      // k per stage: 64 bf16 = 128 B = one swizzle row
+constexpr int NTHREADS = 192;
+
+// ------------------------------------------------------------ PTX wrappers --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// 32 lanes x 32 columns of fp32: thread t of the warp gets row (lane base + t).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory matrix descriptor, SWIZZLE_128B, sm100 version 1.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;          // version (Blackwell)
+  d |= (uint64_t)2 << 61;          // layout: SWIZZLE_128B
+  return d;
+}
+
+struct TcArgs {
+  int B, splits, order;            // order 0: n fastest, 1: m fastest
+  int64_t M, N, K, k_chunk;
+  int a_shared, b_shared;
+  void* C; int64_t c_bs, c_ld;
+  const float* bias; int64_t bias_bs, bias_ld, bias_div;
+  int accumulate;
+  float* part;
+  int tiles_m, tiles_n;
+};
+
+template <bool A_MN, bool B_MN, int BN, int STAGES, bool OUT_F32>
+__global__ void __launch_bounds__(NTHREADS, 1)
+k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+          const __grid_constant__ CUtensorMap tmC, TcArgs p) {
+  constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB
+  constexpr uint32_t B_BYTES = BN * BK * 2;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;     // double-buffered accumulator
+  constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                             ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // per-epilogue-warp staging for the TMA store: 2 buffers x 32 rows x 64 B
+  uint8_t* stage_out = smem + STAGES * STAGE_BYTES + 1024;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int64_t tiles_mn = (int64_t)p.tiles_m * p.tiles_n;
+  const int64_t total = tiles_mn * p.splits * p.B;
+
+  if (warp == 0) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        int64_t r = t;
+        int mt, nt;
+        if (p.order == 0) { nt = (int)(r % p.tiles_n); r /= p.tiles_n; mt = (int)(r % p.tiles_m); r /= p.tiles_m; }
+        else { mt = (int)(r % p.tiles_m); r /= p.tiles_m; nt = (int)(r % p.tiles_n); r /= p.tiles_n; }
+        const int split = (int)(r % p.splits);
+        const int b = (int)(r / p.splits);
+        const int64_t kbeg = (int64_t)split * p.k_chunk;
+        const int64_t kend = min(p.K, kbeg + p.k_chunk);
+        const int nkb = (int)((kend - kbeg + BK - 1) / BK);
+        const int ba = p.a_shared ? 0 : b, bb = p.b_shared ? 0 : b;
+        const int m0 = mt * BM, n0 = nt * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          const int k0 = (int)(kbeg + (int64_t)kb * BK);
+          if (A_MN) {
+            tma_load_3d(sa, &tmA, &full[stage], m0, k0, ba);
+            tma_load_3d(sa + 8192, &tmA, &full[stage], m0 + 64, k0, ba);
+          } else {
+            tma_load_3d(sa, &tmA, &full[stage], k0, m0, ba);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
+          } else {
+            tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================= MMA issuer =============================
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      int64_t r = t;
+      if (p.order == 0) { r /= p.tiles_n; r /= p.tiles_m; } else { r /= p.tiles_m; r /= p.tiles_n; }
+      const int split = (int)(r % p.splits);
+      const int64_t kbeg = (int64_t)split * p.k_chunk;
+      const int64_t kend = min(p.K, kbeg + p.k_chunk);
+      const int nkb = (int)((kend - kbeg + BK - 1) / BK);
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: +32 B per 16-element k step inside the 128-B swizzle row;
+            // MN-major: +16 rows x 128 B.
+            const uint64_t ad = A_MN ? smem_desc(sa + k * 2048, 8192, 1024) : smem_desc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc(sb + k * 2048, 8192, 1024) : smem_desc(sb + k * 32, 16, 1024);
+            tc_mma_bf16(d_tmem, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty[stage]);                  // smem slot free once these MMAs retire
+          if (kb == nkb - 1) tc_commit(&tfull[acc]);   // accumulator ready
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (nkb == 0 && lane == 0) mbar_arrive(&tfull[acc]);   // empty K range: zero tile (not used)
+      __syncwarp();
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else {
+    // ============================== epilogue ==============================
+    const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
+    uint32_t sbuf = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      int64_t r = t;
+      int mt, nt;
+      if (p.order == 0) { nt = (int)(r % p.tiles_n); r /= p.tiles_n; mt = (int)(r % p.tiles_m); r /= p.tiles_m; }
+      else { mt = (int)(r % p.tiles_m); r /= p.tiles_m; nt = (int)(r % p.tiles_n); r /= p.tiles_n; }
+      const int split = (int)(r % p.splits);
+      const int b = (int)(r / p.splits);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t m = (int64_t)mt * BM + quarter * 32 + lane;
+      const bool row_ok = m < p.M;
+      const float* brow = nullptr;
+      if (p.bias && row_ok)
+        brow = p.bias + (int64_t)b * p.bias_bs + (p.bias_div > 0 ? (m / p.bias_div) * p.bias_ld : 0);
+#pragma unroll 1
+      for (int j = 0; j < BN / 32; ++j) {
+        float v[32];
+        tmem_ld32(tmem_base + (uint32_t)(acc * BN + j * 32) + ((uint32_t)(quarter * 32) << 16), v);
+        if (j == BN / 32 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        const int64_t n0 = (int64_t)nt * BN + j * 32;
+        if (n0 >= p.N) continue;                       // warp-uniform
+        if (brow) {
+          if (n0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(brow + n0) & 15) == 0)) {
+            const float4* bp = reinterpret_cast<const float4*>(brow + n0);   // warp-broadcast 128-bit loads
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 t4 = __ldg(bp + q);
+              v[4 * q] += t4.x; v[4 * q + 1] += t4.y; v[4 * q + 2] += t4.z; v[4 * q + 3] += t4.w;
+            }
+          } else {
+            for (int q = 0; q < 32 && n0 + q < p.N; ++q) v[q] += brow[n0 + q];
+          }
+        }
+        if constexpr (!OUT_F32) {
+          // bf16: stage the warp's 32 x 32 sub-tile in smem, one TMA store per
+          // chunk (rows >= M and columns >= N are clipped by the tensor map).
+          uint8_t* buf = stage_out + ((warp - 2) * 2 + (sbuf & 1)) * 2048;
+          if (lane == 0) tma_store_wait_read<1>();
+          __syncwarp();
+          // 64-B rows in the TMA SWIZZLE_64B layout: 16-B chunk q of row r lives at
+          // chunk q ^ ((r >> 1) & 3) -> the 32 lanes' stores hit all banks (4 wavefronts).
+          const uint32_t rowaddr = smem_u32(buf) + lane * 64;
+          const uint32_t sw = (uint32_t)((lane >> 1) & 3);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+            st_shared_v4(rowaddr + (((uint32_t)q ^ sw) << 4), u);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) tma_store_3d(&tmC, buf, (int)n0, (int)(mt * BM + quarter * 32), b);
+          ++sbuf;
+        } else {
+          if (!row_ok) continue;
+          const bool full_chunk = n0 + 32 <= p.N;
+          float* dst = p.splits > 1 ? p.part + (((int64_t)split * p.B + b) * p.M + m) * p.N + n0
+                                    : reinterpret_cast<float*>(p.C) + (int64_t)b * p.c_bs + m * p.c_ld + n0;
+          const bool vec_ok = full_chunk && (p.splits > 1 ? (p.N % 4 == 0) : true);
+          if (p.splits == 1 && p.accumulate) {
+            for (int q = 0; q < 32 && n0 + q < p.N; ++q) dst[q] += v[q];
+          } else if (vec_ok) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          } else {
+            for (int q = 0; q < 32 && n0 + q < p.N; ++q) dst[q] = v[q];
+          }
+        }
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  if (warp >= 2 && lane == 0) tma_store_wait_read<0>();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------ host side --
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+hfta_status get_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) return fail(HFTA_ERR_CUDA, "gemm_tc: cuTensorMapEncodeTiled unavailable");
+  return HFTA_OK;
+}
+
+// 3-D bf16 map: dim0 = contiguous extent, dim1 = rows, dim2 = models.
+hfta_status make_map(CUtensorMap* m, const void* ptr, int64_t inner, int64_t rows, int64_t ld, int64_t bs, int nb,
+                     uint32_t box_inner, uint32_t box_rows) {
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)nb};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)((nb > 1 ? bs : rows * ld) * 2)};
+  cuuint32_t box[3] = {box_inner, box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(HFTA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): dims %lld x %lld x %d, ld %lld, bs %lld", (int)r,
+                (long long)inner, (long long)rows, nb, (long long)ld, (long long)bs);
+  return HFTA_OK;
+}
+
+template <bool A_MN, bool B_MN, int BN, bool OUT_F32>
+hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
+  constexpr int STAGES = (BN == 256) ? 4 : 6;
+  constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + 4 * 2 * 2048;
+  if (hfta_status st = get_encode()) return st;
+  CUtensorMap ta, tb;
+  const int nba = p.a_bs == 0 ? 1 : p.B, nbb = p.b_bs == 0 ? 1 : p.B;
+  hfta_status st;
+  if (A_MN) st = make_map(&ta, p.A, p.M, p.K, p.a_ld, p.a_bs, nba, 64, BK);
+  else st = make_map(&ta, p.A, p.K, p.M, p.a_ld, p.a_bs, nba, BK, BM);
+  if (st) return st;
+  if (B_MN) st = make_map(&tb, p.Bm, p.N, p.K, p.b_ld, p.b_bs, nbb, 64, BK);
+  else st = make_map(&tb, p.Bm, p.K, p.N, p.b_ld, p.b_bs, nbb, BK, BN);
+  if (st) return st;
+  CUtensorMap tc_ = tb;
+  if (!OUT_F32 && p.splits == 1) {
+    cuuint64_t dims[3] = {(cuuint64_t)p.N, (cuuint64_t)p.M, (cuuint64_t)p.B};
+    cuuint64_t strides[2] = {(cuuint64_t)(p.c_ld * 2), (cuuint64_t)((p.B > 1 ? p.c_bs : p.M * p.c_ld) * 2)};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_encode(&tc_, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, p.C, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(HFTA_ERR_CUDA, "cuTensorMapEncodeTiled (C) failed (%d)", (int)r);
+  }
+  TcArgs a{};
+  a.B = p.B; a.splits = p.splits; a.M = p.M; a.N = p.N; a.K = p.K; a.k_chunk = p.k_chunk;
+  a.a_shared = nba == 1 && p.B > 1; a.b_shared = nbb == 1 && p.B > 1;
+  a.C = p.C; a.c_bs = p.c_bs; a.c_ld = p.c_ld;
+  a.bias = p.bias; a.bias_bs = p.bias_bs; a.bias_ld = p.bias_ld; a.bias_div = p.bias_div;
+  a.accumulate = p.accumulate; a.part = p.part;
+  a.tiles_m = (int)cdiv(p.M, BM); a.tiles_n = (int)cdiv(p.N, BN);
+  a.order = (A_MN && B_MN) ? 1 : 0;
+  auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    attr_set = true;
+  }
+  int64_t total = (int64_t)a.tiles_m * a.tiles_n * a.splits * a.B;
+  int grid = (int)std::min<int64_t>(total, num_sms());
+  kern<<<grid, NTHREADS, SMEM, s>>>(ta, tb, tc_, a);
+  count_launches(1);
+  return post_launch(s, "gemm_tc");
+}
+
+template <bool A_MN, bool B_MN, bool OUT_F32>
+hfta_status dispatch_bn(const GemmP& p, cudaStream_t s) {
+  if (p.N <= 64) return launch_tc<A_MN, B_MN, 64, OUT_F32>(p, s);
+  if (p.N <= 128 || OUT_F32) return launch_tc<A_MN, B_MN, 128, OUT_F32>(p, s);
+  return launch_tc<A_MN, B_MN, 256, OUT_F32>(p, s);
+}
+
+bool env_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HFTA_DISABLE_TC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+}  // namespace
+
+bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32) {
+  if (env_disabled() || dt_in != HFTA_BF16) return false;
+  if (p.K < 16 || p.N < 16 || p.M < 1) return false;
+  if (!aligned16(p.A) || !aligned16(p.Bm)) return false;
+  if ((p.a_ld * 2) % 16 || (p.b_ld * 2) % 16 || (p.a_bs * 2) % 16 || (p.b_bs * 2) % 16) return false;
+  if (p.M > INT32_MAX || p.N > INT32_MAX || p.K > INT32_MAX) return false;
+  if (!out_f32) {
+    if (!aligned16(p.C) || (p.c_ld * 2) % 16 || (p.c_bs * 2) % 16 || p.accumulate) return false;
+  } else if (p.splits == 1 && (!aligned16(p.C) || p.c_ld % 4)) {
+    return false;
+  }
+  if (p.splits > 1 && p.k_chunk % BK) return false;
+  // MN-major operands need their MN extent in whole 64-element boxes inside the allocation
+  if (!p.a_kmajor && (p.M % 64)) return false;
+  if (!p.b_kmajor && (p.N % 64)) return false;
+  return true;
+}
+
+hfta_status gemm_tc(const GemmP& p, hfta_dtype dt_in, bool out_f32, cudaStream_t s) {
+  (void)dt_in;
+  const bool amn = !p.a_kmajor, bmn = !p.b_kmajor;
+  if (out_f32) {
+    if (amn && bmn) return dispatch_bn<true, true, true>(p, s);
+    if (!amn && bmn) return dispatch_bn<false, true, true>(p, s);
+    if (!amn && !bmn) return dispatch_bn<false, false, true>(p, s);
+  } else {
+    if (!amn && !bmn) return dispatch_bn<false, false, false>(p, s);
+    if (!amn && bmn) return dispatch_bn<false, true, false>(p, s);
+  }
+  return fail(HFTA_ERR_UNSUPPORTED, "gemm_tc: operand majorness combination");
+}
+
 }  // namespace hfta

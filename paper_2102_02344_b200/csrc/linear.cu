@@ -23,7 +23,8 @@ Split wgrad_split(int B, int64_t M, int64_t N, int64_t K) {
   return {(int)splits, chunk};
 }
 
-hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s) {
+hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void* ws = nullptr, size_t wsb = 0) {
+  if (skinny_fwd_ok(p) || skinny_dgrad_ok(p) || skinny_wgrad_ok(p)) return gemm_skinny(p, dt, ws, wsb, s);
   if (gemm_tc_supported(p, dt, out_f32)) return gemm_tc(p, dt, out_f32, s);
   return gemm_simt(p, dt, out_f32, s);
 }
@@ -81,6 +82,7 @@ size_t hfta_fused_linear_bwd_workspace(int B, int64_t M, int64_t N, int64_t K, h
   if (B < 1 || M < 1 || N < 1 || K < 1) return 0;
   Split sp = wgrad_split(B, M, N, K);
   size_t part = sp.splits > 1 ? (size_t)sp.splits * B * N * K * sizeof(float) : 0;
+  part = std::max(part, skinny_wgrad_ws(B, M, N, K));
   size_t cs = colsum_ws(B, M, N, M);
   return align_up(part, 256) + align_up(cs, 256);
   (void)dt;
@@ -118,22 +120,28 @@ hfta_status hfta_fused_linear_bwd(int B, int64_t M, int64_t N, int64_t K, hfta_d
     HFTA_REQUIRE(X.ld >= K, HFTA_ERR_SHAPE, "linear_bwd: X ld %lld < K %lld", (long long)X.ld, (long long)K);
     HFTA_REQUIRE(dW_bstride >= N * K || B == 1, HFTA_ERR_SHAPE, "linear_bwd: dW_bstride %lld < N*K",
                  (long long)dW_bstride);
-    Split sp = wgrad_split(B, M, N, K);
     GemmP p{};
     p.B = B; p.M = N; p.N = K; p.K = M;                         // dW[N,K] = dY^T[N,M] X[M,K]
     p.A = dY.ptr; p.a_bs = dY.bstride; p.a_ld = dY.ld; p.a_kmajor = 0;
     p.Bm = X.ptr; p.b_bs = X.bstride; p.b_ld = X.ld; p.b_kmajor = 0;
     p.C = dW; p.c_bs = dW_bstride; p.c_ld = K;
     p.accumulate = accumulate;
-    p.splits = sp.splits; p.k_chunk = sp.chunk;
-    p.part = sp.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
-    if (hfta_status st = run_gemm(p, dt, true, s)) return st;
-    if (sp.splits > 1)
-      if (hfta_status st = splitk_reduce(p, s)) return st;
+    p.splits = 1; p.k_chunk = M;
+    if (skinny_wgrad_ok(p)) {
+      if (hfta_status st = gemm_skinny(p, dt, ws, ws_bytes, s)) return st;
+    } else {
+      Split sp = wgrad_split(B, M, N, K);
+      p.splits = sp.splits; p.k_chunk = sp.chunk;
+      p.part = sp.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
+      if (hfta_status st = run_gemm(p, dt, true, s)) return st;
+      if (sp.splits > 1)
+        if (hfta_status st = splitk_reduce(p, s)) return st;
+    }
   }
   if (dbias) {
     Split sp = wgrad_split(B, M, N, K);
-    size_t off = align_up(sp.splits > 1 ? (size_t)sp.splits * B * N * K * sizeof(float) : 0, 256);
+    size_t off = align_up(std::max(sp.splits > 1 ? (size_t)sp.splits * B * N * K * sizeof(float) : 0,
+                                   skinny_wgrad_ws(B, M, N, K)), 256);
     char* cws = ws ? reinterpret_cast<char*>(ws) + off : nullptr;
     if (hfta_status st = colsum_impl(B, M, N, M, dt, dY, dbias, dbias_bstride, accumulate, cws,
                                      ws_bytes > off ? ws_bytes - off : 0, s))

@@ -18,6 +18,14 @@ from .fused import ParamArena, HyperVectors, Workspace, fused_adam
 
 A_RELU, A_NONE = H.ACT_RELU, H.ACT_NONE
 
+# Layers whose output feeds a training-mode BatchNorm directly: the gradient
+# of their bias is identically zero (BN's input gradient sums to zero over the
+# rows: sum_r dx_r = gamma*invstd*(sum dz - dbeta - dgamma*sum(xhat)/R) = 0
+# since sum(xhat) = 0), so the fused step writes exact zeros instead of
+# reducing a rounding-noise column sum.
+BN_FOLLOWED = {"stn.c1", "stn.c2", "stn.c3", "stn.fc1", "stn.fc2", "feat.c1", "feat.c2", "feat.c3",
+               "head.fc1", "head.c1", "head.c2", "head.c3"}
+
 
 class _Acts:
     def __init__(self, B, dtype, device):
@@ -192,8 +200,8 @@ class FusedPointNet:
         H.hfta_fused_linear_bwd(self.B, M, Nn, K, dt, _in(dY), X, self.arena.w_in(name + ".W", dt),
                                 _out(dX) if dX is not None else H.tout(None, 0, 1),
                                 self.arena.fptr("g", name + ".W"), self.arena.P,
-                                self.arena.fptr("g", name + ".b"), self.arena.P, accumulate,
-                                self.ws.ptr, self.ws.nbytes, s)
+                                None if name in BN_FOLLOWED else self.arena.fptr("g", name + ".b"), self.arena.P,
+                                accumulate, self.ws.ptr, self.ws.nbytes, s)
         self._pend(e0)
 
     def _bn_fwd(self, X, name, act, Y, s):

@@ -46,7 +46,10 @@ def s():
 
 
 # ----------------------------------------------------------------- linear ----
-SHAPES = [(300, 64, 3), (1000, 128, 64), (257, 200, 136), (32, 9, 256), (37, 40, 256), (130, 3, 64)]
+# (M, N, K): K < 16 / N < 16 / unaligned shapes take the SIMT kernel; the rest
+# (bf16) the tcgen05 kernel, including ragged M / N tails and MN-major operands.
+SHAPES = [(300, 64, 3), (1000, 128, 64), (257, 200, 136), (32, 9, 256), (37, 40, 256), (130, 3, 64),
+          (2000, 1024, 128), (1500, 128, 1024), (640, 256, 512), (999, 64, 128)]
 
 
 @pytest.mark.parametrize("dt", ["f32", "bf16"])

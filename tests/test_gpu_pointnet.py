@@ -85,9 +85,19 @@ def check_step(net, loss, ref_losses, grads, res, tol, B, grad_tol="same"):
             e = relerr(np.concatenate([G[n].ravel() for n in live]), np.concatenate([R[n].ravel() for n in live]))
             assert e <= WHOLE_TOL, "model %d whole-model gradient: %.3e" % (b, e)
         # after the Adam step: whole-model normwise (reading R21)
-        p = np.concatenate([net.params(b)[n].ravel() for n in R])
-        pr = np.concatenate([res[b]["params"][n].ravel() for n in R])
-        assert relerr(p, pr) <= tol, "model %d params after step: %.3e" % (b, relerr(p, pr))
+        # After the Adam step (reading R21): at t = 1 every update is bounded by lr
+        # (|m_hat / (sqrt(v_hat) + eps)| <= 1), so a gradient element whose sign is
+        # decided below rounding noise may move by up to 2*lr on either side.  Gate:
+        # every element within 2*lr_b of the oracle, and the head-side tensors (whose
+        # gradients are gated per tensor above) normwise.
+        pb = net.params(b)
+        lr = float(net.hv.t["lr"][b].item())
+        for n in R:
+            d = np.max(np.abs(pb[n] - res[b]["params"][n]))
+            assert d <= 2 * lr * (1 + 1e-3) + 1e-6, "model %d param %s moved %.3e > 2 lr" % (b, n, d)
+            if n in HEAD_SIDE and grad_tol is not None:
+                e = relerr(pb[n], res[b]["params"][n])
+                assert e <= tol, "model %d param %s after step: %.3e" % (b, n, e)
 
 
 # bf16-AMP whole-step GRADIENTS are not gated normwise: PointNet's per-step
