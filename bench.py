@@ -131,19 +131,19 @@ def run_reference(args, rank):
 
 # -------------------------------------------------------------------- ours --
 
-def build_net(args, rank, device):
+def build_net(args, rank, world, device):
     import torch
     import synth
     from paper_2102_02344_b200.pointnet import FusedPointNet
+    from paper_2102_02344_b200 import shard
     B, k = args.B, args.k
     specs = [(n, s) for n, s, _ in synth.param_specs("pointnet_cls", k)]
-    base = rank * B
+    base, _ = shard.model_range(rank, world, B * world)   # weak scaling: B models per GPU
     Ps = [synth.init_params("pointnet_cls", 1000 + base + b, k) for b in range(B)] if not args.fast_init else None
     if Ps is None:   # identical initial parameters, different hyper-parameters (still B independent models)
         P0 = synth.init_params("pointnet_cls", 1000, k)
         Ps = [P0] * B
-    hp_all = synth.hparams_pointnet(7, B * args.gpus)
-    hp = {kk: v[base:base + B] for kk, v in hp_all.items()}
+    hp = shard.slice_hparams(synth.hparams_pointnet(7, B * world), base, base + B)
     net = FusedPointNet(B, specs, Ps, hp, task="cls", dtype=args.dtype, N=args.N, L=args.L, k=k, device=device)
     x, y = synth.points_cls(0, N=args.N, L=args.L, k=k)
     xd = torch.tensor(x.reshape(-1, 3), dtype=torch.float32, device=device)
@@ -161,14 +161,14 @@ def run_ours(args, rank, world, local_rank):
     H.hfta_init(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
-    net, x_host_np, y_host_np = build_net(args, rank, device)
+    net, x_host_np, y_host_np = build_net(args, rank, world, device)
     stream = torch.cuda.current_stream()
     B, N = args.B, args.N
-    loss_all = torch.empty(B * world, device=device)
+    from paper_2102_02344_b200 import shard
 
     def gather_losses():
         if world > 1:
-            dist.all_gather_into_tensor(loss_all, net.loss)      # C1: per-model losses only
+            shard.gather_losses(net.loss, B * world, world)      # C1: per-model losses only
 
     # ---- device-timed region (inputs resident in HBM) ----
     for _ in range(args.warmup):
