@@ -244,7 +244,16 @@ def run_ours(args, rank, world, local_rank):
                 "e2e": {"value": e2e_value, "unit": UNIT,
                         "h2d_bytes_per_step": int(xh.numel() * 4 + yh.numel() * 4),
                         "d2h_bytes_per_step": int(B * 4)}}
-        line["roofline"] = net.probe_roofline(probe_name, probe_ms, pk)
+        path = "tc" if args.dtype == "bf16" else "simt"
+        roof = net.probe_roofline(probe_name, probe_ms, pk, path=path)
+        try:   # DRAM traffic of the probed kernel from the committed ncu --set full capture
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic_r01.json")))[probe_name]
+            if path == "tc":
+                roof["traffic"] = tr["dram_bytes_per_model"] * B
+                roof["traffic_source"] = tr["source"]
+        except Exception:
+            pass
+        line["roofline"] = roof
         if world == 1 and not args.no_cpu_baseline:
             v, dt = cpu_oracle_sample(args.ref_samples, args.L, args.k)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
