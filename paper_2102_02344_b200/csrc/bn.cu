@@ -13,6 +13,7 @@ namespace hfta {
 namespace {
 
 constexpr int NT = 256;
+constexpr int UNR = 1;      // rows per thread per iteration (UNR=4 measured slower: 76-150 regs cut occupancy)
 
 struct Geo {
   int vec, tpr, cb, rpb, colgroups, chunks;
@@ -58,15 +59,21 @@ __global__ void __launch_bounds__(NT) k_bn_stats(int64_t R, int64_t C, const T* 
     ld_vec<T, VEC>(Xb + c0, sh);
     const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
     const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-    for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
-      float x[VEC];
-      ld_vec<T, VEC>(Xb + r * ld + c0, x);
+    for (int64_t r = r0 + rl; r < r1; r += UNR * g.rpb) {
+      float x[UNR][VEC];
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        float d = x[v] - sh[v];
-        a1[v] += d;
-        a2[v] = fmaf(d, d, a2[v]);
-      }
+      for (int u = 0; u < UNR; ++u)
+        if (r + u * g.rpb < r1) ld_vec<T, VEC>(Xb + (r + u * g.rpb) * ld + c0, x[u]);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (r + u * g.rpb < r1) {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            float d = x[u][v] - sh[v];
+            a1[v] += d;
+            a2[v] = fmaf(d, d, a2[v]);
+          }
+        }
     }
   }
 #pragma unroll
@@ -132,12 +139,18 @@ __global__ void __launch_bounds__(NT) k_bn_apply(int64_t R, int64_t C, const T* 
   T* Yb = Y + (int64_t)b * ybs;
   const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
   const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-  for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
-    float x[VEC];
-    ld_vec<T, VEC>(Xb + r * xld + c0, x);
+  for (int64_t r = r0 + rl; r < r1; r += UNR * g.rpb) {
+    float x[UNR][VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) x[v] = act_fwd(fmaf(x[v], sc[v], sf[v]), act, alpha);
-    st_vec<T, VEC>(Yb + r * yld + c0, x);
+    for (int u = 0; u < UNR; ++u)
+      if (r + u * g.rpb < r1) ld_vec<T, VEC>(Xb + (r + u * g.rpb) * xld + c0, x[u]);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+      if (r + u * g.rpb < r1) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) x[u][v] = act_fwd(fmaf(x[u][v], sc[v], sf[v]), act, alpha);
+        st_vec<T, VEC>(Yb + (r + u * g.rpb) * yld + c0, x[u]);
+      }
   }
 }
 
@@ -167,17 +180,25 @@ __global__ void __launch_bounds__(NT) k_bn_bwd_reduce(int64_t R, int64_t C, cons
     const T* Db = dY + (int64_t)b * dbs;
     const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
     const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-    for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
-      float x[VEC], d[VEC];
-      ld_vec<T, VEC>(Xb + r * xld + c0, x);
-      ld_vec<T, VEC>(Db + r * dld + c0, d);
+    for (int64_t r = r0 + rl; r < r1; r += UNR * g.rpb) {
+      float x[UNR][VEC], d[UNR][VEC];
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        float xh = (x[v] - m[v]) * is[v];
-        float dz = d[v] * act_grad(fmaf(ga[v], xh, be[v]), act, alpha);
-        a1[v] += dz;
-        a2[v] = fmaf(dz, xh, a2[v]);
-      }
+      for (int u = 0; u < UNR; ++u)
+        if (r + u * g.rpb < r1) {
+          ld_vec<T, VEC>(Xb + (r + u * g.rpb) * xld + c0, x[u]);
+          ld_vec<T, VEC>(Db + (r + u * g.rpb) * dld + c0, d[u]);
+        }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (r + u * g.rpb < r1) {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            float xh = (x[u][v] - m[v]) * is[v];
+            float dz = d[u][v] * act_grad(fmaf(ga[v], xh, be[v]), act, alpha);
+            a1[v] += dz;
+            a2[v] = fmaf(dz, xh, a2[v]);
+          }
+        }
     }
   }
 #pragma unroll
@@ -245,17 +266,25 @@ __global__ void __launch_bounds__(NT) k_bn_bwd_apply(int B, int64_t R, int64_t C
   T* Ob = dX + (int64_t)b * obs;
   const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
   const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-  for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
-    float x[VEC], d[VEC];
-    ld_vec<T, VEC>(Xb + r * xld + c0, x);
-    ld_vec<T, VEC>(Db + r * dld + c0, d);
+  for (int64_t r = r0 + rl; r < r1; r += UNR * g.rpb) {
+    float x[UNR][VEC], d[UNR][VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      float xh = (x[v] - m[v]) * is[v];
-      float dz = d[v] * act_grad(fmaf(ga[v], xh, be[v]), act, alpha);
-      x[v] = k1[v] * (dz - k2[v] - xh * k3[v]);
-    }
-    st_vec<T, VEC>(Ob + r * old + c0, x);
+    for (int u = 0; u < UNR; ++u)
+      if (r + u * g.rpb < r1) {
+        ld_vec<T, VEC>(Xb + (r + u * g.rpb) * xld + c0, x[u]);
+        ld_vec<T, VEC>(Db + (r + u * g.rpb) * dld + c0, d[u]);
+      }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+      if (r + u * g.rpb < r1) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          float xh = (x[u][v] - m[v]) * is[v];
+          float dz = d[u][v] * act_grad(fmaf(ga[v], xh, be[v]), act, alpha);
+          x[u][v] = k1[v] * (dz - k2[v] - xh * k3[v]);
+        }
+        st_vec<T, VEC>(Ob + (r + u * g.rpb) * old + c0, x[u]);
+      }
   }
 }
 
@@ -288,14 +317,20 @@ __global__ void __launch_bounds__(NT) k_bn_max_fwd(int64_t L, int64_t C, const T
       sf[v] = be - m * ga * is;
     }
     const T* Xb = X + (int64_t)b * xbs + n * L * xld;
-    for (int64_t l = rl; l < L; l += g.rpb) {
-      float x[VEC];
-      ld_vec<T, VEC>(Xb + l * xld + c0, x);
+    for (int64_t l = rl; l < L; l += UNR * g.rpb) {
+      float x[UNR][VEC];
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        float z = act_fwd(fmaf(x[v], sc[v], sf[v]), act, alpha);
-        if (z > best[v]) { best[v] = z; bi[v] = (int)l; }   // rows visited in increasing l per lane
-      }
+      for (int u = 0; u < UNR; ++u)
+        if (l + u * g.rpb < L) ld_vec<T, VEC>(Xb + (l + u * g.rpb) * xld + c0, x[u]);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (l + u * g.rpb < L) {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            float z = act_fwd(fmaf(x[u][v], sc[v], sf[v]), act, alpha);
+            if (z > best[v]) { best[v] = z; bi[v] = (int)(l + u * g.rpb); }   // increasing l per lane
+          }
+        }
     }
   }
 #pragma unroll
@@ -379,12 +414,18 @@ __global__ void __launch_bounds__(NT) k_bn_max_bwd_apply(int B, int64_t N, int64
   T* Ob = dX + (int64_t)b * obs;
   const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
   const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-  for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
-    float x[VEC];
-    ld_vec<T, VEC>(Xb + r * xld + c0, x);
+  for (int64_t r = r0 + rl; r < r1; r += UNR * g.rpb) {
+    float x[UNR][VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) x[v] = fmaf(x[v], sc[v], sf[v]);
-    st_vec<T, VEC>(Ob + r * old + c0, x);
+    for (int u = 0; u < UNR; ++u)
+      if (r + u * g.rpb < r1) ld_vec<T, VEC>(Xb + (r + u * g.rpb) * xld + c0, x[u]);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+      if (r + u * g.rpb < r1) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) x[u][v] = fmaf(x[u][v], sc[v], sf[v]);
+        st_vec<T, VEC>(Ob + (r + u * g.rpb) * old + c0, x[u]);
+      }
   }
 }
 

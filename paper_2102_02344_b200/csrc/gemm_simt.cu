@@ -11,33 +11,37 @@ namespace hfta {
 namespace {
 constexpr int BM = 128, BN = 128, BK = 16, NT = 256;
 
-template <typename Tin, typename Tout, bool AK, bool BKM>
+// Tile BM_ x 128 with 256 threads: BM_ = 128 -> 16 x 16 threads of 8 x 8 outputs;
+// BM_ = 32 (per-sample FC layers, M = batch = 32) -> 8 x 32 threads of 4 x 4.
+template <typename Tin, typename Tout, bool AK, bool BKM, int BM_>
 __global__ void __launch_bounds__(NT) k_gemm_simt(GemmP p) {
-  __shared__ float As[BK][BM + 4];
+  constexpr int TY = BM_ == 128 ? 16 : 8, TX = NT / TY;   // thread grid
+  constexpr int RM = BM_ / TY, RN = BN / TX;               // outputs per thread
+  __shared__ float As[BK][BM_ + 4];
   __shared__ float Bs[BK][BN + 4];
   const int b = blockIdx.z;
   const int split = blockIdx.y;
   const int64_t tiles_n = (p.N + BN - 1) / BN;
-  const int64_t m0 = (blockIdx.x / tiles_n) * BM;
+  const int64_t m0 = (blockIdx.x / tiles_n) * BM_;
   const int64_t n0 = (blockIdx.x % tiles_n) * BN;
   const int64_t kbeg = (int64_t)split * p.k_chunk;
   const int64_t kend = min(p.K, kbeg + p.k_chunk);
   const Tin* A = reinterpret_cast<const Tin*>(p.A) + (int64_t)b * p.a_bs;
   const Tin* Bm = reinterpret_cast<const Tin*>(p.Bm) + (int64_t)b * p.b_bs;
-  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
 
-  float acc[8][8];
+  float acc[RM][RN];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < RM; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < RN; ++j) acc[i][j] = 0.f;
 
   for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
 #pragma unroll
-    for (int i = 0; i < (BM * BK) / NT; ++i) {
+    for (int i = 0; i < (BM_ * BK) / NT; ++i) {
       int e = tid + i * NT;
       int mm, kk;
-      if (AK) { mm = e / BK; kk = e % BK; } else { mm = e % BM; kk = e / BM; }
+      if (AK) { mm = e / BK; kk = e % BK; } else { mm = e % BM_; kk = e / BM_; }
       int64_t gm = m0 + mm, gk = k0 + kk;
       float v = 0.f;
       if (gm < p.M && gk < kend) v = ldf(AK ? A + gm * p.a_ld + gk : A + gk * p.a_ld + gm);
@@ -56,15 +60,15 @@ __global__ void __launch_bounds__(NT) k_gemm_simt(GemmP p) {
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      float a[8], bb[8];
+      float a[RM], bb[RN];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = As[kk][ty + 16 * i];
+      for (int i = 0; i < RM; ++i) a[i] = As[kk][ty + TY * i];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) bb[j] = Bs[kk][tx + 16 * j];
+      for (int j = 0; j < RN; ++j) bb[j] = Bs[kk][tx + TX * j];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < RM; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+        for (int j = 0; j < RN; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
     }
     __syncthreads();
   }
@@ -72,12 +76,12 @@ __global__ void __launch_bounds__(NT) k_gemm_simt(GemmP p) {
   if (p.splits > 1) {
     float* part = p.part + ((int64_t)split * p.B + b) * p.M * p.N;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int64_t gm = m0 + ty + 16 * i;
+    for (int i = 0; i < RM; ++i) {
+      int64_t gm = m0 + ty + TY * i;
       if (gm >= p.M) continue;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        int64_t gn = n0 + tx + 16 * j;
+      for (int j = 0; j < RN; ++j) {
+        int64_t gn = n0 + tx + TX * j;
         if (gn < p.N) part[gm * p.N + gn] = acc[i][j];
       }
     }
@@ -85,13 +89,13 @@ __global__ void __launch_bounds__(NT) k_gemm_simt(GemmP p) {
   }
   Tout* C = reinterpret_cast<Tout*>(p.C) + (int64_t)b * p.c_bs;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    int64_t gm = m0 + ty + 16 * i;
+  for (int i = 0; i < RM; ++i) {
+    int64_t gm = m0 + ty + TY * i;
     if (gm >= p.M) continue;
     const float* brow = p.bias ? p.bias + (int64_t)b * p.bias_bs + (p.bias_div > 0 ? (gm / p.bias_div) * p.bias_ld : 0) : nullptr;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      int64_t gn = n0 + tx + 16 * j;
+    for (int j = 0; j < RN; ++j) {
+      int64_t gn = n0 + tx + TX * j;
       if (gn >= p.N) continue;
       float v = acc[i][j];
       if (brow) v += brow[gn];
@@ -115,17 +119,23 @@ __global__ void k_splitk_reduce(GemmP p) {
   }
 }
 
+template <typename Tin, typename Tout, int BM_>
+void launch_bm(const GemmP& p, dim3 grid, cudaStream_t s) {
+  if (p.a_kmajor && p.b_kmajor) k_gemm_simt<Tin, Tout, true, true, BM_><<<grid, NT, 0, s>>>(p);
+  else if (p.a_kmajor) k_gemm_simt<Tin, Tout, true, false, BM_><<<grid, NT, 0, s>>>(p);
+  else if (p.b_kmajor) k_gemm_simt<Tin, Tout, false, true, BM_><<<grid, NT, 0, s>>>(p);
+  else k_gemm_simt<Tin, Tout, false, false, BM_><<<grid, NT, 0, s>>>(p);
+}
 template <typename Tin, typename Tout>
 void launch(const GemmP& p, dim3 grid, cudaStream_t s) {
-  if (p.a_kmajor && p.b_kmajor) k_gemm_simt<Tin, Tout, true, true><<<grid, NT, 0, s>>>(p);
-  else if (p.a_kmajor) k_gemm_simt<Tin, Tout, true, false><<<grid, NT, 0, s>>>(p);
-  else if (p.b_kmajor) k_gemm_simt<Tin, Tout, false, true><<<grid, NT, 0, s>>>(p);
-  else k_gemm_simt<Tin, Tout, false, false><<<grid, NT, 0, s>>>(p);
+  if (p.M <= 32) launch_bm<Tin, Tout, 32>(p, grid, s);
+  else launch_bm<Tin, Tout, 128>(p, grid, s);
 }
 }  // namespace
 
 hfta_status gemm_simt(const GemmP& p, hfta_dtype dt_in, bool out_f32, cudaStream_t s) {
-  dim3 grid((unsigned)(cdiv(p.M, BM) * cdiv(p.N, BN)), (unsigned)p.splits, (unsigned)p.B);
+  const int bm = p.M <= 32 ? 32 : BM;
+  dim3 grid((unsigned)(cdiv(p.M, bm) * cdiv(p.N, BN)), (unsigned)p.splits, (unsigned)p.B);
   if (dt_in == HFTA_F32) launch<float, float>(p, grid, s);
   else if (out_f32) launch<__nv_bfloat16, float>(p, grid, s);
   else launch<__nv_bfloat16, __nv_bfloat16>(p, grid, s);

@@ -29,7 +29,8 @@ namespace {
 
 constexpr int BM = 128;     // UMMA M (one CTA, cta_group::1)
 constexpr int BK = 64;      // k per stage: 64 bf16 = 128 B = one swizzle row
-constexpr int NTHREADS = 192;
+constexpr int NTHREADS = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quarter)
+constexpr int NEPI = 8;
 
 // ------------------------------------------------------------ PTX wrappers --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -132,31 +133,43 @@ struct TcArgs {
   int tiles_m, tiles_n;
 };
 
-template <bool A_MN, bool B_MN, int BN, int STAGES, bool OUT_F32>
+// BRES ("B resident", forward layers with K <= 128): the B operand (the
+// weight slice of one model / n-tile, <= 2 k-blocks) stays in shared memory
+// while the CTA sweeps consecutive m-tiles of the same (model, n-tile) --
+// the static schedule gives each CTA ~M/128/148*B such tiles in a row -- so
+// only the activation tile streams through the ring (cuts L2->SM traffic 3x).
+template <bool A_MN, bool B_MN, int BN, int STAGES, bool OUT_F32, bool BRES>
 __global__ void __launch_bounds__(NTHREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmC, TcArgs p) {
   constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB
   constexpr uint32_t B_BYTES = BN * BK * 2;
-  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t STAGE_BYTES = BRES ? A_BYTES : A_BYTES + B_BYTES;
+  constexpr uint32_t BRES_BYTES = BRES ? 2 * B_BYTES : 0;
   constexpr uint32_t TMEM_COLS = 2 * BN;     // double-buffered accumulator
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
                              ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* bres = smem + STAGES * STAGE_BYTES;                      // BRES: 2 k-blocks of B
+  uint64_t* full = reinterpret_cast<uint64_t*>(bres + BRES_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfull = tempty + 2;
+  uint64_t* bempty = bfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 1);
   // per-epilogue-warp staging for the TMA store: 2 buffers x 32 rows x 64 B
-  uint8_t* stage_out = smem + STAGES * STAGE_BYTES + 1024;
+  uint8_t* stage_out = bres + BRES_BYTES + 1024;                   // NEPI warps x 2 x 2 KB
+  float* sbias_all = reinterpret_cast<float*>(stage_out + NEPI * 2 * 2048);   // NEPI warps x BN floats
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], NEPI); }
+    mbar_init(bfull, 1);
+    mbar_init(bempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -180,6 +193,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
       int stage = 0;
       uint32_t phase = 0;
+      int64_t bkey = -1;
+      uint32_t epoch = 0;
       for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
         int64_t r = t;
         int mt, nt;
@@ -192,11 +207,23 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int nkb = (int)((kend - kbeg + BK - 1) / BK);
         const int ba = p.a_shared ? 0 : b, bb = p.b_shared ? 0 : b;
         const int m0 = mt * BM, n0 = nt * BN;
+        if constexpr (BRES) {
+          const int64_t key = (int64_t)bb * p.tiles_n + nt;
+          if (key != bkey) {                       // new (model, n-tile): reload the resident B
+            if (bkey >= 0) { mbar_wait(bempty, (epoch - 1) & 1); }
+            mbar_expect_tx(bfull, (uint32_t)nkb * B_BYTES);
+            for (int kb = 0; kb < nkb; ++kb)
+              tma_load_3d(bres + kb * B_BYTES, &tmB, bfull, (int)(kbeg + (int64_t)kb * BK), n0, bb);
+            bkey = key;
+            ++epoch;
+          }
+        }
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
           mbar_expect_tx(&full[stage], STAGE_BYTES);
+          (void)sb;
           const int k0 = (int)(kbeg + (int64_t)kb * BK);
           if (A_MN) {
             tma_load_3d(sa, &tmA, &full[stage], m0, k0, ba);
@@ -204,11 +231,13 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           } else {
             tma_load_3d(sa, &tmA, &full[stage], k0, m0, ba);
           }
-          if (B_MN) {
+          if constexpr (!BRES) {
+            if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
-          } else {
-            tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
+              for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
+            } else {
+              tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -220,10 +249,25 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int64_t bkey = -1;
+    uint32_t epoch = 0;
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
       int64_t r = t;
-      if (p.order == 0) { r /= p.tiles_n; r /= p.tiles_m; } else { r /= p.tiles_m; r /= p.tiles_n; }
+      int nt_ = 0;
+      if (p.order == 0) { nt_ = (int)(r % p.tiles_n); r /= p.tiles_n; r /= p.tiles_m; }
+      else { r /= p.tiles_m; nt_ = (int)(r % p.tiles_n); r /= p.tiles_n; }
       const int split = (int)(r % p.splits);
+      if constexpr (BRES) {
+        const int bb_ = p.b_shared ? 0 : (int)(r / p.splits);
+        const int64_t key = (int64_t)bb_ * p.tiles_n + nt_;
+        if (key != bkey) {
+          if (bkey >= 0 && lane == 0) tc_commit(bempty);   // old B free once all prior MMAs retire
+          __syncwarp();
+          mbar_wait(bfull, epoch & 1);
+          bkey = key;
+          ++epoch;
+        }
+      }
       const int64_t kbeg = (int64_t)split * p.k_chunk;
       const int64_t kend = min(p.K, kbeg + p.k_chunk);
       const int nkb = (int)((kend - kbeg + BK - 1) / BK);
@@ -235,7 +279,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+          const uint32_t sb = BRES ? smem_u32(bres + kb * B_BYTES) : sa + A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // K-major: +32 B per 16-element k step inside the 128-B swizzle row;
@@ -257,6 +301,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   } else {
     // ============================== epilogue ==============================
     const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;             // two warps per quarter split the column chunks
+    float* sbias = sbias_all + (warp - 2) * BN;
     uint32_t sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -271,31 +317,39 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       tc_fence_after();
       const int64_t m = (int64_t)mt * BM + quarter * 32 + lane;
       const bool row_ok = m < p.M;
-      const float* brow = nullptr;
-      if (p.bias && row_ok)
-        brow = p.bias + (int64_t)b * p.bias_bs + (p.bias_div > 0 ? (m / p.bias_div) * p.bias_ld : 0);
+      const float* brow = nullptr;       // per-row bias table (row-grouped bias only)
+      if (p.bias && p.bias_div > 0 && row_ok)
+        brow = p.bias + (int64_t)b * p.bias_bs + (m / p.bias_div) * p.bias_ld;
+      const bool vbias = p.bias && p.bias_div == 0;
+      if (vbias) {                       // per-tile bias slice -> this warp's smem (broadcast reads later)
+        const float* bsrc = p.bias + (int64_t)b * p.bias_bs + (int64_t)nt * BN;
+#pragma unroll
+        for (int j = 0; j < BN / 32; ++j) {
+          const int64_t n = (int64_t)nt * BN + j * 32 + lane;
+          sbias[j * 32 + lane] = n < p.N ? bsrc[j * 32 + lane] : 0.f;
+        }
+        __syncwarp();
+      }
 #pragma unroll 1
-      for (int j = 0; j < BN / 32; ++j) {
+      for (int j = half; j < BN / 32; j += 2) {
         float v[32];
         tmem_ld32(tmem_base + (uint32_t)(acc * BN + j * 32) + ((uint32_t)(quarter * 32) << 16), v);
-        if (j == BN / 32 - 1) {
+        if (j + 2 >= BN / 32) {          // this warp's last chunk of the tile: release the accumulator
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
         const int64_t n0 = (int64_t)nt * BN + j * 32;
         if (n0 >= p.N) continue;                       // warp-uniform
-        if (brow) {
-          if (n0 + 32 <= p.N && ((reinterpret_cast<uintptr_t>(brow + n0) & 15) == 0)) {
-            const float4* bp = reinterpret_cast<const float4*>(brow + n0);   // warp-broadcast 128-bit loads
+        if (vbias) {
+          const float4* bp = reinterpret_cast<const float4*>(sbias + j * 32);   // smem broadcast
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 t4 = __ldg(bp + q);
-              v[4 * q] += t4.x; v[4 * q + 1] += t4.y; v[4 * q + 2] += t4.z; v[4 * q + 3] += t4.w;
-            }
-          } else {
-            for (int q = 0; q < 32 && n0 + q < p.N; ++q) v[q] += brow[n0 + q];
+          for (int q = 0; q < 8; ++q) {
+            const float4 t4 = bp[q];
+            v[4 * q] += t4.x; v[4 * q + 1] += t4.y; v[4 * q + 2] += t4.z; v[4 * q + 3] += t4.w;
           }
+        } else if (brow) {
+          for (int q = 0; q < 32 && n0 + q < p.N; ++q) v[q] += brow[n0 + q];
         }
         if constexpr (!OUT_F32) {
           // bf16: stage the warp's 32 x 32 sub-tile in smem, one TMA store per
@@ -380,10 +434,12 @@ hfta_status make_map(CUtensorMap* m, const void* ptr, int64_t inner, int64_t row
   return HFTA_OK;
 }
 
-template <bool A_MN, bool B_MN, int BN, bool OUT_F32>
+template <bool A_MN, bool B_MN, int BN, bool OUT_F32, bool BRES>
 hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
-  constexpr int STAGES = (BN == 256) ? 4 : 6;
-  constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + 4 * 2 * 2048;
+  constexpr int STAGES = BRES ? 6 : ((BN == 256) ? 3 : (BN == 128 ? 5 : 6));
+  constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + (BRES ? 0 : BN * BK * 2)) +
+                          (BRES ? 2 * BN * BK * 2 : 0) + 1024 + NEPI * 2 * 2048 + NEPI * BN * 4;
+  static_assert(SMEM <= 232448, "shared memory budget");
   if (hfta_status st = get_encode()) return st;
   CUtensorMap ta, tb;
   const int nba = p.a_bs == 0 ? 1 : p.B, nbb = p.b_bs == 0 ? 1 : p.B;
@@ -413,7 +469,7 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   a.accumulate = p.accumulate; a.part = p.part;
   a.tiles_m = (int)cdiv(p.M, BM); a.tiles_n = (int)cdiv(p.N, BN);
   a.order = (A_MN && B_MN) ? 1 : 0;
-  auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32>;
+  auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, BRES>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
@@ -428,9 +484,16 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
 
 template <bool A_MN, bool B_MN, bool OUT_F32>
 hfta_status dispatch_bn(const GemmP& p, cudaStream_t s) {
-  if (p.N <= 64) return launch_tc<A_MN, B_MN, 64, OUT_F32>(p, s);
-  if (p.N <= 128 || OUT_F32) return launch_tc<A_MN, B_MN, 128, OUT_F32>(p, s);
-  return launch_tc<A_MN, B_MN, 256, OUT_F32>(p, s);
+  if constexpr (!A_MN && !B_MN && !OUT_F32) {
+    if (p.K <= 2 * BK && p.splits == 1) {        // forward with small K: B-resident schedule
+      if (p.N <= 64) return launch_tc<A_MN, B_MN, 64, OUT_F32, true>(p, s);
+      if (p.N <= 128) return launch_tc<A_MN, B_MN, 128, OUT_F32, true>(p, s);
+      return launch_tc<A_MN, B_MN, 256, OUT_F32, true>(p, s);
+    }
+  }
+  if (p.N <= 64) return launch_tc<A_MN, B_MN, 64, OUT_F32, false>(p, s);
+  if (p.N <= 128 || OUT_F32) return launch_tc<A_MN, B_MN, 128, OUT_F32, false>(p, s);
+  return launch_tc<A_MN, B_MN, 256, OUT_F32, false>(p, s);
 }
 
 bool env_disabled() {
