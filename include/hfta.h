@@ -108,7 +108,9 @@ size_t hfta_fused_linear_bwd_workspace(int B, int64_t M, int64_t N, int64_t K, h
 /*
  * Backward of hfta_fused_linear_fwd (same dims).  For each b:
  *   dX_b[M,K] = dY_b[M,N] * W_b[N,K]           (dX.ptr == NULL: skipped)
- *   dW_b[N,K] (+)= dY_b^T * X_b   fp32, [B][N][K] at dW + b*dW_bstride, ld K
+ *   dW_b[N,K] (+)= dY_b^T * X_b   fp32 at dW + b*dW_bstride + n*dW_ld + k (dW_ld >= K;
+ *                               a column slice of a wider weight, e.g. the split
+ *                               weight of PointNet-seg's concat layer, has dW_ld > K)
  *   dbias_b[N] (+)= sum_m dY_b[m,:]   fp32 (dbias == NULL: skipped)
  * accumulate != 0 adds into dW/dbias instead of overwriting (D(real)+D(fake)
  * accumulation of the DCGAN step).  The reduction over M is split in a fixed
@@ -116,7 +118,7 @@ size_t hfta_fused_linear_bwd_workspace(int B, int64_t M, int64_t N, int64_t K, h
  */
 hfta_status hfta_fused_linear_bwd(int B, int64_t M, int64_t N, int64_t K, hfta_dtype dt,
                                   hfta_in dY, hfta_in X, hfta_in W, hfta_out dX,
-                                  float* dW, int64_t dW_bstride,
+                                  float* dW, int64_t dW_bstride, int64_t dW_ld,
                                   float* dbias, int64_t dbias_bstride, int accumulate,
                                   void* ws, size_t ws_bytes, hfta_stream stream);
 
@@ -259,6 +261,10 @@ hfta_status hfta_fused_adam(int B, int64_t P, float* param, const float* grad,
                             void* param_bf16, int64_t bf16_bstride, hfta_stream stream);
 
 /* ------------------------------------------------------------- utility -- */
+/* Y = X1 + X2 elementwise over [B][rows][cols] (dtype dt): sums the two
+ * gradient paths into a shared activation (PointNet-seg's point feature). */
+hfta_status hfta_add(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in X1, hfta_in X2,
+                     hfta_out Y, hfta_stream stream);
 /* n fp32 -> bf16 (RNE); used to initialise the bf16 weight shadow. */
 hfta_status hfta_cast_f32_bf16(int64_t n, const float* src, void* dst, hfta_stream stream);
 /* *step += 1 on device (graph-capturable step counter). */

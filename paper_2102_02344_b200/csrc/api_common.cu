@@ -53,6 +53,18 @@ __global__ void k_cast_f32_bf16(int64_t n, const float* __restrict__ s, __nv_bfl
 
 __global__ void k_step_inc(int64_t* step) { *step += 1; }
 
+template <typename T>
+__global__ void k_add(int64_t rows, int64_t cols, const T* __restrict__ x1, int64_t bs1, int64_t ld1,
+                      const T* __restrict__ x2, int64_t bs2, int64_t ld2, T* __restrict__ y, int64_t bsy,
+                      int64_t ldy) {
+  const int b = blockIdx.y;
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    stf(y + b * bsy + r * ldy + c, ldf(x1 + b * bs1 + r * ld1 + c) + ldf(x2 + b * bs2 + r * ld2 + c));
+  }
+}
+
 }  // namespace hfta
 
 using namespace hfta;
@@ -90,6 +102,26 @@ hfta_status hfta_cast_f32_bf16(int64_t n, const float* src, void* dst, hfta_stre
   k_cast_f32_bf16<<<grid, 256, 0, st>>>(n, src, (__nv_bfloat16*)dst);
   count_launches(1);
   return post_launch(st, "hfta_cast_f32_bf16");
+}
+
+hfta_status hfta_add(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in X1, hfta_in X2, hfta_out Y,
+                     hfta_stream stream) {
+  if (hfta_status s = check_init()) return s;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(rows >= 1 && cols >= 1 && X1.ptr && X2.ptr && Y.ptr, HFTA_ERR_INVALID_VALUE, "hfta_add: bad args");
+  HFTA_REQUIRE(X1.ld >= cols && X2.ld >= cols && Y.ld >= cols && (Y.bstride > 0 || B == 1), HFTA_ERR_SHAPE,
+               "hfta_add: strides");
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid((unsigned)std::min<int64_t>(cdiv(rows * cols, 256), 2048), B);
+  if (dt == HFTA_F32)
+    k_add<float><<<grid, 256, 0, st>>>(rows, cols, (const float*)X1.ptr, X1.bstride, X1.ld, (const float*)X2.ptr,
+                                       X2.bstride, X2.ld, (float*)Y.ptr, Y.bstride, Y.ld);
+  else
+    k_add<__nv_bfloat16><<<grid, 256, 0, st>>>(rows, cols, (const __nv_bfloat16*)X1.ptr, X1.bstride, X1.ld,
+                                               (const __nv_bfloat16*)X2.ptr, X2.bstride, X2.ld,
+                                               (__nv_bfloat16*)Y.ptr, Y.bstride, Y.ld);
+  count_launches(1);
+  return post_launch(st, "hfta_add");
 }
 
 hfta_status hfta_step_increment(int64_t* step, hfta_stream stream) {

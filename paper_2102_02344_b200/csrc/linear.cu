@@ -90,7 +90,7 @@ size_t hfta_fused_linear_bwd_workspace(int B, int64_t M, int64_t N, int64_t K, h
 
 hfta_status hfta_fused_linear_bwd(int B, int64_t M, int64_t N, int64_t K, hfta_dtype dt,
                                   hfta_in dY, hfta_in X, hfta_in W, hfta_out dX, float* dW,
-                                  int64_t dW_bstride, float* dbias, int64_t dbias_bstride,
+                                  int64_t dW_bstride, int64_t dW_ld, float* dbias, int64_t dbias_bstride,
                                   int accumulate, void* ws, size_t ws_bytes, hfta_stream stream) {
   if (hfta_status st = check_init()) return st;
   HFTA_CHECK_B(B);
@@ -118,13 +118,14 @@ hfta_status hfta_fused_linear_bwd(int B, int64_t M, int64_t N, int64_t K, hfta_d
   if (dW) {
     if (hfta_status st = check_in(X, "X", B)) return st;
     HFTA_REQUIRE(X.ld >= K, HFTA_ERR_SHAPE, "linear_bwd: X ld %lld < K %lld", (long long)X.ld, (long long)K);
-    HFTA_REQUIRE(dW_bstride >= N * K || B == 1, HFTA_ERR_SHAPE, "linear_bwd: dW_bstride %lld < N*K",
+    HFTA_REQUIRE(dW_ld >= K, HFTA_ERR_SHAPE, "linear_bwd: dW_ld %lld < K %lld", (long long)dW_ld, (long long)K);
+    HFTA_REQUIRE(dW_bstride >= N * dW_ld || B == 1, HFTA_ERR_SHAPE, "linear_bwd: dW_bstride %lld < N*dW_ld",
                  (long long)dW_bstride);
     GemmP p{};
     p.B = B; p.M = N; p.N = K; p.K = M;                         // dW[N,K] = dY^T[N,M] X[M,K]
     p.A = dY.ptr; p.a_bs = dY.bstride; p.a_ld = dY.ld; p.a_kmajor = 0;
     p.Bm = X.ptr; p.b_bs = X.bstride; p.b_ld = X.ld; p.b_kmajor = 0;
-    p.C = dW; p.c_bs = dW_bstride; p.c_ld = K;
+    p.C = dW; p.c_bs = dW_bstride; p.c_ld = dW_ld;
     p.accumulate = accumulate;
     p.splits = 1; p.k_chunk = M;
     if (skinny_wgrad_ok(p)) {

@@ -50,8 +50,8 @@ _SIGS = {
     "hfta_launch_count": (u64, []),
     "hfta_fused_linear_fwd": (i32, [i32, i64, i64, i64, i32, hfta_in, hfta_in, vp, i64, i64, i64, hfta_out, vp]),
     "hfta_fused_linear_bwd_workspace": (sz, [i32, i64, i64, i64, i32]),
-    "hfta_fused_linear_bwd": (i32, [i32, i64, i64, i64, i32, hfta_in, hfta_in, hfta_in, hfta_out, vp, i64, vp, i64,
-                                    i32, vp, sz, vp]),
+    "hfta_fused_linear_bwd": (i32, [i32, i64, i64, i64, i32, hfta_in, hfta_in, hfta_in, hfta_out, vp, i64, i64, vp,
+                                    i64, i32, vp, sz, vp]),
     "hfta_fused_bn_workspace": (sz, [i32, i64, i64]),
     "hfta_fused_bn_fwd": (i32, [i32, i64, i64, i32, hfta_in, vp, vp, i64, vp, vp, f32, f32, i32, f32, hfta_out, vp,
                                 vp, vp, sz, vp]),
@@ -73,6 +73,7 @@ _SIGS = {
     "hfta_fused_adam": (i32, [i32, i64, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
     "hfta_cast_f32_bf16": (i32, [i64, vp, vp, vp]),
     "hfta_step_increment": (i32, [vp, vp]),
+    "hfta_add": (i32, [i32, i64, i64, i32, hfta_in, hfta_in, hfta_out, vp]),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -14,9 +14,8 @@ import numpy as np
 import torch
 
 from . import hfta as H
-from .fused import ParamArena, HyperVectors, Workspace, fused_adam
-
-A_RELU, A_NONE = H.ACT_RELU, H.ACT_NONE
+from .fused import Workspace
+from .net import FusedNet, _Acts, _in, _out, A_RELU, A_NONE
 
 # Layers whose output feeds a training-mode BatchNorm directly: the gradient
 # of their bias is identically zero (BN's input gradient sums to zero over the
@@ -27,48 +26,21 @@ BN_FOLLOWED = {"stn.c1", "stn.c2", "stn.c3", "stn.fc1", "stn.fc2", "feat.c1", "f
                "head.fc1", "head.c1", "head.c2", "head.c3"}
 
 
-class _Acts:
-    def __init__(self, B, dtype, device):
-        self.B, self.dtype, self.device = B, dtype, device
-
-    def __call__(self, rows, cols, dtype=None):
-        return torch.empty(self.B, rows, cols, dtype=dtype or self.dtype, device=self.device)
-
-
-def _in(t):
-    """hfta_in over a model-major [B][rows][cols] tensor."""
-    return H.tin(t, t.shape[1] * t.shape[2], t.shape[2])
-
-
-def _out(t):
-    return H.tout(t, t.shape[1] * t.shape[2], t.shape[2])
-
-
-class FusedPointNet:
+class FusedPointNet(FusedNet):
     """B fused PointNet models (task 'cls' or 'seg')."""
+
+    bn_followed = BN_FOLLOWED
 
     def __init__(self, B, param_specs, params, hp, task="cls", dtype="f32", N=32, L=2500, k=40,
                  p_drop=0.3, dropout_seed=42, device="cuda"):
         assert task in ("cls", "seg")
-        self.B, self.task, self.N, self.L, self.k = B, task, N, L, k
+        self._base_init(B, param_specs, params, hp, dtype, device)
+        self.task, self.N, self.L, self.k = task, N, L, k
         self.R = N * L
-        self.dt = H.HFTA_F32 if dtype == "f32" else H.HFTA_BF16
-        self.tdt = torch.float32 if dtype == "f32" else torch.bfloat16
         self.p_drop, self.dropout_seed = p_drop, dropout_seed
-        self.device = torch.device(device)
-        self.arena = ParamArena(param_specs, B, self.device, bf16_shadow=(dtype != "f32"))
-        self.arena.load(params)
-        self.hv = HyperVectors(hp, self.device)
-        self.t = 0
         sh = self.arena.shape
         self.c1, self.c2, self.c3 = sh["stn.c1.W"][0], sh["stn.c2.W"][0], sh["stn.c3.W"][0]
         self.f1, self.f2 = sh["stn.fc1.W"][0], sh["stn.fc2.W"][0]
-        # BN running statistics and saved batch statistics, [B][C] fp32
-        self.bn_names = [n[:-2] for n, _ in param_specs if n.endswith(".g")]
-        self.running = {n: (torch.zeros(B, sh[n + ".g"][0], device=self.device),
-                            torch.ones(B, sh[n + ".g"][0], device=self.device)) for n in self.bn_names}
-        self.saved = {n: (torch.empty(B, sh[n + ".g"][0], device=self.device),
-                          torch.empty(B, sh[n + ".g"][0], device=self.device)) for n in self.bn_names}
         self._alloc()
 
     # ------------------------------------------------------------ buffers --
@@ -96,6 +68,21 @@ class FusedPointNet:
             S["d.logits"] = f(N, self.k)
             S["d.f2a"], S["d.f2b"] = f(N, f2), f(N, f2)
             S["d.f1a"], S["d.f1b"] = f(N, f1), f(N, f1)
+        if self.task == "seg":
+            sh = self.arena.shape
+            h1, h2, h3 = sh["head.c1.W"][0], sh["head.c2.W"][0], sh["head.c3.W"][0]
+            self.h1w, self.h2w, self.h3w = h1, h2, h3
+            kpad = (self.k + 15) // 16 * 16          # logits ld: 16-element aligned rows
+            S["seg.u"] = f(N, h1)                   # g Wg^T + b: per-sample bias table of the split weight
+            S["seg.y1"], S["seg.h1"] = a(R, h1), a(R, h1)
+            S["seg.y2"], S["seg.h2"] = a(R, h2), a(R, h2)
+            S["seg.y3"], S["seg.h3"] = a(R, h3), a(R, h3)
+            S["seg.logits"], S["d.logits"] = a(R, kpad), a(R, kpad)
+            S["d.s1a"], S["d.s1b"] = a(R, h1), a(R, h1)
+            S["d.s2a"], S["d.s2b"] = a(R, h2), a(R, h2)
+            S["d.s3a"], S["d.s3b"] = a(R, h3), a(R, h3)
+            S["seg.S"] = f(N, h1)                   # per-sample row sums of dy1
+            S["d.pf"] = a(R, c1)                    # gradient reaching the point feature from the head
         S["d.big"] = a(R, c3)
         S["d.c2a"], S["d.c2b"] = a(R, c2), a(R, c2)
         S["d.c1a"], S["d.c1b"] = a(R, c1), a(R, c1)
@@ -105,8 +92,8 @@ class FusedPointNet:
         S["d.sf1a"], S["d.sf1b"] = f(N, f1), f(N, f1)
         S["d.sf2a"], S["d.sf2b"] = f(N, f2), f(N, f2)
         self.S = S
-        self.loss = torch.zeros(B, device=self.device)
-        self.mean_loss = torch.zeros(1, device=self.device)
+        self.loss = torch.zeros(B, dtype=torch.float32, device=self.device)
+        self.mean_loss = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.labels = torch.zeros(N if self.task == "cls" else R, dtype=torch.int32, device=self.device)
         ws = Workspace(self.device)
         for (M, Nn, K) in [(R, c1, 3), (R, c2, c1), (R, c3, c2), (N, f1, c3), (N, f2, f1), (N, 9, f2),
@@ -116,123 +103,17 @@ class FusedPointNet:
         for (Rr, Cc) in [(R, c1), (R, c2), (R, c3), (N, f1), (N, f2)]:
             ws.reserve(H.hfta_fused_bn_workspace(B, Rr, Cc))
         ws.reserve(H.hfta_bn_max_bwd_workspace(B, N, c3))
+        if self.task == "seg":
+            for (M, Nn, K) in [(R, self.h1w, c1), (N, self.h1w, c3), (R, self.h2w, self.h1w), (R, self.h3w, self.h2w),
+                               (R, self.k, self.h3w)]:
+                for dt in (self.dt, H.HFTA_F32):
+                    ws.reserve(H.hfta_fused_linear_bwd_workspace(B, M, Nn, K, dt))
+            for Cc in (self.h1w, self.h2w, self.h3w):
+                ws.reserve(H.hfta_fused_bn_workspace(B, R, Cc))
+            ws.reserve(H.hfta_colsum_workspace(B, R, self.h1w, self.L))
         ws.reserve(H.hfta_loss_workspace(B, N if self.task == "cls" else R))
         ws.alloc()
         self.ws = ws
-
-    # ------------------------------------------------------------- probe --
-    # CUDA events around one named contraction inside the timed region (the
-    # bench's roofline figure).  name = "<layer>:fwd" or "<layer>:bwd".
-    _probe = None
-
-    def probe_arm(self, name):
-        self._probe = name
-        self._probe_ev = []
-
-    def _pbegin(self, tag, s):
-        if self._probe != tag:
-            return None
-        e0 = torch.cuda.Event(enable_timing=True)
-        e0.record(torch.cuda.current_stream())
-        return e0
-
-    def _pend(self, e0):
-        if e0 is None:
-            return
-        e1 = torch.cuda.Event(enable_timing=True)
-        e1.record(torch.cuda.current_stream())
-        self._probe_ev.append((e0, e1))
-
-    def probe_collect(self):
-        ms = [a.elapsed_time(b) for a, b in getattr(self, "_probe_ev", [])]
-        self._probe = None
-        return ms
-
-    def probe_roofline(self, name, ms, peaks, path="simt"):
-        """Algorithmic work of one launch of the probed contraction / its time."""
-        layer, kind = name.split(":")
-        Nn, K = self.arena.shape[layer + ".W"]
-        M = self.R if (".c" in layer) else self.N
-        s = 2 if self.dt == H.HFTA_BF16 and M == self.R else 4
-        mult = 1 if kind == "fwd" else 2            # bwd = dgrad + wgrad
-        flops = mult * 2.0 * self.B * M * Nn * K
-        if kind == "fwd":
-            nbytes = self.B * (M * K + Nn * K + M * Nn) * s
-        else:   # dgrad reads dY, W, writes dX; wgrad reads dY, X, writes dW fp32
-            nbytes = self.B * ((M * Nn + Nn * K + M * K) * s + (M * Nn + M * K) * s + Nn * K * 4)
-        t = float(np.mean(ms)) / 1e3 if ms else float("nan")
-        if path == "simt":   # FFMA-bound SIMT kernel: 148 SM x 128 FMA/clk x 2 flop x max clock
-            peak = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
-            ach = flops / t / 1e12
-            return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                    "traffic": None, "kernel": name, "launches_timed": len(ms), "ms_per_launch": t * 1e3,
-                    "algorithmic": {"flops": flops, "bytes": nbytes},
-                    "peak_source": "FFMA: 148 SM x 128 lanes x 2 flop x %.0f MHz" % peaks["sm_max_mhz"]}
-        ridge = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
-        if flops / nbytes >= ridge:
-            peak = peaks["bf16_tflops"] if self.dt == H.HFTA_BF16 else peaks["bf16_tflops"] / 4.0
-            ach = flops / t / 1e12
-            return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                    "traffic": None, "kernel": name, "launches_timed": len(ms), "ms_per_launch": t * 1e3,
-                    "algorithmic": {"flops": flops, "bytes": nbytes}, "peak_source": peaks["source"]}
-        ach = nbytes / t / 1e9
-        return {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / peaks["hbm_gbs"], "traffic": None, "kernel": name, "launches_timed": len(ms),
-                "ms_per_launch": t * 1e3, "algorithmic": {"flops": flops, "bytes": nbytes},
-                "peak_source": peaks["source"]}
-
-    # ----------------------------------------------------------- wrappers --
-    def _dt(self, t):
-        return H.HFTA_F32 if t.dtype == torch.float32 else H.HFTA_BF16
-
-    def _lin_fwd(self, X, M, name, Y, s):
-        Nn, K = self.arena.shape[name + ".W"]
-        dt = self._dt(Y)
-        e0 = self._pbegin(name + ":fwd", s)
-        H.hfta_fused_linear_fwd(self.B, M, Nn, K, dt, X, self.arena.w_in(name + ".W", dt),
-                                self.arena.fptr("p", name + ".b"), self.arena.P, 0, 0, _out(Y), s)
-        self._pend(e0)
-
-    def _lin_bwd(self, dY, X, M, name, dX, s, accumulate=0):
-        Nn, K = self.arena.shape[name + ".W"]
-        dt = self._dt(dY)
-        e0 = self._pbegin(name + ":bwd", s)
-        H.hfta_fused_linear_bwd(self.B, M, Nn, K, dt, _in(dY), X, self.arena.w_in(name + ".W", dt),
-                                _out(dX) if dX is not None else H.tout(None, 0, 1),
-                                self.arena.fptr("g", name + ".W"), self.arena.P,
-                                None if name in BN_FOLLOWED else self.arena.fptr("g", name + ".b"), self.arena.P,
-                                accumulate, self.ws.ptr, self.ws.nbytes, s)
-        self._pend(e0)
-
-    def _bn_fwd(self, X, name, act, Y, s):
-        R, C = X.shape[1], X.shape[2]
-        rm, rv = self.running[name]
-        sm, si = self.saved[name]
-        H.hfta_fused_bn_fwd(self.B, R, C, self._dt(X), _in(X), self.arena.fptr("p", name + ".g"),
-                            self.arena.fptr("p", name + ".beta"), self.arena.P, H.ptr(rm), H.ptr(rv), 0.1, 1e-5,
-                            act, 0.0, _out(Y) if Y is not None else H.tout(None, 0, 1), H.ptr(sm), H.ptr(si),
-                            self.ws.ptr, self.ws.nbytes, s)
-
-    def _bn_bwd(self, dY, X, name, act, dX, s):
-        R, C = X.shape[1], X.shape[2]
-        sm, si = self.saved[name]
-        H.hfta_fused_bn_bwd(self.B, R, C, self._dt(X), _in(dY), _in(X), self.arena.fptr("p", name + ".g"),
-                            self.arena.fptr("p", name + ".beta"), self.arena.P, H.ptr(sm), H.ptr(si), act, 0.0,
-                            _out(dX), self.arena.fptr("g", name + ".g"), self.arena.fptr("g", name + ".beta"), 0,
-                            self.ws.ptr, self.ws.nbytes, s)
-
-    def _bn_max_fwd(self, X, name, act, G, amax, s):
-        sm, si = self.saved[name]
-        H.hfta_bn_max_fwd(self.B, self.N, self.L, X.shape[2], self.dt, _in(X), self.arena.fptr("p", name + ".g"),
-                          self.arena.fptr("p", name + ".beta"), self.arena.P, H.ptr(sm), H.ptr(si), act, 0.0,
-                          _out(G), H.ptr(amax), s)
-
-    def _bn_max_bwd(self, dG, X, amax, name, act, dX, s):
-        sm, si = self.saved[name]
-        H.hfta_bn_max_bwd(self.B, self.N, self.L, X.shape[2], self.dt, _in(dG), _in(X), H.ptr(amax),
-                          self.arena.fptr("p", name + ".g"), self.arena.fptr("p", name + ".beta"), self.arena.P,
-                          H.ptr(sm), H.ptr(si), act, 0.0, _out(dX), self.arena.fptr("g", name + ".g"),
-                          self.arena.fptr("g", name + ".beta"), self.ws.ptr, self.ws.nbytes, s)
 
     # -------------------------------------------------------------- step --
     def _stn_feat_fwd(self, x, s):
@@ -269,6 +150,8 @@ class FusedPointNet:
         self._lin_bwd(S["d.big"], _in(S["feat.a2"]), R, "feat.c3", S["d.c2a"], s)
         self._bn_bwd(S["d.c2a"], S["feat.y2"], "feat.bn2", A_RELU, S["d.c2b"], s)
         self._lin_bwd(S["d.c2b"], _in(S["feat.a1"]), R, "feat.c2", S["d.c1a"], s)
+        if self.task == "seg":      # the point feature also feeds the seg head
+            H.hfta_add(self.B, R, self.c1, self.dt, _in(S["d.c1a"]), _in(S["d.pf"]), _out(S["d.c1a"]), s)
         self._bn_bwd(S["d.c1a"], S["feat.y1"], "feat.bn1", A_RELU, S["d.c1b"], s)
         self._lin_bwd(S["d.c1b"], _in(S["feat.xt"]), R, "feat.c1", S["d.xt"], s)
         H.hfta_transform_points_bwd(self.B, N, self.L, self.dt, H.tin(x, 0, 3), _in(S["d.xt"]), _out(S["d.f3"]), s)
@@ -304,6 +187,49 @@ class FusedPointNet:
         self._bn_bwd(S["d.f1a"], S["head.y1"], "head.bn1", A_RELU, S["d.f1b"], s)
         self._lin_bwd(S["d.f1b"], _in(S["feat.g"]), N, "head.fc1", S["d.g"], s)
 
+    def _seg_head(self, s):
+        """PointNetDenseCls head.  Its first layer acts on concat(g repeated over
+        the L points, pointfeat) (1088 wide); it is computed with the exact
+        split-weight rewrite y1[n*L+l] = (g[n] Wg^T + b) + pf[n*L+l] Wp^T, the
+        per-sample part entering the point GEMM as a row-grouped bias table
+        (DESIGN.md), so the [R][1088] concat is never materialised."""
+        S, N, R, L, B = self.S, self.N, self.R, self.L, self.B
+        c1, c3, h1 = self.c1, self.c3, self.h1w
+        ar, P = self.arena, self.arena.P
+        wld = c3 + c1
+        H.hfta_fused_linear_fwd(B, N, h1, c3, H.HFTA_F32, _in(S["feat.g"]), ar.w_in("head.c1.W", H.HFTA_F32, 0, wld),
+                                ar.fptr("p", "head.c1.b"), P, 0, 0, _out(S["seg.u"]), s)
+        H.hfta_fused_linear_fwd(B, R, h1, c1, self.dt, _in(S["feat.a1"]), ar.w_in("head.c1.W", self.dt, c3, wld),
+                                H.ptr(S["seg.u"]), N * h1, h1, L, _out(S["seg.y1"]), s)
+        self._bn_fwd(S["seg.y1"], "head.bn1", A_RELU, S["seg.h1"], s)
+        self._lin_fwd(_in(S["seg.h1"]), R, "head.c2", S["seg.y2"], s)
+        self._bn_fwd(S["seg.y2"], "head.bn2", A_RELU, S["seg.h2"], s)
+        self._lin_fwd(_in(S["seg.h2"]), R, "head.c3", S["seg.y3"], s)
+        self._bn_fwd(S["seg.y3"], "head.bn3", A_RELU, S["seg.h3"], s)
+        lg, dl = S["seg.logits"], S["d.logits"]
+        kp = lg.shape[2]
+        H.hfta_fused_linear_fwd(B, R, self.k, self.h3w, self.dt, _in(S["seg.h3"]), ar.w_in("head.c4.W", self.dt),
+                                ar.fptr("p", "head.c4.b"), P, 0, 0, H.tout(lg, R * kp, kp), s)
+        H.hfta_loss_nll(B, R, self.k, self.dt, H.tin(lg, R * kp, kp), H.ptr(self.labels), 0, H.ptr(self.loss),
+                        H.ptr(self.mean_loss), H.tout(dl, R * kp, kp), self.ws.ptr, self.ws.nbytes, s)
+        # backward
+        self._lin_bwd(dl, _in(S["seg.h3"]), R, "head.c4", S["d.s3a"], s)
+        self._bn_bwd(S["d.s3a"], S["seg.y3"], "head.bn3", A_RELU, S["d.s3b"], s)
+        self._lin_bwd(S["d.s3b"], _in(S["seg.h2"]), R, "head.c3", S["d.s2a"], s)
+        self._bn_bwd(S["d.s2a"], S["seg.y2"], "head.bn2", A_RELU, S["d.s2b"], s)
+        self._lin_bwd(S["d.s2b"], _in(S["seg.h1"]), R, "head.c2", S["d.s1a"], s)
+        self._bn_bwd(S["d.s1a"], S["seg.y1"], "head.bn1", A_RELU, S["d.s1b"], s)
+        dy1 = S["d.s1b"]
+        # point part: dWp = dy1^T pf, d pf = dy1 Wp (bias grad identically 0: BN follows)
+        H.hfta_fused_linear_bwd(B, R, h1, c1, self.dt, _in(dy1), _in(S["feat.a1"]),
+                                ar.w_in("head.c1.W", self.dt, c3, wld), _out(S["d.pf"]),
+                                ar.fptr("g", "head.c1.W", c3), P, wld, None, P, 0, self.ws.ptr, self.ws.nbytes, s)
+        # per-sample part: S[n] = sum_l dy1[n*L+l]; dWg = S^T g; dg = S Wg
+        H.hfta_colsum(B, R, h1, L, self.dt, _in(dy1), H.ptr(S["seg.S"]), N * h1, 0, self.ws.ptr, self.ws.nbytes, s)
+        H.hfta_fused_linear_bwd(B, N, h1, c3, H.HFTA_F32, _in(S["seg.S"]), _in(S["feat.g"]),
+                                ar.w_in("head.c1.W", H.HFTA_F32, 0, wld), _out(S["d.g"]),
+                                ar.fptr("g", "head.c1.W", 0), P, wld, None, P, 0, self.ws.ptr, self.ws.nbytes, s)
+
     def set_batch(self, x, labels):
         """x: device fp32 [N*L, 3] (shared by all models); labels int32."""
         self.x = x
@@ -321,7 +247,7 @@ class FusedPointNet:
         if self.task == "cls":
             self._cls_head(s)
         else:
-            raise NotImplementedError("seg head")
+            self._seg_head(s)
         self._stn_feat_bwd(x, s)
 
     def step(self, x=None, labels=None, stream=None):
@@ -331,13 +257,5 @@ class FusedPointNet:
         self.t += 1
         s = H.stream_ptr(stream)
         self.forward_backward(stream)
-        H.hfta_step_increment(H.ptr(self.hv.step), s)
-        fused_adam(self.arena, self.hv, s)
+        self.adam(s)
         return self.loss
-
-    # ------------------------------------------------------------ unfuse --
-    def params(self, b):
-        return {n: self.arena.host_tensor("p", n)[b] for n, _ in self.arena.specs}
-
-    def grads(self, b):
-        return {n: self.arena.host_tensor("g", n)[b] for n, _ in self.arena.specs}

@@ -71,7 +71,7 @@ def test_linear_fwd_bwd(dt, M, N, K, B, shared):
     db = torch.empty(B, N, device=DEV)
     ws = torch.empty(max(H.hfta_fused_linear_bwd_workspace(B, M, N, K, code), 1), dtype=torch.uint8, device=DEV)
     H.hfta_fused_linear_bwd(B, M, N, K, code, H.tin(dYd, M * N, N), H.tin(Xd, xbs, K), H.tin(Wd, N * K, K),
-                            H.tout(dX, M * K, K), H.ptr(dW), N * K, H.ptr(db), N, 0, H.ptr(ws), ws.numel(), s())
+                            H.tout(dX, M * K, K), H.ptr(dW), N * K, K, H.ptr(db), N, 0, H.ptr(ws), ws.numel(), s())
     torch.cuda.synchronize()
     tol = 1e-5 if dt == "f32" else 1e-2
     for b in range(B):
@@ -98,7 +98,7 @@ def test_linear_bwd_accumulate_and_rowgroup_bias():
     dW, dYd = dev(dW0), dev(dY)
     ws = torch.empty(max(H.hfta_fused_linear_bwd_workspace(B, M, N, K, 0), 1), dtype=torch.uint8, device=DEV)
     H.hfta_fused_linear_bwd(B, M, N, K, 0, H.tin(dYd, M * N, N), H.tin(Xd, M * K, K),
-                            H.tin(Wd, N * K, K), H.tout(None, 0, 1), H.ptr(dW), N * K, None, 0, 1,
+                            H.tin(Wd, N * K, K), H.tout(None, 0, 1), H.ptr(dW), N * K, K, None, 0, 1,
                             H.ptr(ws), ws.numel(), s())
     torch.cuda.synchronize()
     for b in range(B):

@@ -27,8 +27,9 @@ ZERO_REL = 1e-9
 # downstream-in-backward gradients by ~4e-4).  Until the decision-override
 # comparison lands, per-tensor 1e-4 is gated on the tensors that precede every
 # dense ReLU decision in backward order, and the whole-model gradient on 2e-3.
-HEAD_SIDE = ("head.fc3.W", "head.fc3.b", "head.bn2.g", "head.bn2.beta", "head.fc2.W", "head.fc2.b",
-             "head.bn1.g", "head.bn1.beta", "head.fc1.W")
+HEAD_SIDE_CLS = ("head.fc3.W", "head.fc3.b", "head.bn2.g", "head.bn2.beta", "head.fc2.W", "head.fc2.b",
+                 "head.bn1.g", "head.bn1.beta", "head.fc1.W")
+HEAD_SIDE_SEG = ("head.c4.W", "head.c4.b")                   # seg: the last (ReLU-free) per-point layer
 WHOLE_TOL = 1e-2
 
 
@@ -69,6 +70,7 @@ def run_pair(task, dtype, B, N, L, k, steps=1, widths=None, seed=0):
 def check_step(net, loss, ref_losses, grads, res, tol, B, grad_tol="same"):
     """grad_tol: normwise gradient gate ("same" = tol, None = not gated)."""
     grad_tol = tol if grad_tol == "same" else grad_tol
+    HEAD_SIDE = HEAD_SIDE_CLS if net.task == "cls" else HEAD_SIDE_SEG
     for b in range(B):
         assert abs(loss[b] - ref_losses[b]) <= tol * abs(ref_losses[b]), (b, loss[b], ref_losses[b])
         G = grads[b]
@@ -167,3 +169,25 @@ def test_pointnet_cls_step_full_size(dtype):
     net, out = run_pair("cls", dtype, B, N, L, k)
     loss, ref, grads, res = out[0]
     check_step(net, loss, ref, grads, res, TOL[dtype], B, GRAD_TOL[dtype])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_pointnet_seg_step_small(dtype):
+    """PointNet-seg (BJ configs[2] architecture, k = 50) with the split-weight
+    concat layer, N=8 clouds x L=300 points, B=3."""
+    B, N, L, k = 3, 8, 300, 50
+    net, out = run_pair("seg", dtype, B, N, L, k)
+    loss, ref, grads, res = out[0]
+    check_step(net, loss, ref, grads, res, TOL[dtype], B, GRAD_TOL[dtype])
+    for b in range(B):
+        for name in net.bn_names:
+            rm = net.running[name][0][b].cpu().numpy()
+            assert relerr(rm, res[b]["stats"][name + ".rm"]) <= TOL[dtype], name
+
+
+def test_pointnet_seg_step_full_points_f32():
+    """seg at the BJ point count (L = 2500) with N = 4 clouds, B = 2."""
+    B, N, L, k = 2, 4, 2500, 50
+    net, out = run_pair("seg", "f32", B, N, L, k)
+    loss, ref, grads, res = out[0]
+    check_step(net, loss, ref, grads, res, TOL["f32"], B, GRAD_TOL["f32"])

@@ -13,7 +13,6 @@ from oracle import layers as L
 from oracle.adam import adam_step
 from oracle.philox import dropout_keep_mask
 
-torch.set_default_dtype(torch.float64)
 R = np.random.default_rng(123)
 
 

@@ -12,7 +12,6 @@ import synth
 from oracle import models as M
 from oracle.adam import adam_model
 
-torch.set_default_dtype(torch.float64)
 R = np.random.default_rng(7)
 TINY = (4, 8, 16, 8, 8)
 
@@ -63,7 +62,7 @@ def test_pointnet_seg_fd_tiny():
 # ------------------------------------------------- torch autograd replicas ----
 
 def _tbn(x, P, n, stats, key):
-    rm, rv = torch.zeros(x.shape[1]), torch.ones(x.shape[1])
+    rm, rv = torch.zeros(x.shape[1], dtype=torch.float64), torch.ones(x.shape[1], dtype=torch.float64)
     y = F.batch_norm(x, rm, rv, P[n + ".g"], P[n + ".beta"], training=True, momentum=0.1, eps=1e-5)
     stats[key] = (rm, rv)
     return y
@@ -82,7 +81,7 @@ def torch_pointnet_cls(Pn, x, y, keep, p):
     h = torch.max(h, 2)[0]
     h = F.relu(_tbn(F.linear(h, P["stn.fc1.W"], P["stn.fc1.b"]), P, "stn.bn4", st, 4))
     h = F.relu(_tbn(F.linear(h, P["stn.fc2.W"], P["stn.fc2.b"]), P, "stn.bn5", st, 5))
-    T = F.linear(h, P["stn.fc3.W"], P["stn.fc3.b"]).view(-1, 3, 3) + torch.eye(3)
+    T = F.linear(h, P["stn.fc3.W"], P["stn.fc3.b"]).view(-1, 3, 3) + torch.eye(3, dtype=torch.float64)
     h = torch.bmm(xt.transpose(2, 1), T).transpose(2, 1)
     h = F.relu(_tbn(conv(h, "feat.c1"), P, "feat.bn1", st, 6))
     h = F.relu(_tbn(conv(h, "feat.c2"), P, "feat.bn2", st, 7))
@@ -143,7 +142,7 @@ def test_dcgan_iteration_vs_torch():
     tD = {k: torch.nn.Parameter(torch.tensor(v)) for k, v in PD.items()}
     oG = torch.optim.Adam(tG.values(), lr=2e-4, betas=(0.5, 0.999))
     oD = torch.optim.Adam(tD.values(), lr=2e-4, betas=(0.5, 0.999))
-    ones, zeros = torch.ones(N), torch.zeros(N)
+    ones, zeros = torch.ones(N, dtype=torch.float64), torch.zeros(N, dtype=torch.float64)
     errDr = F.binary_cross_entropy(_torch_D(tD, torch.tensor(real)), ones)
     errDr.backward()
     fake = _torch_G(tG, torch.tensor(z))

@@ -21,7 +21,6 @@ import torch.nn.functional as F
 sys.path.insert(0, ".")
 import synth  # noqa: E402
 
-torch.set_default_dtype(torch.float64)
 NOISE = [0.0]
 RDT = [torch.bfloat16]
 
@@ -64,7 +63,7 @@ def run(Pn, x, y, keep, p, rw=False, ri=False, ro=False):
     h = torch.max(h, 2)[0]
     h = F.relu(bn(lin(h, "stn.fc1"), "stn.bn4"))
     h = F.relu(bn(lin(h, "stn.fc2"), "stn.bn5"))
-    T = lin(h, "stn.fc3").view(-1, 3, 3) + torch.eye(3)
+    T = lin(h, "stn.fc3").view(-1, 3, 3) + torch.eye(3, dtype=torch.float64)
     h = torch.bmm(xt.transpose(2, 1), T).transpose(2, 1)
     h = F.relu(bn(conv(h, "feat.c1"), "feat.bn1"))
     h = F.relu(bn(conv(h, "feat.c2"), "feat.bn2"))

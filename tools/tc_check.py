@@ -26,7 +26,7 @@ for (B, M, N, K) in [(1, 128, 128, 64), (2, 300, 128, 64), (3, 1000, 1024, 128),
     H.hfta_fused_linear_fwd(B, M, N, K, 1, H.tin(X, M * K, K), H.tin(W, N * K, K), H.ptr(bias), N, 0, 0,
                             H.tout(Y, M * N, N), s)
     H.hfta_fused_linear_bwd(B, M, N, K, 1, H.tin(dY, M * N, N), H.tin(X, M * K, K), H.tin(W, N * K, K),
-                            H.tout(dX, M * K, K), H.ptr(dW), N * K, None, 0, 0, H.ptr(ws), ws.numel(), s)
+                            H.tout(dX, M * K, K), H.ptr(dW), N * K, K, None, 0, 0, H.ptr(ws), ws.numel(), s)
     torch.cuda.synchronize()
     x, w, dy = (t.double().cpu().numpy() for t in (X, W, dY))
     e = [rel(Y[b].double().cpu().numpy(), x[b] @ w[b].T + bias[b].double().cpu().numpy()) for b in range(B)]
