@@ -64,7 +64,10 @@ enum {
 };
 
 typedef enum { HFTA_F32 = 0, HFTA_BF16 = 1 } hfta_dtype;
-typedef enum { HFTA_ACT_NONE = 0, HFTA_ACT_RELU = 1, HFTA_ACT_LEAKY_RELU = 2 } hfta_act;
+typedef enum {
+  HFTA_ACT_NONE = 0, HFTA_ACT_RELU = 1, HFTA_ACT_LEAKY_RELU = 2,
+  HFTA_ACT_TANH = 3, HFTA_ACT_SIGMOID = 4      /* standalone hfta_act_* only */
+} hfta_act;
 
 typedef struct { const void* ptr; int64_t bstride; int64_t ld; } hfta_in;
 typedef struct { void* ptr; int64_t bstride; int64_t ld; } hfta_out;
@@ -121,6 +124,33 @@ hfta_status hfta_fused_linear_bwd(int B, int64_t M, int64_t N, int64_t K, hfta_d
                                   float* dW, int64_t dW_bstride, int64_t dW_ld,
                                   float* dbias, int64_t dbias_bstride, int accumulate,
                                   void* ws, size_t ws_bytes, hfta_stream stream);
+
+/* -------------------------------------------- fused Conv2d / ConvT2d -- */
+/*
+ * Fused Conv2d / ConvTranspose2d (App. B rows P:L1262-1263, P:L1268-1269;
+ * grouped convolution with G = B, Fig. 3), NHWC per model.
+ * desc: N images of H x W x C_in (the layer INPUT), C_out channels, kernel
+ * kh x kw, stride, pad; transposed = 1 selects ConvTranspose2d (output size
+ * (H-1)*stride - 2*pad + kh), else output (H + 2 pad - kh)/stride + 1.
+ * Layouts (elements): X [B][N][H][W][C_in] (bstride 0 = shared images),
+ * Y [B][N][Ho][Wo][C_out];
+ * Conv2d weight W [B][C_out][kh][kw][C_in]   (PyTorch [Co][Ci][kh][kw] permuted),
+ * ConvT2d weight W [B][kh][kw][C_out][C_in]  (PyTorch [Ci][Co][kh][kw] permuted).
+ * dW fp32 in the same layout at dW + b*dW_bstride (accumulate != 0 adds: the
+ * D(real) + D(fake) gradient accumulation of the DCGAN step).  dX.ptr NULL /
+ * dW NULL skip that output.  No bias (the DCGAN convolutions have none).
+ * Channel counts: TMA/tensor-core path when rows are 16-B multiples (pad C_in
+ * 100 -> 104 for the generator input), SIMT otherwise.
+ */
+typedef struct {
+  int N, H, W, C_in, C_out, kh, kw, stride, pad, transposed;
+} hfta_conv_desc;
+size_t hfta_fused_conv_workspace(int B, const hfta_conv_desc* desc, hfta_dtype dt);
+hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* desc, hfta_dtype dt, hfta_in X, hfta_in W,
+                                hfta_out Y, void* ws, size_t ws_bytes, hfta_stream stream);
+hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* desc, hfta_dtype dt, hfta_in dY, hfta_in X,
+                                hfta_in W, hfta_out dX, float* dW, int64_t dW_bstride, int accumulate,
+                                void* ws, size_t ws_bytes, hfta_stream stream);
 
 /* ------------------------------------------------------- fused BatchNorm -- */
 /*
@@ -235,6 +265,15 @@ hfta_status hfta_loss_nll(int B, int64_t rows, int64_t K, hfta_dtype dt, hfta_in
                           const int32_t* labels, int64_t labels_bstride, float* loss,
                           float* mean_loss, hfta_out dlogits, void* ws, size_t ws_bytes,
                           hfta_stream stream);
+/*
+ * Sigmoid + BCE (DCGAN discriminator output, PyTorch BCELoss with its log clamp
+ * at -100): p = sigmoid(z), l_b = -(1/rows) sum_r [y log p + (1-y) log(1-p)],
+ * dz = (p - y)/rows (the BCELoss backward (p-y)/max(p(1-p),1e-12) times
+ * sigmoid' p(1-p)).  Z, dZ dtype dt [B][rows] (ld = row stride); y scalar.
+ */
+hfta_status hfta_loss_bce_logits(int B, int64_t rows, hfta_dtype dt, hfta_in Z, float target, float* loss,
+                                 float* mean_loss, hfta_out dZ, void* ws, size_t ws_bytes,
+                                 hfta_stream stream);
 /* MSE (mean over rows*C): A [B][rows][C] dtype dt vs T fp32 [rows][C] (T_bstride 0 = shared). */
 hfta_status hfta_loss_mse(int B, int64_t rows, int64_t C, hfta_dtype dt, hfta_in A,
                           const float* T, int64_t T_bstride, int64_t T_ld, float* loss,
@@ -259,6 +298,18 @@ hfta_status hfta_fused_adam(int B, int64_t P, float* param, const float* grad,
                             const float* lr, const float* beta1, const float* beta2,
                             const float* eps, const float* weight_decay, const int64_t* step,
                             void* param_bf16, int64_t bf16_bstride, hfta_stream stream);
+
+/*
+ * Standalone activations over [B][rows][cols] (dtype dt): act in {ReLU,
+ * LeakyReLU(alpha), Tanh, Sigmoid} (App. B rows P:L1298-1311).  Backward:
+ * dX = dY * act'(.), where act' is evaluated from the INPUT X for ReLU /
+ * LeakyReLU and from the OUTPUT Y for Tanh (1 - y^2) / Sigmoid (y(1-y));
+ * XY is that tensor.
+ */
+hfta_status hfta_act_fwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_act act, float alpha,
+                         hfta_in X, hfta_out Y, hfta_stream stream);
+hfta_status hfta_act_bwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_act act, float alpha,
+                         hfta_in XY, hfta_in dY, hfta_out dX, hfta_stream stream);
 
 /* ------------------------------------------------------------- utility -- */
 /* Y = X1 + X2 elementwise over [B][rows][cols] (dtype dt): sums the two

@@ -269,10 +269,12 @@ def disc_bwd(P, dout, out, cache, need_wgrad=True, need_dx=False):
     return dh, G
 
 
-def dcgan_iteration(PG, PD, SG, SD, optG, optD, real, z, t, hp_b):
+def dcgan_iteration(PG, PD, SG, SD, optG, optD, real, z, t, hp_b, hpD_b=None):
     """One DCGAN iteration for ONE model, in the order of the cited example
     (reading R4): D(real) backward, D(fake.detach) backward accumulating,
-    Adam(D), D'(fake) backward into G, Adam(G)."""
+    Adam(D), D'(fake) backward into G, Adam(G).  hpD_b (default hp_b) lets a
+    test give D its own hyper-parameters (e.g. lr 0)."""
+    hpD_b = hp_b if hpD_b is None else hpD_b
     newSD1, newSD2, newSD3, newSG = {}, {}, {}, {}
     N = real.shape[0]
     ones, zeros = np.ones(N), np.zeros(N)
@@ -284,7 +286,7 @@ def dcgan_iteration(PG, PD, SG, SD, optG, optD, real, z, t, hp_b):
     errD_fake, dout = Lr.bce_mean(out_f, zeros)
     _, GD_f = disc_bwd(PD, dout, out_f, cf)
     GD = {k: GD_r[k] + GD_f[k] for k in GD_r}
-    PD2, optD2 = adam_model(PD, GD, optD, t, hp_b)
+    PD2, optD2 = adam_model(PD, GD, optD, t, hpD_b)
     out_g, cg2 = disc_fwd(PD2, newSD2, newSD3, fake)
     errG, dout = Lr.bce_mean(out_g, ones)
     dfake, _ = disc_bwd(PD2, dout, out_g, cg2, need_wgrad=False, need_dx=True)

@@ -1,0 +1,284 @@
+// conv.cu -- fused Conv2d / ConvTranspose2d for B models (K3/K4/K5).
+// App. B rows Conv2d and ConvT2d: B same-shape
+// (de)convolutions fused into one, here as model-batched GEMMs on the
+// tcgen05 engine plus two gather kernels, NHWC per model:
+//   im2col : col[(n,sy,sx)][(ky,kx,c)] = img[n, sy*s-p+ky, sx*s-p+kx, c]   (0 outside)
+//   col2im : img[n, by, bx, c] = sum_{ky,kx: sy=(by+p-ky)/s integral, in range} col[(n,sy,sx)][(ky,kx,c)]
+// ("big" grid = conv input / convT output, "small" grid = conv output / convT input).
+//   conv  fwd : Y  = im2col(X) W^T                       W [Co][(ky,kx,ci)]
+//   conv  bwd : dW = dY^T im2col(X) ; dX = col2im(dY W)
+//   convT fwd : Y  = col2im(X Wt^T)                      Wt [(ky,kx,co)][ci]
+//   convT bwd : dWt = im2col(dY)^T X ; dX = im2col(dY) Wt
+// col2im is a deterministic gather (no atomics).  The col matrix lives in the
+// caller's workspace.  (An implicit-GEMM producer that gathers the im2col rows
+// straight into the swizzled smem ring is the next step.)
+#include "gemm.cuh"
+
+namespace hfta {
+hfta_status colsum_impl(int B, int64_t rows, int64_t C, int64_t group, hfta_dtype dt, hfta_in X, float* S,
+                        int64_t S_bstride, int accumulate, void* ws, size_t ws_bytes, cudaStream_t s);
+size_t colsum_ws(int B, int64_t rows, int64_t C, int64_t group);
+
+namespace {
+
+struct Geo2 {
+  int64_t N, Hb, Wb, Hs, Ws, C;   // big / small grids, channels of the gathered image
+  int kh, kw, stride, pad;
+};
+
+template <typename T, int VEC>
+__global__ void k_im2col(Geo2 g, const T* __restrict__ img, int64_t ibs, T* __restrict__ col, int64_t cbs) {
+  const int b = blockIdx.y;
+  const int64_t cv = g.C / VEC;
+  const int64_t K = (int64_t)g.kh * g.kw * g.C;
+  const int64_t total = g.N * g.Hs * g.Ws * g.kh * g.kw * cv;
+  const T* I = img + (int64_t)b * ibs;
+  T* O = col + (int64_t)b * cbs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int64_t c = (t % cv) * VEC; t /= cv;
+    const int kx = (int)(t % g.kw); t /= g.kw;
+    const int ky = (int)(t % g.kh); t /= g.kh;
+    const int64_t m = t;                         // (n, sy, sx)
+    const int64_t sx = t % g.Ws; t /= g.Ws;
+    const int64_t sy = t % g.Hs;
+    const int64_t n = t / g.Hs;
+    const int64_t by = sy * g.stride - g.pad + ky, bx = sx * g.stride - g.pad + kx;
+    float v[VEC];
+    if (by >= 0 && by < g.Hb && bx >= 0 && bx < g.Wb) {
+      ld_vec<T, VEC>(I + ((n * g.Hb + by) * g.Wb + bx) * g.C + c, v);
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) v[q] = 0.f;
+    }
+    st_vec<T, VEC>(O + m * K + ((int64_t)ky * g.kw + kx) * g.C + c, v);
+  }
+}
+
+template <typename T, int VEC>
+__global__ void k_col2im(Geo2 g, const T* __restrict__ col, int64_t cbs, int64_t cld, T* __restrict__ img,
+                         int64_t ibs) {
+  const int b = blockIdx.y;
+  const int64_t cv = g.C / VEC;
+  const int64_t total = g.N * g.Hb * g.Wb * cv;
+  const T* Cm = col + (int64_t)b * cbs;
+  T* O = img + (int64_t)b * ibs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int64_t c = (t % cv) * VEC; t /= cv;
+    const int64_t bx = t % g.Wb; t /= g.Wb;
+    const int64_t by = t % g.Hb;
+    const int64_t n = t / g.Hb;
+    float acc[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) acc[q] = 0.f;
+    for (int ky = 0; ky < g.kh; ++ky) {               // fixed order: deterministic
+      const int64_t ty = by + g.pad - ky;
+      if (ty < 0 || ty % g.stride) continue;
+      const int64_t sy = ty / g.stride;
+      if (sy >= g.Hs) continue;
+      for (int kx = 0; kx < g.kw; ++kx) {
+        const int64_t tx = bx + g.pad - kx;
+        if (tx < 0 || tx % g.stride) continue;
+        const int64_t sx = tx / g.stride;
+        if (sx >= g.Ws) continue;
+        float v[VEC];
+        ld_vec<T, VEC>(Cm + ((n * g.Hs + sy) * g.Ws + sx) * cld + ((int64_t)ky * g.kw + kx) * g.C + c, v);
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) acc[q] += v[q];
+      }
+    }
+    st_vec<T, VEC>(O + ((n * g.Hb + by) * g.Wb + bx) * g.C + c, acc);
+  }
+}
+
+template <typename T>
+void launch_im2col(const Geo2& g, const void* img, int64_t ibs, void* col, int64_t cbs, int B, cudaStream_t s) {
+  const int vec = (g.C % (16 / (int)sizeof(T)) == 0) ? 16 / (int)sizeof(T) : 1;
+  int64_t total = g.N * g.Hs * g.Ws * g.kh * g.kw * (g.C / vec);
+  dim3 grid((unsigned)std::min<int64_t>(cdiv(total, 256), 8192), B);
+  if (vec == 8) k_im2col<T, 8><<<grid, 256, 0, s>>>(g, (const T*)img, ibs, (T*)col, cbs);
+  else if (vec == 4) k_im2col<T, 4><<<grid, 256, 0, s>>>(g, (const T*)img, ibs, (T*)col, cbs);
+  else k_im2col<T, 1><<<grid, 256, 0, s>>>(g, (const T*)img, ibs, (T*)col, cbs);
+}
+
+template <typename T>
+void launch_col2im(const Geo2& g, const void* col, int64_t cbs, int64_t cld, void* img, int64_t ibs, int B,
+                   cudaStream_t s) {
+  const int vec = (g.C % (16 / (int)sizeof(T)) == 0 && cld % (16 / (int)sizeof(T)) == 0) ? 16 / (int)sizeof(T) : 1;
+  int64_t total = g.N * g.Hb * g.Wb * (g.C / vec);
+  dim3 grid((unsigned)std::min<int64_t>(cdiv(total, 256), 8192), B);
+  if (vec == 8) k_col2im<T, 8><<<grid, 256, 0, s>>>(g, (const T*)col, cbs, cld, (T*)img, ibs);
+  else if (vec == 4) k_col2im<T, 4><<<grid, 256, 0, s>>>(g, (const T*)col, cbs, cld, (T*)img, ibs);
+  else k_col2im<T, 1><<<grid, 256, 0, s>>>(g, (const T*)col, cbs, cld, (T*)img, ibs);
+}
+
+void im2col(hfta_dtype dt, const Geo2& g, const void* img, int64_t ibs, void* col, int64_t cbs, int B,
+            cudaStream_t s) {
+  if (dt == HFTA_F32) launch_im2col<float>(g, img, ibs, col, cbs, B, s);
+  else launch_im2col<__nv_bfloat16>(g, img, ibs, col, cbs, B, s);
+  count_launches(1);
+}
+void col2im(hfta_dtype dt, const Geo2& g, const void* col, int64_t cbs, int64_t cld, void* img, int64_t ibs, int B,
+            cudaStream_t s) {
+  if (dt == HFTA_F32) launch_col2im<float>(g, col, cbs, cld, img, ibs, B, s);
+  else launch_col2im<__nv_bfloat16>(g, col, cbs, cld, img, ibs, B, s);
+  count_launches(1);
+}
+
+hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void* ws = nullptr, size_t wsb = 0) {
+  if (skinny_fwd_ok(p) || skinny_dgrad_ok(p) || skinny_wgrad_ok(p)) return gemm_skinny(p, dt, ws, wsb, s);
+  if (gemm_tc_supported(p, dt, out_f32)) return gemm_tc(p, dt, out_f32, s);
+  return gemm_simt(p, dt, out_f32, s);
+}
+
+// Shape bookkeeping of one (de)convolution.
+struct Shape {
+  Geo2 g;             // gather geometry
+  int64_t Ho, Wo;     // output spatial dims
+  int64_t Ms;         // small-grid rows N*Hs*Ws (GEMM M)
+  int64_t Kc;         // im2col width kh*kw*C (C = gathered image channels)
+  int64_t Ci, Co;
+  bool transposed;
+};
+
+hfta_status make_shape(const hfta_conv_desc* d, Shape* sh) {
+  HFTA_REQUIRE(d, HFTA_ERR_INVALID_VALUE, "conv: desc is NULL");
+  HFTA_REQUIRE(d->N >= 1 && d->H >= 1 && d->W >= 1 && d->C_in >= 1 && d->C_out >= 1 && d->kh >= 1 && d->kw >= 1 &&
+                   d->stride >= 1 && d->pad >= 0,
+               HFTA_ERR_SHAPE, "conv: bad descriptor (N %d H %d W %d Ci %d Co %d k %dx%d s %d p %d)", d->N, d->H, d->W,
+               d->C_in, d->C_out, d->kh, d->kw, d->stride, d->pad);
+  Shape s{};
+  s.Ci = d->C_in; s.Co = d->C_out; s.transposed = d->transposed != 0;
+  if (!s.transposed) {
+    s.Ho = ((int64_t)d->H + 2 * d->pad - d->kh) / d->stride + 1;
+    s.Wo = ((int64_t)d->W + 2 * d->pad - d->kw) / d->stride + 1;
+    HFTA_REQUIRE(s.Ho >= 1 && s.Wo >= 1, HFTA_ERR_SHAPE, "conv: empty output");
+    s.g = Geo2{d->N, d->H, d->W, s.Ho, s.Wo, d->C_in, d->kh, d->kw, d->stride, d->pad};
+    s.Kc = (int64_t)d->kh * d->kw * d->C_in;
+  } else {
+    s.Ho = ((int64_t)d->H - 1) * d->stride - 2 * d->pad + d->kh;
+    s.Wo = ((int64_t)d->W - 1) * d->stride - 2 * d->pad + d->kw;
+    HFTA_REQUIRE(s.Ho >= 1 && s.Wo >= 1, HFTA_ERR_SHAPE, "convT: empty output");
+    s.g = Geo2{d->N, s.Ho, s.Wo, d->H, d->W, d->C_out, d->kh, d->kw, d->stride, d->pad};
+    s.Kc = (int64_t)d->kh * d->kw * d->C_out;
+  }
+  s.Ms = (int64_t)d->N * s.g.Hs * s.g.Ws;
+  *sh = s;
+  return HFTA_OK;
+}
+
+}  // namespace
+}  // namespace hfta
+
+using namespace hfta;
+
+extern "C" {
+
+size_t hfta_fused_conv_workspace(int B, const hfta_conv_desc* d, hfta_dtype dt) {
+  Shape sh;
+  if (B < 1 || make_shape(d, &sh) != HFTA_OK) return 0;
+  const size_t col = align_up((size_t)B * sh.Ms * sh.Kc * dsize(dt), 256);
+  // weight-gradient GEMM (split-K partials) of either orientation
+  const int64_t M = sh.Ms;
+  size_t lin = std::max(hfta_fused_linear_bwd_workspace(B, M, sh.Co, sh.Kc, dt),
+                        hfta_fused_linear_bwd_workspace(B, M, sh.Kc, sh.Ci, dt));
+  return col + align_up(lin, 256);
+}
+
+hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* d, hfta_dtype dt, hfta_in X, hfta_in W, hfta_out Y,
+                                void* ws, size_t ws_bytes, hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  Shape sh;
+  if (hfta_status st = make_shape(d, &sh)) return st;
+  HFTA_REQUIRE(X.ptr && W.ptr && Y.ptr && (Y.bstride > 0 || B == 1), HFTA_ERR_INVALID_VALUE, "conv_fwd: bad args");
+  size_t need = hfta_fused_conv_workspace(B, d, dt);
+  HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "conv_fwd: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  char* col = reinterpret_cast<char*>(ws);
+  GemmP p{};
+  p.B = B; p.splits = 1;
+  if (!sh.transposed) {
+    // Y[(n,oy,ox)][co] = im2col(X) W^T ; a shared input image gives a shared col (bstride 0)
+    const int nb = X.bstride == 0 ? 1 : B;
+    im2col(dt, sh.g, X.ptr, X.bstride, col, sh.Ms * sh.Kc, nb, s);
+    p.M = sh.Ms; p.N = sh.Co; p.K = sh.Kc;
+    p.A = col; p.a_bs = X.bstride == 0 ? 0 : sh.Ms * sh.Kc; p.a_ld = sh.Kc; p.a_kmajor = 1;
+    p.Bm = W.ptr; p.b_bs = W.bstride; p.b_ld = W.ld; p.b_kmajor = 1;
+    p.C = Y.ptr; p.c_bs = Y.bstride; p.c_ld = Y.ld;
+    p.k_chunk = sh.Kc;
+    if (hfta_status st = run_gemm(p, dt, false, s)) return st;
+  } else {
+    // col[(n,iy,ix)][(ky,kx,co)] = X Wt^T, then Y = col2im(col)
+    p.M = sh.Ms; p.N = sh.Kc; p.K = sh.Ci;
+    p.A = X.ptr; p.a_bs = X.bstride; p.a_ld = X.ld; p.a_kmajor = 1;
+    p.Bm = W.ptr; p.b_bs = W.bstride; p.b_ld = W.ld; p.b_kmajor = 1;
+    p.C = col; p.c_bs = sh.Ms * sh.Kc; p.c_ld = sh.Kc;
+    p.k_chunk = sh.Ci;
+    if (hfta_status st = run_gemm(p, dt, false, s)) return st;
+    col2im(dt, sh.g, col, sh.Ms * sh.Kc, sh.Kc, Y.ptr, Y.bstride, B, s);
+  }
+  return post_launch(s, "hfta_fused_conv_fwd");
+}
+
+hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* d, hfta_dtype dt, hfta_in dY, hfta_in X, hfta_in W,
+                                hfta_out dX, float* dW, int64_t dW_bstride, int accumulate, void* ws, size_t ws_bytes,
+                                hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  Shape sh;
+  if (hfta_status st = make_shape(d, &sh)) return st;
+  HFTA_REQUIRE(dY.ptr && X.ptr && W.ptr, HFTA_ERR_INVALID_VALUE, "conv_bwd: dY, X, W are required");
+  size_t need = hfta_fused_conv_workspace(B, d, dt);
+  HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "conv_bwd: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  char* col = reinterpret_cast<char*>(ws);
+  const size_t colb = align_up((size_t)B * sh.Ms * sh.Kc * dsize(dt), 256);
+  char* lws = col + colb;
+  const size_t lwsb = ws_bytes - colb;
+  if (!sh.transposed) {
+    const int nb = X.bstride == 0 ? 1 : B;
+    const int64_t cbs = X.bstride == 0 ? 0 : sh.Ms * sh.Kc;
+    if (dW) {
+      im2col(dt, sh.g, X.ptr, X.bstride, col, sh.Ms * sh.Kc, nb, s);
+      // dW[co][k] = sum_m dY[m][co] col[m][k]
+      if (hfta_status st = hfta_fused_linear_bwd(B, sh.Ms, sh.Co, sh.Kc, dt, dY, hfta_in{col, cbs, sh.Kc},
+                                                 W, hfta_out{nullptr, 0, 1}, dW, dW_bstride, sh.Kc, nullptr, 0,
+                                                 accumulate, lws, lwsb, stream))
+        return st;
+    }
+    if (dX.ptr) {
+      // dcol[m][k] = sum_co dY[m][co] W[co][k] ; dX = col2im(dcol)
+      GemmP p{};
+      p.B = B; p.splits = 1; p.M = sh.Ms; p.N = sh.Kc; p.K = sh.Co; p.k_chunk = sh.Co;
+      p.A = dY.ptr; p.a_bs = dY.bstride; p.a_ld = dY.ld; p.a_kmajor = 1;
+      p.Bm = W.ptr; p.b_bs = W.bstride; p.b_ld = W.ld; p.b_kmajor = 0;
+      p.C = col; p.c_bs = sh.Ms * sh.Kc; p.c_ld = sh.Kc;
+      if (hfta_status st = run_gemm(p, dt, false, s)) return st;
+      col2im(dt, sh.g, col, sh.Ms * sh.Kc, sh.Kc, dX.ptr, dX.bstride, B, s);
+    }
+  } else {
+    // dcol = im2col(dY) over the input grid
+    im2col(dt, sh.g, dY.ptr, dY.bstride, col, sh.Ms * sh.Kc, B, s);
+    const hfta_in dcol{col, sh.Ms * sh.Kc, sh.Kc};
+    if (dW) {
+      // dWt[(ky,kx,co)][ci] = sum_m dcol[m][(ky,kx,co)] X[m][ci]
+      if (hfta_status st = hfta_fused_linear_bwd(B, sh.Ms, sh.Kc, sh.Ci, dt, dcol, X, W, hfta_out{nullptr, 0, 1}, dW,
+                                                 dW_bstride, sh.Ci, nullptr, 0, accumulate, lws, lwsb, stream))
+        return st;
+    }
+    if (dX.ptr) {
+      // dX[m][ci] = sum_k dcol[m][k] Wt[k][ci]
+      GemmP p{};
+      p.B = B; p.splits = 1; p.M = sh.Ms; p.N = sh.Ci; p.K = sh.Kc; p.k_chunk = sh.Kc;
+      p.A = col; p.a_bs = sh.Ms * sh.Kc; p.a_ld = sh.Kc; p.a_kmajor = 1;
+      p.Bm = W.ptr; p.b_bs = W.bstride; p.b_ld = W.ld; p.b_kmajor = 0;
+      p.C = dX.ptr; p.c_bs = dX.bstride; p.c_ld = dX.ld;
+      if (hfta_status st = run_gemm(p, dt, false, s)) return st;
+    }
+  }
+  return post_launch(s, "hfta_fused_conv_bwd");
+}
+
+}  // extern "C"

@@ -147,6 +147,30 @@ ColsumGeo colsum_geo(int B, int64_t rows, int64_t C, int64_t group) {
   return g;
 }
 
+template <typename T>
+__global__ void k_act(int64_t rows, int64_t cols, int act, float alpha, const T* __restrict__ X, int64_t xbs,
+                      int64_t xld, const T* __restrict__ D, int64_t dbs, int64_t dld, T* __restrict__ Y, int64_t ybs,
+                      int64_t yld, int bwd) {
+  const int b = blockIdx.y;
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const float x = ldf(X + b * xbs + r * xld + c);
+    float out;
+    if (!bwd) {
+      if (act == HFTA_ACT_TANH) out = tanhf(x);
+      else if (act == HFTA_ACT_SIGMOID) out = 1.f / (1.f + expf(-x));
+      else out = act_fwd(x, act, alpha);
+    } else {
+      const float d = ldf(D + b * dbs + r * dld + c);
+      if (act == HFTA_ACT_TANH) out = d * (1.f - x * x);            // x is the output y
+      else if (act == HFTA_ACT_SIGMOID) out = d * x * (1.f - x);
+      else out = d * act_grad(x, act, alpha);
+    }
+    stf(Y + b * ybs + r * yld + c, out);
+  }
+}
+
 }  // namespace
 
 size_t colsum_ws(int B, int64_t rows, int64_t C, int64_t group) {
@@ -254,6 +278,36 @@ hfta_status hfta_dropout_fwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, h
 hfta_status hfta_dropout_bwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in dY, hfta_out dX,
                              uint64_t seed, int64_t step, int32_t layer, float p, hfta_stream stream) {
   return dropout_common(B, rows, cols, dt, dY, dX, seed, step, layer, p, stream, "hfta_dropout_bwd");
+}
+
+static hfta_status act_common(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_act act, float alpha,
+                              hfta_in X, hfta_in D, hfta_out Y, int bwd, hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(rows >= 1 && cols >= 1 && X.ptr && Y.ptr && (!bwd || D.ptr), HFTA_ERR_INVALID_VALUE, "act: bad args");
+  HFTA_REQUIRE((int)act >= 1 && (int)act <= 4, HFTA_ERR_UNSUPPORTED, "act: activation %d", (int)act);
+  HFTA_REQUIRE(X.ld >= cols && Y.ld >= cols && (Y.bstride > 0 || B == 1), HFTA_ERR_SHAPE, "act: strides");
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid((unsigned)std::min<int64_t>(cdiv(rows * cols, 256), 4096), B);
+  if (dt == HFTA_F32)
+    k_act<float><<<grid, 256, 0, s>>>(rows, cols, (int)act, alpha, (const float*)X.ptr, X.bstride, X.ld,
+                                     (const float*)D.ptr, D.bstride, D.ld, (float*)Y.ptr, Y.bstride, Y.ld, bwd);
+  else
+    k_act<__nv_bfloat16><<<grid, 256, 0, s>>>(rows, cols, (int)act, alpha, (const __nv_bfloat16*)X.ptr, X.bstride,
+                                             X.ld, (const __nv_bfloat16*)D.ptr, D.bstride, D.ld,
+                                             (__nv_bfloat16*)Y.ptr, Y.bstride, Y.ld, bwd);
+  count_launches(1);
+  return post_launch(s, bwd ? "hfta_act_bwd" : "hfta_act_fwd");
+}
+
+hfta_status hfta_act_fwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_act act, float alpha, hfta_in X,
+                         hfta_out Y, hfta_stream stream) {
+  return act_common(B, rows, cols, dt, act, alpha, X, hfta_in{nullptr, 0, 1}, Y, 0, stream);
+}
+
+hfta_status hfta_act_bwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_act act, float alpha, hfta_in XY,
+                         hfta_in dY, hfta_out dX, hfta_stream stream) {
+  return act_common(B, rows, cols, dt, act, alpha, XY, dY, dX, 1, stream);
 }
 
 size_t hfta_colsum_workspace(int B, int64_t rows, int64_t C, int64_t group) { return colsum_ws(B, rows, C, group); }

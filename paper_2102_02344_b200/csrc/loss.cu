@@ -77,6 +77,36 @@ __global__ void __launch_bounds__(NT) k_mse(int64_t rows, int64_t C, const T* __
   if (threadIdx.x == 0) part[(int64_t)b * gridDim.x + blockIdx.x] = red[0];
 }
 
+template <typename T>
+__global__ void __launch_bounds__(NT) k_bce(int64_t rows, const T* __restrict__ Z, int64_t zbs, int64_t zld,
+                                            float y, T* __restrict__ dZ, int64_t dbs, int64_t dld,
+                                            float* __restrict__ part) {
+  __shared__ float red[NT];
+  const int b = blockIdx.y;
+  float s = 0.f;
+  const int64_t r0 = (int64_t)blockIdx.x * ROWS_PER_BLOCK;
+  const int64_t r1 = min(rows, r0 + ROWS_PER_BLOCK);
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += NT) {
+    const float z = ldf(Z + (int64_t)b * zbs + r * zld);
+    // log p = -softplus(-z), log(1-p) = -softplus(z), both clamped at -100 (BCELoss)
+    const float sp_pos = fmaxf(z, 0.f) + log1pf(expf(-fabsf(z)));     // softplus(z)
+    const float lp = fmaxf(-(sp_pos - z), -100.f);
+    const float l1p = fmaxf(-sp_pos, -100.f);
+    s -= y * lp + (1.f - y) * l1p;
+    const float p = 1.f / (1.f + expf(-z));
+    const float pq = p * (1.f - p);
+    const float g = (p - y) / fmaxf(pq, 1e-12f) * pq;                  // BCELoss backward x sigmoid'
+    stf(dZ + (int64_t)b * dbs + r * dld, g / (float)rows);
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = NT / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[(int64_t)b * gridDim.x + blockIdx.x] = red[0];
+}
+
 // loss[b] = scale * sum_chunks part (fixed order, fp64); mean over b.
 __global__ void k_loss_fin(int B, int chunks, const float* __restrict__ part, double scale, float* __restrict__ loss,
                            float* __restrict__ mean_loss) {
@@ -129,6 +159,29 @@ hfta_status hfta_loss_nll(int B, int64_t rows, int64_t K, hfta_dtype dt, hfta_in
   k_loss_fin<<<1, 32, 0, s>>>(B, chunks, part, 1.0 / (double)rows, loss, mean_loss);
   count_launches(2);
   return post_launch(s, "hfta_loss_nll");
+}
+
+hfta_status hfta_loss_bce_logits(int B, int64_t rows, hfta_dtype dt, hfta_in Z, float target, float* loss,
+                                 float* mean_loss, hfta_out dZ, void* ws, size_t ws_bytes, hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(rows >= 1 && Z.ptr && loss && dZ.ptr, HFTA_ERR_INVALID_VALUE, "loss_bce: bad args");
+  HFTA_REQUIRE(dZ.bstride > 0 || B == 1, HFTA_ERR_SHAPE, "loss_bce: dZ stride");
+  size_t need = hfta_loss_workspace(B, rows);
+  HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "loss_bce: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  int chunks = (int)cdiv(rows, ROWS_PER_BLOCK);
+  float* part = reinterpret_cast<float*>(ws);
+  dim3 grid(chunks, B);
+  if (dt == HFTA_F32)
+    k_bce<float><<<grid, NT, 0, s>>>(rows, (const float*)Z.ptr, Z.bstride, Z.ld, target, (float*)dZ.ptr, dZ.bstride,
+                                    dZ.ld, part);
+  else
+    k_bce<__nv_bfloat16><<<grid, NT, 0, s>>>(rows, (const __nv_bfloat16*)Z.ptr, Z.bstride, Z.ld, target,
+                                            (__nv_bfloat16*)dZ.ptr, dZ.bstride, dZ.ld, part);
+  k_loss_fin<<<1, 32, 0, s>>>(B, chunks, part, 1.0 / (double)rows, loss, mean_loss);
+  count_launches(2);
+  return post_launch(s, "hfta_loss_bce_logits");
 }
 
 hfta_status hfta_loss_mse(int B, int64_t rows, int64_t C, hfta_dtype dt, hfta_in A, const float* T, int64_t T_bstride,

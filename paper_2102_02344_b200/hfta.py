@@ -20,7 +20,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 HFTA_F32, HFTA_BF16 = 0, 1
-ACT_NONE, ACT_RELU, ACT_LEAKY_RELU = 0, 1, 2
+ACT_NONE, ACT_RELU, ACT_LEAKY_RELU, ACT_TANH, ACT_SIGMOID = 0, 1, 2, 3, 4
 STATUS = {0: "HFTA_OK", 1: "HFTA_ERR_INVALID_VALUE", 2: "HFTA_ERR_SHAPE", 3: "HFTA_ERR_ALIGNMENT",
           4: "HFTA_ERR_UNSUPPORTED", 5: "HFTA_ERR_ARCH", 6: "HFTA_ERR_WORKSPACE", 7: "HFTA_ERR_CUDA",
           8: "HFTA_ERR_NOT_INITIALIZED"}
@@ -38,6 +38,10 @@ class hfta_in(C.Structure):
 
 class hfta_out(C.Structure):
     _fields_ = [("ptr", C.c_void_p), ("bstride", C.c_int64), ("ld", C.c_int64)]
+
+
+class hfta_conv_desc(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("N", "H", "W", "C_in", "C_out", "kh", "kw", "stride", "pad", "transposed")]
 
 
 i32, i64, u64, f32, vp, sz = C.c_int, C.c_int64, C.c_uint64, C.c_float, C.c_void_p, C.c_size_t
@@ -74,6 +78,13 @@ _SIGS = {
     "hfta_cast_f32_bf16": (i32, [i64, vp, vp, vp]),
     "hfta_step_increment": (i32, [vp, vp]),
     "hfta_add": (i32, [i32, i64, i64, i32, hfta_in, hfta_in, hfta_out, vp]),
+    "hfta_fused_conv_workspace": (sz, [i32, C.POINTER(hfta_conv_desc), i32]),
+    "hfta_fused_conv_fwd": (i32, [i32, C.POINTER(hfta_conv_desc), i32, hfta_in, hfta_in, hfta_out, vp, sz, vp]),
+    "hfta_fused_conv_bwd": (i32, [i32, C.POINTER(hfta_conv_desc), i32, hfta_in, hfta_in, hfta_in, hfta_out, vp, i64,
+                                  i32, vp, sz, vp]),
+    "hfta_loss_bce_logits": (i32, [i32, i64, i32, hfta_in, f32, vp, vp, hfta_out, vp, sz, vp]),
+    "hfta_act_fwd": (i32, [i32, i64, i64, i32, i32, f32, hfta_in, hfta_out, vp]),
+    "hfta_act_bwd": (i32, [i32, i64, i64, i32, i32, f32, hfta_in, hfta_in, hfta_out, vp]),
 }
 
 EXPORTED = sorted(_SIGS)
