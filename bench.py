@@ -28,7 +28,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "fused models x samples/sec per B200 (PointNet-cls, HFTA fused training step)"
+METRIC = "fused models x samples/sec per B200 (HFTA fused training step)"
 UNIT = "model-samples/s"
 
 
@@ -132,24 +132,78 @@ def run_reference(args, rank):
 # -------------------------------------------------------------------- ours --
 
 def build_net(args, rank, world, device):
+    """Workload adapter: .net, .step() (inputs resident), .e2e_step() (pinned host
+    inputs copied in, per-model losses read back), .loss (device [B]), h2d/d2h bytes."""
     import torch
     import synth
-    from paper_2102_02344_b200.pointnet import FusedPointNet
     from paper_2102_02344_b200 import shard
-    B, k = args.B, args.k
-    specs = [(n, s) for n, s, _ in synth.param_specs("pointnet_cls", k)]
+    B = args.B
     base, _ = shard.model_range(rank, world, B * world)   # weak scaling: B models per GPU
-    Ps = [synth.init_params("pointnet_cls", 1000 + base + b, k) for b in range(B)] if not args.fast_init else None
-    if Ps is None:   # identical initial parameters, different hyper-parameters (still B independent models)
-        P0 = synth.init_params("pointnet_cls", 1000, k)
-        Ps = [P0] * B
-    hp = shard.slice_hparams(synth.hparams_pointnet(7, B * world), base, base + B)
-    net = FusedPointNet(B, specs, Ps, hp, task="cls", dtype=args.dtype, N=args.N, L=args.L, k=k, device=device)
-    x, y = synth.points_cls(0, N=args.N, L=args.L, k=k)
-    xd = torch.tensor(x.reshape(-1, 3), dtype=torch.float32, device=device)
-    yd = torch.tensor(y, dtype=torch.int32, device=device)
-    net.set_batch(xd, yd)
-    return net, x, y
+
+    class W:
+        pass
+    w = W()
+    if args.workload in ("pointnet_cls", "pointnet_seg"):
+        from paper_2102_02344_b200.pointnet import FusedPointNet
+        task = args.workload.split("_")[1]
+        k = args.k if task == "cls" else args.k_seg
+        arch = "pointnet_" + task
+        specs = [(n, s) for n, s, _ in synth.param_specs(arch, k)]
+        if args.fast_init:   # identical initial parameters, different hyper-parameters
+            P0 = synth.init_params(arch, 1000, k)
+            Ps = [P0] * B
+        else:
+            Ps = [synth.init_params(arch, 1000 + base + b, k) for b in range(B)]
+        hp = shard.slice_hparams(synth.hparams_pointnet(7, B * world), base, base + B)
+        net = FusedPointNet(B, specs, Ps, hp, task=task, dtype=args.dtype, N=args.N, L=args.L, k=k, device=device)
+        x, y = (synth.points_cls if task == "cls" else synth.points_seg)(0, N=args.N, L=args.L, k=k)
+        net.set_batch(torch.tensor(x.reshape(-1, 3), dtype=torch.float32, device=device),
+                      torch.tensor(y, dtype=torch.int32, device=device))
+        xh = torch.from_numpy(x.reshape(-1, 3).astype(np.float32)).pin_memory()
+        yh = torch.from_numpy(y.astype(np.int32).reshape(-1)).pin_memory()
+        lh = torch.empty(B, dtype=torch.float32).pin_memory()
+        xd, yd = torch.empty_like(xh, device=device), torch.empty_like(yh, device=device)
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            yd.copy_(yh, non_blocking=True)
+            lh.copy_(net.step(xd, yd), non_blocking=True)
+        w.net, w.step, w.e2e_step, w.loss = net, net.step, e2e_step, lambda: net.loss
+        w.samples = args.N
+        w.h2d, w.d2h = xh.numel() * 4 + yh.numel() * 4, B * 4
+        w.x_host, w.y_host = x, y
+        w.desc = "%s (BJ configs[%d]), N=%d clouds x %d points, k=%d" % (arch, 1 if task == "cls" else 2, args.N,
+                                                                       args.L, k)
+    else:
+        from paper_2102_02344_b200.dcgan import FusedDCGAN
+        Nd = args.N_dcgan
+        gs = [(n, s) for n, s, _ in synth.param_specs("dcgan_g")]
+        ds = [(n, s) for n, s, _ in synth.param_specs("dcgan_d")]
+        PG = [synth.init_params("dcgan_g", 1000 + base + b) for b in range(B)]
+        PD = [synth.init_params("dcgan_d", 2000 + base + b) for b in range(B)]
+        hp = shard.slice_hparams(synth.hparams_dcgan(3, B * world), base, base + B)
+        net = FusedDCGAN(B, gs, ds, PG, PD, hp, N=Nd, dtype=args.dtype, device=device)
+        real = synth.images(0, N=Nd).transpose(0, 2, 3, 1).astype(np.float32)
+        z = np.stack([synth.noise(0, base + b, 1, N=Nd) for b in range(B)]).astype(np.float32)
+        rh, zh = torch.from_numpy(np.ascontiguousarray(real)).pin_memory(), torch.from_numpy(z).pin_memory()
+        rd, zd = torch.empty_like(rh, device=device), torch.empty_like(zh, device=device)
+        rd.copy_(rh)
+        zd.copy_(zh)
+        net.set_inputs(rd, zd)
+        lh = torch.empty(3, B, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            rd.copy_(rh, non_blocking=True)
+            zd.copy_(zh, non_blocking=True)
+            net.set_inputs(rd, zd)
+            e = net.step()
+            for i in range(3):
+                lh[i].copy_(e[i], non_blocking=True)
+        w.net, w.step, w.e2e_step, w.loss = net, net.step, e2e_step, lambda: net.errG
+        w.samples = Nd
+        w.h2d, w.d2h = rh.numel() * 4 + zh.numel() * 4, 3 * B * 4
+        w.desc = "dcgan 64x64 G+D (BJ configs[3]), N=%d images, per-model noise" % Nd
+    return w
 
 
 def run_ours(args, rank, world, local_rank):
@@ -161,22 +215,24 @@ def run_ours(args, rank, world, local_rank):
     H.hfta_init(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
-    net, x_host_np, y_host_np = build_net(args, rank, world, device)
+    wl = build_net(args, rank, world, device)
+    net = wl.net
     stream = torch.cuda.current_stream()
-    B, N = args.B, args.N
+    B, N = args.B, wl.samples
     from paper_2102_02344_b200 import shard
 
     def gather_losses():
         if world > 1:
-            shard.gather_losses(net.loss, B * world, world)      # C1: per-model losses only
+            shard.gather_losses(wl.loss(), B * world, world)      # C1: per-model losses only
 
     # ---- device-timed region (inputs resident in HBM) ----
     for _ in range(args.warmup):
-        net.step()
+        wl.step()
         gather_losses()
     torch.cuda.synchronize()
-    probe_name = args.probe
-    net.probe_arm(probe_name)
+    probe_name = args.probe if args.workload == "pointnet_cls" else None
+    if probe_name:
+        net.probe_arm(probe_name)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -186,7 +242,7 @@ def run_ours(args, rank, world, local_rank):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        net.step()
+        wl.step()
         gather_losses()
     e1.record(stream)
     torch.cuda.synchronize()
@@ -195,7 +251,7 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
-    probe_ms = net.probe_collect()
+    probe_ms = net.probe_collect() if probe_name else []
     t = torch.tensor([ms], device=device, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -204,22 +260,14 @@ def run_ours(args, rank, world, local_rank):
     mem_peak = torch.cuda.max_memory_allocated(device)
 
     # ---- end to end through the public API: pinned host inputs in, losses out ----
-    xh = torch.from_numpy(x_host_np.reshape(-1, 3).astype(np.float32)).pin_memory()
-    yh = torch.from_numpy(y_host_np.astype(np.int32)).pin_memory()
-    lh = torch.empty(B, dtype=torch.float32).pin_memory()
-    xd = torch.empty_like(xh, device=device)
-    yd = torch.empty_like(yh, device=device)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     for _ in range(args.steps):
-        xd.copy_(xh, non_blocking=True)
-        yd.copy_(yh, non_blocking=True)
-        loss = net.step(xd, yd)
+        wl.e2e_step()
         gather_losses()
-        lh.copy_(loss, non_blocking=True)
         stream.synchronize()            # the host reads the step's per-model losses
     f1.record(stream)
     torch.cuda.synchronize()
@@ -233,19 +281,17 @@ def run_ours(args, rank, world, local_rank):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if args.dtype == "bf16" else "f32",
-                "data": "synthetic (seeded point clouds, random-init models)",
-                "config": {"workload": "pointnet_cls cfg2 (BJ configs[1])", "B_per_gpu": B, "batch": N,
-                           "points": args.L, "classes": args.k, "precision": args.dtype,
+                "data": "synthetic (seeded inputs, random-init models of the named architecture)",
+                "config": {"workload": wl.desc, "B_per_gpu": B, "batch": N, "precision": args.dtype,
                            "l2": "working set >> L2 (activations ~%.0f GB/step)" % (mem_peak / 1e9),
                            "parallelism": "model-array sharding, %d x %d models" % (world, B)},
                 "gpu_launches": int(launches),
                 "peak_mem_gb": mem_peak / 1e9,
                 "clocks": clk,
-                "e2e": {"value": e2e_value, "unit": UNIT,
-                        "h2d_bytes_per_step": int(xh.numel() * 4 + yh.numel() * 4),
-                        "d2h_bytes_per_step": int(B * 4)}}
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(wl.h2d),
+                        "d2h_bytes_per_step": int(wl.d2h)}}
         path = "tc" if args.dtype == "bf16" else "simt"
-        roof = net.probe_roofline(probe_name, probe_ms, pk, path=path)
+        roof = net.probe_roofline(probe_name, probe_ms, pk, path=path) if probe_name else None
         try:   # DRAM traffic of the probed kernel from the committed ncu --set full capture
             tr = json.load(open(os.path.join(ROOT, "profiles", "traffic_r01.json")))[probe_name]
             if path == "tc":
@@ -254,7 +300,21 @@ def run_ours(args, rank, world, local_rank):
         except Exception:
             pass
         line["roofline"] = roof
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_serial and args.workload == "pointnet_cls":
+            import serial_baselines as SB
+            xd = torch.tensor(wl.x_host, dtype=torch.float32, device=device)
+            yd = torch.tensor(wl.y_host, dtype=torch.int64, device=device)
+            v_pt = SB.serial_pytorch(xd, yd, n_models=4, steps=3, warmup=2, dtype=args.dtype, device=device)
+            import copy
+            a1 = copy.copy(args)
+            a1.B = 1
+            w1 = build_net(a1, 0, 1, device)
+            v_b1 = SB.serial_libhfta_b1(w1.net, steps=3, warmup=2)
+            del w1
+            line["serial"] = {"pytorch_eager_per_model_loop": v_pt, "libhfta_B1_loop": v_b1, "unit": UNIT,
+                              "speedup_vs_pytorch_serial": value / v_pt, "speedup_vs_libhfta_B1": value / v_b1,
+                              "note": "same-precision (%s) serial loops on this GPU, 4 / 1 models timed" % args.dtype}
+        if world == 1 and not args.no_cpu_baseline and args.workload == "pointnet_cls":
             v, dt = cpu_oracle_sample(args.ref_samples, args.L, args.k)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
                                     "sample": "1 model x %d samples of cfg2, one fp64 step (%.1f s)" %
@@ -275,10 +335,14 @@ def main():
     ap.add_argument("--N", type=int, default=32)
     ap.add_argument("--L", type=int, default=2500)
     ap.add_argument("--k", type=int, default=40)
+    ap.add_argument("--k-seg", type=int, default=50)
+    ap.add_argument("--N-dcgan", type=int, default=128)
     ap.add_argument("--probe", default="feat.c3:fwd")
     ap.add_argument("--ref-samples", type=int, default=8)
     ap.add_argument("--fast-init", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-serial", action="store_true")
+    ap.add_argument("--workload", default="pointnet_cls", choices=["pointnet_cls", "pointnet_seg", "dcgan"])
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

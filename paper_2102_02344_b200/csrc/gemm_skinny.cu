@@ -139,23 +139,153 @@ __global__ void k_skinny_wgrad_fin(GemmP p, int chunks, const float* __restrict_
 
 int pow2ceil(int64_t x) { int q = 1; while (q < x) q <<= 1; return q; }
 
+// ---- tiny output width / tiny reduction (e.g. DCGAN D c5: Conv 512->1 on 4x4) ----
+// fwd, N <= 8 outputs per row, long K: one warp per row, lanes split K.
+template <typename T>
+__global__ void k_gemv_fwd(GemmP p) {
+  const int b = blockIdx.y;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  const T* A = reinterpret_cast<const T*>(p.A) + (int64_t)b * p.a_bs;
+  const T* Bw = reinterpret_cast<const T*>(p.Bm) + (int64_t)b * p.b_bs;
+  T* C = reinterpret_cast<T*>(p.C) + (int64_t)b * p.c_bs;
+  for (int64_t m = warp; m < p.M; m += nwarps) {
+    float acc[KMAX];
+#pragma unroll
+    for (int n = 0; n < KMAX; ++n) acc[n] = 0.f;
+    for (int64_t k = lane; k < p.K; k += 32) {
+      const float a = ldf(A + m * p.a_ld + k);
+#pragma unroll
+      for (int n = 0; n < KMAX; ++n)
+        if (n < p.N) acc[n] = fmaf(a, ldf(Bw + n * p.b_ld + k), acc[n]);
+    }
+#pragma unroll
+    for (int n = 0; n < KMAX; ++n) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[n] += __shfl_xor_sync(0xffffffffu, acc[n], o);
+    }
+    if (lane == 0)
+      for (int n = 0; n < p.N; ++n) {
+        float v = acc[n];
+        if (p.bias) v += p.bias[(int64_t)b * p.bias_bs + (p.bias_div > 0 ? (m / p.bias_div) * p.bias_ld : 0) + n];
+        stf(C + m * p.c_ld + n, v);
+      }
+  }
+}
+
+// any majorness, reduction K <= 8: C[m][n] = sum_k A(m,k) B(n,k); thread per output element.
+template <typename T, bool AK, bool BKM>
+__global__ void k_smallk(GemmP p) {
+  const int b = blockIdx.y;
+  const T* A = reinterpret_cast<const T*>(p.A) + (int64_t)b * p.a_bs;
+  const T* Bw = reinterpret_cast<const T*>(p.Bm) + (int64_t)b * p.b_bs;
+  T* C = reinterpret_cast<T*>(p.C) + (int64_t)b * p.c_bs;
+  const int64_t tot = p.M * p.N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / p.N, n = i % p.N;
+    float acc = 0.f;
+    for (int64_t k = 0; k < p.K; ++k)
+      acc = fmaf(ldf(AK ? A + m * p.a_ld + k : A + k * p.a_ld + m), ldf(BKM ? Bw + n * p.b_ld + k : Bw + k * p.b_ld + n),
+                 acc);
+    if (p.bias) acc += p.bias[(int64_t)b * p.bias_bs + (p.bias_div > 0 ? (m / p.bias_div) * p.bias_ld : 0) + n];
+    stf(C + m * p.c_ld + n, acc);
+  }
+}
+
+// wgrad with M <= 8 output rows (both operands MN-major), fp32 out, fixed-order chunks:
+// part[chunk][b][m][n] = sum_{r in chunk} A[r][m] * X[r][n]; thread = column n.
+template <typename T>
+__global__ void k_smallm_wgrad(GemmP p, int64_t rows_per_chunk, float* __restrict__ part) {
+  const int b = blockIdx.z, chunk = blockIdx.y;
+  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (n >= p.N) return;
+  const T* A = reinterpret_cast<const T*>(p.A) + (int64_t)b * p.a_bs;
+  const T* X = reinterpret_cast<const T*>(p.Bm) + (int64_t)b * p.b_bs;
+  float acc[KMAX];
+#pragma unroll
+  for (int m = 0; m < KMAX; ++m) acc[m] = 0.f;
+  const int64_t r0 = chunk * rows_per_chunk, r1 = min(p.K, r0 + rows_per_chunk);
+  for (int64_t r = r0; r < r1; ++r) {
+    const float x = ldf(X + r * p.b_ld + n);
+#pragma unroll
+    for (int m = 0; m < KMAX; ++m)
+      if (m < p.M) acc[m] = fmaf(ldf(A + r * p.a_ld + m), x, acc[m]);
+  }
+  for (int m = 0; m < p.M; ++m) part[(((int64_t)chunk * p.B + b) * p.M + m) * p.N + n] = acc[m];
+}
+
+__global__ void k_smallm_fin(GemmP p, int chunks, const float* __restrict__ part) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)p.B * p.M * p.N) return;
+  const int64_t b = i / (p.M * p.N), rem = i % (p.M * p.N), m = rem / p.N, n = rem % p.N;
+  double s = 0.0;
+  for (int c = 0; c < chunks; ++c) s += part[(((int64_t)c * p.B + b) * p.M + m) * p.N + n];
+  float* o = reinterpret_cast<float*>(p.C) + b * p.c_bs + m * p.c_ld + n;
+  *o = p.accumulate ? *o + (float)s : (float)s;
+}
+
 }  // namespace
 
-// ---- dispatch predicates (called from linear.cu) ----
-bool skinny_fwd_ok(const GemmP& p) { return p.a_kmajor && p.b_kmajor && p.K <= KMAX && p.N <= 512 && p.splits == 1; }
+// ---- dispatch predicates (called from linear.cu / conv.cu) ----
+static bool gemv_fwd_ok(const GemmP& p) { return p.a_kmajor && p.b_kmajor && p.N <= KMAX && p.splits == 1; }
+static bool smallk_ok(const GemmP& p) { return p.a_kmajor && p.K <= KMAX && p.splits == 1 && !p.accumulate; }
+static bool smallm_wgrad_ok(const GemmP& p) { return !p.a_kmajor && !p.b_kmajor && p.M <= KMAX; }
+bool skinny_fwd_ok_base(const GemmP& p) { return p.a_kmajor && p.b_kmajor && p.K <= KMAX && p.N <= 512 && p.splits == 1; }
 bool skinny_dgrad_ok(const GemmP& p) {
   return p.a_kmajor && !p.b_kmajor && p.N <= KMAX && p.K <= 1024 && p.splits == 1 && p.K % 8 == 0 && p.a_ld % 8 == 0;
 }
-bool skinny_wgrad_ok(const GemmP& p) { return !p.a_kmajor && !p.b_kmajor && p.N <= 3 && p.M <= 128; }
+bool skinny_wgrad_ok_base(const GemmP& p) { return !p.a_kmajor && !p.b_kmajor && p.N <= 3 && p.M <= 128; }
+bool skinny_fwd_ok(const GemmP& p) { return skinny_fwd_ok_base(p) || gemv_fwd_ok(p) || smallk_ok(p); }
+bool skinny_wgrad_ok(const GemmP& p) { return skinny_wgrad_ok_base(p) || smallm_wgrad_ok(p); }
+
+static int64_t smallm_chunks(int B, int64_t rows, int64_t N) {
+  const int64_t colblocks = cdiv(N, 256);
+  return std::max<int64_t>(1, std::min<int64_t>(cdiv(4 * 148, (int64_t)B * colblocks), cdiv(rows, 64)));
+}
 
 size_t skinny_wgrad_ws(int B, int64_t rows, int64_t N, int64_t Ko) {
   int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(4 * 148, B), cdiv(rows, 2048)));
-  return (size_t)chunks * B * N * Ko * sizeof(float);
+  size_t a = (size_t)chunks * B * N * Ko * sizeof(float);
+  size_t c = N <= KMAX ? (size_t)smallm_chunks(B, rows, Ko) * B * N * Ko * sizeof(float) : 0;   // dW is [N][Ko]
+  return std::max(a, c);
 }
 
 hfta_status gemm_skinny(const GemmP& p, hfta_dtype dt, void* ws, size_t ws_bytes, cudaStream_t s) {
   const bool bf = dt == HFTA_BF16;
-  if (skinny_fwd_ok(p)) {
+  if (!skinny_fwd_ok_base(p) && !skinny_dgrad_ok(p) && !skinny_wgrad_ok_base(p)) {
+    if (smallm_wgrad_ok(p)) {
+      const int64_t chunks = smallm_chunks(p.B, p.K, p.N);
+      const int64_t rpc = cdiv(p.K, chunks);
+      const size_t need = (size_t)chunks * p.B * p.M * p.N * sizeof(float);
+      HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "small-M wgrad: workspace %zu < %zu", ws_bytes, need);
+      float* part = reinterpret_cast<float*>(ws);
+      dim3 grid((unsigned)cdiv(p.N, 256), (unsigned)chunks, p.B);
+      if (bf) k_smallm_wgrad<__nv_bfloat16><<<grid, 256, 0, s>>>(p, rpc, part);
+      else k_smallm_wgrad<float><<<grid, 256, 0, s>>>(p, rpc, part);
+      k_smallm_fin<<<(unsigned)cdiv((int64_t)p.B * p.M * p.N, 256), 256, 0, s>>>(p, (int)chunks, part);
+      count_launches(2);
+      return post_launch(s, "gemm_smallm_wgrad");
+    }
+    if (gemv_fwd_ok(p)) {
+      dim3 grid((unsigned)std::min<int64_t>(cdiv(p.M, 8), 1024), p.B);
+      if (bf) k_gemv_fwd<__nv_bfloat16><<<grid, 256, 0, s>>>(p);
+      else k_gemv_fwd<float><<<grid, 256, 0, s>>>(p);
+      count_launches(1);
+      return post_launch(s, "gemm_gemv_fwd");
+    }
+    if (smallk_ok(p)) {
+      dim3 grid((unsigned)std::min<int64_t>(cdiv(p.M * p.N, 256), 8192), p.B);
+#define SK(AK, BK) (bf ? (void)k_smallk<__nv_bfloat16, AK, BK><<<grid, 256, 0, s>>>(p) : (void)k_smallk<float, AK, BK><<<grid, 256, 0, s>>>(p))
+      if (p.a_kmajor && p.b_kmajor) SK(true, true);
+      else if (p.a_kmajor) SK(true, false);
+      else if (p.b_kmajor) SK(false, true);
+      else SK(false, false);
+#undef SK
+      count_launches(1);
+      return post_launch(s, "gemm_smallk");
+    }
+  }
+  if (skinny_fwd_ok_base(p)) {
     int vec = bf ? 8 : 4;
     if (p.N % vec || p.c_ld % vec || !aligned16(p.C) || p.c_bs % vec) vec = 1;
     int tpr = std::min(32, pow2ceil(cdiv(p.N, vec)));
@@ -186,7 +316,7 @@ hfta_status gemm_skinny(const GemmP& p, hfta_dtype dt, void* ws, size_t ws_bytes
     count_launches(1);
     return post_launch(s, "gemm_skinny_dgrad");
   }
-  if (skinny_wgrad_ok(p)) {
+  if (skinny_wgrad_ok_base(p)) {
     const int64_t rows = p.K, N = p.M, Ko = p.N;
     int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(4 * 148, p.B), cdiv(rows, 2048)));
     size_t need = (size_t)chunks * p.B * N * Ko * sizeof(float);

@@ -8,8 +8,9 @@ D(real) backward, D(fake.detach) backward accumulating into D's gradients,
 Adam(D), D'(fake) backward into G (D's parameter gradients not needed),
 Adam(G).  Layouts are NHWC per model; conv weights live in the arena permuted
 to [Co][kh][kw][Ci] (Conv2d) / [kh][kw][Co][Ci] (ConvT2d); the generator input
-channel count is padded 100 -> 104 (16-B rows; pad values and their weights
-are zero and stay zero).
+channel count is padded 100 -> 104 and the image channels 3 -> 8 (16-B bf16
+rows for TMA and 128-bit gathers); pad values and their weights are zero,
+their gradients are exactly zero, so they stay zero.
 """
 import numpy as np
 import torch
@@ -17,9 +18,18 @@ import torch
 from . import hfta as H
 from .fused import ParamArena, HyperVectors, Workspace, fused_adam
 
-NZ, NZP = 100, 104
+NZ, NZP = 100, 104        # generator input channels, padded to 16-B bf16 rows
+NC, NCP = 3, 8            # image channels (G output / D input), padded to 16-B bf16 rows
 G_LAYERS = [(1, 0), (2, 1), (2, 1), (2, 1), (2, 1)]      # (stride, pad) of t1..t5 (ConvT, k=4)
 D_LAYERS = [(2, 1), (2, 1), (2, 1), (2, 1), (1, 0)]      # c1..c5 (Conv, k=4)
+
+
+def _pad(a, axis, n):
+    if a.shape[axis] == n:
+        return a
+    w = [(0, 0)] * a.ndim
+    w[axis] = (0, n - a.shape[axis])
+    return np.pad(a, w)
 
 
 def _to_gpu(name, a):
@@ -27,10 +37,15 @@ def _to_gpu(name, a):
     if name.startswith("t") and name.endswith(".W"):     # ConvT [Ci][Co][kh][kw] -> [kh][kw][Co][Ci]
         g = np.transpose(a, (2, 3, 1, 0))
         if a.shape[0] == NZ:
-            g = np.concatenate([g, np.zeros(g.shape[:3] + (NZP - NZ,))], axis=3)
+            g = _pad(g, 3, NZP)
+        if a.shape[1] == NC:
+            g = _pad(g, 2, NCP)
         return g
     if name.startswith("c") and name.endswith(".W"):     # Conv [Co][Ci][kh][kw] -> [Co][kh][kw][Ci]
-        return np.transpose(a, (0, 2, 3, 1))
+        g = np.transpose(a, (0, 2, 3, 1))
+        if a.shape[1] == NC:
+            g = _pad(g, 3, NCP)
+        return g
     return a
 
 
@@ -38,8 +53,12 @@ def _to_torch(name, g):
     if name.startswith("t") and name.endswith(".W"):
         if g.shape[3] == NZP:
             g = g[..., :NZ]
+        if name == "t5.W":
+            g = g[:, :, :NC, :]
         return np.transpose(g, (3, 2, 0, 1))
     if name.startswith("c") and name.endswith(".W"):
+        if name == "c1.W":
+            g = g[..., :NC]
         return np.transpose(g, (0, 3, 1, 2))
     return g
 
@@ -90,27 +109,27 @@ class FusedDCGAN:
         B, N, dev = self.B, self.N, self.device
         a = lambda *shape: torch.empty((B,) + shape, dtype=self.tdt, device=dev)
         # generator: 1 -> 4 -> 8 -> 16 -> 32 -> 64, channels 104(100) -> 512 -> 256 -> 128 -> 64 -> 3
-        gch = [NZP, 512, 256, 128, 64, 3]
+        gch = [NZP, 512, 256, 128, 64, NCP]
         gsz = [1, 4, 8, 16, 32, 64]
         self.gdesc = [self._desc(gsz[i], gch[i], gch[i + 1], *G_LAYERS[i], True) for i in range(5)]
         self.gch, self.gsz = gch, gsz
         self.z = a(N, NZP)
         self.gy = [a(N, gsz[i + 1], gsz[i + 1], gch[i + 1]) for i in range(5)]     # pre-BN / pre-tanh
         self.gh = [a(N, gsz[i + 1], gsz[i + 1], gch[i + 1]) for i in range(4)]     # post BN+ReLU
-        self.fake = a(N, 64, 64, 3)
+        self.fake = a(N, 64, 64, NCP)
         self.dgy = [a(N, gsz[i + 1], gsz[i + 1], gch[i + 1]) for i in range(5)]
         self.dgh = [a(N, gsz[i + 1], gsz[i + 1], gch[i + 1]) for i in range(4)]
         # discriminator: 64 -> 32 -> 16 -> 8 -> 4 -> 1, channels 3 -> 64 -> 128 -> 256 -> 512 -> 1
-        dch = [3, 64, 128, 256, 512, 1]
+        dch = [NCP, 64, 128, 256, 512, 1]
         dsz = [64, 32, 16, 8, 4, 1]
         self.ddesc = [self._desc(dsz[i], dch[i], dch[i + 1], *D_LAYERS[i], False) for i in range(5)]
         self.dch, self.dsz = dch, dsz
-        self.real = torch.empty(N, 64, 64, 3, dtype=self.tdt, device=dev)
+        self.real = torch.zeros(N, 64, 64, NCP, dtype=self.tdt, device=dev)
         self.dy = [a(N, dsz[i + 1], dsz[i + 1], dch[i + 1]) for i in range(5)]     # pre-activation
         self.dh = [a(N, dsz[i + 1], dsz[i + 1], dch[i + 1]) for i in range(4)]     # post activation
         self.ddy = [a(N, dsz[i + 1], dsz[i + 1], dch[i + 1]) for i in range(5)]
         self.ddh = [a(N, dsz[i + 1], dsz[i + 1], dch[i + 1]) for i in range(4)]
-        self.dimg = a(N, 64, 64, 3)
+        self.dimg = a(N, 64, 64, NCP)
         f32 = lambda *shape: torch.zeros(shape, dtype=torch.float32, device=dev)
         self.errD_real, self.errD_fake, self.errG = f32(B), f32(B), f32(B)
         self.mean = f32(1)
@@ -228,7 +247,7 @@ class FusedDCGAN:
 
     def set_inputs(self, real_nhwc, z_bn):
         """real: device fp32 [N,64,64,3] (shared); z: device fp32 [B,N,100] (per model)."""
-        self.real.copy_(real_nhwc.to(self.tdt))
+        self.real[..., :NC].copy_(real_nhwc.to(self.tdt))
         self.z.zero_()
         self.z[:, :, :NZ].copy_(z_bn.to(self.tdt))
 
@@ -236,7 +255,7 @@ class FusedDCGAN:
         """One DCGAN iteration for all B models; returns (errD_real, errD_fake, errG) [B] each."""
         s = H.stream_ptr(stream)
         self.t += 1
-        real = H.tin(self.real, 0, 3)                     # shared by all models
+        real = H.tin(self.real, 0, NCP)                   # shared by all models
         # (1) D on real, label 1
         self._D_forward(real, s)
         self._bce(1.0, self.errD_real, s)

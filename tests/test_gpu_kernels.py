@@ -49,7 +49,9 @@ def s():
 # (M, N, K): K < 16 / N < 16 / unaligned shapes take the SIMT kernel; the rest
 # (bf16) the tcgen05 kernel, including ragged M / N tails and MN-major operands.
 SHAPES = [(300, 64, 3), (1000, 128, 64), (257, 200, 136), (32, 9, 256), (37, 40, 256), (130, 3, 64),
-          (2000, 1024, 128), (1500, 128, 1024), (640, 256, 512), (999, 64, 128)]
+          (2000, 1024, 128), (1500, 128, 1024), (640, 256, 512), (999, 64, 128),
+          (2000, 48, 64), (1000, 64, 48), (700, 16, 80),       # ragged MN-major extents (TMA OOB boxes)
+          (300, 1, 2048), (200, 2, 5), (130, 7, 300)]          # tiny N: GEMV fwd, small-K dgrad, small-M wgrad
 
 
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
