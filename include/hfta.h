@@ -311,6 +311,36 @@ hfta_status hfta_act_fwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_
 hfta_status hfta_act_bwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_act act, float alpha,
                          hfta_in XY, hfta_in dY, hfta_out dX, hfta_stream stream);
 
+/*
+ * Fused SGD (BJ north_star "fused Adam/SGD step"; P:L910-911 tunes momentum),
+ * PyTorch-1.6 form: d = grad + wd[b]*p; with momentum[b] != 0:
+ * buf = (t == 1) ? d : momentum[b]*buf + (1-dampening[b])*d,
+ * d = nesterov ? d + momentum[b]*buf : buf;  p -= lr[b]*d.
+ * momentum_buf [b*bstride + j] (may be NULL if every momentum is 0);
+ * hyper-parameters device fp32 [B]; step device int64 (shared t).
+ */
+hfta_status hfta_fused_sgd(int B, int64_t P, float* param, const float* grad, float* momentum_buf,
+                           int64_t bstride, const float* lr, const float* momentum,
+                           const float* dampening, const float* weight_decay, int nesterov,
+                           const int64_t* step, void* param_bf16, int64_t bf16_bstride,
+                           hfta_stream stream);
+/*
+ * Fused Adadelta ("Adam and Adadelta"), PyTorch-1.6 form:
+ * g = grad + wd[b]*p; sq = rho*sq + (1-rho) g^2; delta = sqrt(acc+eps)/sqrt(sq+eps)*g;
+ * acc = rho*acc + (1-rho) delta^2; p -= lr[b]*delta.
+ */
+hfta_status hfta_fused_adadelta(int B, int64_t P, float* param, const float* grad, float* square_avg,
+                                float* acc_delta, int64_t bstride, const float* lr, const float* rho,
+                                const float* eps, const float* weight_decay, void* param_bf16,
+                                int64_t bf16_bstride, hfta_stream stream);
+/*
+ * Fused StepLR (per-model "Factor/Period of Learning Rate Decay",
+ * P:L978-979): lr[b] = lr0[b] * gamma[b]^floor(epoch / period[b]),
+ * device arrays [B]; a graph-capturable per-epoch update of the lr vector.
+ */
+hfta_status hfta_steplr(int B, const float* lr0, const float* gamma, const int32_t* period, int64_t epoch,
+                        float* lr, hfta_stream stream);
+
 /* ------------------------------------------------------------- utility -- */
 /* Y = X1 + X2 elementwise over [B][rows][cols] (dtype dt): sums the two
  * gradient paths into a shared activation (PointNet-seg's point feature). */

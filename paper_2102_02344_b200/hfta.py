@@ -85,6 +85,9 @@ _SIGS = {
     "hfta_loss_bce_logits": (i32, [i32, i64, i32, hfta_in, f32, vp, vp, hfta_out, vp, sz, vp]),
     "hfta_act_fwd": (i32, [i32, i64, i64, i32, i32, f32, hfta_in, hfta_out, vp]),
     "hfta_act_bwd": (i32, [i32, i64, i64, i32, i32, f32, hfta_in, hfta_in, hfta_out, vp]),
+    "hfta_fused_sgd": (i32, [i32, i64, vp, vp, vp, i64, vp, vp, vp, vp, i32, vp, vp, i64, vp]),
+    "hfta_fused_adadelta": (i32, [i32, i64, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, i64, vp]),
+    "hfta_steplr": (i32, [i32, vp, vp, vp, i64, vp, vp]),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -306,3 +306,60 @@ def test_fused_adam(P, shadow):
         assert_close(host(vd[b]), vs[b], 1e-6, "v")
         if shadow:
             assert np.array_equal(host(sh[b]), rounded(host(pd[b]), torch.bfloat16))
+
+
+@pytest.mark.parametrize("nesterov", [0, 1])
+def test_fused_sgd(nesterov):
+    from oracle.optim import sgd_step
+    B, P, T = 3, 1000, 4
+    hp = dict(lr=np.float32([1e-2, 5e-2, 1e-3]), mom=np.float32([0.9, 0.5, 0.0]), damp=np.float32([0.0, 0.1, 0.0]),
+              wd=np.float32([0.0, 1e-2, 3e-2]))
+    p0 = R.standard_normal((B, P)).astype(np.float32)
+    pd, gd, bd = dev(p0), torch.empty(B, P, device=DEV), torch.zeros(B, P, device=DEV)
+    hv = {k: dev(v) for k, v in hp.items()}
+    step = torch.zeros(1, dtype=torch.int64, device=DEV)
+    ps = [p0[b].astype(np.float64) for b in range(B)]
+    bufs = [None] * B
+    for t in range(1, T + 1):
+        g = R.standard_normal((B, P)).astype(np.float32)
+        gd.copy_(torch.from_numpy(g))
+        H.hfta_step_increment(H.ptr(step), s())
+        H.hfta_fused_sgd(B, P, H.ptr(pd), H.ptr(gd), H.ptr(bd), P, H.ptr(hv["lr"]), H.ptr(hv["mom"]),
+                         H.ptr(hv["damp"]), H.ptr(hv["wd"]), nesterov, H.ptr(step), None, P, s())
+        for b in range(B):
+            ps[b], bufs[b] = sgd_step(ps[b], g[b].astype(np.float64), bufs[b], t, *(float(hp[k][b]) for k in
+                                      ("lr", "mom", "damp", "wd")), bool(nesterov))
+    torch.cuda.synchronize()
+    for b in range(B):
+        assert_close(host(pd[b]), ps[b], 1e-6, "sgd param")
+
+
+def test_fused_adadelta_and_steplr():
+    from oracle.optim import adadelta_step, steplr
+    B, P, T = 2, 999, 3
+    hp = dict(lr=np.float32([1.0, 0.5]), rho=np.float32([0.9, 0.5]), eps=np.float32([1e-6, 1e-4]),
+              wd=np.float32([0.0, 1e-2]))
+    p0 = R.standard_normal((B, P)).astype(np.float32)
+    pd, gd = dev(p0), torch.empty(B, P, device=DEV)
+    sq, ac = torch.zeros(B, P, device=DEV), torch.zeros(B, P, device=DEV)
+    hv = {k: dev(v) for k, v in hp.items()}
+    st = [(p0[b].astype(np.float64), np.zeros(P), np.zeros(P)) for b in range(B)]
+    for t in range(T):
+        g = R.standard_normal((B, P)).astype(np.float32)
+        gd.copy_(torch.from_numpy(g))
+        H.hfta_fused_adadelta(B, P, H.ptr(pd), H.ptr(gd), H.ptr(sq), H.ptr(ac), P, H.ptr(hv["lr"]), H.ptr(hv["rho"]),
+                              H.ptr(hv["eps"]), H.ptr(hv["wd"]), None, P, s())
+        for b in range(B):
+            st[b] = adadelta_step(st[b][0], g[b].astype(np.float64), st[b][1], st[b][2],
+                                  *(float(hp[k][b]) for k in ("lr", "rho", "eps", "wd")))
+    torch.cuda.synchronize()
+    for b in range(B):
+        assert_close(host(pd[b]), st[b][0], 1e-6, "adadelta param")
+    lr0, gam, per = dev([0.1, 1e-3]), dev([0.5, 0.9]), torch.tensor([10, 3], dtype=torch.int32, device=DEV)
+    out = torch.empty(2, device=DEV)
+    for ep in (0, 9, 10, 25):
+        H.hfta_steplr(2, H.ptr(lr0), H.ptr(gam), H.ptr(per), ep, H.ptr(out), s())
+        torch.cuda.synchronize()
+        ref = [steplr(float(np.float32(0.1)), float(np.float32(0.5)), 10, ep),
+               steplr(float(np.float32(1e-3)), float(np.float32(0.9)), 3, ep)]
+        assert np.allclose(host(out), ref, rtol=1e-6)

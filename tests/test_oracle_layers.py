@@ -327,3 +327,58 @@ def test_adam_vs_torch_one_group_per_model():
         opt.step()
     for b in range(B):
         assert np.allclose(ps[b], tp[b].detach().numpy(), rtol=1e-13, atol=1e-15)
+
+
+# ------------------------------------------------- SGD / Adadelta / StepLR ----
+
+def test_sgd_vs_torch_one_group_per_model():
+    from oracle.optim import sgd_step
+    B = 3
+    cfg = [dict(lr=1e-2, momentum=0.9, dampening=0.0, weight_decay=0.0, nesterov=False),
+           dict(lr=5e-2, momentum=0.5, dampening=0.1, weight_decay=1e-2, nesterov=False),
+           dict(lr=1e-3, momentum=0.8, dampening=0.0, weight_decay=3e-2, nesterov=True)]
+    p0 = R.standard_normal((B, 17))
+    grads = R.standard_normal((6, B, 17))
+    tp = [torch.nn.Parameter(t(p0[b].copy())) for b in range(B)]
+    opt = torch.optim.SGD([dict(params=[tp[b]], **cfg[b]) for b in range(B)])
+    ps, bufs = [p0[b].copy() for b in range(B)], [None] * B
+    for step in range(6):
+        for b in range(B):
+            tp[b].grad = t(grads[step, b])
+            c = cfg[b]
+            ps[b], bufs[b] = sgd_step(ps[b], grads[step, b], bufs[b], step + 1, c["lr"], c["momentum"],
+                                      c["dampening"], c["weight_decay"], c["nesterov"])
+        opt.step()
+    for b in range(B):
+        assert np.allclose(ps[b], tp[b].detach().numpy(), rtol=1e-13, atol=1e-15)
+
+
+def test_adadelta_vs_torch_and_first_step_closed_form():
+    from oracle.optim import adadelta_step
+    B = 2
+    cfg = [dict(lr=1.0, rho=0.9, eps=1e-6, weight_decay=0.0), dict(lr=0.5, rho=0.5, eps=1e-4, weight_decay=1e-2)]
+    p0 = R.standard_normal((B, 11))
+    grads = R.standard_normal((5, B, 11))
+    tp = [torch.nn.Parameter(t(p0[b].copy())) for b in range(B)]
+    opt = torch.optim.Adadelta([dict(params=[tp[b]], **cfg[b]) for b in range(B)])
+    st = [(p0[b].copy(), np.zeros(11), np.zeros(11)) for b in range(B)]
+    for step in range(5):
+        for b in range(B):
+            tp[b].grad = t(grads[step, b])
+            c = cfg[b]
+            st[b] = adadelta_step(st[b][0], grads[step, b], st[b][1], st[b][2], c["lr"], c["rho"], c["eps"],
+                                  c["weight_decay"])
+            if step == 0:   # |update| = lr g sqrt(eps) / sqrt(eps + (1-rho) g^2)
+                g = grads[0, b] + c["weight_decay"] * p0[b]
+                up = c["lr"] * g * np.sqrt(c["eps"]) / np.sqrt(c["eps"] + (1 - c["rho"]) * g * g)
+                assert np.allclose(p0[b] - st[b][0], up, rtol=1e-12)
+        opt.step()
+    for b in range(B):
+        assert np.allclose(st[b][0], tp[b].detach().numpy(), rtol=1e-12, atol=1e-15)
+
+
+def test_steplr_closed_form():
+    from oracle.optim import steplr
+    assert steplr(0.1, 0.5, 10, 25) == pytest.approx(0.025, rel=1e-15)
+    assert steplr(0.1, 1.0, 10, 25) == 0.1
+    assert [steplr(1.0, 0.5, 5, e) for e in (0, 4, 5, 9, 10)] == [1.0, 1.0, 0.5, 0.5, 0.25]
