@@ -4,6 +4,7 @@
 // B*C channels, i.e. statistics per (model b, channel c) (reading R13).
 // HBM-bound: 128-bit loads along C (4 fp32 / 8 bf16 per access), one CTA row
 // of threads per row slice, fixed-order partial merges in fp64.
+#include <cstdlib>
 #include <initializer_list>
 #include <tuple>
 
@@ -13,6 +14,7 @@ namespace hfta {
 namespace {
 
 constexpr int NT = 256;
+constexpr int UNRM = 1;     // max-over-points: rows in flight per thread (loop-carried max)
 constexpr int UNR = 1;      // rows per thread per iteration (UNR=4 measured slower: 76-150 regs cut occupancy)
 
 struct Geo {
@@ -22,18 +24,28 @@ struct Geo {
 
 int pow2ceil(int64_t x) { int p = 1; while (p < x) p <<= 1; return p; }
 
+int bn_blocks_per_sm() {   // row-chunk parallelism target (env HFTA_BN_BPS for tuning)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HFTA_BN_BPS");
+    v = e ? atoi(e) : 4;
+    if (v < 1) v = 4;
+  }
+  return v;
+}
+
 bool vec_ok(const void* p, int64_t ld, int64_t bs, int64_t C, int vec) {
   return p == nullptr || (aligned16(p) && ld % vec == 0 && bs % vec == 0 && C % vec == 0);
 }
 
-Geo make_geo(int B, int64_t R, int64_t C, int vec) {
+Geo make_geo(int B, int64_t R, int64_t C, int vec, int bps = 0) {
   Geo g;
   g.vec = vec;
   g.tpr = (int)std::min<int64_t>(32, pow2ceil(cdiv(C, vec)));
   g.cb = g.tpr * vec;
   g.rpb = NT / g.tpr;
   g.colgroups = (int)cdiv(C, g.cb);
-  int64_t target = 4 * (int64_t)std::max(num_sms(), 148);
+  int64_t target = (int64_t)(bps > 0 ? bps : bn_blocks_per_sm()) * std::max(num_sms(), 148);
   int64_t chunks = std::max<int64_t>(1, target / ((int64_t)g.colgroups * B));
   chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, cdiv(R, (int64_t)g.rpb * 8)));
   g.rows_per_chunk = cdiv(cdiv(R, chunks), g.rpb) * g.rpb;
@@ -155,13 +167,19 @@ __global__ void __launch_bounds__(NT) k_bn_apply(int64_t R, int64_t C, const T* 
 }
 
 // ------------------------------------------------------------- backward --
+// Per column the pre-activation is z = a*x + c (a = gamma*invstd, c = beta - mean*a);
+// act'(z) is a select on the sign of z.  The reduce pass accumulates sum dz and
+// sum dz*(x - mean) (shifted by the exact mean: no cancellation); the apply pass
+// evaluates dx = A*act'(z)*dy + Bx*x + Cc with three per-column constants.
+// Few live per-column values keep these kernels at <= 80 registers (3 CTAs/SM).
 template <typename T, int VEC>
-__global__ void __launch_bounds__(NT) k_bn_bwd_reduce(int64_t R, int64_t C, const T* __restrict__ dY, int64_t dbs,
-                                                      int64_t dld, const T* __restrict__ X, int64_t xbs, int64_t xld,
-                                                      const float* __restrict__ gamma, const float* __restrict__ beta,
-                                                      int64_t gbs, const float* __restrict__ smean,
-                                                      const float* __restrict__ sinv, int act, float alpha, Geo g,
-                                                      float* __restrict__ p1, float* __restrict__ p2) {
+__global__ void __launch_bounds__(NT, 3) k_bn_bwd_reduce(int64_t R, int64_t C, const T* __restrict__ dY, int64_t dbs,
+                                                         int64_t dld, const T* __restrict__ X, int64_t xbs, int64_t xld,
+                                                         const float* __restrict__ gamma,
+                                                         const float* __restrict__ beta, int64_t gbs,
+                                                         const float* __restrict__ smean,
+                                                         const float* __restrict__ sinv, int act, float alpha, Geo g,
+                                                         float* __restrict__ p1, float* __restrict__ p2) {
   __shared__ float s1[NT * VEC], s2[NT * VEC];
   const int b = blockIdx.z, chunk = blockIdx.y;
   const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
@@ -170,35 +188,27 @@ __global__ void __launch_bounds__(NT) k_bn_bwd_reduce(int64_t R, int64_t C, cons
 #pragma unroll
   for (int v = 0; v < VEC; ++v) { a1[v] = 0.f; a2[v] = 0.f; }
   if (c0 < C) {
-    float m[VEC], is[VEC], ga[VEC], be[VEC];
+    float ka[VEC], kc[VEC], m[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
-      m[v] = smean[(int64_t)b * C + c0 + v]; is[v] = sinv[(int64_t)b * C + c0 + v];
-      ga[v] = gamma[(int64_t)b * gbs + c0 + v]; be[v] = beta[(int64_t)b * gbs + c0 + v];
+      m[v] = smean[(int64_t)b * C + c0 + v];
+      ka[v] = gamma[(int64_t)b * gbs + c0 + v] * sinv[(int64_t)b * C + c0 + v];
+      kc[v] = beta[(int64_t)b * gbs + c0 + v] - m[v] * ka[v];
     }
     const T* Xb = X + (int64_t)b * xbs;
     const T* Db = dY + (int64_t)b * dbs;
     const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
     const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-    for (int64_t r = r0 + rl; r < r1; r += UNR * g.rpb) {
-      float x[UNR][VEC], d[UNR][VEC];
+    for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
+      float x[VEC], d[VEC];
+      ld_vec<T, VEC>(Xb + r * xld + c0, x);
+      ld_vec<T, VEC>(Db + r * dld + c0, d);
 #pragma unroll
-      for (int u = 0; u < UNR; ++u)
-        if (r + u * g.rpb < r1) {
-          ld_vec<T, VEC>(Xb + (r + u * g.rpb) * xld + c0, x[u]);
-          ld_vec<T, VEC>(Db + (r + u * g.rpb) * dld + c0, d[u]);
-        }
-#pragma unroll
-      for (int u = 0; u < UNR; ++u)
-        if (r + u * g.rpb < r1) {
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            float xh = (x[u][v] - m[v]) * is[v];
-            float dz = d[u][v] * act_grad(fmaf(ga[v], xh, be[v]), act, alpha);
-            a1[v] += dz;
-            a2[v] = fmaf(dz, xh, a2[v]);
-          }
-        }
+      for (int v = 0; v < VEC; ++v) {
+        const float dz = d[v] * act_grad(fmaf(ka[v], x[v], kc[v]), act, alpha);
+        a1[v] += dz;
+        a2[v] = fmaf(dz, x[v] - m[v], a2[v]);
+      }
     }
   }
 #pragma unroll
@@ -218,10 +228,13 @@ __global__ void __launch_bounds__(NT) k_bn_bwd_reduce(int64_t R, int64_t C, cons
   }
 }
 
-// dbeta, dgamma (fp32, written to the gradient arena) and the per-(b,c)
-// coefficients of the apply pass stored in ws: k1 = gamma*invstd, k2 = dbeta/R, k3 = dgamma/R.
+// dbeta = sum dz, dgamma = invstd * sum dz (x - mean) (fp32, written to the
+// gradient arena) and the apply-pass constants in ws (5 x [B][C]):
+// A = gamma*invstd, Bx = -A*invstd*dgamma/R, Cc = A*(mean*invstd*dgamma/R - dbeta/R),
+// ka = gamma*invstd, kc = beta - mean*ka.
 __global__ void k_bn_bwd_finalize(int B, int64_t R, int64_t C, int chunks, const float* __restrict__ p1,
-                                  const float* __restrict__ p2, const float* __restrict__ gamma, int64_t gbs,
+                                  const float* __restrict__ p2, const float* __restrict__ gamma,
+                                  const float* __restrict__ beta, int64_t gbs, const float* __restrict__ smean,
                                   const float* __restrict__ sinv, float* __restrict__ dgamma,
                                   float* __restrict__ dbeta, int accumulate, float* __restrict__ coef) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -232,66 +245,58 @@ __global__ void k_bn_bwd_finalize(int B, int64_t R, int64_t C, int chunks, const
     s1 += p1[(b * chunks + k) * C + c];
     s2 += p2[(b * chunks + k) * C + c];
   }
-  float db = (float)s1, dg = (float)s2;
-  if (dbeta) dbeta[b * gbs + c] = accumulate ? dbeta[b * gbs + c] + db : db;
-  if (dgamma) dgamma[b * gbs + c] = accumulate ? dgamma[b * gbs + c] + dg : dg;
-  coef[i] = gamma[b * gbs + c] * sinv[i];
-  coef[(int64_t)B * C + i] = (float)(s1 / (double)R);
-  coef[2 * (int64_t)B * C + i] = (float)(s2 / (double)R);
+  const double is = sinv[i], m = smean[i], ga = gamma[b * gbs + c], be = beta[b * gbs + c];
+  const double db = s1, dg = s2 * is;
+  if (dbeta) dbeta[b * gbs + c] = accumulate ? dbeta[b * gbs + c] + (float)db : (float)db;
+  if (dgamma) dgamma[b * gbs + c] = accumulate ? dgamma[b * gbs + c] + (float)dg : (float)dg;
+  const double A = ga * is, k2 = db / (double)R, k3 = dg / (double)R;
+  const int64_t BC = (int64_t)B * C;
+  coef[i] = (float)A;
+  coef[BC + i] = (float)(-A * k3 * is);
+  coef[2 * BC + i] = (float)(A * (k3 * m * is - k2));
+  coef[3 * BC + i] = (float)A;
+  coef[4 * BC + i] = (float)(be - m * A);
 }
 
 template <typename T, int VEC>
-__global__ void __launch_bounds__(NT) k_bn_bwd_apply(int B, int64_t R, int64_t C, const T* __restrict__ dY,
-                                                     int64_t dbs, int64_t dld, const T* __restrict__ X, int64_t xbs,
-                                                     int64_t xld, T* __restrict__ dX, int64_t obs, int64_t old,
-                                                     const float* __restrict__ gamma, const float* __restrict__ beta,
-                                                     int64_t gbs, const float* __restrict__ smean,
-                                                     const float* __restrict__ sinv, int act, float alpha, Geo g,
-                                                     const float* __restrict__ coef) {
+__global__ void __launch_bounds__(NT, 3) k_bn_bwd_apply(int B, int64_t R, int64_t C, const T* __restrict__ dY,
+                                                        int64_t dbs, int64_t dld, const T* __restrict__ X, int64_t xbs,
+                                                        int64_t xld, T* __restrict__ dX, int64_t obs, int64_t old,
+                                                        int act, float alpha, Geo g, const float* __restrict__ coef) {
   const int b = blockIdx.z, chunk = blockIdx.y;
   const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
   const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
   if (c0 >= C) return;
   const int64_t BC = (int64_t)B * C;
-  float m[VEC], is[VEC], ga[VEC], be[VEC], k1[VEC], k2[VEC], k3[VEC];
+  float kA[VEC], kB[VEC], kC[VEC], ka[VEC], kc[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
     int64_t i = (int64_t)b * C + c0 + v;
-    m[v] = smean[i]; is[v] = sinv[i];
-    ga[v] = gamma[(int64_t)b * gbs + c0 + v]; be[v] = beta[(int64_t)b * gbs + c0 + v];
-    k1[v] = coef[i]; k2[v] = coef[BC + i]; k3[v] = coef[2 * BC + i];
+    kA[v] = coef[i]; kB[v] = coef[BC + i]; kC[v] = coef[2 * BC + i];
+    ka[v] = coef[3 * BC + i]; kc[v] = coef[4 * BC + i];
   }
   const T* Xb = X + (int64_t)b * xbs;
   const T* Db = dY + (int64_t)b * dbs;
   T* Ob = dX + (int64_t)b * obs;
   const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
   const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-  for (int64_t r = r0 + rl; r < r1; r += UNR * g.rpb) {
-    float x[UNR][VEC], d[UNR][VEC];
+  for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
+    float x[VEC], d[VEC];
+    ld_vec<T, VEC>(Xb + r * xld + c0, x);
+    ld_vec<T, VEC>(Db + r * dld + c0, d);
 #pragma unroll
-    for (int u = 0; u < UNR; ++u)
-      if (r + u * g.rpb < r1) {
-        ld_vec<T, VEC>(Xb + (r + u * g.rpb) * xld + c0, x[u]);
-        ld_vec<T, VEC>(Db + (r + u * g.rpb) * dld + c0, d[u]);
-      }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u)
-      if (r + u * g.rpb < r1) {
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          float xh = (x[u][v] - m[v]) * is[v];
-          float dz = d[u][v] * act_grad(fmaf(ga[v], xh, be[v]), act, alpha);
-          x[u][v] = k1[v] * (dz - k2[v] - xh * k3[v]);
-        }
-        st_vec<T, VEC>(Ob + (r + u * g.rpb) * old + c0, x[u]);
-      }
+    for (int v = 0; v < VEC; ++v) {
+      const float gd = d[v] * act_grad(fmaf(ka[v], x[v], kc[v]), act, alpha);
+      x[v] = fmaf(kA[v], gd, fmaf(kB[v], x[v], kC[v]));
+    }
+    st_vec<T, VEC>(Ob + r * old + c0, x);
   }
 }
 
 // --------------------------------------------------- BN + act + max (K8a) --
 // grid (colgroups, N, B); block reduces max/argmax over the L rows of sample n.
 template <typename T, int VEC>
-__global__ void __launch_bounds__(NT) k_bn_max_fwd(int64_t L, int64_t C, const T* __restrict__ X, int64_t xbs,
+__global__ void __launch_bounds__(NT, 4) k_bn_max_fwd(int64_t L, int64_t C, const T* __restrict__ X, int64_t xbs,
                                                    int64_t xld, const float* __restrict__ gamma,
                                                    const float* __restrict__ beta, int64_t gbs,
                                                    const float* __restrict__ smean, const float* __restrict__ sinv,
@@ -317,20 +322,28 @@ __global__ void __launch_bounds__(NT) k_bn_max_fwd(int64_t L, int64_t C, const T
       sf[v] = be - m * ga * is;
     }
     const T* Xb = X + (int64_t)b * xbs + n * L * xld;
-    for (int64_t l = rl; l < L; l += UNR * g.rpb) {
-      float x[UNR][VEC];
+    // two rows in flight per thread (bulk), then the tail row: loads issued before use
+    int64_t l = rl;
+    for (; l + g.rpb < L; l += 2 * g.rpb) {
+      float x0[VEC], x1[VEC];
+      ld_vec<T, VEC>(Xb + l * xld + c0, x0);
+      ld_vec<T, VEC>(Xb + (l + g.rpb) * xld + c0, x1);
 #pragma unroll
-      for (int u = 0; u < UNR; ++u)
-        if (l + u * g.rpb < L) ld_vec<T, VEC>(Xb + (l + u * g.rpb) * xld + c0, x[u]);
+      for (int v = 0; v < VEC; ++v) {
+        const float z0 = act_fwd(fmaf(x0[v], sc[v], sf[v]), act, alpha);
+        const float z1 = act_fwd(fmaf(x1[v], sc[v], sf[v]), act, alpha);
+        if (z0 > best[v]) { best[v] = z0; bi[v] = (int)l; }          // increasing l per lane
+        if (z1 > best[v]) { best[v] = z1; bi[v] = (int)(l + g.rpb); }
+      }
+    }
+    if (l < L) {
+      float x0[VEC];
+      ld_vec<T, VEC>(Xb + l * xld + c0, x0);
 #pragma unroll
-      for (int u = 0; u < UNR; ++u)
-        if (l + u * g.rpb < L) {
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            float z = act_fwd(fmaf(x[u][v], sc[v], sf[v]), act, alpha);
-            if (z > best[v]) { best[v] = z; bi[v] = (int)(l + u * g.rpb); }   // increasing l per lane
-          }
-        }
+      for (int v = 0; v < VEC; ++v) {
+        const float z0 = act_fwd(fmaf(x0[v], sc[v], sf[v]), act, alpha);
+        if (z0 > best[v]) { best[v] = z0; bi[v] = (int)l; }
+      }
     }
   }
 #pragma unroll
@@ -453,9 +466,12 @@ int pick_vec(hfta_dtype dt, int64_t C, std::initializer_list<std::tuple<const vo
   return vec;
 }
 
+constexpr int BWD_BPS = 32;   // backward passes read 2 tensors: more row chunks in flight (measured)
+
 size_t bn_parts_bytes(int B, int64_t R, int64_t C) {
-  Geo g1 = make_geo(B, R, C, 1), g4 = make_geo(B, R, C, 4), g8 = make_geo(B, R, C, 8);
-  int ch = std::max(g1.chunks, std::max(g4.chunks, g8.chunks));
+  int ch = 1;
+  for (int vec : {1, 4, 8})
+    for (int bps : {0, BWD_BPS}) ch = std::max(ch, make_geo(B, R, C, vec, bps).chunks);
   return align_up(2 * (size_t)B * ch * C * sizeof(float), 256);
 }
 
@@ -481,7 +497,7 @@ extern "C" {
 
 size_t hfta_fused_bn_workspace(int B, int64_t R, int64_t C) {
   if (B < 1 || R < 1 || C < 1) return 0;
-  return bn_parts_bytes(B, R, C) + align_up(3 * (size_t)B * C * sizeof(float), 256);
+  return bn_parts_bytes(B, R, C) + align_up(5 * (size_t)B * C * sizeof(float), 256);
 }
 
 hfta_status hfta_fused_bn_fwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_in X, const float* gamma,
@@ -532,7 +548,7 @@ hfta_status hfta_fused_bn_bwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_i
   HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "bn_bwd: workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = (cudaStream_t)stream;
   int vec = pick_vec(dt, C, {{X.ptr, X.ld, X.bstride}, {dY.ptr, dY.ld, dY.bstride}, {dX.ptr, dX.ld, dX.bstride}});
-  Geo g = make_geo(B, R, C, vec);
+  Geo g = make_geo(B, R, C, vec, BWD_BPS);
   float* p1 = reinterpret_cast<float*>(ws);
   float* p2 = p1 + (size_t)B * g.chunks * C;
   size_t parts_bytes = bn_parts_bytes(B, R, C);
@@ -542,10 +558,9 @@ hfta_status hfta_fused_bn_bwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_i
     LAUNCH_VEC(T, vec, k_bn_bwd_reduce, grid, R, C, (const T*)dY.ptr, dY.bstride, dY.ld, (const T*)X.ptr,
                X.bstride, X.ld, gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, g, p1, p2);
     k_bn_bwd_finalize<<<(unsigned)cdiv((int64_t)B * C, 256), 256, 0, s>>>(
-        B, R, C, g.chunks, p1, p2, gamma, gb_bstride, save_invstd, dgamma, dbeta, accumulate, coef);
+        B, R, C, g.chunks, p1, p2, gamma, beta, gb_bstride, save_mean, save_invstd, dgamma, dbeta, accumulate, coef);
     LAUNCH_VEC(T, vec, k_bn_bwd_apply, grid, B, R, C, (const T*)dY.ptr, dY.bstride, dY.ld, (const T*)X.ptr,
-               X.bstride, X.ld, (T*)dX.ptr, dX.bstride, dX.ld, gamma, beta, gb_bstride, save_mean, save_invstd,
-               (int)act, act_alpha, g, coef);
+               X.bstride, X.ld, (T*)dX.ptr, dX.bstride, dX.ld, (int)act, act_alpha, g, coef);
   });
   count_launches(3);
   return post_launch(s, "hfta_fused_bn_bwd");

@@ -111,6 +111,26 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
 // UMMA shared-memory matrix descriptor, SWIZZLE_128B, sm100 version 1.
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -161,8 +181,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* bempty = bfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 1);
   // per-epilogue-warp staging for the TMA store: 2 buffers x 32 rows x 64 B
-  uint8_t* stage_out = bres + BRES_BYTES + 1024;                   // NEPI warps x 2 x 2 KB
-  float* sbias_all = reinterpret_cast<float*>(stage_out + NEPI * 2 * 2048);   // NEPI warps x BN floats
+  uint8_t* stage_out = bres + BRES_BYTES + 1024;                   // NEPI warps x 2 x 4 KB
+  float* sbias_all = reinterpret_cast<float*>(stage_out + NEPI * 2 * 4096);   // NEPI warps x BN floats
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -301,8 +321,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   } else {
     // ============================== epilogue ==============================
     const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
-    const int half = (warp - 2) >> 2;             // two warps per quarter split the column chunks
-    float* sbias = sbias_all + (warp - 2) * BN;
+    const int half = (warp - 2) >> 2;             // two warps per quarter split the 64-column steps
+    const uint32_t sbias = smem_u32(sbias_all + (warp - 2) * BN);
+    constexpr int NSTEP = BN / 64;
+    const int my_steps = (NSTEP - half + 1) / 2;
     uint32_t sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -324,50 +346,60 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       if (vbias) {                       // per-tile bias slice -> this warp's smem (broadcast reads later)
         const float* bsrc = p.bias + (int64_t)b * p.bias_bs + (int64_t)nt * BN;
 #pragma unroll
-        for (int j = 0; j < BN / 32; ++j) {
-          const int64_t n = (int64_t)nt * BN + j * 32 + lane;
-          sbias[j * 32 + lane] = n < p.N ? bsrc[j * 32 + lane] : 0.f;
+        for (int jj = 0; jj < BN / 32; ++jj) {
+          const int64_t n = (int64_t)nt * BN + jj * 32 + lane;
+          st_shared_f32(sbias + (jj * 32 + lane) * 4, n < p.N ? bsrc[jj * 32 + lane] : 0.f);
         }
         __syncwarp();
       }
+      if (my_steps == 0) {               // nothing for this warp in this tile: release at once
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
 #pragma unroll 1
-      for (int j = half; j < BN / 32; j += 2) {
-        float v[32];
-        tmem_ld32(tmem_base + (uint32_t)(acc * BN + j * 32) + ((uint32_t)(quarter * 32) << 16), v);
-        if (j + 2 >= BN / 32) {          // this warp's last chunk of the tile: release the accumulator
+      for (int si = 0; si < my_steps; ++si) {
+        const int j = half + 2 * si;     // 64-column step
+        uint32_t u[64];
+        const uint32_t ta = tmem_base + (uint32_t)(acc * BN + j * 64) + ((uint32_t)(quarter * 32) << 16);
+        tmem_ld32_nowait(ta, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
+        tmem_ld32_nowait(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
+        tmem_wait_ld();
+        if (si == my_steps - 1) {        // this warp's last step of the tile: release the accumulator
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        const int64_t n0 = (int64_t)nt * BN + j * 32;
+        const int64_t n0 = (int64_t)nt * BN + j * 64;
         if (n0 >= p.N) continue;                       // warp-uniform
-        if (vbias) {
-          const float4* bp = reinterpret_cast<const float4*>(sbias + j * 32);   // smem broadcast
+        float v[64];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 t4 = bp[q];
+        for (int q = 0; q < 64; ++q) v[q] = __uint_as_float(u[q]);
+        if (vbias) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {               // smem broadcast
+            const float4 t4 = ld_shared_f4(sbias + (j * 64 + 4 * q) * 4);
             v[4 * q] += t4.x; v[4 * q + 1] += t4.y; v[4 * q + 2] += t4.z; v[4 * q + 3] += t4.w;
           }
         } else if (brow) {
-          for (int q = 0; q < 32 && n0 + q < p.N; ++q) v[q] += brow[n0 + q];
+          for (int q = 0; q < 64 && n0 + q < p.N; ++q) v[q] += brow[n0 + q];
         }
         if constexpr (!OUT_F32) {
-          // bf16: stage the warp's 32 x 32 sub-tile in smem, one TMA store per
-          // chunk (rows >= M and columns >= N are clipped by the tensor map).
-          uint8_t* buf = stage_out + ((warp - 2) * 2 + (sbuf & 1)) * 2048;
+          // bf16: stage the warp's 32 x 64 sub-tile (128-B rows, TMA SWIZZLE_128B layout:
+          // 16-B chunk q of row r at chunk q ^ (r & 7) -> conflict-free), one TMA store per
+          // step (rows >= M and columns >= N are clipped by the tensor map).
+          uint8_t* buf = stage_out + ((warp - 2) * 2 + (sbuf & 1)) * 4096;
           if (lane == 0) tma_store_wait_read<1>();
           __syncwarp();
-          // 64-B rows in the TMA SWIZZLE_64B layout: 16-B chunk q of row r lives at
-          // chunk q ^ ((r >> 1) & 3) -> the 32 lanes' stores hit all banks (4 wavefronts).
-          const uint32_t rowaddr = smem_u32(buf) + lane * 64;
-          const uint32_t sw = (uint32_t)((lane >> 1) & 3);
+          const uint32_t rowaddr = smem_u32(buf) + lane * 128;
+          const uint32_t sw = (uint32_t)(lane & 7);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 u;
-            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+          for (int q = 0; q < 8; ++q) {
+            uint4 w4;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w4);
 #pragma unroll
             for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
-            st_shared_v4(rowaddr + (((uint32_t)q ^ sw) << 4), u);
+            st_shared_v4(rowaddr + (((uint32_t)q ^ sw) << 4), w4);
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -375,18 +407,25 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           ++sbuf;
         } else {
           if (!row_ok) continue;
-          const bool full_chunk = n0 + 32 <= p.N;
-          float* dst = p.splits > 1 ? p.part + (((int64_t)split * p.B + b) * p.M + m) * p.N + n0
-                                    : reinterpret_cast<float*>(p.C) + (int64_t)b * p.c_bs + m * p.c_ld + n0;
-          const bool vec_ok = full_chunk && (p.splits > 1 ? (p.N % 4 == 0) : true);
-          if (p.splits == 1 && p.accumulate) {
-            for (int q = 0; q < 32 && n0 + q < p.N; ++q) dst[q] += v[q];
-          } else if (vec_ok) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          } else {
-            for (int q = 0; q < 32 && n0 + q < p.N; ++q) dst[q] = v[q];
+          for (int hh = 0; hh < 2; ++hh) {
+            const int64_t c0 = n0 + hh * 32;
+            if (c0 >= p.N) break;
+            const float* vv = v + hh * 32;
+            const bool full_chunk = c0 + 32 <= p.N;
+            float* dst = p.splits > 1 ? p.part + (((int64_t)split * p.B + b) * p.M + m) * p.N + c0
+                                      : reinterpret_cast<float*>(p.C) + (int64_t)b * p.c_bs + m * p.c_ld + c0;
+            const bool vec_ok = full_chunk && (p.splits > 1 ? (p.N % 4 == 0) : true);
+            if (p.splits == 1 && p.accumulate) {
+              for (int q = 0; q < 32 && c0 + q < p.N; ++q) dst[q] += vv[q];
+            } else if (vec_ok) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                *reinterpret_cast<float4*>(dst + 4 * q) =
+                    make_float4(vv[4 * q], vv[4 * q + 1], vv[4 * q + 2], vv[4 * q + 3]);
+            } else {
+              for (int q = 0; q < 32 && c0 + q < p.N; ++q) dst[q] = vv[q];
+            }
           }
         }
       }
@@ -436,9 +475,9 @@ hfta_status make_map(CUtensorMap* m, const void* ptr, int64_t inner, int64_t row
 
 template <bool A_MN, bool B_MN, int BN, bool OUT_F32, bool BRES>
 hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
-  constexpr int STAGES = BRES ? 6 : ((BN == 256) ? 3 : (BN == 128 ? 5 : 6));
+  constexpr int STAGES = BRES ? 4 : ((BN == 256) ? 3 : 4);
   constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + (BRES ? 0 : BN * BK * 2)) +
-                          (BRES ? 2 * BN * BK * 2 : 0) + 1024 + NEPI * 2 * 2048 + NEPI * BN * 4;
+                          (BRES ? 2 * BN * BK * 2 : 0) + 1024 + NEPI * 2 * 4096 + NEPI * BN * 4;
   static_assert(SMEM <= 232448, "shared memory budget");
   if (hfta_status st = get_encode()) return st;
   CUtensorMap ta, tb;
@@ -454,10 +493,10 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   if (!OUT_F32 && p.splits == 1) {
     cuuint64_t dims[3] = {(cuuint64_t)p.N, (cuuint64_t)p.M, (cuuint64_t)p.B};
     cuuint64_t strides[2] = {(cuuint64_t)(p.c_ld * 2), (cuuint64_t)((p.B > 1 ? p.c_bs : p.M * p.c_ld) * 2)};
-    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t box[3] = {64, 32, 1};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = g_encode(&tc_, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, p.C, dims, strides, box, es,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(HFTA_ERR_CUDA, "cuTensorMapEncodeTiled (C) failed (%d)", (int)r);
   }
