@@ -216,6 +216,57 @@ hfta_status hfta_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C, hfta_dtype d
                             hfta_act act, float act_alpha, hfta_out dX,
                             float* dgamma, float* dbeta, void* ws, size_t ws_bytes,
                             hfta_stream stream);
+/* ------------------------------ fused Linear -> BN -> max block (K10) -- */
+/*
+ * The PointNet point-feature block as ONE fused operation per pass (App. B
+ * rows Conv1d P:L1265-1266, BatchNorm1d P:L1280-1281, MaxPool P:L1286-1287,
+ * composed as in the cited PointNetfeat/STN3d, reading R1):
+ *   Y[b][r][c] = sum_k X[b][r][k] W[b][c][k] + bias[b][c]      r = n*L + l
+ *   mean/var over the R = N*L rows (biased var normalises, unbiased var
+ *   enters running_var, reading R6), xhat = (Y - mean)*invstd,
+ *   G[b][n][c] = max_l act(gamma*xhat + beta), argmax[b][n][c] = first l
+ *   attaining it (reading R15), ext[b][n][c] = Y at that row.
+ * The [B][R][C] tensor Y is never written: the forward reduces it out of
+ * tensor memory and the backward recomputes it tile by tile (K10).
+ * Precision: bf16 X/W (dt must be HFTA_BF16), fp32 accumulation, statistics
+ * from fp32 partials combined in fp64.  Layouts: X [B][R][K] (bstride 0 =
+ * shared), W [B][C][K] (hfta_in), per-channel vectors at [b*bstride + c];
+ * G, ext fp32 [B][N][C] (hfta_out), argmax int32 contiguous [B][N][C].
+ * Constraints (else HFTA_ERR_UNSUPPORTED): K in {64, 128}, C % 128 == 0,
+ * 16-B aligned X/W/dX with 16-B row strides.  Workspace:
+ * hfta_fused_linear_bn_max_workspace() bytes, caller-owned, shared by fwd
+ * and bwd (no state carried in it between the two calls).
+ */
+size_t hfta_fused_linear_bn_max_workspace(int B, int64_t N, int64_t L, int64_t C, int64_t K);
+hfta_status hfta_fused_linear_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C, int64_t K,
+                                         hfta_dtype dt, hfta_in X, hfta_in W,
+                                         const float* bias, int64_t bias_bstride,
+                                         const float* gamma, const float* beta, int64_t gb_bstride,
+                                         float* running_mean, float* running_var,
+                                         float momentum, float eps, hfta_act act, float act_alpha,
+                                         hfta_out G, int32_t* argmax, hfta_out ext,
+                                         float* save_mean, float* save_invstd,
+                                         void* ws, size_t ws_bytes, hfta_stream stream);
+/*
+ * Backward: dG fp32 [B][N][C] -> dZ at the argmax rows (act' at the pooled
+ * pre-activation), BN backward dY = gamma*invstd/R*(R*dZ - dbeta - xhat*dgamma)
+ * (dense), dX = dY W (bf16, skipped if dX.ptr is NULL), dW = dY^T X (fp32 at
+ * dW[b*dW_bstride + c*dW_ld + k]), dgamma/dbeta fp32, dbias (may be NULL)
+ * written as exact zeros (BN-absorbed).  accumulate != 0 adds to
+ * dW/dgamma/dbeta instead of overwriting.  ext/argmax/save_* are the forward's
+ * outputs.
+ */
+hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C, int64_t K,
+                                         hfta_dtype dt, hfta_in dG, hfta_in X, hfta_in W,
+                                         const int32_t* argmax, hfta_in ext,
+                                         const float* bias, int64_t bias_bstride,
+                                         const float* gamma, const float* beta, int64_t gb_bstride,
+                                         const float* save_mean, const float* save_invstd,
+                                         hfta_act act, float act_alpha, hfta_out dX,
+                                         float* dW, int64_t dW_bstride, int64_t dW_ld,
+                                         float* dbias, int64_t dbias_bstride,
+                                         float* dgamma, float* dbeta, int accumulate,
+                                         void* ws, size_t ws_bytes, hfta_stream stream);
 /*
  * PointNet input transform (STN): T_b,n = F_b[n] viewed as 3x3 row-major
  * (+ I3 if add_identity), x'_b[n*L+l][:] = x[n*L+l][:] * T_b,n.
