@@ -18,7 +18,6 @@ Prints ONE JSON line on rank 0.
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -46,46 +45,48 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (recipe clocks line)."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled DURING the timed region (the
+    recipe's clocks line) through NVML every 20 ms in a background thread;
+    nvidia-smi as the fallback sampler."""
+    BITS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, device):
-        self.device, self.rows, self.proc = device, [], None
+        self.device, self.rows, self.stop_ev = device, [], threading.Event()
+        self.max_mhz = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.th = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def loop():
+                while not self.stop_ev.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((float(sm), int(rs)))
+                    except Exception:
+                        pass
+                    self.stop_ev.wait(0.02)
+            self.th = threading.Thread(target=loop, daemon=True)
             self.th.start()
         except Exception:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.th = None
 
     def stop(self):
-        if self.proc is None:
+        if self.th is None:
             return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        self.stop_ev.set()
         self.th.join(timeout=2)
-        rows = [r for r in self.rows if len(r) >= 9]
-        if not rows:
+        if not self.rows:
             return None
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({k for _, m in self.rows for k, bit in self.BITS.items() if m & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows), "sampler": "nvml 20 ms"}
 
 
 # ------------------------------------------------------------------ oracle --
@@ -230,7 +231,7 @@ def run_ours(args, rank, world, local_rank):
         wl.step()
         gather_losses()
     torch.cuda.synchronize()
-    probe_name = args.probe if args.workload == "pointnet_cls" else None
+    probe_name = args.probe if args.workload in ("pointnet_cls", "pointnet_seg") else None
     if probe_name:
         net.probe_arm(probe_name)
     if world > 1:
@@ -293,7 +294,8 @@ def run_ours(args, rank, world, local_rank):
         path = "tc" if args.dtype == "bf16" else "simt"
         roof = net.probe_roofline(probe_name, probe_ms, pk, path=path) if probe_name else None
         try:   # DRAM traffic of the probed kernel from the committed ncu --set full capture
-            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic_r01.json")))[probe_name]
+            key = probe_name + (":lbm" if getattr(net, "fuse_lbm", False) and ".c3:" in probe_name else "")
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic_r01.json")))[key]
             if path == "tc":
                 roof["traffic"] = tr["dram_bytes_per_model"] * B
                 roof["traffic_source"] = tr["source"]

@@ -41,9 +41,12 @@ constexpr int NEPIW = 8;
 constexpr int CBLK = 128;                      // channels per UMMA M block
 constexpr uint32_t WKB = CBLK * 64 * 2;        // one 64-wide k block of a 128-channel W block: 16 KB
 // forward
-constexpr int FR = 64;                         // points per chunk (UMMA N)
-constexpr int FG = 4;                          // channel blocks per unit: TMEM 2 x FG x FR = 512 columns
-constexpr int FSTAGES = 4;
+constexpr int FR = 128;                        // points per chunk (UMMA N): smem operand reads 8 KB / 64 MMA cycles
+constexpr int FG = 2;                          // channel blocks per unit: TMEM 2 x FG x FR = 512 columns
+constexpr int FSTAGES = 3;
+constexpr int NBW = FG / 2;                    // channel blocks per epilogue warp
+constexpr int LPB = FR / 32;                   // 32-column TMEM loads per block and chunk
+static_assert(NBW * LPB == 4, "epilogue load schedule assumes 4 loads per warp and chunk");
 constexpr uint32_t FA_KB = FR * 64 * 2;        // 8 KB per k block of an X chunk
 // backward
 constexpr int BR = 128;                        // points per tile / chunk
@@ -79,37 +82,76 @@ __device__ __forceinline__ void ld64(uint32_t ta, uint32_t (&u)[64]) {
 // ================================================================ forward ==
 
 struct FwdArgs {
-  int B, Ncl, nblk, ngroups, teams, nkb, a_shared;
+  int B, Ncl, nblk, ngroups, teams, nkb, a_shared, mode;
   int64_t L, C;
   float* s1; float* s2; float* mx; int32_t* idx;   // per-cloud partials [B][Ncl][C]
 };
 
-// One channel's pass over a 64-point chunk: 4 independent segments (ILP) of
-// 16 points each, merged in point order so ties keep the first index.
+// Packed fp32x2 arithmetic (FADD2 / FFMA2) and 3-input max (FMNMX3) keep the
+// epilogue's issue count at ~2 instructions per accumulator element, below
+// the MMA rate for K = 128 (one 64-point chunk: 1024 MMA cycles per SM).
+__device__ __forceinline__ unsigned long long pk2(uint32_t lo, uint32_t hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+__device__ __forceinline__ void add2(unsigned long long& acc, unsigned long long v) {
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(v));
+}
+__device__ __forceinline__ void sq2(unsigned long long& acc, unsigned long long v) {
+  asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc) : "l"(v));
+}
+__device__ __forceinline__ float hsum2(unsigned long long v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo + hi;
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float uf(uint32_t x) { return __uint_as_float(x); }
+
+// Per-channel running state of the forward epilogue: packed sums, running
+// max m and the 16-point group it came from; the group's values sit in this
+// lane's smem slot so the exact first index is resolved once per cloud.
+struct FwdAcc {
+  unsigned long long s1[2], s2[2];
+  float m;
+  int gid;
+};
+
+// One 16-point group (values u[o..o+15]) of one channel.  FULL = all valid.
 template <bool FULL>
-__device__ __forceinline__ void fwd_reduce(const uint32_t (&u)[64], int valid, int base, float& s1, float& s2,
-                                           float& m, int& id) {
-  float a1[4] = {0.f, 0.f, 0.f, 0.f}, a2[4] = {0.f, 0.f, 0.f, 0.f};
-  float cm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-  int cj[4] = {0, 0, 0, 0};
+__device__ __forceinline__ void fwd_group(const uint32_t* u, int valid, int gid, FwdAcc& A, uint32_t slot) {
+  uint32_t v[16];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
+  for (int j = 0; j < 16; ++j) v[j] = (FULL || j < valid) ? u[j] : 0u;
 #pragma unroll
-    for (int sg = 0; sg < 4; ++sg) {
-      const int j = sg * 16 + q;
-      if (FULL || j < valid) {
-        const float v = __uint_as_float(u[j]);
-        a1[sg] += v;
-        a2[sg] = fmaf(v, v, a2[sg]);
-        if (v > cm[sg]) { cm[sg] = v; cj[sg] = j; }
-      }
+  for (int q = 0; q < 8; ++q) {
+    const unsigned long long w = pk2(v[2 * q], v[2 * q + 1]);
+    add2(A.s1[q & 1], w);
+    sq2(A.s2[q & 1], w);
+  }
+  if (!FULL) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = j < valid ? v[j] : __float_as_uint(-INFINITY);
+  }
+  const float a0 = max3(uf(v[0]), uf(v[1]), uf(v[2])), a1 = max3(uf(v[3]), uf(v[4]), uf(v[5]));
+  const float a2 = max3(uf(v[6]), uf(v[7]), uf(v[8])), a3 = max3(uf(v[9]), uf(v[10]), uf(v[11]));
+  const float a4 = max3(uf(v[12]), uf(v[13]), uf(v[14]));
+  const float gm = fmaxf(max3(a0, a1, a2), max3(a3, a4, uf(v[15])));
+  const bool p = gm > A.m;
+  if (__any_sync(0xffffffffu, p)) {
+    if (p) {
+      A.m = gm;
+      A.gid = gid;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        st_shared_v4(slot + q * 512, make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
     }
   }
-  s1 += (a1[0] + a1[1]) + (a1[2] + a1[3]);
-  s2 += (a2[0] + a2[1]) + (a2[2] + a2[3]);
-#pragma unroll
-  for (int sg = 0; sg < 4; ++sg)
-    if (cm[sg] > m) { m = cm[sg]; id = base + cj[sg]; }
 }
 
 __global__ void __launch_bounds__(LT, 1)
@@ -125,6 +167,7 @@ k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* wfull = tempty + 2;
   uint64_t* wempty = wfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + 1);
+  uint8_t* slot_base = reinterpret_cast<uint8_t*>(full) + 256;        // NEPIW x NBW ch x 4 x 32 lanes x 16 B
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -218,43 +261,91 @@ k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     }
   } else {
     const int quarter = warp & 3, half = (warp - 2) >> 2;
+    // per-lane slots [warp][jj][q][lane] x 16 B (conflict-free v4 stores)
+    const uint32_t slots = smem_u32(slot_base) + (uint32_t)(((warp - 2) * (NBW * 4 * 32) + lane) * 16);
     int acc = 0;
     uint32_t aph = 0;
     for (int64_t u = u0; u < u1; ++u) {
       const int b = (int)(u / p.Ncl), n = (int)(u % p.Ncl);
-      float s1[2] = {0.f, 0.f}, s2[2] = {0.f, 0.f}, m[2] = {-INFINITY, -INFINITY};
-      int id[2] = {0, 0};
+      FwdAcc A[NBW];
+#pragma unroll
+      for (int jj = 0; jj < NBW; ++jj) {
+        A[jj].s1[0] = A[jj].s1[1] = A[jj].s2[0] = A[jj].s2[1] = 0ull;
+        A[jj].m = -INFINITY;
+        A[jj].gid = 0;
+      }
+      // this warp owns blocks half + 2 jj (when present): nld 32-column loads per chunk
+      int nld = 0;
+#pragma unroll
+      for (int jj = 0; jj < NBW; ++jj) nld += half + 2 * jj < nb ? LPB : 0;
       for (int ch = 0; ch < nch; ++ch) {
         const int valid = (int)min((int64_t)FR, p.L - (int64_t)ch * FR);
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int j = half + 2 * jj;
-          uint32_t uu[64];
-          if (j < nb) ld64(tmem_base + (uint32_t)(acc * FG * FR + j * FR) + ((uint32_t)(quarter * 32) << 16), uu);
-          if (jj == 1) {                    // both blocks read: hand the buffer back to the MMA warp
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+        const uint32_t ta = tmem_base + (uint32_t)(acc * FG * FR + half * FR) + ((uint32_t)(quarter * 32) << 16);
+        auto release = [&]() {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        };
+        // load i+1 is in flight while load i is reduced; i -> (block jj = i/2, columns hh = i%2)
+        auto proc = [&](const uint32_t (&r)[32], int i) {
+          const int jj = i / LPB, hh = i % LPB;
+          const int g0 = ch * (FR / 16) + hh * 2;
+          const uint32_t sl = slots + (uint32_t)(jj * 4 * 32 * 16);
+          if (p.mode == 1) {
+            if (r[0] == 0x7f800001u && r[31] == 0x7f800001u) A[jj].m = 1.f;   // diagnostics: keep the load live
+          } else if (valid == FR) {
+            fwd_group<true>(r, 16, g0, A[jj], sl);
+            fwd_group<true>(r + 16, 16, g0 + 1, A[jj], sl);
+          } else {
+            fwd_group<false>(r, valid - hh * 32, g0, A[jj], sl);
+            fwd_group<false>(r + 16, valid - hh * 32 - 16, g0 + 1, A[jj], sl);
           }
-          if (j < nb) {
-            if (valid == FR) fwd_reduce<true>(uu, FR, ch * FR, s1[jj], s2[jj], m[jj], id[jj]);
-            else fwd_reduce<false>(uu, valid, ch * FR, s1[jj], s2[jj], m[jj], id[jj]);
+        };
+        uint32_t r0[32], r1[32];
+        if (nld == 0) {
+          release();
+        } else {
+          tmem_ld32_nowait(ta, r0);
+          tmem_wait_ld();
+          auto col = [](int i) { return (uint32_t)(2 * (i / LPB) * FR + (i % LPB) * 32); };
+          tmem_ld32_nowait(ta + col(1), r1);
+          proc(r0, 0);
+          tmem_wait_ld();
+          if (nld == 4) tmem_ld32_nowait(ta + col(2), r0);
+          else release();
+          proc(r1, 1);
+          if (nld == 4) {
+            tmem_wait_ld();
+            tmem_ld32_nowait(ta + col(3), r1);
+            proc(r0, 2);
+            tmem_wait_ld();
+            release();
+            proc(r1, 3);
           }
         }
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
+      for (int jj = 0; jj < NBW; ++jj) {
         const int j = half + 2 * jj;
         if (j >= nb) continue;
+        int first = 15;                               // first point of the winning group equal to the max
+#pragma unroll
+        for (int q = 3; q >= 0; --q) {
+          const float4 t4 = ld_shared_f4(slots + (uint32_t)((jj * 4 + q) * 512));
+          if (t4.w == A[jj].m) first = 4 * q + 3;
+          if (t4.z == A[jj].m) first = 4 * q + 2;
+          if (t4.y == A[jj].m) first = 4 * q + 1;
+          if (t4.x == A[jj].m) first = 4 * q;
+        }
         const int64_t c = (int64_t)(blk0 + j) * CBLK + quarter * 32 + lane;
         const int64_t o = ((int64_t)b * p.Ncl + n) * p.C + c;
-        p.s1[o] = s1[jj];
-        p.s2[o] = s2[jj];
-        p.mx[o] = m[jj];
-        p.idx[o] = id[jj];
+        p.s1[o] = hsum2(A[jj].s1[0]) + hsum2(A[jj].s1[1]);
+        p.s2[o] = hsum2(A[jj].s2[0]) + hsum2(A[jj].s2[1]);
+        p.mx[o] = A[jj].m;
+        p.idx[o] = A[jj].gid * 16 + first;
       }
     }
   }
@@ -828,7 +919,7 @@ __global__ void k_lbm_wreduce(int B, int S, int64_t C, int64_t K, const float* _
 }
 
 // ------------------------------------------------------------ host side --
-constexpr size_t FWD_SMEM = 1024 + FG * 2 * WKB + FSTAGES * 2 * FA_KB + 256;
+constexpr size_t FWD_SMEM = 1024 + FG * 2 * WKB + FSTAGES * 2 * FA_KB + 256 + NEPIW * NBW * 4 * 32 * 16;
 constexpr size_t DG_SMEM = 1024 + 2 * 2 * BA_KB + DG_WST * 2 * WKB + 2 * DY_BYTES + 256;
 constexpr size_t WG_SMEM = 1024 + 2 * WKB + WG_AST * 2 * BA_KB + 2 * DY_BYTES + 256;
 static_assert(FWD_SMEM <= 232448 && DG_SMEM <= 232448 && WG_SMEM <= 232448, "shared memory budget");
@@ -924,6 +1015,10 @@ hfta_status hfta_fused_linear_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C,
   a.a_shared = nba == 1 && B > 1;
   a.L = L; a.C = C;
   a.s1 = s1; a.s2 = s2; a.mx = mx; a.idx = idx;
+  {
+    const char* e = getenv("HFTA_LBM_MODE");   // diagnostics: 1 = epilogue only drains TMEM
+    a.mode = e ? atoi(e) : 0;
+  }
   const int64_t npairs = (int64_t)B * N;
   a.teams = (int)std::max<int64_t>(1, std::min<int64_t>(npairs, num_sms() / a.ngroups));
   static bool attr = false;

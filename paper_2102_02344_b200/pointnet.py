@@ -41,6 +41,9 @@ class FusedPointNet(FusedNet):
         sh = self.arena.shape
         self.c1, self.c2, self.c3 = sh["stn.c1.W"][0], sh["stn.c2.W"][0], sh["stn.c3.W"][0]
         self.f1, self.f2 = sh["stn.fc1.W"][0], sh["stn.fc2.W"][0]
+        # bf16: c3 -> bn3 -> max runs as the fused tensor-core block (K10);
+        # the [R][1024] pre-BN activation is never materialised.
+        self.fuse_lbm = self.dt == H.HFTA_BF16 and self.c3 % 128 == 0 and self.c2 in (64, 128)
         self._alloc()
 
     # ------------------------------------------------------------ buffers --
@@ -54,7 +57,10 @@ class FusedPointNet(FusedNet):
         for p in ("stn", "feat"):
             S[p + ".y1"], S[p + ".a1"] = a(R, c1), a(R, c1)
             S[p + ".y2"], S[p + ".a2"] = a(R, c2), a(R, c2)
-            S[p + ".y3"] = a(R, c3)
+            if self.fuse_lbm:
+                S[p + ".ext"] = f(N, c3)            # Y at the argmax rows (the block's saved tensor)
+            else:
+                S[p + ".y3"] = a(R, c3)
             S[p + ".g"] = f(N, c3)
             S[p + ".amax"] = torch.empty(B, N, c3, dtype=torch.int32, device=self.device)
         S["stn.f1"], S["stn.h4"] = f(N, f1), f(N, f1)
@@ -83,7 +89,8 @@ class FusedPointNet(FusedNet):
             S["d.s3a"], S["d.s3b"] = a(R, h3), a(R, h3)
             S["seg.S"] = f(N, h1)                   # per-sample row sums of dy1
             S["d.pf"] = a(R, c1)                    # gradient reaching the point feature from the head
-        S["d.big"] = a(R, c3)
+        if not self.fuse_lbm:
+            S["d.big"] = a(R, c3)
         S["d.c2a"], S["d.c2b"] = a(R, c2), a(R, c2)
         S["d.c1a"], S["d.c1b"] = a(R, c1), a(R, c1)
         S["d.g"] = f(N, c3)
@@ -103,6 +110,8 @@ class FusedPointNet(FusedNet):
         for (Rr, Cc) in [(R, c1), (R, c2), (R, c3), (N, f1), (N, f2)]:
             ws.reserve(H.hfta_fused_bn_workspace(B, Rr, Cc))
         ws.reserve(H.hfta_bn_max_bwd_workspace(B, N, c3))
+        if self.fuse_lbm:
+            ws.reserve(H.hfta_fused_linear_bn_max_workspace(B, N, self.L, c3, c2))
         if self.task == "seg":
             for (M, Nn, K) in [(R, self.h1w, c1), (N, self.h1w, c3), (R, self.h2w, self.h1w), (R, self.h3w, self.h2w),
                                (R, self.k, self.h3w)]:
@@ -116,6 +125,67 @@ class FusedPointNet(FusedNet):
         self.ws = ws
 
     # -------------------------------------------------------------- step --
+    def probe_roofline(self, name, ms, peaks, path="simt"):
+        """Roofline of the fused c3 block (K10): algorithmic flops = the
+        block's contractions (fwd: Y = X W^T; bwd: dgrad + wgrad -- the
+        recompute of Y is NOT counted), algorithmic bytes = X, W and the
+        per-sample tensors once (+ dX, dW for bwd).  Arithmetic intensity ~C
+        flop/B >> the ridge: tensor-bound against the measured bf16 peak."""
+        layer, kind = name.split(":")
+        if not (self.fuse_lbm and layer.endswith(".c3")):
+            return super().probe_roofline(name, ms, peaks, path)
+        B, R, C, K, N = self.B, self.R, self.c3, self.c2, self.N
+        if kind == "fwd":
+            flops = 2.0 * B * R * C * K
+            nbytes = B * (R * K * 2 + C * K * 2 + N * C * 12 + C * 16)
+        else:
+            flops = 2.0 * 2.0 * B * R * C * K
+            nbytes = B * (2 * R * K * 2 + C * K * 2 + C * K * 4 + N * C * 12 + C * 16)
+        t = float(np.mean(ms)) / 1e3 if ms else float("nan")
+        ach = flops / t / 1e12
+        return {"bound": "tensor", "achieved": ach, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                "frac": ach / peaks["bf16_tflops_sustained"], "traffic": None, "kernel": name + " (fused c3->bn3->max block)",
+                "launches_timed": len(ms), "ms_per_launch": t * 1e3,
+                "algorithmic": {"flops": flops, "bytes": nbytes}, "peak_source": peaks["source"]}
+
+    def _block_fwd(self, p, act, s):
+        """c3 -> bn3 -> act -> max over points (STN: ReLU, feat: none)."""
+        S, R = self.S, self.R
+        if not self.fuse_lbm:
+            self._lin_fwd(_in(S[p + ".a2"]), R, p + ".c3", S[p + ".y3"], s)
+            self._bn_fwd(S[p + ".y3"], p + ".bn3", act, None, s)
+            self._bn_max_fwd(S[p + ".y3"], p + ".bn3", act, S[p + ".g"], S[p + ".amax"], s)
+            return
+        ar, P, bn = self.arena, self.arena.P, p + ".bn3"
+        rm, rv = self.running[bn]
+        sm, si = self.saved[bn]
+        e0 = self._pbegin(p + ".c3:fwd", s)
+        H.hfta_fused_linear_bn_max_fwd(self.B, self.N, self.L, self.c3, self.c2, self.dt, _in(S[p + ".a2"]),
+                                       ar.w_in(p + ".c3.W", self.dt), ar.fptr("p", p + ".c3.b"), P,
+                                       ar.fptr("p", bn + ".g"), ar.fptr("p", bn + ".beta"), P, H.ptr(rm), H.ptr(rv),
+                                       0.1, 1e-5, act, self.act_alpha, _out(S[p + ".g"]), H.ptr(S[p + ".amax"]),
+                                       _out(S[p + ".ext"]), H.ptr(sm), H.ptr(si), self.ws.ptr, self.ws.nbytes, s)
+        self._pend(e0)
+
+    def _block_bwd(self, p, act, s):
+        """Backward of _block_fwd from d.g; writes d.c2a (grad of a2) and the c3/bn3 gradients."""
+        S, R = self.S, self.R
+        if not self.fuse_lbm:
+            self._bn_max_bwd(S["d.g"], S[p + ".y3"], S[p + ".amax"], p + ".bn3", act, S["d.big"], s)
+            self._lin_bwd(S["d.big"], _in(S[p + ".a2"]), R, p + ".c3", S["d.c2a"], s)
+            return
+        ar, P, bn = self.arena, self.arena.P, p + ".bn3"
+        sm, si = self.saved[bn]
+        e0 = self._pbegin(p + ".c3:bwd", s)
+        H.hfta_fused_linear_bn_max_bwd(self.B, self.N, self.L, self.c3, self.c2, self.dt, _in(S["d.g"]),
+                                       _in(S[p + ".a2"]), ar.w_in(p + ".c3.W", self.dt), H.ptr(S[p + ".amax"]),
+                                       _in(S[p + ".ext"]), ar.fptr("p", p + ".c3.b"), P, ar.fptr("p", bn + ".g"),
+                                       ar.fptr("p", bn + ".beta"), P, H.ptr(sm), H.ptr(si), act, self.act_alpha,
+                                       _out(S["d.c2a"]), ar.fptr("g", p + ".c3.W"), P, self.c2,
+                                       ar.fptr("g", p + ".c3.b"), P, ar.fptr("g", bn + ".g"), ar.fptr("g", bn + ".beta"),
+                                       0, self.ws.ptr, self.ws.nbytes, s)
+        self._pend(e0)
+
     def _stn_feat_fwd(self, x, s):
         S, R = self.S, self.R
         xin = H.tin(self.x_dt, 0, 3)
@@ -124,9 +194,7 @@ class FusedPointNet(FusedNet):
         self._bn_fwd(S["stn.y1"], "stn.bn1", A_RELU, S["stn.a1"], s)
         self._lin_fwd(_in(S["stn.a1"]), R, "stn.c2", S["stn.y2"], s)
         self._bn_fwd(S["stn.y2"], "stn.bn2", A_RELU, S["stn.a2"], s)
-        self._lin_fwd(_in(S["stn.a2"]), R, "stn.c3", S["stn.y3"], s)
-        self._bn_fwd(S["stn.y3"], "stn.bn3", A_RELU, None, s)
-        self._bn_max_fwd(S["stn.y3"], "stn.bn3", A_RELU, S["stn.g"], S["stn.amax"], s)
+        self._block_fwd("stn", A_RELU, s)
         self._lin_fwd(_in(S["stn.g"]), self.N, "stn.fc1", S["stn.f1"], s)
         self._bn_fwd(S["stn.f1"], "stn.bn4", A_RELU, S["stn.h4"], s)
         self._lin_fwd(_in(S["stn.h4"]), self.N, "stn.fc2", S["stn.f2"], s)
@@ -139,15 +207,12 @@ class FusedPointNet(FusedNet):
         self._bn_fwd(S["feat.y1"], "feat.bn1", A_RELU, S["feat.a1"], s)
         self._lin_fwd(_in(S["feat.a1"]), R, "feat.c2", S["feat.y2"], s)
         self._bn_fwd(S["feat.y2"], "feat.bn2", A_RELU, S["feat.a2"], s)
-        self._lin_fwd(_in(S["feat.a2"]), R, "feat.c3", S["feat.y3"], s)
-        self._bn_fwd(S["feat.y3"], "feat.bn3", A_NONE, None, s)
-        self._bn_max_fwd(S["feat.y3"], "feat.bn3", A_NONE, S["feat.g"], S["feat.amax"], s)
+        self._block_fwd("feat", A_NONE, s)
 
     def _stn_feat_bwd(self, x, s):
         S, R, N = self.S, self.R, self.N
         # feat
-        self._bn_max_bwd(S["d.g"], S["feat.y3"], S["feat.amax"], "feat.bn3", A_NONE, S["d.big"], s)
-        self._lin_bwd(S["d.big"], _in(S["feat.a2"]), R, "feat.c3", S["d.c2a"], s)
+        self._block_bwd("feat", A_NONE, s)
         self._bn_bwd(S["d.c2a"], S["feat.y2"], "feat.bn2", A_RELU, S["d.c2b"], s)
         self._lin_bwd(S["d.c2b"], _in(S["feat.a1"]), R, "feat.c2", S["d.c1a"], s)
         if self.task == "seg":      # the point feature also feeds the seg head
@@ -161,8 +226,7 @@ class FusedPointNet(FusedNet):
         self._lin_bwd(S["d.sf2b"], _in(S["stn.h4"]), N, "stn.fc2", S["d.sf1a"], s)
         self._bn_bwd(S["d.sf1a"], S["stn.f1"], "stn.bn4", A_RELU, S["d.sf1b"], s)
         self._lin_bwd(S["d.sf1b"], _in(S["stn.g"]), N, "stn.fc1", S["d.g"], s)
-        self._bn_max_bwd(S["d.g"], S["stn.y3"], S["stn.amax"], "stn.bn3", A_RELU, S["d.big"], s)
-        self._lin_bwd(S["d.big"], _in(S["stn.a2"]), R, "stn.c3", S["d.c2a"], s)
+        self._block_bwd("stn", A_RELU, s)
         self._bn_bwd(S["d.c2a"], S["stn.y2"], "stn.bn2", A_RELU, S["d.c2b"], s)
         self._lin_bwd(S["d.c2b"], _in(S["stn.a1"]), R, "stn.c2", S["d.c1a"], s)
         self._bn_bwd(S["d.c1a"], S["stn.y1"], "stn.bn1", A_RELU, S["d.c1b"], s)
