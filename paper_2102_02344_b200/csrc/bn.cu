@@ -147,22 +147,16 @@ __global__ void __launch_bounds__(NT) k_bn_apply(int64_t R, int64_t C, const T* 
     sc[v] = ga * is;
     sf[v] = be - m * ga * is;
   }
-  const T* Xb = X + (int64_t)b * xbs;
-  T* Yb = Y + (int64_t)b * ybs;
-  const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
-  const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-  for (int64_t r = r0 + rl; r < r1; r += UNR * g.rpb) {
-    float x[UNR][VEC];
+  const T* Xb = X + (int64_t)b * xbs + c0;
+  T* Yb = Y + (int64_t)b * ybs + c0;
+  const int r0 = (int)((int64_t)chunk * g.rows_per_chunk);
+  const int r1 = (int)min(R, (int64_t)r0 + g.rows_per_chunk);
+  for (int r = r0 + rl; r < r1; r += g.rpb) {
+    float x[VEC];
+    ld_vec<T, VEC>(Xb + (int64_t)r * xld, x);
 #pragma unroll
-    for (int u = 0; u < UNR; ++u)
-      if (r + u * g.rpb < r1) ld_vec<T, VEC>(Xb + (r + u * g.rpb) * xld + c0, x[u]);
-#pragma unroll
-    for (int u = 0; u < UNR; ++u)
-      if (r + u * g.rpb < r1) {
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) x[u][v] = act_fwd(fmaf(x[u][v], sc[v], sf[v]), act, alpha);
-        st_vec<T, VEC>(Yb + (r + u * g.rpb) * yld + c0, x[u]);
-      }
+    for (int v = 0; v < VEC; ++v) x[v] = act_fwd(fmaf(x[v], sc[v], sf[v]), act, alpha);
+    st_vec<T, VEC>(Yb + (int64_t)r * yld, x);
   }
 }
 

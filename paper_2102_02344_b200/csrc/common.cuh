@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <type_traits>
 #include <string>
 
 #include "../../include/hfta.h"
@@ -45,21 +46,37 @@ template <> struct Cvt<__nv_bfloat16> {
 template <typename T> __device__ __forceinline__ float ldf(const T* p) { return Cvt<T>::to_f(*p); }
 template <typename T> __device__ __forceinline__ void stf(T* p, float v) { *p = Cvt<T>::from_f(v); }
 
+// bf16x2 <-> 2 x fp32 in registers (bit operations: no byte-addressed
+// temporaries, which the compiler would place in local memory).
+__device__ __forceinline__ void unpack_bf2(uint32_t w, float& lo, float& hi) {
+  lo = __uint_as_float(w << 16);
+  hi = __uint_as_float(w & 0xffff0000u);
+}
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 // Vector of VEC elements of T loaded/stored as one (or a few) wide accesses.
 template <typename T, int VEC>
 __device__ __forceinline__ void ld_vec(const T* p, float (&v)[VEC]) {
   if constexpr (VEC == 1) {
     v[0] = Cvt<T>::to_f(*p);
-  } else if constexpr (sizeof(T) * VEC == 16) {
-    uint4 u = *reinterpret_cast<const uint4*>(p);
-    const T* e = reinterpret_cast<const T*>(&u);
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) v[i] = Cvt<T>::to_f(e[i]);
-  } else if constexpr (sizeof(T) * VEC == 8) {
-    uint2 u = *reinterpret_cast<const uint2*>(p);
-    const T* e = reinterpret_cast<const T*>(&u);
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) v[i] = Cvt<T>::to_f(e[i]);
+  } else if constexpr (std::is_same<T, __nv_bfloat16>::value && VEC == 8) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    unpack_bf2(u.x, v[0], v[1]); unpack_bf2(u.y, v[2], v[3]); unpack_bf2(u.z, v[4], v[5]); unpack_bf2(u.w, v[6], v[7]);
+  } else if constexpr (std::is_same<T, __nv_bfloat16>::value && VEC == 4) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    unpack_bf2(u.x, v[0], v[1]); unpack_bf2(u.y, v[2], v[3]);
+  } else if constexpr (std::is_same<T, __nv_bfloat16>::value && VEC == 2) {
+    unpack_bf2(*reinterpret_cast<const uint32_t*>(p), v[0], v[1]);
+  } else if constexpr (std::is_same<T, float>::value && VEC == 4) {
+    const float4 u = *reinterpret_cast<const float4*>(p);
+    v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+  } else if constexpr (std::is_same<T, float>::value && VEC == 2) {
+    const float2 u = *reinterpret_cast<const float2*>(p);
+    v[0] = u.x; v[1] = u.y;
   } else {
 #pragma unroll
     for (int i = 0; i < VEC; ++i) v[i] = Cvt<T>::to_f(p[i]);
@@ -70,18 +87,17 @@ template <typename T, int VEC>
 __device__ __forceinline__ void st_vec(T* p, const float (&v)[VEC]) {
   if constexpr (VEC == 1) {
     *p = Cvt<T>::from_f(v[0]);
-  } else if constexpr (sizeof(T) * VEC == 16) {
-    uint4 u;
-    T* e = reinterpret_cast<T*>(&u);
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) e[i] = Cvt<T>::from_f(v[i]);
-    *reinterpret_cast<uint4*>(p) = u;
-  } else if constexpr (sizeof(T) * VEC == 8) {
-    uint2 u;
-    T* e = reinterpret_cast<T*>(&u);
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) e[i] = Cvt<T>::from_f(v[i]);
-    *reinterpret_cast<uint2*>(p) = u;
+  } else if constexpr (std::is_same<T, __nv_bfloat16>::value && VEC == 8) {
+    *reinterpret_cast<uint4*>(p) =
+        make_uint4(pack_bf2(v[0], v[1]), pack_bf2(v[2], v[3]), pack_bf2(v[4], v[5]), pack_bf2(v[6], v[7]));
+  } else if constexpr (std::is_same<T, __nv_bfloat16>::value && VEC == 4) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf2(v[0], v[1]), pack_bf2(v[2], v[3]));
+  } else if constexpr (std::is_same<T, __nv_bfloat16>::value && VEC == 2) {
+    *reinterpret_cast<uint32_t*>(p) = pack_bf2(v[0], v[1]);
+  } else if constexpr (std::is_same<T, float>::value && VEC == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (std::is_same<T, float>::value && VEC == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
   } else {
 #pragma unroll
     for (int i = 0; i < VEC; ++i) p[i] = Cvt<T>::from_f(v[i]);

@@ -167,7 +167,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int bb_ = p.b_shared ? 0 : (int)(r / p.splits);
         const int64_t key = (int64_t)bb_ * p.tiles_n + nt_;
         if (key != bkey) {
-          if (bkey >= 0 && lane == 0) tc_commit(bempty);   // old B free once all prior MMAs retire
+          if (bkey >= 0) tc_commit_w(bempty);   // old B free once all prior MMAs retire
           __syncwarp();
           mbar_wait(bfull, epoch & 1);
           bkey = key;
@@ -183,19 +183,20 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (lane == 0) {
+        {
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sb = BRES ? smem_u32(bres + kb * B_BYTES) : sa + A_BYTES;
+          const uint64_t ad0 = A_MN ? smem_desc(sa, 8192, 1024) : smem_desc(sa, 16, 1024);
+          const uint64_t bd0 = B_MN ? smem_desc(sb, 8192, 1024) : smem_desc(sb, 16, 1024);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // K-major: +32 B per 16-element k step inside the 128-B swizzle row;
-            // MN-major: +16 rows x 128 B.
-            const uint64_t ad = A_MN ? smem_desc(sa + k * 2048, 8192, 1024) : smem_desc(sa + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? smem_desc(sb + k * 2048, 8192, 1024) : smem_desc(sb + k * 32, 16, 1024);
-            tc_mma_bf16(d_tmem, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+            // MN-major: +16 rows x 128 B (descriptor address unit: 16 B).
+            tc_mma_ss(d_tmem, ad0 + (uint64_t)(A_MN ? k * 128 : k * 2), bd0 + (uint64_t)(B_MN ? k * 128 : k * 2), IDESC,
+                      (kb | k) != 0 ? 1u : 0u);
           }
-          tc_commit(&empty[stage]);                  // smem slot free once these MMAs retire
-          if (kb == nkb - 1) tc_commit(&tfull[acc]);   // accumulator ready
+          tc_commit_w(&empty[stage]);                  // smem slot free once these MMAs retire
+          if (kb == nkb - 1) tc_commit_w(&tfull[acc]);   // accumulator ready
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -268,7 +269,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             v[4 * q] += t4.x; v[4 * q + 1] += t4.y; v[4 * q + 2] += t4.z; v[4 * q + 3] += t4.w;
           }
         } else if (brow) {
-          for (int q = 0; q < 64 && n0 + q < p.N; ++q) v[q] += brow[n0 + q];
+#pragma unroll
+          for (int q = 0; q < 64; ++q)
+            if (n0 + q < p.N) v[q] += brow[n0 + q];
         }
         if constexpr (!OUT_F32) {
           // bf16: stage the warp's 32 x 64 sub-tile (128-B rows, TMA SWIZZLE_128B layout:
@@ -297,20 +300,23 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           for (int hh = 0; hh < 2; ++hh) {
             const int64_t c0 = n0 + hh * 32;
             if (c0 >= p.N) break;
-            const float* vv = v + hh * 32;
             const bool full_chunk = c0 + 32 <= p.N;
             float* dst = p.splits > 1 ? p.part + (((int64_t)split * p.B + b) * p.M + m) * p.N + c0
                                       : reinterpret_cast<float*>(p.C) + (int64_t)b * p.c_bs + m * p.c_ld + c0;
             const bool vec_ok = full_chunk && (p.splits > 1 ? (p.N % 4 == 0) : true);
             if (p.splits == 1 && p.accumulate) {
-              for (int q = 0; q < 32 && c0 + q < p.N; ++q) dst[q] += vv[q];
+#pragma unroll
+              for (int q = 0; q < 32; ++q)
+                if (c0 + q < p.N) dst[q] += v[hh * 32 + q];
             } else if (vec_ok) {
 #pragma unroll
               for (int q = 0; q < 8; ++q)
                 *reinterpret_cast<float4*>(dst + 4 * q) =
-                    make_float4(vv[4 * q], vv[4 * q + 1], vv[4 * q + 2], vv[4 * q + 3]);
+                    make_float4(v[hh * 32 + 4 * q], v[hh * 32 + 4 * q + 1], v[hh * 32 + 4 * q + 2], v[hh * 32 + 4 * q + 3]);
             } else {
-              for (int q = 0; q < 32 && c0 + q < p.N; ++q) dst[q] = vv[q];
+#pragma unroll
+              for (int q = 0; q < 32; ++q)
+                if (c0 + q < p.N) dst[q] = v[hh * 32 + q];
             }
           }
         }

@@ -229,7 +229,7 @@ k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     for (int64_t u = u0; u < u1; ++u) {
       const int b = (int)(u / p.Ncl);
       if (b != curb) {
-        if (curb >= 0 && lane == 0) tc_commit(wempty);
+        if (curb >= 0) tc_commit_w(wempty);
         __syncwarp();
         mbar_wait(wfull, wep & 1);
         curb = b;
@@ -239,20 +239,20 @@ k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         mbar_wait(&tempty[acc], aph ^ 1);
         mbar_wait(&full[stage], ph);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sa = smem_u32(ast + stage * 2 * FA_KB);
+        {
+          const uint64_t bd0 = smem_desc(smem_u32(ast + stage * 2 * FA_KB), 16, 1024);
           for (int j = 0; j < nb; ++j) {
             const uint32_t d = tmem_base + (uint32_t)(acc * FG * FR + j * FR);
-            const uint32_t sw = smem_u32(wres + j * 2 * WKB);
+            const uint64_t ad0 = smem_desc(smem_u32(wres + j * 2 * WKB), 16, 1024);
             for (int kb = 0; kb < p.nkb; ++kb) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                tc_mma_bf16(d, smem_desc(sw + kb * WKB + k * 32, 16, 1024), smem_desc(sa + kb * FA_KB + k * 32, 16, 1024),
-                            IDESC, (kb | k) != 0 ? 1u : 0u);
+              for (int k = 0; k < 4; ++k)   // +32 B per k step, +WKB / FA_KB per k block (descriptor units of 16 B)
+                tc_mma_ss(d, ad0 + (uint64_t)(kb * (WKB >> 4) + 2 * k), bd0 + (uint64_t)(kb * (FA_KB >> 4) + 2 * k), IDESC,
+                          (kb | k) != 0 ? 1u : 0u);
             }
           }
-          tc_commit(&empty[stage]);
-          tc_commit(&tfull[acc]);
+          tc_commit_w(&empty[stage]);
+          tc_commit_w(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == FSTAGES) { stage = 0; ph ^= 1; }
@@ -471,34 +471,79 @@ struct BwdArgs {
   float* part;                                  // wgrad split partials [S][B][C][K]
 };
 
+// Per-thread operands of one transform (channel c, points r0h..r0h+63):
+// the affine coefficients and the argmax rows of the (at most two) clouds
+// overlapping the points.  Loaded BEFORE the wait for the recomputed tile so
+// their global-load latency overlaps it.
+struct BwdPre {
+  float bx, cc, v0, v1;
+  int a0, a1;            // argmax point index within cloud n0 / n0 + 1 (-1: none)
+  int n0, slow;          // slow: more than two clouds overlap (L < 64)
+};
+
+__device__ __forceinline__ BwdPre bwd_prefetch(const BwdArgs& p, int b, int64_t c, int64_t r0h) {
+  BwdPre q;
+  const float2 cf = p.coef[(int64_t)b * p.C + c];
+  q.bx = cf.x;
+  q.cc = cf.y;
+  q.a0 = q.a1 = -1;
+  q.v0 = q.v1 = 0.f;
+  q.slow = 0;
+  q.n0 = 0;
+  if (r0h < p.R) {
+    const int L = (int)p.L;
+    const int n_lo = (int)r0h / L;
+    const int n_hi = min(p.Ncl - 1, ((int)r0h + 63) / L);
+    q.n0 = n_lo;
+    if (n_hi - n_lo > 1) {
+      q.slow = 1;
+    } else {
+      const int32_t* am = p.am + (int64_t)b * p.am_bs + c;
+      const float* pv = p.pv + (int64_t)b * p.Ncl * p.C + c;
+      q.a0 = am[(int64_t)n_lo * p.am_ld];
+      q.v0 = pv[(int64_t)n_lo * p.C];
+      if (n_hi > n_lo) {
+        q.a1 = am[(int64_t)n_hi * p.am_ld];
+        q.v1 = pv[(int64_t)n_hi * p.C];
+      }
+    }
+  }
+  return q;
+}
+
+__device__ __forceinline__ void patch_u16(uint32_t rowaddr, uint32_t sw, int64_t j, float v) {
+  if (j >= 0 && j < 64) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    st_shared_u16(rowaddr + ((((uint32_t)j >> 3) ^ sw) << 4) + ((uint32_t)j & 7) * 2,
+                  *reinterpret_cast<const unsigned short*>(&h));
+  }
+}
+
 // Transform one thread's 64 recomputed Y^T values (channel c, points
 // r0h..r0h+63) into bf16 dY in the dY^T sub-tile row (SW128 layout: 16-B chunk
-// q of row cl at q ^ (cl & 7)), then patch the argmax rows of the clouds that
-// overlap the points.
-__device__ __forceinline__ void bwd_transform(const uint32_t (&u)[64], const BwdArgs& p, int b, int64_t c,
-                                              int64_t r0h, uint32_t rowaddr, uint32_t sw) {
-  const float2 cf = p.coef[(int64_t)b * p.C + c];
+// q of row cl at q ^ (cl & 7)), then patch the argmax rows.
+__device__ __forceinline__ void bwd_transform(const uint32_t (&u)[64], const BwdPre& q, const BwdArgs& p, int b,
+                                              int64_t c, int64_t r0h, uint32_t rowaddr, uint32_t sw) {
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int k = 0; k < 8; ++k) {
     uint4 w4;
     __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w4);
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      h[e] = __floats2bfloat162_rn(fmaf(cf.x, __uint_as_float(u[8 * q + 2 * e]), cf.y),
-                                   fmaf(cf.x, __uint_as_float(u[8 * q + 2 * e + 1]), cf.y));
-    st_shared_v4(rowaddr + (((uint32_t)q ^ sw) << 4), w4);
+      h[e] = __floats2bfloat162_rn(fmaf(q.bx, __uint_as_float(u[8 * k + 2 * e]), q.cc),
+                                   fmaf(q.bx, __uint_as_float(u[8 * k + 2 * e + 1]), q.cc));
+    st_shared_v4(rowaddr + (((uint32_t)k ^ sw) << 4), w4);
   }
   if (r0h >= p.R) return;
-  const int n_lo = (int)(r0h / p.L);
+  if (!q.slow) {
+    if (q.a0 >= 0) patch_u16(rowaddr, sw, (int64_t)q.n0 * p.L + q.a0 - r0h, q.v0);
+    if (q.a1 >= 0) patch_u16(rowaddr, sw, (int64_t)(q.n0 + 1) * p.L + q.a1 - r0h, q.v1);
+    return;
+  }
   const int n_hi = (int)min((int64_t)p.Ncl - 1, (r0h + 63) / p.L);
-  for (int n = n_lo; n <= n_hi; ++n) {
+  for (int n = q.n0; n <= n_hi; ++n) {
     const int64_t row = (int64_t)n * p.L + p.am[(int64_t)b * p.am_bs + (int64_t)n * p.am_ld + c];
-    const int64_t j = row - r0h;
-    if (j >= 0 && j < 64) {
-      const __nv_bfloat16 v = __float2bfloat16_rn(p.pv[((int64_t)b * p.Ncl + n) * p.C + c]);
-      st_shared_u16(rowaddr + ((((uint32_t)j >> 3) ^ sw) << 4) + ((uint32_t)j & 7) * 2,
-                    *reinterpret_cast<const unsigned short*>(&v));
-    }
+    patch_u16(rowaddr, sw, row - r0h, p.pv[((int64_t)b * p.Ncl + n) * p.C + c]);
   }
 }
 
@@ -586,17 +631,17 @@ k_lbm_dgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           mbar_wait(&w_full[ws], wph);
           mbar_wait(&y_empty[yb], yph ^ 1);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t sw = smem_u32(wst + ws * 2 * WKB);
+          {
+            const uint64_t ad0 = smem_desc(smem_u32(wst + ws * 2 * WKB), 16, 1024), bd0 = smem_desc(sa, 16, 1024);
             const uint32_t d = tmem_base + (uint32_t)(yb * 128);
             for (int kb = 0; kb < p.nkb; ++kb) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                tc_mma_bf16(d, smem_desc(sw + kb * WKB + k * 32, 16, 1024), smem_desc(sa + kb * BA_KB + k * 32, 16, 1024),
-                            idesc_y, (kb | k) != 0 ? 1u : 0u);
+                tc_mma_ss(d, ad0 + (uint64_t)(kb * (WKB >> 4) + 2 * k), bd0 + (uint64_t)(kb * (BA_KB >> 4) + 2 * k), idesc_y,
+                          (kb | k) != 0 ? 1u : 0u);
             }
-            tc_commit(&y_full[yb]);
-            if (cb == p.nblk - 1) tc_commit(&a_empty[ab]);
+            tc_commit_w(&y_full[yb]);
+            if (cb == p.nblk - 1) tc_commit_w(&a_empty[ab]);
           }
           __syncwarp();
           if (++yb == 2) { yb = 0; yph ^= 1; }
@@ -604,16 +649,15 @@ k_lbm_dgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         if (cb > 0) {                                   // dX += dY[cb-1] W[cb-1]
           mbar_wait(&dy_full[dyb], dyph);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t sd = smem_u32(dyt + dyb * DY_BYTES);
-            const uint32_t sw = smem_u32(wst + pws * 2 * WKB);
+          {
+            const uint64_t ad0 = smem_desc(smem_u32(dyt + dyb * DY_BYTES), CBLK * 128, 1024);
+            const uint64_t bd0 = smem_desc(smem_u32(wst + pws * 2 * WKB), WKB, 1024);
 #pragma unroll
-            for (int k = 0; k < CBLK / 16; ++k)
-              tc_mma_bf16(dacc, smem_desc(sd + k * 2048, CBLK * 128, 1024), smem_desc(sw + k * 2048, WKB, 1024),
-                          idesc_d, (cb > 1 || k > 0) ? 1u : 0u);
-            tc_commit(&dy_empty[dyb]);
-            tc_commit(&w_empty[pws]);
-            if (cb == p.nblk) tc_commit(&d_full[db]);
+            for (int k = 0; k < CBLK / 16; ++k)   // MN-major: +16 rows x 128 B per k step
+              tc_mma_ss(dacc, ad0 + (uint64_t)(k * 128), bd0 + (uint64_t)(k * 128), idesc_d, (cb > 1 || k > 0) ? 1u : 0u);
+            tc_commit_w(&dy_empty[dyb]);
+            tc_commit_w(&w_empty[pws]);
+            if (cb == p.nblk) tc_commit_w(&d_full[db]);
           }
           __syncwarp();
           if (++dyb == 2) { dyb = 0; dyph ^= 1; }
@@ -637,6 +681,7 @@ k_lbm_dgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       const int64_t r0 = (t % p.tiles) * BR;
       for (int cb = 0; cb < p.nblk; ++cb) {
         uint32_t u[64];
+        const BwdPre pre = bwd_prefetch(p, b, (int64_t)cb * CBLK + cl, r0 + half * 64);
         mbar_wait(&y_full[yb], yph);
         tc_fence_after();
         ld64(tmem_base + (uint32_t)(yb * 128 + half * 64) + ((uint32_t)(quarter * 32) << 16), u);
@@ -646,7 +691,7 @@ k_lbm_dgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         if (++yb == 2) { yb = 0; yph ^= 1; }
         mbar_wait(&dy_empty[dyb], dyph ^ 1);
         const uint32_t rowaddr = smem_u32(dyt + dyb * DY_BYTES + half * (CBLK * 128)) + cl * 128;
-        bwd_transform(u, p, b, (int64_t)cb * CBLK + cl, r0 + half * 64, rowaddr, sw);
+        bwd_transform(u, pre, p, b, (int64_t)cb * CBLK + cl, r0 + half * 64, rowaddr, sw);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&dy_full[dyb]);
@@ -785,16 +830,16 @@ k_lbm_wgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           mbar_wait(&a_full[st], ph);
           mbar_wait(&y_empty[yb], yph ^ 1);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t sa = smem_u32(ast + st * 2 * BA_KB);
+          {
+            const uint64_t ad0 = smem_desc(sw, 16, 1024), bd0 = smem_desc(smem_u32(ast + st * 2 * BA_KB), 16, 1024);
             const uint32_t d = tmem_base + (uint32_t)(yb * 128);
             for (int kb = 0; kb < p.nkb; ++kb) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                tc_mma_bf16(d, smem_desc(sw + kb * WKB + k * 32, 16, 1024), smem_desc(sa + kb * BA_KB + k * 32, 16, 1024),
-                            idesc_y, (kb | k) != 0 ? 1u : 0u);
+                tc_mma_ss(d, ad0 + (uint64_t)(kb * (WKB >> 4) + 2 * k), bd0 + (uint64_t)(kb * (BA_KB >> 4) + 2 * k), idesc_y,
+                          (kb | k) != 0 ? 1u : 0u);
             }
-            tc_commit(&y_full[yb]);
+            tc_commit_w(&y_full[yb]);
           }
           __syncwarp();
           if (++yb == 2) { yb = 0; yph ^= 1; }
@@ -802,21 +847,20 @@ k_lbm_wgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         if (j > 0) {                                    // dW += dY^T[j-1] X[j-1]
           mbar_wait(&dy_full[dyb], dyph);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t sd = smem_u32(dyt + dyb * DY_BYTES);
-            const uint32_t sa = smem_u32(ast + pst * 2 * BA_KB);
+          {
+            const uint64_t ad0 = smem_desc(smem_u32(dyt + dyb * DY_BYTES), 16, 1024);
+            const uint64_t bd0 = smem_desc(smem_u32(ast + pst * 2 * BA_KB), BA_KB, 1024);
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                tc_mma_bf16(dacc, smem_desc(sd + h * (CBLK * 128) + k * 32, 16, 1024),
-                            smem_desc(sa + (h * 64 + k * 16) * 128, BA_KB, 1024), idesc_w,
-                            (j > 1 || h > 0 || k > 0) ? 1u : 0u);
-            tc_commit(&dy_empty[dyb]);
-            tc_commit(&a_empty[pst]);
+              for (int k = 0; k < 4; ++k)   // A: K-major +32 B per k step; B: MN-major +16 rows x 128 B
+                tc_mma_ss(dacc, ad0 + (uint64_t)(h * (CBLK * 128 >> 4) + 2 * k), bd0 + (uint64_t)((h * 64 + k * 16) * 8),
+                          idesc_w, (j > 1 || h > 0 || k > 0) ? 1u : 0u);
+            tc_commit_w(&dy_empty[dyb]);
+            tc_commit_w(&a_empty[pst]);
             if (j == nch) {
-              tc_commit(&d_full[db]);
-              tc_commit(w_empty);
+              tc_commit_w(&d_full[db]);
+              tc_commit_w(w_empty);
             }
           }
           __syncwarp();
@@ -827,7 +871,10 @@ k_lbm_wgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           if (++st == WG_AST) { st = 0; ph ^= 1; }
         }
       }
-      if (nch == 0 && lane == 0) { mbar_arrive(&d_full[db]); tc_commit(w_empty); }
+      if (nch == 0) {
+        if (lane == 0) mbar_arrive(&d_full[db]);
+        tc_commit_w(w_empty);
+      }
       __syncwarp();
       if (++db == 2) { db = 0; dph ^= 1; }
     }
@@ -844,6 +891,7 @@ k_lbm_wgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       const int64_t c = (int64_t)cb * CBLK + cl;
       for (int j = 0; j < nch; ++j) {
         uint32_t u[64];
+        const BwdPre pre = bwd_prefetch(p, b, c, rbeg + (int64_t)j * BR + half * 64);
         mbar_wait(&y_full[yb], yph);
         tc_fence_after();
         ld64(tmem_base + (uint32_t)(yb * 128 + half * 64) + ((uint32_t)(quarter * 32) << 16), u);
@@ -853,7 +901,7 @@ k_lbm_wgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         if (++yb == 2) { yb = 0; yph ^= 1; }
         mbar_wait(&dy_empty[dyb], dyph ^ 1);
         const uint32_t rowaddr = smem_u32(dyt + dyb * DY_BYTES + half * (CBLK * 128)) + cl * 128;
-        bwd_transform(u, p, b, c, rbeg + (int64_t)j * BR + half * 64, rowaddr, sw);
+        bwd_transform(u, pre, p, b, c, rbeg + (int64_t)j * BR + half * 64, rowaddr, sw);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&dy_full[dyb]);
