@@ -249,12 +249,15 @@ hfta_status hfta_fused_linear_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C,
                                          void* ws, size_t ws_bytes, hfta_stream stream);
 /*
  * Backward: dG fp32 [B][N][C] -> dZ at the argmax rows (act' at the pooled
- * pre-activation), BN backward dY = gamma*invstd/R*(R*dZ - dbeta - xhat*dgamma)
- * (dense), dX = dY W (bf16, skipped if dX.ptr is NULL), dW = dY^T X (fp32 at
+ * pre-activation), BN backward dY = gamma*invstd/R*(R*dZ - dbeta - xhat*dgamma),
+ * dX = dY W (bf16, skipped if dX.ptr is NULL), dW = dY^T X (fp32 at
  * dW[b*dW_bstride + c*dW_ld + k]), dgamma/dbeta fp32, dbias (may be NULL)
- * written as exact zeros (BN-absorbed).  accumulate != 0 adds to
- * dW/dgamma/dbeta instead of overwriting.  ext/argmax/save_* are the forward's
- * outputs.
+ * written as exact zeros (BN-absorbed).  dY = bx*Y + cc + S (S:
+ * one nonzero per cloud and channel) is never formed: dX = X M + 1 v^T + S W
+ * and dW = diag(bx) W G + cc s^T + S^T X with M = W^T diag(bx) W (rounded to
+ * bf16), v = W^T cc, G = X^T X, s = X^T 1 (K10).  accumulate != 0
+ * adds to dW/dgamma/dbeta instead of overwriting.  ext/argmax/save_* are the
+ * forward's outputs.  C <= 1024.
  */
 hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C, int64_t K,
                                          hfta_dtype dt, hfta_in dG, hfta_in X, hfta_in W,

@@ -101,26 +101,50 @@ __global__ void k_dropout(int64_t rows, int64_t cols, const T* __restrict__ X, i
 }
 
 // ------------------------------------------------------------- colsum --
-// grid (cdiv(C,32), ngroups*cpg, B), block (32, 8): partial sums per chunk.
-template <typename T>
-__global__ void k_colsum_part(int64_t C, int64_t group, int cpg, int64_t rpc, const T* __restrict__ X, int64_t xbs,
-                              int64_t xld, float* __restrict__ part) {
-  __shared__ float red[8][33];
+// grid (cdiv(C, tpr*VEC), ngroups*cpg, B), 256 threads = tpr column lanes x
+// (256/tpr) row lanes; each thread sums VEC adjacent columns (one 16-B load
+// per row for bf16 VEC=8), then a shared-memory reduction over the row lanes.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) k_colsum_part(int64_t C, int64_t group, int cpg, int64_t rpc, int tpr,
+                                                     const T* __restrict__ X, int64_t xbs, int64_t xld,
+                                                     float* __restrict__ part) {
+  __shared__ float red[256 * VEC];
   const int b = blockIdx.z;
   const int64_t chunk = blockIdx.y;
   const int64_t g = chunk / cpg, j = chunk % cpg;
-  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int lane = threadIdx.x % tpr, rl = threadIdx.x / tpr, rpb = 256 / tpr;
+  const int64_t cbase = (int64_t)blockIdx.x * tpr * VEC;
+  const int64_t c0 = cbase + (int64_t)lane * VEC;
   const int64_t r0 = g * group + j * rpc;
   const int64_t r1 = min((g + 1) * group, r0 + rpc);
-  float acc = 0.f;
-  if (c < C)
-    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) acc += ldf(X + (int64_t)b * xbs + r * xld + c);
-  red[threadIdx.y][threadIdx.x] = acc;
+  float a0[VEC], a1[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) a0[v] = a1[v] = 0.f;
+  if (c0 < C) {
+    const T* Xb = X + (int64_t)b * xbs + c0;
+    int64_t r = r0 + rl;
+    for (; r + rpb < r1; r += 2 * rpb) {
+      float x0[VEC], x1[VEC];
+      ld_vec<T, VEC>(Xb + r * xld, x0);
+      ld_vec<T, VEC>(Xb + (r + rpb) * xld, x1);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) { a0[v] += x0[v]; a1[v] += x1[v]; }
+    }
+    if (r < r1) {
+      float x0[VEC];
+      ld_vec<T, VEC>(Xb + r * xld, x0);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) a0[v] += x0[v];
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) red[(rl * tpr + lane) * VEC + v] = a0[v] + a1[v];
   __syncthreads();
-  if (threadIdx.y == 0 && c < C) {
-    float s = 0.f;
-    for (int y = 0; y < 8; ++y) s += red[y][threadIdx.x];
-    part[((int64_t)b * gridDim.y + chunk) * C + c] = s;
+  const int t = threadIdx.x;
+  if (t < tpr * VEC && cbase + t < C) {
+    float sum = 0.f;
+    for (int y = 0; y < rpb; ++y) sum += red[(y * tpr + t / VEC) * VEC + t % VEC];
+    part[((int64_t)b * gridDim.y + chunk) * C + cbase + t] = sum;
   }
 }
 
@@ -139,8 +163,8 @@ struct ColsumGeo { int64_t ngroups; int cpg; int64_t rpc; };
 ColsumGeo colsum_geo(int B, int64_t rows, int64_t C, int64_t group) {
   ColsumGeo g;
   g.ngroups = cdiv(rows, group);
-  int64_t blocks_per = cdiv(C, 32) * (int64_t)B * g.ngroups;
-  int64_t target = 4 * (int64_t)std::max(num_sms(), 148);
+  int64_t blocks_per = cdiv(C, 128) * (int64_t)B * g.ngroups;
+  int64_t target = 8 * (int64_t)std::max(num_sms(), 148);
   int64_t cpg = std::max<int64_t>(1, std::min<int64_t>(cdiv(target, blocks_per), cdiv(group, 256)));
   g.rpc = cdiv(group, cpg);
   g.cpg = (int)cdiv(group, g.rpc);
@@ -187,12 +211,27 @@ hfta_status colsum_impl(int B, int64_t rows, int64_t C, int64_t group, hfta_dtyp
   HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "colsum: workspace %zu < %zu", ws_bytes, need);
   ColsumGeo g = colsum_geo(B, rows, C, group);
   float* part = reinterpret_cast<float*>(ws);
-  dim3 grid((unsigned)cdiv(C, 32), (unsigned)(g.ngroups * g.cpg), B);
-  if (dt == HFTA_F32)
-    k_colsum_part<float><<<grid, dim3(32, 8), 0, s>>>(C, group, g.cpg, g.rpc, (const float*)X.ptr, X.bstride, X.ld, part);
-  else
-    k_colsum_part<__nv_bfloat16><<<grid, dim3(32, 8), 0, s>>>(C, group, g.cpg, g.rpc, (const __nv_bfloat16*)X.ptr,
-                                                               X.bstride, X.ld, part);
+  const int esz = dt == HFTA_F32 ? 4 : 2;
+  const int vec = (esz == 2 && C % 8 == 0 && X.ld % 8 == 0 && X.bstride % 8 == 0 && aligned16(X.ptr)) ? 8
+                  : (esz == 4 && C % 4 == 0 && X.ld % 4 == 0 && X.bstride % 4 == 0 && aligned16(X.ptr)) ? 4 : 1;
+  int tpr = 1;
+  while (tpr < 32 && tpr * vec < C) tpr <<= 1;
+  dim3 grid((unsigned)cdiv(C, (int64_t)tpr * vec), (unsigned)(g.ngroups * g.cpg), B);
+  if (dt == HFTA_F32) {
+    if (vec == 4)
+      k_colsum_part<float, 4><<<grid, 256, 0, s>>>(C, group, g.cpg, g.rpc, tpr, (const float*)X.ptr, X.bstride, X.ld,
+                                                   part);
+    else
+      k_colsum_part<float, 1><<<grid, 256, 0, s>>>(C, group, g.cpg, g.rpc, tpr, (const float*)X.ptr, X.bstride, X.ld,
+                                                   part);
+  } else {
+    if (vec == 8)
+      k_colsum_part<__nv_bfloat16, 8><<<grid, 256, 0, s>>>(C, group, g.cpg, g.rpc, tpr, (const __nv_bfloat16*)X.ptr,
+                                                           X.bstride, X.ld, part);
+    else
+      k_colsum_part<__nv_bfloat16, 1><<<grid, 256, 0, s>>>(C, group, g.cpg, g.rpc, tpr, (const __nv_bfloat16*)X.ptr,
+                                                           X.bstride, X.ld, part);
+  }
   int64_t tot = (int64_t)B * g.ngroups * C;
   k_colsum_fin<<<(unsigned)cdiv(tot, 256), 256, 0, s>>>(B, C, g.ngroups, g.cpg, part, S, S_bstride, accumulate);
   count_launches(2);

@@ -31,6 +31,9 @@
 // Roles per CTA (320 threads, 1 CTA/SM, persistent): warp 0 TMA producer,
 // warp 1 single-thread MMA issuer, warps 2..9 epilogue / transform (two per
 // TMEM lane quarter).
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
+
 #include "tc_common.cuh"
 
 namespace hfta {
@@ -48,12 +51,6 @@ constexpr int NBW = FG / 2;                    // channel blocks per epilogue wa
 constexpr int LPB = FR / 32;                   // 32-column TMEM loads per block and chunk
 static_assert(NBW * LPB == 4, "epilogue load schedule assumes 4 loads per warp and chunk");
 constexpr uint32_t FA_KB = FR * 64 * 2;        // 8 KB per k block of an X chunk
-// backward
-constexpr int BR = 128;                        // points per tile / chunk
-constexpr uint32_t BA_KB = BR * 64 * 2;        // 16 KB per k block of an X tile
-constexpr uint32_t DY_BYTES = 2 * CBLK * 64 * 2;   // dY^T tile [128 c][128 r] as two [128][64] sub-tiles
-constexpr int DG_WST = 3;                      // dgrad: W block stages
-constexpr int WG_AST = 3;                      // wgrad: X chunk stages
 
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
@@ -63,20 +60,12 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
-__device__ __forceinline__ void st_shared_u16(uint32_t addr, unsigned short v) {
-  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
-}
 __device__ __forceinline__ void tmem_alloc512(uint32_t* slot) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
 }
 __device__ __forceinline__ void tmem_free512(uint32_t base) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base));
-}
-__device__ __forceinline__ void ld64(uint32_t ta, uint32_t (&u)[64]) {
-  tmem_ld32_nowait(ta, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
-  tmem_ld32_nowait(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
-  tmem_wait_ld();
 }
 
 // ================================================================ forward ==
@@ -421,15 +410,28 @@ __global__ void k_lbm_fwd_fin(int B, int Ncl, int64_t L, int64_t C, const float*
 }
 
 // =============================================================== backward ==
+//
+// With dZ nonzero only at the argmax rows, the BN backward is
+//   dY[r][c] = bx_c Y[r][c] + cc_c + S[r][c],   S = a_c dz at r = argmax(n, c),
+// an affine map of Y = X W^T plus a sparse matrix, so both contractions
+// collapse onto K x K quantities of the layer input (K = 128 << C = 1024):
+//   dX = dY W   = X M + 1 v^T + S W,       M = W^T diag(bx) W,  v = W^T cc
+//   dW = dY^T X = diag(bx) W G + cc s^T + S^T X,   G = X^T X,  s = X^T 1
+// (exact algebra; only the rounding order differs from forming dY).  The
+// dense parts are one Gram contraction over the R points (tensor cores,
+// hfta_fused_linear_bwd's wgrad path) and one R x K x K GEMM (dX = X M^T + v,
+// M symmetric); the sparse parts touch one row per (cloud, channel).  No
+// [R][C] tensor is formed, no Y is recomputed: the backward reads X once for
+// G/s, once for dX, and writes dX -- HBM-bound.
 
-// Per (model, channel): dz at the pooled rows, dgamma/dbeta, and the affine
-// form dY = bx*Y + cc (+ a*dz at the argmax row; pv = the full value there).
+// Per (model, channel): dz at the pooled rows, dgamma/dbeta, the affine
+// coefficients (bx, cc) of dY and the sparse values sp = a*dz.
 __global__ void k_lbm_bwd_coef(int B, int Ncl, int64_t L, int64_t C, const float* __restrict__ dG, int64_t dg_bs,
                                int64_t dg_ld, const float* __restrict__ ext, int64_t ext_bs, int64_t ext_ld,
                                const float* __restrict__ bias, int64_t bias_bs, const float* __restrict__ gamma,
                                const float* __restrict__ beta, int64_t gbs, const float* __restrict__ smean,
                                const float* __restrict__ sinv, int act, float alpha, float2* __restrict__ coef,
-                               float* __restrict__ pv, float* __restrict__ dgamma, float* __restrict__ dbeta,
+                               float* __restrict__ sp, float* __restrict__ dgamma, float* __restrict__ dbeta,
                                float* __restrict__ dbias, int64_t dbias_bs, int accumulate) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)B * C) return;
@@ -437,558 +439,278 @@ __global__ void k_lbm_bwd_coef(int B, int Ncl, int64_t L, int64_t C, const float
   const float ga = gamma[b * gbs + c], be = beta[b * gbs + c];
   const float mb = smean[i], inv = sinv[i];
   const float bi = bias ? bias[b * bias_bs + c] : 0.f;
+  const double a = (double)ga * inv;
   double dbe = 0.0, dga = 0.0;
   for (int n = 0; n < Ncl; ++n) {
     const float xh = (ext[b * ext_bs + n * ext_ld + c] - mb) * inv;
     const float dz = dG[b * dg_bs + n * dg_ld + c] * act_grad(ga * xh + be, act, alpha);
     dbe += dz;
     dga += (double)dz * xh;
+    sp[(b * Ncl + n) * C + c] = (float)(a * dz);
   }
   const double R = (double)Ncl * (double)L;
-  const double a = (double)ga * inv;
   const double bx = -a * inv * dga / R;
-  const double cc = -a * dbe / R - bx * ((double)mb - (double)bi);
+  const double cc = -a * dbe / R - bx * ((double)mb - (double)bi);   // affine in Y without its bias
   coef[i] = make_float2((float)bx, (float)cc);
-  for (int n = 0; n < Ncl; ++n) {
-    const float e = ext[b * ext_bs + n * ext_ld + c];
-    const float xh = (e - mb) * inv;
-    const float dz = dG[b * dg_bs + n * dg_ld + c] * act_grad(ga * xh + be, act, alpha);
-    pv[(b * Ncl + n) * C + c] = (float)(a * dz + bx * ((double)e - (double)bi) + cc);
-  }
   const int64_t go = b * gbs + c;
   if (accumulate) { dgamma[go] += (float)dga; dbeta[go] += (float)dbe; }
   else { dgamma[go] = (float)dga; dbeta[go] = (float)dbe; }
   if (dbias && !accumulate) dbias[b * dbias_bs + c] = 0.f;   // BN-absorbed bias: exact zero
 }
 
-struct BwdArgs {
-  int B, Ncl, nblk, nkb, a_shared, splits;
-  int64_t L, C, R, K, tiles, rps;
-  const float2* coef; const float* pv;          // [B][C], [B][Ncl][C]
-  const int32_t* am; int64_t am_bs, am_ld;      // argmax (point index within its cloud)
-  __nv_bfloat16* dX; int64_t dx_bs, dx_ld;      // dgrad output
-  float* dW; int64_t dw_bs, dw_ld; int accumulate;
-  float* part;                                  // wgrad split partials [S][B][C][K]
-};
-
-// Per-thread operands of one transform (channel c, points r0h..r0h+63):
-// the affine coefficients and the argmax rows of the (at most two) clouds
-// overlapping the points.  Loaded BEFORE the wait for the recomputed tile so
-// their global-load latency overlaps it.
-struct BwdPre {
-  float bx, cc, v0, v1;
-  int a0, a1;            // argmax point index within cloud n0 / n0 + 1 (-1: none)
-  int n0, slow;          // slow: more than two clouds overlap (L < 64)
-};
-
-__device__ __forceinline__ BwdPre bwd_prefetch(const BwdArgs& p, int b, int64_t c, int64_t r0h) {
-  BwdPre q;
-  const float2 cf = p.coef[(int64_t)b * p.C + c];
-  q.bx = cf.x;
-  q.cc = cf.y;
-  q.a0 = q.a1 = -1;
-  q.v0 = q.v1 = 0.f;
-  q.slow = 0;
-  q.n0 = 0;
-  if (r0h < p.R) {
-    const int L = (int)p.L;
-    const int n_lo = (int)r0h / L;
-    const int n_hi = min(p.Ncl - 1, ((int)r0h + 63) / L);
-    q.n0 = n_lo;
-    if (n_hi - n_lo > 1) {
-      q.slow = 1;
-    } else {
-      const int32_t* am = p.am + (int64_t)b * p.am_bs + c;
-      const float* pv = p.pv + (int64_t)b * p.Ncl * p.C + c;
-      q.a0 = am[(int64_t)n_lo * p.am_ld];
-      q.v0 = pv[(int64_t)n_lo * p.C];
-      if (n_hi > n_lo) {
-        q.a1 = am[(int64_t)n_hi * p.am_ld];
-        q.v1 = pv[(int64_t)n_hi * p.C];
+// M[b] = W^T diag(bx) W (bf16, the dX GEMM's weight; symmetric), v[b] = W^T cc.
+// Grid (K/64, B): a CTA owns 64 rows of M; thread = 4 rows x 8 columns
+// register tile; W streamed through smem 32 channels at a time (fp32).
+constexpr int MV_ROWS = 64;
+__global__ void __launch_bounds__(256) k_lbm_mv(int64_t C, int K, const __nv_bfloat16* __restrict__ W, int64_t w_bs,
+                                                int64_t w_ld, const float2* __restrict__ coef,
+                                                __nv_bfloat16* __restrict__ Mout, float* __restrict__ v) {
+  __shared__ __align__(16) float swa[32][128];   // bx_c * W[c][k]
+  __shared__ __align__(16) float swb[32][128];   // W[c][k]
+  __shared__ float scc[32];
+  const int b = blockIdx.y, rbase = blockIdx.x * MV_ROWS;
+  const int t = threadIdx.x;
+  const int ncg = K / 8;                          // column groups of 8
+  const int rg = t / ncg, cg = t % ncg;           // rows rbase + 4 rg .. +3, columns 8 cg .. +7
+  const bool act = rg * 4 < MV_ROWS && rbase + rg * 4 < K;
+  float acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  float vacc = 0.f;
+  const __nv_bfloat16* Wb = W + (int64_t)b * w_bs;
+  for (int64_t c0 = 0; c0 < C; c0 += 32) {
+    __syncthreads();
+    for (int e = t; e < 32 * (K / 8); e += 256) {          // 8 bf16 per load
+      const int q = e / (K / 8), k8 = (e % (K / 8)) * 8;
+      float x[8];
+      ld_vec<__nv_bfloat16, 8>(Wb + (c0 + q) * w_ld + k8, x);
+      const float bx = coef[(int64_t)b * C + c0 + q].x;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { swb[q][k8 + i] = x[i]; swa[q][k8 + i] = x[i] * bx; }
+    }
+    if (t < 32) scc[t] = coef[(int64_t)b * C + c0 + t].y;
+    __syncthreads();
+    if (act) {
+#pragma unroll 4
+      for (int q = 0; q < 32; ++q) {
+        const float4 a4 = *reinterpret_cast<const float4*>(&swa[q][rbase + rg * 4]);
+        const float4 b0 = *reinterpret_cast<const float4*>(&swb[q][cg * 8]);
+        const float4 b1 = *reinterpret_cast<const float4*>(&swb[q][cg * 8 + 4]);
+        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
       }
     }
-  }
-  return q;
-}
-
-__device__ __forceinline__ void patch_u16(uint32_t rowaddr, uint32_t sw, int64_t j, float v) {
-  if (j >= 0 && j < 64) {
-    const __nv_bfloat16 h = __float2bfloat16_rn(v);
-    st_shared_u16(rowaddr + ((((uint32_t)j >> 3) ^ sw) << 4) + ((uint32_t)j & 7) * 2,
-                  *reinterpret_cast<const unsigned short*>(&h));
-  }
-}
-
-// Transform one thread's 64 recomputed Y^T values (channel c, points
-// r0h..r0h+63) into bf16 dY in the dY^T sub-tile row (SW128 layout: 16-B chunk
-// q of row cl at q ^ (cl & 7)), then patch the argmax rows.
-__device__ __forceinline__ void bwd_transform(const uint32_t (&u)[64], const BwdPre& q, const BwdArgs& p, int b,
-                                              int64_t c, int64_t r0h, uint32_t rowaddr, uint32_t sw) {
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    uint4 w4;
-    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w4);
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      h[e] = __floats2bfloat162_rn(fmaf(q.bx, __uint_as_float(u[8 * k + 2 * e]), q.cc),
-                                   fmaf(q.bx, __uint_as_float(u[8 * k + 2 * e + 1]), q.cc));
-    st_shared_v4(rowaddr + (((uint32_t)k ^ sw) << 4), w4);
-  }
-  if (r0h >= p.R) return;
-  if (!q.slow) {
-    if (q.a0 >= 0) patch_u16(rowaddr, sw, (int64_t)q.n0 * p.L + q.a0 - r0h, q.v0);
-    if (q.a1 >= 0) patch_u16(rowaddr, sw, (int64_t)(q.n0 + 1) * p.L + q.a1 - r0h, q.v1);
-    return;
-  }
-  const int n_hi = (int)min((int64_t)p.Ncl - 1, (r0h + 63) / p.L);
-  for (int n = q.n0; n <= n_hi; ++n) {
-    const int64_t row = (int64_t)n * p.L + p.am[(int64_t)b * p.am_bs + (int64_t)n * p.am_ld + c];
-    patch_u16(rowaddr, sw, row - r0h, p.pv[((int64_t)b * p.Ncl + n) * p.C + c]);
-  }
-}
-
-// ---------------------------------------------------------------- dgrad --
-// Unit = (model, 128-point tile).  Per channel block cb: recompute Y^T[cb]
-// (M = 128 channels, N = 128 points, K), transform to dY^T[cb] in smem, then
-// dX_tile += dY[cb] W[cb] (M = 128 points from the MN-major dY^T tile,
-// N = K from the MN-major W block, K = 128 channels).  The recompute of cb+1
-// overlaps the transform of cb.
-__global__ void __launch_bounds__(LT, 1)
-k_lbm_dgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW, BwdArgs p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = align1024(smem_raw);
-  uint8_t* at = smem;                                  // 2 x 2 k blocks x 16 KB
-  uint8_t* wst = at + 2 * 2 * BA_KB;                   // DG_WST x 2 k blocks x 16 KB
-  uint8_t* dyt = wst + DG_WST * 2 * WKB;               // 2 x 32 KB
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(dyt + 2 * DY_BYTES);
-  uint64_t* a_empty = a_full + 2;
-  uint64_t* w_full = a_empty + 2;
-  uint64_t* w_empty = w_full + DG_WST;
-  uint64_t* y_full = w_empty + DG_WST;
-  uint64_t* y_empty = y_full + 2;
-  uint64_t* dy_full = y_empty + 2;
-  uint64_t* dy_empty = dy_full + 2;
-  uint64_t* d_full = dy_empty + 2;
-  uint64_t* d_empty = d_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&a_full[s], 1); mbar_init(&a_empty[s], 1);
-      mbar_init(&y_full[s], 1); mbar_init(&y_empty[s], NEPIW);
-      mbar_init(&dy_full[s], NEPIW); mbar_init(&dy_empty[s], 1);
-      mbar_init(&d_full[s], 1); mbar_init(&d_empty[s], NEPIW);
+    if (blockIdx.x == 0 && t < K) {
+#pragma unroll 4
+      for (int q = 0; q < 32; ++q) vacc = fmaf(swb[q][t], scc[q], vacc);
     }
-    for (int s = 0; s < DG_WST; ++s) { mbar_init(&w_full[s], 1); mbar_init(&w_empty[s], 1); }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
-  if (warp == 1) tmem_alloc512(tmem_slot);
-  tc_fence_before();
+  if (act) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = acc[i][j];
+      st_vec<__nv_bfloat16, 8>(Mout + (int64_t)b * K * K + (int64_t)(rbase + rg * 4 + i) * K + cg * 8, r);
+    }
+  }
+  if (blockIdx.x == 0 && t < K) v[(int64_t)b * K + t] = vacc;
+}
+
+// Sparse part of dX: dX[n*L + l] += sum over channels c with argmax(n, c) = l
+// of sp(n, c) W[c].  One CTA per (model, cloud): a stable radix sort of the
+// channels by argmax row (so each row's channels stay in channel order), a
+// scan of the segment heads, then (segment, 8-column slice) work items spread
+// over all threads; each row is written by exactly one item per slice
+// (deterministic, no atomics).
+constexpr int SDX_T = 256, SDX_ITEMS = 4;   // C <= 1024
+__global__ void __launch_bounds__(SDX_T) k_lbm_sparse_dx(int Ncl, int64_t L, int64_t C, int K, int end_bit,
+                                                         const int32_t* __restrict__ am, const float* __restrict__ sp,
+                                                         const __nv_bfloat16* __restrict__ W, int64_t w_bs,
+                                                         int64_t w_ld, __nv_bfloat16* __restrict__ dX, int64_t dx_bs,
+                                                         int64_t dx_ld) {
+  using Sort = cub::BlockRadixSort<uint32_t, SDX_T, SDX_ITEMS, int>;
+  using Scan = cub::BlockScan<int, SDX_T>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+  } tmp;
+  __shared__ uint32_t srow[SDX_T * SDX_ITEMS];
+  __shared__ int schan[SDX_T * SDX_ITEMS];
+  __shared__ int shead[SDX_T * SDX_ITEMS + 1];
+  __shared__ int snseg;
+  const int b = blockIdx.y, n = blockIdx.x;
+  const int t = threadIdx.x;
+  const uint32_t sentinel = (1u << end_bit) - 1u;
+  uint32_t key[SDX_ITEMS];
+  int val[SDX_ITEMS];
+  const int32_t* amn = am + ((int64_t)b * Ncl + n) * C;
+#pragma unroll
+  for (int i = 0; i < SDX_ITEMS; ++i) {
+    const int c = t * SDX_ITEMS + i;
+    key[i] = c < C ? (uint32_t)amn[c] : sentinel;
+    val[i] = c;
+  }
+  Sort(tmp.sort).Sort(key, val, 0, end_bit);
+#pragma unroll
+  for (int i = 0; i < SDX_ITEMS; ++i) {
+    srow[t * SDX_ITEMS + i] = key[i];
+    schan[t * SDX_ITEMS + i] = val[i];
+  }
   __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;           // cols [0,256): Y^T x2, [256,512): dX x2
-  const int64_t total = (int64_t)p.B * p.tiles;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
-      int ab = 0, ws = 0;
-      uint32_t aph = 0, wph = 0;
-      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-        const int b = (int)(t / p.tiles);
-        const int r0 = (int)((t % p.tiles) * BR);
-        mbar_wait(&a_empty[ab], aph ^ 1);
-        mbar_expect_tx(&a_full[ab], (uint32_t)p.nkb * BA_KB);
-        for (int kb = 0; kb < p.nkb; ++kb)
-          tma_load_3d(at + (ab * 2 + kb) * BA_KB, &tmA, &a_full[ab], kb * 64, r0, p.a_shared ? 0 : b);
-        if (++ab == 2) { ab = 0; aph ^= 1; }
-        for (int cb = 0; cb < p.nblk; ++cb) {
-          mbar_wait(&w_empty[ws], wph ^ 1);
-          mbar_expect_tx(&w_full[ws], (uint32_t)p.nkb * WKB);
-          for (int kb = 0; kb < p.nkb; ++kb)
-            tma_load_3d(wst + (ws * 2 + kb) * WKB, &tmW, &w_full[ws], kb * 64, cb * CBLK, b);
-          if (++ws == DG_WST) { ws = 0; wph ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    const uint32_t idesc_y = idesc_bf16(CBLK, BR, false, false);
-    const uint32_t idesc_d = idesc_bf16(BR, (int)p.K, true, true);
-    int ab = 0, ws = 0, yb = 0, dyb = 0, db = 0;
-    uint32_t aph = 0, wph = 0, yph = 0, dyph = 0, dph = 0;
-    int pws = 0;                                      // W stage of the block awaiting its dgrad
-    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-      mbar_wait(&a_full[ab], aph);
-      mbar_wait(&d_empty[db], dph ^ 1);
-      tc_fence_after();
-      const uint32_t sa = smem_u32(at + ab * 2 * BA_KB);
-      const uint32_t dacc = tmem_base + 256 + (uint32_t)(db * 128);
-      for (int cb = 0; cb <= p.nblk; ++cb) {
-        if (cb < p.nblk) {                              // recompute Y^T[cb]
-          mbar_wait(&w_full[ws], wph);
-          mbar_wait(&y_empty[yb], yph ^ 1);
-          tc_fence_after();
-          {
-            const uint64_t ad0 = smem_desc(smem_u32(wst + ws * 2 * WKB), 16, 1024), bd0 = smem_desc(sa, 16, 1024);
-            const uint32_t d = tmem_base + (uint32_t)(yb * 128);
-            for (int kb = 0; kb < p.nkb; ++kb) {
+  // segment heads -> compacted list of segment starts
+  int flag[SDX_ITEMS], pos[SDX_ITEMS];
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                tc_mma_ss(d, ad0 + (uint64_t)(kb * (WKB >> 4) + 2 * k), bd0 + (uint64_t)(kb * (BA_KB >> 4) + 2 * k), idesc_y,
-                          (kb | k) != 0 ? 1u : 0u);
-            }
-            tc_commit_w(&y_full[yb]);
-            if (cb == p.nblk - 1) tc_commit_w(&a_empty[ab]);
-          }
-          __syncwarp();
-          if (++yb == 2) { yb = 0; yph ^= 1; }
-        }
-        if (cb > 0) {                                   // dX += dY[cb-1] W[cb-1]
-          mbar_wait(&dy_full[dyb], dyph);
-          tc_fence_after();
-          {
-            const uint64_t ad0 = smem_desc(smem_u32(dyt + dyb * DY_BYTES), CBLK * 128, 1024);
-            const uint64_t bd0 = smem_desc(smem_u32(wst + pws * 2 * WKB), WKB, 1024);
-#pragma unroll
-            for (int k = 0; k < CBLK / 16; ++k)   // MN-major: +16 rows x 128 B per k step
-              tc_mma_ss(dacc, ad0 + (uint64_t)(k * 128), bd0 + (uint64_t)(k * 128), idesc_d, (cb > 1 || k > 0) ? 1u : 0u);
-            tc_commit_w(&dy_empty[dyb]);
-            tc_commit_w(&w_empty[pws]);
-            if (cb == p.nblk) tc_commit_w(&d_full[db]);
-          }
-          __syncwarp();
-          if (++dyb == 2) { dyb = 0; dyph ^= 1; }
-        }
-        if (cb < p.nblk) {
-          pws = ws;
-          if (++ws == DG_WST) { ws = 0; wph ^= 1; }
-        }
-      }
-      if (++ab == 2) { ab = 0; aph ^= 1; }
-      if (++db == 2) { db = 0; dph ^= 1; }
-    }
-  } else {
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
-    const int cl = quarter * 32 + lane;               // channel within the block (TMEM lane)
-    const uint32_t sw = (uint32_t)(cl & 7);
-    int yb = 0, dyb = 0, db = 0;
-    uint32_t yph = 0, dyph = 0, dph = 0;
-    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-      const int b = (int)(t / p.tiles);
-      const int64_t r0 = (t % p.tiles) * BR;
-      for (int cb = 0; cb < p.nblk; ++cb) {
-        uint32_t u[64];
-        const BwdPre pre = bwd_prefetch(p, b, (int64_t)cb * CBLK + cl, r0 + half * 64);
-        mbar_wait(&y_full[yb], yph);
-        tc_fence_after();
-        ld64(tmem_base + (uint32_t)(yb * 128 + half * 64) + ((uint32_t)(quarter * 32) << 16), u);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&y_empty[yb]);
-        if (++yb == 2) { yb = 0; yph ^= 1; }
-        mbar_wait(&dy_empty[dyb], dyph ^ 1);
-        const uint32_t rowaddr = smem_u32(dyt + dyb * DY_BYTES + half * (CBLK * 128)) + cl * 128;
-        bwd_transform(u, pre, p, b, (int64_t)cb * CBLK + cl, r0 + half * 64, rowaddr, sw);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&dy_full[dyb]);
-        if (++dyb == 2) { dyb = 0; dyph ^= 1; }
-      }
-      // dX tile: TMEM lane = point, columns = k
-      mbar_wait(&d_full[db], dph);
-      tc_fence_after();
-      const int64_t r = r0 + quarter * 32 + lane;
-      if (half * 64 < p.K) {
-        uint32_t u[64];
-        ld64(tmem_base + 256 + (uint32_t)(db * 128 + half * 64) + ((uint32_t)(quarter * 32) << 16), u);
-        if (r < p.R) {
-          __nv_bfloat16* dst = p.dX + (int64_t)b * p.dx_bs + r * p.dx_ld + half * 64;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            uint4 w4;
-            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w4);
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              h[e] = __floats2bfloat162_rn(__uint_as_float(u[8 * q + 2 * e]), __uint_as_float(u[8 * q + 2 * e + 1]));
-            *reinterpret_cast<uint4*>(dst + 8 * q) = w4;
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&d_empty[db]);
-      if (++db == 2) { db = 0; dph ^= 1; }
-    }
+  for (int i = 0; i < SDX_ITEMS; ++i) {
+    const int j = t * SDX_ITEMS + i;
+    flag[i] = (j < C && (j == 0 || srow[j - 1] != srow[j])) ? 1 : 0;
   }
-  tc_fence_before();
+  int total;
+  Scan(tmp.scan).ExclusiveSum(flag, pos, total);
+#pragma unroll
+  for (int i = 0; i < SDX_ITEMS; ++i)
+    if (flag[i]) shead[pos[i]] = t * SDX_ITEMS + i;
+  if (t == 0) { shead[total] = (int)C; snseg = total; }
   __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_free512(tmem_base);
+  const int nseg = snseg, nsl = K / 8;
+  const float* spn = sp + ((int64_t)b * Ncl + n) * C;
+  const __nv_bfloat16* Wb = W + (int64_t)b * w_bs;
+  __nv_bfloat16* dXn = dX + (int64_t)b * dx_bs + (int64_t)n * L * dx_ld;
+  for (int it = t; it < nseg * nsl; it += SDX_T) {
+    const int sg = it / nsl, k8 = (it % nsl) * 8;
+    const int j0 = shead[sg], j1 = shead[sg + 1];
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    for (int j = j0; j < j1; ++j) {
+      const int c = schan[j];
+      const float w = spn[c];
+      float x[8];
+      ld_vec<__nv_bfloat16, 8>(Wb + (int64_t)c * w_ld + k8, x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = fmaf(w, x[e], acc[e]);
+    }
+    __nv_bfloat16* d = dXn + (int64_t)srow[j0] * dx_ld + k8;
+    float y[8];
+    ld_vec<__nv_bfloat16, 8>(d, y);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) y[e] += acc[e];
+    st_vec<__nv_bfloat16, 8>(d, y);
   }
 }
 
-// ---------------------------------------------------------------- wgrad --
-// Unit = (model, point split, channel block cb), cb fastest so the nblk CTAs
-// of one (model, split) stream the same X chunks together (L2 hits).  Per
-// 128-point chunk: recompute Y^T[cb] chunk, transform to dY^T, then
-// dW[cb] += dY^T X_chunk (M = 128 channels, K-major dY^T; N = K, MN-major X).
-__global__ void __launch_bounds__(LT, 1)
-k_lbm_wgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW, BwdArgs p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = align1024(smem_raw);
-  uint8_t* wr = smem;                                  // W[cb]: 2 k blocks x 16 KB
-  uint8_t* ast = wr + 2 * WKB;                         // WG_AST x 2 k blocks x 16 KB
-  uint8_t* dyt = ast + WG_AST * 2 * BA_KB;             // 2 x 32 KB
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(dyt + 2 * DY_BYTES);
-  uint64_t* a_empty = a_full + WG_AST;
-  uint64_t* w_full = a_empty + WG_AST;
-  uint64_t* w_empty = w_full + 1;
-  uint64_t* y_full = w_empty + 1;
-  uint64_t* y_empty = y_full + 2;
-  uint64_t* dy_full = y_empty + 2;
-  uint64_t* dy_empty = dy_full + 2;
-  uint64_t* d_full = dy_empty + 2;
-  uint64_t* d_empty = d_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&y_full[s], 1); mbar_init(&y_empty[s], NEPIW);
-      mbar_init(&dy_full[s], NEPIW); mbar_init(&dy_empty[s], 1);
-      mbar_init(&d_full[s], 1); mbar_init(&d_empty[s], NEPIW);
-    }
-    for (int s = 0; s < WG_AST; ++s) { mbar_init(&a_full[s], 1); mbar_init(&a_empty[s], 1); }
-    mbar_init(w_full, 1);
-    mbar_init(w_empty, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (warp == 1) tmem_alloc512(tmem_slot);
-  tc_fence_before();
+// dW[c] (+)= bx_c (W G)[c] + cc_c s + sum_n sp(n, c) X[n*L + argmax(n, c)].
+// One CTA per (model, 64 channels) with G (fp32 K x K) in shared memory; a
+// warp per channel, lane l owns k = 4l .. 4l+3 (K = 128; K = 64 uses lanes
+// 0-15).  The per-cloud (sp, argmax) pairs are loaded one per lane and
+// broadcast with shuffles, so the row gathers are independent loads.
+__global__ void __launch_bounds__(256) k_lbm_dw(int Ncl, int64_t L, int64_t C, int K, const float* __restrict__ G,
+                                                const float* __restrict__ svec, const __nv_bfloat16* __restrict__ W,
+                                                int64_t w_bs, int64_t w_ld, const float2* __restrict__ coef,
+                                                const int32_t* __restrict__ am, const float* __restrict__ sp,
+                                                const __nv_bfloat16* __restrict__ X, int64_t x_bs, int64_t x_ld,
+                                                float* __restrict__ dW, int64_t dw_bs, int64_t dw_ld,
+                                                int accumulate) {
+  extern __shared__ float sG[];                 // [K][K] then s[K]
+  float* ss = sG + K * K;
+  __shared__ float swrow[8][128];
+  const int b = blockIdx.y;
+  const int t = threadIdx.x, warp = t / 32, lane = t % 32;
+  for (int e = t; e < K * K; e += 256) sG[e] = G[(int64_t)b * K * K + e];
+  for (int e = t; e < K; e += 256) ss[e] = svec[(int64_t)b * K + e];
   __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;           // cols [0,256): Y^T x2, [256,512): dW x2
-  const int64_t total = (int64_t)p.B * p.splits * p.nblk;
-
-  auto unit = [&](int64_t t, int& b, int& cb, int64_t& rbeg, int& nch) {
-    cb = (int)(t % p.nblk);
-    const int64_t r = t / p.nblk;
-    const int s = (int)(r % p.splits);
-    b = (int)(r / p.splits);
-    rbeg = (int64_t)s * p.rps;
-    const int64_t rend = min(p.R, rbeg + p.rps);
-    nch = rend > rbeg ? (int)((rend - rbeg + BR - 1) / BR) : 0;
-  };
-
-  if (warp == 0) {
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
-      int st = 0;
-      uint32_t ph = 0, wep = 0;
-      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-        int b, cb, nch;
-        int64_t rbeg;
-        unit(t, b, cb, rbeg, nch);
-        if (wep > 0) mbar_wait(w_empty, (wep - 1) & 1);
-        mbar_expect_tx(w_full, (uint32_t)p.nkb * WKB);
-        for (int kb = 0; kb < p.nkb; ++kb) tma_load_3d(wr + kb * WKB, &tmW, w_full, kb * 64, cb * CBLK, b);
-        ++wep;
-        for (int j = 0; j < nch; ++j) {
-          mbar_wait(&a_empty[st], ph ^ 1);
-          mbar_expect_tx(&a_full[st], (uint32_t)p.nkb * BA_KB);
-          for (int kb = 0; kb < p.nkb; ++kb)
-            tma_load_3d(ast + (st * 2 + kb) * BA_KB, &tmA, &a_full[st], kb * 64, (int)(rbeg + (int64_t)j * BR),
-                        p.a_shared ? 0 : b);
-          if (++st == WG_AST) { st = 0; ph ^= 1; }
+  const bool on = lane * 4 < K;
+  const __nv_bfloat16* Wb = W + (int64_t)b * w_bs;
+  const __nv_bfloat16* Xb = X + (int64_t)b * x_bs;
+  for (int ci = warp; ci < 64; ci += 8) {
+    const int64_t c = (int64_t)blockIdx.x * 64 + ci;
+    if (c >= C) break;
+    float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int nb = 0; nb < Ncl; nb += 32) {         // sparse gathers: 32 clouds per round
+      const int nl = nb + lane;
+      float vl = 0.f;
+      int64_t rl = 0;
+      if (nl < Ncl) {
+        const int64_t o = ((int64_t)b * Ncl + nl) * C + c;
+        vl = sp[o];
+        rl = (int64_t)nl * L + am[o];
+      }
+      const int cnt = min(32, Ncl - nb);
+#pragma unroll 8
+      for (int q = 0; q < cnt; ++q) {
+        const float v = __shfl_sync(0xffffffffu, vl, q);
+        const int64_t row = __shfl_sync(0xffffffffu, rl, q);
+        if (on) {
+          float x4[4];
+          ld_vec<__nv_bfloat16, 4>(Xb + row * x_ld + lane * 4, x4);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sacc[e] = fmaf(v, x4[e], sacc[e]);
         }
       }
     }
-  } else if (warp == 1) {
-    const uint32_t idesc_y = idesc_bf16(CBLK, BR, false, false);
-    const uint32_t idesc_w = idesc_bf16(CBLK, (int)p.K, false, true);
-    int st = 0, yb = 0, dyb = 0, db = 0;
-    uint32_t ph = 0, yph = 0, dyph = 0, dph = 0, wep = 0;
-    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-      int b, cb, nch;
-      int64_t rbeg;
-      unit(t, b, cb, rbeg, nch);
-      mbar_wait(w_full, wep & 1);
-      ++wep;
-      mbar_wait(&d_empty[db], dph ^ 1);
-      tc_fence_after();
-      const uint32_t sw = smem_u32(wr);
-      const uint32_t dacc = tmem_base + 256 + (uint32_t)(db * 128);
-      int pst = 0;
-      for (int j = 0; j <= nch; ++j) {
-        if (j < nch) {
-          mbar_wait(&a_full[st], ph);
-          mbar_wait(&y_empty[yb], yph ^ 1);
-          tc_fence_after();
-          {
-            const uint64_t ad0 = smem_desc(sw, 16, 1024), bd0 = smem_desc(smem_u32(ast + st * 2 * BA_KB), 16, 1024);
-            const uint32_t d = tmem_base + (uint32_t)(yb * 128);
-            for (int kb = 0; kb < p.nkb; ++kb) {
+    if (on) {
+      float w4[4];
+      ld_vec<__nv_bfloat16, 4>(Wb + c * w_ld + lane * 4, w4);
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                tc_mma_ss(d, ad0 + (uint64_t)(kb * (WKB >> 4) + 2 * k), bd0 + (uint64_t)(kb * (BA_KB >> 4) + 2 * k), idesc_y,
-                          (kb | k) != 0 ? 1u : 0u);
-            }
-            tc_commit_w(&y_full[yb]);
-          }
-          __syncwarp();
-          if (++yb == 2) { yb = 0; yph ^= 1; }
-        }
-        if (j > 0) {                                    // dW += dY^T[j-1] X[j-1]
-          mbar_wait(&dy_full[dyb], dyph);
-          tc_fence_after();
-          {
-            const uint64_t ad0 = smem_desc(smem_u32(dyt + dyb * DY_BYTES), 16, 1024);
-            const uint64_t bd0 = smem_desc(smem_u32(ast + pst * 2 * BA_KB), BA_KB, 1024);
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-              for (int k = 0; k < 4; ++k)   // A: K-major +32 B per k step; B: MN-major +16 rows x 128 B
-                tc_mma_ss(dacc, ad0 + (uint64_t)(h * (CBLK * 128 >> 4) + 2 * k), bd0 + (uint64_t)((h * 64 + k * 16) * 8),
-                          idesc_w, (j > 1 || h > 0 || k > 0) ? 1u : 0u);
-            tc_commit_w(&dy_empty[dyb]);
-            tc_commit_w(&a_empty[pst]);
-            if (j == nch) {
-              tc_commit_w(&d_full[db]);
-              tc_commit_w(w_empty);
-            }
-          }
-          __syncwarp();
-          if (++dyb == 2) { dyb = 0; dyph ^= 1; }
-        }
-        if (j < nch) {
-          pst = st;
-          if (++st == WG_AST) { st = 0; ph ^= 1; }
-        }
-      }
-      if (nch == 0) {
-        if (lane == 0) mbar_arrive(&d_full[db]);
-        tc_commit_w(w_empty);
-      }
-      __syncwarp();
-      if (++db == 2) { db = 0; dph ^= 1; }
+      for (int e = 0; e < 4; ++e) swrow[warp][lane * 4 + e] = w4[e];
     }
-  } else {
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
-    const int cl = quarter * 32 + lane;
-    const uint32_t sw = (uint32_t)(cl & 7);
-    int yb = 0, dyb = 0, db = 0;
-    uint32_t yph = 0, dyph = 0, dph = 0;
-    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-      int b, cb, nch;
-      int64_t rbeg;
-      unit(t, b, cb, rbeg, nch);
-      const int64_t c = (int64_t)cb * CBLK + cl;
-      for (int j = 0; j < nch; ++j) {
-        uint32_t u[64];
-        const BwdPre pre = bwd_prefetch(p, b, c, rbeg + (int64_t)j * BR + half * 64);
-        mbar_wait(&y_full[yb], yph);
-        tc_fence_after();
-        ld64(tmem_base + (uint32_t)(yb * 128 + half * 64) + ((uint32_t)(quarter * 32) << 16), u);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&y_empty[yb]);
-        if (++yb == 2) { yb = 0; yph ^= 1; }
-        mbar_wait(&dy_empty[dyb], dyph ^ 1);
-        const uint32_t rowaddr = smem_u32(dyt + dyb * DY_BYTES + half * (CBLK * 128)) + cl * 128;
-        bwd_transform(u, pre, p, b, c, rbeg + (int64_t)j * BR + half * 64, rowaddr, sw);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&dy_full[dyb]);
-        if (++dyb == 2) { dyb = 0; dyph ^= 1; }
+    __syncwarp();
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (on) {
+#pragma unroll 8
+      for (int k2 = 0; k2 < K; ++k2) {
+        const float w = swrow[warp][k2];
+        const float4 g4 = *reinterpret_cast<const float4*>(sG + k2 * K + lane * 4);
+        acc[0] = fmaf(w, g4.x, acc[0]); acc[1] = fmaf(w, g4.y, acc[1]);
+        acc[2] = fmaf(w, g4.z, acc[2]); acc[3] = fmaf(w, g4.w, acc[3]);
       }
-      // dW[cb] block: TMEM lane = channel, columns = k
-      mbar_wait(&d_full[db], dph);
-      tc_fence_after();
-      if (half * 64 < p.K) {
-        uint32_t u[64];
-        if (nch > 0) ld64(tmem_base + 256 + (uint32_t)(db * 128 + half * 64) + ((uint32_t)(quarter * 32) << 16), u);
-        else {
-#pragma unroll
-          for (int q = 0; q < 64; ++q) u[q] = 0u;
-        }
-        const int s = (int)((t / p.nblk) % p.splits);
-        float* dst;
-        bool acc_into = false;
-        if (p.splits > 1) {
-          dst = p.part + (((int64_t)s * p.B + b) * p.C + c) * p.K + half * 64;
-        } else {
-          dst = p.dW + (int64_t)b * p.dw_bs + c * p.dw_ld + half * 64;
-          acc_into = p.accumulate != 0;
-        }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          float4 v = make_float4(__uint_as_float(u[4 * q]), __uint_as_float(u[4 * q + 1]), __uint_as_float(u[4 * q + 2]),
-                                 __uint_as_float(u[4 * q + 3]));
-          if (acc_into) {
-            dst[4 * q] += v.x; dst[4 * q + 1] += v.y; dst[4 * q + 2] += v.z; dst[4 * q + 3] += v.w;
-          } else if (p.splits > 1) {
-            *reinterpret_cast<float4*>(dst + 4 * q) = v;
-          } else {
-            dst[4 * q] = v.x; dst[4 * q + 1] = v.y; dst[4 * q + 2] = v.z; dst[4 * q + 3] = v.w;
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&d_empty[db]);
-      if (++db == 2) { db = 0; dph ^= 1; }
     }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_free512(tmem_base);
-  }
-}
-
-// dW = sum_s part[s] in split order (deterministic).
-__global__ void k_lbm_wreduce(int B, int S, int64_t C, int64_t K, const float* __restrict__ part, float* __restrict__ dW,
-                              int64_t dw_bs, int64_t dw_ld, int accumulate) {
-  const int64_t n = (int64_t)B * C * K;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float a = 0.f;
-    for (int s = 0; s < S; ++s) a += part[(int64_t)s * n + i];
-    const int64_t k = i % K, c = (i / K) % C, b = i / (K * C);
-    float* d = dW + b * dw_bs + c * dw_ld + k;
-    *d = accumulate ? *d + a : a;
+    __syncwarp();
+    const float2 cf = coef[(int64_t)b * C + c];
+    if (on) {
+      float* d = dW + (int64_t)b * dw_bs + c * dw_ld + lane * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float r = fmaf(cf.x, acc[e], fmaf(cf.y, ss[lane * 4 + e], sacc[e]));
+        d[e] = accumulate ? d[e] + r : r;
+      }
+    }
   }
 }
 
 // ------------------------------------------------------------ host side --
 constexpr size_t FWD_SMEM = 1024 + FG * 2 * WKB + FSTAGES * 2 * FA_KB + 256 + NEPIW * NBW * 4 * 32 * 16;
-constexpr size_t DG_SMEM = 1024 + 2 * 2 * BA_KB + DG_WST * 2 * WKB + 2 * DY_BYTES + 256;
-constexpr size_t WG_SMEM = 1024 + 2 * WKB + WG_AST * 2 * BA_KB + 2 * DY_BYTES + 256;
-static_assert(FWD_SMEM <= 232448 && DG_SMEM <= 232448 && WG_SMEM <= 232448, "shared memory budget");
+static_assert(FWD_SMEM <= 232448, "shared memory budget");
 
 size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
-
-int wgrad_splits(int B, int64_t C, int64_t R) {
-  const int64_t nblk = C / CBLK;
-  int64_t s = cdiv(4 * 148, (int64_t)B * nblk);
-  s = std::max<int64_t>(1, std::min<int64_t>(s, 16));
-  s = std::min<int64_t>(s, std::max<int64_t>(1, cdiv(R, BR)));
-  return (int)s;
-}
 
 size_t fwd_ws(int B, int64_t N, int64_t C, int64_t K) {
   return al256((size_t)B * C * K * 2) + 4 * al256((size_t)B * N * C * 4);
 }
-size_t bwd_ws(int B, int64_t N, int64_t L, int64_t C, int64_t K) {
-  const int S = wgrad_splits(B, C, N * L);
-  return al256((size_t)B * C * 8) + al256((size_t)B * N * C * 4) + (S > 1 ? al256((size_t)S * B * C * K * 4) : 0);
+// backward workspace: coef, sp, G, s, M, v, then hfta_fused_linear_bwd's own
+struct BwdWs {
+  size_t coef, sp, G, sv, M, v, lin, total;
+};
+BwdWs bwd_layout(int B, int64_t N, int64_t L, int64_t C, int64_t K) {
+  BwdWs w{};
+  size_t o = 0;
+  w.coef = o; o += al256((size_t)B * C * 8);
+  w.sp = o; o += al256((size_t)B * N * C * 4);
+  w.G = o; o += al256((size_t)B * K * K * 4);
+  w.sv = o; o += al256((size_t)B * K * 4);
+  w.M = o; o += al256((size_t)B * K * K * 2);
+  w.v = o; o += al256((size_t)B * K * 4);
+  w.lin = o; o += al256(hfta_fused_linear_bwd_workspace(B, N * L, K, K, HFTA_BF16));
+  w.total = o;
+  return w;
 }
+size_t bwd_ws(int B, int64_t N, int64_t L, int64_t C, int64_t K) { return bwd_layout(B, N, L, C, K).total; }
 
 template <typename K_>
 void set_smem(K_ kern, size_t bytes, bool& done) {
@@ -1094,55 +816,53 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
                "linear_bn_max_bwd: dG, argmax, ext, gamma, beta, save_*, dW, dgamma, dbeta are required");
   HFTA_REQUIRE(!dX.ptr || (aligned16(dX.ptr) && (dX.ld * 2) % 16 == 0 && (dX.bstride * 2) % 16 == 0 && dX.ld >= K),
                HFTA_ERR_UNSUPPORTED, "linear_bn_max_bwd: dX must be 16-B aligned with 16-B row strides");
+  HFTA_REQUIRE(C <= SDX_T * SDX_ITEMS, HFTA_ERR_UNSUPPORTED, "linear_bn_max_bwd: C=%lld > %d", (long long)C,
+               SDX_T * SDX_ITEMS);
   HFTA_REQUIRE(dW_ld >= K, HFTA_ERR_SHAPE, "linear_bn_max_bwd: dW_ld < K");
   const size_t need = hfta_fused_linear_bn_max_workspace(B, N, L, C, K);
   HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "linear_bn_max_bwd: workspace %zu < %zu", ws_bytes, need);
-  if (hfta_status st = get_encode()) return st;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t R = N * L;
-  const int S = wgrad_splits(B, C, R);
+  const BwdWs lay = bwd_layout(B, N, L, C, K);
   char* w = reinterpret_cast<char*>(ws);
-  float2* coef = reinterpret_cast<float2*>(w);
-  w += al256((size_t)B * C * 8);
-  float* pv = reinterpret_cast<float*>(w);
-  w += al256((size_t)B * N * C * 4);
-  float* part = reinterpret_cast<float*>(w);
+  float2* coef = reinterpret_cast<float2*>(w + lay.coef);
+  float* sp = reinterpret_cast<float*>(w + lay.sp);
+  float* G = reinterpret_cast<float*>(w + lay.G);
+  float* sv = reinterpret_cast<float*>(w + lay.sv);
+  __nv_bfloat16* M = reinterpret_cast<__nv_bfloat16*>(w + lay.M);
+  float* v = reinterpret_cast<float*>(w + lay.v);
+  const __nv_bfloat16* Wp = (const __nv_bfloat16*)W.ptr;
+  const int64_t wbs = B > 1 ? W.bstride : 0;
 
   k_lbm_bwd_coef<<<(unsigned)cdiv((int64_t)B * C, 128), 128, 0, s>>>(
       B, (int)N, L, C, (const float*)dG.ptr, dG.bstride, dG.ld, (const float*)ext.ptr, ext.bstride, ext.ld, bias,
-      bias_bstride, gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, coef, pv, dgamma, dbeta,
+      bias_bstride, gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, coef, sp, dgamma, dbeta,
       dbias, dbias_bstride, accumulate);
-
-  CUtensorMap ta, tw;
-  const int nba = (X.bstride == 0 && B > 1) ? 1 : B;
-  if (hfta_status st = make_map(&ta, X.ptr, K, R, X.ld, X.bstride, nba, 64, BR)) return st;
-  if (hfta_status st = make_map(&tw, W.ptr, K, C, W.ld, W.bstride, B, 64, CBLK)) return st;
-  BwdArgs a{};
-  a.B = B; a.Ncl = (int)N; a.nblk = (int)(C / CBLK); a.nkb = (int)(K / 64); a.a_shared = nba == 1 && B > 1;
-  a.L = L; a.C = C; a.R = R; a.K = K; a.tiles = cdiv(R, BR);
-  a.coef = coef; a.pv = pv; a.am = argmax; a.am_bs = N * C; a.am_ld = C;
-  a.dX = (__nv_bfloat16*)dX.ptr; a.dx_bs = dX.bstride; a.dx_ld = dX.ld;
-  a.dW = dW; a.dw_bs = dW_bstride; a.dw_ld = dW_ld; a.accumulate = accumulate;
-  a.splits = S; a.rps = cdiv(cdiv(R, S), BR) * BR; a.part = part;
-  int launches = 1;
+  // G = X^T X, s = X^T 1 (tensor-core wgrad contraction + column sums over the R points)
+  if (hfta_status st = hfta_fused_linear_bwd(B, R, K, K, HFTA_BF16, X, X, W, hfta_out{nullptr, 0, 1}, G, K * K, K,
+                                             sv, K, 0, w + lay.lin, lay.total - lay.lin, stream))
+    return st;
+  int launches = 2;
   if (dX.ptr) {
-    static bool attr = false;
-    set_smem(k_lbm_dgrad, DG_SMEM, attr);
-    const int grid = (int)std::min<int64_t>((int64_t)B * a.tiles, num_sms());
-    k_lbm_dgrad<<<grid, LT, DG_SMEM, s>>>(ta, tw, a);
-    ++launches;
+    k_lbm_mv<<<dim3((unsigned)cdiv(K, MV_ROWS), (unsigned)B), 256, 0, s>>>(C, (int)K, Wp, wbs, W.ld, coef, M, v);
+    // dX = X M^T + v (M symmetric): the fused forward GEMM with a per-model bias
+    if (hfta_status st = hfta_fused_linear_fwd(B, R, K, K, HFTA_BF16, X, hfta_in{M, K * K, K}, v, K, 0, 0, dX,
+                                               stream))
+      return st;
+    int end_bit = 1;
+    while ((int64_t(1) << end_bit) <= L) ++end_bit;       // argmax < L < 2^end_bit - 1 (sentinel)
+    k_lbm_sparse_dx<<<dim3((unsigned)N, (unsigned)B), SDX_T, 0, s>>>((int)N, L, C, (int)K, end_bit, argmax, sp, Wp,
+                                                                     wbs, W.ld, (__nv_bfloat16*)dX.ptr, dX.bstride,
+                                                                     dX.ld);
+    launches += 2;
   }
   {
+    const size_t smem = (size_t)(K * K + K) * 4;
     static bool attr = false;
-    set_smem(k_lbm_wgrad, WG_SMEM, attr);
-    const int grid = (int)std::min<int64_t>((int64_t)B * S * a.nblk, num_sms());
-    k_lbm_wgrad<<<grid, LT, WG_SMEM, s>>>(ta, tw, a);
-    ++launches;
-  }
-  if (S > 1) {
-    k_lbm_wreduce<<<(unsigned)std::min<int64_t>(cdiv((int64_t)B * C * K, 256), 148 * 16), 256, 0, s>>>(
-        B, S, C, K, part, dW, dW_bstride, dW_ld, accumulate);
-    ++launches;
+    set_smem(k_lbm_dw, smem, attr);
+    k_lbm_dw<<<dim3((unsigned)cdiv(C, 64), (unsigned)B), 256, smem, s>>>(
+        (int)N, L, C, (int)K, G, sv, Wp, wbs, W.ld, coef, argmax, sp, (const __nv_bfloat16*)X.ptr,
+        X.bstride, X.ld, dW, dW_bstride, dW_ld, accumulate);
   }
   count_launches(launches);
   return post_launch(s, "hfta_fused_linear_bn_max_bwd");

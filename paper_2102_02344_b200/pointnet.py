@@ -43,7 +43,7 @@ class FusedPointNet(FusedNet):
         self.f1, self.f2 = sh["stn.fc1.W"][0], sh["stn.fc2.W"][0]
         # bf16: c3 -> bn3 -> max runs as the fused tensor-core block (K10);
         # the [R][1024] pre-BN activation is never materialised.
-        self.fuse_lbm = self.dt == H.HFTA_BF16 and self.c3 % 128 == 0 and self.c2 in (64, 128)
+        self.fuse_lbm = self.dt == H.HFTA_BF16 and self.c3 % 128 == 0 and self.c3 <= 1024 and self.c2 in (64, 128)
         self._alloc()
 
     # ------------------------------------------------------------ buffers --
