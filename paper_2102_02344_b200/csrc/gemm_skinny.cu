@@ -12,15 +12,17 @@ namespace {
 constexpr int NT = 256;
 constexpr int KMAX = 8;
 
-// fwd, small K: C[m][n] = sum_k A[m][k] * Bw[n][k] + bias.  Thread = (row, VEC columns).
-template <typename T, int VEC>
+// fwd, small K: C[m][n] = sum_k A[m][k] * Bw[n][k] + bias.  Thread = (row, VEC
+// columns) with its KT x VEC weights and VEC biases in registers (KT = K, a
+// compile-time constant: 3 for the xyz layers; 0 = generic K <= KMAX from smem).
+template <typename T, int VEC, int KT>
 __global__ void __launch_bounds__(NT) k_skinny_fwd(GemmP p, int tpr, int rpb, int64_t rows_per_block) {
   __shared__ float w[KMAX * 512];
   const int b = blockIdx.y;
   const T* A = reinterpret_cast<const T*>(p.A) + (int64_t)b * p.a_bs;
   const T* Bw = reinterpret_cast<const T*>(p.Bm) + (int64_t)b * p.b_bs;
   T* C = reinterpret_cast<T*>(p.C) + (int64_t)b * p.c_bs;
-  const int K = (int)p.K, N = (int)p.N;
+  const int K = KT > 0 ? KT : (int)p.K, N = (int)p.N;
   for (int i = threadIdx.x; i < N * K; i += NT) w[(i % K) * N + i / K] = ldf(Bw + (int64_t)(i / K) * p.b_ld + i % K);
   __syncthreads();
   const int lane = threadIdx.x % tpr, rl = threadIdx.x / tpr;
@@ -29,7 +31,16 @@ __global__ void __launch_bounds__(NT) k_skinny_fwd(GemmP p, int tpr, int rpb, in
   float bias[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) bias[v] = p.bias ? p.bias[(int64_t)b * p.bias_bs + n0 + v] : 0.f;
+  constexpr int KR = KT > 0 ? KT : 1;
+  float wr[KR][VEC];
+  if constexpr (KT > 0) {
+#pragma unroll
+    for (int k = 0; k < KT; ++k)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) wr[k][v] = w[k * N + n0 + v];
+  }
   const int64_t r0 = blockIdx.x * rows_per_block, r1 = min(p.M, r0 + rows_per_block);
+#pragma unroll 2
   for (int64_t m = r0 + rl; m < r1; m += rpb) {
     float a[KMAX];
 #pragma unroll
@@ -39,44 +50,75 @@ __global__ void __launch_bounds__(NT) k_skinny_fwd(GemmP p, int tpr, int rpb, in
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       float acc = br ? br[n0 + v] : bias[v];
+      if constexpr (KT > 0) {
 #pragma unroll
-      for (int k = 0; k < KMAX; ++k)
-        if (k < K) acc = fmaf(a[k], w[k * N + n0 + v], acc);
+        for (int k = 0; k < KT; ++k) acc = fmaf(a[k], wr[k][v], acc);
+      } else {
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+          if (k < K) acc = fmaf(a[k], w[k * N + n0 + v], acc);
+      }
       o[v] = acc;
     }
     st_vec<T, VEC>(C + m * p.c_ld + n0, o);
   }
 }
 
-// dgrad, small N-out: C[m][j] = sum_n A[m][n] * Bw(n, j) with Bw MN-major (W[n][j]), j < N <= 8,
-// reduction length K (= layer width, e.g. 64).  Thread per row; A row read with 128-bit loads.
+// dgrad, small N-out: C[m][j] = sum_n A[m][n] * Bw(n, j) with Bw MN-major
+// (W[n][j]), j < NJ <= 4, reduction length K (layer width, e.g. 64, a
+// multiple of VEC).  A row is read by TPR = K/VEC threads with one 16-B load
+// each (coalesced), partial sums combined with shuffles.
 template <typename T, int VEC>
-__global__ void __launch_bounds__(NT) k_skinny_dgrad(GemmP p) {
-  __shared__ float w[KMAX * 1024];
+__global__ void __launch_bounds__(NT) k_skinny_dgrad(GemmP p, int tpr) {
+  __shared__ float4 w[1024];                           // w[n] = (W[n][0..3])
   const int b = blockIdx.y;
   const T* A = reinterpret_cast<const T*>(p.A) + (int64_t)b * p.a_bs;
   const T* Bw = reinterpret_cast<const T*>(p.Bm) + (int64_t)b * p.b_bs;
   T* C = reinterpret_cast<T*>(p.C) + (int64_t)b * p.c_bs;
   const int Kr = (int)p.K, Nj = (int)p.N;
-  for (int i = threadIdx.x; i < Kr * Nj; i += NT) {
-    int n = i / Nj, j = i % Nj;                       // element (j, n) of B = W[n][j]
-    w[n * KMAX + j] = ldf(Bw + (int64_t)n * p.b_ld + j);
+  for (int n = threadIdx.x; n < Kr; n += NT) {
+    float e[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) e[j] = j < Nj ? ldf(Bw + (int64_t)n * p.b_ld + j) : 0.f;
+    w[n] = make_float4(e[0], e[1], e[2], e[3]);
   }
   __syncthreads();
-  for (int64_t m = blockIdx.x * (int64_t)NT + threadIdx.x; m < p.M; m += (int64_t)gridDim.x * NT) {
-    float acc[KMAX];
+  const int lane = threadIdx.x % tpr, rl = threadIdx.x / tpr, rpb = NT / tpr;
+  const int n0 = lane * VEC;
+  for (int64_t m = blockIdx.x * (int64_t)rpb + rl; m < p.M; m += (int64_t)gridDim.x * rpb) {
+    float av[VEC];
+    ld_vec<T, VEC>(A + m * p.a_ld + n0, av);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int j = 0; j < KMAX; ++j) acc[j] = 0.f;
-    const T* a = A + m * p.a_ld;
-    for (int n = 0; n < Kr; n += VEC) {
-      float av[VEC];
-      ld_vec<T, VEC>(a + n, av);
-#pragma unroll
-      for (int v = 0; v < VEC; ++v)
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j) acc[j] = fmaf(av[v], w[(n + v) * KMAX + j], acc[j]);
+    for (int v = 0; v < VEC; ++v) {
+      const float4 wv = w[n0 + v];
+      acc[0] = fmaf(av[v], wv.x, acc[0]); acc[1] = fmaf(av[v], wv.y, acc[1]);
+      acc[2] = fmaf(av[v], wv.z, acc[2]); acc[3] = fmaf(av[v], wv.w, acc[3]);
     }
-    for (int j = 0; j < Nj; ++j) stf(C + m * p.c_ld + j, acc[j]);
+    for (int o = tpr / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < Nj) stf(C + m * p.c_ld + j, acc[j]);
+    }
+  }
+}
+
+// dgrad fallback (K not a power-of-two multiple of the vector width): thread per row.
+template <typename T>
+__global__ void __launch_bounds__(NT) k_skinny_dgrad_row(GemmP p) {
+  const int b = blockIdx.y;
+  const T* A = reinterpret_cast<const T*>(p.A) + (int64_t)b * p.a_bs;
+  const T* Bw = reinterpret_cast<const T*>(p.Bm) + (int64_t)b * p.b_bs;
+  T* C = reinterpret_cast<T*>(p.C) + (int64_t)b * p.c_bs;
+  for (int64_t m = blockIdx.x * (int64_t)NT + threadIdx.x; m < p.M; m += (int64_t)gridDim.x * NT) {
+    for (int j = 0; j < (int)p.N; ++j) {
+      float acc = 0.f;
+      for (int64_t n = 0; n < p.K; ++n) acc = fmaf(ldf(A + m * p.a_ld + n), ldf(Bw + n * p.b_ld + j), acc);
+      stf(C + m * p.c_ld + j, acc);
+    }
   }
 }
 
@@ -99,6 +141,7 @@ __global__ void __launch_bounds__(NT) k_skinny_wgrad(GemmP p, int tpr, int rpb, 
     for (int k = 0; k < 3; ++k) acc[v][k] = 0.f;
   if (n0 < N) {
     const int64_t r0 = (int64_t)chunk * rows_per_chunk, r1 = min(p.K, r0 + rows_per_chunk);
+#pragma unroll 4
     for (int64_t r = r0 + rl; r < r1; r += rpb) {
       float dy[VEC];
       ld_vec<T, VEC>(A + r * p.a_ld + n0, dy);
@@ -164,12 +207,15 @@ __global__ void k_gemv_fwd(GemmP p) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc[n] += __shfl_xor_sync(0xffffffffu, acc[n], o);
     }
-    if (lane == 0)
-      for (int n = 0; n < p.N; ++n) {
+    if (lane == 0) {
+#pragma unroll
+      for (int n = 0; n < KMAX; ++n) {
+        if (n >= p.N) break;
         float v = acc[n];
         if (p.bias) v += p.bias[(int64_t)b * p.bias_bs + (p.bias_div > 0 ? (m / p.bias_div) * p.bias_ld : 0) + n];
         stf(C + m * p.c_ld + n, v);
       }
+    }
   }
 }
 
@@ -211,7 +257,9 @@ __global__ void k_smallm_wgrad(GemmP p, int64_t rows_per_chunk, float* __restric
     for (int m = 0; m < KMAX; ++m)
       if (m < p.M) acc[m] = fmaf(ldf(A + r * p.a_ld + m), x, acc[m]);
   }
-  for (int m = 0; m < p.M; ++m) part[(((int64_t)chunk * p.B + b) * p.M + m) * p.N + n] = acc[m];
+#pragma unroll
+  for (int m = 0; m < KMAX; ++m)
+    if (m < p.M) part[(((int64_t)chunk * p.B + b) * p.M + m) * p.N + n] = acc[m];
 }
 
 __global__ void k_smallm_fin(GemmP p, int chunks, const float* __restrict__ part) {
@@ -232,7 +280,8 @@ static bool smallk_ok(const GemmP& p) { return p.a_kmajor && p.K <= KMAX && p.sp
 static bool smallm_wgrad_ok(const GemmP& p) { return !p.a_kmajor && !p.b_kmajor && p.M <= KMAX; }
 bool skinny_fwd_ok_base(const GemmP& p) { return p.a_kmajor && p.b_kmajor && p.K <= KMAX && p.N <= 512 && p.splits == 1; }
 bool skinny_dgrad_ok(const GemmP& p) {
-  return p.a_kmajor && !p.b_kmajor && p.N <= KMAX && p.K <= 1024 && p.splits == 1 && p.K % 8 == 0 && p.a_ld % 8 == 0;
+  return p.a_kmajor && !p.b_kmajor && p.N <= 4 && p.K <= 1024 && p.splits == 1 && p.K % 8 == 0 && p.a_ld % 8 == 0 &&
+         p.K / 8 <= 32;
 }
 bool skinny_wgrad_ok_base(const GemmP& p) { return !p.a_kmajor && !p.b_kmajor && p.N <= 3 && p.M <= 128; }
 bool skinny_fwd_ok(const GemmP& p) { return skinny_fwd_ok_base(p) || gemv_fwd_ok(p) || smallk_ok(p); }
@@ -244,7 +293,7 @@ static int64_t smallm_chunks(int B, int64_t rows, int64_t N) {
 }
 
 size_t skinny_wgrad_ws(int B, int64_t rows, int64_t N, int64_t Ko) {
-  int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(4 * 148, B), cdiv(rows, 2048)));
+  int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(16 * 148, B), cdiv(rows, 1024)));
   size_t a = (size_t)chunks * B * N * Ko * sizeof(float);
   size_t c = N <= KMAX ? (size_t)smallm_chunks(B, rows, Ko) * B * N * Ko * sizeof(float) : 0;   // dW is [N][Ko]
   return std::max(a, c);
@@ -290,35 +339,44 @@ hfta_status gemm_skinny(const GemmP& p, hfta_dtype dt, void* ws, size_t ws_bytes
     if (p.N % vec || p.c_ld % vec || !aligned16(p.C) || p.c_bs % vec) vec = 1;
     int tpr = std::min(32, pow2ceil(cdiv(p.N, vec)));
     int rpb = NT / tpr;
-    int64_t blocks_per = std::max<int64_t>(1, std::min<int64_t>(cdiv(p.M, rpb * 4), cdiv(8 * 148, p.B)));
+    int64_t blocks_per = std::max<int64_t>(1, std::min<int64_t>(cdiv(p.M, rpb * 4), cdiv(16 * 148, p.B)));
     int64_t rows_per_block = cdiv(p.M, blocks_per);
     dim3 grid((unsigned)cdiv(p.M, rows_per_block), p.B);
+    const bool k3 = p.K == 3;
     if (bf) {
-      if (vec == 8) k_skinny_fwd<__nv_bfloat16, 8><<<grid, NT, 0, s>>>(p, tpr, rpb, rows_per_block);
-      else k_skinny_fwd<__nv_bfloat16, 1><<<grid, NT, 0, s>>>(p, tpr, rpb, rows_per_block);
+      if (vec == 8 && k3) k_skinny_fwd<__nv_bfloat16, 8, 3><<<grid, NT, 0, s>>>(p, tpr, rpb, rows_per_block);
+      else if (vec == 8) k_skinny_fwd<__nv_bfloat16, 8, 0><<<grid, NT, 0, s>>>(p, tpr, rpb, rows_per_block);
+      else k_skinny_fwd<__nv_bfloat16, 1, 0><<<grid, NT, 0, s>>>(p, tpr, rpb, rows_per_block);
     } else {
-      if (vec == 4) k_skinny_fwd<float, 4><<<grid, NT, 0, s>>>(p, tpr, rpb, rows_per_block);
-      else k_skinny_fwd<float, 1><<<grid, NT, 0, s>>>(p, tpr, rpb, rows_per_block);
+      if (vec == 4 && k3) k_skinny_fwd<float, 4, 3><<<grid, NT, 0, s>>>(p, tpr, rpb, rows_per_block);
+      else if (vec == 4) k_skinny_fwd<float, 4, 0><<<grid, NT, 0, s>>>(p, tpr, rpb, rows_per_block);
+      else k_skinny_fwd<float, 1, 0><<<grid, NT, 0, s>>>(p, tpr, rpb, rows_per_block);
     }
     count_launches(1);
     return post_launch(s, "gemm_skinny_fwd");
   }
   if (skinny_dgrad_ok(p)) {
-    dim3 grid((unsigned)std::min<int64_t>(cdiv(p.M, NT), cdiv(8 * 148, p.B)), p.B);
     const bool v = aligned16(p.A) && (p.a_bs % 8 == 0);
-    if (bf) {
-      if (v) k_skinny_dgrad<__nv_bfloat16, 8><<<grid, NT, 0, s>>>(p);
-      else k_skinny_dgrad<__nv_bfloat16, 1><<<grid, NT, 0, s>>>(p);
+    const int vec = v ? (bf ? 8 : 4) : 1;
+    int tpr = 1;
+    while (tpr * vec < p.K && tpr < 32) tpr <<= 1;     // K / vec lanes per row (power of 2 up to 32)
+    if (tpr * vec != p.K) { tpr = 1; }
+    const int rpb = NT / tpr;
+    dim3 grid((unsigned)std::min<int64_t>(cdiv(p.M, rpb), cdiv(16 * 148, p.B)), p.B);
+    if (tpr == 1) {   // generic: one thread per row, the whole row
+      if (bf) k_skinny_dgrad_row<__nv_bfloat16><<<grid, NT, 0, s>>>(p);
+      else k_skinny_dgrad_row<float><<<grid, NT, 0, s>>>(p);
+    } else if (bf) {
+      k_skinny_dgrad<__nv_bfloat16, 8><<<grid, NT, 0, s>>>(p, tpr);
     } else {
-      if (v) k_skinny_dgrad<float, 4><<<grid, NT, 0, s>>>(p);
-      else k_skinny_dgrad<float, 1><<<grid, NT, 0, s>>>(p);
+      k_skinny_dgrad<float, 4><<<grid, NT, 0, s>>>(p, tpr);
     }
     count_launches(1);
     return post_launch(s, "gemm_skinny_dgrad");
   }
   if (skinny_wgrad_ok_base(p)) {
     const int64_t rows = p.K, N = p.M, Ko = p.N;
-    int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(4 * 148, p.B), cdiv(rows, 2048)));
+    int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(16 * 148, p.B), cdiv(rows, 1024)));
     size_t need = (size_t)chunks * p.B * N * Ko * sizeof(float);
     HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "skinny wgrad: workspace %zu < %zu", ws_bytes, need);
     int vec = bf ? 8 : 4;
