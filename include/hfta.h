@@ -257,7 +257,8 @@ hfta_status hfta_fused_linear_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C,
  * and dW = diag(bx) W G + cc s^T + S^T X with M = W^T diag(bx) W (rounded to
  * bf16), v = W^T cc, G = X^T X, s = X^T 1 (K10).  accumulate != 0
  * adds to dW/dgamma/dbeta instead of overwriting.  ext/argmax/save_* are the
- * forward's outputs.  C <= 1024.
+ * forward's outputs.  dX_act != NONE multiplies dX by act'(X) (X being the
+ * previous layer's activation output), so dX is that layer's dZ.  C <= 1024.
  */
 hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C, int64_t K,
                                          hfta_dtype dt, hfta_in dG, hfta_in X, hfta_in W,
@@ -266,10 +267,53 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
                                          const float* gamma, const float* beta, int64_t gb_bstride,
                                          const float* save_mean, const float* save_invstd,
                                          hfta_act act, float act_alpha, hfta_out dX,
+                                         hfta_act dX_act, float dX_alpha,
                                          float* dW, int64_t dW_bstride, int64_t dW_ld,
                                          float* dbias, int64_t dbias_bstride,
                                          float* dgamma, float* dbeta, int accumulate,
                                          void* ws, size_t ws_bytes, hfta_stream stream);
+
+/* ------------------------- fused Linear -> BN -> act, Gram form (K11) -- */
+/*
+ * Conv1d(k=1)/Linear -> training-mode BatchNorm -> act for all B models
+ * (App. B rows P:L1265-1266; R6 conventions) with the batch
+ * statistics taken from the Gram of the layer input instead of a pass over
+ * the [M][N] pre-BN tensor (which is never written):
+ *   G = X^T X [K][K], s = X^T 1 [K]   (fp32, outputs: kept for the backward)
+ *   mean_n = (W_n . s)/M + bias_n,  var_n = W_n G W_n^T / M - ((W_n . s)/M)^2
+ *   A = act(gamma*(X W^T + bias - mean)*invstd + beta)     (bf16 [B][M][N])
+ * (fp64 from the fp32 G, s).  K <= 8 (streaming kernels) or K in {64, 128}
+ * (tensor cores), N <= 512 (N <= 128 for K >= 64), dt must be HFTA_BF16.
+ * Workspace: hfta_fused_linear_bn_workspace(B, M, N, K), shared by fwd/bwd.
+ */
+size_t hfta_fused_linear_bn_workspace(int B, int64_t M, int64_t N, int64_t K);
+hfta_status hfta_fused_linear_bn_fwd(int B, int64_t M, int64_t N, int64_t K, hfta_dtype dt,
+                                     hfta_in X, hfta_in W, const float* bias, int64_t bias_bstride,
+                                     const float* gamma, const float* beta, int64_t gb_bstride,
+                                     float* running_mean, float* running_var, float momentum, float eps,
+                                     hfta_act act, float act_alpha, hfta_out A,
+                                     float* save_mean, float* save_invstd, float* G, float* s,
+                                     void* ws, size_t ws_bytes, hfta_stream stream);
+/*
+ * Backward from dZ = dL/dz (the gradient at BN's output BEFORE act, i.e. the
+ * consumer already multiplied by act'): dbeta = 1^T dZ, Zm = dZ^T X,
+ * dgamma = invstd*(W.Zm - mean'*dbeta), and with a = gamma*invstd,
+ * bx = -a*invstd*dgamma/M, cc = -a*dbeta/M - bx*mean' (mean' = mean - bias):
+ *   dW = diag(a) Zm + diag(bx) W G + cc s^T                (fp32, accumulate adds)
+ *   dX = (dZ diag(a) W + X W^T diag(bx) W + 1 (W^T cc)^T) * act'(X)   (bf16)
+ * where act'(X) is dX_act's derivative evaluated on X (X = the previous
+ * layer's activation output; HFTA_ACT_NONE: no gating) -- so dX is the
+ * previous layer's dZ.  dbias (may be NULL) = exact zeros (BN-absorbed).
+ * dX.ptr NULL skips dX.  G, s: the forward's outputs.
+ */
+hfta_status hfta_fused_linear_bn_bwd(int B, int64_t M, int64_t N, int64_t K, hfta_dtype dt,
+                                     hfta_in dZ, hfta_in X, hfta_in W, const float* bias,
+                                     int64_t bias_bstride, const float* gamma, int64_t gb_bstride,
+                                     const float* save_mean, const float* save_invstd,
+                                     const float* G, const float* s, hfta_out dX, hfta_act dX_act,
+                                     float dX_alpha, float* dW, int64_t dW_bstride, int64_t dW_ld,
+                                     float* dbias, int64_t dbias_bstride, float* dgamma, float* dbeta,
+                                     int accumulate, void* ws, size_t ws_bytes, hfta_stream stream);
 /*
  * PointNet input transform (STN): T_b,n = F_b[n] viewed as 3x3 row-major
  * (+ I3 if add_identity), x'_b[n*L+l][:] = x[n*L+l][:] * T_b,n.

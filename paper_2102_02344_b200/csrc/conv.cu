@@ -126,12 +126,6 @@ void col2im(hfta_dtype dt, const Geo2& g, const void* col, int64_t cbs, int64_t 
   count_launches(1);
 }
 
-hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void* ws = nullptr, size_t wsb = 0) {
-  if (skinny_fwd_ok(p) || skinny_dgrad_ok(p) || skinny_wgrad_ok(p)) return gemm_skinny(p, dt, ws, wsb, s);
-  if (gemm_tc_supported(p, dt, out_f32)) return gemm_tc(p, dt, out_f32, s);
-  return gemm_simt(p, dt, out_f32, s);
-}
-
 // Shape bookkeeping of one (de)convolution.
 struct Shape {
   Geo2 g;             // gather geometry

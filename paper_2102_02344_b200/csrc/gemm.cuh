@@ -22,6 +22,17 @@ struct GemmP {
   int splits;       // split-K chunks (>= 1); > 1 needs `part`
   int64_t k_chunk;  // reduction rows per split (multiple of the K tile)
   float* part;      // [splits][B][M][N] fp32 partials
+  // ---- epilogue / operand extensions (tensor-core path, bf16 output) ----
+  // v = act(v * scale[b][n] + bias) then v *= act'(mask[b][m][n]) where the
+  // mask is the activation output that fed this layer (ReLU: mask > 0).
+  const float* scale; int64_t scale_bs;          // NULL: no scale
+  int act; float act_alpha;                      // hfta_act after the affine
+  const void* mask; int64_t mask_bs, mask_ld;    // NULL: no mask
+  int mask_act; float mask_alpha;
+  // second K segment: C += sum_k A2(m,k) B2(n,k), k < K2 (both K-major, K2 % 64 == 0)
+  const void* A2; int64_t a2_bs, a2_ld;
+  const void* Bm2; int64_t b2_bs, b2_ld;
+  int64_t K2;
 };
 
 // dt_in: operand dtype; out_f32: C is fp32 (else dt_in).
@@ -32,6 +43,9 @@ hfta_status splitk_reduce(const GemmP& p, cudaStream_t s);   // C (+)= sum_s par
 // does not qualify (caller then uses gemm_simt).
 hfta_status gemm_tc(const GemmP& p, hfta_dtype dt_in, bool out_f32, cudaStream_t s);
 bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32);
+
+// Dispatch: skinny -> tcgen05 -> SIMT (EPI features: skinny / tcgen05 only).
+hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void* ws = nullptr, size_t wsb = 0);
 
 // HBM-bound skinny contractions (K <= 8 fwd, N-out <= 8 dgrad, K-out <= 3 wgrad).
 bool skinny_fwd_ok(const GemmP& p);

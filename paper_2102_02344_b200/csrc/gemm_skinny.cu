@@ -28,9 +28,12 @@ __global__ void __launch_bounds__(NT) k_skinny_fwd(GemmP p, int tpr, int rpb, in
   const int lane = threadIdx.x % tpr, rl = threadIdx.x / tpr;
   const int n0 = lane * VEC;
   if (n0 >= N) return;
-  float bias[VEC];
+  float bias[VEC], sc[VEC];
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) bias[v] = p.bias ? p.bias[(int64_t)b * p.bias_bs + n0 + v] : 0.f;
+  for (int v = 0; v < VEC; ++v) {
+    bias[v] = p.bias ? p.bias[(int64_t)b * p.bias_bs + n0 + v] : 0.f;
+    sc[v] = p.scale ? p.scale[(int64_t)b * p.scale_bs + n0 + v] : 1.f;   // fused BN apply: act(acc*sc + bias)
+  }
   constexpr int KR = KT > 0 ? KT : 1;
   float wr[KR][VEC];
   if constexpr (KT > 0) {
@@ -49,7 +52,7 @@ __global__ void __launch_bounds__(NT) k_skinny_fwd(GemmP p, int tpr, int rpb, in
     const float* br = p.bias && p.bias_div > 0 ? p.bias + (int64_t)b * p.bias_bs + (m / p.bias_div) * p.bias_ld : nullptr;
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
-      float acc = br ? br[n0 + v] : bias[v];
+      float acc = 0.f;
       if constexpr (KT > 0) {
 #pragma unroll
         for (int k = 0; k < KT; ++k) acc = fmaf(a[k], wr[k][v], acc);
@@ -58,7 +61,7 @@ __global__ void __launch_bounds__(NT) k_skinny_fwd(GemmP p, int tpr, int rpb, in
         for (int k = 0; k < KMAX; ++k)
           if (k < K) acc = fmaf(a[k], w[k * N + n0 + v], acc);
       }
-      o[v] = acc;
+      o[v] = act_fwd(fmaf(acc, sc[v], br ? br[n0 + v] : bias[v]), p.act, p.act_alpha);
     }
     st_vec<T, VEC>(C + m * p.c_ld + n0, o);
   }
@@ -99,9 +102,26 @@ __global__ void __launch_bounds__(NT) k_skinny_dgrad(GemmP p, int tpr) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
     if (lane == 0) {
+      if (p.K2 > 0) {   // + A2[m] M2 + bias: the Gram-form BN backward's X M + v term (M2 fp32 [K2][Nj])
+        const T* a2 = reinterpret_cast<const T*>(p.A2) + (int64_t)b * p.a2_bs + m * p.a2_ld;
+        const float* M2 = reinterpret_cast<const float*>(p.Bm2) + (int64_t)b * p.b2_bs;
+        for (int k = 0; k < (int)p.K2; ++k) {
+          const float xk = ldf(a2 + k);
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < Nj) stf(C + m * p.c_ld + j, acc[j]);
+          for (int j = 0; j < 4; ++j)
+            if (j < Nj) acc[j] = fmaf(xk, M2[k * Nj + j], acc[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j >= Nj) break;
+        float vj = acc[j] + (p.bias ? p.bias[(int64_t)b * p.bias_bs + j] : 0.f);
+        if (p.mask) {
+          const float mk = ldf(reinterpret_cast<const T*>(p.mask) + (int64_t)b * p.mask_bs + m * p.mask_ld + j);
+          vj *= mk > 0.f ? 1.f : (p.mask_act == HFTA_ACT_LEAKY_RELU ? p.mask_alpha : 0.f);
+        }
+        stf(C + m * p.c_ld + j, vj);
+      }
     }
   }
 }
@@ -275,8 +295,9 @@ __global__ void k_smallm_fin(GemmP p, int chunks, const float* __restrict__ part
 }  // namespace
 
 // ---- dispatch predicates (called from linear.cu / conv.cu) ----
-static bool gemv_fwd_ok(const GemmP& p) { return p.a_kmajor && p.b_kmajor && p.N <= KMAX && p.splits == 1; }
-static bool smallk_ok(const GemmP& p) { return p.a_kmajor && p.K <= KMAX && p.splits == 1 && !p.accumulate; }
+static bool plain(const GemmP& p) { return !p.scale && p.act == HFTA_ACT_NONE && !p.mask && p.K2 == 0; }
+static bool gemv_fwd_ok(const GemmP& p) { return p.a_kmajor && p.b_kmajor && p.N <= KMAX && p.splits == 1 && plain(p); }
+static bool smallk_ok(const GemmP& p) { return p.a_kmajor && p.K <= KMAX && p.splits == 1 && !p.accumulate && plain(p); }
 static bool smallm_wgrad_ok(const GemmP& p) { return !p.a_kmajor && !p.b_kmajor && p.M <= KMAX; }
 bool skinny_fwd_ok_base(const GemmP& p) { return p.a_kmajor && p.b_kmajor && p.K <= KMAX && p.N <= 512 && p.splits == 1; }
 bool skinny_dgrad_ok(const GemmP& p) {
@@ -363,6 +384,7 @@ hfta_status gemm_skinny(const GemmP& p, hfta_dtype dt, void* ws, size_t ws_bytes
     if (tpr * vec != p.K) { tpr = 1; }
     const int rpb = NT / tpr;
     dim3 grid((unsigned)std::min<int64_t>(cdiv(p.M, rpb), cdiv(16 * 148, p.B)), p.B);
+    HFTA_REQUIRE(tpr > 1 || plain(p), HFTA_ERR_UNSUPPORTED, "skinny dgrad: fused terms need K %% 8 == 0");
     if (tpr == 1) {   // generic: one thread per row, the whole row
       if (bf) k_skinny_dgrad_row<__nv_bfloat16><<<grid, NT, 0, s>>>(p);
       else k_skinny_dgrad_row<float><<<grid, NT, 0, s>>>(p);

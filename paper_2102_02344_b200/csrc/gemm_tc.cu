@@ -37,6 +37,11 @@ struct TcArgs {
   int accumulate;
   float* part;
   int tiles_m, tiles_n;
+  // EPI extensions
+  const float* scale; int64_t scale_bs;
+  int act; float act_alpha;
+  const __nv_bfloat16* mask; int64_t mask_bs, mask_ld; int mask_act; float mask_alpha;
+  int64_t K2;                        // second K segment (maps tmA2 / tmB2)
 };
 
 // BRES ("B resident", forward layers with K <= 128): the B operand (the
@@ -44,10 +49,14 @@ struct TcArgs {
 // while the CTA sweeps consecutive m-tiles of the same (model, n-tile) --
 // the static schedule gives each CTA ~M/128/148*B such tiles in a row -- so
 // only the activation tile streams through the ring (cuts L2->SM traffic 3x).
-template <bool A_MN, bool B_MN, int BN, int STAGES, bool OUT_F32, bool BRES>
+// EPI: bf16-output epilogue with per-column scale, activation and an
+// activation-derivative mask (fused BatchNorm apply / backward gating), and a
+// second K segment (A2, B2) accumulated into the same tile (non-BRES only).
+template <bool A_MN, bool B_MN, int BN, int STAGES, bool OUT_F32, bool BRES, bool EPI>
 __global__ void __launch_bounds__(NTHREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-          const __grid_constant__ CUtensorMap tmC, TcArgs p) {
+          const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
+          const __grid_constant__ CUtensorMap tmB2, TcArgs p) {
   constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB
   constexpr uint32_t B_BYTES = BN * BK * 2;
   constexpr uint32_t STAGE_BYTES = BRES ? A_BYTES : A_BYTES + B_BYTES;
@@ -69,6 +78,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   // per-epilogue-warp staging for the TMA store: 2 buffers x 32 rows x 64 B
   uint8_t* stage_out = bres + BRES_BYTES + 1024;                   // NEPI warps x 2 x 4 KB
   float* sbias_all = reinterpret_cast<float*>(stage_out + NEPI * 2 * 4096);   // NEPI warps x BN floats
+  float* sscale_all = sbias_all + NEPI * BN;                                   // EPI: NEPI warps x BN floats
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -110,7 +120,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int b = (int)(r / p.splits);
         const int64_t kbeg = (int64_t)split * p.k_chunk;
         const int64_t kend = min(p.K, kbeg + p.k_chunk);
-        const int nkb = (int)((kend - kbeg + BK - 1) / BK);
+        const int nkb1 = (int)((kend - kbeg + BK - 1) / BK);
+        const int nkb = nkb1 + (EPI ? (int)((p.K2 + BK - 1) / BK) : 0);
         const int ba = p.a_shared ? 0 : b, bb = p.b_shared ? 0 : b;
         const int m0 = mt * BM, n0 = nt * BN;
         if constexpr (BRES) {
@@ -131,13 +142,18 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           (void)sb;
           const int k0 = (int)(kbeg + (int64_t)kb * BK);
-          if (A_MN) {
+          if (EPI && kb >= nkb1) {                        // second K segment (K-major A2, B2)
+            const int k2 = (kb - nkb1) * BK;
+            tma_load_3d(sa, &tmA2, &full[stage], k2, m0, b);
+            if constexpr (!BRES) tma_load_3d(sb, &tmB2, &full[stage], k2, n0, b);
+          } else if (A_MN) {
             tma_load_3d(sa, &tmA, &full[stage], m0, k0, ba);
             tma_load_3d(sa + 8192, &tmA, &full[stage], m0 + 64, k0, ba);
           } else {
             tma_load_3d(sa, &tmA, &full[stage], k0, m0, ba);
           }
-          if constexpr (!BRES) {
+          if (EPI && kb >= nkb1) {
+          } else if constexpr (!BRES) {
             if (B_MN) {
 #pragma unroll
               for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
@@ -176,7 +192,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
       const int64_t kbeg = (int64_t)split * p.k_chunk;
       const int64_t kend = min(p.K, kbeg + p.k_chunk);
-      const int nkb = (int)((kend - kbeg + BK - 1) / BK);
+      const int nkb = (int)((kend - kbeg + BK - 1) / BK) + (EPI ? (int)((p.K2 + BK - 1) / BK) : 0);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -210,6 +226,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;             // two warps per quarter split the 64-column steps
     const uint32_t sbias = smem_u32(sbias_all + (warp - 2) * BN);
+    const uint32_t sscale = smem_u32(sscale_all + (warp - 2) * BN);
     constexpr int NSTEP = BN / 64;
     const int my_steps = (NSTEP - half + 1) / 2;
     uint32_t sbuf = 0;
@@ -239,6 +256,15 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         __syncwarp();
       }
+      if (EPI && p.scale) {               // per-tile scale slice -> this warp's smem
+        const float* ssrc = p.scale + (int64_t)b * p.scale_bs + (int64_t)nt * BN;
+#pragma unroll
+        for (int jj = 0; jj < BN / 32; ++jj) {
+          const int64_t n = (int64_t)nt * BN + jj * 32 + lane;
+          st_shared_f32(sscale + (jj * 32 + lane) * 4, n < p.N ? ssrc[jj * 32 + lane] : 0.f);
+        }
+        __syncwarp();
+      }
       if (my_steps == 0) {               // nothing for this warp in this tile: release at once
         tc_fence_before();
         __syncwarp();
@@ -262,6 +288,13 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         float v[64];
 #pragma unroll
         for (int q = 0; q < 64; ++q) v[q] = __uint_as_float(u[q]);
+        if (EPI && p.scale) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float4 t4 = ld_shared_f4(sscale + (j * 64 + 4 * q) * 4);
+            v[4 * q] *= t4.x; v[4 * q + 1] *= t4.y; v[4 * q + 2] *= t4.z; v[4 * q + 3] *= t4.w;
+          }
+        }
         if (vbias) {
 #pragma unroll
           for (int q = 0; q < 16; ++q) {               // smem broadcast
@@ -272,6 +305,29 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
           for (int q = 0; q < 64; ++q)
             if (n0 + q < p.N) v[q] += brow[n0 + q];
+        }
+        if constexpr (EPI) {
+          if (p.act != HFTA_ACT_NONE) {
+#pragma unroll
+            for (int q = 0; q < 64; ++q) v[q] = act_fwd(v[q], p.act, p.act_alpha);
+          }
+          if (p.mask && row_ok) {            // v *= act'(previous activation) (ReLU: mask > 0)
+            const __nv_bfloat16* mrow = p.mask + (int64_t)b * p.mask_bs + m * p.mask_ld + n0;
+            const bool full = n0 + 64 <= p.N;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float mv[8];
+              if (full) {
+                ld_vec<__nv_bfloat16, 8>(mrow + 8 * q, mv);
+              } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) mv[e] = n0 + 8 * q + e < p.N ? __bfloat162float(mrow[8 * q + e]) : 0.f;
+              }
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                v[8 * q + e] *= mv[e] > 0.f ? 1.f : (p.mask_act == HFTA_ACT_LEAKY_RELU ? p.mask_alpha : 0.f);
+            }
+          }
         }
         if constexpr (!OUT_F32) {
           // bf16: stage the warp's 32 x 64 sub-tile (128-B rows, TMA SWIZZLE_128B layout:
@@ -333,11 +389,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   }
 }
 
-template <bool A_MN, bool B_MN, int BN, bool OUT_F32, bool BRES>
+template <bool A_MN, bool B_MN, int BN, bool OUT_F32, bool BRES, bool EPI = false>
 hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   constexpr int STAGES = BRES ? 4 : ((BN == 256) ? 3 : 4);
   constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + (BRES ? 0 : BN * BK * 2)) +
-                          (BRES ? 2 * BN * BK * 2 : 0) + 1024 + NEPI * 2 * 4096 + NEPI * BN * 4;
+                          (BRES ? 2 * BN * BK * 2 : 0) + 1024 + NEPI * 2 * 4096 + NEPI * BN * 4 * (EPI ? 2 : 1);
   static_assert(SMEM <= 232448, "shared memory budget");
   if (hfta_status st = get_encode()) return st;
   CUtensorMap ta, tb;
@@ -349,6 +405,11 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   if (B_MN) st = make_map(&tb, p.Bm, p.N, p.K, p.b_ld, p.b_bs, nbb, 64, BK);
   else st = make_map(&tb, p.Bm, p.K, p.N, p.b_ld, p.b_bs, nbb, BK, BN);
   if (st) return st;
+  CUtensorMap ta2 = ta, tb2 = tb;
+  if (EPI && p.K2 > 0) {
+    if (hfta_status st2 = make_map(&ta2, p.A2, p.K2, p.M, p.a2_ld, p.a2_bs, p.B, BK, BM)) return st2;
+    if (hfta_status st2 = make_map(&tb2, p.Bm2, p.K2, p.N, p.b2_ld, p.b2_bs, p.B, BK, BN)) return st2;
+  }
   CUtensorMap tc_ = tb;
   if (!OUT_F32 && p.splits == 1) {
     cuuint64_t dims[3] = {(cuuint64_t)p.N, (cuuint64_t)p.M, (cuuint64_t)p.B};
@@ -368,7 +429,11 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   a.accumulate = p.accumulate; a.part = p.part;
   a.tiles_m = (int)cdiv(p.M, BM); a.tiles_n = (int)cdiv(p.N, BN);
   a.order = (A_MN && B_MN) ? 1 : 0;
-  auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, BRES>;
+  a.scale = p.scale; a.scale_bs = p.scale_bs; a.act = p.act; a.act_alpha = p.act_alpha;
+  a.mask = reinterpret_cast<const __nv_bfloat16*>(p.mask); a.mask_bs = p.mask_bs; a.mask_ld = p.mask_ld;
+  a.mask_act = p.mask_act; a.mask_alpha = p.mask_alpha;
+  a.K2 = EPI ? p.K2 : 0;
+  auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, BRES, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
@@ -376,14 +441,23 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   }
   int64_t total = (int64_t)a.tiles_m * a.tiles_n * a.splits * a.B;
   int grid = (int)std::min<int64_t>(total, num_sms());
-  kern<<<grid, NTHREADS, SMEM, s>>>(ta, tb, tc_, a);
+  kern<<<grid, NTHREADS, SMEM, s>>>(ta, tb, tc_, ta2, tb2, a);
   count_launches(1);
   return post_launch(s, "gemm_tc");
 }
 
+bool needs_epi(const GemmP& p) { return p.scale || p.act != HFTA_ACT_NONE || p.mask || p.K2 > 0; }
+
 template <bool A_MN, bool B_MN, bool OUT_F32>
 hfta_status dispatch_bn(const GemmP& p, cudaStream_t s) {
   if constexpr (!A_MN && !B_MN && !OUT_F32) {
+    if (needs_epi(p)) {                          // fused BN apply / gated dgrad (N <= 128)
+      const bool bres = p.K2 == 0 && p.K <= 2 * BK;
+      if (p.N <= 64) return bres ? launch_tc<false, false, 64, false, true, true>(p, s)
+                                 : launch_tc<false, false, 64, false, false, true>(p, s);
+      return bres ? launch_tc<false, false, 128, false, true, true>(p, s)
+                  : launch_tc<false, false, 128, false, false, true>(p, s);
+    }
     if (p.K <= 2 * BK && p.splits == 1) {        // forward with small K: B-resident schedule
       if (p.N <= 64) return launch_tc<A_MN, B_MN, 64, OUT_F32, true>(p, s);
       if (p.N <= 128) return launch_tc<A_MN, B_MN, 128, OUT_F32, true>(p, s);
@@ -408,6 +482,13 @@ bool env_disabled() {
 
 bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32) {
   if (env_disabled() || dt_in != HFTA_BF16) return false;
+  if (needs_epi(p)) {
+    if (out_f32 || p.splits != 1 || !p.a_kmajor || !p.b_kmajor || p.N > 128 || p.accumulate) return false;
+    if (p.K2 > 0 && (p.K % BK || p.K2 % BK || !aligned16(p.A2) || !aligned16(p.Bm2) || (p.a2_ld * 2) % 16 ||
+                     (p.b2_ld * 2) % 16 || (p.a2_bs * 2) % 16 || (p.b2_bs * 2) % 16))
+      return false;
+    if (p.mask && (!aligned16(p.mask) || p.mask_ld % 8 || p.mask_bs % 8)) return false;
+  }
   if (p.K < 16 || p.N < 16 || p.M < 1) return false;
   if (!aligned16(p.A) || !aligned16(p.Bm)) return false;
   if ((p.a_ld * 2) % 16 || (p.b_ld * 2) % 16 || (p.a_bs * 2) % 16 || (p.b_bs * 2) % 16) return false;

@@ -34,6 +34,7 @@
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
+#include "gemm.cuh"
 #include "tc_common.cuh"
 
 namespace hfta {
@@ -534,7 +535,8 @@ __global__ void __launch_bounds__(SDX_T) k_lbm_sparse_dx(int Ncl, int64_t L, int
                                                          const int32_t* __restrict__ am, const float* __restrict__ sp,
                                                          const __nv_bfloat16* __restrict__ W, int64_t w_bs,
                                                          int64_t w_ld, __nv_bfloat16* __restrict__ dX, int64_t dx_bs,
-                                                         int64_t dx_ld) {
+                                                         int64_t dx_ld, const __nv_bfloat16* __restrict__ mask,
+                                                         int64_t m_bs, int64_t m_ld, int m_act, float m_alpha) {
   using Sort = cub::BlockRadixSort<uint32_t, SDX_T, SDX_ITEMS, int>;
   using Scan = cub::BlockScan<int, SDX_T>;
   __shared__ union {
@@ -597,6 +599,12 @@ __global__ void __launch_bounds__(SDX_T) k_lbm_sparse_dx(int Ncl, int64_t L, int
       for (int e = 0; e < 8; ++e) acc[e] = fmaf(w, x[e], acc[e]);
     }
     __nv_bfloat16* d = dXn + (int64_t)srow[j0] * dx_ld + k8;
+    if (mask) {        // the dense part was gated by act'(X) in the GEMM epilogue: gate the sparse part too
+      float mv[8];
+      ld_vec<__nv_bfloat16, 8>(mask + (int64_t)b * m_bs + ((int64_t)n * L + srow[j0]) * m_ld + k8, mv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] *= mv[e] > 0.f ? 1.f : (m_act == HFTA_ACT_LEAKY_RELU ? m_alpha : 0.f);
+    }
     float y[8];
     ld_vec<__nv_bfloat16, 8>(d, y);
 #pragma unroll
@@ -807,9 +815,10 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
                                          const float* bias, int64_t bias_bstride, const float* gamma,
                                          const float* beta, int64_t gb_bstride, const float* save_mean,
                                          const float* save_invstd, hfta_act act, float act_alpha, hfta_out dX,
-                                         float* dW, int64_t dW_bstride, int64_t dW_ld, float* dbias,
-                                         int64_t dbias_bstride, float* dgamma, float* dbeta, int accumulate,
-                                         void* ws, size_t ws_bytes, hfta_stream stream) {
+                                         hfta_act dX_act, float dX_alpha, float* dW, int64_t dW_bstride,
+                                         int64_t dW_ld, float* dbias, int64_t dbias_bstride, float* dgamma,
+                                         float* dbeta, int accumulate, void* ws, size_t ws_bytes,
+                                         hfta_stream stream) {
   if (hfta_status st = check_common(B, N, L, C, K, dt, X, W)) return st;
   HFTA_REQUIRE(dG.ptr && argmax && ext.ptr && gamma && beta && save_mean && save_invstd && dW && dgamma && dbeta,
                HFTA_ERR_INVALID_VALUE,
@@ -845,15 +854,23 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
   int launches = 2;
   if (dX.ptr) {
     k_lbm_mv<<<dim3((unsigned)cdiv(K, MV_ROWS), (unsigned)B), 256, 0, s>>>(C, (int)K, Wp, wbs, W.ld, coef, M, v);
-    // dX = X M^T + v (M symmetric): the fused forward GEMM with a per-model bias
-    if (hfta_status st = hfta_fused_linear_fwd(B, R, K, K, HFTA_BF16, X, hfta_in{M, K * K, K}, v, K, 0, 0, dX,
-                                               stream))
-      return st;
+    // dX = X M^T + v (M symmetric), times act'(X) when X is an activation output
+    GemmP p{};
+    p.B = B; p.M = R; p.N = K; p.K = K;
+    p.A = X.ptr; p.a_bs = X.bstride; p.a_ld = X.ld; p.a_kmajor = 1;
+    p.Bm = M; p.b_bs = K * K; p.b_ld = K; p.b_kmajor = 1;
+    p.C = dX.ptr; p.c_bs = dX.bstride; p.c_ld = dX.ld;
+    p.bias = v; p.bias_bs = K;
+    if (dX_act != HFTA_ACT_NONE) {
+      p.mask = X.ptr; p.mask_bs = X.bstride; p.mask_ld = X.ld; p.mask_act = (int)dX_act; p.mask_alpha = dX_alpha;
+    }
+    p.splits = 1; p.k_chunk = K;
+    if (hfta_status st = run_gemm(p, HFTA_BF16, false, s)) return st;
     int end_bit = 1;
     while ((int64_t(1) << end_bit) <= L) ++end_bit;       // argmax < L < 2^end_bit - 1 (sentinel)
-    k_lbm_sparse_dx<<<dim3((unsigned)N, (unsigned)B), SDX_T, 0, s>>>((int)N, L, C, (int)K, end_bit, argmax, sp, Wp,
-                                                                     wbs, W.ld, (__nv_bfloat16*)dX.ptr, dX.bstride,
-                                                                     dX.ld);
+    k_lbm_sparse_dx<<<dim3((unsigned)N, (unsigned)B), SDX_T, 0, s>>>(
+        (int)N, L, C, (int)K, end_bit, argmax, sp, Wp, wbs, W.ld, (__nv_bfloat16*)dX.ptr, dX.bstride, dX.ld,
+        dX_act != HFTA_ACT_NONE ? (const __nv_bfloat16*)X.ptr : nullptr, X.bstride, X.ld, (int)dX_act, dX_alpha);
     launches += 2;
   }
   {

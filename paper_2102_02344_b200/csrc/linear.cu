@@ -10,6 +10,14 @@ hfta_status colsum_impl(int B, int64_t rows, int64_t C, int64_t group, hfta_dtyp
                         cudaStream_t s);
 size_t colsum_ws(int B, int64_t rows, int64_t C, int64_t group);
 
+hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void* ws, size_t wsb) {
+  const bool epi = p.scale || p.act != HFTA_ACT_NONE || p.mask || p.K2 > 0;
+  if (skinny_fwd_ok(p) || skinny_dgrad_ok(p) || skinny_wgrad_ok(p)) return gemm_skinny(p, dt, ws, wsb, s);
+  if (gemm_tc_supported(p, dt, out_f32)) return gemm_tc(p, dt, out_f32, s);
+  if (epi) return fail(HFTA_ERR_UNSUPPORTED, "fused epilogue / second K segment needs the tensor-core or skinny path");
+  return gemm_simt(p, dt, out_f32, s);
+}
+
 namespace {
 // split-K policy of the weight-gradient contraction (reduction over M rows).
 struct Split { int splits; int64_t chunk; };
@@ -23,11 +31,6 @@ Split wgrad_split(int B, int64_t M, int64_t N, int64_t K) {
   return {(int)splits, chunk};
 }
 
-hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void* ws = nullptr, size_t wsb = 0) {
-  if (skinny_fwd_ok(p) || skinny_dgrad_ok(p) || skinny_wgrad_ok(p)) return gemm_skinny(p, dt, ws, wsb, s);
-  if (gemm_tc_supported(p, dt, out_f32)) return gemm_tc(p, dt, out_f32, s);
-  return gemm_simt(p, dt, out_f32, s);
-}
 
 hfta_status check_in(const hfta_in& t, const char* name, int B) {
   HFTA_REQUIRE(t.ptr, HFTA_ERR_INVALID_VALUE, "%s.ptr is NULL", name);

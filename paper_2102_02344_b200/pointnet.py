@@ -44,6 +44,10 @@ class FusedPointNet(FusedNet):
         # bf16: c3 -> bn3 -> max runs as the fused tensor-core block (K10);
         # the [R][1024] pre-BN activation is never materialised.
         self.fuse_lbm = self.dt == H.HFTA_BF16 and self.c3 % 128 == 0 and self.c3 <= 1024 and self.c2 in (64, 128)
+        # bf16: c1 -> bn1 -> relu and c2 -> bn2 -> relu run in Gram form (K11):
+        # statistics from G = X^T X, BN apply in the GEMM epilogue, backward
+        # without forming dY; the pre-BN y1 / y2 are never stored.
+        self.fuse_bn = self.fuse_lbm and self.c1 in (64, 128) and self.c2 <= 128
         self._alloc()
 
     # ------------------------------------------------------------ buffers --
@@ -55,8 +59,13 @@ class FusedPointNet(FusedNet):
         self.x_dt = torch.empty(R, 3, dtype=self.tdt, device=self.device)
         S = {}
         for p in ("stn", "feat"):
-            S[p + ".y1"], S[p + ".a1"] = a(R, c1), a(R, c1)
-            S[p + ".y2"], S[p + ".a2"] = a(R, c2), a(R, c2)
+            if self.fuse_bn:
+                S[p + ".a1"], S[p + ".a2"] = a(R, c1), a(R, c2)
+                S[p + ".G1"], S[p + ".s1"] = f(3, 3), f(1, 3)          # Gram / column sums of the layer inputs
+                S[p + ".G2"], S[p + ".s2"] = f(c1, c1), f(1, c1)
+            else:
+                S[p + ".y1"], S[p + ".a1"] = a(R, c1), a(R, c1)
+                S[p + ".y2"], S[p + ".a2"] = a(R, c2), a(R, c2)
             if self.fuse_lbm:
                 S[p + ".ext"] = f(N, c3)            # Y at the argmax rows (the block's saved tensor)
             else:
@@ -91,8 +100,11 @@ class FusedPointNet(FusedNet):
             S["d.pf"] = a(R, c1)                    # gradient reaching the point feature from the head
         if not self.fuse_lbm:
             S["d.big"] = a(R, c3)
-        S["d.c2a"], S["d.c2b"] = a(R, c2), a(R, c2)
-        S["d.c1a"], S["d.c1b"] = a(R, c1), a(R, c1)
+        if self.fuse_bn:
+            S["d.c2a"], S["d.c1a"] = a(R, c2), a(R, c1)
+        else:
+            S["d.c2a"], S["d.c2b"] = a(R, c2), a(R, c2)
+            S["d.c1a"], S["d.c1b"] = a(R, c1), a(R, c1)
         S["d.g"] = f(N, c3)
         S["d.xt"] = a(R, 3)
         S["d.f3"] = f(N, 9)
@@ -112,6 +124,9 @@ class FusedPointNet(FusedNet):
         ws.reserve(H.hfta_bn_max_bwd_workspace(B, N, c3))
         if self.fuse_lbm:
             ws.reserve(H.hfta_fused_linear_bn_max_workspace(B, N, self.L, c3, c2))
+        if self.fuse_bn:
+            ws.reserve(H.hfta_fused_linear_bn_workspace(B, R, c1, 3))
+            ws.reserve(H.hfta_fused_linear_bn_workspace(B, R, c2, c1))
         if self.task == "seg":
             for (M, Nn, K) in [(R, self.h1w, c1), (N, self.h1w, c3), (R, self.h2w, self.h1w), (R, self.h3w, self.h2w),
                                (R, self.k, self.h3w)]:
@@ -167,8 +182,9 @@ class FusedPointNet(FusedNet):
                                        _out(S[p + ".ext"]), H.ptr(sm), H.ptr(si), self.ws.ptr, self.ws.nbytes, s)
         self._pend(e0)
 
-    def _block_bwd(self, p, act, s):
-        """Backward of _block_fwd from d.g; writes d.c2a (grad of a2) and the c3/bn3 gradients."""
+    def _block_bwd(self, p, act, s, dx_act=A_NONE):
+        """Backward of _block_fwd from d.g; writes d.c2a (grad of a2, times act'(a2) when dx_act is
+        set, i.e. the c2 layer's dZ) and the c3/bn3 gradients."""
         S, R = self.S, self.R
         if not self.fuse_lbm:
             self._bn_max_bwd(S["d.g"], S[p + ".y3"], S[p + ".amax"], p + ".bn3", act, S["d.big"], s)
@@ -181,10 +197,83 @@ class FusedPointNet(FusedNet):
                                        _in(S[p + ".a2"]), ar.w_in(p + ".c3.W", self.dt), H.ptr(S[p + ".amax"]),
                                        _in(S[p + ".ext"]), ar.fptr("p", p + ".c3.b"), P, ar.fptr("p", bn + ".g"),
                                        ar.fptr("p", bn + ".beta"), P, H.ptr(sm), H.ptr(si), act, self.act_alpha,
-                                       _out(S["d.c2a"]), ar.fptr("g", p + ".c3.W"), P, self.c2,
+                                       _out(S["d.c2a"]), dx_act, self.act_alpha, ar.fptr("g", p + ".c3.W"), P, self.c2,
                                        ar.fptr("g", p + ".c3.b"), P, ar.fptr("g", bn + ".g"), ar.fptr("g", bn + ".beta"),
                                        0, self.ws.ptr, self.ws.nbytes, s)
         self._pend(e0)
+
+    def _lbn_fwd(self, p, i, X, K, s):
+        """Fused c{i} -> bn{i} -> relu of branch p (Gram form).  X: hfta_in of the layer input."""
+        S, ar, P = self.S, self.arena, self.arena.P
+        lin, bn = "%s.c%d" % (p, i), "%s.bn%d" % (p, i)
+        Nn = self.arena.shape[lin + ".W"][0]
+        rm, rv = self.running[bn]
+        sm, si = self.saved[bn]
+        H.hfta_fused_linear_bn_fwd(self.B, self.R, Nn, K, self.dt, X, ar.w_in(lin + ".W", self.dt),
+                                   ar.fptr("p", lin + ".b"), P, ar.fptr("p", bn + ".g"), ar.fptr("p", bn + ".beta"), P,
+                                   H.ptr(rm), H.ptr(rv), 0.1, 1e-5, A_RELU, self.act_alpha,
+                                   _out(S["%s.a%d" % (p, i)]), H.ptr(sm), H.ptr(si), H.ptr(S["%s.G%d" % (p, i)]),
+                                   H.ptr(S["%s.s%d" % (p, i)]), self.ws.ptr, self.ws.nbytes, s)
+
+    def _lbn_bwd(self, p, i, dZ, X, K, dX, dx_act, s):
+        """Backward of _lbn_fwd from dZ (gradient at bn{i}'s output, relu' applied)."""
+        S, ar, P = self.S, self.arena, self.arena.P
+        lin, bn = "%s.c%d" % (p, i), "%s.bn%d" % (p, i)
+        Nn = self.arena.shape[lin + ".W"][0]
+        sm, si = self.saved[bn]
+        H.hfta_fused_linear_bn_bwd(self.B, self.R, Nn, K, self.dt, _in(dZ), X, ar.w_in(lin + ".W", self.dt),
+                                   ar.fptr("p", lin + ".b"), P, ar.fptr("p", bn + ".g"), P, H.ptr(sm), H.ptr(si),
+                                   H.ptr(S["%s.G%d" % (p, i)]), H.ptr(S["%s.s%d" % (p, i)]),
+                                   _out(dX) if dX is not None else H.tout(None, 0, 1), dx_act, self.act_alpha,
+                                   ar.fptr("g", lin + ".W"), P, K, ar.fptr("g", lin + ".b"), P,
+                                   ar.fptr("g", bn + ".g"), ar.fptr("g", bn + ".beta"), 0, self.ws.ptr,
+                                   self.ws.nbytes, s)
+
+    def _stn_feat_fwd_fused(self, x, s):
+        S = self.S
+        self._lbn_fwd("stn", 1, H.tin(self.x_dt, 0, 3), 3, s)
+        self._lbn_fwd("stn", 2, _in(S["stn.a1"]), self.c1, s)
+        self._block_fwd("stn", A_RELU, s)
+        self._stn_head_fwd(s)
+        H.hfta_transform_points_fwd(self.B, self.N, self.L, self.dt, H.tin(x, 0, 3), _in(S["stn.f3"]), 1,
+                                    _out(S["feat.xt"]), s)
+        self._lbn_fwd("feat", 1, _in(S["feat.xt"]), 3, s)
+        self._lbn_fwd("feat", 2, _in(S["feat.a1"]), self.c1, s)
+        self._block_fwd("feat", A_NONE, s)
+
+    def _stn_feat_bwd_fused(self, x, s):
+        S, R, N = self.S, self.R, self.N
+        seg = self.task == "seg"
+        # feat: K10 bwd -> dZ2 (gated by relu'(a2)); c2 -> dZ1 (gated by relu'(a1), after the
+        # seg head's gradient is added for seg); c1 -> d xt
+        self._block_bwd("feat", A_NONE, s, dx_act=A_RELU)
+        self._lbn_bwd("feat", 2, S["d.c2a"], _in(S["feat.a1"]), self.c1, S["d.c1a"], A_NONE if seg else A_RELU, s)
+        if seg:      # the point feature a1 also feeds the seg head: add its gradient, then relu'
+            H.hfta_add(self.B, R, self.c1, self.dt, _in(S["d.c1a"]), _in(S["d.pf"]), _out(S["d.c1a"]), s)
+            H.hfta_act_bwd(self.B, R, self.c1, self.dt, A_RELU, self.act_alpha, _in(S["feat.a1"]), _in(S["d.c1a"]),
+                           _out(S["d.c1a"]), s)
+        self._lbn_bwd("feat", 1, S["d.c1a"], _in(S["feat.xt"]), 3, S["d.xt"], A_NONE, s)
+        H.hfta_transform_points_bwd(self.B, N, self.L, self.dt, H.tin(x, 0, 3), _in(S["d.xt"]), _out(S["d.f3"]), s)
+        self._stn_head_bwd(s)
+        self._block_bwd("stn", A_RELU, s, dx_act=A_RELU)
+        self._lbn_bwd("stn", 2, S["d.c2a"], _in(S["stn.a1"]), self.c1, S["d.c1a"], A_RELU, s)
+        self._lbn_bwd("stn", 1, S["d.c1a"], H.tin(self.x_dt, 0, 3), 3, None, A_NONE, s)
+
+    def _stn_head_fwd(self, s):
+        S = self.S
+        self._lin_fwd(_in(S["stn.g"]), self.N, "stn.fc1", S["stn.f1"], s)
+        self._bn_fwd(S["stn.f1"], "stn.bn4", A_RELU, S["stn.h4"], s)
+        self._lin_fwd(_in(S["stn.h4"]), self.N, "stn.fc2", S["stn.f2"], s)
+        self._bn_fwd(S["stn.f2"], "stn.bn5", A_RELU, S["stn.h5"], s)
+        self._lin_fwd(_in(S["stn.h5"]), self.N, "stn.fc3", S["stn.f3"], s)
+
+    def _stn_head_bwd(self, s):
+        S, N = self.S, self.N
+        self._lin_bwd(S["d.f3"], _in(S["stn.h5"]), N, "stn.fc3", S["d.sf2a"], s)
+        self._bn_bwd(S["d.sf2a"], S["stn.f2"], "stn.bn5", A_RELU, S["d.sf2b"], s)
+        self._lin_bwd(S["d.sf2b"], _in(S["stn.h4"]), N, "stn.fc2", S["d.sf1a"], s)
+        self._bn_bwd(S["d.sf1a"], S["stn.f1"], "stn.bn4", A_RELU, S["d.sf1b"], s)
+        self._lin_bwd(S["d.sf1b"], _in(S["stn.g"]), N, "stn.fc1", S["d.g"], s)
 
     def _stn_feat_fwd(self, x, s):
         S, R = self.S, self.R
@@ -307,12 +396,14 @@ class FusedPointNet(FusedNet):
             self.x_dt = x
         else:
             H.hfta_cast_f32_bf16(self.R * 3, H.ptr(x), H.ptr(self.x_dt), s)
-        self._stn_feat_fwd(x, s)
+        fwd, bwd = ((self._stn_feat_fwd_fused, self._stn_feat_bwd_fused) if self.fuse_bn
+                    else (self._stn_feat_fwd, self._stn_feat_bwd))
+        fwd(x, s)
         if self.task == "cls":
             self._cls_head(s)
         else:
             self._seg_head(s)
-        self._stn_feat_bwd(x, s)
+        bwd(x, s)
 
     def step(self, x=None, labels=None, stream=None):
         """One fused training step for all B models; returns the loss vector [B]."""

@@ -47,7 +47,7 @@ def host(t):
 ACT = {0: (lambda z: z, lambda d, z: d), 1: (OL.relu, OL.relu_bwd)}
 
 
-def run_block(B, N, L, C, K, act, shared=False, seed=0, accumulate=0, neg_gamma=True):
+def run_block(B, N, L, C, K, act, shared=False, seed=0, accumulate=0, neg_gamma=True, dx_act=0):
     rng = np.random.default_rng(seed)
     R = N * L
     X = bf(np.maximum(rng.standard_normal((1 if shared else B, R, K)), 0) + 0.1 * rng.standard_normal((1 if shared else B, R, K)))
@@ -82,13 +82,22 @@ def run_block(B, N, L, C, K, act, shared=False, seed=0, accumulate=0, neg_gamma=
     dbias = torch.full((B, C), 7.0, device=DEV)
     H.hfta_fused_linear_bn_max_bwd(B, N, L, C, K, 1, H.tin(dGd, N * C, C), H.tin(Xd, xbs, K), H.tin(Wd, C * K, K),
                                    H.ptr(am), H.tin(ext, N * C, C), H.ptr(bd), C, H.ptr(gd), H.ptr(bed), C, H.ptr(sm),
-                                   H.ptr(si), act, 0.0, H.tout(dX, R * K, K), H.ptr(dW), C * K, K, H.ptr(dbias), C,
+                                   H.ptr(si), act, 0.0, H.tout(dX, R * K, K), dx_act, 0.0, H.ptr(dW), C * K, K, H.ptr(dbias), C,
                                    H.ptr(dgam), H.ptr(dbet), accumulate, H.ptr(ws), ws.numel(), s())
     torch.cuda.synchronize()
     out = dict(G=host(G), ext=host(ext), am=am.cpu().numpy().astype(np.int64), sm=host(sm), si=host(si),
                rm=host(rm), rv=host(rv), dX=host(dX), dW=host(dW), dg=host(dgam), db=host(dbet), dbias=host(dbias))
     inp = dict(X=X, W=W, bias=bias, g=g, be=be, rm0=rm0, rv0=rv0, dG=dG, dW0=dW0, dg0=dg0)
     return out, inp
+
+
+def test_linear_bn_max_gated_dx():
+    """dX_act = ReLU: dX is multiplied by act'(X) (X > 0), the previous layer's dZ."""
+    B, N, L, C, K, act = 2, 3, 700, 256, 128, 1
+    out, inp = run_block(B, N, L, C, K, act, seed=11, dx_act=1)
+    for b in range(B):
+        o = oracle_block(inp, b, N, L, act, False)
+        assert_close(out["dX"][b], o["dX"] * (inp["X"][b] > 0), 2e-2, "gated dX")
 
 
 def oracle_block(inp, b, N, L, act, shared):

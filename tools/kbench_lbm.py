@@ -41,7 +41,7 @@ def fwd():
 def bwd():
     H.hfta_fused_linear_bn_max_bwd(B, N, L, C, K, 1, H.tin(dG, N * C, C), H.tin(X, R * K, K), H.tin(W, C * K, K),
                                    H.ptr(am), H.tin(ext, N * C, C), H.ptr(bias), C, H.ptr(g), H.ptr(be), C, H.ptr(sm),
-                                   H.ptr(si), 1, 0.0, H.tout(dX, R * K, K), H.ptr(dW), C * K, K, H.ptr(dbias), C,
+                                   H.ptr(si), 1, 0.0, H.tout(dX, R * K, K), 1, 0.0, H.ptr(dW), C * K, K, H.ptr(dbias), C,
                                    H.ptr(dg), H.ptr(db), 0, H.ptr(ws), ws.numel(), s)
 
 
