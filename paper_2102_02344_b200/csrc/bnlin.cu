@@ -44,9 +44,9 @@ __global__ void k_bnl_stats(int B, int64_t R, int64_t C, int K, const float* __r
   const float* Gb = G + b * (int64_t)K * K;
   // q = W_c G W_c^T, m1 = W_c . s  (lanes over k)
   double q = 0.0, m1 = 0.0;
-  for (int k = lane; k < K; k += 32) {
+  for (int k = lane; k < K; k += 32) {      // G symmetric: read column k (lanes consecutive -> coalesced)
     double t = 0.0;
-    for (int j = 0; j < K; ++j) t += (double)Gb[(int64_t)k * K + j] * (double)__bfloat162float(Wc[j]);
+    for (int j = 0; j < K; ++j) t += (double)Gb[(int64_t)j * K + k] * (double)__bfloat162float(Wc[j]);
     const double wk = (double)__bfloat162float(Wc[k]);
     q += wk * t;
     m1 += wk * (double)sv[b * K + k];

@@ -42,6 +42,8 @@ struct TcArgs {
   int act; float act_alpha;
   const __nv_bfloat16* mask; int64_t mask_bs, mask_ld; int mask_act; float mask_alpha;
   int64_t K2;                        // second K segment (maps tmA2 / tmB2)
+  int mask_kb;                       // >= 0: the gating tensor is the A tile of k-blocks mask_kb..:
+                                     // read from the resident smem stage (released by the epilogue)
 };
 
 // BRES ("B resident", forward layers with K <= 128): the B operand (the
@@ -82,7 +84,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], (EPI && p.mask_kb >= 0) ? 1 + NEPI : 1);   // + epilogue arrivals (mask read)
+    }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], NEPI); }
     mbar_init(bfull, 1);
     mbar_init(bempty, 1);
@@ -232,6 +237,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     uint32_t sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int64_t cur_key = -1;
+    int estage = 0;                               // stage counter mirrored from the producer (mask_kb >= 0)
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
       int64_t r = t;
       int mt, nt;
@@ -239,31 +246,42 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       else { mt = (int)(r % p.tiles_m); r /= p.tiles_m; nt = (int)(r % p.tiles_n); r /= p.tiles_n; }
       const int split = (int)(r % p.splits);
       const int b = (int)(r / p.splits);
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
       const int64_t m = (int64_t)mt * BM + quarter * 32 + lane;
       const bool row_ok = m < p.M;
+      // per-(model, n-tile) bias / scale slices: reloaded only when the key
+      // changes (BRES schedules sweep many m-tiles per key), loaded into
+      // registers BEFORE the accumulator wait so the latency overlaps the MMAs
+      const bool vbias = p.bias && p.bias_div == 0;
+      const int64_t key = (int64_t)b * p.tiles_n + nt;
+      const bool reload = key != cur_key;
+      float bpre[BN / 32], spre[BN / 32];
+      if (reload) {
+#pragma unroll
+        for (int jj = 0; jj < BN / 32; ++jj) {
+          const int64_t n = (int64_t)nt * BN + jj * 32 + lane;
+          bpre[jj] = (vbias && n < p.N) ? p.bias[(int64_t)b * p.bias_bs + n] : 0.f;
+          spre[jj] = (EPI && p.scale && n < p.N) ? p.scale[(int64_t)b * p.scale_bs + n] : 0.f;
+        }
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
       const float* brow = nullptr;       // per-row bias table (row-grouped bias only)
       if (p.bias && p.bias_div > 0 && row_ok)
         brow = p.bias + (int64_t)b * p.bias_bs + (m / p.bias_div) * p.bias_ld;
-      const bool vbias = p.bias && p.bias_div == 0;
-      if (vbias) {                       // per-tile bias slice -> this warp's smem (broadcast reads later)
-        const float* bsrc = p.bias + (int64_t)b * p.bias_bs + (int64_t)nt * BN;
+      if (reload) {                      // this warp's smem copies (broadcast reads later)
 #pragma unroll
         for (int jj = 0; jj < BN / 32; ++jj) {
-          const int64_t n = (int64_t)nt * BN + jj * 32 + lane;
-          st_shared_f32(sbias + (jj * 32 + lane) * 4, n < p.N ? bsrc[jj * 32 + lane] : 0.f);
+          st_shared_f32(sbias + (jj * 32 + lane) * 4, bpre[jj]);
+          if (EPI) st_shared_f32(sscale + (jj * 32 + lane) * 4, spre[jj]);
         }
         __syncwarp();
+        cur_key = key;
       }
-      if (EPI && p.scale) {               // per-tile scale slice -> this warp's smem
-        const float* ssrc = p.scale + (int64_t)b * p.scale_bs + (int64_t)nt * BN;
-#pragma unroll
-        for (int jj = 0; jj < BN / 32; ++jj) {
-          const int64_t n = (int64_t)nt * BN + jj * 32 + lane;
-          st_shared_f32(sscale + (jj * 32 + lane) * 4, n < p.N ? ssrc[jj * 32 + lane] : 0.f);
-        }
-        __syncwarp();
+      const bool mask_smem = EPI && p.mask_kb >= 0;
+      int tile_nkb = 0;
+      if (mask_smem) {
+        const int64_t kbeg_ = (int64_t)split * p.k_chunk, kend_ = min(p.K, kbeg_ + p.k_chunk);
+        tile_nkb = (int)((kend_ - kbeg_ + BK - 1) / BK) + (int)((p.K2 + BK - 1) / BK);
       }
       if (my_steps == 0) {               // nothing for this warp in this tile: release at once
         tc_fence_before();
@@ -288,14 +306,21 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         float v[64];
 #pragma unroll
         for (int q = 0; q < 64; ++q) v[q] = __uint_as_float(u[q]);
-        if (EPI && p.scale) {
+        if (EPI && p.scale && vbias) {       // fused BN apply: v = v * scale + shift (one FMA)
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float4 s4 = ld_shared_f4(sscale + (j * 64 + 4 * q) * 4);
+            const float4 t4 = ld_shared_f4(sbias + (j * 64 + 4 * q) * 4);
+            v[4 * q] = fmaf(v[4 * q], s4.x, t4.x); v[4 * q + 1] = fmaf(v[4 * q + 1], s4.y, t4.y);
+            v[4 * q + 2] = fmaf(v[4 * q + 2], s4.z, t4.z); v[4 * q + 3] = fmaf(v[4 * q + 3], s4.w, t4.w);
+          }
+        } else if (EPI && p.scale) {
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const float4 t4 = ld_shared_f4(sscale + (j * 64 + 4 * q) * 4);
             v[4 * q] *= t4.x; v[4 * q + 1] *= t4.y; v[4 * q + 2] *= t4.z; v[4 * q + 3] *= t4.w;
           }
-        }
-        if (vbias) {
+        } else if (vbias) {
 #pragma unroll
           for (int q = 0; q < 16; ++q) {               // smem broadcast
             const float4 t4 = ld_shared_f4(sbias + (j * 64 + 4 * q) * 4);
@@ -307,13 +332,31 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             if (n0 + q < p.N) v[q] += brow[n0 + q];
         }
         if constexpr (EPI) {
-          if (p.act != HFTA_ACT_NONE) {
+          if (p.act == HFTA_ACT_RELU) {      // branch once per step, not per element
 #pragma unroll
-            for (int q = 0; q < 64; ++q) v[q] = act_fwd(v[q], p.act, p.act_alpha);
+            for (int q = 0; q < 64; ++q) v[q] = fmaxf(v[q], 0.f);
+          } else if (p.act == HFTA_ACT_LEAKY_RELU) {
+#pragma unroll
+            for (int q = 0; q < 64; ++q) v[q] = v[q] > 0.f ? v[q] : p.act_alpha * v[q];
           }
-          if (p.mask && row_ok) {            // v *= act'(previous activation) (ReLU: mask > 0)
+          if (mask_smem) {                  // gating values = this tile's A operand, still resident in smem
+            const float neg = p.mask_act == HFTA_ACT_LEAKY_RELU ? p.mask_alpha : 0.f;
+            const int st = (estage + p.mask_kb + j) % STAGES;
+            const uint32_t arow = smem_u32(smem + st * STAGE_BYTES) + (uint32_t)((quarter * 32 + lane) * 128);
+            const uint32_t swz = (uint32_t)(lane & 7);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 raw = ld_shared_f4(arow + (((uint32_t)q ^ swz) << 4));
+              float mv[8];
+              unpack_bf2(__float_as_uint(raw.x), mv[0], mv[1]); unpack_bf2(__float_as_uint(raw.y), mv[2], mv[3]);
+              unpack_bf2(__float_as_uint(raw.z), mv[4], mv[5]); unpack_bf2(__float_as_uint(raw.w), mv[6], mv[7]);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[8 * q + e] *= mv[e] > 0.f ? 1.f : neg;
+            }
+          } else if (p.mask && row_ok) {     // v *= act'(previous activation) (ReLU: mask > 0)
             const __nv_bfloat16* mrow = p.mask + (int64_t)b * p.mask_bs + m * p.mask_ld + n0;
             const bool full = n0 + 64 <= p.N;
+            const float neg = p.mask_act == HFTA_ACT_LEAKY_RELU ? p.mask_alpha : 0.f;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               float mv[8];
@@ -324,8 +367,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 for (int e = 0; e < 8; ++e) mv[e] = n0 + 8 * q + e < p.N ? __bfloat162float(mrow[8 * q + e]) : 0.f;
               }
 #pragma unroll
-              for (int e = 0; e < 8; ++e)
-                v[8 * q + e] *= mv[e] > 0.f ? 1.f : (p.mask_act == HFTA_ACT_LEAKY_RELU ? p.mask_alpha : 0.f);
+              for (int e = 0; e < 8; ++e) v[8 * q + e] *= mv[e] > 0.f ? 1.f : neg;
             }
           }
         }
@@ -377,6 +419,12 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
         }
       }
+      if (mask_smem) {                   // this tile's smem stages may now be refilled
+        __syncwarp();
+        if (lane == 0)
+          for (int k = 0; k < tile_nkb; ++k) mbar_arrive(&empty[(estage + k) % STAGES]);
+        estage = (estage + tile_nkb) % STAGES;
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
@@ -391,7 +439,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
 template <bool A_MN, bool B_MN, int BN, bool OUT_F32, bool BRES, bool EPI = false>
 hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
-  constexpr int STAGES = BRES ? 4 : ((BN == 256) ? 3 : 4);
+  // EPI non-BRES BN=64 (the two-segment gated dgrad): 6 stages so a tile's 3
+  // k-blocks can stay resident for the epilogue while the next tile loads
+  constexpr int STAGES = BRES ? 4 : ((BN == 256) ? 3 : ((EPI && BN == 64) ? 6 : 4));
   constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + (BRES ? 0 : BN * BK * 2)) +
                           (BRES ? 2 * BN * BK * 2 : 0) + 1024 + NEPI * 2 * 4096 + NEPI * BN * 4 * (EPI ? 2 : 1);
   static_assert(SMEM <= 232448, "shared memory budget");
@@ -433,6 +483,15 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   a.mask = reinterpret_cast<const __nv_bfloat16*>(p.mask); a.mask_bs = p.mask_bs; a.mask_ld = p.mask_ld;
   a.mask_act = p.mask_act; a.mask_alpha = p.mask_alpha;
   a.K2 = EPI ? p.K2 : 0;
+  a.mask_kb = -1;
+  // the gating tensor is the A operand itself (same rows, its columns = the
+  // output's): read it from the resident A stage instead of global memory
+  if (EPI && p.mask && p.splits == 1 && p.N <= BN) {
+    if (p.K2 > 0 && p.mask == p.A2 && p.mask_bs == p.a2_bs && p.mask_ld == p.a2_ld && p.K2 == p.N)
+      a.mask_kb = (int)cdiv(p.K, BK);
+    else if (p.K2 == 0 && p.mask == p.A && p.mask_bs == p.a_bs && p.mask_ld == p.a_ld && p.K == p.N && p.a_kmajor)
+      a.mask_kb = 0;
+  }
   auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, BRES, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -488,6 +547,7 @@ bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32) {
                      (p.b2_ld * 2) % 16 || (p.a2_bs * 2) % 16 || (p.b2_bs * 2) % 16))
       return false;
     if (p.mask && (!aligned16(p.mask) || p.mask_ld % 8 || p.mask_bs % 8)) return false;
+    if (p.scale && p.bias && p.bias_div > 0) return false;
   }
   if (p.K < 16 || p.N < 16 || p.M < 1) return false;
   if (!aligned16(p.A) || !aligned16(p.Bm)) return false;
