@@ -33,11 +33,17 @@ struct GemmP {
   const void* A2; int64_t a2_bs, a2_ld;
   const void* Bm2; int64_t b2_bs, b2_ld;
   int64_t K2;
+  // fused column sums of A over the reduction (wgrad: colsum[b][m] = sum_k A(m,k)
+  // = the dbias / Gram column-sum vector), computed on the tensor cores with a
+  // constant ones operand (MN-major A, fp32-output tcgen05 path only)
+  float* colsum; int64_t colsum_bs; int colsum_acc;   // colsum_acc: add into colsum
+  float* colsum_part;                                 // [splits][B][M] when splits > 1
 };
 
 // dt_in: operand dtype; out_f32: C is fp32 (else dt_in).
 hfta_status gemm_simt(const GemmP& p, hfta_dtype dt_in, bool out_f32, cudaStream_t s);
 hfta_status splitk_reduce(const GemmP& p, cudaStream_t s);   // C (+)= sum_s part[s]
+hfta_status colsum_reduce(const GemmP& p, cudaStream_t s);   // colsum (+)= sum_s colsum_part[s]
 
 // tcgen05 / TMA path; returns HFTA_ERR_UNSUPPORTED if the shape/alignment
 // does not qualify (caller then uses gemm_simt).
@@ -51,6 +57,7 @@ hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void
 bool skinny_fwd_ok(const GemmP& p);
 bool skinny_dgrad_ok(const GemmP& p);
 bool skinny_wgrad_ok(const GemmP& p);
+bool skinny_wgrad_ok_base(const GemmP& p);
 size_t skinny_wgrad_ws(int B, int64_t rows, int64_t N, int64_t Ko);
 hfta_status gemm_skinny(const GemmP& p, hfta_dtype dt, void* ws, size_t ws_bytes, cudaStream_t s);
 

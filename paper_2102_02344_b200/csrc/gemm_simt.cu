@@ -187,6 +187,22 @@ hfta_status gemm_simt(const GemmP& p, hfta_dtype dt_in, bool out_f32, cudaStream
   return post_launch(s, "gemm_simt");
 }
 
+__global__ void k_colsum_reduce(GemmP p) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)p.B * p.M) return;
+  const int64_t b = i / p.M, m = i % p.M;
+  float v = 0.f;
+  for (int s = 0; s < p.splits; ++s) v += p.colsum_part[((int64_t)s * p.B + b) * p.M + m];   // fixed order
+  float* o = p.colsum + b * p.colsum_bs + m;
+  *o = p.colsum_acc ? *o + v : v;
+}
+
+hfta_status colsum_reduce(const GemmP& p, cudaStream_t s) {
+  k_colsum_reduce<<<(unsigned)cdiv((int64_t)p.B * p.M, 256), 256, 0, s>>>(p);
+  count_launches(1);
+  return post_launch(s, "colsum_reduce");
+}
+
 hfta_status splitk_reduce(const GemmP& p, cudaStream_t s) {
   int64_t MN = p.M * p.N;
   dim3 grid((unsigned)std::min<int64_t>(cdiv(MN, 256), 4096), (unsigned)p.B);

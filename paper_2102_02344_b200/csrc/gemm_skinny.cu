@@ -143,22 +143,24 @@ __global__ void __launch_bounds__(NT) k_skinny_dgrad_row(GemmP p) {
 }
 
 // wgrad, small K-out: part[chunk][b][n][k] = sum_{rows in chunk} A(n, r) * Bx(k, r), both MN-major:
-// A = dY[r][n] (n < N), Bx = X[r][k] (k < K_out <= 8).  Thread = (row lane, VEC n-columns).
+// A = dY[r][n] (n < N), Bx = X[r][k] (k < K_out <= 3).  Thread = (row lane, VEC n-columns).
+// With p.colsum, a 4th column k = 3 accumulates sum_r A(n, r) (x = 1): the fused dbias.
 template <typename T, int VEC>
 __global__ void __launch_bounds__(NT) k_skinny_wgrad(GemmP p, int tpr, int rpb, int64_t rows_per_chunk,
                                                      float* __restrict__ part) {
-  __shared__ float red[NT * VEC * 3];
+  __shared__ float red[NT * VEC * 4];
   const int b = blockIdx.y, chunk = blockIdx.x;
   const T* A = reinterpret_cast<const T*>(p.A) + (int64_t)b * p.a_bs;
   const T* X = reinterpret_cast<const T*>(p.Bm) + (int64_t)b * p.b_bs;
   const int N = (int)p.M, Ko = (int)p.N;               // dW is [N][Ko]
+  const int KE = p.colsum ? Ko + 1 : Ko;              // columns written to part
   const int lane = threadIdx.x % tpr, rl = threadIdx.x / tpr;
   const int n0 = lane * VEC;
-  float acc[VEC][3];
+  float acc[VEC][4];
 #pragma unroll
   for (int v = 0; v < VEC; ++v)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) acc[v][k] = 0.f;
+    for (int k = 0; k < 4; ++k) acc[v][k] = 0.f;
   if (n0 < N) {
     const int64_t r0 = (int64_t)chunk * rows_per_chunk, r1 = min(p.K, r0 + rows_per_chunk);
 #pragma unroll 4
@@ -169,35 +171,40 @@ __global__ void __launch_bounds__(NT) k_skinny_wgrad(GemmP p, int tpr, int rpb, 
 #pragma unroll
       for (int k = 0; k < 3; ++k) x[k] = k < Ko ? ldf(X + r * p.b_ld + k) : 0.f;
 #pragma unroll
-      for (int v = 0; v < VEC; ++v)
+      for (int v = 0; v < VEC; ++v) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) acc[v][k] = fmaf(dy[v], x[k], acc[v][k]);
+        acc[v][3] += dy[v];
+      }
     }
   }
   const int cb = tpr * VEC;
 #pragma unroll
   for (int v = 0; v < VEC; ++v)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) red[(rl * cb + lane * VEC + v) * 3 + k] = acc[v][k];
+    for (int k = 0; k < 4; ++k) red[(rl * cb + lane * VEC + v) * 4 + k] = acc[v][k];
   __syncthreads();
-  for (int e = threadIdx.x; e < cb * 3; e += NT) {
-    const int col = e / 3, k = e % 3;
-    if (col >= N || k >= Ko) continue;
-    float s = 0.f;
-    for (int r = 0; r < rpb; ++r) s += red[(r * cb + col) * 3 + k];
-    part[(((int64_t)chunk * p.B + b) * N + col) * Ko + k] = s;
+  for (int e = threadIdx.x; e < cb * 4; e += NT) {
+    const int col = e / 4, k = e % 4;
+    const int kk = k == 3 ? Ko : k;                   // slot 3 = column sum
+    if (col >= N || (k < 3 && k >= Ko) || (k == 3 && !p.colsum)) continue;
+    float sum = 0.f;
+    for (int r = 0; r < rpb; ++r) sum += red[(r * cb + col) * 4 + k];
+    part[(((int64_t)chunk * p.B + b) * N + col) * KE + kk] = sum;
   }
 }
 
 __global__ void k_skinny_wgrad_fin(GemmP p, int chunks, const float* __restrict__ part) {
   const int N = (int)p.M, Ko = (int)p.N;
+  const int KE = p.colsum ? Ko + 1 : Ko;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)p.B * N * Ko) return;
-  int64_t b = i / (N * Ko), rem = i % (N * Ko), n = rem / Ko, k = rem % Ko;
+  if (i >= (int64_t)p.B * N * KE) return;
+  int64_t b = i / (N * KE), rem = i % (N * KE), n = rem / KE, k = rem % KE;
   double s = 0.0;
-  for (int c = 0; c < chunks; ++c) s += part[(((int64_t)c * p.B + b) * N + n) * Ko + k];
-  float* o = reinterpret_cast<float*>(p.C) + b * p.c_bs + n * p.c_ld + k;
-  *o = p.accumulate ? *o + (float)s : (float)s;
+  for (int c = 0; c < chunks; ++c) s += part[(((int64_t)c * p.B + b) * N + n) * KE + k];
+  float* o = k < Ko ? reinterpret_cast<float*>(p.C) + b * p.c_bs + n * p.c_ld + k : p.colsum + b * p.colsum_bs + n;
+  const int acc = k < Ko ? p.accumulate : p.colsum_acc;
+  *o = acc ? *o + (float)s : (float)s;
 }
 
 int pow2ceil(int64_t x) { int q = 1; while (q < x) q <<= 1; return q; }
@@ -315,7 +322,7 @@ static int64_t smallm_chunks(int B, int64_t rows, int64_t N) {
 
 size_t skinny_wgrad_ws(int B, int64_t rows, int64_t N, int64_t Ko) {
   int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(16 * 148, B), cdiv(rows, 1024)));
-  size_t a = (size_t)chunks * B * N * Ko * sizeof(float);
+  size_t a = (size_t)chunks * B * N * (Ko + 1) * sizeof(float);   // + fused column sums
   size_t c = N <= KMAX ? (size_t)smallm_chunks(B, rows, Ko) * B * N * Ko * sizeof(float) : 0;   // dW is [N][Ko]
   return std::max(a, c);
 }
@@ -399,7 +406,7 @@ hfta_status gemm_skinny(const GemmP& p, hfta_dtype dt, void* ws, size_t ws_bytes
   if (skinny_wgrad_ok_base(p)) {
     const int64_t rows = p.K, N = p.M, Ko = p.N;
     int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(cdiv(16 * 148, p.B), cdiv(rows, 1024)));
-    size_t need = (size_t)chunks * p.B * N * Ko * sizeof(float);
+    size_t need = (size_t)chunks * p.B * N * (p.colsum ? Ko + 1 : Ko) * sizeof(float);
     HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "skinny wgrad: workspace %zu < %zu", ws_bytes, need);
     int vec = bf ? 8 : 4;
     if (N % vec || p.a_ld % vec || !aligned16(p.A) || p.a_bs % vec) vec = 1;
@@ -416,7 +423,7 @@ hfta_status gemm_skinny(const GemmP& p, hfta_dtype dt, void* ws, size_t ws_bytes
       if (vec == 4) k_skinny_wgrad<float, 4><<<grid, NT, 0, s>>>(p, tpr, rpb, rows_per_chunk, part);
       else k_skinny_wgrad<float, 1><<<grid, NT, 0, s>>>(p, tpr, rpb, rows_per_chunk, part);
     }
-    k_skinny_wgrad_fin<<<(unsigned)cdiv((int64_t)p.B * N * Ko, 256), 256, 0, s>>>(p, (int)chunks, part);
+    k_skinny_wgrad_fin<<<(unsigned)cdiv((int64_t)p.B * N * (Ko + 1), 256), 256, 0, s>>>(p, (int)chunks, part);
     count_launches(2);
     return post_launch(s, "gemm_skinny_wgrad");
   }

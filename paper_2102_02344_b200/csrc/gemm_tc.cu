@@ -44,6 +44,7 @@ struct TcArgs {
   int64_t K2;                        // second K segment (maps tmA2 / tmB2)
   int mask_kb;                       // >= 0: the gating tensor is the A tile of k-blocks mask_kb..:
                                      // read from the resident smem stage (released by the epilogue)
+  float* colsum; int64_t colsum_bs; int colsum_acc; float* colsum_part;   // fused column sums of A
 };
 
 // BRES ("B resident", forward layers with K <= 128): the B operand (the
@@ -63,7 +64,12 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   constexpr uint32_t B_BYTES = BN * BK * 2;
   constexpr uint32_t STAGE_BYTES = BRES ? A_BYTES : A_BYTES + B_BYTES;
   constexpr uint32_t BRES_BYTES = BRES ? 2 * B_BYTES : 0;
-  constexpr uint32_t TMEM_COLS = 2 * BN;     // double-buffered accumulator
+  // double-buffered accumulator (+ 2 x 16 columns for the fused column sums
+  // of the MN-major A operand in the fp32-output wgrad variant)
+  constexpr bool CSUM = A_MN && OUT_F32;
+  constexpr uint32_t TMEM_COLS = CSUM ? (BN == 64 ? 256 : 512) : 2 * BN;
+  constexpr uint32_t IDESC_CS = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(16 >> 3) << 17) |
+                                ((uint32_t)(BM >> 4) << 24);
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
                              ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
@@ -81,6 +87,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint8_t* stage_out = bres + BRES_BYTES + 1024;                   // NEPI warps x 2 x 4 KB
   float* sbias_all = reinterpret_cast<float*>(stage_out + NEPI * 2 * 4096);   // NEPI warps x BN floats
   float* sscale_all = sbias_all + NEPI * BN;                                   // EPI: NEPI warps x BN floats
+  uint8_t* sones = reinterpret_cast<uint8_t*>(sscale_all + (EPI ? NEPI * BN : 0));   // CSUM: 16 x 64 bf16 ones (2 KB)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -93,6 +100,12 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     mbar_init(bempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if constexpr (CSUM) {
+    if (p.colsum) {
+      for (int i = threadIdx.x; i < 512; i += NTHREADS) reinterpret_cast<uint32_t*>(sones)[i] = 0x3F803F80u;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -201,6 +214,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      const bool cs_tile = CSUM && p.colsum && nt_ == 0;      // column sums once per m-tile
+      const uint32_t d_cs = tmem_base + 2 * BN + (uint32_t)(acc * 16);
+      const uint64_t ones_d = smem_desc(smem_u32(sones), 16, 1024);
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -215,6 +231,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             // MN-major: +16 rows x 128 B (descriptor address unit: 16 B).
             tc_mma_ss(d_tmem, ad0 + (uint64_t)(A_MN ? k * 128 : k * 2), bd0 + (uint64_t)(B_MN ? k * 128 : k * 2), IDESC,
                       (kb | k) != 0 ? 1u : 0u);
+            if (cs_tile)   // D_cs[m][0..15] += sum_k A(m, k) * 1
+              tc_mma_ss(d_cs, ad0 + (uint64_t)(k * 128), ones_d, IDESC_CS, (kb | k) != 0 ? 1u : 0u);
           }
           tc_commit_w(&empty[stage]);                  // smem slot free once these MMAs retire
           if (kb == nkb - 1) tc_commit_w(&tfull[acc]);   // accumulator ready
@@ -276,6 +294,21 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         __syncwarp();
         cur_key = key;
+      }
+      if (CSUM && p.colsum && nt == 0 && half == 0) {   // fused column sums: TMEM lane = m, column 0
+        uint32_t cs;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                     : "=r"(cs) : "r"(tmem_base + 2 * BN + (uint32_t)(acc * 16) + ((uint32_t)(quarter * 32) << 16)));
+        tmem_wait_ld();
+        if (row_ok) {
+          const float v = __uint_as_float(cs);
+          if (p.splits > 1) {
+            p.colsum_part[((int64_t)split * p.B + b) * p.M + m] = v;
+          } else {
+            float* o = p.colsum + (int64_t)b * p.colsum_bs + m;
+            *o = p.colsum_acc ? *o + v : v;
+          }
+        }
       }
       const bool mask_smem = EPI && p.mask_kb >= 0;
       int tile_nkb = 0;
@@ -443,7 +476,8 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   // k-blocks can stay resident for the epilogue while the next tile loads
   constexpr int STAGES = BRES ? 4 : ((BN == 256) ? 3 : ((EPI && BN == 64) ? 6 : 4));
   constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + (BRES ? 0 : BN * BK * 2)) +
-                          (BRES ? 2 * BN * BK * 2 : 0) + 1024 + NEPI * 2 * 4096 + NEPI * BN * 4 * (EPI ? 2 : 1);
+                          (BRES ? 2 * BN * BK * 2 : 0) + 1024 + NEPI * 2 * 4096 + NEPI * BN * 4 * (EPI ? 2 : 1) +
+                          ((A_MN && OUT_F32) ? 2048 : 0);
   static_assert(SMEM <= 232448, "shared memory budget");
   if (hfta_status st = get_encode()) return st;
   CUtensorMap ta, tb;
@@ -483,6 +517,7 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   a.mask = reinterpret_cast<const __nv_bfloat16*>(p.mask); a.mask_bs = p.mask_bs; a.mask_ld = p.mask_ld;
   a.mask_act = p.mask_act; a.mask_alpha = p.mask_alpha;
   a.K2 = EPI ? p.K2 : 0;
+  a.colsum = p.colsum; a.colsum_bs = p.colsum_bs; a.colsum_acc = p.colsum_acc; a.colsum_part = p.colsum_part;
   a.mask_kb = -1;
   // the gating tensor is the A operand itself (same rows, its columns = the
   // output's): read it from the resident A stage instead of global memory

@@ -87,7 +87,8 @@ size_t hfta_fused_linear_bwd_workspace(int B, int64_t M, int64_t N, int64_t K, h
   size_t part = sp.splits > 1 ? (size_t)sp.splits * B * N * K * sizeof(float) : 0;
   part = std::max(part, skinny_wgrad_ws(B, M, N, K));
   size_t cs = colsum_ws(B, M, N, M);
-  return align_up(part, 256) + align_up(cs, 256);
+  size_t csp = sp.splits > 1 ? (size_t)sp.splits * B * N * sizeof(float) : 0;   // fused column-sum partials
+  return align_up(part, 256) + align_up(std::max(cs, csp), 256);
   (void)dt;
 }
 
@@ -132,14 +133,29 @@ hfta_status hfta_fused_linear_bwd(int B, int64_t M, int64_t N, int64_t K, hfta_d
     p.accumulate = accumulate;
     p.splits = 1; p.k_chunk = M;
     if (skinny_wgrad_ok(p)) {
+      if (dbias && skinny_wgrad_ok_base(p)) {   // dbias fused into the streaming wgrad (column k = K)
+        p.colsum = dbias; p.colsum_bs = dbias_bstride; p.colsum_acc = accumulate;
+        dbias = nullptr;
+      }
       if (hfta_status st = gemm_skinny(p, dt, ws, ws_bytes, s)) return st;
     } else {
       Split sp = wgrad_split(B, M, N, K);
       p.splits = sp.splits; p.k_chunk = sp.chunk;
       p.part = sp.splits > 1 ? reinterpret_cast<float*>(ws) : nullptr;
+      if (dbias && gemm_tc_supported(p, dt, true)) {
+        // dbias = column sums of dY, fused into the tensor-core wgrad (ones operand)
+        const size_t off = align_up(std::max(sp.splits > 1 ? (size_t)sp.splits * B * N * K * sizeof(float) : 0,
+                                             skinny_wgrad_ws(B, M, N, K)), 256);
+        p.colsum = dbias; p.colsum_bs = dbias_bstride; p.colsum_acc = accumulate;
+        p.colsum_part = sp.splits > 1 ? reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + off) : nullptr;
+        dbias = nullptr;
+      }
       if (hfta_status st = run_gemm(p, dt, true, s)) return st;
-      if (sp.splits > 1)
+      if (sp.splits > 1) {
         if (hfta_status st = splitk_reduce(p, s)) return st;
+        if (p.colsum)
+          if (hfta_status st = colsum_reduce(p, s)) return st;
+      }
     }
   }
   if (dbias) {
