@@ -60,18 +60,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
           const __grid_constant__ CUtensorMap tmB2, TcArgs p) {
+  // CSUM (wgrad, fp32 out): B is augmented with a constant 64-column MN-major
+  // atom of ones after its BN columns, and MMAs of column-sum tiles use
+  // N = BN + 16: accumulator columns BN..BN+15 then hold sum_k A(m, k) (the
+  // fused dbias / Gram column sums) at no extra MMA instruction.
+  constexpr bool CSUM = A_MN && B_MN && OUT_F32;
   constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB
-  constexpr uint32_t B_BYTES = BN * BK * 2;
+  constexpr uint32_t B_LOAD = BN * BK * 2;    // bytes of B loaded per stage
+  constexpr uint32_t B_BYTES = B_LOAD + (CSUM ? 8192 : 0);
   constexpr uint32_t STAGE_BYTES = BRES ? A_BYTES : A_BYTES + B_BYTES;
+  constexpr uint32_t LOAD_BYTES = BRES ? A_BYTES : A_BYTES + B_LOAD;
   constexpr uint32_t BRES_BYTES = BRES ? 2 * B_BYTES : 0;
-  // double-buffered accumulator (+ 2 x 16 columns for the fused column sums
-  // of the MN-major A operand in the fp32-output wgrad variant)
-  constexpr bool CSUM = A_MN && OUT_F32;
-  constexpr uint32_t TMEM_COLS = CSUM ? (BN == 64 ? 256 : 512) : 2 * BN;
-  constexpr uint32_t IDESC_CS = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(16 >> 3) << 17) |
-                                ((uint32_t)(BM >> 4) << 24);
+  constexpr uint32_t ABUF = BN + (CSUM ? 16 : 0);   // TMEM columns per accumulator buffer
+  constexpr uint32_t TMEM_COLS = (2 * ABUF <= 128) ? 128 : (2 * ABUF <= 256 ? 256 : 512);
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
                              ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  constexpr uint32_t IDESC_CS = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                                ((B_MN ? 1u : 0u) << 16) | ((uint32_t)((BN + 16) >> 3) << 17) |
+                                ((uint32_t)(BM >> 4) << 24);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -85,9 +91,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 1);
   // per-epilogue-warp staging for the TMA store: 2 buffers x 32 rows x 64 B
   uint8_t* stage_out = bres + BRES_BYTES + 1024;                   // NEPI warps x 2 x 4 KB
-  float* sbias_all = reinterpret_cast<float*>(stage_out + NEPI * 2 * 4096);   // NEPI warps x BN floats
+  constexpr uint32_t STG_BYTES = OUT_F32 ? 0 : NEPI * 2 * 4096;              // bf16 TMA-store staging
+  float* sbias_all = reinterpret_cast<float*>(stage_out + STG_BYTES);         // NEPI warps x BN floats
   float* sscale_all = sbias_all + NEPI * BN;                                   // EPI: NEPI warps x BN floats
-  uint8_t* sones = reinterpret_cast<uint8_t*>(sscale_all + (EPI ? NEPI * BN : 0));   // CSUM: 16 x 64 bf16 ones (2 KB)
+
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -102,8 +109,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if constexpr (CSUM) {
-    if (p.colsum) {
-      for (int i = threadIdx.x; i < 512; i += NTHREADS) reinterpret_cast<uint32_t*>(sones)[i] = 0x3F803F80u;
+    if (p.colsum) {   // the ones atom of every stage (never written by TMA)
+      for (int st = 0; st < STAGES; ++st) {
+        uint32_t* ones = reinterpret_cast<uint32_t*>(smem + st * STAGE_BYTES + A_BYTES + B_LOAD);
+        for (int i = threadIdx.x; i < 2048; i += NTHREADS) ones[i] = 0x3F803F80u;
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
   }
@@ -157,7 +167,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          mbar_expect_tx(&full[stage], LOAD_BYTES);
           (void)sb;
           const int k0 = (int)(kbeg + (int64_t)kb * BK);
           if (EPI && kb >= nkb1) {                        // second K segment (K-major A2, B2)
@@ -213,10 +223,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       const int nkb = (int)((kend - kbeg + BK - 1) / BK) + (EPI ? (int)((p.K2 + BK - 1) / BK) : 0);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * ABUF);
       const bool cs_tile = CSUM && p.colsum && nt_ == 0;      // column sums once per m-tile
-      const uint32_t d_cs = tmem_base + 2 * BN + (uint32_t)(acc * 16);
-      const uint64_t ones_d = smem_desc(smem_u32(sones), 16, 1024);
+      const uint32_t idesc = cs_tile ? IDESC_CS : IDESC;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -229,10 +238,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           for (int k = 0; k < BK / 16; ++k) {
             // K-major: +32 B per 16-element k step inside the 128-B swizzle row;
             // MN-major: +16 rows x 128 B (descriptor address unit: 16 B).
-            tc_mma_ss(d_tmem, ad0 + (uint64_t)(A_MN ? k * 128 : k * 2), bd0 + (uint64_t)(B_MN ? k * 128 : k * 2), IDESC,
+            tc_mma_ss(d_tmem, ad0 + (uint64_t)(A_MN ? k * 128 : k * 2), bd0 + (uint64_t)(B_MN ? k * 128 : k * 2), idesc,
                       (kb | k) != 0 ? 1u : 0u);
-            if (cs_tile)   // D_cs[m][0..15] += sum_k A(m, k) * 1
-              tc_mma_ss(d_cs, ad0 + (uint64_t)(k * 128), ones_d, IDESC_CS, (kb | k) != 0 ? 1u : 0u);
           }
           tc_commit_w(&empty[stage]);                  // smem slot free once these MMAs retire
           if (kb == nkb - 1) tc_commit_w(&tfull[acc]);   // accumulator ready
@@ -298,7 +305,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       if (CSUM && p.colsum && nt == 0 && half == 0) {   // fused column sums: TMEM lane = m, column 0
         uint32_t cs;
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
-                     : "=r"(cs) : "r"(tmem_base + 2 * BN + (uint32_t)(acc * 16) + ((uint32_t)(quarter * 32) << 16)));
+                     : "=r"(cs) : "r"(tmem_base + (uint32_t)(acc * ABUF + BN) + ((uint32_t)(quarter * 32) << 16)));
         tmem_wait_ld();
         if (row_ok) {
           const float v = __uint_as_float(cs);
@@ -325,7 +332,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (int si = 0; si < my_steps; ++si) {
         const int j = half + 2 * si;     // 64-column step
         uint32_t u[64];
-        const uint32_t ta = tmem_base + (uint32_t)(acc * BN + j * 64) + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t ta = tmem_base + (uint32_t)(acc * ABUF + j * 64) + ((uint32_t)(quarter * 32) << 16);
         tmem_ld32_nowait(ta, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
         tmem_ld32_nowait(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
         tmem_wait_ld();
@@ -476,8 +483,9 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   // k-blocks can stay resident for the epilogue while the next tile loads
   constexpr int STAGES = BRES ? 4 : ((BN == 256) ? 3 : ((EPI && BN == 64) ? 6 : 4));
   constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + (BRES ? 0 : BN * BK * 2)) +
-                          (BRES ? 2 * BN * BK * 2 : 0) + 1024 + NEPI * 2 * 4096 + NEPI * BN * 4 * (EPI ? 2 : 1) +
-                          ((A_MN && OUT_F32) ? 2048 : 0);
+                          (BRES ? 2 * BN * BK * 2 : 0) + 1024 + (OUT_F32 ? 0 : NEPI * 2 * 4096) +
+                          NEPI * BN * 4 * (EPI ? 2 : 1) +
+                          ((A_MN && B_MN && OUT_F32) ? (size_t)STAGES * 8192 : 0);
   static_assert(SMEM <= 232448, "shared memory budget");
   if (hfta_status st = get_encode()) return st;
   CUtensorMap ta, tb;
