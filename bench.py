@@ -231,9 +231,26 @@ def run_ours(args, rank, world, local_rank):
         wl.step()
         gather_losses()
     torch.cuda.synchronize()
-    probe_name = args.probe if args.workload in ("pointnet_cls", "pointnet_seg") else None
-    if probe_name:
-        net.probe_arm(probe_name)
+    # The whole training step (all B models: forward, backward, optimizer) is
+    # captured once as a CUDA graph and replayed (--no-graph: eager launches).
+    graph = None
+    l0 = H.hfta_launch_count()
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            wl.step()
+        torch.cuda.synchronize()
+        launches_per_step = H.hfta_launch_count() - l0
+        graph.replay()                     # (warm replay; the captured step is a real step)
+        torch.cuda.synchronize()
+
+    def run_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            wl.step()
+        gather_losses()
+
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -243,16 +260,14 @@ def run_ours(args, rank, world, local_rank):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        wl.step()
-        gather_losses()
+        run_step()
     e1.record(stream)
     torch.cuda.synchronize()
-    launches = H.hfta_launch_count() - l0
+    launches = (launches_per_step * args.steps) if graph is not None else H.hfta_launch_count() - l0
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
-    probe_ms = net.probe_collect() if probe_name else []
     t = torch.tensor([ms], device=device, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -260,14 +275,33 @@ def run_ours(args, rank, world, local_rank):
     value = B * N * args.steps * world / (ms_max / 1e3)
     mem_peak = torch.cuda.max_memory_allocated(device)
 
+    # ---- roofline probe: CUDA events around the probed kernel in eager steps ----
+    probe_name = args.probe if args.workload in ("pointnet_cls", "pointnet_seg") else None
+    probe_ms = []
+    if probe_name:
+        net.probe_arm(probe_name)
+        for _ in range(3):
+            wl.step()
+        torch.cuda.synchronize()
+        probe_ms = net.probe_collect()
+
     # ---- end to end through the public API: pinned host inputs in, losses out ----
+    graph_e2e = None
+    if not args.no_graph:
+        graph_e2e = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_e2e):
+            wl.e2e_step()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     for _ in range(args.steps):
-        wl.e2e_step()
+        if graph_e2e is not None:
+            graph_e2e.replay()
+        else:
+            wl.e2e_step()
         gather_losses()
         stream.synchronize()            # the host reads the step's per-model losses
     f1.record(stream)
@@ -287,6 +321,7 @@ def run_ours(args, rank, world, local_rank):
                            "l2": "working set >> L2 (activations ~%.0f GB/step)" % (mem_peak / 1e9),
                            "parallelism": "model-array sharding, %d x %d models" % (world, B)},
                 "gpu_launches": int(launches),
+                "cuda_graph": graph is not None,
                 "peak_mem_gb": mem_peak / 1e9,
                 "clocks": clk,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(wl.h2d),
@@ -344,6 +379,7 @@ def main():
     ap.add_argument("--fast-init", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-serial", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of the captured step graph")
     ap.add_argument("--workload", default="pointnet_cls", choices=["pointnet_cls", "pointnet_seg", "dcgan"])
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))

@@ -614,33 +614,62 @@ __global__ void __launch_bounds__(SDX_T) k_lbm_sparse_dx(int Ncl, int64_t L, int
 }
 
 // dW[c] (+)= bx_c (W G)[c] + cc_c s + sum_n sp(n, c) X[n*L + argmax(n, c)].
-// One CTA per (model, 64 channels) with G (fp32 K x K) in shared memory; a
-// warp per channel, lane l owns k = 4l .. 4l+3 (K = 128; K = 64 uses lanes
-// 0-15).  The per-cloud (sp, argmax) pairs are loaded one per lane and
-// broadcast with shuffles, so the row gathers are independent loads.
-__global__ void __launch_bounds__(256) k_lbm_dw(int Ncl, int64_t L, int64_t C, int K, const float* __restrict__ G,
+// CTA = (model, 32 channels), 256 threads = 8 warps x 4 channels; lane l owns
+// k = 4l .. 4l+3 (K = 128; K = 64: lanes 0-15).  (W G): the CTA's 32 W rows
+// in smem (fp32), one G row segment (L1) per k2 reused by the warp's 4
+// channels.  Sparse part: per-cloud (sp, argmax) one per lane, broadcast by
+// shuffles, 8 row gathers issued back to back.
+__global__ void __launch_bounds__(256, 2) k_lbm_dw(int Ncl, int64_t L, int64_t C, int K, const float* __restrict__ G,
                                                 const float* __restrict__ svec, const __nv_bfloat16* __restrict__ W,
                                                 int64_t w_bs, int64_t w_ld, const float2* __restrict__ coef,
                                                 const int32_t* __restrict__ am, const float* __restrict__ sp,
                                                 const __nv_bfloat16* __restrict__ X, int64_t x_bs, int64_t x_ld,
                                                 float* __restrict__ dW, int64_t dw_bs, int64_t dw_ld,
                                                 int accumulate) {
-  extern __shared__ float sG[];                 // [K][K] then s[K]
-  float* ss = sG + K * K;
-  __shared__ float swrow[8][128];
+  __shared__ float sw[32][128];
+  extern __shared__ float4 sG4[];                 // G [K][K] fp32 (the model's Gram, shared by all its CTAs)
   const int b = blockIdx.y;
-  const int t = threadIdx.x, warp = t / 32, lane = t % 32;
-  for (int e = t; e < K * K; e += 256) sG[e] = G[(int64_t)b * K * K + e];
-  for (int e = t; e < K; e += 256) ss[e] = svec[(int64_t)b * K + e];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t c0 = (int64_t)blockIdx.x * 32;
+  const __nv_bfloat16* Wb = W + (int64_t)b * w_bs;
+  for (int e = threadIdx.x; e < 32 * K; e += 256) {
+    const int ci = e / K, k = e % K;
+    sw[ci][k] = c0 + ci < C ? __bfloat162float(Wb[(c0 + ci) * w_ld + k]) : 0.f;
+  }
+  {
+    const float4* g4 = reinterpret_cast<const float4*>(G + (int64_t)b * K * K);
+    for (int e = threadIdx.x; e < K * K / 4; e += 256) sG4[e] = g4[e];
+  }
   __syncthreads();
   const bool on = lane * 4 < K;
-  const __nv_bfloat16* Wb = W + (int64_t)b * w_bs;
   const __nv_bfloat16* Xb = X + (int64_t)b * x_bs;
-  for (int ci = warp; ci < 64; ci += 8) {
-    const int64_t c = (int64_t)blockIdx.x * 64 + ci;
+  const float* sG = reinterpret_cast<const float*>(sG4);
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[i][e] = 0.f;
+  if (on) {
+#pragma unroll 2
+    for (int k2 = 0; k2 < K; ++k2) {
+      const float4 g4 = *reinterpret_cast<const float4*>(sG + k2 * K + lane * 4);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float w = sw[warp * 4 + i][k2];
+        acc[i][0] = fmaf(w, g4.x, acc[i][0]); acc[i][1] = fmaf(w, g4.y, acc[i][1]);
+        acc[i][2] = fmaf(w, g4.z, acc[i][2]); acc[i][3] = fmaf(w, g4.w, acc[i][3]);
+      }
+    }
+  }
+  float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (on) s4 = __ldg(reinterpret_cast<const float4*>(svec + (int64_t)b * K + lane * 4));
+  const float ss[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t c = c0 + warp * 4 + i;
     if (c >= C) break;
     float sacc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int nb = 0; nb < Ncl; nb += 32) {         // sparse gathers: 32 clouds per round
+    for (int nb = 0; nb < Ncl; nb += 32) {          // sparse gathers: 32 clouds per round
       const int nl = nb + lane;
       float vl = 0.f;
       int64_t rl = 0;
@@ -650,42 +679,29 @@ __global__ void __launch_bounds__(256) k_lbm_dw(int Ncl, int64_t L, int64_t C, i
         rl = (int64_t)nl * L + am[o];
       }
       const int cnt = min(32, Ncl - nb);
-#pragma unroll 8
-      for (int q = 0; q < cnt; ++q) {
-        const float v = __shfl_sync(0xffffffffu, vl, q);
-        const int64_t row = __shfl_sync(0xffffffffu, rl, q);
-        if (on) {
-          float x4[4];
-          ld_vec<__nv_bfloat16, 4>(Xb + row * x_ld + lane * 4, x4);
+      for (int q0 = 0; q0 < cnt; q0 += 8) {
+        float xv[8][4];
+        float vv[8];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) sacc[e] = fmaf(v, x4[e], sacc[e]);
+        for (int dq = 0; dq < 8; ++dq) {             // 8 independent row gathers in flight
+          const int q = min(q0 + dq, cnt - 1);
+          vv[dq] = q0 + dq < cnt ? __shfl_sync(0xffffffffu, vl, q) : 0.f;
+          const int64_t row = __shfl_sync(0xffffffffu, rl, q);
+          if (on) ld_vec<__nv_bfloat16, 4>(Xb + row * x_ld + lane * 4, xv[dq]);
+          else xv[dq][0] = xv[dq][1] = xv[dq][2] = xv[dq][3] = 0.f;
         }
-      }
-    }
-    if (on) {
-      float w4[4];
-      ld_vec<__nv_bfloat16, 4>(Wb + c * w_ld + lane * 4, w4);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) swrow[warp][lane * 4 + e] = w4[e];
-    }
-    __syncwarp();
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    if (on) {
-#pragma unroll 8
-      for (int k2 = 0; k2 < K; ++k2) {
-        const float w = swrow[warp][k2];
-        const float4 g4 = *reinterpret_cast<const float4*>(sG + k2 * K + lane * 4);
-        acc[0] = fmaf(w, g4.x, acc[0]); acc[1] = fmaf(w, g4.y, acc[1]);
-        acc[2] = fmaf(w, g4.z, acc[2]); acc[3] = fmaf(w, g4.w, acc[3]);
+        for (int dq = 0; dq < 8; ++dq)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sacc[e] = fmaf(vv[dq], xv[dq][e], sacc[e]);
       }
     }
-    __syncwarp();
-    const float2 cf = coef[(int64_t)b * C + c];
     if (on) {
+      const float2 cf = coef[(int64_t)b * C + c];
       float* d = dW + (int64_t)b * dw_bs + c * dw_ld + lane * 4;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float r = fmaf(cf.x, acc[e], fmaf(cf.y, ss[lane * 4 + e], sacc[e]));
+        const float r = fmaf(cf.x, acc[i][e], fmaf(cf.y, ss[e], sacc[e]));
         d[e] = accumulate ? d[e] + r : r;
       }
     }
@@ -874,13 +890,12 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
     launches += 2;
   }
   {
-    const size_t smem = (size_t)(K * K + K) * 4;
     static bool attr = false;
-    set_smem(k_lbm_dw, smem, attr);
-    k_lbm_dw<<<dim3((unsigned)cdiv(C, 64), (unsigned)B), 256, smem, s>>>(
-        (int)N, L, C, (int)K, G, sv, Wp, wbs, W.ld, coef, argmax, sp, (const __nv_bfloat16*)X.ptr,
-        X.bstride, X.ld, dW, dW_bstride, dW_ld, accumulate);
+    set_smem(k_lbm_dw, (size_t)128 * 128 * 4, attr);   // K <= 128
   }
+  k_lbm_dw<<<dim3((unsigned)cdiv(C, 32), (unsigned)B), 256, (size_t)K * K * 4, s>>>(
+      (int)N, L, C, (int)K, G, sv, Wp, wbs, W.ld, coef, argmax, sp, (const __nv_bfloat16*)X.ptr, X.bstride, X.ld, dW,
+      dW_bstride, dW_ld, accumulate);
   count_launches(launches);
   return post_launch(s, "hfta_fused_linear_bn_max_bwd");
 }

@@ -326,8 +326,10 @@ class FusedPointNet(FusedNet):
         self._lin_fwd(_in(S["feat.g"]), N, "head.fc1", S["head.y1"], s)
         self._bn_fwd(S["head.y1"], "head.bn1", A_RELU, S["head.h1"], s)
         self._lin_fwd(_in(S["head.h1"]), N, "head.fc2", S["head.y2"], s)
+        # the Philox step comes from the device step counter (+1: it is advanced by the
+        # optimizer at the end of the step), so a captured CUDA graph replays correctly
         H.hfta_dropout_fwd(self.B, N, self.f2, H.HFTA_F32, _in(S["head.y2"]), _out(S["head.d2"]), self.dropout_seed,
-                           self.t, 0, self.p_drop, s)
+                           1, H.ptr(self.hv.step), 0, self.p_drop, s)
         self._bn_fwd(S["head.d2"], "head.bn2", A_RELU, S["head.h2"], s)
         self._lin_fwd(_in(S["head.h2"]), N, "head.fc3", S["head.logits"], s)
         H.hfta_loss_nll(self.B, N, self.k, H.HFTA_F32, _in(S["head.logits"]), H.ptr(self.labels), 0, H.ptr(self.loss),
@@ -335,7 +337,7 @@ class FusedPointNet(FusedNet):
         self._lin_bwd(S["d.logits"], _in(S["head.h2"]), N, "head.fc3", S["d.f2a"], s)
         self._bn_bwd(S["d.f2a"], S["head.d2"], "head.bn2", A_RELU, S["d.f2b"], s)
         H.hfta_dropout_bwd(self.B, N, self.f2, H.HFTA_F32, _in(S["d.f2b"]), _out(S["d.f2a"]), self.dropout_seed,
-                           self.t, 0, self.p_drop, s)
+                           1, H.ptr(self.hv.step), 0, self.p_drop, s)
         self._lin_bwd(S["d.f2a"], _in(S["head.h1"]), N, "head.fc2", S["d.f1a"], s)
         self._bn_bwd(S["d.f1a"], S["head.y1"], "head.bn1", A_RELU, S["d.f1b"], s)
         self._lin_bwd(S["d.f1b"], _in(S["feat.g"]), N, "head.fc1", S["d.g"], s)

@@ -233,7 +233,14 @@ def test_dropout_mask_bit_exact(dt):
     X = rounded(R.standard_normal((B, rows, cols)), tdt)
     Y = torch.empty(B, rows, cols, dtype=tdt, device=DEV)
     H.hfta_dropout_fwd(B, rows, cols, code, H.tin(dev(X, tdt), rows * cols, cols), H.tout(Y, rows * cols, cols), 42,
-                       5, 0, p, s())
+                       5, None, 0, p, s())
+    # the same mask when the step comes from a device counter (graph-capturable form): 4 + 1
+    Y2 = torch.empty_like(Y)
+    stepd = torch.tensor([4], dtype=torch.int64, device=DEV)
+    H.hfta_dropout_fwd(B, rows, cols, code, H.tin(dev(X, tdt), rows * cols, cols), H.tout(Y2, rows * cols, cols), 42,
+                       1, H.ptr(stepd), 0, p, s())
+    torch.cuda.synchronize()
+    assert torch.equal(Y, Y2)
     torch.cuda.synchronize()
     for b in range(B):
         keep = dropout_keep_mask(42, b, 5, 0, rows * cols, p).reshape(rows, cols)
