@@ -52,10 +52,12 @@ struct TcArgs {
 // while the CTA sweeps consecutive m-tiles of the same (model, n-tile) --
 // the static schedule gives each CTA ~M/128/148*B such tiles in a row -- so
 // only the activation tile streams through the ring (cuts L2->SM traffic 3x).
-// EPI: bf16-output epilogue with per-column scale, activation and an
-// activation-derivative mask (fused BatchNorm apply / backward gating), and a
-// second K segment (A2, B2) accumulated into the same tile (non-BRES only).
-template <bool A_MN, bool B_MN, int BN, int STAGES, bool OUT_F32, bool BRES, bool EPI>
+// EPI (bf16 output): 1 = fused BatchNorm apply, v = act(v * scale + shift);
+// 2 = gated dgrad, v = (v + bias) * act'(A) with the gating values read from
+// this tile's A (or A2) stage still resident in smem, optionally with a second
+// K segment (A2, B2) accumulated into the same tile (non-BRES).  Separate
+// instantiations keep each epilogue branch-free and small.
+template <bool A_MN, bool B_MN, int BN, int STAGES, bool OUT_F32, bool BRES, int EPI>
 __global__ void __launch_bounds__(NTHREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
@@ -100,7 +102,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], (EPI && p.mask_kb >= 0) ? 1 + NEPI : 1);   // + epilogue arrivals (mask read)
+      mbar_init(&empty[s], (EPI == 2 && p.mask_kb >= 0) ? 1 + NEPI : 1);   // + epilogue arrivals (gating from A)
     }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], NEPI); }
     mbar_init(bfull, 1);
@@ -149,7 +151,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int64_t kbeg = (int64_t)split * p.k_chunk;
         const int64_t kend = min(p.K, kbeg + p.k_chunk);
         const int nkb1 = (int)((kend - kbeg + BK - 1) / BK);
-        const int nkb = nkb1 + (EPI ? (int)((p.K2 + BK - 1) / BK) : 0);
+        const int nkb = nkb1 + (EPI == 2 ? (int)((p.K2 + BK - 1) / BK) : 0);
         const int ba = p.a_shared ? 0 : b, bb = p.b_shared ? 0 : b;
         const int m0 = mt * BM, n0 = nt * BN;
         if constexpr (BRES) {
@@ -170,7 +172,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           mbar_expect_tx(&full[stage], LOAD_BYTES);
           (void)sb;
           const int k0 = (int)(kbeg + (int64_t)kb * BK);
-          if (EPI && kb >= nkb1) {                        // second K segment (K-major A2, B2)
+          if (EPI == 2 && kb >= nkb1) {                   // second K segment (K-major A2, B2)
             const int k2 = (kb - nkb1) * BK;
             tma_load_3d(sa, &tmA2, &full[stage], k2, m0, b);
             if constexpr (!BRES) tma_load_3d(sb, &tmB2, &full[stage], k2, n0, b);
@@ -180,7 +182,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           } else {
             tma_load_3d(sa, &tmA, &full[stage], k0, m0, ba);
           }
-          if (EPI && kb >= nkb1) {
+          if (EPI == 2 && kb >= nkb1) {
           } else if constexpr (!BRES) {
             if (B_MN) {
 #pragma unroll
@@ -220,7 +222,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
       const int64_t kbeg = (int64_t)split * p.k_chunk;
       const int64_t kend = min(p.K, kbeg + p.k_chunk);
-      const int nkb = (int)((kend - kbeg + BK - 1) / BK) + (EPI ? (int)((p.K2 + BK - 1) / BK) : 0);
+      const int nkb = (int)((kend - kbeg + BK - 1) / BK) + (EPI == 2 ? (int)((p.K2 + BK - 1) / BK) : 0);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * ABUF);
@@ -285,7 +287,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         for (int jj = 0; jj < BN / 32; ++jj) {
           const int64_t n = (int64_t)nt * BN + jj * 32 + lane;
           bpre[jj] = (vbias && n < p.N) ? p.bias[(int64_t)b * p.bias_bs + n] : 0.f;
-          spre[jj] = (EPI && p.scale && n < p.N) ? p.scale[(int64_t)b * p.scale_bs + n] : 0.f;
+          spre[jj] = (EPI == 1 && n < p.N) ? p.scale[(int64_t)b * p.scale_bs + n] : 0.f;
         }
       }
       mbar_wait(&tfull[acc], acc_phase);
@@ -297,7 +299,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
         for (int jj = 0; jj < BN / 32; ++jj) {
           st_shared_f32(sbias + (jj * 32 + lane) * 4, bpre[jj]);
-          if (EPI) st_shared_f32(sscale + (jj * 32 + lane) * 4, spre[jj]);
+          if (EPI == 1) st_shared_f32(sscale + (jj * 32 + lane) * 4, spre[jj]);
         }
         __syncwarp();
         cur_key = key;
@@ -317,7 +319,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
         }
       }
-      const bool mask_smem = EPI && p.mask_kb >= 0;
+      const bool mask_smem = EPI == 2 && p.mask_kb >= 0;
+      bool released = false;
       int tile_nkb = 0;
       if (mask_smem) {
         const int64_t kbeg_ = (int64_t)split * p.k_chunk, kend_ = min(p.K, kbeg_ + p.k_chunk);
@@ -346,7 +349,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         float v[64];
 #pragma unroll
         for (int q = 0; q < 64; ++q) v[q] = __uint_as_float(u[q]);
-        if (EPI && p.scale && vbias) {       // fused BN apply: v = v * scale + shift (one FMA)
+        if constexpr (EPI == 1) {            // fused BN apply: v = act(v * scale + shift)
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const float4 s4 = ld_shared_f4(sscale + (j * 64 + 4 * q) * 4);
@@ -354,61 +357,45 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             v[4 * q] = fmaf(v[4 * q], s4.x, t4.x); v[4 * q + 1] = fmaf(v[4 * q + 1], s4.y, t4.y);
             v[4 * q + 2] = fmaf(v[4 * q + 2], s4.z, t4.z); v[4 * q + 3] = fmaf(v[4 * q + 3], s4.w, t4.w);
           }
-        } else if (EPI && p.scale) {
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float4 t4 = ld_shared_f4(sscale + (j * 64 + 4 * q) * 4);
-            v[4 * q] *= t4.x; v[4 * q + 1] *= t4.y; v[4 * q + 2] *= t4.z; v[4 * q + 3] *= t4.w;
-          }
-        } else if (vbias) {
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {               // smem broadcast
-            const float4 t4 = ld_shared_f4(sbias + (j * 64 + 4 * q) * 4);
-            v[4 * q] += t4.x; v[4 * q + 1] += t4.y; v[4 * q + 2] += t4.z; v[4 * q + 3] += t4.w;
-          }
-        } else if (brow) {
-#pragma unroll
-          for (int q = 0; q < 64; ++q)
-            if (n0 + q < p.N) v[q] += brow[n0 + q];
-        }
-        if constexpr (EPI) {
-          if (p.act == HFTA_ACT_RELU) {      // branch once per step, not per element
+          if (p.act == HFTA_ACT_RELU) {
 #pragma unroll
             for (int q = 0; q < 64; ++q) v[q] = fmaxf(v[q], 0.f);
           } else if (p.act == HFTA_ACT_LEAKY_RELU) {
 #pragma unroll
             for (int q = 0; q < 64; ++q) v[q] = v[q] > 0.f ? v[q] : p.act_alpha * v[q];
           }
-          if (mask_smem) {                  // gating values = this tile's A operand, still resident in smem
-            const float neg = p.mask_act == HFTA_ACT_LEAKY_RELU ? p.mask_alpha : 0.f;
-            const int st = (estage + p.mask_kb + j) % STAGES;
-            const uint32_t arow = smem_u32(smem + st * STAGE_BYTES) + (uint32_t)((quarter * 32 + lane) * 128);
-            const uint32_t swz = (uint32_t)(lane & 7);
+        } else {
+          if (vbias) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 raw = ld_shared_f4(arow + (((uint32_t)q ^ swz) << 4));
-              float mv[8];
-              unpack_bf2(__float_as_uint(raw.x), mv[0], mv[1]); unpack_bf2(__float_as_uint(raw.y), mv[2], mv[3]);
-              unpack_bf2(__float_as_uint(raw.z), mv[4], mv[5]); unpack_bf2(__float_as_uint(raw.w), mv[6], mv[7]);
-#pragma unroll
-              for (int e = 0; e < 8; ++e) v[8 * q + e] *= mv[e] > 0.f ? 1.f : neg;
+            for (int q = 0; q < 16; ++q) {             // smem broadcast
+              const float4 t4 = ld_shared_f4(sbias + (j * 64 + 4 * q) * 4);
+              v[4 * q] += t4.x; v[4 * q + 1] += t4.y; v[4 * q + 2] += t4.z; v[4 * q + 3] += t4.w;
             }
-          } else if (p.mask && row_ok) {     // v *= act'(previous activation) (ReLU: mask > 0)
-            const __nv_bfloat16* mrow = p.mask + (int64_t)b * p.mask_bs + m * p.mask_ld + n0;
-            const bool full = n0 + 64 <= p.N;
-            const float neg = p.mask_act == HFTA_ACT_LEAKY_RELU ? p.mask_alpha : 0.f;
+          } else if (brow) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              float mv[8];
-              if (full) {
-                ld_vec<__nv_bfloat16, 8>(mrow + 8 * q, mv);
-              } else {
+            for (int q = 0; q < 64; ++q)
+              if (n0 + q < p.N) v[q] += brow[n0 + q];
+          }
+        }
+        if (EPI == 2 && mask_smem) {         // gating values = this tile's A operand, still resident in smem
+          const int st = (estage + p.mask_kb + j) % STAGES;
+          const uint32_t arow = smem_u32(smem + st * STAGE_BYTES) + (uint32_t)((quarter * 32 + lane) * 128);
+          const uint32_t swz = (uint32_t)(lane & 7);
 #pragma unroll
-                for (int e = 0; e < 8; ++e) mv[e] = n0 + 8 * q + e < p.N ? __bfloat162float(mrow[8 * q + e]) : 0.f;
-              }
+          for (int q = 0; q < 8; ++q) {
+            const uint4 raw = ld_shared_u4(arow + (((uint32_t)q ^ swz) << 4));
+            const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
-              for (int e = 0; e < 8; ++e) v[8 * q + e] *= mv[e] > 0.f ? 1.f : neg;
+            for (int e = 0; e < 4; ++e) {      // bf16 > 0 <=> sign bit clear and nonzero (ReLU')
+              v[8 * q + 2 * e] = (int32_t)(w4[e] << 16) > 0 ? v[8 * q + 2 * e] : 0.f;
+              v[8 * q + 2 * e + 1] = (int32_t)(w4[e] & 0xffff0000u) > 0 ? v[8 * q + 2 * e + 1] : 0.f;
             }
+          }
+          if (si == my_steps - 1) {          // last read of this tile's A stages by this warp: release them
+            __syncwarp();
+            if (lane == 0)
+              for (int k = 0; k < tile_nkb; ++k) mbar_arrive(&empty[(estage + k) % STAGES]);
+            released = true;
           }
         }
         if constexpr (!OUT_F32) {
@@ -459,10 +446,12 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
         }
       }
-      if (mask_smem) {                   // this tile's smem stages may now be refilled
-        __syncwarp();
-        if (lane == 0)
-          for (int k = 0; k < tile_nkb; ++k) mbar_arrive(&empty[(estage + k) % STAGES]);
+      if (mask_smem) {                   // warps that read no mask this tile release here
+        if (!released) {
+          __syncwarp();
+          if (lane == 0)
+            for (int k = 0; k < tile_nkb; ++k) mbar_arrive(&empty[(estage + k) % STAGES]);
+        }
         estage = (estage + tile_nkb) % STAGES;
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -477,14 +466,14 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   }
 }
 
-template <bool A_MN, bool B_MN, int BN, bool OUT_F32, bool BRES, bool EPI = false>
+template <bool A_MN, bool B_MN, int BN, bool OUT_F32, bool BRES, int EPI = 0>
 hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   // EPI non-BRES BN=64 (the two-segment gated dgrad): 6 stages so a tile's 3
   // k-blocks can stay resident for the epilogue while the next tile loads
-  constexpr int STAGES = BRES ? 4 : ((BN == 256) ? 3 : ((EPI && BN == 64) ? 6 : 4));
+  constexpr int STAGES = BRES ? 4 : ((BN == 256) ? 3 : ((EPI == 2 && BN == 64) ? 6 : 4));
   constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + (BRES ? 0 : BN * BK * 2)) +
                           (BRES ? 2 * BN * BK * 2 : 0) + 1024 + (OUT_F32 ? 0 : NEPI * 2 * 4096) +
-                          NEPI * BN * 4 * (EPI ? 2 : 1) +
+                          NEPI * BN * 4 * (EPI == 1 ? 2 : 1) +
                           ((A_MN && B_MN && OUT_F32) ? (size_t)STAGES * 8192 : 0);
   static_assert(SMEM <= 232448, "shared memory budget");
   if (hfta_status st = get_encode()) return st;
@@ -498,7 +487,7 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   else st = make_map(&tb, p.Bm, p.K, p.N, p.b_ld, p.b_bs, nbb, BK, BN);
   if (st) return st;
   CUtensorMap ta2 = ta, tb2 = tb;
-  if (EPI && p.K2 > 0) {
+  if (EPI == 2 && p.K2 > 0) {
     if (hfta_status st2 = make_map(&ta2, p.A2, p.K2, p.M, p.a2_ld, p.a2_bs, p.B, BK, BM)) return st2;
     if (hfta_status st2 = make_map(&tb2, p.Bm2, p.K2, p.N, p.b2_ld, p.b2_bs, p.B, BK, BN)) return st2;
   }
@@ -524,12 +513,12 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   a.scale = p.scale; a.scale_bs = p.scale_bs; a.act = p.act; a.act_alpha = p.act_alpha;
   a.mask = reinterpret_cast<const __nv_bfloat16*>(p.mask); a.mask_bs = p.mask_bs; a.mask_ld = p.mask_ld;
   a.mask_act = p.mask_act; a.mask_alpha = p.mask_alpha;
-  a.K2 = EPI ? p.K2 : 0;
+  a.K2 = EPI == 2 ? p.K2 : 0;
   a.colsum = p.colsum; a.colsum_bs = p.colsum_bs; a.colsum_acc = p.colsum_acc; a.colsum_part = p.colsum_part;
   a.mask_kb = -1;
   // the gating tensor is the A operand itself (same rows, its columns = the
   // output's): read it from the resident A stage instead of global memory
-  if (EPI && p.mask && p.splits == 1 && p.N <= BN) {
+  if (EPI == 2 && p.mask && p.splits == 1 && p.N <= BN) {
     if (p.K2 > 0 && p.mask == p.A2 && p.mask_bs == p.a2_bs && p.mask_ld == p.a2_ld && p.K2 == p.N)
       a.mask_kb = (int)cdiv(p.K, BK);
     else if (p.K2 == 0 && p.mask == p.A && p.mask_bs == p.a_bs && p.mask_ld == p.a_ld && p.K == p.N && p.a_kmajor)
@@ -549,16 +538,31 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
 }
 
 bool needs_epi(const GemmP& p) { return p.scale || p.act != HFTA_ACT_NONE || p.mask || p.K2 > 0; }
+bool epi1(const GemmP& p) { return p.scale && p.bias && p.bias_div == 0 && !p.mask && p.K2 == 0; }
+bool epi2(const GemmP& p) {   // bias, second K segment, gating by the A operand (or A2) itself (ReLU'), N <= 128
+  if (p.scale || p.act != HFTA_ACT_NONE || p.N > 128) return false;
+  if (!p.mask) return true;
+  if (p.mask_act != HFTA_ACT_RELU) return false;
+  if (p.K2 > 0) return p.mask == p.A2 && p.mask_bs == p.a2_bs && p.mask_ld == p.a2_ld && p.K2 == p.N;
+  return p.mask == p.A && p.mask_bs == p.a_bs && p.mask_ld == p.a_ld && p.K == p.N;
+}
 
 template <bool A_MN, bool B_MN, bool OUT_F32>
 hfta_status dispatch_bn(const GemmP& p, cudaStream_t s) {
   if constexpr (!A_MN && !B_MN && !OUT_F32) {
-    if (needs_epi(p)) {                          // fused BN apply / gated dgrad (N <= 128)
+    if (needs_epi(p)) {
       const bool bres = p.K2 == 0 && p.K <= 2 * BK;
-      if (p.N <= 64) return bres ? launch_tc<false, false, 64, false, true, true>(p, s)
-                                 : launch_tc<false, false, 64, false, false, true>(p, s);
-      return bres ? launch_tc<false, false, 128, false, true, true>(p, s)
-                  : launch_tc<false, false, 128, false, false, true>(p, s);
+      if (epi1(p)) {                              // fused BN apply (forward)
+        if (p.N <= 64) return bres ? launch_tc<false, false, 64, false, true, 1>(p, s)
+                                   : launch_tc<false, false, 64, false, false, 1>(p, s);
+        if (p.N <= 128) return bres ? launch_tc<false, false, 128, false, true, 1>(p, s)
+                                    : launch_tc<false, false, 128, false, false, 1>(p, s);
+        return launch_tc<false, false, 128, false, false, 1>(p, s);
+      }
+      if (p.N <= 64) return bres ? launch_tc<false, false, 64, false, true, 2>(p, s)
+                                 : launch_tc<false, false, 64, false, false, 2>(p, s);
+      return bres ? launch_tc<false, false, 128, false, true, 2>(p, s)
+                  : launch_tc<false, false, 128, false, false, 2>(p, s);
     }
     if (p.K <= 2 * BK && p.splits == 1) {        // forward with small K: B-resident schedule
       if (p.N <= 64) return launch_tc<A_MN, B_MN, 64, OUT_F32, true>(p, s);
@@ -585,12 +589,11 @@ bool env_disabled() {
 bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32) {
   if (env_disabled() || dt_in != HFTA_BF16) return false;
   if (needs_epi(p)) {
-    if (out_f32 || p.splits != 1 || !p.a_kmajor || !p.b_kmajor || p.N > 128 || p.accumulate) return false;
+    if (out_f32 || p.splits != 1 || !p.a_kmajor || !p.b_kmajor || p.accumulate) return false;
+    if (!epi1(p) && !epi2(p)) return false;
     if (p.K2 > 0 && (p.K % BK || p.K2 % BK || !aligned16(p.A2) || !aligned16(p.Bm2) || (p.a2_ld * 2) % 16 ||
                      (p.b2_ld * 2) % 16 || (p.a2_bs * 2) % 16 || (p.b2_bs * 2) % 16))
       return false;
-    if (p.mask && (!aligned16(p.mask) || p.mask_ld % 8 || p.mask_bs % 8)) return false;
-    if (p.scale && p.bias && p.bias_div > 0) return false;
   }
   if (p.K < 16 || p.N < 16 || p.M < 1) return false;
   if (!aligned16(p.A) || !aligned16(p.Bm)) return false;
