@@ -226,10 +226,15 @@ hfta_status hfta_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C, hfta_dtype d
  *   enters running_var, reading R6), xhat = (Y - mean)*invstd,
  *   G[b][n][c] = max_l act(gamma*xhat + beta), argmax[b][n][c] = first l
  *   attaining it (reading R15), ext[b][n][c] = Y at that row.
- * The [B][R][C] tensor Y is never written: the forward reduces it out of
- * tensor memory and the backward recomputes it tile by tile (K10).
- * Precision: bf16 X/W (dt must be HFTA_BF16), fp32 accumulation, statistics
- * from fp32 partials combined in fp64.  Layouts: X [B][R][K] (bstride 0 =
+ * The [B][R][C] tensor Y is never written: the forward reduces only its
+ * per-cloud max out of tensor memory and takes the statistics from the Gram
+ * of the layer input (reading R27):
+ *   gram = X^T X [K][K], xsum = X^T 1 [K]  (fp32 outputs, caller-owned,
+ *   contiguous [B][K][K] / [B][K]; inputs of the backward),
+ *   mean_c = W_c xsum/R + bias_c,  var_c = W_c (gram - xsum xsum^T/R) W_c^T / R
+ * (centred in fp64 before the fp32 quadratic form); the backward works in
+ * the same Gram form (K10).  Precision: bf16 X/W (dt must be
+ * HFTA_BF16), fp32 accumulation.  Layouts: X [B][R][K] (bstride 0 =
  * shared), W [B][C][K] (hfta_in), per-channel vectors at [b*bstride + c];
  * G, ext fp32 [B][N][C] (hfta_out), argmax int32 contiguous [B][N][C].
  * Constraints (else HFTA_ERR_UNSUPPORTED): K in {64, 128}, C % 128 == 0,
@@ -246,6 +251,7 @@ hfta_status hfta_fused_linear_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C,
                                          float momentum, float eps, hfta_act act, float act_alpha,
                                          hfta_out G, int32_t* argmax, hfta_out ext,
                                          float* save_mean, float* save_invstd,
+                                         float* gram, float* xsum,
                                          void* ws, size_t ws_bytes, hfta_stream stream);
 /*
  * Backward: dG fp32 [B][N][C] -> dZ at the argmax rows (act' at the pooled
@@ -256,9 +262,10 @@ hfta_status hfta_fused_linear_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C,
  * one nonzero per cloud and channel) is never formed: dX = X M + 1 v^T + S W
  * and dW = diag(bx) W G + cc s^T + S^T X with M = W^T diag(bx) W (rounded to
  * bf16), v = W^T cc, G = X^T X, s = X^T 1 (K10).  accumulate != 0
- * adds to dW/dgamma/dbeta instead of overwriting.  ext/argmax/save_* are the
- * forward's outputs.  dX_act != NONE multiplies dX by act'(X) (X being the
- * previous layer's activation output), so dX is that layer's dZ.  C <= 1024.
+ * adds to dW/dgamma/dbeta instead of overwriting.  ext, argmax, save_mean,
+ * save_invstd, gram (= G) and xsum (= s) are the forward's outputs.
+ * dX_act != NONE multiplies dX by act'(X) (X being the previous layer's
+ * activation output), so dX is that layer's dZ.  C <= 1024.
  */
 hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C, int64_t K,
                                          hfta_dtype dt, hfta_in dG, hfta_in X, hfta_in W,
@@ -266,6 +273,7 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
                                          const float* bias, int64_t bias_bstride,
                                          const float* gamma, const float* beta, int64_t gb_bstride,
                                          const float* save_mean, const float* save_invstd,
+                                         const float* gram, const float* xsum,
                                          hfta_act act, float act_alpha, hfta_out dX,
                                          hfta_act dX_act, float dX_alpha,
                                          float* dW, int64_t dW_bstride, int64_t dW_ld,

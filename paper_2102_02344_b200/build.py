@@ -10,6 +10,7 @@ LIB = os.path.join(HERE, "libhfta.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+FLAGS += os.environ.get("HFTA_NVCC_EXTRA", "").split()   # developer builds only (e.g. -DHFTA_LBM_PROF)
 
 
 def sources():

@@ -41,6 +41,8 @@ namespace hfta {
 namespace {
 
 constexpr int LT = 320;
+constexpr int FWD_LT = 352;         // forward: producer, MMA issuers (warps 1, 10), 8 epilogue warps
+constexpr int MMA2_WARP = 10;
 constexpr int NEPIW = 8;
 constexpr int CBLK = 128;                      // channels per UMMA M block
 constexpr uint32_t WKB = CBLK * 64 * 2;        // one 64-wide k block of a 128-channel W block: 16 KB
@@ -50,7 +52,7 @@ constexpr int FG = 2;                          // channel blocks per unit: TMEM 
 constexpr int FSTAGES = 3;
 constexpr int NBW = FG / 2;                    // channel blocks per epilogue warp
 constexpr int LPB = FR / 32;                   // 32-column TMEM loads per block and chunk
-static_assert(NBW * LPB == 4, "epilogue load schedule assumes 4 loads per warp and chunk");
+static_assert(NBW == 1 && LPB == 4, "epilogue: one 128-channel block and four 32-column loads per warp and chunk");
 constexpr uint32_t FA_KB = FR * 64 * 2;        // 8 KB per k block of an X chunk
 
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
@@ -69,33 +71,33 @@ __device__ __forceinline__ void tmem_free512(uint32_t base) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base));
 }
 
+
+#ifdef HFTA_LBM_PROF
+// developer build only: per-CTA cycle counters of the forward's waits
+}  // namespace
+__device__ unsigned long long g_lbm_prof[512][8];
+namespace {
+#define PROF_WAIT(slot, call)                  \
+  do {                                         \
+    const long long t0_ = clock64();           \
+    call;                                      \
+    prof[slot] += clock64() - t0_;             \
+  } while (0)
+#else
+#define PROF_WAIT(slot, call) call
+#endif
+
 // ================================================================ forward ==
 
 struct FwdArgs {
-  int B, Ncl, nblk, ngroups, teams, nkb, a_shared, mode;
+  int B, Ncl, nblk, ngroups, teams, nkb, a_shared;
   int64_t L, C;
-  float* s1; float* s2; float* mx; int32_t* idx;   // per-cloud partials [B][Ncl][C]
+  float* mx; int32_t* idx;   // per-cloud max of Y' and its first row [B][Ncl][C]
 };
 
-// Packed fp32x2 arithmetic (FADD2 / FFMA2) and 3-input max (FMNMX3) keep the
-// epilogue's issue count at ~2 instructions per accumulator element, below
-// the MMA rate for K = 128 (one 64-point chunk: 1024 MMA cycles per SM).
-__device__ __forceinline__ unsigned long long pk2(uint32_t lo, uint32_t hi) {
-  unsigned long long r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
-  return r;
-}
-__device__ __forceinline__ void add2(unsigned long long& acc, unsigned long long v) {
-  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(v));
-}
-__device__ __forceinline__ void sq2(unsigned long long& acc, unsigned long long v) {
-  asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc) : "l"(v));
-}
-__device__ __forceinline__ float hsum2(unsigned long long v) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-  return lo + hi;
-}
+// The epilogue reduces only the max: BN statistics come from the Gram of X
+// (k_lbm_stats), so per accumulator element the epilogue issues ~0.4
+// instructions (FMNMX3 tree) instead of ~2 (sums and squares as well).
 __device__ __forceinline__ float max3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -103,56 +105,45 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
 }
 __device__ __forceinline__ float uf(uint32_t x) { return __uint_as_float(x); }
 
-// Per-channel running state of the forward epilogue: packed sums, running
-// max m and the 16-point group it came from; the group's values sit in this
-// lane's smem slot so the exact first index is resolved once per cloud.
+// Per-channel running state of the forward epilogue: running max m and the
+// 16-point group it came from; the group's values sit in this lane's smem
+// slot so the exact first index is resolved once per cloud.
 struct FwdAcc {
-  unsigned long long s1[2], s2[2];
   float m;
   int gid;
 };
 
-// One 16-point group (values u[o..o+15]) of one channel.  FULL = all valid.
+// One 16-point group (values u[0..15]) of one channel; FULL = all valid.
+// Predicated update (no vote / branch): improvements are rare after the
+// first groups of a cloud.
 template <bool FULL>
 __device__ __forceinline__ void fwd_group(const uint32_t* u, int valid, int gid, FwdAcc& A, uint32_t slot) {
   uint32_t v[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = (FULL || j < valid) ? u[j] : 0u;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const unsigned long long w = pk2(v[2 * q], v[2 * q + 1]);
-    add2(A.s1[q & 1], w);
-    sq2(A.s2[q & 1], w);
-  }
-  if (!FULL) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = j < valid ? v[j] : __float_as_uint(-INFINITY);
-  }
+  for (int j = 0; j < 16; ++j) v[j] = (FULL || j < valid) ? u[j] : __float_as_uint(-INFINITY);
   const float a0 = max3(uf(v[0]), uf(v[1]), uf(v[2])), a1 = max3(uf(v[3]), uf(v[4]), uf(v[5]));
   const float a2 = max3(uf(v[6]), uf(v[7]), uf(v[8])), a3 = max3(uf(v[9]), uf(v[10]), uf(v[11]));
   const float a4 = max3(uf(v[12]), uf(v[13]), uf(v[14]));
   const float gm = fmaxf(max3(a0, a1, a2), max3(a3, a4, uf(v[15])));
   const bool p = gm > A.m;
-  if (__any_sync(0xffffffffu, p)) {
-    if (p) {
-      A.m = gm;
-      A.gid = gid;
+  A.m = p ? gm : A.m;
+  A.gid = p ? gid : A.gid;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        st_shared_v4(slot + q * 512, make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-    }
-  }
+  for (int q = 0; q < 4; ++q)
+    if (p) st_shared_v4(slot + q * 512, make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
 }
 
-__global__ void __launch_bounds__(LT, 1)
+__global__ void __launch_bounds__(FWD_LT, 1)
 k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW, FwdArgs p) {
+  constexpr int NST = FSTAGES;                                 // X chunk stages
+  constexpr uint32_t SKB = FA_KB;                              // bytes per k block of a chunk
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* wres = smem;                                        // FG blocks x 2 k blocks x 16 KB
-  uint8_t* ast = wres + FG * 2 * WKB;                          // FSTAGES x 2 k blocks x 8 KB
-  uint64_t* full = reinterpret_cast<uint64_t*>(ast + FSTAGES * 2 * FA_KB);
-  uint64_t* empty = full + FSTAGES;
-  uint64_t* tfull = empty + FSTAGES;
+  uint8_t* ast = wres + FG * 2 * WKB;                          // NST x 2 k blocks x SKB
+  uint64_t* full = reinterpret_cast<uint64_t*>(ast + NST * 2 * SKB);
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
   uint64_t* wfull = tempty + 2;
   uint64_t* wempty = wfull + 1;
@@ -160,11 +151,15 @@ k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint8_t* slot_base = reinterpret_cast<uint8_t*>(full) + 256;        // NEPIW x NBW ch x 4 x 32 lanes x 16 B
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+#ifdef HFTA_LBM_PROF
+  long long prof[4] = {0, 0, 0, 0};
+  const long long tstart = clock64();
+#endif
   if (threadIdx.x == 0) {
-    for (int s = 0; s < FSTAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], NEPIW); }
     mbar_init(wfull, 1);
-    mbar_init(wempty, 1);
+    mbar_init(wempty, 2);                                      // one commit per issuing warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -182,7 +177,7 @@ k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   const int64_t npairs = (int64_t)p.B * p.Ncl;
   const int64_t u0 = npairs * team / p.teams, u1 = npairs * (team + 1) / p.teams;
   const int nch = (int)((p.L + FR - 1) / FR);
-  const int blk0 = g * FG;
+  const int blk0 = g * FG;                                     // this CTA's channel blocks blk0 + j, j < nb
   const int nb = min(FG, p.nblk - blk0);
 
   if (warp == 0) {
@@ -204,49 +199,60 @@ k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         const int ba = p.a_shared ? 0 : b;
         for (int ch = 0; ch < nch; ++ch) {
-          mbar_wait(&empty[stage], ph ^ 1);
-          mbar_expect_tx(&full[stage], (uint32_t)p.nkb * FA_KB);
+          PROF_WAIT(0, mbar_wait(&empty[stage], ph ^ 1));
+          mbar_expect_tx(&full[stage], (uint32_t)p.nkb * SKB);
           for (int kb = 0; kb < p.nkb; ++kb)
-            tma_load_3d(ast + (stage * 2 + kb) * FA_KB, &tmA, &full[stage], kb * 64, (int)(n * p.L + ch * FR), ba);
-          if (++stage == FSTAGES) { stage = 0; ph ^= 1; }
+            tma_load_3d(ast + (stage * 2 + kb) * SKB, &tmA, &full[stage], kb * 64, (int)(n * p.L + ch * FR), ba);
+          if (++stage == NST) { stage = 0; ph ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || warp == MMA2_WARP) {
+    // Two issuing warps alternate chunks (warp 1: even, MMA2_WARP: odd) and
+    // pass a token (named barriers 1/2) after each chunk's MMAs are issued:
+    // the tcgen05 queue is shallow, so a single issuer's per-chunk barrier
+    // waits (~100+ cycles) would idle the tensor pipe; here one warp waits
+    // while the other issues.  Accumulator buffer = chunk parity.
     constexpr uint32_t IDESC = idesc_bf16(CBLK, FR, false, false);
-    int stage = 0, acc = 0, curb = -1;
-    uint32_t ph = 0, aph = 0, wep = 0;
+    const int mw = warp == 1 ? 0 : 1;
+    const int64_t gtot = (u1 - u0) * nch;
+    int curb = -1;
+    uint32_t wep = 0;
+    int64_t gc = 0;
     for (int64_t u = u0; u < u1; ++u) {
       const int b = (int)(u / p.Ncl);
       if (b != curb) {
-        if (curb >= 0) tc_commit_w(wempty);
+        if (curb >= 0) tc_commit_w(wempty);   // both issuers' MMAs on the old W (wempty counts 2 commits)
         __syncwarp();
         mbar_wait(wfull, wep & 1);
         curb = b;
         ++wep;
       }
-      for (int ch = 0; ch < nch; ++ch) {
-        mbar_wait(&tempty[acc], aph ^ 1);
-        mbar_wait(&full[stage], ph);
+      for (int ch = 0; ch < nch; ++ch, ++gc) {
+        if ((int)(gc & 1) != mw) continue;
+        const int acc = (int)(gc & 1);
+        const int stage = (int)(gc % NST);
+        PROF_WAIT(0, mbar_wait(&tempty[acc], (uint32_t)((gc >> 1) & 1) ^ 1u));
+        PROF_WAIT(1, mbar_wait(&full[stage], (uint32_t)((gc / NST) & 1)));
         tc_fence_after();
-        {
-          const uint64_t bd0 = smem_desc(smem_u32(ast + stage * 2 * FA_KB), 16, 1024);
-          for (int j = 0; j < nb; ++j) {
-            const uint32_t d = tmem_base + (uint32_t)(acc * FG * FR + j * FR);
-            const uint64_t ad0 = smem_desc(smem_u32(wres + j * 2 * WKB), 16, 1024);
-            for (int kb = 0; kb < p.nkb; ++kb) {
+        if (gc > 0) asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)(gc & 1)) : "memory");   // token from chunk gc-1
+        const uint64_t bd0 = smem_desc(smem_u32(ast + stage * 2 * SKB), 16, 1024);
+        for (int j = 0; j < nb; ++j) {
+          const uint32_t d = tmem_base + (uint32_t)(acc * FG * FR + j * FR);
+          const uint64_t ad0 = smem_desc(smem_u32(wres + j * 2 * WKB), 16, 1024);
+          for (int kb = 0; kb < p.nkb; ++kb) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k)   // +32 B per k step, +WKB / FA_KB per k block (descriptor units of 16 B)
-                tc_mma_ss(d, ad0 + (uint64_t)(kb * (WKB >> 4) + 2 * k), bd0 + (uint64_t)(kb * (FA_KB >> 4) + 2 * k), IDESC,
-                          (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < 4; ++k) {   // +32 B per k step, +WKB / SKB per k block (descriptor units of 16 B)
+              const uint64_t ad = ad0 + (uint64_t)(kb * (WKB >> 4) + 2 * k);
+              const uint64_t bd = bd0 + (uint64_t)(kb * (SKB >> 4) + 2 * k);
+              tc_mma_ss(d, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
             }
           }
-          tc_commit_w(&empty[stage]);
-          tc_commit_w(&tfull[acc]);
         }
+        tc_commit_w(&empty[stage]);
+        tc_commit_w(&tfull[acc]);
+        if (gc + 1 < gtot) asm volatile("bar.arrive %0, 64;" ::"r"(1 + (int)((gc + 1) & 1)) : "memory");   // token
         __syncwarp();
-        if (++stage == FSTAGES) { stage = 0; ph ^= 1; }
-        if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
   } else {
@@ -260,7 +266,6 @@ k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       FwdAcc A[NBW];
 #pragma unroll
       for (int jj = 0; jj < NBW; ++jj) {
-        A[jj].s1[0] = A[jj].s1[1] = A[jj].s2[0] = A[jj].s2[1] = 0ull;
         A[jj].m = -INFINITY;
         A[jj].gid = 0;
       }
@@ -270,49 +275,45 @@ k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (int jj = 0; jj < NBW; ++jj) nld += half + 2 * jj < nb ? LPB : 0;
       for (int ch = 0; ch < nch; ++ch) {
         const int valid = (int)min((int64_t)FR, p.L - (int64_t)ch * FR);
-        mbar_wait(&tfull[acc], aph);
+        PROF_WAIT(0, mbar_wait(&tfull[acc], aph));
         tc_fence_after();
+        // all four 32-column loads in flight, one wait, release the
+        // accumulator, then reduce while the next chunks' MMAs run
         const uint32_t ta = tmem_base + (uint32_t)(acc * FG * FR + half * FR) + ((uint32_t)(quarter * 32) << 16);
-        auto release = [&]() {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        };
-        // load i+1 is in flight while load i is reduced; i -> (block jj = i/2, columns hh = i%2)
-        auto proc = [&](const uint32_t (&r)[32], int i) {
-          const int jj = i / LPB, hh = i % LPB;
-          const int g0 = ch * (FR / 16) + hh * 2;
-          const uint32_t sl = slots + (uint32_t)(jj * 4 * 32 * 16);
-          if (p.mode == 1) {
-            if (r[0] == 0x7f800001u && r[31] == 0x7f800001u) A[jj].m = 1.f;   // diagnostics: keep the load live
-          } else if (valid == FR) {
-            fwd_group<true>(r, 16, g0, A[jj], sl);
-            fwd_group<true>(r + 16, 16, g0 + 1, A[jj], sl);
-          } else {
-            fwd_group<false>(r, valid - hh * 32, g0, A[jj], sl);
-            fwd_group<false>(r + 16, valid - hh * 32 - 16, g0 + 1, A[jj], sl);
-          }
-        };
-        uint32_t r0[32], r1[32];
-        if (nld == 0) {
-          release();
-        } else {
+        uint32_t r0[32], r1[32], r2[32], r3[32];
+        const bool work = nld != 0;
+        if (work) {
           tmem_ld32_nowait(ta, r0);
+          tmem_ld32_nowait(ta + 32, r1);
+          tmem_ld32_nowait(ta + 64, r2);
+          tmem_ld32_nowait(ta + 96, r3);
           tmem_wait_ld();
-          auto col = [](int i) { return (uint32_t)(2 * (i / LPB) * FR + (i % LPB) * 32); };
-          tmem_ld32_nowait(ta + col(1), r1);
-          proc(r0, 0);
-          tmem_wait_ld();
-          if (nld == 4) tmem_ld32_nowait(ta + col(2), r0);
-          else release();
-          proc(r1, 1);
-          if (nld == 4) {
-            tmem_wait_ld();
-            tmem_ld32_nowait(ta + col(3), r1);
-            proc(r0, 2);
-            tmem_wait_ld();
-            release();
-            proc(r1, 3);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&tempty[acc]);
+        }
+        if (work) {
+          const int g0 = ch * (FR / 16);
+          if (valid == FR) {
+            fwd_group<true>(r0, 16, g0, A[0], slots);
+            fwd_group<true>(r0 + 16, 16, g0 + 1, A[0], slots);
+            fwd_group<true>(r1, 16, g0 + 2, A[0], slots);
+            fwd_group<true>(r1 + 16, 16, g0 + 3, A[0], slots);
+            fwd_group<true>(r2, 16, g0 + 4, A[0], slots);
+            fwd_group<true>(r2 + 16, 16, g0 + 5, A[0], slots);
+            fwd_group<true>(r3, 16, g0 + 6, A[0], slots);
+            fwd_group<true>(r3 + 16, 16, g0 + 7, A[0], slots);
+          } else {
+            fwd_group<false>(r0, valid, g0, A[0], slots);
+            fwd_group<false>(r0 + 16, valid - 16, g0 + 1, A[0], slots);
+            fwd_group<false>(r1, valid - 32, g0 + 2, A[0], slots);
+            fwd_group<false>(r1 + 16, valid - 48, g0 + 3, A[0], slots);
+            fwd_group<false>(r2, valid - 64, g0 + 4, A[0], slots);
+            fwd_group<false>(r2 + 16, valid - 80, g0 + 5, A[0], slots);
+            fwd_group<false>(r3, valid - 96, g0 + 6, A[0], slots);
+            fwd_group<false>(r3 + 16, valid - 112, g0 + 7, A[0], slots);
           }
         }
         if (++acc == 2) { acc = 0; aph ^= 1; }
@@ -332,13 +333,20 @@ k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         const int64_t c = (int64_t)(blk0 + j) * CBLK + quarter * 32 + lane;
         const int64_t o = ((int64_t)b * p.Ncl + n) * p.C + c;
-        p.s1[o] = hsum2(A[jj].s1[0]) + hsum2(A[jj].s1[1]);
-        p.s2[o] = hsum2(A[jj].s2[0]) + hsum2(A[jj].s2[1]);
         p.mx[o] = A[jj].m;
         p.idx[o] = A[jj].gid * 16 + first;
       }
     }
   }
+#ifdef HFTA_LBM_PROF
+  if (lane == 0 && warp <= 2) {
+    const int base = warp == 0 ? 0 : warp == 1 ? 2 : 4;
+    g_lbm_prof[blockIdx.x][base] = prof[0];
+    if (warp == 1) g_lbm_prof[blockIdx.x][base + 1] = prof[1];
+    if (warp == 2) g_lbm_prof[blockIdx.x][base + 1] = prof[2];
+    if (warp == 2) g_lbm_prof[blockIdx.x][7] = clock64() - tstart;
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -351,63 +359,187 @@ k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 // reduces a max.  Sign flips are exact, so Y' = s * Y bit for bit.
 __global__ void k_lbm_flip(int B, int64_t C, int64_t K, const __nv_bfloat16* __restrict__ W, int64_t wbs, int64_t wld,
                            const float* __restrict__ gamma, int64_t gbs, __nv_bfloat16* __restrict__ Wf) {
-  const int64_t n = (int64_t)B * C * K;
+  // 8 bf16 (16 B) per thread; rows are 16-B aligned (check_common); sign flip = XOR of the sign bits
+  const int kv = (int)(K / 8);
+  const int64_t n = (int64_t)B * C * kv;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = i % K, c = (i / K) % C, b = i / (K * C);
-    const __nv_bfloat16 w = W[b * wbs + c * wld + k];
-    Wf[i] = gamma[b * gbs + c] < 0.f ? __hneg(w) : w;
+    const int64_t row = i / kv;
+    const int k8 = (int)(i - row * kv);
+    const int64_t b = row / C, c = row - b * C;
+    uint4 w = *reinterpret_cast<const uint4*>(W + b * wbs + c * wld + k8 * 8);
+    if (gamma[b * gbs + c] < 0.f) { w.x ^= 0x80008000u; w.y ^= 0x80008000u; w.z ^= 0x80008000u; w.w ^= 0x80008000u; }
+    *reinterpret_cast<uint4*>(Wf + row * K + k8 * 8) = w;
   }
 }
 
-// Per (model, channel): Chan's parallel combination of the per-cloud moments
-// in fp64 (fixed cloud order), then statistics, running averages and the
-// pooled outputs.
-__global__ void k_lbm_fwd_fin(int B, int Ncl, int64_t L, int64_t C, const float* __restrict__ s1,
-                              const float* __restrict__ s2, const float* __restrict__ mx,
-                              const int32_t* __restrict__ idx, const float* __restrict__ bias, int64_t bias_bs,
-                              const float* __restrict__ gamma, const float* __restrict__ beta, int64_t gbs,
-                              float* __restrict__ rmean, float* __restrict__ rvar, float momentum, float eps, int act,
-                              float alpha, float* __restrict__ G, int64_t g_bs, int64_t g_ld,
-                              int32_t* __restrict__ amax, int64_t am_bs, int64_t am_ld, float* __restrict__ ext,
-                              int64_t ext_bs, int64_t ext_ld, float* __restrict__ smean, float* __restrict__ sinv) {
+// BN batch statistics of Y = X W^T from the Gram of the layer input (exact
+// algebra, reading R27): with mu = s/R and the centred Gram
+//   Gc = G - R mu mu^T   (fp64 -> fp32: centring first avoids the
+//                         E[y^2] - E[y]^2 cancellation),
+//   mean_c = W_c . mu (+ bias_c),   var_c = W_c Gc W_c^T / R   (biased).
+// One CTA per (model, 64 channels), Gc [K][K] and W^T [K][64] in smem;
+// thread (channel group cg of 4, k group kg of 16) accumulates
+// t[c][k] = sum_j Gc[j][k] W_c[j] for 4 channels x K/16 k (register blocked:
+// 2-3 LDS.128 per 32 FMA), then the dot with W_c in fp64 reduced over the 16
+// k groups of a half-warp.  Writes save_mean / save_invstd and the running
+// statistics.  K in {64, 128}.
+constexpr int ST_CH = 64;                // channels per CTA
+template <int K>
+__global__ void __launch_bounds__(256) k_lbm_stats(int B, int64_t R, int64_t C, const float* __restrict__ G,
+                                                   const float* __restrict__ xs, const __nv_bfloat16* __restrict__ W,
+                                                   int64_t wbs, int64_t wld, const float* __restrict__ bias,
+                                                   int64_t bias_bs, float* __restrict__ rmean,
+                                                   float* __restrict__ rvar, float momentum, float eps,
+                                                   float* __restrict__ smean, float* __restrict__ sinv) {
+  extern __shared__ __align__(16) float st_smem[];
+  float* Gc = st_smem;                             // [K][K]
+  float* Wt = st_smem + K * K;                     // [K][ST_CH]
+  __shared__ double mu[128];
+  const int b = blockIdx.y;
+  const int64_t c0 = (int64_t)blockIdx.x * ST_CH;
+  const float* Gb = G + (int64_t)b * K * K;
+  const double Rd = (double)R;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) mu[k] = (double)xs[(int64_t)b * K + k] / Rd;
+  __syncthreads();
+  constexpr int lk = K == 128 ? 7 : 6;
+  // vector loads, 4 in flight per thread (the prologue is L2-latency bound otherwise)
+  const float4* G4 = reinterpret_cast<const float4*>(Gb);
+  const int n4 = K * K / 4;
+  for (int i0 = threadIdx.x; i0 < n4; i0 += 4 * blockDim.x) {
+    float4 g[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < n4) g[u] = __ldg(G4 + i);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < n4) {
+        const int j = (4 * i) >> lk, k = (4 * i) & (K - 1);
+        const double mj = Rd * mu[j];
+        float4 o;
+        o.x = (float)((double)g[u].x - mj * mu[k]);
+        o.y = (float)((double)g[u].y - mj * mu[k + 1]);
+        o.z = (float)((double)g[u].z - mj * mu[k + 2]);
+        o.w = (float)((double)g[u].w - mj * mu[k + 3]);
+        *reinterpret_cast<float4*>(Gc + 4 * i) = o;
+      }
+    }
+  }
+  const __nv_bfloat16* Wb = W + (int64_t)b * wbs;
+  constexpr int kv = K / 8;                        // 16-B vectors per W row (rows 16-B aligned)
+  for (int i0 = threadIdx.x; i0 < ST_CH * kv; i0 += 2 * blockDim.x) {
+    uint4 wv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u * blockDim.x;
+      const int cl = i % ST_CH, k8 = i / ST_CH;    // lanes over channels: conflict-free transposed stores
+      const int64_t c = c0 + cl;
+      wv[u] = (i < ST_CH * kv && c < C) ? __ldg(reinterpret_cast<const uint4*>(Wb + c * wld) + k8)
+                                        : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i >= ST_CH * kv) continue;
+      const int cl = i % ST_CH, k8 = i / ST_CH;
+      const uint32_t e[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        Wt[(k8 * 8 + 2 * q) * ST_CH + cl] = __uint_as_float(e[q] << 16);
+        Wt[(k8 * 8 + 2 * q + 1) * ST_CH + cl] = __uint_as_float(e[q] & 0xffff0000u);
+      }
+    }
+  }
+  __syncthreads();
+  const int kg = threadIdx.x & 15, cg = threadIdx.x >> 4;     // 16 channel groups x 16 k groups
+  constexpr int nh = K / 64;                                  // k = kg*4 + 64*h + i, h < nh, i < 4
+  float t[4][8];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t[c][i] = 0.f;
+  for (int j = 0; j < K; ++j) {
+    const float4 w4 = *reinterpret_cast<const float4*>(Wt + j * ST_CH + cg * 4);
+    const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h < nh) {
+        const float4 g4 = *reinterpret_cast<const float4*>(Gc + j * K + kg * 4 + 64 * h);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          t[c][4 * h + 0] = fmaf(g4.x, wv[c], t[c][4 * h + 0]);
+          t[c][4 * h + 1] = fmaf(g4.y, wv[c], t[c][4 * h + 1]);
+          t[c][4 * h + 2] = fmaf(g4.z, wv[c], t[c][4 * h + 2]);
+          t[c][4 * h + 3] = fmaf(g4.w, wv[c], t[c][4 * h + 3]);
+        }
+      }
+    }
+  }
+  double q[4], m1[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    q[c] = 0.0;
+    m1[c] = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h < nh) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int k = kg * 4 + 64 * h + i;
+          const double wk = (double)Wt[k * ST_CH + cg * 4 + c];
+          q[c] += wk * (double)t[c][4 * h + i];
+          m1[c] += wk * mu[k];
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      q[c] += __shfl_xor_sync(0xffffffffu, q[c], o);
+      m1[c] += __shfl_xor_sync(0xffffffffu, m1[c], o);
+    }
+  }
+  if (kg >= 4) return;
+  const int c_ = kg;                               // lanes kg = 0..3 write channel cg*4 + kg
+  double qq = q[0], mm = m1[0];
+#pragma unroll
+  for (int c = 1; c < 4; ++c)
+    if (c_ == c) { qq = q[c]; mm = m1[c]; }
+  const int64_t c = c0 + cg * 4 + c_;
+  if (c >= C) return;
+  double var = qq / Rd;
+  if (var < 0.0) var = 0.0;
+  const double bi = bias ? (double)bias[(int64_t)b * bias_bs + c] : 0.0;
+  const double mean = mm + bi;                     // the layer output includes its bias
+  const int64_t i = (int64_t)b * C + c;
+  smean[i] = (float)mean;
+  sinv[i] = (float)(1.0 / sqrt(var + (double)eps));
+  if (rmean) rmean[i] = (float)((1.0 - momentum) * (double)rmean[i] + momentum * mean);
+  if (rvar) rvar[i] = (float)((1.0 - momentum) * (double)rvar[i] + momentum * var * Rd / (Rd - 1.0));
+}
+size_t stats_smem(int K) { return ((size_t)K * K + (size_t)K * ST_CH) * 4; }
+
+// Per (model, channel, cloud): the pooled output from the per-cloud max of
+// Y' = s_c Y (sign-flipped), the statistics and the affine BN.
+__global__ void k_lbm_fwd_fin(int B, int Ncl, int64_t C, const float* __restrict__ mx, const int32_t* __restrict__ idx,
+                              const float* __restrict__ bias, int64_t bias_bs, const float* __restrict__ gamma,
+                              const float* __restrict__ beta, int64_t gbs, const float* __restrict__ smean,
+                              const float* __restrict__ sinv, int act, float alpha, float* __restrict__ G,
+                              int64_t g_bs, int64_t g_ld, int32_t* __restrict__ amax, int64_t am_bs, int64_t am_ld,
+                              float* __restrict__ ext, int64_t ext_bs, int64_t ext_ld) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)B * C) return;
-  const int64_t b = i / C, c = i % C;
+  if (i >= (int64_t)B * Ncl * C) return;
+  const int64_t c = i % C, n = (i / C) % Ncl, b = i / (C * Ncl);
   const float ga = gamma[b * gbs + c], be = beta[b * gbs + c];
-  const double sg = ga < 0.f ? -1.0 : 1.0;
   const float bi = bias ? bias[b * bias_bs + c] : 0.f;
-  double mean = 0.0, M2 = 0.0, cnt = 0.0;
-  const double Ld = (double)L;
-  for (int n = 0; n < Ncl; ++n) {
-    const int64_t o = (b * Ncl + n) * C + c;
-    const double t1 = s1[o], t2 = s2[o];
-    const double mn = t1 / Ld;
-    double m2 = t2 - t1 * mn;
-    if (m2 < 0.0) m2 = 0.0;
-    const double tot = cnt + Ld, d = mn - mean;
-    mean += d * Ld / tot;
-    M2 += m2 + d * d * cnt * Ld / tot;
-    cnt = tot;
-  }
-  const double R = cnt;
-  const double var = M2 / R;
-  const double mean_y = sg * mean;                 // statistics of Y (bias excluded)
-  const double inv = 1.0 / sqrt(var + (double)eps);
-  const double mean_b = mean_y + (double)bi;       // the layer output includes its bias
-  smean[i] = (float)mean_b;
-  sinv[i] = (float)inv;
-  if (rmean) rmean[i] = (float)((1.0 - momentum) * (double)rmean[i] + momentum * mean_b);
-  if (rvar) rvar[i] = (float)((1.0 - momentum) * (double)rvar[i] + momentum * var * R / (R - 1.0));
-  const float scale = (float)((double)ga * inv);
-  const float mean_f = (float)mean_y;
-  for (int n = 0; n < Ncl; ++n) {
-    const int64_t o = (b * Ncl + n) * C + c;
-    const float ey = (float)(sg * (double)mx[o]);   // Y at the argmax row (bias excluded)
-    const float z = scale * (ey - mean_f) + be;
-    G[b * g_bs + n * g_ld + c] = act_fwd(z, act, alpha);
-    amax[b * am_bs + n * am_ld + c] = idx[o];
-    ext[b * ext_bs + n * ext_ld + c] = ey + bi;
-  }
+  const float inv = sinv[b * C + c];
+  const float mean_y = smean[b * C + c] - bi;      // statistics of Y (bias excluded)
+  const float ey = ga < 0.f ? -mx[i] : mx[i];      // Y at the argmax row (bias excluded)
+  const float z = ga * inv * (ey - mean_y) + be;
+  G[b * g_bs + n * g_ld + c] = act_fwd(z, act, alpha);
+  amax[b * am_bs + n * am_ld + c] = idx[i];
+  ext[b * ext_bs + n * ext_ld + c] = ey + bi;
 }
 
 // =============================================================== backward ==
@@ -714,23 +846,31 @@ static_assert(FWD_SMEM <= 232448, "shared memory budget");
 
 size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-size_t fwd_ws(int B, int64_t N, int64_t C, int64_t K) {
-  return al256((size_t)B * C * K * 2) + 4 * al256((size_t)B * N * C * 4);
+// forward workspace: flipped W, per-cloud max / argmax, then the Gram call's own
+struct FwdWs {
+  size_t wf, mx, idx, lin, total;
+};
+FwdWs fwd_layout(int B, int64_t N, int64_t L, int64_t C, int64_t K) {
+  FwdWs w{};
+  size_t o = 0;
+  w.wf = o; o += al256((size_t)B * C * K * 2);
+  w.mx = o; o += al256((size_t)B * N * C * 4);
+  w.idx = o; o += al256((size_t)B * N * C * 4);
+  w.lin = o; o += al256(hfta_fused_linear_bwd_workspace(B, N * L, K, K, HFTA_BF16));
+  w.total = o;
+  return w;
 }
-// backward workspace: coef, sp, G, s, M, v, then hfta_fused_linear_bwd's own
+// backward workspace: coef, sp, M, v
 struct BwdWs {
-  size_t coef, sp, G, sv, M, v, lin, total;
+  size_t coef, sp, M, v, total;
 };
 BwdWs bwd_layout(int B, int64_t N, int64_t L, int64_t C, int64_t K) {
   BwdWs w{};
   size_t o = 0;
   w.coef = o; o += al256((size_t)B * C * 8);
   w.sp = o; o += al256((size_t)B * N * C * 4);
-  w.G = o; o += al256((size_t)B * K * K * 4);
-  w.sv = o; o += al256((size_t)B * K * 4);
   w.M = o; o += al256((size_t)B * K * K * 2);
   w.v = o; o += al256((size_t)B * K * 4);
-  w.lin = o; o += al256(hfta_fused_linear_bwd_workspace(B, N * L, K, K, HFTA_BF16));
   w.total = o;
   return w;
 }
@@ -770,7 +910,7 @@ extern "C" {
 
 size_t hfta_fused_linear_bn_max_workspace(int B, int64_t N, int64_t L, int64_t C, int64_t K) {
   if (B < 1 || N < 1 || L < 1 || C < 1 || K < 1) return 0;
-  return std::max(fwd_ws(B, N, C, K), bwd_ws(B, N, L, C, K));
+  return std::max(fwd_layout(B, N, L, C, K).total, bwd_ws(B, N, L, C, K));
 }
 
 hfta_status hfta_fused_linear_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C, int64_t K, hfta_dtype dt, hfta_in X,
@@ -778,51 +918,72 @@ hfta_status hfta_fused_linear_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C,
                                          const float* beta, int64_t gb_bstride, float* running_mean,
                                          float* running_var, float momentum, float eps, hfta_act act,
                                          float act_alpha, hfta_out G, int32_t* argmax, hfta_out ext,
-                                         float* save_mean, float* save_invstd, void* ws, size_t ws_bytes,
-                                         hfta_stream stream) {
+                                         float* save_mean, float* save_invstd, float* gram, float* xsum, void* ws,
+                                         size_t ws_bytes, hfta_stream stream) {
   if (hfta_status st = check_common(B, N, L, C, K, dt, X, W)) return st;
-  HFTA_REQUIRE(gamma && beta && G.ptr && argmax && ext.ptr && save_mean && save_invstd, HFTA_ERR_INVALID_VALUE,
-               "linear_bn_max_fwd: gamma, beta, G, argmax, ext, save_mean, save_invstd are required");
+  HFTA_REQUIRE(gamma && beta && G.ptr && argmax && ext.ptr && save_mean && save_invstd && gram && xsum,
+               HFTA_ERR_INVALID_VALUE,
+               "linear_bn_max_fwd: gamma, beta, G, argmax, ext, save_mean, save_invstd, gram, xsum are required");
   const size_t need = hfta_fused_linear_bn_max_workspace(B, N, L, C, K);
   HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "linear_bn_max_fwd: workspace %zu < %zu", ws_bytes, need);
   if (hfta_status st = get_encode()) return st;
   cudaStream_t s = (cudaStream_t)stream;
+  const FwdWs lay = fwd_layout(B, N, L, C, K);
   char* w = reinterpret_cast<char*>(ws);
-  __nv_bfloat16* wf = reinterpret_cast<__nv_bfloat16*>(w);
-  w += al256((size_t)B * C * K * 2);
-  const size_t pb = al256((size_t)B * N * C * 4);
-  float* s1 = reinterpret_cast<float*>(w);
-  float* s2 = reinterpret_cast<float*>(w + pb);
-  float* mx = reinterpret_cast<float*>(w + 2 * pb);
-  int32_t* idx = reinterpret_cast<int32_t*>(w + 3 * pb);
+  __nv_bfloat16* wf = reinterpret_cast<__nv_bfloat16*>(w + lay.wf);
+  float* mx = reinterpret_cast<float*>(w + lay.mx);
+  int32_t* idx = reinterpret_cast<int32_t*>(w + lay.idx);
+  const int64_t R = N * L;
 
-  const int64_t nw = (int64_t)B * C * K;
+  // 1. gram = X^T X, xsum = X^T 1 (tensor-core wgrad contraction + fused column sums); also the backward's input
+  if (hfta_status st = hfta_fused_linear_bwd(B, R, K, K, HFTA_BF16, X, X, W, hfta_out{nullptr, 0, 1}, gram, K * K, K,
+                                             xsum, K, 0, w + lay.lin, lay.total - lay.lin, stream))
+    return st;
+  // 2. W' = s_c W (sign of gamma folded in: the epilogue always takes a max)
+  const int64_t nw = (int64_t)B * C * K / 8;
   k_lbm_flip<<<(unsigned)std::min<int64_t>(cdiv(nw, 256), 148 * 16), 256, 0, s>>>(
       B, C, K, (const __nv_bfloat16*)W.ptr, W.bstride, W.ld, gamma, gb_bstride, wf);
-
+  // 3. per-cloud max / first argmax of Y' = X W'^T (tensor cores, Y' never leaves TMEM)
   CUtensorMap ta, tw;
   const int nba = (X.bstride == 0 && B > 1) ? 1 : B;
   if (hfta_status st = make_map(&ta, X.ptr, K, N * L, X.ld, X.bstride, nba, 64, FR)) return st;
   if (hfta_status st = make_map(&tw, wf, K, C, K, C * K, B, 64, CBLK)) return st;
   FwdArgs a{};
-  a.B = B; a.Ncl = (int)N; a.nblk = (int)(C / CBLK); a.ngroups = (int)cdiv(a.nblk, FG); a.nkb = (int)(K / 64);
+  a.B = B; a.Ncl = (int)N; a.nblk = (int)(C / CBLK); a.nkb = (int)(K / 64);
+  a.ngroups = (int)cdiv(a.nblk, FG);
   a.a_shared = nba == 1 && B > 1;
   a.L = L; a.C = C;
-  a.s1 = s1; a.s2 = s2; a.mx = mx; a.idx = idx;
-  {
-    const char* e = getenv("HFTA_LBM_MODE");   // diagnostics: 1 = epilogue only drains TMEM
-    a.mode = e ? atoi(e) : 0;
-  }
+  a.mx = mx; a.idx = idx;
   const int64_t npairs = (int64_t)B * N;
   a.teams = (int)std::max<int64_t>(1, std::min<int64_t>(npairs, num_sms() / a.ngroups));
-  static bool attr = false;
-  set_smem(k_lbm_fwd, FWD_SMEM, attr);
-  k_lbm_fwd<<<a.teams * a.ngroups, LT, FWD_SMEM, s>>>(ta, tw, a);
-  k_lbm_fwd_fin<<<(unsigned)cdiv((int64_t)B * C, 128), 128, 0, s>>>(
-      B, (int)N, L, C, s1, s2, mx, idx, bias, bias_bstride, gamma, beta, gb_bstride, running_mean, running_var,
-      momentum, eps, (int)act, act_alpha, (float*)G.ptr, G.bstride, G.ld, argmax, N * C, C, (float*)ext.ptr,
-      ext.bstride, ext.ld, save_mean, save_invstd);
-  count_launches(3);
+  {
+    static bool attr = false;
+    set_smem(k_lbm_fwd, FWD_SMEM, attr);
+  }
+  k_lbm_fwd<<<a.teams * a.ngroups, FWD_LT, FWD_SMEM, s>>>(ta, tw, a);
+  // 4. batch statistics from the Gram, 5. pooled outputs
+  {
+    static bool attr_st = false, attr_st64 = false;
+    set_smem(k_lbm_stats<128>, stats_smem(128), attr_st);
+    set_smem(k_lbm_stats<64>, stats_smem(64), attr_st64);
+  }
+  {
+    const dim3 grid((unsigned)cdiv(C, ST_CH), (unsigned)B);
+    const __nv_bfloat16* Wp = (const __nv_bfloat16*)W.ptr;
+    const int64_t wbs = B > 1 ? W.bstride : 0;
+    if (K == 128)
+      k_lbm_stats<128><<<grid, 256, stats_smem(128), s>>>(B, R, C, gram, xsum, Wp, wbs, W.ld, bias, bias_bstride,
+                                                          running_mean, running_var, momentum, eps, save_mean,
+                                                          save_invstd);
+    else
+      k_lbm_stats<64><<<grid, 256, stats_smem(64), s>>>(B, R, C, gram, xsum, Wp, wbs, W.ld, bias, bias_bstride,
+                                                        running_mean, running_var, momentum, eps, save_mean,
+                                                        save_invstd);
+  }
+  k_lbm_fwd_fin<<<(unsigned)cdiv((int64_t)B * N * C, 256), 256, 0, s>>>(
+      B, (int)N, C, mx, idx, bias, bias_bstride, gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha,
+      (float*)G.ptr, G.bstride, G.ld, argmax, N * C, C, (float*)ext.ptr, ext.bstride, ext.ld);
+  count_launches(4);
   return post_launch(s, "hfta_fused_linear_bn_max_fwd");
 }
 
@@ -830,15 +991,17 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
                                          hfta_in dG, hfta_in X, hfta_in W, const int32_t* argmax, hfta_in ext,
                                          const float* bias, int64_t bias_bstride, const float* gamma,
                                          const float* beta, int64_t gb_bstride, const float* save_mean,
-                                         const float* save_invstd, hfta_act act, float act_alpha, hfta_out dX,
+                                         const float* save_invstd, const float* gram, const float* xsum,
+                                         hfta_act act, float act_alpha, hfta_out dX,
                                          hfta_act dX_act, float dX_alpha, float* dW, int64_t dW_bstride,
                                          int64_t dW_ld, float* dbias, int64_t dbias_bstride, float* dgamma,
                                          float* dbeta, int accumulate, void* ws, size_t ws_bytes,
                                          hfta_stream stream) {
   if (hfta_status st = check_common(B, N, L, C, K, dt, X, W)) return st;
-  HFTA_REQUIRE(dG.ptr && argmax && ext.ptr && gamma && beta && save_mean && save_invstd && dW && dgamma && dbeta,
+  HFTA_REQUIRE(dG.ptr && argmax && ext.ptr && gamma && beta && save_mean && save_invstd && gram && xsum && dW &&
+                   dgamma && dbeta,
                HFTA_ERR_INVALID_VALUE,
-               "linear_bn_max_bwd: dG, argmax, ext, gamma, beta, save_*, dW, dgamma, dbeta are required");
+               "linear_bn_max_bwd: dG, argmax, ext, gamma, beta, save_*, gram, xsum, dW, dgamma, dbeta are required");
   HFTA_REQUIRE(!dX.ptr || (aligned16(dX.ptr) && (dX.ld * 2) % 16 == 0 && (dX.bstride * 2) % 16 == 0 && dX.ld >= K),
                HFTA_ERR_UNSUPPORTED, "linear_bn_max_bwd: dX must be 16-B aligned with 16-B row strides");
   HFTA_REQUIRE(C <= SDX_T * SDX_ITEMS, HFTA_ERR_UNSUPPORTED, "linear_bn_max_bwd: C=%lld > %d", (long long)C,
@@ -852,8 +1015,6 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
   char* w = reinterpret_cast<char*>(ws);
   float2* coef = reinterpret_cast<float2*>(w + lay.coef);
   float* sp = reinterpret_cast<float*>(w + lay.sp);
-  float* G = reinterpret_cast<float*>(w + lay.G);
-  float* sv = reinterpret_cast<float*>(w + lay.sv);
   __nv_bfloat16* M = reinterpret_cast<__nv_bfloat16*>(w + lay.M);
   float* v = reinterpret_cast<float*>(w + lay.v);
   const __nv_bfloat16* Wp = (const __nv_bfloat16*)W.ptr;
@@ -863,11 +1024,7 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
       B, (int)N, L, C, (const float*)dG.ptr, dG.bstride, dG.ld, (const float*)ext.ptr, ext.bstride, ext.ld, bias,
       bias_bstride, gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, coef, sp, dgamma, dbeta,
       dbias, dbias_bstride, accumulate);
-  // G = X^T X, s = X^T 1 (tensor-core wgrad contraction + column sums over the R points)
-  if (hfta_status st = hfta_fused_linear_bwd(B, R, K, K, HFTA_BF16, X, X, W, hfta_out{nullptr, 0, 1}, G, K * K, K,
-                                             sv, K, 0, w + lay.lin, lay.total - lay.lin, stream))
-    return st;
-  int launches = 2;
+  int launches = 2;   // coef, dw
   if (dX.ptr) {
     k_lbm_mv<<<dim3((unsigned)cdiv(K, MV_ROWS), (unsigned)B), 256, 0, s>>>(C, (int)K, Wp, wbs, W.ld, coef, M, v);
     // dX = X M^T + v (M symmetric), times act'(X) when X is an activation output
@@ -894,10 +1051,16 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
     set_smem(k_lbm_dw, (size_t)128 * 128 * 4, attr);   // K <= 128
   }
   k_lbm_dw<<<dim3((unsigned)cdiv(C, 32), (unsigned)B), 256, (size_t)K * K * 4, s>>>(
-      (int)N, L, C, (int)K, G, sv, Wp, wbs, W.ld, coef, argmax, sp, (const __nv_bfloat16*)X.ptr, X.bstride, X.ld, dW,
+      (int)N, L, C, (int)K, gram, xsum, Wp, wbs, W.ld, coef, argmax, sp, (const __nv_bfloat16*)X.ptr, X.bstride, X.ld, dW,
       dW_bstride, dW_ld, accumulate);
   count_launches(launches);
   return post_launch(s, "hfta_fused_linear_bn_max_bwd");
 }
 
 }  // extern "C"
+
+#ifdef HFTA_LBM_PROF
+extern "C" __attribute__((visibility("default"))) int hfta_lbm_prof_dump(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, hfta::g_lbm_prof, sizeof(unsigned long long) * 8 * (size_t)n);
+}
+#endif

@@ -67,10 +67,11 @@ _SIGS = {
                               vp, vp, vp, sz, vp]),
     "hfta_fused_linear_bn_max_workspace": (sz, [i32, i64, i64, i64, i64]),
     "hfta_fused_linear_bn_max_fwd": (i32, [i32, i64, i64, i64, i64, i32, hfta_in, hfta_in, vp, i64, vp, vp, i64, vp,
-                                           vp, f32, f32, i32, f32, hfta_out, vp, hfta_out, vp, vp, vp, sz, vp]),
+                                           vp, f32, f32, i32, f32, hfta_out, vp, hfta_out, vp, vp, vp, vp, vp, sz,
+                                           vp]),
     "hfta_fused_linear_bn_max_bwd": (i32, [i32, i64, i64, i64, i64, i32, hfta_in, hfta_in, hfta_in, vp, hfta_in, vp,
-                                           i64, vp, vp, i64, vp, vp, i32, f32, hfta_out, i32, f32, vp, i64, i64, vp,
-                                           i64, vp, vp, i32, vp, sz, vp]),
+                                           i64, vp, vp, i64, vp, vp, vp, vp, i32, f32, hfta_out, i32, f32, vp, i64,
+                                           i64, vp, i64, vp, vp, i32, vp, sz, vp]),
     "hfta_fused_linear_bn_workspace": (sz, [i32, i64, i64, i64]),
     "hfta_fused_linear_bn_fwd": (i32, [i32, i64, i64, i64, i32, hfta_in, hfta_in, vp, i64, vp, vp, i64, vp, vp, f32,
                                        f32, i32, f32, hfta_out, vp, vp, vp, vp, vp, sz, vp]),

@@ -68,6 +68,7 @@ class FusedPointNet(FusedNet):
                 S[p + ".y2"], S[p + ".a2"] = a(R, c2), a(R, c2)
             if self.fuse_lbm:
                 S[p + ".ext"] = f(N, c3)            # Y at the argmax rows (the block's saved tensor)
+                S[p + ".G3"], S[p + ".s3"] = f(c2, c2), f(1, c2)     # Gram / column sums of the c3 input
             else:
                 S[p + ".y3"] = a(R, c3)
             S[p + ".g"] = f(N, c3)
@@ -179,7 +180,8 @@ class FusedPointNet(FusedNet):
                                        ar.w_in(p + ".c3.W", self.dt), ar.fptr("p", p + ".c3.b"), P,
                                        ar.fptr("p", bn + ".g"), ar.fptr("p", bn + ".beta"), P, H.ptr(rm), H.ptr(rv),
                                        0.1, 1e-5, act, self.act_alpha, _out(S[p + ".g"]), H.ptr(S[p + ".amax"]),
-                                       _out(S[p + ".ext"]), H.ptr(sm), H.ptr(si), self.ws.ptr, self.ws.nbytes, s)
+                                       _out(S[p + ".ext"]), H.ptr(sm), H.ptr(si), H.ptr(S[p + ".G3"]),
+                                       H.ptr(S[p + ".s3"]), self.ws.ptr, self.ws.nbytes, s)
         self._pend(e0)
 
     def _block_bwd(self, p, act, s, dx_act=A_NONE):
@@ -196,7 +198,8 @@ class FusedPointNet(FusedNet):
         H.hfta_fused_linear_bn_max_bwd(self.B, self.N, self.L, self.c3, self.c2, self.dt, _in(S["d.g"]),
                                        _in(S[p + ".a2"]), ar.w_in(p + ".c3.W", self.dt), H.ptr(S[p + ".amax"]),
                                        _in(S[p + ".ext"]), ar.fptr("p", p + ".c3.b"), P, ar.fptr("p", bn + ".g"),
-                                       ar.fptr("p", bn + ".beta"), P, H.ptr(sm), H.ptr(si), act, self.act_alpha,
+                                       ar.fptr("p", bn + ".beta"), P, H.ptr(sm), H.ptr(si), H.ptr(S[p + ".G3"]),
+                                       H.ptr(S[p + ".s3"]), act, self.act_alpha,
                                        _out(S["d.c2a"]), dx_act, self.act_alpha, ar.fptr("g", p + ".c3.W"), P, self.c2,
                                        ar.fptr("g", p + ".c3.b"), P, ar.fptr("g", bn + ".g"), ar.fptr("g", bn + ".beta"),
                                        0, self.ws.ptr, self.ws.nbytes, s)

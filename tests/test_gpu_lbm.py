@@ -70,11 +70,13 @@ def run_block(B, N, L, C, K, act, shared=False, seed=0, accumulate=0, neg_gamma=
     ext = torch.empty(B, N, C, device=DEV)
     am = torch.empty(B, N, C, dtype=torch.int32, device=DEV)
     sm, si = torch.empty(B, C, device=DEV), torch.empty(B, C, device=DEV)
+    gram, xsum = torch.empty(B, K, K, device=DEV), torch.empty(B, K, device=DEV)
     ws = torch.empty(H.hfta_fused_linear_bn_max_workspace(B, N, L, C, K), dtype=torch.uint8, device=DEV)
     xbs = 0 if shared else R * K
     H.hfta_fused_linear_bn_max_fwd(B, N, L, C, K, 1, H.tin(Xd, xbs, K), H.tin(Wd, C * K, K), H.ptr(bd), C, H.ptr(gd),
                                    H.ptr(bed), C, H.ptr(rm), H.ptr(rv), 0.1, 1e-5, act, 0.0, H.tout(G, N * C, C),
-                                   H.ptr(am), H.tout(ext, N * C, C), H.ptr(sm), H.ptr(si), H.ptr(ws), ws.numel(), s())
+                                   H.ptr(am), H.tout(ext, N * C, C), H.ptr(sm), H.ptr(si), H.ptr(gram), H.ptr(xsum),
+                                   H.ptr(ws), ws.numel(), s())
     dX = torch.empty(B, R, K, dtype=torch.bfloat16, device=DEV)
     dW = dev(dW0) if accumulate else torch.empty(B, C, K, device=DEV)
     dgam = dev(dg0) if accumulate else torch.empty(B, C, device=DEV)
@@ -82,11 +84,12 @@ def run_block(B, N, L, C, K, act, shared=False, seed=0, accumulate=0, neg_gamma=
     dbias = torch.full((B, C), 7.0, device=DEV)
     H.hfta_fused_linear_bn_max_bwd(B, N, L, C, K, 1, H.tin(dGd, N * C, C), H.tin(Xd, xbs, K), H.tin(Wd, C * K, K),
                                    H.ptr(am), H.tin(ext, N * C, C), H.ptr(bd), C, H.ptr(gd), H.ptr(bed), C, H.ptr(sm),
-                                   H.ptr(si), act, 0.0, H.tout(dX, R * K, K), dx_act, 0.0, H.ptr(dW), C * K, K, H.ptr(dbias), C,
+                                   H.ptr(si), H.ptr(gram), H.ptr(xsum), act, 0.0, H.tout(dX, R * K, K), dx_act, 0.0, H.ptr(dW), C * K, K, H.ptr(dbias), C,
                                    H.ptr(dgam), H.ptr(dbet), accumulate, H.ptr(ws), ws.numel(), s())
     torch.cuda.synchronize()
     out = dict(G=host(G), ext=host(ext), am=am.cpu().numpy().astype(np.int64), sm=host(sm), si=host(si),
-               rm=host(rm), rv=host(rv), dX=host(dX), dW=host(dW), dg=host(dgam), db=host(dbet), dbias=host(dbias))
+               rm=host(rm), rv=host(rv), gram=host(gram), xsum=host(xsum), dX=host(dX), dW=host(dW), dg=host(dgam),
+               db=host(dbet), dbias=host(dbias))
     inp = dict(X=X, W=W, bias=bias, g=g, be=be, rm0=rm0, rv0=rv0, dG=dG, dW0=dW0, dg0=dg0)
     return out, inp
 
@@ -123,6 +126,10 @@ CASES = [  # B, N, L, C, K, act, shared
     (3, 40, 5, 128, 64, 1, True),        # tiny clouds: one tile spans many; shared input; K = 64
     (1, 1, 100, 128, 128, 0, False),     # a single partial chunk; unsplit wgrad
     (4, 8, 333, 384, 128, 1, False),
+    (2, 3, 700, 512, 128, 1, False),
+    (2, 2, 1000, 1024, 128, 0, False),
+    (3, 40, 5, 512, 64, 1, True),
+    (1, 1, 100, 1024, 128, 1, False),
 ]
 
 
@@ -140,6 +147,9 @@ def test_linear_bn_max(B, N, L, C, K, act, shared):
         assert_close(out["G"][b], o["G"], 1e-5, "G")
         ext_ref = np.take_along_axis(o["y"].reshape(N, L, -1), out["am"][b][:, None, :], axis=1)[:, 0, :]
         assert_close(out["ext"][b], ext_ref, 1e-5, "ext")
+        Xb = inp["X"][0 if shared else b]
+        assert_close(out["gram"][b], Xb.T @ Xb, 1e-5, "gram = X^T X")
+        assert_close(out["xsum"][b], Xb.sum(0), 1e-5, "xsum = X^T 1")
         assert_close(out["sm"][b], o["mean"], 1e-5, "save_mean")
         assert_close(out["si"][b], o["invstd"], 1e-5, "save_invstd")
         assert_close(out["rm"][b], o["rm"], 1e-5, "running_mean")
@@ -175,10 +185,10 @@ def test_linear_bn_max_errors():
     with pytest.raises(H.HftaError) as e:      # K must be 64 or 128
         H.hfta_fused_linear_bn_max_fwd(1, 1, 64, 128, 96, 1, H.tin(x, 0, 96), H.tin(x, 0, 96), None, 0, None, None,
                                        0, None, None, 0.1, 1e-5, 0, 0.0, H.tout(x, 0, 1), None, H.tout(x, 0, 1), None,
-                                       None, None, 0, s())
+                                       None, None, None, None, 0, s())
     assert e.value.code == 4
     with pytest.raises(H.HftaError) as e:      # fp32 operands are not this path
         H.hfta_fused_linear_bn_max_fwd(1, 1, 64, 128, 64, 0, H.tin(x, 0, 64), H.tin(x, 0, 64), None, 0, None, None,
                                        0, None, None, 0.1, 1e-5, 0, 0.0, H.tout(x, 0, 1), None, H.tout(x, 0, 1), None,
-                                       None, None, 0, s())
+                                       None, None, None, None, 0, s())
     assert e.value.code == 4

@@ -28,6 +28,7 @@ sm, si = torch.empty(B, C, device=dev), torch.empty(B, C, device=dev)
 ws = torch.empty(H.hfta_fused_linear_bn_max_workspace(B, N, L, C, K), dtype=torch.uint8, device=dev)
 dG = torch.randn(B, N, C, device=dev)
 dX = torch.empty(B, R, K, dtype=torch.bfloat16, device=dev)
+gram, xsum = torch.empty(B, K, K, device=dev), torch.empty(B, K, device=dev)
 dW = torch.empty(B, C, K, device=dev)
 dg, db, dbias = torch.empty(B, C, device=dev), torch.empty(B, C, device=dev), torch.empty(B, C, device=dev)
 
@@ -35,13 +36,14 @@ dg, db, dbias = torch.empty(B, C, device=dev), torch.empty(B, C, device=dev), to
 def fwd():
     H.hfta_fused_linear_bn_max_fwd(B, N, L, C, K, 1, H.tin(X, R * K, K), H.tin(W, C * K, K), H.ptr(bias), C, H.ptr(g),
                                    H.ptr(be), C, H.ptr(rm), H.ptr(rv), 0.1, 1e-5, 1, 0.0, H.tout(G, N * C, C),
-                                   H.ptr(am), H.tout(ext, N * C, C), H.ptr(sm), H.ptr(si), H.ptr(ws), ws.numel(), s)
+                                   H.ptr(am), H.tout(ext, N * C, C), H.ptr(sm), H.ptr(si), H.ptr(gram), H.ptr(xsum), H.ptr(ws),
+                                   ws.numel(), s)
 
 
 def bwd():
     H.hfta_fused_linear_bn_max_bwd(B, N, L, C, K, 1, H.tin(dG, N * C, C), H.tin(X, R * K, K), H.tin(W, C * K, K),
                                    H.ptr(am), H.tin(ext, N * C, C), H.ptr(bias), C, H.ptr(g), H.ptr(be), C, H.ptr(sm),
-                                   H.ptr(si), 1, 0.0, H.tout(dX, R * K, K), 1, 0.0, H.ptr(dW), C * K, K, H.ptr(dbias), C,
+                                   H.ptr(si), H.ptr(gram), H.ptr(xsum), 1, 0.0, H.tout(dX, R * K, K), 1, 0.0, H.ptr(dW), C * K, K, H.ptr(dbias), C,
                                    H.ptr(dg), H.ptr(db), 0, H.ptr(ws), ws.numel(), s)
 
 
