@@ -143,17 +143,18 @@ class FusedPointNet(FusedNet):
     # -------------------------------------------------------------- step --
     def probe_roofline(self, name, ms, peaks, path="simt"):
         """Roofline of the fused c3 block (K10): algorithmic flops = the
-        block's contractions (fwd: Y = X W^T; bwd: dgrad + wgrad -- the
-        recompute of Y is NOT counted), algorithmic bytes = X, W and the
-        per-sample tensors once (+ dX, dW for bwd).  Arithmetic intensity ~C
-        flop/B >> the ridge: tensor-bound against the measured bf16 peak."""
+        block's contractions (fwd: Y = X W^T and the Gram X^T X its
+        statistics come from; bwd: dgrad + wgrad in Gram form counted as the
+        dense dgrad + wgrad), algorithmic bytes = X, W and the per-sample
+        tensors once (+ dX, dW for bwd).  Arithmetic intensity ~C flop/B >>
+        the ridge: tensor-bound against the measured bf16 peak."""
         layer, kind = name.split(":")
         if not (self.fuse_lbm and layer.endswith(".c3")):
             return super().probe_roofline(name, ms, peaks, path)
         B, R, C, K, N = self.B, self.R, self.c3, self.c2, self.N
         if kind == "fwd":
-            flops = 2.0 * B * R * C * K
-            nbytes = B * (R * K * 2 + C * K * 2 + N * C * 12 + C * 16)
+            flops = 2.0 * B * R * C * K + 2.0 * B * R * K * K
+            nbytes = B * (R * K * 2 + C * K * 2 + N * C * 12 + C * 16 + K * K * 4)
         else:
             flops = 2.0 * 2.0 * B * R * C * K
             nbytes = B * (2 * R * K * 2 + C * K * 2 + C * K * 4 + N * C * 12 + C * 16)
