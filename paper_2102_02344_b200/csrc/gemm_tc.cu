@@ -25,8 +25,12 @@ namespace {
 
 constexpr int BM = 128;     // UMMA M (one CTA, cta_group::1)
 constexpr int BK = 64;      // k per stage: 64 bf16 = 128 B = one swizzle row
-constexpr int NTHREADS = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quarter)
-constexpr int NEPI = 8;
+// warp 0 TMA, warp 1 MMA, warps 2..17 epilogue: two groups of 8 (2 per TMEM lane
+// quarter) that take alternate tiles, so each group has two tiles' time for its
+// (latency-bound) epilogue while the tensor core and TMA stream
+constexpr int NTHREADS = 576;
+constexpr int NEPI = 8;           // epilogue warps per group (= arrivals per tile)
+constexpr int NEPI_ALL = 16;
 
 struct TcArgs {
   int B, splits, order;            // order 0: n fastest, 1: m fastest
@@ -91,11 +95,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* bfull = tempty + 2;
   uint64_t* bempty = bfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 1);
-  // per-epilogue-warp staging for the TMA store: 2 buffers x 32 rows x 64 B
-  uint8_t* stage_out = bres + BRES_BYTES + 1024;                   // NEPI warps x 2 x 4 KB
-  constexpr uint32_t STG_BYTES = OUT_F32 ? 0 : NEPI * 2 * 4096;              // bf16 TMA-store staging
-  float* sbias_all = reinterpret_cast<float*>(stage_out + STG_BYTES);         // NEPI warps x BN floats
-  float* sscale_all = sbias_all + NEPI * BN;                                   // EPI: NEPI warps x BN floats
+  // per-epilogue-warp staging for the TMA store: 32 rows x 128 B
+  uint8_t* stage_out = bres + BRES_BYTES + 1024;                   // NEPI_ALL warps x 4 KB
+  constexpr uint32_t STG_BYTES = OUT_F32 ? 0 : NEPI_ALL * 4096;              // bf16 TMA-store staging
+  float* sbias_all = reinterpret_cast<float*>(stage_out + STG_BYTES);         // NEPI_ALL warps x BN floats
+  float* sscale_all = sbias_all + NEPI_ALL * BN;                               // EPI: NEPI_ALL warps x BN floats
 
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -255,24 +259,36 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     }
   } else {
     // ============================== epilogue ==============================
+    const int ew = warp - 2;                      // 0 .. NEPI_ALL-1
+    const int grp = ew / NEPI;                    // this warp's group takes tiles of local parity grp
     const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
-    const int half = (warp - 2) >> 2;             // two warps per quarter split the 64-column steps
-    const uint32_t sbias = smem_u32(sbias_all + (warp - 2) * BN);
-    const uint32_t sscale = smem_u32(sscale_all + (warp - 2) * BN);
+    const int half = (ew % NEPI) >> 2;            // two warps per quarter split the 64-column steps
+    const uint32_t sbias = smem_u32(sbias_all + ew * BN);
+    const uint32_t sscale = smem_u32(sscale_all + ew * BN);
     constexpr int NSTEP = BN / 64;
     const int my_steps = (NSTEP - half + 1) / 2;
-    uint32_t sbuf = 0;
-    int acc = 0;
+    const int acc = grp;                          // local tile parity = accumulator buffer
     uint32_t acc_phase = 0;
     int64_t cur_key = -1;
     int estage = 0;                               // stage counter mirrored from the producer (mask_kb >= 0)
-    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const bool mask_smem = EPI == 2 && p.mask_kb >= 0;
+    int64_t li = 0;                               // local tile ordinal
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++li) {
       int64_t r = t;
       int mt, nt;
       if (p.order == 0) { nt = (int)(r % p.tiles_n); r /= p.tiles_n; mt = (int)(r % p.tiles_m); r /= p.tiles_m; }
       else { mt = (int)(r % p.tiles_m); r /= p.tiles_m; nt = (int)(r % p.tiles_n); r /= p.tiles_n; }
       const int split = (int)(r % p.splits);
       const int b = (int)(r / p.splits);
+      int tile_nkb = 0;
+      if (mask_smem) {
+        const int64_t kbeg_ = (int64_t)split * p.k_chunk, kend_ = min(p.K, kbeg_ + p.k_chunk);
+        tile_nkb = (int)((kend_ - kbeg_ + BK - 1) / BK) + (int)((p.K2 + BK - 1) / BK);
+      }
+      if ((int)(li & 1) != grp) {                 // the other group's tile
+        if (mask_smem) estage = (estage + tile_nkb) % STAGES;
+        continue;
+      }
       const int64_t m = (int64_t)mt * BM + quarter * 32 + lane;
       const bool row_ok = m < p.M;
       // per-(model, n-tile) bias / scale slices: reloaded only when the key
@@ -319,13 +335,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
         }
       }
-      const bool mask_smem = EPI == 2 && p.mask_kb >= 0;
       bool released = false;
-      int tile_nkb = 0;
-      if (mask_smem) {
-        const int64_t kbeg_ = (int64_t)split * p.k_chunk, kend_ = min(p.K, kbeg_ + p.k_chunk);
-        tile_nkb = (int)((kend_ - kbeg_ + BK - 1) / BK) + (int)((p.K2 + BK - 1) / BK);
-      }
       if (my_steps == 0) {               // nothing for this warp in this tile: release at once
         tc_fence_before();
         __syncwarp();
@@ -333,98 +343,98 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
 #pragma unroll 1
       for (int si = 0; si < my_steps; ++si) {
-        const int j = half + 2 * si;     // 64-column step
-        uint32_t u[64];
-        const uint32_t ta = tmem_base + (uint32_t)(acc * ABUF + j * 64) + ((uint32_t)(quarter * 32) << 16);
-        tmem_ld32_nowait(ta, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
-        tmem_ld32_nowait(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
-        tmem_wait_ld();
-        if (si == my_steps - 1) {        // this warp's last step of the tile: release the accumulator
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
+        const int j = half + 2 * si;     // 64-column step, processed as two 32-column halves
         const int64_t n0 = (int64_t)nt * BN + j * 64;
-        if (n0 >= p.N) continue;                       // warp-uniform
-        float v[64];
-#pragma unroll
-        for (int q = 0; q < 64; ++q) v[q] = __uint_as_float(u[q]);
-        if constexpr (EPI == 1) {            // fused BN apply: v = act(v * scale + shift)
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float4 s4 = ld_shared_f4(sscale + (j * 64 + 4 * q) * 4);
-            const float4 t4 = ld_shared_f4(sbias + (j * 64 + 4 * q) * 4);
-            v[4 * q] = fmaf(v[4 * q], s4.x, t4.x); v[4 * q + 1] = fmaf(v[4 * q + 1], s4.y, t4.y);
-            v[4 * q + 2] = fmaf(v[4 * q + 2], s4.z, t4.z); v[4 * q + 3] = fmaf(v[4 * q + 3], s4.w, t4.w);
-          }
-          if (p.act == HFTA_ACT_RELU) {
-#pragma unroll
-            for (int q = 0; q < 64; ++q) v[q] = fmaxf(v[q], 0.f);
-          } else if (p.act == HFTA_ACT_LEAKY_RELU) {
-#pragma unroll
-            for (int q = 0; q < 64; ++q) v[q] = v[q] > 0.f ? v[q] : p.act_alpha * v[q];
-          }
-        } else {
-          if (vbias) {
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {             // smem broadcast
-              const float4 t4 = ld_shared_f4(sbias + (j * 64 + 4 * q) * 4);
-              v[4 * q] += t4.x; v[4 * q + 1] += t4.y; v[4 * q + 2] += t4.z; v[4 * q + 3] += t4.w;
-            }
-          } else if (brow) {
-#pragma unroll
-            for (int q = 0; q < 64; ++q)
-              if (n0 + q < p.N) v[q] += brow[n0 + q];
-          }
+        const bool last = si == my_steps - 1;
+        uint8_t* buf = stage_out + ew * 4096;  // bf16 staging: this warp's 32 x 64 sub-tile
+        const uint32_t rowaddr = smem_u32(buf) + lane * 128;
+        const uint32_t sw = (uint32_t)(lane & 7);
+        if (!OUT_F32 && n0 < p.N) {      // the previous store of this warp (a tile ago) has read its staging
+          if (lane == 0) tma_store_wait_read<0>();
+          __syncwarp();
         }
-        if (EPI == 2 && mask_smem) {         // gating values = this tile's A operand, still resident in smem
-          const int st = (estage + p.mask_kb + j) % STAGES;
-          const uint32_t arow = smem_u32(smem + st * STAGE_BYTES) + (uint32_t)((quarter * 32 + lane) * 128);
-          const uint32_t swz = (uint32_t)(lane & 7);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const uint4 raw = ld_shared_u4(arow + (((uint32_t)q ^ swz) << 4));
-            const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {      // bf16 > 0 <=> sign bit clear and nonzero (ReLU')
-              v[8 * q + 2 * e] = (int32_t)(w4[e] << 16) > 0 ? v[8 * q + 2 * e] : 0.f;
-              v[8 * q + 2 * e + 1] = (int32_t)(w4[e] & 0xffff0000u) > 0 ? v[8 * q + 2 * e + 1] : 0.f;
-            }
-          }
-          if (si == my_steps - 1) {          // last read of this tile's A stages by this warp: release them
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t u[32];
+          const uint32_t ta = tmem_base + (uint32_t)(acc * ABUF + j * 64 + hh * 32) + ((uint32_t)(quarter * 32) << 16);
+          tmem_ld32_nowait(ta, u);
+          tmem_wait_ld();
+          if (last && hh == 1) {         // this warp's last TMEM read of the tile: release the accumulator
+            tc_fence_before();
             __syncwarp();
-            if (lane == 0)
-              for (int k = 0; k < tile_nkb; ++k) mbar_arrive(&empty[(estage + k) % STAGES]);
-            released = true;
+            if (lane == 0) mbar_arrive(&tempty[acc]);
           }
-        }
-        if constexpr (!OUT_F32) {
-          // bf16: stage the warp's 32 x 64 sub-tile (128-B rows, TMA SWIZZLE_128B layout:
-          // 16-B chunk q of row r at chunk q ^ (r & 7) -> conflict-free), one TMA store per
-          // step (rows >= M and columns >= N are clipped by the tensor map).
-          uint8_t* buf = stage_out + ((warp - 2) * 2 + (sbuf & 1)) * 4096;
-          if (lane == 0) tma_store_wait_read<1>();
-          __syncwarp();
-          const uint32_t rowaddr = smem_u32(buf) + lane * 128;
-          const uint32_t sw = (uint32_t)(lane & 7);
+          if (n0 >= p.N) continue;                       // warp-uniform
+          const int64_t c0 = n0 + hh * 32;
+          float v[32];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            uint4 w4;
-            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w4);
+          for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(u[q]);
+          if constexpr (EPI == 1) {            // fused BN apply: v = act(v * scale + shift)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
-            st_shared_v4(rowaddr + (((uint32_t)q ^ sw) << 4), w4);
+            for (int q = 0; q < 8; ++q) {
+              const float4 s4 = ld_shared_f4(sscale + (j * 64 + hh * 32 + 4 * q) * 4);
+              const float4 t4 = ld_shared_f4(sbias + (j * 64 + hh * 32 + 4 * q) * 4);
+              v[4 * q] = fmaf(v[4 * q], s4.x, t4.x); v[4 * q + 1] = fmaf(v[4 * q + 1], s4.y, t4.y);
+              v[4 * q + 2] = fmaf(v[4 * q + 2], s4.z, t4.z); v[4 * q + 3] = fmaf(v[4 * q + 3], s4.w, t4.w);
+            }
+            if (p.act == HFTA_ACT_RELU) {
+#pragma unroll
+              for (int q = 0; q < 32; ++q) v[q] = fmaxf(v[q], 0.f);
+            } else if (p.act == HFTA_ACT_LEAKY_RELU) {
+#pragma unroll
+              for (int q = 0; q < 32; ++q) v[q] = v[q] > 0.f ? v[q] : p.act_alpha * v[q];
+            }
+          } else {
+            if (vbias) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {             // smem broadcast
+                const float4 t4 = ld_shared_f4(sbias + (j * 64 + hh * 32 + 4 * q) * 4);
+                v[4 * q] += t4.x; v[4 * q + 1] += t4.y; v[4 * q + 2] += t4.z; v[4 * q + 3] += t4.w;
+              }
+            } else if (brow) {
+#pragma unroll
+              for (int q = 0; q < 32; ++q)
+                if (c0 + q < p.N) v[q] += brow[c0 + q];
+            }
           }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) tma_store_3d(&tmC, buf, (int)n0, (int)(mt * BM + quarter * 32), b);
-          ++sbuf;
-        } else {
-          if (!row_ok) continue;
+          if (EPI == 2 && mask_smem) {         // gating values = this tile's A operand, still resident in smem
+            const int st = (estage + p.mask_kb + j) % STAGES;
+            const uint32_t arow = smem_u32(smem + st * STAGE_BYTES) + (uint32_t)((quarter * 32 + lane) * 128);
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int64_t c0 = n0 + hh * 32;
-            if (c0 >= p.N) break;
+            for (int q = 0; q < 4; ++q) {
+              const uint4 raw = ld_shared_u4(arow + (((uint32_t)(hh * 4 + q) ^ sw) << 4));
+              const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {      // bf16 > 0 <=> sign bit clear and nonzero (ReLU')
+                v[8 * q + 2 * e] = (int32_t)(w4[e] << 16) > 0 ? v[8 * q + 2 * e] : 0.f;
+                v[8 * q + 2 * e + 1] = (int32_t)(w4[e] & 0xffff0000u) > 0 ? v[8 * q + 2 * e + 1] : 0.f;
+              }
+            }
+            if (last && hh == 1) {             // last read of this tile's A stages by this warp: release them
+              __syncwarp();
+              if (lane == 0)
+                for (int k = 0; k < tile_nkb; ++k) mbar_arrive(&empty[(estage + k) % STAGES]);
+              released = true;
+            }
+          }
+          if constexpr (!OUT_F32) {
+            // bf16: 16-B chunk q of row r at chunk q ^ (r & 7) (TMA SWIZZLE_128B layout, conflict-free);
+            // rows >= M and columns >= N are clipped by the tensor map
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 w4;
+              __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+              st_shared_v4(rowaddr + (((uint32_t)(hh * 4 + q) ^ sw) << 4), w4);
+            }
+            if (hh == 1) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) tma_store_3d(&tmC, buf, (int)n0, (int)(mt * BM + quarter * 32), b);
+            }
+          } else {
+            if (!row_ok || c0 >= p.N) continue;
             const bool full_chunk = c0 + 32 <= p.N;
             float* dst = p.splits > 1 ? p.part + (((int64_t)split * p.B + b) * p.M + m) * p.N + c0
                                       : reinterpret_cast<float*>(p.C) + (int64_t)b * p.c_bs + m * p.c_ld + c0;
@@ -432,16 +442,15 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             if (p.splits == 1 && p.accumulate) {
 #pragma unroll
               for (int q = 0; q < 32; ++q)
-                if (c0 + q < p.N) dst[q] += v[hh * 32 + q];
+                if (c0 + q < p.N) dst[q] += v[q];
             } else if (vec_ok) {
 #pragma unroll
               for (int q = 0; q < 8; ++q)
-                *reinterpret_cast<float4*>(dst + 4 * q) =
-                    make_float4(v[hh * 32 + 4 * q], v[hh * 32 + 4 * q + 1], v[hh * 32 + 4 * q + 2], v[hh * 32 + 4 * q + 3]);
+                *reinterpret_cast<float4*>(dst + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
             } else {
 #pragma unroll
               for (int q = 0; q < 32; ++q)
-                if (c0 + q < p.N) dst[q] = v[hh * 32 + q];
+                if (c0 + q < p.N) dst[q] = v[q];
             }
           }
         }
@@ -454,7 +463,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         estage = (estage + tile_nkb) % STAGES;
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      acc_phase ^= 1;
     }
   }
   if (warp >= 2 && lane == 0) tma_store_wait_read<0>();
@@ -470,10 +479,12 @@ template <bool A_MN, bool B_MN, int BN, bool OUT_F32, bool BRES, int EPI = 0>
 hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   // EPI non-BRES BN=64 (the two-segment gated dgrad): 6 stages so a tile's 3
   // k-blocks can stay resident for the epilogue while the next tile loads
-  constexpr int STAGES = BRES ? 4 : ((BN == 256) ? 3 : ((EPI == 2 && BN == 64) ? 6 : 4));
+  // B-resident (K <= 128, HBM-bound streaming of A): 7 stages keep ~112 KB of A
+  // in flight per SM (latency x per-SM share of HBM bandwidth)
+  constexpr int STAGES = BRES ? (BN <= 128 ? 7 : 4) : ((BN == 256) ? 3 : ((EPI == 2 && BN == 64) ? 6 : 4));
   constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + (BRES ? 0 : BN * BK * 2)) +
-                          (BRES ? 2 * BN * BK * 2 : 0) + 1024 + (OUT_F32 ? 0 : NEPI * 2 * 4096) +
-                          NEPI * BN * 4 * (EPI == 1 ? 2 : 1) +
+                          (BRES ? 2 * BN * BK * 2 : 0) + 1024 + (OUT_F32 ? 0 : NEPI_ALL * 4096) +
+                          NEPI_ALL * BN * 4 * (EPI == 1 ? 2 : 1) +
                           ((A_MN && B_MN && OUT_F32) ? (size_t)STAGES * 8192 : 0);
   static_assert(SMEM <= 232448, "shared memory budget");
   if (hfta_status st = get_encode()) return st;

@@ -678,6 +678,7 @@ __global__ void __launch_bounds__(SDX_T) k_lbm_sparse_dx(int Ncl, int64_t L, int
   __shared__ uint32_t srow[SDX_T * SDX_ITEMS];
   __shared__ int schan[SDX_T * SDX_ITEMS];
   __shared__ int shead[SDX_T * SDX_ITEMS + 1];
+  __shared__ float spv[SDX_T * SDX_ITEMS];      // sp of the sorted channels
   __shared__ int snseg;
   const int b = blockIdx.y, n = blockIdx.x;
   const int t = threadIdx.x;
@@ -692,10 +693,12 @@ __global__ void __launch_bounds__(SDX_T) k_lbm_sparse_dx(int Ncl, int64_t L, int
     val[i] = c;
   }
   Sort(tmp.sort).Sort(key, val, 0, end_bit);
+  const float* spc = sp + ((int64_t)b * Ncl + n) * C;
 #pragma unroll
   for (int i = 0; i < SDX_ITEMS; ++i) {
     srow[t * SDX_ITEMS + i] = key[i];
     schan[t * SDX_ITEMS + i] = val[i];
+    spv[t * SDX_ITEMS + i] = val[i] < C ? spc[val[i]] : 0.f;
   }
   __syncthreads();
   // segment heads -> compacted list of segment starts
@@ -712,36 +715,67 @@ __global__ void __launch_bounds__(SDX_T) k_lbm_sparse_dx(int Ncl, int64_t L, int
     if (flag[i]) shead[pos[i]] = t * SDX_ITEMS + i;
   if (t == 0) { shead[total] = (int)C; snseg = total; }
   __syncthreads();
-  const int nseg = snseg, nsl = K / 8;
-  const float* spn = sp + ((int64_t)b * Ncl + n) * C;
+  const int nseg = snseg;
   const __nv_bfloat16* Wb = W + (int64_t)b * w_bs;
   __nv_bfloat16* dXn = dX + (int64_t)b * dx_bs + (int64_t)n * L * dx_ld;
+  // item = (segment = one distinct argmax row, 16-element k slice): the dX
+  // slice load is issued with the first W loads, the segment's W rows are
+  // gathered two at a time, then one gated add and store
+  const int nsl = K / 16;
   for (int it = t; it < nseg * nsl; it += SDX_T) {
-    const int sg = it / nsl, k8 = (it % nsl) * 8;
+    const int sg = it / nsl, k16 = (it % nsl) * 16;
     const int j0 = shead[sg], j1 = shead[sg + 1];
-    float acc[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-    for (int j = j0; j < j1; ++j) {
-      const int c = schan[j];
-      const float w = spn[c];
-      float x[8];
-      ld_vec<__nv_bfloat16, 8>(Wb + (int64_t)c * w_ld + k8, x);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] = fmaf(w, x[e], acc[e]);
+    const int64_t r = srow[j0];
+    __nv_bfloat16* d = dXn + r * dx_ld + k16;
+    const uint4 y0 = *reinterpret_cast<const uint4*>(d), y1 = *reinterpret_cast<const uint4*>(d + 8);
+    uint4 m0 = make_uint4(0u, 0u, 0u, 0u), m1 = m0;
+    if (mask) {
+      const __nv_bfloat16* mr = mask + (int64_t)b * m_bs + ((int64_t)n * L + r) * m_ld + k16;
+      m0 = *reinterpret_cast<const uint4*>(mr);
+      m1 = *reinterpret_cast<const uint4*>(mr + 8);
     }
-    __nv_bfloat16* d = dXn + (int64_t)srow[j0] * dx_ld + k8;
-    if (mask) {        // the dense part was gated by act'(X) in the GEMM epilogue: gate the sparse part too
-      float mv[8];
-      ld_vec<__nv_bfloat16, 8>(mask + (int64_t)b * m_bs + ((int64_t)n * L + srow[j0]) * m_ld + k8, mv);
+    float acc[16];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] *= mv[e] > 0.f ? 1.f : (m_act == HFTA_ACT_LEAKY_RELU ? m_alpha : 0.f);
+    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+    for (int j = j0; j < j1; j += 2) {
+      const bool two = j + 1 < j1;
+      const __nv_bfloat16* w0 = Wb + (int64_t)schan[j] * w_ld + k16;
+      const __nv_bfloat16* w1 = Wb + (int64_t)schan[two ? j + 1 : j] * w_ld + k16;
+      const uint4 a0 = *reinterpret_cast<const uint4*>(w0), a1 = *reinterpret_cast<const uint4*>(w0 + 8);
+      const uint4 c0 = *reinterpret_cast<const uint4*>(w1), c1 = *reinterpret_cast<const uint4*>(w1 + 8);
+      const float s0 = spv[j], s1 = two ? spv[j + 1] : 0.f;
+      const uint32_t ua[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const uint32_t uc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float lo, hi;
+        unpack_bf2(ua[q], lo, hi);
+        acc[2 * q] = fmaf(s0, lo, acc[2 * q]);
+        acc[2 * q + 1] = fmaf(s0, hi, acc[2 * q + 1]);
+        unpack_bf2(uc[q], lo, hi);
+        acc[2 * q] = fmaf(s1, lo, acc[2 * q]);
+        acc[2 * q + 1] = fmaf(s1, hi, acc[2 * q + 1]);
+      }
     }
-    float y[8];
-    ld_vec<__nv_bfloat16, 8>(d, y);
+    const uint32_t uy[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+    const uint32_t um[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+    const float neg = m_act == HFTA_ACT_LEAKY_RELU ? m_alpha : 0.f;
+    uint32_t out[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) y[e] += acc[e];
-    st_vec<__nv_bfloat16, 8>(d, y);
+    for (int q = 0; q < 8; ++q) {
+      float lo, hi;
+      unpack_bf2(uy[q], lo, hi);
+      float g0 = acc[2 * q], g1 = acc[2 * q + 1];
+      if (mask) {   // the dense part was gated by act'(X) in the GEMM epilogue: gate the sparse part too
+        float ml, mh;
+        unpack_bf2(um[q], ml, mh);
+        g0 *= ml > 0.f ? 1.f : neg;
+        g1 *= mh > 0.f ? 1.f : neg;
+      }
+      out[q] = pack_bf2(lo + g0, hi + g1);
+    }
+    *reinterpret_cast<uint4*>(d) = make_uint4(out[0], out[1], out[2], out[3]);
+    *reinterpret_cast<uint4*>(d + 8) = make_uint4(out[4], out[5], out[6], out[7]);
   }
 }
 
@@ -750,7 +784,7 @@ __global__ void __launch_bounds__(SDX_T) k_lbm_sparse_dx(int Ncl, int64_t L, int
 // k = 4l .. 4l+3 (K = 128; K = 64: lanes 0-15).  (W G): the CTA's 32 W rows
 // in smem (fp32), one G row segment (L1) per k2 reused by the warp's 4
 // channels.  Sparse part: per-cloud (sp, argmax) one per lane, broadcast by
-// shuffles, 8 row gathers issued back to back.
+// shuffles, 16 row gathers issued back to back.
 __global__ void __launch_bounds__(256, 2) k_lbm_dw(int Ncl, int64_t L, int64_t C, int K, const float* __restrict__ G,
                                                 const float* __restrict__ svec, const __nv_bfloat16* __restrict__ W,
                                                 int64_t w_bs, int64_t w_ld, const float2* __restrict__ coef,
@@ -811,11 +845,11 @@ __global__ void __launch_bounds__(256, 2) k_lbm_dw(int Ncl, int64_t L, int64_t C
         rl = (int64_t)nl * L + am[o];
       }
       const int cnt = min(32, Ncl - nb);
-      for (int q0 = 0; q0 < cnt; q0 += 8) {
-        float xv[8][4];
-        float vv[8];
+      for (int q0 = 0; q0 < cnt; q0 += 16) {
+        float xv[16][4];
+        float vv[16];
 #pragma unroll
-        for (int dq = 0; dq < 8; ++dq) {             // 8 independent row gathers in flight
+        for (int dq = 0; dq < 16; ++dq) {            // 16 independent row gathers in flight
           const int q = min(q0 + dq, cnt - 1);
           vv[dq] = q0 + dq < cnt ? __shfl_sync(0xffffffffu, vl, q) : 0.f;
           const int64_t row = __shfl_sync(0xffffffffu, rl, q);
@@ -823,7 +857,7 @@ __global__ void __launch_bounds__(256, 2) k_lbm_dw(int Ncl, int64_t L, int64_t C
           else xv[dq][0] = xv[dq][1] = xv[dq][2] = xv[dq][3] = 0.f;
         }
 #pragma unroll
-        for (int dq = 0; dq < 8; ++dq)
+        for (int dq = 0; dq < 16; ++dq)
 #pragma unroll
           for (int e = 0; e < 4; ++e) sacc[e] = fmaf(vv[dq], xv[dq][e], sacc[e]);
       }

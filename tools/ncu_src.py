@@ -1,6 +1,6 @@
 """Per-SASS-line warp-stall samples of one kernel in an ncu report (needs
 --import-source / source page).  Prints the top lines and the lines around
-mbarrier waits (SYNCS) with their samples.  Usage: python tools/ncu_src.py rep kernel-regex [N]"""
+mbarrier waits (SYNCS) with their samples.  Usage: python tools/ncu_src.py rep kernel-regex [N] [skip]"""
 import csv
 import io
 import subprocess
@@ -8,7 +8,9 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", "regex:" + kern],
+skip = int(sys.argv[4]) if len(sys.argv) > 4 else 0      # which matching launch (0 = first)
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", "regex:" + kern,
+                      "--launch-skip", str(skip), "--launch-count", "1"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
