@@ -21,6 +21,9 @@
  *   fp32-accurate.  HFTA_BF16 (bf16-AMP, reading R16): activations and GEMM
  *   operands are bf16, accumulation fp32; weight gradients, BN statistics,
  *   BN affine parameters, biases, losses and optimizer state are always fp32.
+ *   HFTA_BF16_F32 (hfta_fused_linear_fwd/bwd only, reading R16b): bf16 GEMM
+ *   operands X, W, dY with fp32 outputs Y, dX -- the bf16-AMP contraction of
+ *   a layer whose activations are kept fp32 (the per-sample FC head).
  * Ownership.  The caller owns every buffer (allocated with cudaMalloc or by
  *   PyTorch).  The library never allocates device memory, never frees, and
  *   keeps no pointer beyond the stream-ordered completion of the call.
@@ -63,7 +66,7 @@ enum {
   HFTA_ERR_NOT_INITIALIZED = 8
 };
 
-typedef enum { HFTA_F32 = 0, HFTA_BF16 = 1 } hfta_dtype;
+typedef enum { HFTA_F32 = 0, HFTA_BF16 = 1, HFTA_BF16_F32 = 2 } hfta_dtype;
 typedef enum {
   HFTA_ACT_NONE = 0, HFTA_ACT_RELU = 1, HFTA_ACT_LEAKY_RELU = 2,
   HFTA_ACT_TANH = 3, HFTA_ACT_SIGMOID = 4      /* standalone hfta_act_* only */

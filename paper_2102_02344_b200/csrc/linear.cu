@@ -12,7 +12,10 @@ size_t colsum_ws(int B, int64_t rows, int64_t C, int64_t group);
 
 hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void* ws, size_t wsb) {
   const bool epi = p.scale || p.act != HFTA_ACT_NONE || p.mask || p.K2 > 0;
-  if (skinny_fwd_ok(p) || skinny_dgrad_ok(p) || skinny_wgrad_ok(p)) return gemm_skinny(p, dt, ws, wsb, s);
+  // the streaming fwd/dgrad kernels write C in the input dtype: not for bf16 -> fp32 (HFTA_BF16_F32)
+  const bool same_out = !out_f32 || dt == HFTA_F32;
+  if ((same_out && (skinny_fwd_ok(p) || skinny_dgrad_ok(p))) || skinny_wgrad_ok(p))
+    return gemm_skinny(p, dt, ws, wsb, s);
   if (gemm_tc_supported(p, dt, out_f32)) return gemm_tc(p, dt, out_f32, s);
   if (epi) return fail(HFTA_ERR_UNSUPPORTED, "fused epilogue / second K segment needs the tensor-core or skinny path");
   return gemm_simt(p, dt, out_f32, s);
@@ -60,7 +63,9 @@ hfta_status hfta_fused_linear_fwd(int B, int64_t M, int64_t N, int64_t K, hfta_d
   HFTA_CHECK_B(B);
   HFTA_REQUIRE(M >= 1 && N >= 1 && K >= 1, HFTA_ERR_SHAPE, "linear_fwd: M,N,K = %lld,%lld,%lld",
                (long long)M, (long long)N, (long long)K);
-  HFTA_REQUIRE(dt == HFTA_F32 || dt == HFTA_BF16, HFTA_ERR_UNSUPPORTED, "linear_fwd: dtype %d", (int)dt);
+  HFTA_REQUIRE(dt == HFTA_F32 || dt == HFTA_BF16 || dt == HFTA_BF16_F32, HFTA_ERR_UNSUPPORTED, "linear_fwd: dtype %d",
+               (int)dt);
+  const bool mixed = dt == HFTA_BF16_F32;         // bf16 operands, fp32 Y
   if (hfta_status st = check_in(X, "X", B)) return st;
   if (hfta_status st = check_in(W, "W", B)) return st;
   if (hfta_status st = check_out(Y, "Y", B)) return st;
@@ -78,7 +83,7 @@ hfta_status hfta_fused_linear_fwd(int B, int64_t M, int64_t N, int64_t K, hfta_d
   p.bias = bias; p.bias_bs = bias_bstride; p.bias_ld = bias_ld;
   p.bias_div = (bias_ld > 0 && bias_row_div > 0) ? bias_row_div : 0;
   p.splits = 1; p.k_chunk = cdiv(K, 16) * 16;
-  return run_gemm(p, dt, false, (cudaStream_t)stream);
+  return run_gemm(p, mixed ? HFTA_BF16 : dt, mixed, (cudaStream_t)stream);
 }
 
 size_t hfta_fused_linear_bwd_workspace(int B, int64_t M, int64_t N, int64_t K, hfta_dtype dt) {
@@ -100,7 +105,10 @@ hfta_status hfta_fused_linear_bwd(int B, int64_t M, int64_t N, int64_t K, hfta_d
   HFTA_CHECK_B(B);
   HFTA_REQUIRE(M >= 1 && N >= 1 && K >= 1, HFTA_ERR_SHAPE, "linear_bwd: M,N,K = %lld,%lld,%lld",
                (long long)M, (long long)N, (long long)K);
-  HFTA_REQUIRE(dt == HFTA_F32 || dt == HFTA_BF16, HFTA_ERR_UNSUPPORTED, "linear_bwd: dtype %d", (int)dt);
+  HFTA_REQUIRE(dt == HFTA_F32 || dt == HFTA_BF16 || dt == HFTA_BF16_F32, HFTA_ERR_UNSUPPORTED, "linear_bwd: dtype %d",
+               (int)dt);
+  const bool mixed = dt == HFTA_BF16_F32;         // bf16 operands, fp32 dX
+  if (mixed) dt = HFTA_BF16;
   if (hfta_status st = check_in(dY, "dY", B)) return st;
   HFTA_REQUIRE(dY.ld >= N, HFTA_ERR_SHAPE, "linear_bwd: dY ld %lld < N %lld", (long long)dY.ld, (long long)N);
   cudaStream_t s = (cudaStream_t)stream;
@@ -117,7 +125,7 @@ hfta_status hfta_fused_linear_bwd(int B, int64_t M, int64_t N, int64_t K, hfta_d
     p.Bm = W.ptr; p.b_bs = W.bstride; p.b_ld = W.ld; p.b_kmajor = 0;
     p.C = dX.ptr; p.c_bs = dX.bstride; p.c_ld = dX.ld;
     p.splits = 1; p.k_chunk = cdiv(N, 16) * 16;
-    if (hfta_status st = run_gemm(p, dt, false, s)) return st;
+    if (hfta_status st = run_gemm(p, dt, mixed, s)) return st;
   }
   if (dW) {
     if (hfta_status st = check_in(X, "X", B)) return st;

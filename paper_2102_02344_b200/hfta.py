@@ -19,7 +19,7 @@ if not os.path.exists(LIB_PATH):
                       "(no CPU fallback exists)" % LIB_PATH)
 _lib = C.CDLL(LIB_PATH)
 
-HFTA_F32, HFTA_BF16 = 0, 1
+HFTA_F32, HFTA_BF16, HFTA_BF16_F32 = 0, 1, 2
 ACT_NONE, ACT_RELU, ACT_LEAKY_RELU, ACT_TANH, ACT_SIGMOID = 0, 1, 2, 3, 4
 STATUS = {0: "HFTA_OK", 1: "HFTA_ERR_INVALID_VALUE", 2: "HFTA_ERR_SHAPE", 3: "HFTA_ERR_ALIGNMENT",
           4: "HFTA_ERR_UNSUPPORTED", 5: "HFTA_ERR_ARCH", 6: "HFTA_ERR_WORKSPACE", 7: "HFTA_ERR_CUDA",

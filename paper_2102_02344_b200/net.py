@@ -118,19 +118,51 @@ class FusedNet:
     def _dt(self, t):
         return H.HFTA_F32 if t.dtype == torch.float32 else H.HFTA_BF16
 
+    def _mixed(self, Y, M, Nn, K, X=None):
+        """bf16-AMP contraction of an fp32-activation layer (reading R16b): in
+        bf16 mode the per-sample FC layers keep fp32 activations but run
+        their GEMMs on the tensor cores with bf16 operands (HFTA_BF16_F32)."""
+        if self.dt != H.HFTA_BF16 or Y.dtype != torch.float32 or Nn < 16 or K < 16 or K % 8 or Nn % 8:
+            return False
+        return X is None or (X.bstride == M * K and X.ld == K)
+
+    def _bf(self, key, rows, cols):
+        """Persistent bf16 scratch (graph-capture safe: allocated on first use)."""
+        if not hasattr(self, "_bf_bufs"):
+            self._bf_bufs = {}
+        t = self._bf_bufs.get(key)
+        if t is None or t.shape[1] != rows or t.shape[2] != cols:
+            t = torch.empty(self.B, rows, cols, dtype=torch.bfloat16, device=self.device)
+            self._bf_bufs[key] = t
+        return t
+
     def _lin_fwd(self, X, M, name, Y, s):
         Nn, K = self.arena.shape[name + ".W"]
         dt = self._dt(Y)
         e0 = self._pbegin(name + ":fwd", s)
-        H.hfta_fused_linear_fwd(self.B, M, Nn, K, dt, X, self.arena.w_in(name + ".W", dt),
-                                self.arena.fptr("p", name + ".b"), self.arena.P, 0, 0, _out(Y), s)
+        if self._mixed(Y, M, Nn, K, X):
+            xb = self._bf(name + ".x", M, K)          # kept for the backward's wgrad
+            H.hfta_cast_f32_bf16(self.B * M * K, X.ptr, H.ptr(xb), s)
+            H.hfta_fused_linear_fwd(self.B, M, Nn, K, H.HFTA_BF16_F32, _in(xb), self.arena.w_in(name + ".W", H.HFTA_BF16),
+                                    self.arena.fptr("p", name + ".b"), self.arena.P, 0, 0, _out(Y), s)
+        else:
+            H.hfta_fused_linear_fwd(self.B, M, Nn, K, dt, X, self.arena.w_in(name + ".W", dt),
+                                    self.arena.fptr("p", name + ".b"), self.arena.P, 0, 0, _out(Y), s)
         self._pend(e0)
 
     def _lin_bwd(self, dY, X, M, name, dX, s, accumulate=0):
         Nn, K = self.arena.shape[name + ".W"]
         dt = self._dt(dY)
         e0 = self._pbegin(name + ":bwd", s)
-        H.hfta_fused_linear_bwd(self.B, M, Nn, K, dt, _in(dY), X, self.arena.w_in(name + ".W", dt),
+        xb = getattr(self, "_bf_bufs", {}).get(name + ".x")
+        if xb is not None and self._mixed(dY, M, Nn, K) and (dX is None or dX.dtype == torch.float32):
+            dyb = self._bf("dy.%d.%d" % (M, Nn), M, Nn)
+            H.hfta_cast_f32_bf16(self.B * M * Nn, H.ptr(dY), H.ptr(dyb), s)
+            dt, dY_in, X = H.HFTA_BF16_F32, _in(dyb), _in(xb)
+            w = self.arena.w_in(name + ".W", H.HFTA_BF16)
+        else:
+            dY_in, w = _in(dY), self.arena.w_in(name + ".W", dt)
+        H.hfta_fused_linear_bwd(self.B, M, Nn, K, dt, dY_in, X, w,
                                 _out(dX) if dX is not None else H.tout(None, 0, 1),
                                 self.arena.fptr("g", name + ".W"), self.arena.P, K,
                                 None if name in self.bn_followed else self.arena.fptr("g", name + ".b"), self.arena.P,

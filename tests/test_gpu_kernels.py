@@ -86,6 +86,38 @@ def test_linear_fwd_bwd(dt, M, N, K, B, shared):
         assert_close(host(db[b]), dbb, 1e-5, "dbias")
 
 
+@pytest.mark.parametrize("M,N,K,B", [(32, 512, 1024, 3), (32, 40, 256, 2), (32, 9, 256, 2), (77, 64, 96, 2)])
+def test_linear_bf16_f32(M, N, K, B):
+    """HFTA_BF16_F32 (reading R16b): bf16 X, W, dY operands, fp32 Y and dX --
+    the per-sample FC head's contraction in bf16 mode (tensor cores where
+    N, K >= 16, SIMT otherwise).  Outputs are compared with the oracle on
+    the same bf16-rounded operands at fp32-accumulation tolerance."""
+    X = rounded(R.standard_normal((B, M, K)), torch.bfloat16)
+    W = rounded(R.standard_normal((B, N, K)) / np.sqrt(K), torch.bfloat16)
+    bias = R.standard_normal((B, N)).astype(np.float32).astype(np.float64)
+    dY = rounded(R.standard_normal((B, M, N)), torch.bfloat16)
+    Xd, Wd, bd, dYd = dev(X, torch.bfloat16), dev(W, torch.bfloat16), dev(bias), dev(dY, torch.bfloat16)
+    Y = torch.empty(B, M, N, device=DEV)
+    H.hfta_fused_linear_fwd(B, M, N, K, H.HFTA_BF16_F32, H.tin(Xd, M * K, K), H.tin(Wd, N * K, K), H.ptr(bd), N, 0, 0,
+                            H.tout(Y, M * N, N), s())
+    dX = torch.empty(B, M, K, device=DEV)
+    dW = torch.empty(B, N, K, device=DEV)
+    db = torch.empty(B, N, device=DEV)
+    code = H.HFTA_BF16_F32
+    ws = torch.empty(max(H.hfta_fused_linear_bwd_workspace(B, M, N, K, code), 1), dtype=torch.uint8, device=DEV)
+    H.hfta_fused_linear_bwd(B, M, N, K, code, H.tin(dYd, M * N, N), H.tin(Xd, M * K, K), H.tin(Wd, N * K, K),
+                            H.tout(dX, M * K, K), H.ptr(dW), N * K, K, H.ptr(db), N, 0, H.ptr(ws), ws.numel(), s())
+    torch.cuda.synchronize()
+    assert Y.dtype == torch.float32 and dX.dtype == torch.float32
+    for b in range(B):
+        y = OL.linear_fwd(X[b], W[b], bias[b])
+        dx, dw, dbb = OL.linear_bwd(dY[b], X[b], W[b])
+        assert_close(host(Y[b]), y, 1e-5, "Y (fp32 out)")
+        assert_close(host(dX[b]), dx, 1e-5, "dX (fp32 out)")
+        assert_close(host(dW[b]), dw, 1e-5, "dW")
+        assert_close(host(db[b]), dbb, 1e-5, "dbias")
+
+
 def test_linear_bwd_accumulate_and_rowgroup_bias():
     B, M, N, K, L = 2, 500, 48, 32, 125
     X = R.standard_normal((B, M, K)).astype(np.float32).astype(np.float64)
