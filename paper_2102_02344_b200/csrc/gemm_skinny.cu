@@ -74,53 +74,85 @@ __global__ void __launch_bounds__(NT) k_skinny_fwd(GemmP p, int tpr, int rpb, in
 template <typename T, int VEC>
 __global__ void __launch_bounds__(NT) k_skinny_dgrad(GemmP p, int tpr) {
   __shared__ float4 w[1024];                           // w[n] = (W[n][0..3])
+  __shared__ float4 m2s[32];                           // M2[k][0..3] (K2 <= 32)
   const int b = blockIdx.y;
   const T* A = reinterpret_cast<const T*>(p.A) + (int64_t)b * p.a_bs;
   const T* Bw = reinterpret_cast<const T*>(p.Bm) + (int64_t)b * p.b_bs;
   T* C = reinterpret_cast<T*>(p.C) + (int64_t)b * p.c_bs;
-  const int Kr = (int)p.K, Nj = (int)p.N;
+  const int Kr = (int)p.K, Nj = (int)p.N, K2 = (int)p.K2;
   for (int n = threadIdx.x; n < Kr; n += NT) {
     float e[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) e[j] = j < Nj ? ldf(Bw + (int64_t)n * p.b_ld + j) : 0.f;
     w[n] = make_float4(e[0], e[1], e[2], e[3]);
   }
+  if (K2 > 0) {
+    const float* M2 = reinterpret_cast<const float*>(p.Bm2) + (int64_t)b * p.b2_bs;
+    for (int k = threadIdx.x; k < K2; k += NT) {
+      float e[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) e[j] = j < Nj ? M2[k * Nj + j] : 0.f;
+      m2s[k] = make_float4(e[0], e[1], e[2], e[3]);
+    }
+  }
+  float bj[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) bj[j] = (p.bias && j < Nj) ? p.bias[(int64_t)b * p.bias_bs + j] : 0.f;
   __syncthreads();
   const int lane = threadIdx.x % tpr, rl = threadIdx.x / tpr, rpb = NT / tpr;
   const int n0 = lane * VEC;
-  for (int64_t m = blockIdx.x * (int64_t)rpb + rl; m < p.M; m += (int64_t)gridDim.x * rpb) {
-    float av[VEC];
-    ld_vec<T, VEC>(A + m * p.a_ld + n0, av);
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  // this lane's W slice (VEC rows x 4 outputs) and M2 row in registers: no
+  // shared-memory traffic in the row loop
+  float4 wr[VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      const float4 wv = w[n0 + v];
-      acc[0] = fmaf(av[v], wv.x, acc[0]); acc[1] = fmaf(av[v], wv.y, acc[1]);
-      acc[2] = fmaf(av[v], wv.z, acc[2]); acc[3] = fmaf(av[v], wv.w, acc[3]);
-    }
-    for (int o = tpr / 2; o > 0; o >>= 1)
+  for (int v = 0; v < VEC; ++v) wr[v] = w[n0 + v];
+  const float4 mr = (K2 > 0 && lane < K2) ? m2s[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const T* A2 = K2 > 0 ? reinterpret_cast<const T*>(p.A2) + (int64_t)b * p.a2_bs : nullptr;
+  const T* Mk = p.mask ? reinterpret_cast<const T*>(p.mask) + (int64_t)b * p.mask_bs : nullptr;
+  const float neg = p.mask_act == HFTA_ACT_LEAKY_RELU ? p.mask_alpha : 0.f;
+  constexpr int U = 2;                                 // rows per group in flight
+  const int64_t stride = (int64_t)gridDim.x * rpb;
+  for (int64_t m0 = blockIdx.x * (int64_t)rpb + rl; m0 < p.M; m0 += stride * U) {
+    float av[U][VEC];
+    float xa[U], mk[U];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-    if (lane == 0) {
-      if (p.K2 > 0) {   // + A2[m] M2 + bias: the Gram-form BN backward's X M + v term (M2 fp32 [K2][Nj])
-        const T* a2 = reinterpret_cast<const T*>(p.A2) + (int64_t)b * p.a2_bs + m * p.a2_ld;
-        const float* M2 = reinterpret_cast<const float*>(p.Bm2) + (int64_t)b * p.b2_bs;
-        for (int k = 0; k < (int)p.K2; ++k) {
-          const float xk = ldf(a2 + k);
+    for (int u = 0; u < U; ++u) {                      // all loads of U rows issued up front
+      const int64_t m = m0 + u * stride;
+      const bool ok = m < p.M;
+      if (ok) ld_vec<T, VEC>(A + m * p.a_ld + n0, av[u]);
+      else {
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (j < Nj) acc[j] = fmaf(xk, M2[k * Nj + j], acc[j]);
-        }
+        for (int v = 0; v < VEC; ++v) av[u][v] = 0.f;
       }
+      xa[u] = (ok && lane < K2) ? ldf(A2 + m * p.a2_ld + lane) : 0.f;     // lane k holds x[m][k]
+      mk[u] = (ok && Mk && lane < Nj) ? ldf(Mk + m * p.mask_ld + lane) : 1.f;
+    }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (j >= Nj) break;
-        float vj = acc[j] + (p.bias ? p.bias[(int64_t)b * p.bias_bs + j] : 0.f);
-        if (p.mask) {
-          const float mk = ldf(reinterpret_cast<const T*>(p.mask) + (int64_t)b * p.mask_bs + m * p.mask_ld + j);
-          vj *= mk > 0.f ? 1.f : (p.mask_act == HFTA_ACT_LEAKY_RELU ? p.mask_alpha : 0.f);
-        }
-        stf(C + m * p.c_ld + j, vj);
+    for (int u = 0; u < U; ++u) {
+      const int64_t m = m0 + u * stride;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        acc[0] = fmaf(av[u][v], wr[v].x, acc[0]); acc[1] = fmaf(av[u][v], wr[v].y, acc[1]);
+        acc[2] = fmaf(av[u][v], wr[v].z, acc[2]); acc[3] = fmaf(av[u][v], wr[v].w, acc[3]);
+      }
+      // the Gram-form BN backward's X M2 term, one k per lane (mr = 0 on the other lanes)
+      acc[0] = fmaf(xa[u], mr.x, acc[0]); acc[1] = fmaf(xa[u], mr.y, acc[1]);
+      acc[2] = fmaf(xa[u], mr.z, acc[2]); acc[3] = fmaf(xa[u], mr.w, acc[3]);
+      for (int o = tpr / 2; o > 0; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+      if (m < p.M && lane < Nj) {                      // lane j stores column j
+        float vj = acc[0];
+#pragma unroll
+        for (int j = 1; j < 4; ++j)
+          if (lane == j) vj = acc[j];
+        vj += bj[0];
+#pragma unroll
+        for (int j = 1; j < 4; ++j)
+          if (lane == j) vj += bj[j] - bj[0];
+        if (Mk) vj *= mk[u] > 0.f ? 1.f : neg;
+        stf(C + m * p.c_ld + lane, vj);
       }
     }
   }
@@ -389,6 +421,7 @@ hfta_status gemm_skinny(const GemmP& p, hfta_dtype dt, void* ws, size_t ws_bytes
     int tpr = 1;
     while (tpr * vec < p.K && tpr < 32) tpr <<= 1;     // K / vec lanes per row (power of 2 up to 32)
     if (tpr * vec != p.K) { tpr = 1; }
+    if (tpr > 1 && (tpr < p.N || tpr < p.K2 || p.K2 > 32)) tpr = 1;   // lane j stores column j, lane k holds x[k]
     const int rpb = NT / tpr;
     dim3 grid((unsigned)std::min<int64_t>(cdiv(p.M, rpb), cdiv(16 * 148, p.B)), p.B);
     HFTA_REQUIRE(tpr > 1 || plain(p), HFTA_ERR_UNSUPPORTED, "skinny dgrad: fused terms need K %% 8 == 0");

@@ -277,39 +277,45 @@ k_lbm_fwd(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int valid = (int)min((int64_t)FR, p.L - (int64_t)ch * FR);
         PROF_WAIT(0, mbar_wait(&tfull[acc], aph));
         tc_fence_after();
-        // all four 32-column loads in flight, one wait, release the
-        // accumulator, then reduce while the next chunks' MMAs run
+        // TMEM reads are the epilogue's bound (128 KB per chunk over 8 warps):
+        // the first two 32-column loads land, the last two are issued and
+        // the first half is reduced while they are in flight; the
+        // accumulator is released once all four have landed
         const uint32_t ta = tmem_base + (uint32_t)(acc * FG * FR + half * FR) + ((uint32_t)(quarter * 32) << 16);
         uint32_t r0[32], r1[32], r2[32], r3[32];
         const bool work = nld != 0;
         if (work) {
           tmem_ld32_nowait(ta, r0);
           tmem_ld32_nowait(ta + 32, r1);
+          tmem_wait_ld();
           tmem_ld32_nowait(ta + 64, r2);
           tmem_ld32_nowait(ta + 96, r3);
-          tmem_wait_ld();
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&tempty[acc]);
-        }
+        const int g0 = ch * (FR / 16);
         if (work) {
-          const int g0 = ch * (FR / 16);
           if (valid == FR) {
             fwd_group<true>(r0, 16, g0, A[0], slots);
             fwd_group<true>(r0 + 16, 16, g0 + 1, A[0], slots);
             fwd_group<true>(r1, 16, g0 + 2, A[0], slots);
             fwd_group<true>(r1 + 16, 16, g0 + 3, A[0], slots);
-            fwd_group<true>(r2, 16, g0 + 4, A[0], slots);
-            fwd_group<true>(r2 + 16, 16, g0 + 5, A[0], slots);
-            fwd_group<true>(r3, 16, g0 + 6, A[0], slots);
-            fwd_group<true>(r3 + 16, 16, g0 + 7, A[0], slots);
           } else {
             fwd_group<false>(r0, valid, g0, A[0], slots);
             fwd_group<false>(r0 + 16, valid - 16, g0 + 1, A[0], slots);
             fwd_group<false>(r1, valid - 32, g0 + 2, A[0], slots);
             fwd_group<false>(r1 + 16, valid - 48, g0 + 3, A[0], slots);
+          }
+          tmem_wait_ld();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (work) {
+          if (valid == FR) {
+            fwd_group<true>(r2, 16, g0 + 4, A[0], slots);
+            fwd_group<true>(r2 + 16, 16, g0 + 5, A[0], slots);
+            fwd_group<true>(r3, 16, g0 + 6, A[0], slots);
+            fwd_group<true>(r3 + 16, 16, g0 + 7, A[0], slots);
+          } else {
             fwd_group<false>(r2, valid - 64, g0 + 4, A[0], slots);
             fwd_group<false>(r2 + 16, valid - 80, g0 + 5, A[0], slots);
             fwd_group<false>(r3, valid - 96, g0 + 6, A[0], slots);
