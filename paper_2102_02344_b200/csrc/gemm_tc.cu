@@ -49,6 +49,7 @@ struct TcArgs {
   int mask_kb;                       // >= 0: the gating tensor is the A tile of k-blocks mask_kb..:
                                      // read from the resident smem stage (released by the epilogue)
   float* colsum; int64_t colsum_bs; int colsum_acc; float* colsum_part;   // fused column sums of A
+  int ab_same;                       // Gram X^T X (A == B, one 128-wide tile): B is read from the A stage
 };
 
 // BRES ("B resident", forward layers with K <= 128): the B operand (the
@@ -117,7 +118,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   if constexpr (CSUM) {
     if (p.colsum) {   // the ones atom of every stage (never written by TMA)
       for (int st = 0; st < STAGES; ++st) {
-        uint32_t* ones = reinterpret_cast<uint32_t*>(smem + st * STAGE_BYTES + A_BYTES + B_LOAD);
+        // ab_same: B aliases the A tile (two atoms), the ones atom follows it directly
+        uint32_t* ones = reinterpret_cast<uint32_t*>(smem + st * STAGE_BYTES + A_BYTES + (p.ab_same ? 0 : B_LOAD));
         for (int i = threadIdx.x; i < 2048; i += NTHREADS) ones[i] = 0x3F803F80u;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -173,7 +175,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(&full[stage], LOAD_BYTES);
+          mbar_expect_tx(&full[stage], (CSUM && p.ab_same) ? A_BYTES : LOAD_BYTES);
           (void)sb;
           const int k0 = (int)(kbeg + (int64_t)kb * BK);
           if (EPI == 2 && kb >= nkb1) {                   // second K segment (K-major A2, B2)
@@ -187,6 +189,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             tma_load_3d(sa, &tmA, &full[stage], k0, m0, ba);
           }
           if (EPI == 2 && kb >= nkb1) {
+          } else if (CSUM && p.ab_same) {                 // Gram: the A tile is also B
           } else if constexpr (!BRES) {
             if (B_MN) {
 #pragma unroll
@@ -237,7 +240,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tc_fence_after();
         {
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-          const uint32_t sb = BRES ? smem_u32(bres + kb * B_BYTES) : sa + A_BYTES;
+          const uint32_t sb = BRES ? smem_u32(bres + kb * B_BYTES) : ((CSUM && p.ab_same) ? sa : sa + A_BYTES);
           const uint64_t ad0 = A_MN ? smem_desc(sa, 8192, 1024) : smem_desc(sa, 16, 1024);
           const uint64_t bd0 = B_MN ? smem_desc(sb, 8192, 1024) : smem_desc(sb, 16, 1024);
 #pragma unroll
@@ -527,6 +530,9 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   a.K2 = EPI == 2 ? p.K2 : 0;
   a.colsum = p.colsum; a.colsum_bs = p.colsum_bs; a.colsum_acc = p.colsum_acc; a.colsum_part = p.colsum_part;
   a.mask_kb = -1;
+  // Gram X^T X of one 128-wide tile: load the tile once, use it as both operands
+  a.ab_same = (A_MN && B_MN && OUT_F32 && BN == 128 && p.A == p.Bm && p.a_ld == p.b_ld && p.a_bs == p.b_bs &&
+               a.tiles_m == 1 && a.tiles_n == 1 && p.M == p.N) ? 1 : 0;
   // the gating tensor is the A operand itself (same rows, its columns = the
   // output's): read it from the resident A stage instead of global memory
   if (EPI == 2 && p.mask && p.splits == 1 && p.N <= BN) {

@@ -25,13 +25,24 @@ namespace {
 // split-K policy of the weight-gradient contraction (reduction over M rows).
 struct Split { int splits; int64_t chunk; };
 Split wgrad_split(int B, int64_t M, int64_t N, int64_t K) {
-  int64_t tiles = cdiv(N, 128) * cdiv(K, 128) * (int64_t)B;
-  int64_t want = cdiv(2 * (int64_t)std::max(num_sms(), 148), tiles);
-  int64_t maxs = std::max<int64_t>(1, M / 1024);
-  int64_t splits = std::max<int64_t>(1, std::min(want, maxs));
-  int64_t chunk = cdiv(cdiv(M, splits), 128) * 128;
-  splits = cdiv(M, chunk);
-  return {(int)splits, chunk};
+  // Split the reduction over M so the persistent grid's last wave is full:
+  // the busiest CTA streams ceil(tiles / SMs) tiles, each (M/s) rows of
+  // (N + K) bf16 plus an N x K fp32 partial written and re-read by the
+  // reduction; pick the split count s minimising that.
+  const int64_t sms = std::max(num_sms(), 1);
+  const int64_t tiles = cdiv(N, 128) * cdiv(K, 128) * (int64_t)B;
+  const int64_t maxs = std::max<int64_t>(1, M / 1024);
+  int64_t best_s = 1;
+  double best = -1.0;
+  for (int64_t s = 1; s <= std::min<int64_t>(maxs, 64); ++s) {
+    const int64_t chunk = cdiv(cdiv(M, s), 128) * 128;
+    const int64_t sp = cdiv(M, chunk);
+    const double per_tile = (double)chunk * (double)(N + K) * 2.0 + (sp > 1 ? (double)N * K * 8.0 : 0.0);
+    const double cost = (double)cdiv(tiles * sp, sms) * per_tile;
+    if (best < 0.0 || cost < best * 0.999) { best = cost; best_s = sp; }
+  }
+  const int64_t chunk = cdiv(cdiv(M, best_s), 128) * 128;
+  return {(int)cdiv(M, chunk), chunk};
 }
 
 
