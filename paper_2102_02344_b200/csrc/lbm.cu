@@ -40,7 +40,6 @@
 namespace hfta {
 namespace {
 
-constexpr int LT = 320;
 constexpr int FWD_LT = 352;         // forward: producer, MMA issuers (warps 1, 10), 8 epilogue warps
 constexpr int MMA2_WARP = 10;
 constexpr int NEPIW = 8;
@@ -390,9 +389,26 @@ __global__ void k_lbm_flip(int B, int64_t C, int64_t K, const __nv_bfloat16* __r
 // k groups of a half-warp.  Writes save_mean / save_invstd and the running
 // statistics.  K in {64, 128}.
 constexpr int ST_CH = 64;                // channels per CTA
+
+// Gc = G - R mu mu^T in fp64 -> fp32 and mu = s / R (fp64), once per model
+// (the statistics CTAs of a model then just copy Gc into shared memory).
+__global__ void __launch_bounds__(256) k_lbm_center(int K, int64_t R, const float* __restrict__ G,
+                                                    const float* __restrict__ xs, float* __restrict__ Gc,
+                                                    double* __restrict__ mu) {
+  const int b = blockIdx.y;
+  const double Rd = (double)R;
+  const float* xb = xs + (int64_t)b * K;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < K) mu[(int64_t)b * K + i] = (double)xb[i] / Rd;
+  if (i >= (int64_t)K * K) return;
+  const int j = (int)(i / K), k = (int)(i % K);
+  const double mj = (double)xb[j] / Rd, mk = (double)xb[k] / Rd;
+  Gc[(int64_t)b * K * K + i] = (float)((double)G[(int64_t)b * K * K + i] - Rd * mj * mk);
+}
+
 template <int K>
-__global__ void __launch_bounds__(256) k_lbm_stats(int B, int64_t R, int64_t C, const float* __restrict__ G,
-                                                   const float* __restrict__ xs, const __nv_bfloat16* __restrict__ W,
+__global__ void __launch_bounds__(256) k_lbm_stats(int B, int64_t R, int64_t C, const float* __restrict__ Gcg,
+                                                   const double* __restrict__ mug, const __nv_bfloat16* __restrict__ W,
                                                    int64_t wbs, int64_t wld, const float* __restrict__ bias,
                                                    int64_t bias_bs, float* __restrict__ rmean,
                                                    float* __restrict__ rvar, float momentum, float eps,
@@ -403,34 +419,20 @@ __global__ void __launch_bounds__(256) k_lbm_stats(int B, int64_t R, int64_t C, 
   __shared__ double mu[128];
   const int b = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * ST_CH;
-  const float* Gb = G + (int64_t)b * K * K;
   const double Rd = (double)R;
-  for (int k = threadIdx.x; k < K; k += blockDim.x) mu[k] = (double)xs[(int64_t)b * K + k] / Rd;
-  __syncthreads();
-  constexpr int lk = K == 128 ? 7 : 6;
-  // vector loads, 4 in flight per thread (the prologue is L2-latency bound otherwise)
-  const float4* G4 = reinterpret_cast<const float4*>(Gb);
-  const int n4 = K * K / 4;
-  for (int i0 = threadIdx.x; i0 < n4; i0 += 4 * blockDim.x) {
-    float4 g[4];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) mu[k] = mug[(int64_t)b * K + k];
+  {   // Gc (fp32, centred once per model by k_lbm_center): 16-B loads, 4 in flight per thread
+    const float4* G4 = reinterpret_cast<const float4*>(Gcg + (int64_t)b * K * K);
+    float4* S4 = reinterpret_cast<float4*>(Gc);
+    constexpr int n4 = K * K / 4;
+    for (int i0 = threadIdx.x; i0 < n4; i0 += 4 * 256) {
+      float4 g[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * blockDim.x;
-      if (i < n4) g[u] = __ldg(G4 + i);
-    }
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u * 256 < n4) g[u] = __ldg(G4 + i0 + u * 256);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * blockDim.x;
-      if (i < n4) {
-        const int j = (4 * i) >> lk, k = (4 * i) & (K - 1);
-        const double mj = Rd * mu[j];
-        float4 o;
-        o.x = (float)((double)g[u].x - mj * mu[k]);
-        o.y = (float)((double)g[u].y - mj * mu[k + 1]);
-        o.z = (float)((double)g[u].z - mj * mu[k + 2]);
-        o.w = (float)((double)g[u].w - mj * mu[k + 3]);
-        *reinterpret_cast<float4*>(Gc + 4 * i) = o;
-      }
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u * 256 < n4) S4[i0 + u * 256] = g[u];
     }
   }
   const __nv_bfloat16* Wb = W + (int64_t)b * wbs;
@@ -601,65 +603,104 @@ __global__ void k_lbm_bwd_coef(int B, int Ncl, int64_t L, int64_t C, const float
 // Grid (K/64, B): a CTA owns 64 rows of M; thread = 4 rows x 8 columns
 // register tile; W streamed through smem 32 channels at a time (fp32).
 constexpr int MV_ROWS = 64;
-__global__ void __launch_bounds__(256) k_lbm_mv(int64_t C, int K, const __nv_bfloat16* __restrict__ W, int64_t w_bs,
+template <int K>
+__global__ void __launch_bounds__(256) k_lbm_mv(int64_t C, const __nv_bfloat16* __restrict__ W, int64_t w_bs,
                                                 int64_t w_ld, const float2* __restrict__ coef,
-                                                __nv_bfloat16* __restrict__ Mout, float* __restrict__ v) {
-  __shared__ __align__(16) float swa[32][128];   // bx_c * W[c][k]
-  __shared__ __align__(16) float swb[32][128];   // W[c][k]
+                                                float* __restrict__ Mpart, float* __restrict__ vpart) {
+  // M[r][c] = sum_ch bx_ch W[ch][r] W[ch][c] over this CTA's channel range:
+  // 16 x 16 threads, each an (NH*4) x (NH*4) register tile at rows
+  // {4 tr + 64 h + i}, columns {4 tc + 64 h + j} (conflict-free LDS.128:
+  // 64 FFMA per 4 shared loads at K = 128)
+  constexpr int NH = K / 64;
+  __shared__ __align__(16) float swa[32][K];   // bx_c * W[c][k]
+  __shared__ __align__(16) float swb[32][K];   // W[c][k]
   __shared__ float scc[32];
-  const int b = blockIdx.y, rbase = blockIdx.x * MV_ROWS;
-  const int t = threadIdx.x;
-  const int ncg = K / 8;                          // column groups of 8
-  const int rg = t / ncg, cg = t % ncg;           // rows rbase + 4 rg .. +3, columns 8 cg .. +7
-  const bool act = rg * 4 < MV_ROWS && rbase + rg * 4 < K;
-  float acc[4][8];
+  const int b = blockIdx.y;
+  const int64_t cs = C * blockIdx.z / gridDim.z, ce = C * (blockIdx.z + 1) / gridDim.z;
+  const int t = threadIdx.x, tr = t / 16, tc = t % 16;
+  float acc[NH * 4][NH * 4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < NH * 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-  float vacc = 0.f;
+    for (int j = 0; j < NH * 4; ++j) acc[i][j] = 0.f;
+  float vacc[NH * 4];
+#pragma unroll
+  for (int j = 0; j < NH * 4; ++j) vacc[j] = 0.f;
   const __nv_bfloat16* Wb = W + (int64_t)b * w_bs;
-  for (int64_t c0 = 0; c0 < C; c0 += 32) {
+  for (int64_t c0 = cs; c0 < ce; c0 += 32) {
     __syncthreads();
-    for (int e = t; e < 32 * (K / 8); e += 256) {          // 8 bf16 per load
+    for (int e = t; e < 32 * (K / 8); e += 256) {          // 8 bf16 per load, two STS.128 per array
       const int q = e / (K / 8), k8 = (e % (K / 8)) * 8;
       float x[8];
       ld_vec<__nv_bfloat16, 8>(Wb + (c0 + q) * w_ld + k8, x);
       const float bx = coef[(int64_t)b * C + c0 + q].x;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) { swb[q][k8 + i] = x[i]; swa[q][k8 + i] = x[i] * bx; }
+      *reinterpret_cast<float4*>(&swb[q][k8]) = make_float4(x[0], x[1], x[2], x[3]);
+      *reinterpret_cast<float4*>(&swb[q][k8 + 4]) = make_float4(x[4], x[5], x[6], x[7]);
+      *reinterpret_cast<float4*>(&swa[q][k8]) = make_float4(x[0] * bx, x[1] * bx, x[2] * bx, x[3] * bx);
+      *reinterpret_cast<float4*>(&swa[q][k8 + 4]) = make_float4(x[4] * bx, x[5] * bx, x[6] * bx, x[7] * bx);
     }
     if (t < 32) scc[t] = coef[(int64_t)b * C + c0 + t].y;
     __syncthreads();
-    if (act) {
-#pragma unroll 4
-      for (int q = 0; q < 32; ++q) {
-        const float4 a4 = *reinterpret_cast<const float4*>(&swa[q][rbase + rg * 4]);
-        const float4 b0 = *reinterpret_cast<const float4*>(&swb[q][cg * 8]);
-        const float4 b1 = *reinterpret_cast<const float4*>(&swb[q][cg * 8 + 4]);
-        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll 2
+    for (int q = 0; q < 32; ++q) {
+      float av[NH * 4], bv[NH * 4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+      for (int h = 0; h < NH; ++h) {
+        const float4 a4 = *reinterpret_cast<const float4*>(&swa[q][tr * 4 + 64 * h]);
+        const float4 b4 = *reinterpret_cast<const float4*>(&swb[q][tc * 4 + 64 * h]);
+        av[4 * h] = a4.x; av[4 * h + 1] = a4.y; av[4 * h + 2] = a4.z; av[4 * h + 3] = a4.w;
+        bv[4 * h] = b4.x; bv[4 * h + 1] = b4.y; bv[4 * h + 2] = b4.z; bv[4 * h + 3] = b4.w;
+      }
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      for (int i = 0; i < NH * 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NH * 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+      if (tr == 0) {                                        // v = W^T cc on the first row group
+        const float cq = scc[q];
+#pragma unroll
+        for (int j = 0; j < NH * 4; ++j) vacc[j] = fmaf(bv[j], cq, vacc[j]);
       }
     }
-    if (blockIdx.x == 0 && t < K) {
-#pragma unroll 4
-      for (int q = 0; q < 32; ++q) vacc = fmaf(swb[q][t], scc[q], vacc);
-    }
   }
-  if (act) {
+  float* Mp = Mpart + ((int64_t)blockIdx.z * gridDim.y + b) * K * K;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float r[8];
+  for (int hi = 0; hi < NH; ++hi)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = acc[i][j];
-      st_vec<__nv_bfloat16, 8>(Mout + (int64_t)b * K * K + (int64_t)(rbase + rg * 4 + i) * K + cg * 8, r);
-    }
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int hj = 0; hj < NH; ++hj) {
+        const int r = tr * 4 + 64 * hi + i, c = tc * 4 + 64 * hj;
+        *reinterpret_cast<float4*>(Mp + (int64_t)r * K + c) =
+            make_float4(acc[4 * hi + i][4 * hj], acc[4 * hi + i][4 * hj + 1], acc[4 * hi + i][4 * hj + 2],
+                        acc[4 * hi + i][4 * hj + 3]);
+      }
+  if (tr == 0) {
+    float* vp = vpart + ((int64_t)blockIdx.z * gridDim.y + b) * K;
+#pragma unroll
+    for (int hj = 0; hj < NH; ++hj)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) vp[tc * 4 + 64 * hj + j] = vacc[4 * hj + j];
   }
-  if (blockIdx.x == 0 && t < K) v[(int64_t)b * K + t] = vacc;
+}
+constexpr int MV_SPLIT = 4;   // channel splits of k_lbm_mv (C >= 128: >= 32 channels each, 512 CTAs at B = 64)
+
+// M (bf16) and v from the MV_SPLIT partials, fixed order.
+__global__ void k_lbm_mv_sum(int B, int K, const float* __restrict__ Mpart, const float* __restrict__ vpart,
+                             __nv_bfloat16* __restrict__ Mout, float* __restrict__ v) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nm = (int64_t)B * K * K;
+  if (i < nm) {
+    float a = 0.f;
+#pragma unroll
+    for (int z = 0; z < MV_SPLIT; ++z) a += Mpart[z * nm + i];
+    Mout[i] = __float2bfloat16_rn(a);
+  }
+  if (i < (int64_t)B * K) {
+    float a = 0.f;
+#pragma unroll
+    for (int z = 0; z < MV_SPLIT; ++z) a += vpart[z * (int64_t)B * K + i];
+    v[i] = a;
+  }
 }
 
 // Sparse part of dX: dX[n*L + l] += sum over channels c with argmax(n, c) = l
@@ -888,7 +929,7 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // forward workspace: flipped W, per-cloud max / argmax, then the Gram call's own
 struct FwdWs {
-  size_t wf, mx, idx, lin, total;
+  size_t wf, mx, idx, gc, mu, lin, total;
 };
 FwdWs fwd_layout(int B, int64_t N, int64_t L, int64_t C, int64_t K) {
   FwdWs w{};
@@ -896,13 +937,15 @@ FwdWs fwd_layout(int B, int64_t N, int64_t L, int64_t C, int64_t K) {
   w.wf = o; o += al256((size_t)B * C * K * 2);
   w.mx = o; o += al256((size_t)B * N * C * 4);
   w.idx = o; o += al256((size_t)B * N * C * 4);
+  w.gc = o; o += al256((size_t)B * K * K * 4);
+  w.mu = o; o += al256((size_t)B * K * 8);
   w.lin = o; o += al256(hfta_fused_linear_bwd_workspace(B, N * L, K, K, HFTA_BF16));
   w.total = o;
   return w;
 }
 // backward workspace: coef, sp, M, v
 struct BwdWs {
-  size_t coef, sp, M, v, total;
+  size_t coef, sp, M, v, mp, vp, total;
 };
 BwdWs bwd_layout(int B, int64_t N, int64_t L, int64_t C, int64_t K) {
   BwdWs w{};
@@ -911,6 +954,8 @@ BwdWs bwd_layout(int B, int64_t N, int64_t L, int64_t C, int64_t K) {
   w.sp = o; o += al256((size_t)B * N * C * 4);
   w.M = o; o += al256((size_t)B * K * K * 2);
   w.v = o; o += al256((size_t)B * K * 4);
+  w.mp = o; o += al256((size_t)MV_SPLIT * B * K * K * 4);
+  w.vp = o; o += al256((size_t)MV_SPLIT * B * K * 4);
   w.total = o;
   return w;
 }
@@ -1008,22 +1053,25 @@ hfta_status hfta_fused_linear_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C,
     set_smem(k_lbm_stats<64>, stats_smem(64), attr_st64);
   }
   {
+    float* gc = reinterpret_cast<float*>(w + lay.gc);
+    double* mu = reinterpret_cast<double*>(w + lay.mu);
+    k_lbm_center<<<dim3((unsigned)cdiv(K * K, 256), (unsigned)B), 256, 0, s>>>((int)K, R, gram, xsum, gc, mu);
     const dim3 grid((unsigned)cdiv(C, ST_CH), (unsigned)B);
     const __nv_bfloat16* Wp = (const __nv_bfloat16*)W.ptr;
     const int64_t wbs = B > 1 ? W.bstride : 0;
     if (K == 128)
-      k_lbm_stats<128><<<grid, 256, stats_smem(128), s>>>(B, R, C, gram, xsum, Wp, wbs, W.ld, bias, bias_bstride,
+      k_lbm_stats<128><<<grid, 256, stats_smem(128), s>>>(B, R, C, gc, mu, Wp, wbs, W.ld, bias, bias_bstride,
                                                           running_mean, running_var, momentum, eps, save_mean,
                                                           save_invstd);
     else
-      k_lbm_stats<64><<<grid, 256, stats_smem(64), s>>>(B, R, C, gram, xsum, Wp, wbs, W.ld, bias, bias_bstride,
+      k_lbm_stats<64><<<grid, 256, stats_smem(64), s>>>(B, R, C, gc, mu, Wp, wbs, W.ld, bias, bias_bstride,
                                                         running_mean, running_var, momentum, eps, save_mean,
                                                         save_invstd);
   }
   k_lbm_fwd_fin<<<(unsigned)cdiv((int64_t)B * N * C, 256), 256, 0, s>>>(
       B, (int)N, C, mx, idx, bias, bias_bstride, gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha,
       (float*)G.ptr, G.bstride, G.ld, argmax, N * C, C, (float*)ext.ptr, ext.bstride, ext.ld);
-  count_launches(4);
+  count_launches(5);
   return post_launch(s, "hfta_fused_linear_bn_max_fwd");
 }
 
@@ -1066,7 +1114,13 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
       dbias, dbias_bstride, accumulate);
   int launches = 2;   // coef, dw
   if (dX.ptr) {
-    k_lbm_mv<<<dim3((unsigned)cdiv(K, MV_ROWS), (unsigned)B), 256, 0, s>>>(C, (int)K, Wp, wbs, W.ld, coef, M, v);
+    float* mp = reinterpret_cast<float*>(w + lay.mp);
+    float* vp = reinterpret_cast<float*>(w + lay.vp);
+    if (K == 128)
+      k_lbm_mv<128><<<dim3(1u, (unsigned)B, MV_SPLIT), 256, 0, s>>>(C, Wp, wbs, W.ld, coef, mp, vp);
+    else
+      k_lbm_mv<64><<<dim3(1u, (unsigned)B, MV_SPLIT), 256, 0, s>>>(C, Wp, wbs, W.ld, coef, mp, vp);
+    k_lbm_mv_sum<<<(unsigned)cdiv((int64_t)B * K * K, 256), 256, 0, s>>>(B, (int)K, mp, vp, M, v);
     // dX = X M^T + v (M symmetric), times act'(X) when X is an activation output
     GemmP p{};
     p.B = B; p.M = R; p.N = K; p.K = K;
@@ -1084,7 +1138,7 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
     k_lbm_sparse_dx<<<dim3((unsigned)N, (unsigned)B), SDX_T, 0, s>>>(
         (int)N, L, C, (int)K, end_bit, argmax, sp, Wp, wbs, W.ld, (__nv_bfloat16*)dX.ptr, dX.bstride, dX.ld,
         dX_act != HFTA_ACT_NONE ? (const __nv_bfloat16*)X.ptr : nullptr, X.bstride, X.ld, (int)dX_act, dX_alpha);
-    launches += 2;
+    launches += 3;
   }
   {
     static bool attr = false;
