@@ -52,6 +52,21 @@ struct TcArgs {
   int ab_same;                       // Gram X^T X (A == B, one 128-wide tile): B is read from the A stage
 };
 
+// Tile t -> (m-tile, n-tile, split, model) in 32-bit arithmetic (tile counts
+// fit easily; the int64 divisions cost ~150 instructions per tile per warp)
+__device__ __forceinline__ void tile_coords(uint32_t t, const TcArgs& p, int& mt, int& nt, int& split, int& b) {
+  uint32_t r = t;
+  const uint32_t tn = (uint32_t)p.tiles_n, tm = (uint32_t)p.tiles_m, sp = (uint32_t)p.splits;
+  if (p.order == 0) {
+    if (tn == 1) nt = 0; else { nt = (int)(r % tn); r /= tn; }
+    mt = (int)(r % tm); r /= tm;
+  } else {
+    mt = (int)(r % tm); r /= tm;
+    if (tn == 1) nt = 0; else { nt = (int)(r % tn); r /= tn; }
+  }
+  if (sp == 1) { split = 0; b = (int)r; } else { split = (int)(r % sp); b = (int)(r / sp); }
+}
+
 // BRES ("B resident", forward layers with K <= 128): the B operand (the
 // weight slice of one model / n-tile, <= 2 k-blocks) stays in shared memory
 // while the CTA sweeps consecutive m-tiles of the same (model, n-tile) --
@@ -148,12 +163,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       int64_t bkey = -1;
       uint32_t epoch = 0;
       for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-        int64_t r = t;
-        int mt, nt;
-        if (p.order == 0) { nt = (int)(r % p.tiles_n); r /= p.tiles_n; mt = (int)(r % p.tiles_m); r /= p.tiles_m; }
-        else { mt = (int)(r % p.tiles_m); r /= p.tiles_m; nt = (int)(r % p.tiles_n); r /= p.tiles_n; }
-        const int split = (int)(r % p.splits);
-        const int b = (int)(r / p.splits);
+        int mt, nt, split, b;
+        tile_coords((uint32_t)t, p, mt, nt, split, b);
         const int64_t kbeg = (int64_t)split * p.k_chunk;
         const int64_t kend = min(p.K, kbeg + p.k_chunk);
         const int nkb1 = (int)((kend - kbeg + BK - 1) / BK);
@@ -211,13 +222,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     int64_t bkey = -1;
     uint32_t epoch = 0;
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-      int64_t r = t;
-      int nt_ = 0;
-      if (p.order == 0) { nt_ = (int)(r % p.tiles_n); r /= p.tiles_n; r /= p.tiles_m; }
-      else { r /= p.tiles_m; nt_ = (int)(r % p.tiles_n); r /= p.tiles_n; }
-      const int split = (int)(r % p.splits);
+      int mt_, nt_, split, b_;
+      tile_coords((uint32_t)t, p, mt_, nt_, split, b_);
+      (void)mt_;
       if constexpr (BRES) {
-        const int bb_ = p.b_shared ? 0 : (int)(r / p.splits);
+        const int bb_ = p.b_shared ? 0 : b_;
         const int64_t key = (int64_t)bb_ * p.tiles_n + nt_;
         if (key != bkey) {
           if (bkey >= 0) tc_commit_w(bempty);   // old B free once all prior MMAs retire
@@ -277,12 +286,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const bool mask_smem = EPI == 2 && p.mask_kb >= 0;
     int64_t li = 0;                               // local tile ordinal
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++li) {
-      int64_t r = t;
-      int mt, nt;
-      if (p.order == 0) { nt = (int)(r % p.tiles_n); r /= p.tiles_n; mt = (int)(r % p.tiles_m); r /= p.tiles_m; }
-      else { mt = (int)(r % p.tiles_m); r /= p.tiles_m; nt = (int)(r % p.tiles_n); r /= p.tiles_n; }
-      const int split = (int)(r % p.splits);
-      const int b = (int)(r / p.splits);
+      int mt, nt, split, b;
+      tile_coords((uint32_t)t, p, mt, nt, split, b);
       int tile_nkb = 0;
       if (mask_smem) {
         const int64_t kbeg_ = (int64_t)split * p.k_chunk, kend_ = min(p.K, kbeg_ + p.k_chunk);
@@ -548,6 +553,7 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
     attr_set = true;
   }
   int64_t total = (int64_t)a.tiles_m * a.tiles_n * a.splits * a.B;
+  HFTA_REQUIRE(total < ((int64_t)1 << 31), HFTA_ERR_SHAPE, "gemm_tc: %lld tiles exceed int32", (long long)total);
   int grid = (int)std::min<int64_t>(total, num_sms());
   kern<<<grid, NTHREADS, SMEM, s>>>(ta, tb, tc_, ta2, tb2, a);
   count_launches(1);
