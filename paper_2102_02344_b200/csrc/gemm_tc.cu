@@ -52,6 +52,15 @@ struct TcArgs {
   int ab_same;                       // Gram X^T X (A == B, one 128-wide tile): B is read from the A stage
 };
 
+// (a, b) += (c, d) as one packed FADD2
+__device__ __forceinline__ void add_f32x2(float& a, float& b, float c, float d) {
+  unsigned long long x, y;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a), "f"(b));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(c), "f"(d));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(y));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x));
+}
+
 // Tile t -> (m-tile, n-tile, split, model) in 32-bit arithmetic (tile counts
 // fit easily; the int64 divisions cost ~150 instructions per tile per warp)
 __device__ __forceinline__ void tile_coords(uint32_t t, const TcArgs& p, int& mt, int& nt, int& split, int& b) {
@@ -397,7 +406,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
               for (int q = 0; q < 8; ++q) {             // smem broadcast
                 const float4 t4 = ld_shared_f4(sbias + (j * 64 + hh * 32 + 4 * q) * 4);
-                v[4 * q] += t4.x; v[4 * q + 1] += t4.y; v[4 * q + 2] += t4.z; v[4 * q + 3] += t4.w;
+                add_f32x2(v[4 * q], v[4 * q + 1], t4.x, t4.y);
+                add_f32x2(v[4 * q + 2], v[4 * q + 3], t4.z, t4.w);
               }
             } else if (brow) {
 #pragma unroll
@@ -405,7 +415,13 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 if (c0 + q < p.N) v[q] += brow[c0 + q];
             }
           }
-          if (EPI == 2 && mask_smem) {         // gating values = this tile's A operand, still resident in smem
+          // gating values = this tile's A operand, still resident in smem: per
+          // bf16 pair, gate = 0xFFFF where the (signed 16-bit) pattern is > 0
+          // (ReLU'), from two SIMD min/max and one multiply
+          uint32_t gate[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) gate[i] = 0xFFFFFFFFu;
+          if (EPI == 2 && mask_smem) {
             const int st = (estage + p.mask_kb + j) % STAGES;
             const uint32_t arow = smem_u32(smem + st * STAGE_BYTES) + (uint32_t)((quarter * 32 + lane) * 128);
 #pragma unroll
@@ -413,9 +429,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               const uint4 raw = ld_shared_u4(arow + (((uint32_t)(hh * 4 + q) ^ sw) << 4));
               const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {      // bf16 > 0 <=> sign bit clear and nonzero (ReLU')
-                v[8 * q + 2 * e] = (int32_t)(w4[e] << 16) > 0 ? v[8 * q + 2 * e] : 0.f;
-                v[8 * q + 2 * e + 1] = (int32_t)(w4[e] & 0xffff0000u) > 0 ? v[8 * q + 2 * e + 1] : 0.f;
+              for (int e = 0; e < 4; ++e) {
+                uint32_t t;
+                asm("max.s16x2 %0, %1, %2;" : "=r"(t) : "r"(w4[e]), "r"(0u));
+                asm("min.u16x2 %0, %1, %2;" : "=r"(t) : "r"(t), "r"(0x00010001u));
+                gate[4 * q + e] = t * 0xFFFFu;   // per half: 1 -> 0xFFFF, 0 -> 0
               }
             }
             if (last && hh == 1) {             // last read of this tile's A stages by this warp: release them
@@ -434,6 +452,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
 #pragma unroll
               for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+              if (EPI == 2) {
+                w4.x &= gate[4 * q]; w4.y &= gate[4 * q + 1]; w4.z &= gate[4 * q + 2]; w4.w &= gate[4 * q + 3];
+              }
               st_shared_v4(rowaddr + (((uint32_t)(hh * 4 + q) ^ sw) << 4), w4);
             }
             if (hh == 1) {
