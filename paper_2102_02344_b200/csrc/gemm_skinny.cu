@@ -11,6 +11,7 @@ namespace {
 
 constexpr int NT = 256;
 constexpr int KMAX = 8;
+constexpr int XTILE = 1024;   // rows of the narrow operand staged in smem per step
 
 // fwd, small K: C[m][n] = sum_k A[m][k] * Bw[n][k] + bias.  Thread = (row, VEC
 // columns) with its KT x VEC weights and VEC biases in registers (KT = K, a
@@ -27,12 +28,11 @@ __global__ void __launch_bounds__(NT) k_skinny_fwd(GemmP p, int tpr, int rpb, in
   __syncthreads();
   const int lane = threadIdx.x % tpr, rl = threadIdx.x / tpr;
   const int n0 = lane * VEC;
-  if (n0 >= N) return;
   float bias[VEC], sc[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    bias[v] = p.bias ? p.bias[(int64_t)b * p.bias_bs + n0 + v] : 0.f;
-    sc[v] = p.scale ? p.scale[(int64_t)b * p.scale_bs + n0 + v] : 1.f;   // fused BN apply: act(acc*sc + bias)
+    bias[v] = (p.bias && n0 + v < N) ? p.bias[(int64_t)b * p.bias_bs + n0 + v] : 0.f;
+    sc[v] = (p.scale && n0 + v < N) ? p.scale[(int64_t)b * p.scale_bs + n0 + v] : 1.f;   // fused BN apply
   }
   constexpr int KR = KT > 0 ? KT : 1;
   float wr[KR][VEC];
@@ -40,9 +40,40 @@ __global__ void __launch_bounds__(NT) k_skinny_fwd(GemmP p, int tpr, int rpb, in
 #pragma unroll
     for (int k = 0; k < KT; ++k)
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) wr[k][v] = w[k * N + n0 + v];
+      for (int v = 0; v < VEC; ++v) wr[k][v] = n0 + v < N ? w[k * N + n0 + v] : 0.f;
   }
   const int64_t r0 = blockIdx.x * rows_per_block, r1 = min(p.M, r0 + rows_per_block);
+  if constexpr (KT > 0) {
+    // the block's narrow input rows are staged through smem XTILE rows at a
+    // time (one cooperative copy), so the row loop only streams its stores
+    __shared__ float xs[XTILE * KT];
+    for (int64_t t0 = r0; t0 < r1; t0 += XTILE) {
+      const int nr = (int)min((int64_t)XTILE, r1 - t0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < nr * KT; i += NT) {
+        const int rr = i / KT, k = i - rr * KT;
+        xs[i] = ldf(A + (t0 + rr) * p.a_ld + k);
+      }
+      __syncthreads();
+      if (n0 >= N) continue;
+#pragma unroll 4
+      for (int rr = rl; rr < nr; rr += rpb) {
+        const int64_t m = t0 + rr;
+        float o[VEC];
+        const float* br = p.bias && p.bias_div > 0 ? p.bias + (int64_t)b * p.bias_bs + (m / p.bias_div) * p.bias_ld : nullptr;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          float acc = 0.f;
+#pragma unroll
+          for (int k = 0; k < KT; ++k) acc = fmaf(xs[rr * KT + k], wr[k][v], acc);
+          o[v] = act_fwd(fmaf(acc, sc[v], br ? br[n0 + v] : bias[v]), p.act, p.act_alpha);
+        }
+        st_vec<T, VEC>(C + m * p.c_ld + n0, o);
+      }
+    }
+    return;
+  }
+  if (n0 >= N) return;
 #pragma unroll 2
   for (int64_t m = r0 + rl; m < r1; m += rpb) {
     float a[KMAX];
@@ -53,14 +84,9 @@ __global__ void __launch_bounds__(NT) k_skinny_fwd(GemmP p, int tpr, int rpb, in
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       float acc = 0.f;
-      if constexpr (KT > 0) {
 #pragma unroll
-        for (int k = 0; k < KT; ++k) acc = fmaf(a[k], wr[k][v], acc);
-      } else {
-#pragma unroll
-        for (int k = 0; k < KMAX; ++k)
-          if (k < K) acc = fmaf(a[k], w[k * N + n0 + v], acc);
-      }
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) acc = fmaf(a[k], w[k * N + n0 + v], acc);
       o[v] = act_fwd(fmaf(acc, sc[v], br ? br[n0 + v] : bias[v]), p.act, p.act_alpha);
     }
     st_vec<T, VEC>(C + m * p.c_ld + n0, o);
@@ -193,20 +219,32 @@ __global__ void __launch_bounds__(NT) k_skinny_wgrad(GemmP p, int tpr, int rpb, 
   for (int v = 0; v < VEC; ++v)
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc[v][k] = 0.f;
-  if (n0 < N) {
+  {
+    // the narrow operand X (<= 3 columns) is staged through smem XTILE rows at
+    // a time (one cooperative copy): the row loop only streams dY
+    __shared__ float xs[XTILE * 3];
     const int64_t r0 = (int64_t)chunk * rows_per_chunk, r1 = min(p.K, r0 + rows_per_chunk);
+    for (int64_t t0 = r0; t0 < r1; t0 += XTILE) {
+      const int nr = (int)min((int64_t)XTILE, r1 - t0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < nr * 3; i += NT) {
+        const int rr = i / 3, k = i - rr * 3;
+        xs[i] = k < Ko ? ldf(X + (t0 + rr) * p.b_ld + k) : 0.f;
+      }
+      __syncthreads();
+      if (n0 >= N) continue;
 #pragma unroll 4
-    for (int64_t r = r0 + rl; r < r1; r += rpb) {
-      float dy[VEC];
-      ld_vec<T, VEC>(A + r * p.a_ld + n0, dy);
-      float x[3];
+      for (int rr = rl; rr < nr; rr += rpb) {
+        float dy[VEC];
+        ld_vec<T, VEC>(A + (t0 + rr) * p.a_ld + n0, dy);
+        const float x0 = xs[rr * 3], x1 = xs[rr * 3 + 1], x2 = xs[rr * 3 + 2];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) x[k] = k < Ko ? ldf(X + r * p.b_ld + k) : 0.f;
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) acc[v][k] = fmaf(dy[v], x[k], acc[v][k]);
-        acc[v][3] += dy[v];
+        for (int v = 0; v < VEC; ++v) {
+          acc[v][0] = fmaf(dy[v], x0, acc[v][0]);
+          acc[v][1] = fmaf(dy[v], x1, acc[v][1]);
+          acc[v][2] = fmaf(dy[v], x2, acc[v][2]);
+          acc[v][3] += dy[v];
+        }
       }
     }
   }
