@@ -200,6 +200,82 @@ __global__ void __launch_bounds__(NT) k_skinny_dgrad_row(GemmP p) {
   }
 }
 
+// dgrad, thread per row (bf16, K = 8 KB8): C[m][j] = sum_n A[m][n] W[n][j] (+ A2[m] M2
+// + bias, x mask) with W (and M2) broadcast from smem; each thread streams its
+// whole A row with KB8 independent 16-B loads, so no cross-lane reduction is
+// needed and every row's bytes are in flight at once.
+template <int KB8>
+__global__ void __launch_bounds__(NT) k_skinny_dgrad_rows(GemmP p) {
+  __shared__ float4 w[KB8 * 8];                        // w[n] = (W[n][0..3])
+  __shared__ float4 m2s[8];
+  const int b = blockIdx.y;
+  const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(p.A) + (int64_t)b * p.a_bs;
+  const __nv_bfloat16* Bw = reinterpret_cast<const __nv_bfloat16*>(p.Bm) + (int64_t)b * p.b_bs;
+  __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(p.C) + (int64_t)b * p.c_bs;
+  const int Nj = (int)p.N, K2 = (int)p.K2;
+  for (int n = threadIdx.x; n < KB8 * 8; n += NT) {
+    float e[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) e[j] = j < Nj ? ldf(Bw + (int64_t)n * p.b_ld + j) : 0.f;
+    w[n] = make_float4(e[0], e[1], e[2], e[3]);
+  }
+  if (K2 > 0 && threadIdx.x < K2) {
+    const float* M2 = reinterpret_cast<const float*>(p.Bm2) + (int64_t)b * p.b2_bs;
+    float e[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) e[j] = j < Nj ? M2[threadIdx.x * Nj + j] : 0.f;
+    m2s[threadIdx.x] = make_float4(e[0], e[1], e[2], e[3]);
+  }
+  float bj[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) bj[j] = (p.bias && j < Nj) ? p.bias[(int64_t)b * p.bias_bs + j] : 0.f;
+  __syncthreads();
+  const __nv_bfloat16* A2 = K2 > 0 ? reinterpret_cast<const __nv_bfloat16*>(p.A2) + (int64_t)b * p.a2_bs : nullptr;
+  const __nv_bfloat16* Mk = p.mask ? reinterpret_cast<const __nv_bfloat16*>(p.mask) + (int64_t)b * p.mask_bs : nullptr;
+  const float neg = p.mask_act == HFTA_ACT_LEAKY_RELU ? p.mask_alpha : 0.f;
+  for (int64_t m = blockIdx.x * (int64_t)NT + threadIdx.x; m < p.M; m += (int64_t)gridDim.x * NT) {
+    uint4 raw[KB8];
+    const uint4* ar = reinterpret_cast<const uint4*>(A + m * p.a_ld);
+#pragma unroll
+    for (int q = 0; q < KB8; ++q) raw[q] = __ldg(ar + q);
+    float xa[8], mk[4];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) xa[k] = k < K2 ? __bfloat162float(A2[m * p.a2_ld + k]) : 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) mk[j] = (Mk && j < Nj) ? __bfloat162float(Mk[m * p.mask_ld + j]) : 1.f;
+    float acc[4] = {bj[0], bj[1], bj[2], bj[3]};
+#pragma unroll
+    for (int q = 0; q < KB8; ++q) {
+      const uint32_t u4[4] = {raw[q].x, raw[q].y, raw[q].z, raw[q].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float lo, hi;
+        unpack_bf2(u4[e], lo, hi);
+        const float4 w0 = w[q * 8 + 2 * e], w1 = w[q * 8 + 2 * e + 1];
+        acc[0] = fmaf(lo, w0.x, acc[0]); acc[1] = fmaf(lo, w0.y, acc[1]);
+        acc[2] = fmaf(lo, w0.z, acc[2]); acc[3] = fmaf(lo, w0.w, acc[3]);
+        acc[0] = fmaf(hi, w1.x, acc[0]); acc[1] = fmaf(hi, w1.y, acc[1]);
+        acc[2] = fmaf(hi, w1.z, acc[2]); acc[3] = fmaf(hi, w1.w, acc[3]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k < K2) {
+        const float4 mv = m2s[k];
+        acc[0] = fmaf(xa[k], mv.x, acc[0]); acc[1] = fmaf(xa[k], mv.y, acc[1]);
+        acc[2] = fmaf(xa[k], mv.z, acc[2]); acc[3] = fmaf(xa[k], mv.w, acc[3]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j < Nj) {
+        const float vj = Mk ? acc[j] * (mk[j] > 0.f ? 1.f : neg) : acc[j];
+        C[m * p.c_ld + j] = __float2bfloat16_rn(vj);
+      }
+    }
+  }
+}
+
 // wgrad, small K-out: part[chunk][b][n][k] = sum_{rows in chunk} A(n, r) * Bx(k, r), both MN-major:
 // A = dY[r][n] (n < N), Bx = X[r][k] (k < K_out <= 3).  Thread = (row lane, VEC n-columns).
 // With p.colsum, a 4th column k = 3 accumulates sum_r A(n, r) (x = 1): the fused dbias.
@@ -454,6 +530,13 @@ hfta_status gemm_skinny(const GemmP& p, hfta_dtype dt, void* ws, size_t ws_bytes
     return post_launch(s, "gemm_skinny_fwd");
   }
   if (skinny_dgrad_ok(p)) {
+    if (bf && aligned16(p.A) && p.a_bs % 8 == 0 && p.a_ld % 8 == 0 && p.K2 <= 8 && (p.K == 64 || p.K == 128)) {
+      dim3 grid((unsigned)std::min<int64_t>(cdiv(p.M, NT), cdiv(32 * 148, p.B)), p.B);
+      if (p.K == 64) k_skinny_dgrad_rows<8><<<grid, NT, 0, s>>>(p);
+      else k_skinny_dgrad_rows<16><<<grid, NT, 0, s>>>(p);
+      count_launches(1);
+      return post_launch(s, "gemm_skinny_dgrad_rows");
+    }
     const bool v = aligned16(p.A) && (p.a_bs % 8 == 0);
     const int vec = v ? (bf ? 8 : 4) : 1;
     int tpr = 1;
