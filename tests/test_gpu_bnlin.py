@@ -99,6 +99,7 @@ def run(B, M, N, K, shared=False, gate=False, accumulate=0, seed=0):
 CASES = [  # B, M, N, K, shared, gate
     (3, 1000, 64, 3, True, False),       # STN c1: shared xyz input, no dX
     (2, 3000, 64, 3, False, False),      # feat c1: per-model transformed xyz, dX into xyz
+    (2, 1777, 128, 3, False, False),     # K = 3 -> N = 128: the 256-B-row dX kernel (16 x 16-B loads per row)
     (2, 2500, 128, 64, False, True),     # c2: K = 64 tensor cores, dX gated by the c1 ReLU
     (2, 1111, 128, 64, False, False),    # ragged M, ungated
     (2, 777, 64, 128, False, True),      # K = 128, N = 64
