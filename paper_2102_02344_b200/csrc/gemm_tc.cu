@@ -650,9 +650,10 @@ bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32) {
   }
   if (p.splits > 1 && p.k_chunk % BK) return false;
   // MN-major operands are loaded in 64-element boxes along MN; a ragged MN
-  // extent (multiple of 16) leaves the tail of the last box (or a whole second
-  // box) out of bounds, which TMA zero-fills.
-  if (!p.a_kmajor && (p.M % 16)) return false;
+  // extent leaves the tail of the last box (or a whole second box) out of
+  // bounds, which TMA zero-fills (the A side only feeds rows the epilogue
+  // clips; the B side stays at multiples of 16).
+
   if (!p.b_kmajor && (p.N % 16)) return false;
   return true;
 }

@@ -118,6 +118,30 @@ def test_linear_bf16_f32(M, N, K, B):
         assert_close(host(db[b]), dbb, 1e-5, "dbias")
 
 
+@pytest.mark.parametrize("N", [40, 50, 56])
+def test_linear_wgrad_ragged_rows_padded_ld(N):
+    """bf16 wgrad with an output-feature count that is not a multiple of 16
+    (the seg classifier: k = 50) and dY rows padded to a 16-B pitch: the
+    MN-major A tile of the tensor-core wgrad is partly out of bounds
+    (zero-filled by TMA).  dW, dbias vs the oracle on the same operands."""
+    B, M, K, ldy = 2, 3000, 128, 64
+    X = rounded(R.standard_normal((B, M, K)), torch.bfloat16)
+    W = rounded(R.standard_normal((B, N, K)) / np.sqrt(K), torch.bfloat16)
+    dY = np.zeros((B, M, ldy))
+    dY[:, :, :N] = rounded(R.standard_normal((B, M, N)), torch.bfloat16)
+    Xd, Wd, dYd = dev(X, torch.bfloat16), dev(W, torch.bfloat16), dev(dY, torch.bfloat16)
+    dW = torch.empty(B, N, K, device=DEV)
+    db = torch.empty(B, N, device=DEV)
+    ws = torch.empty(max(H.hfta_fused_linear_bwd_workspace(B, M, N, K, 1), 1), dtype=torch.uint8, device=DEV)
+    H.hfta_fused_linear_bwd(B, M, N, K, 1, H.tin(dYd, M * ldy, ldy), H.tin(Xd, M * K, K), H.tin(Wd, N * K, K),
+                            H.tout(None, 0, 1), H.ptr(dW), N * K, K, H.ptr(db), N, 0, H.ptr(ws), ws.numel(), s())
+    torch.cuda.synchronize()
+    for b in range(B):
+        _, dw, dbb = OL.linear_bwd(dY[b][:, :N], X[b], W[b])
+        assert_close(host(dW[b]), dw, 1e-5, "dW")
+        assert_close(host(db[b]), dbb, 1e-5, "dbias")
+
+
 def test_linear_bwd_accumulate_and_rowgroup_bias():
     B, M, N, K, L = 2, 500, 48, 32, 125
     X = R.standard_normal((B, M, K)).astype(np.float32).astype(np.float64)
