@@ -305,6 +305,30 @@ def test_dropout_mask_bit_exact(dt):
         assert_close(got, OL.dropout(X[b], keep, np.float32(p)), 1e-6 if dt == "f32" else 1e-2, "dropout")
 
 
+@pytest.mark.parametrize("K", [50, 40, 7])
+def test_loss_nll_padded_rows(K):
+    """bf16 NLL with 16-B padded rows (the seg classifier's layout, ld = 64):
+    the thread-per-row kernel; loss, mean and dlogits vs the oracle."""
+    B, rows, ld = 3, 1000, 64
+    Z = np.zeros((B, rows, ld))
+    Z[:, :, :K] = rounded(R.standard_normal((B, rows, K)) * 3, torch.bfloat16)
+    y = R.integers(0, K, rows)
+    loss, ml = torch.empty(B, device=DEV), torch.empty(1, device=DEV)
+    dZ = torch.zeros(B, rows, ld, dtype=torch.bfloat16, device=DEV)
+    ws = torch.empty(H.hfta_loss_workspace(B, rows), dtype=torch.uint8, device=DEV)
+    Zd, yd = dev(Z, torch.bfloat16), dev(y, torch.int32)
+    H.hfta_loss_nll(B, rows, K, 1, H.tin(Zd, rows * ld, ld), H.ptr(yd), 0, H.ptr(loss),
+                    H.ptr(ml), H.tout(dZ, rows * ld, ld), H.ptr(ws), ws.numel(), s())
+    torch.cuda.synchronize()
+    refs = []
+    for b in range(B):
+        l, dz = OL.nll_mean(Z[b][:, :K], y)
+        refs.append(l)
+        assert abs(host(loss)[b] - l) <= 1e-5 * abs(l)
+        assert_close(host(dZ[b])[:, :K], dz, 1e-2, "dlogits")
+    assert abs(host(ml)[0] - np.mean(refs)) <= 1e-5 * abs(np.mean(refs))
+
+
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
 def test_loss_nll_mse(dt):
     code, tdt = DT[dt]
