@@ -196,6 +196,41 @@ __global__ void k_act(int64_t rows, int64_t cols, int act, float alpha, const T*
   }
 }
 
+// dense rows (ld == cols): the tensor of each model is one flat run of n
+// elements, 8 bf16 per thread per 16-B access, no index arithmetic per element
+__device__ __forceinline__ float act_apply(float x, float d, int act, float alpha, int bwd) {
+  if (!bwd) {
+    if (act == HFTA_ACT_TANH) return tanhf(x);
+    if (act == HFTA_ACT_SIGMOID) return 1.f / (1.f + expf(-x));
+    return act_fwd(x, act, alpha);
+  }
+  if (act == HFTA_ACT_TANH) return d * (1.f - x * x);            // x is the output y
+  if (act == HFTA_ACT_SIGMOID) return d * x * (1.f - x);
+  return d * act_grad(x, act, alpha);
+}
+__global__ void k_act_flat(int64_t n8, int act, float alpha, const __nv_bfloat16* __restrict__ X, int64_t xbs,
+                           const __nv_bfloat16* __restrict__ D, int64_t dbs, __nv_bfloat16* __restrict__ Y,
+                           int64_t ybs, int bwd) {
+  const int b = blockIdx.y;
+  const uint4* x4 = reinterpret_cast<const uint4*>(X + b * xbs);
+  const uint4* d4 = bwd ? reinterpret_cast<const uint4*>(D + b * dbs) : nullptr;
+  uint4* y4 = reinterpret_cast<uint4*>(Y + b * ybs);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 xv = x4[i];
+    const uint4 dv = bwd ? d4[i] : make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t xs[4] = {xv.x, xv.y, xv.z, xv.w}, ds[4] = {dv.x, dv.y, dv.z, dv.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float xl, xh, dl, dh;
+      unpack_bf2(xs[e], xl, xh);
+      unpack_bf2(ds[e], dl, dh);
+      o[e] = pack_bf2(act_apply(xl, dl, act, alpha, bwd), act_apply(xh, dh, act, alpha, bwd));
+    }
+    y4[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 }  // namespace
 
 size_t colsum_ws(int B, int64_t rows, int64_t C, int64_t group) {
@@ -329,6 +364,16 @@ static hfta_status act_common(int B, int64_t rows, int64_t cols, hfta_dtype dt, 
   HFTA_REQUIRE((int)act >= 1 && (int)act <= 4, HFTA_ERR_UNSUPPORTED, "act: activation %d", (int)act);
   HFTA_REQUIRE(X.ld >= cols && Y.ld >= cols && (Y.bstride > 0 || B == 1), HFTA_ERR_SHAPE, "act: strides");
   cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = rows * cols;
+  if (dt == HFTA_BF16 && X.ld == cols && Y.ld == cols && (!bwd || D.ld == cols) && n % 8 == 0 &&
+      X.bstride % 8 == 0 && Y.bstride % 8 == 0 && (!bwd || D.bstride % 8 == 0) && aligned16(X.ptr) &&
+      aligned16(Y.ptr) && (!bwd || aligned16(D.ptr))) {
+    dim3 g((unsigned)std::min<int64_t>(cdiv(n / 8, 256), 4 * 148), B);
+    k_act_flat<<<g, 256, 0, s>>>(n / 8, (int)act, alpha, (const __nv_bfloat16*)X.ptr, X.bstride,
+                                 (const __nv_bfloat16*)D.ptr, D.bstride, (__nv_bfloat16*)Y.ptr, Y.bstride, bwd);
+    count_launches(1);
+    return post_launch(s, bwd ? "hfta_act_bwd" : "hfta_act_fwd");
+  }
   dim3 grid((unsigned)std::min<int64_t>(cdiv(rows * cols, 256), 4096), B);
   if (dt == HFTA_F32)
     k_act<float><<<grid, 256, 0, s>>>(rows, cols, (int)act, alpha, (const float*)X.ptr, X.bstride, X.ld,
