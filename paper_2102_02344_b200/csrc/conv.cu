@@ -35,15 +35,15 @@ __global__ void k_im2col(Geo2 g, const T* __restrict__ img, int64_t ibs, T* __re
   const T* I = img + (int64_t)b * ibs;
   T* O = col + (int64_t)b * cbs;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = i;
-    const int64_t c = (t % cv) * VEC; t /= cv;
-    const int kx = (int)(t % g.kw); t /= g.kw;
-    const int ky = (int)(t % g.kh); t /= g.kh;
+    uint32_t t = (uint32_t)i;                    // 32-bit index math (host guarantees total < 2^31)
+    const int64_t c = (int64_t)(t % (uint32_t)cv) * VEC; t /= (uint32_t)cv;
+    const int kx = (int)(t % (uint32_t)g.kw); t /= (uint32_t)g.kw;
+    const int ky = (int)(t % (uint32_t)g.kh); t /= (uint32_t)g.kh;
     const int64_t m = t;                         // (n, sy, sx)
-    const int64_t sx = t % g.Ws; t /= g.Ws;
-    const int64_t sy = t % g.Hs;
-    const int64_t n = t / g.Hs;
-    const int64_t by = sy * g.stride - g.pad + ky, bx = sx * g.stride - g.pad + kx;
+    const int sx = (int)(t % (uint32_t)g.Ws); t /= (uint32_t)g.Ws;
+    const int sy = (int)(t % (uint32_t)g.Hs);
+    const int64_t n = t / (uint32_t)g.Hs;
+    const int by = sy * g.stride - g.pad + ky, bx = sx * g.stride - g.pad + kx;
     float v[VEC];
     if (by >= 0 && by < g.Hb && bx >= 0 && bx < g.Wb) {
       ld_vec<T, VEC>(I + ((n * g.Hb + by) * g.Wb + bx) * g.C + c, v);
@@ -64,23 +64,23 @@ __global__ void k_col2im(Geo2 g, const T* __restrict__ col, int64_t cbs, int64_t
   const T* Cm = col + (int64_t)b * cbs;
   T* O = img + (int64_t)b * ibs;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t t = i;
-    const int64_t c = (t % cv) * VEC; t /= cv;
-    const int64_t bx = t % g.Wb; t /= g.Wb;
-    const int64_t by = t % g.Hb;
-    const int64_t n = t / g.Hb;
+    uint32_t t = (uint32_t)i;                    // 32-bit index math (host guarantees total < 2^31)
+    const int64_t c = (int64_t)(t % (uint32_t)cv) * VEC; t /= (uint32_t)cv;
+    const int bx = (int)(t % (uint32_t)g.Wb); t /= (uint32_t)g.Wb;
+    const int by = (int)(t % (uint32_t)g.Hb);
+    const int64_t n = t / (uint32_t)g.Hb;
     float acc[VEC];
 #pragma unroll
     for (int q = 0; q < VEC; ++q) acc[q] = 0.f;
     for (int ky = 0; ky < g.kh; ++ky) {               // fixed order: deterministic
-      const int64_t ty = by + g.pad - ky;
+      const int ty = by + g.pad - ky;
       if (ty < 0 || ty % g.stride) continue;
-      const int64_t sy = ty / g.stride;
+      const int sy = ty / g.stride;
       if (sy >= g.Hs) continue;
       for (int kx = 0; kx < g.kw; ++kx) {
-        const int64_t tx = bx + g.pad - kx;
+        const int tx = bx + g.pad - kx;
         if (tx < 0 || tx % g.stride) continue;
-        const int64_t sx = tx / g.stride;
+        const int sx = tx / g.stride;
         if (sx >= g.Ws) continue;
         float v[VEC];
         ld_vec<T, VEC>(Cm + ((n * g.Hs + sy) * g.Ws + sx) * cld + ((int64_t)ky * g.kw + kx) * g.C + c, v);
@@ -158,6 +158,10 @@ hfta_status make_shape(const hfta_conv_desc* d, Shape* sh) {
     s.Kc = (int64_t)d->kh * d->kw * d->C_out;
   }
   s.Ms = (int64_t)d->N * s.g.Hs * s.g.Ws;
+  // im2col / col2im index arithmetic is 32-bit per model
+  HFTA_REQUIRE(s.Ms * s.Kc < ((int64_t)1 << 31) && (int64_t)d->N * s.g.Hb * s.g.Wb * s.g.C < ((int64_t)1 << 31),
+               HFTA_ERR_SHAPE, "conv: %lld x %lld patch matrix per model exceeds 2^31 elements", (long long)s.Ms,
+               (long long)s.Kc);
   *sh = s;
   return HFTA_OK;
 }
