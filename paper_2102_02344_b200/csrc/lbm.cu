@@ -48,7 +48,7 @@ constexpr uint32_t WKB = CBLK * 64 * 2;        // one 64-wide k block of a 128-c
 // forward
 constexpr int FR = 128;                        // points per chunk (UMMA N): smem operand reads 8 KB / 64 MMA cycles
 constexpr int FG = 2;                          // channel blocks per unit: TMEM 2 x FG x FR = 512 columns
-constexpr int FSTAGES = 3;
+constexpr int FSTAGES = 4;
 constexpr int NBW = FG / 2;                    // channel blocks per epilogue warp
 constexpr int LPB = FR / 32;                   // 32-column TMEM loads per block and chunk
 static_assert(NBW == 1 && LPB == 4, "epilogue: one 128-channel block and four 32-column loads per warp and chunk");
