@@ -72,14 +72,17 @@ __global__ void k_col2im(Geo2 g, const T* __restrict__ col, int64_t cbs, int64_t
     float acc[VEC];
 #pragma unroll
     for (int q = 0; q < VEC; ++q) acc[q] = 0.f;
-    for (int ky = 0; ky < g.kh; ++ky) {               // fixed order: deterministic
+    // only the taps with (b + pad - k) % stride == 0 contribute: start at that
+    // residue and step by the stride (same ascending order: deterministic)
+    const int ky0 = (by + g.pad) % g.stride, kx0 = (bx + g.pad) % g.stride;
+    for (int ky = ky0; ky < g.kh; ky += g.stride) {
       const int ty = by + g.pad - ky;
-      if (ty < 0 || ty % g.stride) continue;
+      if (ty < 0) break;                              // ty decreases with ky
       const int sy = ty / g.stride;
       if (sy >= g.Hs) continue;
-      for (int kx = 0; kx < g.kw; ++kx) {
+      for (int kx = kx0; kx < g.kw; kx += g.stride) {
         const int tx = bx + g.pad - kx;
-        if (tx < 0 || tx % g.stride) continue;
+        if (tx < 0) break;
         const int sx = tx / g.stride;
         if (sx >= g.Ws) continue;
         float v[VEC];
