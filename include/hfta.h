@@ -379,9 +379,13 @@ hfta_status hfta_loss_nll(int B, int64_t rows, int64_t K, hfta_dtype dt, hfta_in
                           hfta_stream stream);
 /*
  * Sigmoid + BCE (DCGAN discriminator output, PyTorch BCELoss with its log clamp
- * at -100): p = sigmoid(z), l_b = -(1/rows) sum_r [y log p + (1-y) log(1-p)],
- * dz = (p - y)/rows (the BCELoss backward (p-y)/max(p(1-p),1e-12) times
- * sigmoid' p(1-p)).  Z, dZ dtype dt [B][rows] (ld = row stride); y scalar.
+ * at -100; reading R29): p = sigmoid(z),
+ * l_b = -(1/rows) sum_r [y max(log p, -100) + (1-y) max(log(1-p), -100)] with
+ * log p = -softplus(-z), log(1-p) = -softplus(z);
+ * dz = (p - y) q / max(q, 1e-12) / rows, q = p(1-p) = sigmoid(z) sigmoid(-z)
+ * (the BCELoss backward (p-y)/max(p(1-p),1e-12) times sigmoid' p(1-p)),
+ * evaluated from z so saturated logits keep their exact value.
+ * Z, dZ dtype dt [B][rows] (ld = row stride); y scalar.
  */
 hfta_status hfta_loss_bce_logits(int B, int64_t rows, hfta_dtype dt, hfta_in Z, float target, float* loss,
                                  float* mean_loss, hfta_out dZ, void* ws, size_t ws_bytes,

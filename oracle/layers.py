@@ -187,6 +187,32 @@ def bce_mean(p, y):
     return loss, dp
 
 
+def softplus(z):
+    """log(1 + e^z), written without overflow: max(z, 0) + log1p(e^-|z|)."""
+    return np.maximum(z, 0.0) + np.log1p(np.exp(-np.abs(z)))
+
+
+def bce_sigmoid_mean(z, y):
+    """The discriminator's Sigmoid -> BCELoss(mean) as a function of its
+    logit z (reading R29): with p = sigmoid(z), log p = -softplus(-z) and
+    log(1 - p) = -softplus(z) (identities), so
+
+      l = -mean(y * max(-softplus(-z), -100) + (1 - y) * max(-softplus(z), -100))
+
+    and, chaining BCELoss's backward dp = (p - y) / max(p (1 - p), 1e-12) with
+    sigmoid's dz = dp p (1 - p), dz = (p - y) q / max(q, 1e-12) / n with
+    q = p (1 - p) = sigmoid(z) sigmoid(-z).  Evaluated from z, the value is
+    the exact one for every z (computing p first saturates p to 1 at
+    z > ~37 in fp64)."""
+    sp_pos, sp_neg = softplus(z), softplus(-z)
+    loss = -(y * np.maximum(-sp_neg, -100.0) + (1.0 - y) * np.maximum(-sp_pos, -100.0)).mean()
+    p, pn = np.exp(-sp_neg), np.exp(-sp_pos)          # sigmoid(z), sigmoid(-z)
+    q = p * pn
+    pmy = np.where(y == 1.0, -pn, p - y)              # p - y, written as -sigmoid(-z) when y = 1
+    dz = pmy * q / np.maximum(q, 1e-12) / z.size
+    return loss, dz
+
+
 # ---------------------------------------------------------- Conv2d ----
 # App. B row Conv2d (P:L1262-1263); Fig. 3 (P:L904).  Definition written as a
 # sum over kernel taps, each tap one tensordot over input channels.

@@ -227,6 +227,7 @@ def gen_bwd(P, dimg, img, cache):
 
 
 def disc_fwd(P, S, newS, img):
+    """D forward; returns (sigmoid output [N], logit [N], cache)."""
     h = img
     cache = []
     for i, (s, p) in enumerate(D_LAYERS):
@@ -243,15 +244,17 @@ def disc_fwd(P, S, newS, img):
             h = Lr.leaky_relu(zz)
         else:
             cache.append((h, None, None))
+            logit = y.reshape(-1)
             h = Lr.sigmoid(y)
-    return h.reshape(-1), cache
+    return h.reshape(-1), logit, cache
 
 
-def disc_bwd(P, dout, out, cache, need_wgrad=True, need_dx=False):
-    """Backward through D from d(out) [N]; returns (dimg or None, grads)."""
+def disc_bwd(P, dlogit, cache, need_wgrad=True, need_dx=False):
+    """Backward through D from d(logit) [N] (the Sigmoid -> BCE gradient,
+    reading R29); returns (dimg or None, grads)."""
     G = {}
-    N = out.shape[0]
-    dy = Lr.sigmoid_bwd(dout, out).reshape(N, 1, 1, 1)
+    N = dlogit.shape[0]
+    dy = dlogit.reshape(N, 1, 1, 1)
     dh = None
     for i in range(4, -1, -1):
         s, p = D_LAYERS[i]
@@ -278,18 +281,18 @@ def dcgan_iteration(PG, PD, SG, SD, optG, optD, real, z, t, hp_b, hpD_b=None):
     newSD1, newSD2, newSD3, newSG = {}, {}, {}, {}
     N = real.shape[0]
     ones, zeros = np.ones(N), np.zeros(N)
-    out_r, cr = disc_fwd(PD, SD, newSD1, real)
-    errD_real, dout = Lr.bce_mean(out_r, ones)
-    _, GD_r = disc_bwd(PD, dout, out_r, cr)
+    out_r, zr, cr = disc_fwd(PD, SD, newSD1, real)
+    errD_real, dz = Lr.bce_sigmoid_mean(zr, ones)
+    _, GD_r = disc_bwd(PD, dz, cr)
     fake, cg = gen_fwd(PG, SG, newSG, z)
-    out_f, cf = disc_fwd(PD, newSD1, newSD2, fake)
-    errD_fake, dout = Lr.bce_mean(out_f, zeros)
-    _, GD_f = disc_bwd(PD, dout, out_f, cf)
+    out_f, zf, cf = disc_fwd(PD, newSD1, newSD2, fake)
+    errD_fake, dz = Lr.bce_sigmoid_mean(zf, zeros)
+    _, GD_f = disc_bwd(PD, dz, cf)
     GD = {k: GD_r[k] + GD_f[k] for k in GD_r}
     PD2, optD2 = adam_model(PD, GD, optD, t, hpD_b)
-    out_g, cg2 = disc_fwd(PD2, newSD2, newSD3, fake)
-    errG, dout = Lr.bce_mean(out_g, ones)
-    dfake, _ = disc_bwd(PD2, dout, out_g, cg2, need_wgrad=False, need_dx=True)
+    out_g, zg, cg2 = disc_fwd(PD2, newSD2, newSD3, fake)
+    errG, dz = Lr.bce_sigmoid_mean(zg, ones)
+    dfake, _ = disc_bwd(PD2, dz, cg2, need_wgrad=False, need_dx=True)
     GG = gen_bwd(PG, dfake, fake, cg)
     PG2, optG2 = adam_model(PG, GG, optG, t, hp_b)
     return dict(errD_real=errD_real, errD_fake=errD_fake, errG=errG, GD=GD, GG=GG,

@@ -3,6 +3,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "common.cuh"
 
@@ -31,6 +34,16 @@ hfta_status check_init() {
 
 int num_sms() { return g_sms.load(); }
 void count_launches(uint64_t n) { g_launches += n; }
+
+void set_max_smem(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, size_t>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.insert(std::make_tuple(kern, dev, bytes)).second)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
 
 hfta_status post_launch(cudaStream_t s, const char* what) {
   cudaError_t e = cudaGetLastError();

@@ -21,6 +21,12 @@ int num_sms();
 void count_launches(uint64_t n);
 // Call after every launch sequence: checks the launch status, honours HFTA_SYNC.
 hfta_status post_launch(cudaStream_t s, const char* what);
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device):
+// mutex-protected registry (safe from several host threads and devices).
+void set_max_smem(const void* kern, size_t bytes);
+template <typename K_> inline void ensure_smem(K_* kern, size_t bytes) {
+  set_max_smem(reinterpret_cast<const void*>(kern), bytes);
+}
 
 inline size_t dsize(hfta_dtype dt) { return dt == HFTA_BF16 ? 2 : 4; }
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }

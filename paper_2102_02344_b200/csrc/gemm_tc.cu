@@ -6,14 +6,16 @@
 // per-model GEMMs fill the 148 SMs (the paper's "horizontal fusion",
 // P:L856-857, done in the scheduler instead of by a grouped library call).
 //
-// Per CTA (1 per SM, 192 threads):
-//   warp 0      TMA producer: 3-D tensor maps [B][rows][cols] (bstride = dim 2),
-//               SWIZZLE_128B boxes of 64 elements (128 B) along the contiguous dim.
-//   warp 1      MMA issuer: one elected thread issues tcgen05.mma.kind::f16
-//               (bf16 x bf16 -> fp32 in TMEM), M=128, N=BN, K=16 per instruction.
-//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> bias / convert ->
-//               global stores (row per thread); double-buffered TMEM
-//               accumulators let the epilogue of tile i overlap the MMAs of i+1.
+// Per CTA (1 per SM, 576 threads = 18 warps):
+//   warp 0       TMA producer: 3-D tensor maps [B][rows][cols] (bstride = dim 2),
+//                SWIZZLE_128B boxes of 64 elements (128 B) along the contiguous dim.
+//   warp 1       MMA issuer: one elected thread issues tcgen05.mma.kind::f16
+//                (bf16 x bf16 -> fp32 in TMEM), M=128, N=BN, K=16 per instruction.
+//   warps 2..17  epilogue, two groups of 8 warps taking alternate tiles:
+//                tcgen05.ld 32x32b -> registers -> bias / BN apply / ReLU' gate ->
+//                bf16 SWIZZLE_128B smem staging + TMA store (or fp32 stores);
+//                double-buffered TMEM accumulators let the epilogue of tile i
+//                overlap the MMAs of i+1.
 // Operands: A(m,k), B(n,k) each K-major ([m][k], k contiguous) or MN-major
 // ([k][m], m contiguous); MN-major is what the dgrad (B = W) and wgrad
 // (A = dY, B = X) contractions need, read without a transpose pass.
@@ -421,6 +423,23 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           uint32_t gate[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) gate[i] = 0xFFFFFFFFu;
+          if (EPI == 2 && p.mask && !mask_smem && row_ok) {
+            // gating tensor from global memory (a tile's k-blocks do not all fit
+            // the ring, or the mask is not an operand): 32 bf16 = 4 x 16 B per row
+            const uint4* gp = reinterpret_cast<const uint4*>(p.mask + (int64_t)b * p.mask_bs + m * p.mask_ld + c0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 raw = (c0 + 8 * q < p.N) ? __ldg(gp + q) : make_uint4(0u, 0u, 0u, 0u);
+              const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                uint32_t t;
+                asm("max.s16x2 %0, %1, %2;" : "=r"(t) : "r"(w4[e]), "r"(0u));
+                asm("min.u16x2 %0, %1, %2;" : "=r"(t) : "r"(t), "r"(0x00010001u));
+                gate[4 * q + e] = t * 0xFFFFu;
+              }
+            }
+          }
           if (EPI == 2 && mask_smem) {
             const int st = (estage + p.mask_kb + j) % STAGES;
             const uint32_t arow = smem_u32(smem + st * STAGE_BYTES) + (uint32_t)((quarter * 32 + lane) * 128);
@@ -561,18 +580,18 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
                a.tiles_m == 1 && a.tiles_n == 1 && p.M == p.N) ? 1 : 0;
   // the gating tensor is the A operand itself (same rows, its columns = the
   // output's): read it from the resident A stage instead of global memory
-  if (EPI == 2 && p.mask && p.splits == 1 && p.N <= BN) {
+  // only if every k-block of a tile fits the ring at once (else the producer
+  // would wait on a stage the epilogue frees only after the accumulator is
+  // ready): otherwise the epilogue reads the gate from global memory
+  const bool fits = (int)(cdiv(p.K, BK) + (EPI == 2 ? cdiv(p.K2, BK) : 0)) <= STAGES;
+  if (EPI == 2 && p.mask && p.splits == 1 && p.N <= BN && fits) {
     if (p.K2 > 0 && p.mask == p.A2 && p.mask_bs == p.a2_bs && p.mask_ld == p.a2_ld && p.K2 == p.N)
       a.mask_kb = (int)cdiv(p.K, BK);
     else if (p.K2 == 0 && p.mask == p.A && p.mask_bs == p.a_bs && p.mask_ld == p.a_ld && p.K == p.N && p.a_kmajor)
       a.mask_kb = 0;
   }
   auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, BRES, EPI>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-    attr_set = true;
-  }
+  ensure_smem(kern, SMEM);
   int64_t total = (int64_t)a.tiles_m * a.tiles_n * a.splits * a.B;
   HFTA_REQUIRE(total < ((int64_t)1 << 31), HFTA_ERR_SHAPE, "gemm_tc: %lld tiles exceed int32", (long long)total);
   int grid = (int)std::min<int64_t>(total, num_sms());
@@ -586,9 +605,9 @@ bool epi1(const GemmP& p) { return p.scale && p.bias && p.bias_div == 0 && !p.ma
 bool epi2(const GemmP& p) {   // bias, second K segment, gating by the A operand (or A2) itself (ReLU'), N <= 128
   if (p.scale || p.act != HFTA_ACT_NONE || p.N > 128) return false;
   if (!p.mask) return true;
-  if (p.mask_act != HFTA_ACT_RELU) return false;
-  if (p.K2 > 0) return p.mask == p.A2 && p.mask_bs == p.a2_bs && p.mask_ld == p.a2_ld && p.K2 == p.N;
-  return p.mask == p.A && p.mask_bs == p.a_bs && p.mask_ld == p.a_ld && p.K == p.N;
+  // gating by relu'(mask), mask a bf16 [B][M][N] tensor (read from the resident
+  // A stage when it is the A / A2 operand and fits the ring, else from global)
+  return p.mask_act == HFTA_ACT_RELU && aligned16(p.mask) && (p.mask_ld * 2) % 16 == 0 && (p.mask_bs * 2) % 16 == 0;
 }
 
 template <bool A_MN, bool B_MN, bool OUT_F32>
@@ -619,19 +638,10 @@ hfta_status dispatch_bn(const GemmP& p, cudaStream_t s) {
   return launch_tc<A_MN, B_MN, 256, OUT_F32, false>(p, s);
 }
 
-bool env_disabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HFTA_DISABLE_TC");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
 }  // namespace
 
 bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32) {
-  if (env_disabled() || dt_in != HFTA_BF16) return false;
+  if (dt_in != HFTA_BF16) return false;
   if (needs_epi(p)) {
     if (out_f32 || p.splits != 1 || !p.a_kmajor || !p.b_kmajor || p.accumulate) return false;
     if (!epi1(p) && !epi2(p)) return false;

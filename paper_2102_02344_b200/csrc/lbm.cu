@@ -7,30 +7,32 @@
 // for all B models in one persistent launch per pass, WITHOUT materialising
 // the [B][R][C] pre-BN activation Y in HBM:
 //
-//  forward   k_lbm_fwd: Y^T chunks (channels on the TMEM lanes, points on the
-//            columns) are produced by tcgen05 into TMEM and reduced by the
-//            epilogue warps straight out of TMEM -- per (model, cloud,
-//            channel): sum Y, sum Y^2, and the extreme value + first index
-//            (max over l of act(gamma*xhat+beta) sits at max_l Y when
-//            gamma >= 0 and at min_l Y when gamma < 0; the sign is folded into
-//            a flipped copy of W so the epilogue always takes a max).
-//            k_lbm_fwd_fin combines the per-cloud moments (Chan et al.,
-//            fp64), writes mean/invstd/running statistics and the pooled
-//            output.  HBM traffic: X once (+ W, + B*N*C partials) instead of
-//            writing Y and reading it twice.
-//  backward  dY = gamma*invstd*(dZ - dbeta/R - xhat*dgamma/R) with dZ nonzero
-//            only at the argmax rows (dZ = act'(z) * dG there), i.e.
-//            dY[r][c] = bx_c * Y[r][c] + cc_c  (+ a_c*dz at r = argmax),
-//            an affine function of the recomputable Y.  k_lbm_dgrad
-//            (dX = dY W) and k_lbm_wgrad (dW = dY^T X) each recompute their
-//            Y^T tile in TMEM (tensor cores are idle otherwise: the layer is
-//            HBM-bound by 8x), transform it into a bf16 dY tile in shared
-//            memory (UMMA layout, argmax rows patched) and feed it straight
-//            back into tcgen05 -- dY never reaches HBM either.
+//  forward   Gram G = X^T X and s = X^T 1 of the layer input (the tcgen05
+//            wgrad kernel with fused column sums, X read once), k_lbm_flip
+//            (W' = sign(gamma) W, exact), k_lbm_fwd: Y'^T chunks (channels on
+//            the TMEM lanes, 128 points on the columns) produced by tcgen05
+//            into TMEM and reduced by the epilogue warps straight out of TMEM
+//            -- only the per-(model, cloud, channel) maximum of Y' and its
+//            first index (max over l of act(gamma*xhat+beta) sits at max_l Y
+//            when gamma >= 0 and at min_l Y when gamma < 0).  The batch
+//            statistics come from the Gram (reading R27): k_lbm_center forms
+//            Gc = G - s s^T / R in fp64, k_lbm_stats evaluates
+//            var_c = W_c Gc W_c^T / R and mean_c = W_c s / R + b_c, and
+//            k_lbm_fwd_fin writes mean/invstd/running statistics, the pooled
+//            output, the argmax and ext = Y at the argmax.
+//  backward  dZ is nonzero only at the argmax rows, so the BN backward is
+//            dY = bx Y + cc + S (per-channel affine in Y plus one entry per
+//            cloud and channel).  Substituting Y = X W^T gives, exactly,
+//            dX = X M + 1 v^T + S W  and  dW = diag(bx) W G + cc s^T + S^T X
+//            with M = W^T diag(bx) W, v = W^T cc (k_lbm_mv, k_lbm_mv_sum):
+//            one R x K x K tcgen05 GEMM (gated by relu' of the layer input in
+//            its epilogue), a deterministic sorted scatter of the sparse rows
+//            (k_lbm_sparse_dx) and a per-channel dW kernel with G in shared
+//            memory (k_lbm_dw).  Neither Y nor dY is ever formed.
 //
-// Roles per CTA (320 threads, 1 CTA/SM, persistent): warp 0 TMA producer,
-// warp 1 single-thread MMA issuer, warps 2..9 epilogue / transform (two per
-// TMEM lane quarter).
+// k_lbm_fwd roles per CTA (352 threads, 1 CTA/SM, persistent): warp 0 TMA
+// producer, warps 1 and 10 two token-passing tcgen05 issuers, warps 2..9
+// epilogue (two per TMEM lane quarter).
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -962,12 +964,7 @@ BwdWs bwd_layout(int B, int64_t N, int64_t L, int64_t C, int64_t K) {
 size_t bwd_ws(int B, int64_t N, int64_t L, int64_t C, int64_t K) { return bwd_layout(B, N, L, C, K).total; }
 
 template <typename K_>
-void set_smem(K_ kern, size_t bytes, bool& done) {
-  if (!done) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    done = true;
-  }
-}
+void set_smem(K_ kern, size_t bytes) { ensure_smem(kern, bytes); }
 
 hfta_status check_common(int B, int64_t N, int64_t L, int64_t C, int64_t K, hfta_dtype dt, hfta_in X, hfta_in W) {
   if (hfta_status st = check_init()) return st;
@@ -1041,17 +1038,11 @@ hfta_status hfta_fused_linear_bn_max_fwd(int B, int64_t N, int64_t L, int64_t C,
   a.mx = mx; a.idx = idx;
   const int64_t npairs = (int64_t)B * N;
   a.teams = (int)std::max<int64_t>(1, std::min<int64_t>(npairs, num_sms() / a.ngroups));
-  {
-    static bool attr = false;
-    set_smem(k_lbm_fwd, FWD_SMEM, attr);
-  }
+  set_smem(k_lbm_fwd, FWD_SMEM);
   k_lbm_fwd<<<a.teams * a.ngroups, FWD_LT, FWD_SMEM, s>>>(ta, tw, a);
   // 4. batch statistics from the Gram, 5. pooled outputs
-  {
-    static bool attr_st = false, attr_st64 = false;
-    set_smem(k_lbm_stats<128>, stats_smem(128), attr_st);
-    set_smem(k_lbm_stats<64>, stats_smem(64), attr_st64);
-  }
+  set_smem(k_lbm_stats<128>, stats_smem(128));
+  set_smem(k_lbm_stats<64>, stats_smem(64));
   {
     float* gc = reinterpret_cast<float*>(w + lay.gc);
     double* mu = reinterpret_cast<double*>(w + lay.mu);
@@ -1140,10 +1131,7 @@ hfta_status hfta_fused_linear_bn_max_bwd(int B, int64_t N, int64_t L, int64_t C,
         dX_act != HFTA_ACT_NONE ? (const __nv_bfloat16*)X.ptr : nullptr, X.bstride, X.ld, (int)dX_act, dX_alpha);
     launches += 3;
   }
-  {
-    static bool attr = false;
-    set_smem(k_lbm_dw, (size_t)128 * 128 * 4, attr);   // K <= 128
-  }
+  set_smem(k_lbm_dw, (size_t)128 * 128 * 4);   // K <= 128
   k_lbm_dw<<<dim3((unsigned)cdiv(C, 32), (unsigned)B), 256, (size_t)K * K * 4, s>>>(
       (int)N, L, C, (int)K, gram, xsum, Wp, wbs, W.ld, coef, argmax, sp, (const __nv_bfloat16*)X.ptr, X.bstride, X.ld, dW,
       dW_bstride, dW_ld, accumulate);

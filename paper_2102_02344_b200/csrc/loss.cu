@@ -164,9 +164,16 @@ __global__ void __launch_bounds__(NT) k_bce(int64_t rows, const T* __restrict__ 
     const float lp = fmaxf(-(sp_pos - z), -100.f);
     const float l1p = fmaxf(-sp_pos, -100.f);
     s -= y * lp + (1.f - y) * l1p;
-    const float p = 1.f / (1.f + expf(-z));
-    const float pq = p * (1.f - p);
-    const float g = (p - y) / fmaxf(pq, 1e-12f) * pq;                  // BCELoss backward x sigmoid'
+    // BCELoss backward x sigmoid' (reading R29): (p - y) q / max(q, 1e-12),
+    // q = p (1 - p) = sigmoid(z) sigmoid(-z), all from e = exp(-|z|) so that a
+    // saturated logit keeps its exact (tiny) q instead of rounding p to 1
+    const float e = expf(-fabsf(z));
+    const float ri = 1.f / (1.f + e);
+    const float sg_pos = z >= 0.f ? ri : e * ri;                       // sigmoid(z)
+    const float sg_neg = z >= 0.f ? e * ri : ri;                       // sigmoid(-z)
+    const float q = e * ri * ri;
+    const float pmy = (y == 1.f) ? -sg_neg : sg_pos - y;
+    const float g = q >= 1e-12f ? pmy : pmy * (q * 1e12f);
     stf(dZ + (int64_t)b * dbs + r * dld, g / (float)rows);
   }
   red[threadIdx.x] = s;

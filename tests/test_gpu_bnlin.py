@@ -103,6 +103,12 @@ CASES = [  # B, M, N, K, shared, gate
     (2, 2500, 128, 64, False, True),     # c2: K = 64 tensor cores, dX gated by the c1 ReLU
     (2, 1111, 128, 64, False, False),    # ragged M, ungated
     (2, 777, 64, 128, False, True),      # K = 128, N = 64
+    # gated two-segment dX whose tile has more k-blocks than the ring has
+    # stages (4 + 2 > 4, 6 + 1 > 6): the gate is read from global memory
+    # instead of the resident A stage (a hang before)
+    (2, 1300, 256, 128, False, True),
+    (2, 700, 384, 64, False, True),
+    (1, 500, 512, 128, False, True),
 ]
 
 

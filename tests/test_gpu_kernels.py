@@ -362,6 +362,32 @@ def test_loss_nll_mse(dt):
         assert_close(host(dA[b]), da, 1e-5 if dt == "f32" else 1e-2, "dA")
 
 
+@pytest.mark.parametrize("target", [1.0, 0.0])
+def test_loss_bce_saturated(target):
+    """Sigmoid + BCE on the logit (reading R29) vs oracle.layers.bce_sigmoid_mean,
+    including saturated logits (|z| = 20..150: q = p(1-p) below the 1e-12
+    BCELoss floor, log clamp at -100) and ordinary ones; fp32 in and out."""
+    B, rows = 3, 257
+    Z = (R.standard_normal((B, rows)) * 4).astype(np.float32).astype(np.float64)
+    sat = np.array([20.0, -20.0, 27.0, -27.0, 30.0, -30.0, 40.0, -40.0, 99.0, -101.0, 150.0, -150.0])
+    Z[:, :sat.size] = sat
+    loss, ml = torch.empty(B, device=DEV), torch.empty(1, device=DEV)
+    dZ = torch.empty(B, rows, device=DEV)
+    ws = torch.empty(H.hfta_loss_workspace(B, rows), dtype=torch.uint8, device=DEV)
+    Zd = dev(Z)
+    H.hfta_loss_bce_logits(B, rows, 0, H.tin(Zd, rows, 1), target, H.ptr(loss), H.ptr(ml),
+                           H.tout(dZ, rows, 1), H.ptr(ws), ws.numel(), s())
+    torch.cuda.synchronize()
+    for b in range(B):
+        l, dz = OL.bce_sigmoid_mean(Z[b], np.full(rows, target))
+        assert abs(host(loss)[b] - l) <= 1e-5 * abs(l), (b, host(loss)[b], l)
+        g = host(dZ[b])
+        assert_close(g, dz, 1e-5, "dz")
+        # the saturated entries one by one (relative, elementwise)
+        for i in range(sat.size):
+            assert abs(g[i] - dz[i]) <= 1e-5 * abs(dz[i]) + 1e-30, (Z[b, i], g[i], dz[i])
+
+
 @pytest.mark.parametrize("P,shadow", [(4672, True), (1001, False)])
 def test_fused_adam(P, shadow):
     B, T = 3, 4

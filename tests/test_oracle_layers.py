@@ -208,6 +208,61 @@ def test_loss_closed_forms():
     assert L.mse_mean(np.ones(3), np.ones(3))[0] == 0.0
 
 
+def test_bce_sigmoid_closed_forms_and_torch():
+    """Reading R29 pins: (i) wherever fp64 sigmoid is not saturated, the
+    logit form equals torch's Sigmoid -> BCELoss (fp64, autograd) -- loss and
+    gradient; (ii) closed forms at saturation: BCE(sigmoid(50), 0) = softplus(50)
+    = 50 + log1p(e^-50); BCE(sigmoid(150), 0) = 100 (the -100 clamp);
+    the gradient below the 1e-12 floor is (p - y) q / 1e-12 with
+    q = e^-|z| / (1 + e^-|z|)^2; BCE(sigmoid(0), 1) = ln 2."""
+    z = R.uniform(-12, 12, 40)      # torch's 1 - sigmoid(z) loses digits beyond
+    for y0 in (0.0, 1.0):
+        y = np.full(z.size, y0)
+        loss, dz = L.bce_sigmoid_mean(z, y)
+        zt = t(z).requires_grad_()
+        lt = F.binary_cross_entropy(torch.sigmoid(zt), t(y))
+        lt.backward()
+        assert loss == pytest.approx(lt.item(), rel=1e-10)
+        assert np.allclose(dz, zt.grad.numpy(), rtol=1e-7, atol=0)
+        fd_check(lambda: L.bce_sigmoid_mean(z, y)[0], z, dz)
+    l, _ = L.bce_sigmoid_mean(np.array([50.0]), np.array([0.0]))
+    assert l == pytest.approx(50.0 + math.log1p(math.exp(-50.0)), rel=1e-15)
+    l, d = L.bce_sigmoid_mean(np.array([150.0, -150.0]), np.array([0.0, 1.0]))
+    assert l == pytest.approx(100.0, rel=1e-15)
+    for zz, yy in ((30.0, 0.0), (-30.0, 1.0), (40.0, 0.0), (-35.0, 0.0)):
+        e = math.exp(-abs(zz))
+        q = e / (1 + e) ** 2
+        p = 1 / (1 + math.exp(-zz))
+        sig_neg = 1 / (1 + e) if zz < 0 else e / (1 + e)      # sigmoid(-z)
+        pmy = -sig_neg if yy == 1.0 else p - yy
+        _, d = L.bce_sigmoid_mean(np.array([zz]), np.array([yy]))
+        ref = pmy * q / max(q, 1e-12)
+        assert d[0] == pytest.approx(ref, rel=1e-12), (zz, yy, d[0], ref)
+    l, d = L.bce_sigmoid_mean(np.array([0.0]), np.array([1.0]))
+    assert l == pytest.approx(math.log(2), rel=1e-15) and d[0] == pytest.approx(-0.5, rel=1e-15)
+
+
+def test_philox_known_answers():
+    """oracle/philox.py against the Random123 known-answer vectors
+    (tests/golden/philox_kat.txt), the external pin of reading R14."""
+    import os
+    from oracle.philox import philox4x32_10
+    path = os.path.join(os.path.dirname(__file__), "golden", "philox_kat.txt")
+    n = 0
+    for line in open(path):
+        if not line.strip() or line.startswith("#"):
+            continue
+        f = line.split()
+        assert f[0] == "10"
+        ctr = [int(v, 16) for v in f[1:5]]
+        key = [int(v, 16) for v in f[5:7]]
+        want = [int(v, 16) for v in f[7:11]]
+        got = [int(np.asarray(w).item()) for w in philox4x32_10(ctr, key)]
+        assert got == want, (line, [hex(g) for g in got])
+        n += 1
+    assert n == 3
+
+
 def test_losses_vs_torch_and_fd():
     z, y = R.standard_normal((6, 10)), R.integers(0, 10, 6)
     loss, dz = L.nll_mean(z, y)

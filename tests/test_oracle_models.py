@@ -196,9 +196,39 @@ def test_fused_oracle_permutation_and_duplicates():
     assert ld[0] == ld[1]
 
 
-def test_loss_scaling_eq3_example():
-    # S:L264 / App. C Eq. 3: B=4, every l_b = 1 -> L = 1, scaled B*L = 4, and
-    # d(B*L)/d l_b = 1, i.e. per-model gradients are the serial ones.
-    losses = np.ones(4)
-    Lf = losses.mean()
-    assert Lf == 1.0 and 4 * Lf == 4.0
+def test_loss_scaling_eq3_fused_autograd():
+    """App. C Eq. 1-3 (sum over b = 0..B-1, reading R8): the
+    fused loss L = (1/B) sum_b l_b, scaled by B, has per-model gradients equal
+    to each model's serial gradient.  An independent fused formulation (torch
+    fp64 autograd over all B cfg1 models at once, one graph) is compared with
+    the oracle, which trains every model ALONE: gradients of B*L equal the
+    oracle's per-model gradients, and gradients of L are 1/B of them."""
+    B = 3
+    Ps = [synth.init_params("mlp_cfg1", 1000 + b) for b in range(B)]
+    x, T = synth.mlp_cfg1_batch(0)
+    tp = [{k: torch.tensor(v, requires_grad=True) for k, v in P.items()} for P in Ps]
+    xt, Tt = torch.tensor(x), torch.tensor(T)
+
+    def model_loss(P):
+        h = F.linear(xt, P["c1.W"], P["c1.b"])
+        h = F.relu(F.batch_norm(h, None, None, P["bn1.g"], P["bn1.beta"], training=True, eps=1e-5))
+        h = F.linear(h, P["c2.W"], P["c2.b"])
+        h = F.relu(F.batch_norm(h, None, None, P["bn2.g"], P["bn2.beta"], training=True, eps=1e-5))
+        return F.mse_loss(h, Tt)
+
+    losses = torch.stack([model_loss(P) for P in tp])
+    Lf = losses.mean()                                  # Eq. 1
+    (B * Lf).backward()                                 # Eq. 3's scaling
+    for b in range(B):
+        loss, G, _, _ = M.mlp_cfg1_loss_grads(Ps[b], {}, x, T)
+        assert losses[b].item() == pytest.approx(loss, rel=1e-12)
+        for k in G:
+            assert np.allclose(tp[b][k].grad.numpy(), G[k], rtol=1e-9, atol=1e-14), (b, k)
+    for P in tp:
+        for v in P.values():
+            v.grad = None
+    Lf2 = torch.stack([model_loss(P) for P in tp]).mean()
+    Lf2.backward()                                      # unscaled: 1/B of the serial gradient (Eq. 2)
+    loss, G, _, _ = M.mlp_cfg1_loss_grads(Ps[0], {}, x, T)
+    for k in G:
+        assert np.allclose(B * tp[0][k].grad.numpy(), G[k], rtol=1e-9, atol=1e-14), k
