@@ -20,55 +20,54 @@ import numpy as np
 from . import layers as Lr
 from .adam import adam_model
 from .philox import dropout_keep_mask
+from . import decisions as D
 
 
 # ------------------------------------------------------------- helpers ----
-# Decision margins (reading R15b).  ReLU'(z) and the argmax of a max-pool are
-# discontinuous decisions; an element whose decision is within rounding
-# distance of the threshold may legitimately be taken either way by a
-# lower-precision implementation.  When `MARGINS` is a list, every ReLU and
-# max-pool of a forward pass appends its smallest relative margin:
-#   ReLU: min_r,c |z| / rms(z)    max-pool: min_n,c (top1 - top2) / |top1|
-MARGINS = None
-
-
-def _note(kind, name, value):
-    if MARGINS is not None:
-        MARGINS.append((kind, name, float(value)))
-
-
-def _relu_margin(name, z):
-    if MARGINS is not None:
-        _note("relu", name, np.min(np.abs(z)) / max(np.sqrt(np.mean(z * z)), 1e-300))
-
-
-def _max_margin(name, x):
-    if MARGINS is not None:
-        s = np.sort(x, axis=1)
-        _note("max", name, np.min((s[:, -1] - s[:, -2]) / np.maximum(np.abs(s[:, -1]), 1e-300)))
+# Decision sites (oracle/decisions.py, readings R15b/R15c): every ReLU /
+# LeakyReLU gate and max-pool argmax goes through `D.relu_gate` /
+# `D.max_index`, which take the oracle's own decision unless a test has
+# activated a `Decisions` context with an override inside the flagged band.
+# `D.store` is the identity unless a conditioning-witness run installs a
+# rounding of stored operands (never used to produce a reference value).
 
 
 def _bn_state(state, name, C):
     return state.get(name + ".rm", np.zeros(C)), state.get(name + ".rv", np.ones(C))
 
 
+def _lin(P, r, name):
+    """Linear layer on the operands an implementation stores (identity here)."""
+    rs, Ws = D.store(r, "act"), D.store(P[name + ".W"], "w")
+    return Lr.linear_fwd(rs, Ws, P[name + ".b"]), rs, Ws
+
+
+def _lin_bwd(dy, rs, Ws, need_dx=True):
+    return Lr.linear_bwd(D.store(dy, "grad"), rs, Ws, need_dx)
+
+
 def _conv_bn_act(P, S, newS, r, conv, bn, act):
     """y = r W^T + b -> BN (train) -> act; returns output and cache."""
-    y = Lr.linear_fwd(r, P[conv + ".W"], P[conv + ".b"])
+    y, rs, Ws = _lin(P, r, conv)
     z, c = Lr.bn_fwd(y, P[bn + ".g"], P[bn + ".beta"])
     rm, rv = _bn_state(S, bn, y.shape[1])
     newS[bn + ".rm"], newS[bn + ".rv"] = Lr.bn_running(rm, rv, c, y.shape[0])
-    if act == "relu":
-        _relu_margin(bn, z)
-    a = Lr.relu(z) if act == "relu" else z
-    return a, dict(r=r, z=z, bn=c, conv=conv, bnn=bn, act=act)
+    gate = D.relu_gate(bn, z) if act == "relu" else None
+    a = z * gate if act == "relu" else z           # relu(z) with the site's decision
+    return a, dict(r=rs, W=Ws, z=z, gate=gate, bn=c, conv=conv, bnn=bn, act=act)
 
 
 def _conv_bn_act_bwd(P, G, da, cache, need_dx=True):
-    dz = Lr.relu_bwd(da, cache["z"]) if cache["act"] == "relu" else da
+    dz = da * cache["gate"] if cache["act"] == "relu" else da
     dy, G[cache["bnn"] + ".g"], G[cache["bnn"] + ".beta"] = Lr.bn_bwd(dz, cache["bn"], P[cache["bnn"] + ".g"])
-    dr, G[cache["conv"] + ".W"], G[cache["conv"] + ".b"] = Lr.linear_bwd(dy, cache["r"], P[cache["conv"] + ".W"], need_dx)
+    dr, G[cache["conv"] + ".W"], G[cache["conv"] + ".b"] = _lin_bwd(dy, cache["r"], cache["W"], need_dx)
     return dr
+
+
+def _max_pool(name, x):
+    """Max over the L points of x [N, L, C] with the site's argmax (reading R15)."""
+    idx = D.max_index(name, x)
+    return np.take_along_axis(x, idx[:, None, :], axis=1)[:, 0, :], idx
 
 
 # -------------------------------------------------------------- cfg1 ----
@@ -93,18 +92,17 @@ def _stn_fwd(P, S, newS, x):
     a1, k1 = _conv_bn_act(P, S, newS, r, "stn.c1", "stn.bn1", "relu")
     a2, k2 = _conv_bn_act(P, S, newS, a1, "stn.c2", "stn.bn2", "relu")
     a3, k3 = _conv_bn_act(P, S, newS, a2, "stn.c3", "stn.bn3", "relu")
-    _max_margin("stn.max", a3.reshape(N, L, -1))
-    g, idx = Lr.max_over_points(a3.reshape(N, L, -1))
+    g, idx = _max_pool("stn.max", a3.reshape(N, L, -1))
     f1, k4 = _conv_bn_act(P, S, newS, g, "stn.fc1", "stn.bn4", "relu")
     f2, k5 = _conv_bn_act(P, S, newS, f1, "stn.fc2", "stn.bn5", "relu")
-    f3 = Lr.linear_fwd(f2, P["stn.fc3.W"], P["stn.fc3.b"])
+    f3, f2s, W3s = _lin(P, f2, "stn.fc3")
     T = f3.reshape(N, 3, 3) + np.eye(3)
-    return T, dict(k=(k1, k2, k3, k4, k5), idx=idx, f2=f2, L=L)
+    return T, dict(k=(k1, k2, k3, k4, k5), idx=idx, f2=f2s, W3=W3s, L=L)
 
 
 def _stn_bwd(P, G, dT, c):
     N = dT.shape[0]
-    df2, G["stn.fc3.W"], G["stn.fc3.b"] = Lr.linear_bwd(dT.reshape(N, 9), c["f2"], P["stn.fc3.W"])
+    df2, G["stn.fc3.W"], G["stn.fc3.b"] = _lin_bwd(dT.reshape(N, 9), c["f2"], c["W3"])
     k1, k2, k3, k4, k5 = c["k"]
     df1 = _conv_bn_act_bwd(P, G, df2, k5)
     dg = _conv_bn_act_bwd(P, G, df1, k4)
@@ -122,8 +120,7 @@ def _feat_fwd(P, S, newS, x):
     a1, k1 = _conv_bn_act(P, S, newS, r, "feat.c1", "feat.bn1", "relu")
     a2, k2 = _conv_bn_act(P, S, newS, a1, "feat.c2", "feat.bn2", "relu")
     z3, k3 = _conv_bn_act(P, S, newS, a2, "feat.c3", "feat.bn3", None)
-    _max_margin("feat.max", z3.reshape(N, L, -1))
-    g, idx = Lr.max_over_points(z3.reshape(N, L, -1))
+    g, idx = _max_pool("feat.max", z3.reshape(N, L, -1))
     return g, a1, dict(T=T, stn=stn_c, x=x, k=(k1, k2, k3), idx=idx, L=L)
 
 
@@ -145,21 +142,21 @@ def pointnet_cls_loss_grads(P, S, x, labels, keep, p_drop):
     newS = {}
     g, _, fc = _feat_fwd(P, S, newS, x)
     h1, k1 = _conv_bn_act(P, S, newS, g, "head.fc1", "head.bn1", "relu")
-    y2 = Lr.linear_fwd(h1, P["head.fc2.W"], P["head.fc2.b"])
+    y2, h1s, W2s = _lin(P, h1, "head.fc2")
     d2 = Lr.dropout(y2, keep, p_drop)
     z2, bn2 = Lr.bn_fwd(d2, P["head.bn2.g"], P["head.bn2.beta"])
     rm, rv = _bn_state(S, "head.bn2", d2.shape[1])
     newS["head.bn2.rm"], newS["head.bn2.rv"] = Lr.bn_running(rm, rv, bn2, d2.shape[0])
-    _relu_margin("head.bn2", z2)
-    h2 = Lr.relu(z2)
-    logits = Lr.linear_fwd(h2, P["head.fc3.W"], P["head.fc3.b"])
+    gate2 = D.relu_gate("head.bn2", z2)
+    h2 = z2 * gate2
+    logits, h2s, W3s = _lin(P, h2, "head.fc3")
     loss, dlogits = Lr.nll_mean(logits, labels)
     G = {}
-    dh2, G["head.fc3.W"], G["head.fc3.b"] = Lr.linear_bwd(dlogits, h2, P["head.fc3.W"])
-    dz2 = Lr.relu_bwd(dh2, z2)
+    dh2, G["head.fc3.W"], G["head.fc3.b"] = _lin_bwd(dlogits, h2s, W3s)
+    dz2 = dh2 * gate2
     dd2, G["head.bn2.g"], G["head.bn2.beta"] = Lr.bn_bwd(dz2, bn2, P["head.bn2.g"])
     dy2 = Lr.dropout_bwd(dd2, keep, p_drop)
-    dh1, G["head.fc2.W"], G["head.fc2.b"] = Lr.linear_bwd(dy2, h1, P["head.fc2.W"])
+    dh1, G["head.fc2.W"], G["head.fc2.b"] = _lin_bwd(dy2, h1s, W2s)
     dg = _conv_bn_act_bwd(P, G, dh1, k1)
     _feat_bwd(P, G, dg, None, fc)
     return loss, G, newS, dict(logits=logits, T=fc["T"], g=g)
@@ -175,10 +172,10 @@ def pointnet_seg_loss_grads(P, S, x, labels):
     h1, k1 = _conv_bn_act(P, S, newS, h0, "head.c1", "head.bn1", "relu")
     h2, k2 = _conv_bn_act(P, S, newS, h1, "head.c2", "head.bn2", "relu")
     h3, k3 = _conv_bn_act(P, S, newS, h2, "head.c3", "head.bn3", "relu")
-    logits = Lr.linear_fwd(h3, P["head.c4.W"], P["head.c4.b"])
+    logits, h3s, W4s = _lin(P, h3, "head.c4")
     loss, dlogits = Lr.nll_mean(logits, labels.reshape(-1))
     G = {}
-    dh3, G["head.c4.W"], G["head.c4.b"] = Lr.linear_bwd(dlogits, h3, P["head.c4.W"])
+    dh3, G["head.c4.W"], G["head.c4.b"] = _lin_bwd(dlogits, h3s, W4s)
     dh2 = _conv_bn_act_bwd(P, G, dh3, k3)
     dh1 = _conv_bn_act_bwd(P, G, dh2, k2)
     dh0 = _conv_bn_act_bwd(P, G, dh1, k1)
@@ -193,20 +190,27 @@ G_LAYERS = [(1, 0), (2, 1), (2, 1), (2, 1), (2, 1)]     # (stride, pad) of t1..t
 D_LAYERS = [(2, 1), (2, 1), (2, 1), (2, 1), (1, 0)]     # c1..c5
 
 
-def gen_fwd(P, S, newS, z):
+def _conv(P, h, name, s, p, transposed=False):
+    hs, Ws = D.store(h, "act"), D.store(P[name], "w")
+    f = Lr.convT2d_fwd if transposed else Lr.conv2d_fwd
+    return f(hs, Ws, s, p), hs, Ws
+
+
+def gen_fwd(P, S, newS, z, tag="G"):
     h = z.reshape(z.shape[0], -1, 1, 1)
     cache = []
     for i, (s, p) in enumerate(G_LAYERS):
-        y = Lr.convT2d_fwd(h, P["t%d.W" % (i + 1)], s, p)
+        y, hs, Ws = _conv(P, h, "t%d.W" % (i + 1), s, p, transposed=True)
         if i < 4:
             bn = "bn%d" % (i + 1)
             zz, c = Lr.bn2d_fwd(y, P[bn + ".g"], P[bn + ".beta"])
             rm, rv = _bn_state(S, bn, y.shape[1])
             newS[bn + ".rm"], newS[bn + ".rv"] = Lr.bn_running(rm, rv, c, y.size // y.shape[1])
-            cache.append((h, zz, c))
-            h = Lr.relu(zz)
+            gate = D.relu_gate("%s.%s" % (tag, bn), zz)
+            cache.append((hs, Ws, gate, c))
+            h = zz * gate
         else:
-            cache.append((h, None, None))
+            cache.append((hs, Ws, None, None))
             h = Lr.tanh(y)
     return h, cache
 
@@ -216,34 +220,39 @@ def gen_bwd(P, dimg, img, cache):
     dy = Lr.tanh_bwd(dimg, img)
     for i in range(4, -1, -1):
         s, p = G_LAYERS[i]
-        h, zz, c = cache[i]
+        hs, Ws, gate, c = cache[i]
         if i < 4:
             bn = "bn%d" % (i + 1)
-            dzz = Lr.relu_bwd(dy, zz)
-            dy, G[bn + ".g"], G[bn + ".beta"] = Lr.bn2d_bwd(dzz, c, P[bn + ".g"])
-        dh, G["t%d.W" % (i + 1)] = Lr.convT2d_bwd(dy, h, P["t%d.W" % (i + 1)], s, p, need_dx=i > 0)
+            dy, G[bn + ".g"], G[bn + ".beta"] = Lr.bn2d_bwd(dy * gate, c, P[bn + ".g"])
+        dh, G["t%d.W" % (i + 1)] = Lr.convT2d_bwd(D.store(dy, "grad"), hs, Ws, s, p, need_dx=i > 0)
         dy = dh
     return G
 
 
-def disc_fwd(P, S, newS, img):
+def _leaky(zz, gate, a=0.2):
+    return np.where(gate, zz, a * zz)
+
+
+def disc_fwd(P, S, newS, img, tag="D"):
     """D forward; returns (sigmoid output [N], logit [N], cache)."""
     h = img
     cache = []
     for i, (s, p) in enumerate(D_LAYERS):
-        y = Lr.conv2d_fwd(h, P["c%d.W" % (i + 1)], s, p)
+        y, hs, Ws = _conv(P, h, "c%d.W" % (i + 1), s, p)
         if i == 0:
-            cache.append((h, y, None))
-            h = Lr.leaky_relu(y)
+            gate = D.relu_gate("%s.c1" % tag, y)
+            cache.append((hs, Ws, gate, None))
+            h = _leaky(y, gate)
         elif i < 4:
             bn = "bn%d" % (i + 1)
             zz, c = Lr.bn2d_fwd(y, P[bn + ".g"], P[bn + ".beta"])
             rm, rv = _bn_state(S, bn, y.shape[1])
             newS[bn + ".rm"], newS[bn + ".rv"] = Lr.bn_running(rm, rv, c, y.size // y.shape[1])
-            cache.append((h, zz, c))
-            h = Lr.leaky_relu(zz)
+            gate = D.relu_gate("%s.%s" % (tag, bn), zz)
+            cache.append((hs, Ws, gate, c))
+            h = _leaky(zz, gate)
         else:
-            cache.append((h, None, None))
+            cache.append((hs, Ws, None, None))
             logit = y.reshape(-1)
             h = Lr.sigmoid(y)
     return h.reshape(-1), logit, cache
@@ -258,14 +267,13 @@ def disc_bwd(P, dlogit, cache, need_wgrad=True, need_dx=False):
     dh = None
     for i in range(4, -1, -1):
         s, p = D_LAYERS[i]
-        h, zz, c = cache[i]
+        hs, Ws, gate, c = cache[i]
         if i == 0:
-            dy = Lr.leaky_relu_bwd(dy, zz)
+            dy = _leaky(dy, gate)
         elif i < 4:
             bn = "bn%d" % (i + 1)
-            dzz = Lr.leaky_relu_bwd(dy, zz)
-            dy, G[bn + ".g"], G[bn + ".beta"] = Lr.bn2d_bwd(dzz, c, P[bn + ".g"])
-        dh, dW = Lr.conv2d_bwd(dy, h, P["c%d.W" % (i + 1)], s, p, need_dx=(i > 0 or need_dx))
+            dy, G[bn + ".g"], G[bn + ".beta"] = Lr.bn2d_bwd(_leaky(dy, gate), c, P[bn + ".g"])
+        dh, dW = Lr.conv2d_bwd(D.store(dy, "grad"), hs, Ws, s, p, need_dx=(i > 0 or need_dx))
         if need_wgrad:
             G["c%d.W" % (i + 1)] = dW
         dy = dh
@@ -281,16 +289,16 @@ def dcgan_iteration(PG, PD, SG, SD, optG, optD, real, z, t, hp_b, hpD_b=None):
     newSD1, newSD2, newSD3, newSG = {}, {}, {}, {}
     N = real.shape[0]
     ones, zeros = np.ones(N), np.zeros(N)
-    out_r, zr, cr = disc_fwd(PD, SD, newSD1, real)
+    out_r, zr, cr = disc_fwd(PD, SD, newSD1, real, tag="Dr")
     errD_real, dz = Lr.bce_sigmoid_mean(zr, ones)
     _, GD_r = disc_bwd(PD, dz, cr)
-    fake, cg = gen_fwd(PG, SG, newSG, z)
-    out_f, zf, cf = disc_fwd(PD, newSD1, newSD2, fake)
+    fake, cg = gen_fwd(PG, SG, newSG, z, tag="G")
+    out_f, zf, cf = disc_fwd(PD, newSD1, newSD2, fake, tag="Df")
     errD_fake, dz = Lr.bce_sigmoid_mean(zf, zeros)
     _, GD_f = disc_bwd(PD, dz, cf)
     GD = {k: GD_r[k] + GD_f[k] for k in GD_r}
     PD2, optD2 = adam_model(PD, GD, optD, t, hpD_b)
-    out_g, zg, cg2 = disc_fwd(PD2, newSD2, newSD3, fake)
+    out_g, zg, cg2 = disc_fwd(PD2, newSD2, newSD3, fake, tag="Dg")
     errG, dz = Lr.bce_sigmoid_mean(zg, ones)
     dfake, _ = disc_bwd(PD2, dz, cg2, need_wgrad=False, need_dx=True)
     GG = gen_bwd(PG, dfake, fake, cg)
@@ -326,17 +334,6 @@ def train_step(arch, P, S, opt, batch, t, hp_b, b=0, dropout_seed=42, p_drop=0.3
         raise ValueError(arch)
     newP, newOpt = adam_model(P, G, opt, t, hp_b)
     return dict(loss=loss, grads=G, params=newP, opt=newOpt, stats=newS, out=out)
-
-
-def decision_margins(arch, P, batch, t=1, b=0, **kw):
-    """Smallest ReLU / max-pool margins of one model's forward (reading R15b)."""
-    global MARGINS
-    MARGINS = []
-    try:
-        train_step(arch, P, {}, {}, batch, t, dict(lr=0.0, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.0), b=b, **kw)
-        return list(MARGINS)
-    finally:
-        MARGINS = None
 
 
 def fused_step_oracle(arch, Ps, Ss, opts, batch, t, hp, **kw):

@@ -9,6 +9,7 @@ import torch
 import synth
 from oracle import models as OM
 from tests._cmp import TOL, relerr
+from tests import _decide as DE
 
 pytestmark = pytest.mark.gpu
 
@@ -21,17 +22,6 @@ pytestmark = pytest.mark.gpu
 # normwise.
 ZERO_REL = 1e-9
 
-# ReLU gates and max-pool argmaxes whose oracle margin is within rounding
-# distance may be decided either way by an fp32 implementation (reading R15b;
-# tools/amp_conditioning.py f32: rounding ONE layer's fp32 outputs moves the
-# downstream-in-backward gradients by ~4e-4).  Until the decision-override
-# comparison lands, per-tensor 1e-4 is gated on the tensors that precede every
-# dense ReLU decision in backward order, and the whole-model gradient on 2e-3.
-HEAD_SIDE_CLS = ("head.fc3.W", "head.fc3.b", "head.bn2.g", "head.bn2.beta", "head.fc2.W", "head.fc2.b",
-                 "head.bn1.g", "head.bn1.beta", "head.fc1.W")
-HEAD_SIDE_SEG = ("head.c4.W", "head.c4.b")                   # seg: the last (ReLU-free) per-point layer
-WHOLE_TOL = 1e-2
-
 
 @pytest.fixture(scope="module", autouse=True)
 def _init():
@@ -39,9 +29,13 @@ def _init():
     H.hfta_init(0)
 
 
-def run_pair(task, dtype, B, N, L, k, steps=1, widths=None, seed=0):
+def run_pair(task, dtype, B, N, L, k, steps=1, widths=None, seed=0, witness=None):
+    """GPU fused step(s) and, per model, the oracle re-run with the GPU's
+    decisions inside the oracle's own flagged band (tests/_decide.py).  The
+    bf16 witness (reading R28) is computed on the first step."""
     from paper_2102_02344_b200.pointnet import FusedPointNet
     arch = "pointnet_" + task
+    witness = (dtype == "bf16") if witness is None else witness
     specs = [(n, s) for n, s, _ in synth.param_specs(arch, k, widths)]
     Ps = [synth.init_params(arch, 1000 + b, k, widths) for b in range(B)]
     hp = synth.hparams_pointnet(7, B)
@@ -55,64 +49,81 @@ def run_pair(task, dtype, B, N, L, k, steps=1, widths=None, seed=0):
     out = []
     for t in range(1, steps + 1):
         loss = net.step(xd, yd).detach().cpu().numpy().copy()
-        res, losses, _ = OM.fused_step_oracle(arch, P, S, O, (x, y), t, hp)
+        torch.cuda.synchronize()
+        res = []
         for b in range(B):
-            res[b]["p_before"] = P[b]
-            res[b]["p_gpu_after"] = net.params(b)
-        out.append((loss, losses, [net.grads(b) for b in range(B)], res))
+            gpu = DE.pointnet_gpu_decisions(net, b)
+            r, report, rw = DE.oracle_with_decisions(arch, P[b], S[b], O[b], (x, y), t, OM.hp_of(hp, b), b, gpu,
+                                                     DE.MARGIN[dtype], L=L, witness=witness and t == 1)
+            r["p_before"] = P[b]
+            r["p_gpu_after"] = net.params(b)
+            r["report"] = report
+            r["zerr"] = DE.decision_errors(report["_ctx"], DE.pointnet_gpu_values(net, b))
+            r["witness"] = rw
+            res.append(r)
+        out.append((loss, np.array([r["loss"] for r in res]), [net.grads(b) for b in range(B)], res))
         P = [r["params"] for r in res]
         S = [r["stats"] for r in res]
         O = [r["opt"] for r in res]
-    torch.cuda.synchronize()
     return net, out
 
 
-def check_step(net, loss, ref_losses, grads, res, tol, B, grad_tol="same"):
-    """grad_tol: normwise gradient gate ("same" = tol, None = not gated)."""
-    grad_tol = tol if grad_tol == "same" else grad_tol
-    HEAD_SIDE = HEAD_SIDE_CLS if net.task == "cls" else HEAD_SIDE_SEG
+def check_step(net, loss, ref_losses, grads, res, dtype, B):
+    """Every per-model quantity of the step vs the decision-matched oracle:
+    loss; every gradient tensor (fp32: 1e-4 normwise; bf16: max(2e-2, 2 x the
+    bf16-storage witness of that tensor), reading R28); BN running mean and
+    variance of every layer; Adam m and v; the update on the elements whose
+    sign the oracle alone decides (reading R21)."""
+    tol = TOL[dtype]
+    worst = []
     for b in range(B):
+        r = res[b]
+        margin = DE.MARGIN[dtype]
+        for site, e in r["zerr"].items():      # the margin covers the GPU's decision-variable error
+            assert e <= margin, "model %d site %s: GPU z error %.3e exceeds the margin %.3e" % (b, site, e, margin)
         assert abs(loss[b] - ref_losses[b]) <= tol * abs(ref_losses[b]), (b, loss[b], ref_losses[b])
-        G = grads[b]
-        R = res[b]["grads"]
-        gmax = max(np.linalg.norm(v) for v in R.values())
-        for n in R:
-            if np.linalg.norm(R[n]) < ZERO_REL * gmax:
+        G, Rg = grads[b], r["grads"]
+        gmax = max(np.linalg.norm(v) for v in Rg.values())
+        gtol = {}
+        for n in Rg:
+            if np.linalg.norm(Rg[n]) < ZERO_REL * gmax:
                 assert np.linalg.norm(G[n]) <= 1e-1 * tol * gmax, "model %d grad %s not ~0" % (b, n)
                 continue
-            if grad_tol is None:
-                continue
-            e = relerr(G[n], R[n])
-            if n in HEAD_SIDE:
-                assert e <= grad_tol, "model %d grad %s: %.3e" % (b, n, e)
-        if grad_tol is not None:
-            live = [n for n in R if np.linalg.norm(R[n]) >= ZERO_REL * gmax]
-            e = relerr(np.concatenate([G[n].ravel() for n in live]), np.concatenate([R[n].ravel() for n in live]))
-            assert e <= WHOLE_TOL, "model %d whole-model gradient: %.3e" % (b, e)
-        # after the Adam step: whole-model normwise (reading R21)
-        # After the Adam step (reading R21): with Adam every update is bounded by
-        # lr (|m_hat / (sqrt(v_hat) + eps)| <= 1 at t = 1), and its value is unique
-        # only where the gradient is well above rounding noise.  Gate: the update
-        # Delta p normwise on elements with |g'_ref| > 0.1 rms(g'_ref), g' = g + wd p (decided
-        # by the oracle alone), every element within 2 lr_b of the oracle.
-        pb = res[b]["p_gpu_after"]
-        p0 = res[b]["p_before"]
-        lr = float(net.hv.t["lr"][b].item())
+            gtol[n] = tol
+            if dtype == "bf16":
+                w = relerr(r["witness"]["grads"][n], Rg[n])
+                gtol[n] = max(tol, 2.0 * w)
+            e = relerr(G[n], Rg[n])
+            worst.append((e / gtol[n], e, gtol[n], b, n))
+            assert e <= gtol[n], "model %d grad %s: %.3e > %.3e" % (b, n, e, gtol[n])
+        for name in net.bn_names:
+            rm, rv = (t[b].cpu().numpy() for t in net.running[name])
+            assert relerr(rm, r["stats"][name + ".rm"]) <= tol, (b, name, "running_mean")
+            assert relerr(rv, r["stats"][name + ".rv"]) <= tol, (b, name, "running_var")
+        m_gpu = {n: net.arena.host_tensor("m", n)[b] for n in gtol}
+        v_gpu = {n: net.arena.host_tensor("v", n)[b] for n in gtol}
+        for n in gtol:
+            m_ref, v_ref = r["opt"][n]
+            assert relerr(m_gpu[n], m_ref) <= gtol[n] * 1.01 + 1e-6, (b, n, "exp_avg")
+            assert relerr(v_gpu[n], v_ref) <= 2.0 * gtol[n] * 1.01 + 1e-6, (b, n, "exp_avg_sq")
+        pb, p0 = r["p_gpu_after"], r["p_before"]
         wd = float(net.hv.t["wd"][b].item())
-        for n in R:
-            d = np.max(np.abs(pb[n] - res[b]["params"][n]))
-            assert d <= 2 * lr * (1 + 1e-3) + 1e-6, "model %d param %s moved %.3e > 2 lr" % (b, n, d)
-            g = R[n] + wd * p0[n]            # what Adam normalises (coupled L2 decay)
+        for n in gtol:
+            g = Rg[n] + wd * p0[n]            # what Adam normalises (coupled L2 decay)
             rms = np.sqrt(np.mean(g * g))
-            mask = np.abs(g) > 1e-1 * rms
-            if rms < ZERO_REL * gmax or not mask.any():
+            mask = np.abs(g) > (1e-1 if dtype == "f32" else 5e-1) * rms
+            if not mask.any():
                 continue
-            e = relerr((pb[n] - p0[n])[mask], (res[b]["params"][n] - p0[n])[mask])
-            if n in HEAD_SIDE and grad_tol is not None:
-                assert e <= tol, "model %d update of %s: %.3e" % (b, n, e)
-
-
-GRAD_TOL = {"f32": "same", "bf16": None}
+            e = relerr((pb[n] - p0[n])[mask], (r["params"][n] - p0[n])[mask])
+            assert e <= gtol[n], "model %d update of %s: %.3e" % (b, n, e)
+    worst.sort(reverse=True)
+    print("\n[%s] worst gradient errors (err / gate): %s" % (dtype, " ".join(
+        "%s:%.2e/%.1e" % (n, e, g) for _, e, g, b, n in worst[:6])))
+    for b in range(B):
+        rep = {k: v for k, v in res[b]["report"].items() if not k.startswith("_")}
+        print("  model %d decisions (flagged/size, flips): %s" % (b, " ".join(
+            "%s:%d/%d,%d" % (k, v["flagged"], v["size"], v["flips"]) for k, v in rep.items())))
+        print("  model %d max z error / rms: %s" % (b, " ".join("%s:%.1e" % kv for kv in res[b]["zerr"].items())))
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
@@ -120,12 +131,7 @@ def test_pointnet_cls_step_small(dtype):
     B, N, L, k = 3, 32, 50, 40
     net, out = run_pair("cls", dtype, B, N, L, k)
     loss, ref, grads, res = out[0]
-    check_step(net, loss, ref, grads, res, TOL[dtype], B, GRAD_TOL[dtype])
-    # BN running statistics of every layer
-    for b in range(B):
-        for name in net.bn_names:
-            rm = net.running[name][0][b].cpu().numpy()
-            assert relerr(rm, res[b]["stats"][name + ".rm"]) <= TOL[dtype], name
+    check_step(net, loss, ref, grads, res, dtype, B)
 
 
 def test_pointnet_cls_two_steps_f32():
@@ -135,7 +141,7 @@ def test_pointnet_cls_two_steps_f32():
     B, N, L, k = 2, 32, 50, 10
     net, out = run_pair("cls", "f32", B, N, L, k, steps=2)
     loss, ref, grads, res = out[0]
-    check_step(net, loss, ref, grads, res, TOL["f32"], B)
+    check_step(net, loss, ref, grads, res, "f32", B)
     loss, ref, grads, res = out[1]
     for b in range(B):
         assert abs(loss[b] - ref[b]) <= 1e-3 * abs(ref[b])
@@ -164,11 +170,11 @@ def test_pointnet_cls_duplicate_models_bitwise():
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_pointnet_cls_step_full_size(dtype):
     """BJ configs[1] shapes (N=32, L=2500, k=40) with B=2; the oracle takes
-    ~25 s per model."""
+    ~10-20 s per model and pass."""
     B, N, L, k = 2, 32, 2500, 40
     net, out = run_pair("cls", dtype, B, N, L, k)
     loss, ref, grads, res = out[0]
-    check_step(net, loss, ref, grads, res, TOL[dtype], B, GRAD_TOL[dtype])
+    check_step(net, loss, ref, grads, res, dtype, B)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
@@ -178,16 +184,13 @@ def test_pointnet_seg_step_small(dtype):
     B, N, L, k = 3, 8, 300, 50
     net, out = run_pair("seg", dtype, B, N, L, k)
     loss, ref, grads, res = out[0]
-    check_step(net, loss, ref, grads, res, TOL[dtype], B, GRAD_TOL[dtype])
-    for b in range(B):
-        for name in net.bn_names:
-            rm = net.running[name][0][b].cpu().numpy()
-            assert relerr(rm, res[b]["stats"][name + ".rm"]) <= TOL[dtype], name
+    check_step(net, loss, ref, grads, res, dtype, B)
 
 
-def test_pointnet_seg_step_full_points_f32():
-    """seg at the BJ point count (L = 2500) with N = 4 clouds, B = 2."""
-    B, N, L, k = 2, 4, 2500, 50
-    net, out = run_pair("seg", "f32", B, N, L, k)
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_pointnet_seg_step_full_size(dtype):
+    """seg at BJ configs[2] shapes (N = 32, L = 2500, k = 50), B = 2."""
+    B, N, L, k = 2, 32, 2500, 50
+    net, out = run_pair("seg", dtype, B, N, L, k)
     loss, ref, grads, res = out[0]
-    check_step(net, loss, ref, grads, res, TOL["f32"], B, GRAD_TOL["f32"])
+    check_step(net, loss, ref, grads, res, dtype, B)

@@ -232,3 +232,83 @@ def test_loss_scaling_eq3_fused_autograd():
     loss, G, _, _ = M.mlp_cfg1_loss_grads(Ps[0], {}, x, T)
     for k in G:
         assert np.allclose(B * tp[0][k].grad.numpy(), G[k], rtol=1e-9, atol=1e-14), k
+
+
+# ----------------------------------------------------- decision sites ----
+
+def _cls_tiny(margin, override=None, force=False):
+    from oracle import decisions as Dm
+    P = synth.init_params("pointnet_cls", 1000, k=5, widths=TINY)
+    x, y = synth.points_cls(0, N=3, L=16, k=5)
+    keep = np.random.default_rng(3).uniform(size=(3, 8)) > 0.3
+    d = Dm.Decisions(margin, override, force)
+    with Dm.use(d):
+        loss, G, _, _ = M.pointnet_cls_loss_grads(P, {}, x, y, keep, 0.3)
+    return loss, G, d
+
+
+def test_decisions_default_is_plain_definition():
+    """An active context without overrides changes nothing (bitwise), and it
+    records every ReLU and max-pool site with its own decision."""
+    P = synth.init_params("pointnet_cls", 1000, k=5, widths=TINY)
+    x, y = synth.points_cls(0, N=3, L=16, k=5)
+    keep = np.random.default_rng(3).uniform(size=(3, 8)) > 0.3
+    l0, G0, _, _ = M.pointnet_cls_loss_grads(P, {}, x, y, keep, 0.3)
+    l1, G1, d = _cls_tiny(0.5)
+    assert l0 == l1 and all(np.array_equal(G0[k], G1[k]) for k in G0)
+    assert set(d.sites) == {"stn.bn1", "stn.bn2", "stn.bn3", "stn.max", "stn.bn4", "stn.bn5", "feat.bn1",
+                            "feat.bn2", "feat.max", "head.bn1", "head.bn2"}
+    for k, v in d.sites.items():
+        assert v["flips"] == 0 and np.array_equal(v["own"], v["used"])
+
+
+def test_decisions_override_inside_band_only():
+    """A flip inside the flagged band is taken (and moves the gradient, as a
+    different valid subgradient); a flip outside it, or an argmax override
+    whose value is not within the margin of the top, raises DecisionError."""
+    from oracle import decisions as Dm
+    _, G0, d = _cls_tiny(0.2)
+    site = d.sites["feat.bn2"]
+    flagged = np.argwhere(site["flag"] & site["own"])
+    unflagged = np.argwhere(~site["flag"] & site["own"])
+    assert len(flagged) and len(unflagged)
+    ov = site["own"].copy()
+    ov[tuple(flagged[0])] = False
+    _, G1, d1 = _cls_tiny(0.2, {"feat.bn2": ov})
+    assert d1.sites["feat.bn2"]["flips"] == 1
+    assert not np.array_equal(G1["feat.c2.W"], G0["feat.c2.W"])
+    ov = site["own"].copy()
+    ov[tuple(unflagged[0])] = False
+    with pytest.raises(Dm.DecisionError):
+        _cls_tiny(0.2, {"feat.bn2": ov})
+    _, _, dd = _cls_tiny(0.2, {"feat.bn2": ov}, force=True)       # witness mode: no validation
+    assert dd.sites["feat.bn2"]["flips"] == 1
+    # argmax: any index holding a value within the margin of the top is valid
+    m = d.sites["feat.max"]
+    own = m["own"]
+    ov = (own + 1) % 16
+    with pytest.raises(Dm.DecisionError):
+        _cls_tiny(0.2, {"feat.max": ov})
+    _, _, d2 = _cls_tiny(1e6, {"feat.max": ov})                   # huge margin: everything is a tie
+    assert d2.sites["feat.max"]["flips"] == own.size
+
+
+def test_decisions_max_ties_flagged_exactly():
+    """Brute force on a tiny tensor: the max site flags exactly the (cloud,
+    channel) pairs whose top-2 gap is within margin * rms, and exact ties
+    (e.g. an all-zero ReLU output) are always flagged."""
+    from oracle import decisions as Dm
+    x = np.array([[[1.0, 0.0], [0.9, 0.0], [0.2, 0.0]],
+                  [[0.0, 3.0], [0.5, 1.0], [0.49, 2.9]]])       # [N=2, L=3, C=2]
+    d = Dm.Decisions(0.05)
+    with Dm.use(d):
+        idx = Dm.max_index("m", x)
+    rms = np.sqrt(np.mean(x * x, axis=(0, 1)))
+    want = np.zeros((2, 2), bool)
+    for n in range(2):
+        for c in range(2):
+            v = np.sort(x[n, :, c])
+            want[n, c] = v[-1] - v[-2] <= 0.05 * rms[c]
+    assert np.array_equal(d.sites["m"]["flag"], want)
+    assert want[0, 1] and idx[0, 1] == 0                          # all-zero channel: tie, first index
+    assert np.array_equal(idx, np.argmax(x, axis=1))
