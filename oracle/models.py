@@ -36,10 +36,17 @@ def _bn_state(state, name, C):
     return state.get(name + ".rm", np.zeros(C)), state.get(name + ".rv", np.ones(C))
 
 
+def _bn_err_scale(y, c, gamma):
+    """Magnitude of an implementation's rounding error in z = BN(y) per
+    channel: |gamma| rms(y) invstd (decision sites only, reading R15c)."""
+    axes = tuple(i for i in range(y.ndim) if i != 1)
+    return np.abs(gamma) * np.sqrt(np.mean(y * y, axis=axes)) * c["invstd"]
+
+
 def _lin(P, r, name):
     """Linear layer on the operands an implementation stores (identity here)."""
-    rs, Ws = D.store(r, "act"), D.store(P[name + ".W"], "w")
-    return Lr.linear_fwd(rs, Ws, P[name + ".b"]), rs, Ws
+    rs, Ws = D.store(r, "act", name), D.store(P[name + ".W"], "w", name)
+    return D.store(Lr.linear_fwd(rs, Ws, P[name + ".b"]), "out", name), rs, Ws
 
 
 def _lin_bwd(dy, rs, Ws, need_dx=True):
@@ -52,9 +59,10 @@ def _conv_bn_act(P, S, newS, r, conv, bn, act):
     z, c = Lr.bn_fwd(y, P[bn + ".g"], P[bn + ".beta"])
     rm, rv = _bn_state(S, bn, y.shape[1])
     newS[bn + ".rm"], newS[bn + ".rv"] = Lr.bn_running(rm, rv, c, y.shape[0])
-    gate = D.relu_gate(bn, z) if act == "relu" else None
+    esc = _bn_err_scale(y, c, P[bn + ".g"])
+    gate = D.relu_gate(bn, z, esc) if act == "relu" else None
     a = z * gate if act == "relu" else z           # relu(z) with the site's decision
-    return a, dict(r=rs, W=Ws, z=z, gate=gate, bn=c, conv=conv, bnn=bn, act=act)
+    return a, dict(r=rs, W=Ws, z=z, gate=gate, bn=c, conv=conv, bnn=bn, act=act, esc=esc)
 
 
 def _conv_bn_act_bwd(P, G, da, cache, need_dx=True):
@@ -64,9 +72,9 @@ def _conv_bn_act_bwd(P, G, da, cache, need_dx=True):
     return dr
 
 
-def _max_pool(name, x):
+def _max_pool(name, x, scale=None):
     """Max over the L points of x [N, L, C] with the site's argmax (reading R15)."""
-    idx = D.max_index(name, x)
+    idx = D.max_index(name, x, scale)
     return np.take_along_axis(x, idx[:, None, :], axis=1)[:, 0, :], idx
 
 
@@ -92,7 +100,7 @@ def _stn_fwd(P, S, newS, x):
     a1, k1 = _conv_bn_act(P, S, newS, r, "stn.c1", "stn.bn1", "relu")
     a2, k2 = _conv_bn_act(P, S, newS, a1, "stn.c2", "stn.bn2", "relu")
     a3, k3 = _conv_bn_act(P, S, newS, a2, "stn.c3", "stn.bn3", "relu")
-    g, idx = _max_pool("stn.max", a3.reshape(N, L, -1))
+    g, idx = _max_pool("stn.max", a3.reshape(N, L, -1), k3["esc"])
     f1, k4 = _conv_bn_act(P, S, newS, g, "stn.fc1", "stn.bn4", "relu")
     f2, k5 = _conv_bn_act(P, S, newS, f1, "stn.fc2", "stn.bn5", "relu")
     f3, f2s, W3s = _lin(P, f2, "stn.fc3")
@@ -120,7 +128,7 @@ def _feat_fwd(P, S, newS, x):
     a1, k1 = _conv_bn_act(P, S, newS, r, "feat.c1", "feat.bn1", "relu")
     a2, k2 = _conv_bn_act(P, S, newS, a1, "feat.c2", "feat.bn2", "relu")
     z3, k3 = _conv_bn_act(P, S, newS, a2, "feat.c3", "feat.bn3", None)
-    g, idx = _max_pool("feat.max", z3.reshape(N, L, -1))
+    g, idx = _max_pool("feat.max", z3.reshape(N, L, -1), k3["esc"])
     return g, a1, dict(T=T, stn=stn_c, x=x, k=(k1, k2, k3), idx=idx, L=L)
 
 
@@ -147,7 +155,7 @@ def pointnet_cls_loss_grads(P, S, x, labels, keep, p_drop):
     z2, bn2 = Lr.bn_fwd(d2, P["head.bn2.g"], P["head.bn2.beta"])
     rm, rv = _bn_state(S, "head.bn2", d2.shape[1])
     newS["head.bn2.rm"], newS["head.bn2.rv"] = Lr.bn_running(rm, rv, bn2, d2.shape[0])
-    gate2 = D.relu_gate("head.bn2", z2)
+    gate2 = D.relu_gate("head.bn2", z2, _bn_err_scale(d2, bn2, P["head.bn2.g"]))
     h2 = z2 * gate2
     logits, h2s, W3s = _lin(P, h2, "head.fc3")
     loss, dlogits = Lr.nll_mean(logits, labels)
@@ -191,9 +199,9 @@ D_LAYERS = [(2, 1), (2, 1), (2, 1), (2, 1), (1, 0)]     # c1..c5
 
 
 def _conv(P, h, name, s, p, transposed=False):
-    hs, Ws = D.store(h, "act"), D.store(P[name], "w")
+    hs, Ws = D.store(h, "act", name), D.store(P[name], "w", name)
     f = Lr.convT2d_fwd if transposed else Lr.conv2d_fwd
-    return f(hs, Ws, s, p), hs, Ws
+    return D.store(f(hs, Ws, s, p), "out", name), hs, Ws
 
 
 def gen_fwd(P, S, newS, z, tag="G"):
@@ -206,7 +214,7 @@ def gen_fwd(P, S, newS, z, tag="G"):
             zz, c = Lr.bn2d_fwd(y, P[bn + ".g"], P[bn + ".beta"])
             rm, rv = _bn_state(S, bn, y.shape[1])
             newS[bn + ".rm"], newS[bn + ".rv"] = Lr.bn_running(rm, rv, c, y.size // y.shape[1])
-            gate = D.relu_gate("%s.%s" % (tag, bn), zz)
+            gate = D.relu_gate("%s.%s" % (tag, bn), zz, _bn_err_scale(y, c, P[bn + ".g"]))
             cache.append((hs, Ws, gate, c))
             h = zz * gate
         else:
@@ -248,7 +256,7 @@ def disc_fwd(P, S, newS, img, tag="D"):
             zz, c = Lr.bn2d_fwd(y, P[bn + ".g"], P[bn + ".beta"])
             rm, rv = _bn_state(S, bn, y.shape[1])
             newS[bn + ".rm"], newS[bn + ".rv"] = Lr.bn_running(rm, rv, c, y.size // y.shape[1])
-            gate = D.relu_gate("%s.%s" % (tag, bn), zz)
+            gate = D.relu_gate("%s.%s" % (tag, bn), zz, _bn_err_scale(y, c, P[bn + ".g"]))
             cache.append((hs, Ws, gate, c))
             h = _leaky(zz, gate)
         else:

@@ -14,6 +14,15 @@ namespace hfta {
 namespace {
 
 constexpr int NT = 256;
+
+// Pre-activation z = a*x + c of a BN column, a = gamma*invstd,
+// c = beta - mean*a: ONE fp32 rounding order shared by every forward and
+// backward kernel, so the act'(z) decision recomputed in backward is
+// bit-identical to the one the forward took (reading R15c).
+__device__ __forceinline__ void bn_affine(float ga, float be, float m, float is, float& a, float& c) {
+  a = ga * is;
+  c = fmaf(-m, a, be);
+}
 constexpr int UNRM = 1;     // max-over-points: rows in flight per thread (loop-carried max)
 constexpr int UNR = 1;      // rows per thread per iteration (UNR=4 measured slower: 76-150 regs cut occupancy)
 
@@ -58,15 +67,20 @@ Geo make_geo(int B, int64_t R, int64_t C, int vec, int bps = 0) {
 template <typename T, int VEC>
 __global__ void __launch_bounds__(NT) k_bn_stats(int64_t R, int64_t C, const T* __restrict__ X,
                                                  int64_t xbs, int64_t ld, Geo g,
-                                                 float* __restrict__ p1, float* __restrict__ p2) {
-  __shared__ float s1[NT * VEC], s2[NT * VEC];
+                                                 double* __restrict__ p1, double* __restrict__ p2) {
+  // fp64 accumulation: a thread sums ~R / (chunks * rows per block) shifted
+  // values; in fp32 that sequential sum's error (~n u |x - shift|) reached
+  // 5e-5 of a channel's spread at R = 80 000 and moved the BN output z
+  // (reading R15c); fp64 adds are free in this HBM-bound pass
+  __shared__ double s1[NT * VEC], s2[NT * VEC];
   const int b = blockIdx.z, chunk = blockIdx.y;
   const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
   const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
   const T* Xb = X + (int64_t)b * xbs;
-  float a1[VEC], a2[VEC], sh[VEC];
+  double a1[VEC], a2[VEC];
+  float sh[VEC];
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) { a1[v] = 0.f; a2[v] = 0.f; sh[v] = 0.f; }
+  for (int v = 0; v < VEC; ++v) { a1[v] = 0.0; a2[v] = 0.0; sh[v] = 0.f; }
   if (c0 < C) {
     ld_vec<T, VEC>(Xb + c0, sh);
     const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
@@ -81,9 +95,9 @@ __global__ void __launch_bounds__(NT) k_bn_stats(int64_t R, int64_t C, const T* 
         if (r + u * g.rpb < r1) {
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
-            float d = x[u][v] - sh[v];
+            const double d = (double)(x[u][v] - sh[v]);       // exact for |x - shift| within 2^24 ulps
             a1[v] += d;
-            a2[v] = fmaf(d, d, a2[v]);
+            a2[v] = fma(d, d, a2[v]);
           }
         }
     }
@@ -97,7 +111,7 @@ __global__ void __launch_bounds__(NT) k_bn_stats(int64_t R, int64_t C, const T* 
   for (int col = threadIdx.x; col < g.cb; col += NT) {
     int64_t c = (int64_t)blockIdx.x * g.cb + col;
     if (c >= C) continue;
-    float t1 = 0.f, t2 = 0.f;
+    double t1 = 0.0, t2 = 0.0;
     for (int r = 0; r < g.rpb; ++r) { t1 += s1[r * g.cb + col]; t2 += s2[r * g.cb + col]; }
     int64_t o = ((int64_t)b * g.chunks + chunk) * C + c;
     p1[o] = t1;
@@ -107,7 +121,7 @@ __global__ void __launch_bounds__(NT) k_bn_stats(int64_t R, int64_t C, const T* 
 
 template <typename T>
 __global__ void k_bn_finalize(int B, int64_t R, int64_t C, const T* __restrict__ X, int64_t xbs, int chunks,
-                              const float* __restrict__ p1, const float* __restrict__ p2, float eps,
+                              const double* __restrict__ p1, const double* __restrict__ p2, float eps,
                               float momentum, float* __restrict__ rmean, float* __restrict__ rvar,
                               float* __restrict__ smean, float* __restrict__ sinv) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -144,8 +158,7 @@ __global__ void __launch_bounds__(NT) k_bn_apply(int64_t R, int64_t C, const T* 
   for (int v = 0; v < VEC; ++v) {
     float m = smean[(int64_t)b * C + c0 + v], is = sinv[(int64_t)b * C + c0 + v];
     float ga = gamma[(int64_t)b * gbs + c0 + v], be = beta[(int64_t)b * gbs + c0 + v];
-    sc[v] = ga * is;
-    sf[v] = be - m * ga * is;
+    bn_affine(ga, be, m, is, sc[v], sf[v]);
   }
   const T* Xb = X + (int64_t)b * xbs + c0;
   T* Yb = Y + (int64_t)b * ybs + c0;
@@ -173,21 +186,21 @@ __global__ void __launch_bounds__(NT, 3) k_bn_bwd_reduce(int64_t R, int64_t C, c
                                                          const float* __restrict__ beta, int64_t gbs,
                                                          const float* __restrict__ smean,
                                                          const float* __restrict__ sinv, int act, float alpha, Geo g,
-                                                         float* __restrict__ p1, float* __restrict__ p2) {
-  __shared__ float s1[NT * VEC], s2[NT * VEC];
+                                                         double* __restrict__ p1, double* __restrict__ p2) {
+  __shared__ double s1[NT * VEC], s2[NT * VEC];
   const int b = blockIdx.z, chunk = blockIdx.y;
   const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
   const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
-  float a1[VEC], a2[VEC];
+  double a1[VEC], a2[VEC];          // fp64 sums (as k_bn_stats): dbeta / dgamma can cancel
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) { a1[v] = 0.f; a2[v] = 0.f; }
+  for (int v = 0; v < VEC; ++v) { a1[v] = 0.0; a2[v] = 0.0; }
   if (c0 < C) {
     float ka[VEC], kc[VEC], m[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       m[v] = smean[(int64_t)b * C + c0 + v];
-      ka[v] = gamma[(int64_t)b * gbs + c0 + v] * sinv[(int64_t)b * C + c0 + v];
-      kc[v] = beta[(int64_t)b * gbs + c0 + v] - m[v] * ka[v];
+      bn_affine(gamma[(int64_t)b * gbs + c0 + v], beta[(int64_t)b * gbs + c0 + v], m[v],
+                sinv[(int64_t)b * C + c0 + v], ka[v], kc[v]);
     }
     const T* Xb = X + (int64_t)b * xbs;
     const T* Db = dY + (int64_t)b * dbs;
@@ -200,8 +213,8 @@ __global__ void __launch_bounds__(NT, 3) k_bn_bwd_reduce(int64_t R, int64_t C, c
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         const float dz = d[v] * act_grad(fmaf(ka[v], x[v], kc[v]), act, alpha);
-        a1[v] += dz;
-        a2[v] = fmaf(dz, x[v] - m[v], a2[v]);
+        a1[v] += (double)dz;
+        a2[v] = fma((double)dz, (double)(x[v] - m[v]), a2[v]);
       }
     }
   }
@@ -214,7 +227,7 @@ __global__ void __launch_bounds__(NT, 3) k_bn_bwd_reduce(int64_t R, int64_t C, c
   for (int col = threadIdx.x; col < g.cb; col += NT) {
     int64_t c = (int64_t)blockIdx.x * g.cb + col;
     if (c >= C) continue;
-    float t1 = 0.f, t2 = 0.f;
+    double t1 = 0.0, t2 = 0.0;
     for (int r = 0; r < g.rpb; ++r) { t1 += s1[r * g.cb + col]; t2 += s2[r * g.cb + col]; }
     int64_t o = ((int64_t)b * g.chunks + chunk) * C + c;
     p1[o] = t1;
@@ -226,8 +239,8 @@ __global__ void __launch_bounds__(NT, 3) k_bn_bwd_reduce(int64_t R, int64_t C, c
 // gradient arena) and the apply-pass constants in ws (5 x [B][C]):
 // A = gamma*invstd, Bx = -A*invstd*dgamma/R, Cc = A*(mean*invstd*dgamma/R - dbeta/R),
 // ka = gamma*invstd, kc = beta - mean*ka.
-__global__ void k_bn_bwd_finalize(int B, int64_t R, int64_t C, int chunks, const float* __restrict__ p1,
-                                  const float* __restrict__ p2, const float* __restrict__ gamma,
+__global__ void k_bn_bwd_finalize(int B, int64_t R, int64_t C, int chunks, const double* __restrict__ p1,
+                                  const double* __restrict__ p2, const float* __restrict__ gamma,
                                   const float* __restrict__ beta, int64_t gbs, const float* __restrict__ smean,
                                   const float* __restrict__ sinv, float* __restrict__ dgamma,
                                   float* __restrict__ dbeta, int accumulate, float* __restrict__ coef) {
@@ -248,8 +261,10 @@ __global__ void k_bn_bwd_finalize(int B, int64_t R, int64_t C, int chunks, const
   coef[i] = (float)A;
   coef[BC + i] = (float)(-A * k3 * is);
   coef[2 * BC + i] = (float)(A * (k3 * m * is - k2));
-  coef[3 * BC + i] = (float)A;
-  coef[4 * BC + i] = (float)(be - m * A);
+  float fa, fc;                                   // the forward's z = a x + c, same rounding
+  bn_affine(gamma[b * gbs + c], beta[b * gbs + c], smean[i], sinv[i], fa, fc);
+  coef[3 * BC + i] = fa;
+  coef[4 * BC + i] = fc;
 }
 
 template <typename T, int VEC>
@@ -312,8 +327,7 @@ __global__ void __launch_bounds__(NT, 4) k_bn_max_fwd(int64_t L, int64_t C, cons
     for (int v = 0; v < VEC; ++v) {
       float m = smean[(int64_t)b * C + c0 + v], is = sinv[(int64_t)b * C + c0 + v];
       float ga = gamma[(int64_t)b * gbs + c0 + v], be = beta[(int64_t)b * gbs + c0 + v];
-      sc[v] = ga * is;
-      sf[v] = be - m * ga * is;
+      bn_affine(ga, be, m, is, sc[v], sf[v]);
     }
     const T* Xb = X + (int64_t)b * xbs + n * L * xld;
     // two rows in flight per thread (bulk), then the tail row: loads issued before use
@@ -379,7 +393,9 @@ __global__ void k_bn_max_bwd_small(int B, int64_t N, int64_t L, int64_t C, const
     int64_t l = amax[(b * N + n) * C + c];
     float x = ldf(X + b * xbs + (n * L + l) * xld + c);
     float xh = (x - m) * is;
-    float dz = dG[b * gbs_ + n * gld + c] * act_grad(fmaf(ga, xh, be), act, alpha);
+    float fa, fc;
+    bn_affine(ga, be, m, is, fa, fc);
+    float dz = dG[b * gbs_ + n * gld + c] * act_grad(fmaf(x, fa, fc), act, alpha);
     dz_out[(b * N + n) * C + c] = dz;
     s1 += dz;
     s2 += (double)dz * xh;
@@ -466,7 +482,7 @@ size_t bn_parts_bytes(int B, int64_t R, int64_t C) {
   int ch = 1;
   for (int vec : {1, 4, 8})
     for (int bps : {0, BWD_BPS}) ch = std::max(ch, make_geo(B, R, C, vec, bps).chunks);
-  return align_up(2 * (size_t)B * ch * C * sizeof(float), 256);
+  return align_up(2 * (size_t)B * ch * C * sizeof(double), 256);
 }
 
 }  // namespace
@@ -511,8 +527,8 @@ hfta_status hfta_fused_bn_fwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_i
   cudaStream_t s = (cudaStream_t)stream;
   int vec = pick_vec(dt, C, {{X.ptr, X.ld, X.bstride}, {Y.ptr, Y.ld, Y.bstride}});
   Geo g = make_geo(B, R, C, vec);
-  float* p1 = reinterpret_cast<float*>(ws);
-  float* p2 = p1 + (size_t)B * g.chunks * C;
+  double* p1 = reinterpret_cast<double*>(ws);
+  double* p2 = p1 + (size_t)B * g.chunks * C;
   dim3 grid(g.colgroups, g.chunks, B);
   DT_DISPATCH(dt, {
     LAUNCH_VEC(T, vec, k_bn_stats, grid, R, C, (const T*)X.ptr, X.bstride, X.ld, g, p1, p2);
@@ -543,8 +559,8 @@ hfta_status hfta_fused_bn_bwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_i
   cudaStream_t s = (cudaStream_t)stream;
   int vec = pick_vec(dt, C, {{X.ptr, X.ld, X.bstride}, {dY.ptr, dY.ld, dY.bstride}, {dX.ptr, dX.ld, dX.bstride}});
   Geo g = make_geo(B, R, C, vec, BWD_BPS);
-  float* p1 = reinterpret_cast<float*>(ws);
-  float* p2 = p1 + (size_t)B * g.chunks * C;
+  double* p1 = reinterpret_cast<double*>(ws);
+  double* p2 = p1 + (size_t)B * g.chunks * C;
   size_t parts_bytes = bn_parts_bytes(B, R, C);
   float* coef = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + parts_bytes);
   dim3 grid(g.colgroups, g.chunks, B);

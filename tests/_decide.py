@@ -17,11 +17,21 @@ import torch
 from oracle import decisions as Dm
 from oracle import models as OM
 
-# Decision margins relative to the per-channel rms of the decision variable
-# (reading R15c).  They are >= 8x the largest decision-variable error the GPU
-# path shows (measured by `decision_errors` on positive ReLU outputs, where
-# the stored activation IS the GPU's pre-activation value).
-MARGIN = {"f32": 2.0 ** -14, "bf16": 2.0 ** -5}
+# Decision margins, in units of each site's error scale (reading R15c).
+# fp32: fixed, >= 5x the largest decision-variable error the GPU path shows
+# (`decision_errors`, measured on the box: <= 1.3 x 2^-14).  bf16: calibrated
+# per site from the bf16-storage witness -- WITNESS_SAFETY x the largest
+# change of the site's decision variable that bf16 rounding of the stored
+# operands causes in the oracle itself (at least BF16_FLOOR).
+MARGIN_F32 = 2.0 ** -11
+# bf16 gradient gate per tensor: max(2e-2, WITNESS_GATE x the witness's
+# normwise change of that gradient).  The GPU rounds at a few points the
+# witness does not model (dZ stored in bf16 between kernels, the K10 M matrix
+# in bf16), measured GPU error / witness <= 1.7 on the box (reading R28).
+WITNESS_GATE = 3.0
+WITNESS_SAFETY = 3.0
+BF16_FLOOR = 2.0 ** -8
+MARGIN = {"f32": MARGIN_F32, "bf16": BF16_FLOOR}
 
 
 def _h(t):
@@ -60,10 +70,11 @@ def pointnet_gpu_values(net, b):
     return {k: _h(t) for k, t in v.items()}
 
 
-def decision_errors(ctx, gpu_vals):
-    """max |z_gpu - z_oracle| / rms_c(z) over positions near the threshold
-    (0 < z_oracle <= rms_c, GPU output > 0: there the stored ReLU output is the
-    GPU's z, up to its storage rounding) -- the margin must exceed it."""
+def decision_errors(ctx, gpu_vals, margins):
+    """max |z_gpu - z_oracle| / (scale_c * margin) over positions near the
+    threshold (0 < z_oracle <= rms_c(z), GPU output > 0: there the stored ReLU
+    output is the GPU's z, up to its storage rounding), scale_c the site's
+    error scale (oracle/decisions.py) -- must stay below 1."""
     out = {}
     for site, a in gpu_vals.items():
         if site not in ctx.sites:
@@ -73,17 +84,36 @@ def decision_errors(ctx, gpu_vals):
         axes = tuple(i for i in range(z.ndim) if i != 1)
         rms = np.expand_dims(np.sqrt(np.mean(z * z, axis=axes)), axes)
         sel = (a > 0) & (z > 0) & (z <= rms)
-        out[site] = float(np.max(np.abs(a - z)[sel] / np.broadcast_to(rms, z.shape)[sel])) if sel.any() else 0.0
+        sc = np.broadcast_to(ctx.sites[site]["scale"], z.shape)
+        out[site] = float(np.max(np.abs(a - z)[sel] / sc[sel])) / margins[site] if sel.any() else 0.0
     return out
 
 
-def build_override(own_ctx, gpu, L=None):
-    """Override map from the GPU decisions + a per-site agreement report.
-    Raises AssertionError naming the site if the GPU disagrees with the oracle
-    at an unflagged position."""
+def witness_margins(own, wit):
+    """Per-site margins from the bf16-storage witness (same decisions): the
+    largest |change| of the decision variable over its error scale."""
+    m = {}
+    for site, v in own.sites.items():
+        w = wit.sites[site]
+        key = "z" if v["kind"] == "relu" else "x"
+        sc = v["scale"] if v["kind"] == "relu" else v["scale"][:, None, :]
+        err = float(np.max(np.abs(w[key] - v[key]) / sc))
+        m[site] = max(BF16_FLOOR, WITNESS_SAFETY * err)
+    return m
+
+
+def build_override(own_ctx, gpu, margins, L=None, skip=()):
+    """Override map from the GPU decisions + a per-site agreement report:
+    flagged count, flips, disagreements outside the flagged band and the
+    largest normalised distance of any disagreement from the threshold
+    (|z| / scale for a gate, (top - chosen) / scale for an argmax, in units
+    of the site's margin: <= 1 for every valid override)."""
     override, report = {}, {}
     for site, v in own_ctx.sites.items():
-        own, flag = v["own"], v["flag"]
+        if any(site.startswith(p) for p in skip):
+            continue
+        own = v["own"]
+        flag = Dm.flags(v, margins[site])
         if site == "stn.bn3":
             # only the argmax rows' gates are observable (and used by the backward)
             ov = own.copy()
@@ -98,35 +128,76 @@ def build_override(own_ctx, gpu, L=None):
             continue
         diff = g != own
         bad = diff & ~flag          # (a flagged argmax change is value-checked by the oracle itself)
+        dist = 0.0
+        if diff.any():
+            if v["kind"] == "relu":
+                sc = np.broadcast_to(v["scale"], v["z"].shape)
+                dist = float(np.max(np.abs(v["z"])[diff] / sc[diff]))
+            else:
+                val = np.take_along_axis(v["x"], np.clip(g, 0, v["x"].shape[1] - 1)[:, None, :], axis=1)[:, 0, :]
+                sc = np.broadcast_to(v["scale"], v["top"].shape)
+                dist = float(np.max((v["top"] - val)[diff] / sc[diff]))
         report[site] = dict(flagged=int(flag.sum()), size=int(flag.size), flips=int(diff.sum()),
-                            unflagged_disagree=int(bad.sum()))
-        assert not bad.any(), "GPU decision differs from the oracle outside the flagged band at %s: %s" % (
-            site, report[site])
+                            unflagged_disagree=int(bad.sum()), max_dist=dist / margins[site],
+                            margin=margins[site])
         override[site] = g
     return override, report
 
 
-def bf16_round(x, what):
+def _rb(x):
     return torch.tensor(np.asarray(x, dtype=np.float64)).to(torch.bfloat16).double().numpy()
 
 
-def oracle_with_decisions(arch, P, S, O, batch, t, hp_b, b, gpu, margin, L=None, witness=False, **kw):
+def bf16_store(out_layers=()):
+    """Witness rounding at the bf16-AMP storage points: every contraction's
+    inputs, weights and incoming gradients; its output only for the layers
+    whose pre-activation the GPU path stores in bf16 (`out_layers`)."""
+    def f(x, what, name):
+        if what == "out" and (name is None or not any(name.startswith(p) for p in out_layers)):
+            return x
+        return _rb(x)
+    return f
+
+
+# PointNet: K10/K11 keep y in fp32 (never stored); the seg head stores y1..y3 in bf16
+POINTNET_OUT = ("head.c1", "head.c2", "head.c3")
+
+
+def oracle_with_decisions(arch, P, S, O, batch, t, hp_b, b, gpu, dtype, L=None, witness=False, **kw):
     """(oracle result with the GPU's flagged-band decisions, agreement report,
-    witness result or None).  The witness re-runs the SAME decisions with
-    bf16 rounding of every stored operand (reading R28): the size of the
-    gradient change bf16-AMP storage alone causes on this step."""
-    d1 = Dm.Decisions(margin)
+    witness result or None).
+
+    pass 1: the oracle's own decisions and decision variables;
+    witness (bf16): the same decisions with bf16 rounding of every stored
+      operand (reading R28) -- per-site margins (bf16) and the per-tensor
+      gradient sensitivity to bf16 storage;
+    pass 2: the GPU's decisions inside the flagged bands (validated by the
+      oracle), the reference every GPU quantity is compared with."""
+    step = lambda: OM.train_step(arch, P, S, O, batch, t, hp_b, b=b, **kw)
+    return with_decisions(step, gpu, dtype, L=L, witness=witness, out_layers=POINTNET_OUT)
+
+
+def with_decisions(step, gpu, dtype, L=None, witness=False, out_layers=(), skip=()):
+    """The three-pass flow above for any oracle step callable `step()`.
+    Sites whose name starts with a prefix in `skip` keep the oracle's own
+    decisions and are not compared."""
+    d1 = Dm.Decisions()
     with Dm.use(d1):
-        OM.train_step(arch, P, S, O, batch, t, hp_b, b=b, **kw)
-    override, report = build_override(d1, gpu, L)
-    report["_ctx"] = d1
-    d2 = Dm.Decisions(margin, override)
-    with Dm.use(d2):
-        res = OM.train_step(arch, P, S, O, batch, t, hp_b, b=b, **kw)
+        res1 = step()
     res_w = None
-    if witness:
-        used = {k: v["used"] for k, v in d2.sites.items()}
-        d3 = Dm.Decisions(margin, used, force=True, store=bf16_round)
-        with Dm.use(d3):
-            res_w = OM.train_step(arch, P, S, O, batch, t, hp_b, b=b, **kw)
+    if witness or dtype == "bf16":
+        own = {k: v["own"] for k, v in d1.sites.items()}
+        dw = Dm.Decisions(0.0, own, force=True, store=bf16_store(out_layers))
+        with Dm.use(dw):
+            res_w = step()
+        res_w["own"] = res1                 # the same decisions without the rounding
+    margins = witness_margins(d1, dw) if dtype == "bf16" else {k: MARGIN_F32 for k in d1.sites}
+    override, report = build_override(d1, gpu, margins, L, skip)
+    report["_ctx"] = d1
+    report["_margins"] = margins
+    if any(v["unflagged_disagree"] for k, v in report.items() if not k.startswith("_")):
+        return None, report, res_w          # the caller reports and fails
+    d2 = Dm.Decisions(0.0, override, margins=margins)
+    with Dm.use(d2):
+        res = step()
     return res, report, res_w

@@ -54,12 +54,19 @@ def run_pair(task, dtype, B, N, L, k, steps=1, widths=None, seed=0, witness=None
         for b in range(B):
             gpu = DE.pointnet_gpu_decisions(net, b)
             r, report, rw = DE.oracle_with_decisions(arch, P[b], S[b], O[b], (x, y), t, OM.hp_of(hp, b), b, gpu,
-                                                     DE.MARGIN[dtype], L=L, witness=witness and t == 1)
+                                                     dtype, L=L, witness=witness and t == 1)
+            r = r if r is not None else {"loss": np.nan, "params": P[b], "stats": S[b], "opt": O[b], "grads": {}}
             r["p_before"] = P[b]
-            r["p_gpu_after"] = net.params(b)
             r["report"] = report
-            r["zerr"] = DE.decision_errors(report["_ctx"], DE.pointnet_gpu_values(net, b))
+            r["zerr"] = DE.decision_errors(report["_ctx"], DE.pointnet_gpu_values(net, b), report["_margins"])
             r["witness"] = rw
+            report.pop("_ctx")                    # the per-site arrays (GBs at full size)
+            # the GPU state after this step (later steps overwrite the net)
+            r["gpu_after"] = dict(
+                params=net.params(b),
+                m={n: net.arena.host_tensor("m", n)[b] for n, _ in net.arena.specs},
+                v={n: net.arena.host_tensor("v", n)[b] for n, _ in net.arena.specs},
+                running={n: tuple(t_[b].cpu().numpy() for t_ in net.running[n]) for n in net.bn_names})
             res.append(r)
         out.append((loss, np.array([r["loss"] for r in res]), [net.grads(b) for b in range(B)], res))
         P = [r["params"] for r in res]
@@ -70,17 +77,25 @@ def run_pair(task, dtype, B, N, L, k, steps=1, widths=None, seed=0, witness=None
 
 def check_step(net, loss, ref_losses, grads, res, dtype, B):
     """Every per-model quantity of the step vs the decision-matched oracle:
-    loss; every gradient tensor (fp32: 1e-4 normwise; bf16: max(2e-2, 2 x the
+    loss; every gradient tensor (fp32: 1e-4 normwise; bf16: max(2e-2, 3 x the
     bf16-storage witness of that tensor), reading R28); BN running mean and
     variance of every layer; Adam m and v; the update on the elements whose
     sign the oracle alone decides (reading R21)."""
     tol = TOL[dtype]
     worst = []
     for b in range(B):
+        rep = {k: v for k, v in res[b]["report"].items() if not k.startswith("_")}
+        print("\n  model %d decisions (flagged/size, flips, unflagged disagreements, max dist/margin, margin): %s" % (
+            b, " ".join("%s:%d/%d,%d,%d,%.2f,%.1e" % (k, v["flagged"], v["size"], v["flips"], v["unflagged_disagree"],
+                                                      v["max_dist"], v["margin"]) for k, v in rep.items())))
+        print("  model %d max z error / margin: %s" % (b, " ".join(
+            "%s:%.2f" % (k, e) for k, e in res[b]["zerr"].items())))
+    for b in range(B):
         r = res[b]
-        margin = DE.MARGIN[dtype]
+        bad = {k: v for k, v in r["report"].items() if not k.startswith("_") and v["unflagged_disagree"]}
+        assert not bad, "model %d: GPU decisions differ from the oracle outside the flagged band: %s" % (b, bad)
         for site, e in r["zerr"].items():      # the margin covers the GPU's decision-variable error
-            assert e <= margin, "model %d site %s: GPU z error %.3e exceeds the margin %.3e" % (b, site, e, margin)
+            assert e <= 1.0, "model %d site %s: GPU z error is %.2f x the margin" % (b, site, e)
         assert abs(loss[b] - ref_losses[b]) <= tol * abs(ref_losses[b]), (b, loss[b], ref_losses[b])
         G, Rg = grads[b], r["grads"]
         gmax = max(np.linalg.norm(v) for v in Rg.values())
@@ -91,22 +106,22 @@ def check_step(net, loss, ref_losses, grads, res, dtype, B):
                 continue
             gtol[n] = tol
             if dtype == "bf16":
-                w = relerr(r["witness"]["grads"][n], Rg[n])
-                gtol[n] = max(tol, 2.0 * w)
+                w = relerr(r["witness"]["grads"][n], r["witness"]["own"]["grads"][n])
+                gtol[n] = max(tol, DE.WITNESS_GATE * w)
             e = relerr(G[n], Rg[n])
             worst.append((e / gtol[n], e, gtol[n], b, n))
             assert e <= gtol[n], "model %d grad %s: %.3e > %.3e" % (b, n, e, gtol[n])
+        ga = r["gpu_after"]
         for name in net.bn_names:
-            rm, rv = (t[b].cpu().numpy() for t in net.running[name])
+            rm, rv = ga["running"][name]
             assert relerr(rm, r["stats"][name + ".rm"]) <= tol, (b, name, "running_mean")
             assert relerr(rv, r["stats"][name + ".rv"]) <= tol, (b, name, "running_var")
-        m_gpu = {n: net.arena.host_tensor("m", n)[b] for n in gtol}
-        v_gpu = {n: net.arena.host_tensor("v", n)[b] for n in gtol}
+        m_gpu, v_gpu = ga["m"], ga["v"]
         for n in gtol:
             m_ref, v_ref = r["opt"][n]
             assert relerr(m_gpu[n], m_ref) <= gtol[n] * 1.01 + 1e-6, (b, n, "exp_avg")
             assert relerr(v_gpu[n], v_ref) <= 2.0 * gtol[n] * 1.01 + 1e-6, (b, n, "exp_avg_sq")
-        pb, p0 = r["p_gpu_after"], r["p_before"]
+        pb, p0 = ga["params"], r["p_before"]
         wd = float(net.hv.t["wd"][b].item())
         for n in gtol:
             g = Rg[n] + wd * p0[n]            # what Adam normalises (coupled L2 decay)
@@ -119,11 +134,6 @@ def check_step(net, loss, ref_losses, grads, res, dtype, B):
     worst.sort(reverse=True)
     print("\n[%s] worst gradient errors (err / gate): %s" % (dtype, " ".join(
         "%s:%.2e/%.1e" % (n, e, g) for _, e, g, b, n in worst[:6])))
-    for b in range(B):
-        rep = {k: v for k, v in res[b]["report"].items() if not k.startswith("_")}
-        print("  model %d decisions (flagged/size, flips): %s" % (b, " ".join(
-            "%s:%d/%d,%d" % (k, v["flagged"], v["size"], v["flips"]) for k, v in rep.items())))
-        print("  model %d max z error / rms: %s" % (b, " ".join("%s:%.1e" % kv for kv in res[b]["zerr"].items())))
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
