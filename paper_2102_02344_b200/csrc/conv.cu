@@ -1,7 +1,17 @@
 // conv.cu -- fused Conv2d / ConvTranspose2d for B models (K3/K4/K5).
 // App. B rows Conv2d and ConvT2d: B same-shape
-// (de)convolutions fused into one, here as model-batched GEMMs on the
-// tcgen05 engine plus two gather kernels, NHWC per model:
+// (de)convolutions fused into one launch, model index in the tile scheduler.
+//
+// Tensor-core paths (bf16), no patch matrix in HBM:
+//  * k4 s2 p1 with 64-multiple channels: implicit GEMM on the tcgen05 engine
+//    (gemm_tc.cu CONV modes) -- TMA gathers the stride-2 windows straight into
+//    the swizzled shared-memory ring (Conv2d fwd, ConvT2d dgrad, both wgrads);
+//    ConvT2d fwd and Conv2d dgrad run as 4 sub-pixel phases of dense 2x2
+//    stride-1 convolutions whose epilogue interleaves the phase outputs.
+//  * 1x1 input, stride 1, pad 0 (DCGAN t1) and a window covering the whole
+//    input (D c5): the (de)convolution IS a dense GEMM in NHWC (no gather).
+// Fallback (fp32, and the 8-channel image layers D c1 fwd/wgrad, G t5
+// dgrad/wgrad): explicit patch matrix through the caller's workspace:
 //   im2col : col[(n,sy,sx)][(ky,kx,c)] = img[n, sy*s-p+ky, sx*s-p+kx, c]   (0 outside)
 //   col2im : img[n, by, bx, c] = sum_{ky,kx: sy=(by+p-ky)/s integral, in range} col[(n,sy,sx)][(ky,kx,c)]
 // ("big" grid = conv input / convT output, "small" grid = conv output / convT input).
@@ -9,12 +19,11 @@
 //   conv  bwd : dW = dY^T im2col(X) ; dX = col2im(dY W)
 //   convT fwd : Y  = col2im(X Wt^T)                      Wt [(ky,kx,co)][ci]
 //   convT bwd : dWt = im2col(dY)^T X ; dX = im2col(dY) Wt
-// col2im is a deterministic gather (no atomics).  The col matrix lives in the
-// caller's workspace.  (An implicit-GEMM producer that gathers the im2col rows
-// straight into the swizzled smem ring is the next step.)
+// col2im is a deterministic gather (no atomics).
 #include "gemm.cuh"
 
 namespace hfta {
+void wgrad_split_rows(int B, int64_t rows, int64_t N, int64_t K, int* splits, int64_t* chunk);
 hfta_status colsum_impl(int B, int64_t rows, int64_t C, int64_t group, hfta_dtype dt, hfta_in X, float* S,
                         int64_t S_bstride, int accumulate, void* ws, size_t ws_bytes, cudaStream_t s);
 size_t colsum_ws(int B, int64_t rows, int64_t C, int64_t group);
@@ -169,6 +178,126 @@ hfta_status make_shape(const hfta_conv_desc* d, Shape* sh) {
   return HFTA_OK;
 }
 
+bool k4s2p1(const hfta_conv_desc* d) { return d->kh == 4 && d->kw == 4 && d->stride == 2 && d->pad == 1; }
+
+// 1x1 input, stride 1, pad 0 (ConvT) / window = whole input, pad 0 (Conv): a dense GEMM in NHWC
+bool dense_convT(const hfta_conv_desc* d) { return d->transposed && d->H == 1 && d->W == 1 && d->stride == 1 && d->pad == 0; }
+bool dense_conv(const hfta_conv_desc* d) { return !d->transposed && d->kh == d->H && d->kw == d->W && d->pad == 0; }
+
+// dense model-major NHWC image operand: elements per model
+int64_t img_elems(int N, int64_t H, int64_t W, int64_t C) { return (int64_t)N * H * W * C; }
+
+ConvTcP img_op(int B, const void* ptr, int64_t bs, int N, int H, int W, int C) {
+  ConvTcP p{};
+  p.B = B; p.img = ptr; p.img_bs = bs; p.img_n = N; p.img_h = H; p.img_w = W; p.img_c = C;
+  return p;
+}
+
+// Implicit-GEMM descriptors of the three contractions of a k4 s2 p1 layer
+// (model strides: x_bs / y_bs / w_bs; dense NHWC images).
+ConvTcP fwd_cp(int B, const hfta_conv_desc* d, const Shape& sh, const void* X, int64_t x_bs, const void* W,
+               int64_t w_bs, int64_t w_ld, void* Y, int64_t y_bs) {
+  ConvTcP cp = img_op(B, X, x_bs, d->N, d->H, d->W, d->C_in);
+  cp.opd = W; cp.opd_bs = w_bs;
+  const int64_t ye = img_elems(d->N, sh.Ho, sh.Wo, d->C_out);
+  if (!sh.transposed) {          // stride-2 gather of X
+    cp.mode = 1; cp.M = (int64_t)d->N * sh.Ho * sh.Wo; cp.N = d->C_out; cp.K = 16 * (int64_t)d->C_in;
+    cp.grid_w = (int)sh.Wo; cp.grid_h = (int)sh.Ho; cp.opd_ld = w_ld;
+    cp.C = Y; cp.c_bs = y_bs; cp.c_ld = d->C_out;
+  } else {                       // 4 sub-pixel phases of X against the ConvT taps
+    cp.mode = 2; cp.M = (int64_t)d->N * d->H * d->W; cp.N = d->C_out; cp.K = 4 * (int64_t)d->C_in;
+    cp.grid_w = d->W; cp.grid_h = d->H; cp.w_mn = 0; cp.w_cn = d->C_out; cp.w_ca = d->C_in;
+    cp.C = Y; cp.c_bs = B > 1 ? y_bs : ye; cp.y_h = (int)sh.Ho; cp.y_w = (int)sh.Wo;
+  }
+  return cp;
+}
+ConvTcP wgrad_cp(int B, const hfta_conv_desc* d, const Shape& sh, const void* dY, int64_t dy_bs, const void* X,
+                 int64_t x_bs) {
+  ConvTcP cp;
+  if (!sh.transposed) {          // dW[co][(kh,kw,ci)] = sum_(n,oy,ox) dY (x) stride-2 gather of X
+    cp = img_op(B, X, x_bs, d->N, d->H, d->W, d->C_in);
+    cp.mode = 3; cp.M = d->C_out; cp.N = 16 * (int64_t)d->C_in;
+    cp.grid_w = (int)sh.Wo; cp.grid_h = (int)sh.Ho;
+    cp.opd = dY; cp.opd_bs = dy_bs; cp.opd_ld = d->C_out;
+    cp.K = (int64_t)d->N * sh.Ho * sh.Wo;
+  } else {                       // dWt[(kh,kw,co)][ci] = sum_(n,i,j) stride-2 gather of dY (x) X
+    cp = img_op(B, dY, dy_bs, d->N, (int)sh.Ho, (int)sh.Wo, d->C_out);
+    cp.mode = 4; cp.M = 16 * (int64_t)d->C_out; cp.N = d->C_in;
+    cp.grid_w = d->W; cp.grid_h = d->H;
+    cp.opd = X; cp.opd_bs = x_bs; cp.opd_ld = d->C_in;
+    cp.K = (int64_t)d->N * d->H * d->W;
+  }
+  return cp;
+}
+ConvTcP dgrad_cp(int B, const hfta_conv_desc* d, const Shape& sh, const void* dY, int64_t dy_bs, const void* W,
+                 int64_t w_bs, int64_t w_ld, void* dX, int64_t dx_bs) {
+  ConvTcP cp = img_op(B, dY, dy_bs, d->N, (int)sh.Ho, (int)sh.Wo, d->C_out);
+  cp.opd = W; cp.opd_bs = w_bs;
+  const int64_t xe = img_elems(d->N, d->H, d->W, d->C_in);
+  if (!sh.transposed) {          // 4 sub-pixel phases of dY against the (adjoint) Conv taps
+    cp.mode = 2; cp.M = (int64_t)d->N * sh.Ho * sh.Wo; cp.N = d->C_in; cp.K = 4 * (int64_t)d->C_out;
+    cp.grid_w = (int)sh.Wo; cp.grid_h = (int)sh.Ho; cp.w_mn = 1; cp.w_cn = d->C_in; cp.w_ca = d->C_out;
+    cp.C = dX; cp.c_bs = B > 1 ? dx_bs : xe; cp.y_h = d->H; cp.y_w = d->W;
+  } else {                       // Conv2d(dY, Wt): stride-2 gather of dY, B = Wt MN-major
+    cp.mode = 1; cp.w_mn = 1; cp.M = (int64_t)d->N * d->H * d->W; cp.N = d->C_in; cp.K = 16 * (int64_t)d->C_out;
+    cp.grid_w = d->W; cp.grid_h = d->H; cp.opd_ld = w_ld;
+    cp.C = dX; cp.c_bs = dx_bs; cp.c_ld = d->C_in;
+  }
+  return cp;
+}
+
+// Which contractions of the layer the implicit-GEMM path takes for dense,
+// aligned, model-major operands (the runtime re-checks the real pointers).
+void plan(int B, const hfta_conv_desc* d, hfta_dtype dt, const Shape& sh, bool& f, bool& g, bool& w) {
+  f = g = w = false;
+  if (dt != HFTA_BF16 || !k4s2p1(d)) return;
+  char* a = reinterpret_cast<char*>(256);       // any 16-B aligned address: only eligibility is evaluated
+  const int64_t xe = img_elems(d->N, d->H, d->W, d->C_in), ye = img_elems(d->N, sh.Ho, sh.Wo, d->C_out);
+  const int64_t we = (int64_t)d->kh * d->kw * d->C_in * d->C_out;
+  const int64_t wld = sh.transposed ? d->C_in : (int64_t)d->kh * d->kw * d->C_in;
+  f = conv_tc_supported(fwd_cp(B, d, sh, a, xe, a, we, wld, a, ye));
+  g = conv_tc_supported(dgrad_cp(B, d, sh, a, ye, a, we, wld, a, xe));
+  w = conv_tc_supported(wgrad_cp(B, d, sh, a, ye, a, xe));
+}
+
+// the explicit patch matrix only where a fallback path runs: fp32, or an
+// 8-channel image on the gathered side (D c1 fwd / wgrad, G t5 dgrad / wgrad)
+size_t col_bytes(int B, const hfta_conv_desc* d, hfta_dtype dt, const Shape& sh) {
+  if (dense_conv(d) || dense_convT(d)) return 0;
+  bool f, g, w;
+  plan(B, d, dt, sh, f, g, w);
+  return (f && g && w) ? 0 : align_up((size_t)B * sh.Ms * sh.Kc * dsize(dt), 256);
+}
+
+// split-K partials of a tensor-core conv wgrad (modes 3, 4)
+size_t conv_wgrad_part(int B, int64_t rows, int64_t M, int64_t N) {
+  int sp; int64_t ch;
+  wgrad_split_rows(B, rows, M, N, &sp, &ch);
+  return sp > 1 ? (size_t)sp * B * M * N * sizeof(float) : 0;
+}
+
+hfta_status conv_wgrad_tc(ConvTcP& cp, int64_t rows, float* dW, int64_t dW_bstride, int64_t ld, int accumulate,
+                          char* lws, size_t lwsb, cudaStream_t s) {
+  int sp; int64_t ch;
+  wgrad_split_rows(cp.B, rows, cp.M, cp.N, &sp, &ch);
+  cp.K = rows; cp.splits = sp; cp.k_chunk = ch;
+  cp.C = dW; cp.c_bs = dW_bstride; cp.c_ld = ld; cp.accumulate = accumulate;
+  cp.part = nullptr;
+  if (sp > 1) {
+    HFTA_REQUIRE(lwsb >= (size_t)sp * cp.B * cp.M * cp.N * sizeof(float), HFTA_ERR_WORKSPACE,
+                 "conv wgrad: split-K workspace too small");
+    cp.part = reinterpret_cast<float*>(lws);
+  }
+  if (hfta_status st = conv_tc(cp, s)) return st;
+  if (sp > 1) {
+    GemmP g{};
+    g.B = cp.B; g.M = cp.M; g.N = cp.N; g.splits = sp; g.part = cp.part; g.C = dW; g.c_bs = dW_bstride;
+    g.c_ld = ld; g.accumulate = accumulate;
+    if (hfta_status st = splitk_reduce(g, s)) return st;
+  }
+  return HFTA_OK;
+}
+
 }  // namespace
 }  // namespace hfta
 
@@ -179,11 +308,12 @@ extern "C" {
 size_t hfta_fused_conv_workspace(int B, const hfta_conv_desc* d, hfta_dtype dt) {
   Shape sh;
   if (B < 1 || make_shape(d, &sh) != HFTA_OK) return 0;
-  const size_t col = align_up((size_t)B * sh.Ms * sh.Kc * dsize(dt), 256);
+  const size_t col = col_bytes(B, d, dt, sh);
   // weight-gradient GEMM (split-K partials) of either orientation
   const int64_t M = sh.Ms;
   size_t lin = std::max(hfta_fused_linear_bwd_workspace(B, M, sh.Co, sh.Kc, dt),
                         hfta_fused_linear_bwd_workspace(B, M, sh.Kc, sh.Ci, dt));
+  lin = std::max(lin, std::max(conv_wgrad_part(B, M, sh.Co, sh.Kc), conv_wgrad_part(B, M, sh.Kc, sh.Ci)));
   return col + align_up(lin, 256);
 }
 
@@ -200,6 +330,29 @@ hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
   char* col = reinterpret_cast<char*>(ws);
   GemmP p{};
   p.B = B; p.splits = 1;
+  HFTA_REQUIRE(X.ld == d->C_in && Y.ld == d->C_out, HFTA_ERR_SHAPE,
+               "conv_fwd: images must be dense NHWC (X.ld %lld vs C_in %d, Y.ld %lld vs C_out %d)", (long long)X.ld,
+               d->C_in, (long long)Y.ld, d->C_out);
+  const int64_t xe = img_elems(d->N, d->H, d->W, d->C_in), ye = img_elems(d->N, sh.Ho, sh.Wo, d->C_out);
+  if (dt == HFTA_BF16 && k4s2p1(d) && (X.bstride == 0 || X.bstride == xe) && (Y.bstride == ye || B == 1)) {
+    ConvTcP cp = fwd_cp(B, d, sh, X.ptr, X.bstride, W.ptr, W.bstride, W.ld, Y.ptr, Y.bstride);
+    if (conv_tc_supported(cp)) {
+      if (hfta_status st = conv_tc(cp, s)) return st;
+      return post_launch(s, "hfta_fused_conv_fwd");
+    }
+  }
+  if (dense_convT(d) || dense_conv(d)) {
+    // t1: Y[n][(kh,kw,co)] = X[n] Wt^T ; c5: Y[n][co] = X[n][(h,w,ci)] W^T -- plain GEMMs in NHWC
+    p.M = d->N; p.N = dense_convT(d) ? sh.Kc : d->C_out; p.K = dense_convT(d) ? d->C_in : sh.Kc;
+    p.A = X.ptr; p.a_bs = X.bstride; p.a_ld = p.K; p.a_kmajor = 1;
+    p.Bm = W.ptr; p.b_bs = W.bstride; p.b_ld = W.ld; p.b_kmajor = 1;
+    p.C = Y.ptr; p.c_bs = Y.bstride; p.c_ld = p.N;
+    p.k_chunk = p.K;
+    if (hfta_status st = run_gemm(p, dt, false, s)) return st;
+    return post_launch(s, "hfta_fused_conv_fwd");
+  }
+  HFTA_REQUIRE(col_bytes(B, d, dt, sh) > 0, HFTA_ERR_UNSUPPORTED, "conv_fwd: operands not eligible for the "
+               "implicit-GEMM path (alignment / model strides) and no patch-matrix workspace for this configuration");
   if (!sh.transposed) {
     // Y[(n,oy,ox)][co] = im2col(X) W^T ; a shared input image gives a shared col (bstride 0)
     const int nb = X.bstride == 0 ? 1 : B;
@@ -235,9 +388,45 @@ hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
   HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "conv_bwd: workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = (cudaStream_t)stream;
   char* col = reinterpret_cast<char*>(ws);
-  const size_t colb = align_up((size_t)B * sh.Ms * sh.Kc * dsize(dt), 256);
+  const size_t colb = col_bytes(B, d, dt, sh);
   char* lws = col + colb;
   const size_t lwsb = ws_bytes - colb;
+  HFTA_REQUIRE(dY.ld == d->C_out && X.ld == d->C_in && (!dX.ptr || dX.ld == d->C_in), HFTA_ERR_SHAPE,
+               "conv_bwd: images must be dense NHWC (dY.ld %lld, X.ld %lld, dX.ld %lld; C_in %d, C_out %d)",
+               (long long)dY.ld, (long long)X.ld, (long long)dX.ld, d->C_in, d->C_out);
+  const int64_t xe = img_elems(d->N, d->H, d->W, d->C_in), ye = img_elems(d->N, sh.Ho, sh.Wo, d->C_out);
+  if (dense_convT(d) || dense_conv(d)) {
+    // t1 / c5 are plain Linear layers in NHWC: dgrad + wgrad of the GEMM
+    const int64_t Mg = d->N, Ng = dense_convT(d) ? sh.Kc : d->C_out, Kg = dense_convT(d) ? d->C_in : sh.Kc;
+    if (hfta_status st = hfta_fused_linear_bwd(B, Mg, Ng, Kg, dt, hfta_in{dY.ptr, dY.bstride, Ng},
+                                               hfta_in{X.ptr, X.bstride, Kg}, W,
+                                               dX.ptr ? hfta_out{dX.ptr, dX.bstride, Kg} : hfta_out{nullptr, 0, 1}, dW,
+                                               dW_bstride, Kg, nullptr, 0, accumulate, lws, lwsb, stream))
+      return st;
+    return post_launch(s, "hfta_fused_conv_bwd");
+  }
+  const bool tc = dt == HFTA_BF16 && k4s2p1(d) && (X.bstride == 0 || X.bstride == xe) &&
+                  (dY.bstride == ye || B == 1) && (!dX.ptr || dX.bstride == xe || B == 1);
+  bool need_dW = dW != nullptr, need_dX = dX.ptr != nullptr;
+  if (tc && need_dW) {
+    ConvTcP cp = wgrad_cp(B, d, sh, dY.ptr, dY.bstride, X.ptr, X.bstride);
+    if (conv_tc_supported(cp)) {
+      if (hfta_status st = conv_wgrad_tc(cp, cp.K, dW, dW_bstride, cp.N, accumulate, lws, lwsb, s)) return st;
+      need_dW = false;
+    }
+  }
+  if (tc && need_dX) {
+    ConvTcP cp = dgrad_cp(B, d, sh, dY.ptr, dY.bstride, W.ptr, W.bstride, W.ld, dX.ptr, dX.bstride);
+    if (conv_tc_supported(cp)) {
+      if (hfta_status st = conv_tc(cp, s)) return st;
+      need_dX = false;
+    }
+  }
+  if (!need_dW && !need_dX) return post_launch(s, "hfta_fused_conv_bwd");
+  HFTA_REQUIRE(colb > 0, HFTA_ERR_UNSUPPORTED, "conv_bwd: operands not eligible for the implicit-GEMM path "
+               "(alignment / model strides) and no patch-matrix workspace for this configuration");
+  if (!need_dW) dW = nullptr;
+  if (!need_dX) dX.ptr = nullptr;
   if (!sh.transposed) {
     const int nb = X.bstride == 0 ? 1 : B;
     const int64_t cbs = X.bstride == 0 ? 0 : sh.Ms * sh.Kc;

@@ -50,6 +50,27 @@ hfta_status colsum_reduce(const GemmP& p, cudaStream_t s);   // colsum (+)= sum_
 hfta_status gemm_tc(const GemmP& p, hfta_dtype dt_in, bool out_f32, cudaStream_t s);
 bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32);
 
+// Implicit-GEMM convolution on the tcgen05 engine (kernel 4x4, stride 2, pad 1;
+// gemm_tc.cu CONV modes; no im2col / col2im buffer).  Image tensors are dense
+// NHWC per model [B][n][h][w][c] with c % 64 == 0 (bstride 0 = shared).
+struct ConvTcP {
+  int mode;                 // 1 Conv2d fwd / ConvT2d dgrad, 2 sub-pixel phases (ConvT2d fwd / Conv2d dgrad),
+                            // 3 Conv2d wgrad, 4 ConvT2d wgrad
+  int B;
+  int64_t M, N, K;          // GEMM extents (mode 2: per phase)
+  const void* img; int64_t img_bs; int img_n, img_h, img_w, img_c;   // the gathered / shifted image operand
+  int grid_w, grid_h;       // grid the GEMM rows (1, 2) / reduction rows (3, 4) enumerate
+  const void* opd; int64_t opd_bs, opd_ld;   // 1: W [N][K] (K-major) or Wt [K][N] (w_mn); 2: weights;
+                                             // 3: dY [K][M] (ld M); 4: X [K][N] (ld N)
+  int w_mn;                 // 1: B MN-major (ConvT dgrad); 2: Conv2d weights [Ca][16][Cn] (else ConvT [16][Cn][Ca])
+  int w_cn, w_ca;           // mode 2 weight dims
+  void* C; int64_t c_bs, c_ld;   // 1: Y [B][M][N] bf16; 2: Y image (c_bs = model stride); 3, 4: dW fp32 (ld c_ld)
+  int y_h, y_w;             // mode 2: output image size
+  int accumulate; int splits; int64_t k_chunk; float* part;   // 3, 4: split-K over the reduction rows
+};
+bool conv_tc_supported(const ConvTcP& p);
+hfta_status conv_tc(const ConvTcP& p, cudaStream_t s);
+
 // Dispatch: skinny -> tcgen05 -> SIMT (EPI features: skinny / tcgen05 only).
 hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void* ws = nullptr, size_t wsb = 0);
 

@@ -52,7 +52,29 @@ struct TcArgs {
                                      // read from the resident smem stage (released by the epilogue)
   float* colsum; int64_t colsum_bs; int colsum_acc; float* colsum_part;   // fused column sums of A
   int ab_same;                       // Gram X^T X (A == B, one 128-wide tile): B is read from the A stage
+  // implicit-GEMM convolution geometry (CONV > 0; kernel 4x4, stride 2, pad 1)
+  int gw, gh, ghw;                   // the image grid the GEMM rows (CONV 1, 2) / reduction rows (3, 4) enumerate
+  int cblk;                          // CONV 1, 2: 64-channel blocks per tap of the image operand
+  int cg;                            // CONV 3: channels per tap of B (C_in); CONV 4: rows per tap of A (C_out)
+  int y_c, y_h, y_w; int64_t y_bs;   // CONV 2: output image [B][n][y_h][y_w][y_c] the phases interleave into
 };
+
+// Row index r of a dense NHWC grid (gw x gh per image) -> (image, row, col), 32-bit.
+__device__ __forceinline__ void grid_pos(uint32_t r, const TcArgs& p, int& n, int& y, int& x) {
+  n = (int)(r / (uint32_t)p.ghw);
+  const uint32_t rem = r - (uint32_t)n * (uint32_t)p.ghw;
+  y = (int)(rem / (uint32_t)p.gw);
+  x = (int)(rem - (uint32_t)y * (uint32_t)p.gw);
+}
+
+// Sub-pixel taps of a k4 s2 p1 ConvTranspose2d (and of the matching Conv2d
+// dgrad, its adjoint): output row 2i + par takes input rows i + off from
+// kernel rows kh, for t = 0, 1:  par 0 -> (kh 1, off 0), (kh 3, off -1);
+// par 1 -> (kh 0, off +1), (kh 2, off 0).
+__device__ __forceinline__ void phase_tap(int par, int t, int& k, int& off) {
+  k = par ? (t ? 2 : 0) : (t ? 3 : 1);
+  off = par ? (t ? 0 : 1) : (t ? -1 : 0);
+}
 
 // (a, b) += (c, d) as one packed FADD2
 __device__ __forceinline__ void add_f32x2(float& a, float& b, float c, float d) {
@@ -88,7 +110,18 @@ __device__ __forceinline__ void tile_coords(uint32_t t, const TcArgs& p, int& mt
 // this tile's A (or A2) stage still resident in smem, optionally with a second
 // K segment (A2, B2) accumulated into the same tile (non-BRES).  Separate
 // instantiations keep each epilogue branch-free and small.
-template <bool A_MN, bool B_MN, int BN, int STAGES, bool OUT_F32, bool BRES, int EPI>
+// CONV (implicit-GEMM convolution, no im2col / col2im buffer in HBM; the
+// image operand is gathered by TMA with traversal strides, 5-D maps
+// {C, W, H, N, B}, SWIZZLE_128B boxes of whole grid rows):
+//   1  Conv2d fwd:          A(m = (n,oy,ox), k = (kh,kw,ci)) = X[n][2oy-1+kh][2ox-1+kw][ci]   (stride-2 gather)
+//                           B = W [Co][(kh,kw,ci)] K-major
+//   2  ConvT2d fwd / Conv2d dgrad, one of 4 sub-pixel phases per `split`:
+//                           A(m = (n,i,j), k = (t,c)) = X[n][i+off_t][j+off_t][c]       (shifted box)
+//                           B = the tap's weight slice (K-major ConvT, MN-major Conv dgrad);
+//                           the epilogue interleaves row (n,i,j) into output pixel (n, 2i+ph, 2j+pw)
+//   3  Conv2d wgrad:        A = dY (MN-major), B(k = (n,oy,ox), n = (tap,ci)) gathered (stride 2)
+//   4  ConvT2d wgrad:       A(k = (n,i,j), m = (tap,co)) = dY[n][2i-1+kh][2j-1+kw][co] gathered, B = X (MN-major)
+template <bool A_MN, bool B_MN, int BN, int STAGES, bool OUT_F32, bool BRES, int EPI, int CONV = 0>
 __global__ void __launch_bounds__(NTHREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
@@ -176,12 +209,14 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
         int mt, nt, split, b;
         tile_coords((uint32_t)t, p, mt, nt, split, b);
-        const int64_t kbeg = (int64_t)split * p.k_chunk;
-        const int64_t kend = min(p.K, kbeg + p.k_chunk);
+        const int64_t kbeg = CONV == 2 ? 0 : (int64_t)split * p.k_chunk;
+        const int64_t kend = CONV == 2 ? p.K : min(p.K, kbeg + p.k_chunk);
         const int nkb1 = (int)((kend - kbeg + BK - 1) / BK);
         const int nkb = nkb1 + (EPI == 2 ? (int)((p.K2 + BK - 1) / BK) : 0);
         const int ba = p.a_shared ? 0 : b, bb = p.b_shared ? 0 : b;
         const int m0 = mt * BM, n0 = nt * BN;
+        int gn0 = 0, gy0 = 0, gx0 = 0;            // CONV 1, 2: grid position of the tile's first row
+        if constexpr (CONV == 1 || CONV == 2) grid_pos((uint32_t)m0, p, gn0, gy0, gx0);
         if constexpr (BRES) {
           const int64_t key = (int64_t)bb * p.tiles_n + nt;
           if (key != bkey) {                       // new (model, n-tile): reload the resident B
@@ -200,7 +235,49 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           mbar_expect_tx(&full[stage], (CSUM && p.ab_same) ? A_BYTES : LOAD_BYTES);
           (void)sb;
           const int k0 = (int)(kbeg + (int64_t)kb * BK);
-          if (EPI == 2 && kb >= nkb1) {                   // second K segment (K-major A2, B2)
+          if constexpr (CONV == 1) {                      // stride-2 gather of the input image
+            const int tap = kb / p.cblk, cb = kb - tap * p.cblk;
+            tma_load_5d(sa, &tmA, &full[stage], cb * 64, 2 * gx0 - 1 + (tap & 3), 2 * gy0 - 1 + (tap >> 2), gn0, ba);
+            if constexpr (B_MN) {                         // ConvT dgrad: B(n = ci, k = (tap, co)) = Wt[tap][co][ci]
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
+            } else {
+              tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
+            }
+          } else if constexpr (CONV == 2) {               // sub-pixel phase `split`, tap t of 4
+            const int t4 = kb / p.cblk, cb = kb - t4 * p.cblk;
+            int kh, oh, kw, ow;
+            phase_tap(split >> 1, t4 >> 1, kh, oh);
+            phase_tap(split & 1, t4 & 1, kw, ow);
+            tma_load_5d(sa, &tmA, &full[stage], cb * 64, gx0 + ow, gy0 + oh, gn0, ba);
+            const int tap = kh * 4 + kw;
+            if constexpr (B_MN) {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j) tma_load_4d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, tap, cb * 64, bb);
+            } else {
+              tma_load_4d(sb, &tmB, &full[stage], cb * 64, n0, tap, bb);
+            }
+          } else if constexpr (CONV == 3) {               // dY plain, B = stride-2 gather of X per (tap, ci) atom
+            tma_load_3d(sa, &tmA, &full[stage], m0, k0, ba);
+            tma_load_3d(sa + 8192, &tmA, &full[stage], m0 + 64, k0, ba);
+            int gn, gy, gx;
+            grid_pos((uint32_t)k0, p, gn, gy, gx);
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) {
+              const int ncol = n0 + 64 * j, tap = ncol / p.cg, ci0 = ncol - tap * p.cg;
+              tma_load_5d(sb + j * 8192, &tmB, &full[stage], ci0, 2 * gx - 1 + (tap & 3), 2 * gy - 1 + (tap >> 2), gn, bb);
+            }
+          } else if constexpr (CONV == 4) {               // A = stride-2 gather of dY per (tap, co) atom, X plain
+            int gn, gy, gx;
+            grid_pos((uint32_t)k0, p, gn, gy, gx);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int mm = m0 + 64 * j, tap = mm / p.cg, co0 = mm - tap * p.cg;
+              tma_load_5d(sa + j * 8192, &tmA, &full[stage], co0, 2 * gx - 1 + (tap & 3), 2 * gy - 1 + (tap >> 2), gn, ba);
+            }
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
+          } else if (EPI == 2 && kb >= nkb1) {            // second K segment (K-major A2, B2)
             const int k2 = (kb - nkb1) * BK;
             tma_load_3d(sa, &tmA2, &full[stage], k2, m0, b);
             if constexpr (!BRES) tma_load_3d(sb, &tmB2, &full[stage], k2, n0, b);
@@ -210,7 +287,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           } else {
             tma_load_3d(sa, &tmA, &full[stage], k0, m0, ba);
           }
-          if (EPI == 2 && kb >= nkb1) {
+          if (CONV != 0 || (EPI == 2 && kb >= nkb1)) {
           } else if (CSUM && p.ab_same) {                 // Gram: the A tile is also B
           } else if constexpr (!BRES) {
             if (B_MN) {
@@ -247,8 +324,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           ++epoch;
         }
       }
-      const int64_t kbeg = (int64_t)split * p.k_chunk;
-      const int64_t kend = min(p.K, kbeg + p.k_chunk);
+      const int64_t kbeg = CONV == 2 ? 0 : (int64_t)split * p.k_chunk;
+      const int64_t kend = CONV == 2 ? p.K : min(p.K, kbeg + p.k_chunk);
       const int nkb = (int)((kend - kbeg + BK - 1) / BK) + (EPI == 2 ? (int)((p.K2 + BK - 1) / BK) : 0);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
@@ -368,7 +445,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         uint8_t* buf = stage_out + ew * 4096;  // bf16 staging: this warp's 32 x 64 sub-tile
         const uint32_t rowaddr = smem_u32(buf) + lane * 128;
         const uint32_t sw = (uint32_t)(lane & 7);
-        if (!OUT_F32 && n0 < p.N) {      // the previous store of this warp (a tile ago) has read its staging
+        if (!OUT_F32 && CONV != 2 && n0 < p.N) {   // the previous store of this warp (a tile ago) has read its staging
           if (lane == 0) tma_store_wait_read<0>();
           __syncwarp();
         }
@@ -462,7 +539,26 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               released = true;
             }
           }
-          if constexpr (!OUT_F32) {
+          if constexpr (CONV == 2) {
+            // sub-pixel phase: row m = (n, i, j) of the phase grid -> output pixel (n, 2i+ph, 2j+pw);
+            // each thread stores its row's 32 columns (64 B) directly
+            if (row_ok) {
+              int gn, gy, gx;
+              grid_pos((uint32_t)m, p, gn, gy, gx);
+              const int64_t pix = ((int64_t)gn * p.y_h + 2 * gy + (split >> 1)) * p.y_w + 2 * gx + (split & 1);
+              uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C) + (int64_t)b * p.y_bs +
+                                                    pix * p.y_c + c0);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if (c0 + 8 * q >= p.N) break;
+                uint4 w4;
+                __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+                dst[q] = w4;
+              }
+            }
+          } else if constexpr (!OUT_F32) {
             // bf16: 16-B chunk q of row r at chunk q ^ (r & 7) (TMA SWIZZLE_128B layout, conflict-free);
             // rows >= M and columns >= N are clipped by the tensor map
 #pragma unroll
@@ -638,7 +734,157 @@ hfta_status dispatch_bn(const GemmP& p, cudaStream_t s) {
   return launch_tc<A_MN, B_MN, 256, OUT_F32, false>(p, s);
 }
 
+// `rows` consecutive rows of a dense (n, y, x) enumeration of a gw x gh grid
+// (gn images) as one box of whole grid rows / images: (bw, bh, bn)
+bool grid_box(int gw, int gh, int gn, int rows, uint32_t& bw, uint32_t& bh, uint32_t& bn) {
+  if (gw >= rows) {
+    bw = rows; bh = 1; bn = 1;
+    return gw % rows == 0;
+  }
+  if (rows % gw) return false;
+  bw = gw;
+  const int r = rows / gw;
+  if (gh >= r) {
+    bh = r; bn = 1;
+    return gh % r == 0;
+  }
+  if (r % gh) return false;
+  bh = gh; bn = r / gh;
+  return gn % (int)bn == 0;
+}
+
+// 5-D map of the image operand {C, W, H, N, B} gathering `rows` grid rows per
+// box with traversal stride `st` along W and H (2: Conv2d k4 s2 p1 windows,
+// 1: the shifted ConvT / dgrad phase boxes)
+hfta_status img_map(CUtensorMap* m, const ConvTcP& p, int nb, int rows, int st) {
+  uint32_t bw, bh, bn;
+  if (!grid_box(p.grid_w, p.grid_h, p.img_n, rows, bw, bh, bn))
+    return fail(HFTA_ERR_UNSUPPORTED, "conv_tc: grid %dx%d does not tile into %d-row boxes", p.grid_w, p.grid_h, rows);
+  const int64_t hw = (int64_t)p.img_h * p.img_w * p.img_c;
+  const int64_t dims[5] = {p.img_c, p.img_w, p.img_h, p.img_n, nb};
+  const int64_t str[5] = {1, p.img_c, (int64_t)p.img_w * p.img_c, hw, nb > 1 ? p.img_bs : (int64_t)p.img_n * hw};
+  const uint32_t box[5] = {64, (uint32_t)st * bw, (uint32_t)st * bh, bn, 1};
+  const uint32_t es[5] = {1, (uint32_t)st, (uint32_t)st, 1, 1};
+  return make_map_nd(m, p.img, 5, dims, str, box, es);
+}
+
+template <int CONV, bool A_MN, bool B_MN, int BN, bool OUT_F32>
+hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
+  constexpr int STAGES = (BN == 256) ? 3 : 4;
+  constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + (OUT_F32 ? 0 : NEPI_ALL * 4096) +
+                          NEPI_ALL * BN * 4 + ((A_MN && B_MN && OUT_F32) ? (size_t)STAGES * 8192 : 0);
+  static_assert(SMEM <= 232448, "shared memory budget");
+  if (hfta_status st = get_encode()) return st;
+  CUtensorMap ta, tb, tc_;
+  const int nbi = cp.img_bs == 0 ? 1 : cp.B;
+  const int nbo = cp.opd_bs == 0 ? 1 : cp.B;
+  hfta_status st = HFTA_OK;
+  if (CONV == 1) {
+    st = img_map(&ta, cp, nbi, BM, 2);
+    if (!st) st = B_MN ? make_map(&tb, cp.opd, cp.N, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, BK)
+                       : make_map(&tb, cp.opd, cp.K, cp.N, cp.opd_ld, cp.opd_bs, nbo, BK, BN);
+  } else if (CONV == 2) {
+    st = img_map(&ta, cp, nbi, BM, 1);
+    if (!st) {
+      const int64_t cn = cp.w_cn, ca = cp.w_ca, wbs = nbo > 1 ? cp.opd_bs : 16 * cn * ca;
+      if (B_MN) {        // Conv2d weights W [Ca][16][Cn] (n = ci contiguous, k = co)
+        const int64_t dims[4] = {cn, 16, ca, nbo}, str[4] = {1, cn, 16 * cn, wbs};
+        const uint32_t box[4] = {64, 1, 64, 1}, es[4] = {1, 1, 1, 1};
+        st = make_map_nd(&tb, cp.opd, 4, dims, str, box, es);
+      } else {           // ConvT2d weights Wt [16][Cn][Ca] (rows n = co, k = ci contiguous)
+        const int64_t dims[4] = {ca, cn, 16, nbo}, str[4] = {1, ca, cn * ca, wbs};
+        const uint32_t box[4] = {64, (uint32_t)BN, 1, 1}, es[4] = {1, 1, 1, 1};
+        st = make_map_nd(&tb, cp.opd, 4, dims, str, box, es);
+      }
+    }
+  } else if (CONV == 3) {
+    st = make_map(&ta, cp.opd, cp.M, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, BK);
+    if (!st) st = img_map(&tb, cp, nbi, BK, 2);
+  } else {
+    st = img_map(&ta, cp, nbi, BK, 2);
+    if (!st) st = make_map(&tb, cp.opd, cp.N, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, BK);
+  }
+  if (st) return st;
+  tc_ = tb;
+  if (CONV == 1) {         // Y [B][M][N] bf16 through the TMA-store epilogue
+    cuuint64_t dims[3] = {(cuuint64_t)cp.N, (cuuint64_t)cp.M, (cuuint64_t)cp.B};
+    cuuint64_t strides[2] = {(cuuint64_t)(cp.c_ld * 2), (cuuint64_t)((cp.B > 1 ? cp.c_bs : cp.M * cp.c_ld) * 2)};
+    cuuint32_t box[3] = {64, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_encode(&tc_, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, cp.C, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(HFTA_ERR_CUDA, "cuTensorMapEncodeTiled (conv Y) failed (%d)", (int)r);
+  }
+  TcArgs a{};
+  a.B = cp.B; a.M = cp.M; a.N = cp.N; a.K = cp.K;
+  a.splits = CONV == 2 ? 4 : (CONV == 1 ? 1 : std::max(cp.splits, 1));     // mode 2: the 4 phases
+  a.k_chunk = (CONV == 1 || CONV == 2 || cp.k_chunk <= 0) ? cp.K : cp.k_chunk;
+  a.a_shared = (CONV == 1 || CONV == 2 || CONV == 4) ? (nbi == 1 && cp.B > 1) : (nbo == 1 && cp.B > 1);
+  a.b_shared = (CONV == 3) ? (nbi == 1 && cp.B > 1) : (nbo == 1 && cp.B > 1);
+  a.C = cp.C; a.c_bs = cp.c_bs; a.c_ld = cp.c_ld;
+  a.accumulate = cp.accumulate; a.part = cp.part;
+  a.tiles_m = (int)cdiv(cp.M, BM); a.tiles_n = (int)cdiv(cp.N, BN);
+  a.order = (A_MN && B_MN) ? 1 : 0;
+  a.mask_kb = -1;
+  a.gw = cp.grid_w; a.gh = cp.grid_h; a.ghw = cp.grid_w * cp.grid_h;
+  a.cblk = cp.img_c / 64;
+  a.cg = cp.img_c;   // 3: C_in per tap of B; 4: C_out (the gathered dY's channels) per tap of A
+  a.y_c = (int)cp.N; a.y_h = cp.y_h; a.y_w = cp.y_w; a.y_bs = cp.c_bs;
+  auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, false, 0, CONV>;
+  ensure_smem(kern, SMEM);
+  const int64_t total = (int64_t)a.tiles_m * a.tiles_n * a.splits * a.B;
+  HFTA_REQUIRE(total < ((int64_t)1 << 31), HFTA_ERR_SHAPE, "conv_tc: %lld tiles exceed int32", (long long)total);
+  const int grid = (int)std::min<int64_t>(total, num_sms());
+  kern<<<grid, NTHREADS, SMEM, s>>>(ta, tb, tc_, ta, tb, a);
+  count_launches(1);
+  return post_launch(s, "conv_tc");
+}
+
 }  // namespace
+
+bool conv_tc_supported(const ConvTcP& p) {
+  if (p.M < 1 || p.N < 1 || p.K < 1 || p.img_c % 64 || !aligned16(p.img) || !aligned16(p.opd) || !aligned16(p.C))
+    return false;
+  if ((p.img_bs * 2) % 16 || (p.opd_bs * 2) % 16 || (p.opd_ld * 2) % 16) return false;
+  uint32_t bw, bh, bn;
+  const int rows = (p.mode == 1 || p.mode == 2) ? BM : BK;
+  if (!grid_box(p.grid_w, p.grid_h, p.img_n, rows, bw, bh, bn)) return false;
+  switch (p.mode) {
+    case 1: return p.K == 16 * (int64_t)p.img_c && p.N % 16 == 0 && (p.c_ld * 2) % 16 == 0 && (p.c_bs * 2) % 16 == 0;
+    case 2: return p.K == 4 * (int64_t)p.img_c && p.N % 8 == 0 && p.N <= 256 && p.y_h == 2 * p.grid_h &&
+                   p.y_w == 2 * p.grid_w && (p.c_bs * 2) % 16 == 0;
+    case 3: return p.N == 16 * (int64_t)p.img_c && p.c_ld % 4 == 0;
+    case 4: return p.M == 16 * (int64_t)p.img_c && p.N % 16 == 0 && p.c_ld % 4 == 0;
+    default: return false;
+  }
+}
+
+hfta_status conv_tc(const ConvTcP& p, cudaStream_t s) {
+  if (!conv_tc_supported(p)) return fail(HFTA_ERR_UNSUPPORTED, "conv_tc: configuration not supported");
+  switch (p.mode) {
+    case 1:
+      if (p.w_mn) {
+        if (p.N <= 64) return launch_conv<1, false, true, 64, false>(p, s);
+        if (p.N <= 128) return launch_conv<1, false, true, 128, false>(p, s);
+        return launch_conv<1, false, true, 256, false>(p, s);
+      }
+      if (p.N <= 64) return launch_conv<1, false, false, 64, false>(p, s);
+      if (p.N <= 128) return launch_conv<1, false, false, 128, false>(p, s);
+      return launch_conv<1, false, false, 256, false>(p, s);
+    case 2:
+      if (p.w_mn) {
+        if (p.N <= 64) return launch_conv<2, false, true, 64, false>(p, s);
+        if (p.N <= 128) return launch_conv<2, false, true, 128, false>(p, s);
+        return launch_conv<2, false, true, 256, false>(p, s);
+      }
+      if (p.N <= 64) return launch_conv<2, false, false, 64, false>(p, s);
+      if (p.N <= 128) return launch_conv<2, false, false, 128, false>(p, s);
+      return launch_conv<2, false, false, 256, false>(p, s);
+    case 3: return launch_conv<3, true, true, 128, true>(p, s);
+    default: return launch_conv<4, true, true, 128, true>(p, s);
+  }
+}
 
 bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32) {
   if (dt_in != HFTA_BF16) return false;

@@ -44,7 +44,16 @@ Split wgrad_split(int B, int64_t M, int64_t N, int64_t K) {
   const int64_t chunk = cdiv(cdiv(M, best_s), 128) * 128;
   return {(int)cdiv(M, chunk), chunk};
 }
+}  // namespace
 
+// the same policy for callers outside this file (implicit-GEMM conv wgrad)
+void wgrad_split_rows(int B, int64_t rows, int64_t N, int64_t K, int* splits, int64_t* chunk) {
+  Split sp = wgrad_split(B, rows, N, K);
+  *splits = sp.splits;
+  *chunk = sp.chunk;
+}
+
+namespace {
 
 hfta_status check_in(const hfta_in& t, const char* name, int B) {
   HFTA_REQUIRE(t.ptr, HFTA_ERR_INVALID_VALUE, "%s.ptr is NULL", name);

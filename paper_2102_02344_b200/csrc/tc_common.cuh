@@ -43,6 +43,22 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -185,6 +201,30 @@ hfta_status make_map(CUtensorMap* m, const void* ptr, int64_t inner, int64_t row
   return HFTA_OK;
 }
 
+
+// N-d bf16 map (rank <= 5): dims / strides in elements (strides[0] = 1
+// implied), SWIZZLE_128B, element (traversal) strides es; a box of box[i]
+// elements along dim i delivers ceil(box[i] / es[i]) of them (measured,
+// tools/micro/tma_stride.cu), out-of-bounds coordinates (also negative) zero-fill.
+hfta_status make_map_nd(CUtensorMap* m, const void* ptr, int rank, const int64_t* dims, const int64_t* strides,
+                        const uint32_t* box, const uint32_t* es) {
+  cuuint64_t d[5], st[4];
+  cuuint32_t bx[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = (cuuint64_t)dims[i];
+    bx[i] = box[i];
+    e[i] = es[i];
+    if (i > 0) st[i - 1] = (cuuint64_t)(strides[i] * 2);
+  }
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), d, st, bx, e,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(HFTA_ERR_CUDA, "cuTensorMapEncodeTiled (%d-d) failed (%d): dims %lld %lld %lld %lld %lld", rank, (int)r,
+                (long long)dims[0], (long long)(rank > 1 ? dims[1] : 0), (long long)(rank > 2 ? dims[2] : 0),
+                (long long)(rank > 3 ? dims[3] : 0), (long long)(rank > 4 ? dims[4] : 0));
+  return HFTA_OK;
+}
 
 }  // namespace
 }  // namespace hfta

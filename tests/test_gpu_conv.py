@@ -1,0 +1,141 @@
+"""Per-layer parity of the fused (de)convolution (hfta_fused_conv_fwd/bwd,
+App. B rows Conv2d P:L1262-1263 / ConvT2d P:L1268-1269, Fig. 3)
+against oracle.layers.conv2d_* / convT2d_* at every DCGAN layer shape of the
+benched batch (N = 128 images of 64 x 64, BJ configs[3]), B in {1, 3}, shared
+input images (bstride 0, as D(real) sees them) and per-model ones.
+
+Paths covered: the implicit-GEMM tcgen05 modes (stride-2 TMA gather:
+D c2-c4 fwd and wgrad, G t2-t4 dgrad; sub-pixel phases: G t2-t5 fwd, D c1-c4
+dgrad; ConvT wgrad: G t2-t4), the dense-GEMM layers (G t1, D c5) and the
+patch-matrix fallback (D c1 fwd / wgrad, G t5 dgrad / wgrad: 8-channel
+images); fp32 runs the fallback everywhere.
+
+Inputs are rounded to the operand dtype before the oracle sees them, so the
+oracle and the kernel contract the same values (reading R16).  Gates
+(normwise per model, reading R20): bf16 outputs 1e-2 (their own bf16
+rounding ~2e-3), fp32 outputs 1e-5; dW (fp32 accumulation) 1e-4 bf16 /
+1e-5 fp32.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import layers as OL
+from tests._cmp import assert_close
+
+pytestmark = pytest.mark.gpu
+
+H = None
+DEV = "cuda"
+
+#         name  transposed  H   C_in C_out  k  s  p
+LAYERS = [("D.c1", 0, 64, 8, 64, 4, 2, 1),
+          ("D.c2", 0, 32, 64, 128, 4, 2, 1),
+          ("D.c3", 0, 16, 128, 256, 4, 2, 1),
+          ("D.c4", 0, 8, 256, 512, 4, 2, 1),
+          ("D.c5", 0, 4, 512, 1, 4, 1, 0),
+          ("G.t1", 1, 1, 104, 512, 4, 1, 0),
+          ("G.t2", 1, 4, 512, 256, 4, 2, 1),
+          ("G.t3", 1, 8, 256, 128, 4, 2, 1),
+          ("G.t4", 1, 16, 128, 64, 4, 2, 1),
+          ("G.t5", 1, 32, 64, 8, 4, 2, 1)]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _init():
+    global H
+    import paper_2102_02344_b200.hfta as hfta
+    hfta.hfta_init(0)
+    H = hfta
+
+
+def s():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def rnd(a, tdt):
+    return torch.tensor(a).to(tdt).double().numpy()
+
+
+def host(t):
+    return t.detach().float().cpu().numpy().astype(np.float64)
+
+
+def run_layer(layer, B, N, dtype, shared, seed=0):
+    name, tr, Hs, Ci, Co, k, st, pd = layer
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    code = 1 if dtype == "bf16" else 0
+    rng = np.random.default_rng(seed)
+    Ho = (Hs - 1) * st - 2 * pd + k if tr else (Hs + 2 * pd - k) // st + 1
+    nb = 1 if shared else B
+    X = rnd(rng.standard_normal((nb, N, Hs, Hs, Ci)), tdt)                       # NHWC
+    if tr:    # ConvT weight, arena layout [kh][kw][Co][Ci]; torch [Ci][Co][kh][kw]
+        Wg = rnd(rng.standard_normal((B, k, k, Co, Ci)) / np.sqrt(Ci), tdt)
+        Wt = Wg.transpose(0, 4, 3, 1, 2)
+        wld = Ci
+    else:     # Conv weight, arena layout [Co][kh][kw][Ci]; torch [Co][Ci][kh][kw]
+        Wg = rnd(rng.standard_normal((B, Co, k, k, Ci)) / np.sqrt(k * k * Ci), tdt)
+        Wt = Wg.transpose(0, 1, 4, 2, 3)
+        wld = k * k * Ci
+    dY = rnd(rng.standard_normal((B, N, Ho, Ho, Co)), tdt)
+    dW0 = rng.standard_normal(Wg.shape).astype(np.float32).astype(np.float64)
+
+    d = H.hfta_conv_desc()
+    d.N, d.H, d.W, d.C_in, d.C_out, d.kh, d.kw, d.stride, d.pad, d.transposed = N, Hs, Hs, Ci, Co, k, k, st, pd, tr
+    dev = lambda a: torch.tensor(a).to(tdt).to(DEV).contiguous()
+    Xd, Wd, dYd = dev(X), dev(Wg), dev(dY)
+    Y = torch.empty(B, N, Ho, Ho, Co, dtype=tdt, device=DEV)
+    dX = torch.empty(B, N, Hs, Hs, Ci, dtype=tdt, device=DEV)
+    dW = torch.tensor(dW0, dtype=torch.float32, device=DEV).contiguous()
+    ws = torch.empty(max(H.hfta_fused_conv_workspace(B, d, code), 256), dtype=torch.uint8, device=DEV)
+    xbs = 0 if shared else N * Hs * Hs * Ci
+    wbs = int(np.prod(Wg.shape[1:]))
+    H.hfta_fused_conv_fwd(B, d, code, H.tin(Xd, xbs, Ci), H.tin(Wd, wbs, wld), H.tout(Y, N * Ho * Ho * Co, Co),
+                          H.ptr(ws), ws.numel(), s())
+    H.hfta_fused_conv_bwd(B, d, code, H.tin(dYd, N * Ho * Ho * Co, Co), H.tin(Xd, xbs, Ci), H.tin(Wd, wbs, wld),
+                          H.tout(dX, N * Hs * Hs * Ci, Ci), H.ptr(dW), wbs, 1, H.ptr(ws), ws.numel(), s())
+    torch.cuda.synchronize()
+    return dict(X=X, Wt=Wt, dY=dY, dW0=dW0, Y=host(Y), dX=host(dX), dW=host(dW), Ho=Ho)
+
+
+def check(layer, B, N, dtype, shared):
+    name, tr, Hs, Ci, Co, k, st, pd = layer
+    r = run_layer(layer, B, N, dtype, shared)
+    tol_o = 1e-2 if dtype == "bf16" else 1e-5
+    tol_w = 1e-4 if dtype == "bf16" else 1e-5
+    for b in range(B):
+        xb = r["X"][0 if shared else b].transpose(0, 3, 1, 2)          # NCHW
+        dyb = r["dY"][b].transpose(0, 3, 1, 2)
+        Wt = r["Wt"][b]
+        if tr:
+            y = OL.convT2d_fwd(xb, Wt, st, pd)
+            dx, dw = OL.convT2d_bwd(dyb, xb, Wt, st, pd)
+            dw_g = dw.transpose(2, 3, 1, 0)                            # [Ci][Co][kh][kw] -> [kh][kw][Co][Ci]
+        else:
+            y = OL.conv2d_fwd(xb, Wt, st, pd)
+            dx, dw = OL.conv2d_bwd(dyb, xb, Wt, st, pd)
+            dw_g = dw.transpose(0, 2, 3, 1)                            # [Co][Ci][kh][kw] -> [Co][kh][kw][Ci]
+        assert_close(r["Y"][b], y.transpose(0, 2, 3, 1), tol_o, "%s model %d Y" % (name, b))
+        assert_close(r["dX"][b], dx.transpose(0, 2, 3, 1), tol_o, "%s model %d dX" % (name, b))
+        assert_close(r["dW"][b], r["dW0"][b] + dw_g, tol_w, "%s model %d dW (accumulate)" % (name, b))
+
+
+@pytest.mark.parametrize("layer", LAYERS, ids=[l[0] for l in LAYERS])
+@pytest.mark.parametrize("B", [1, 3])
+def test_conv_layer_bf16_full_batch(layer, B):
+    """Every DCGAN layer at N = 128 (the bench's batch); D layers with the
+    shared input image when B = 3."""
+    check(layer, B, 128, "bf16", shared=(B == 3 and layer[0].startswith("D")))
+
+
+@pytest.mark.parametrize("layer", LAYERS, ids=[l[0] for l in LAYERS])
+def test_conv_layer_f32(layer):
+    """fp32 (patch-matrix path), N = 8, B = 2, per-model inputs."""
+    check(layer, 2, 8, "f32", shared=False)
+
+
+def test_conv_layer_bf16_per_model_inputs():
+    """Implicit-GEMM modes with per-model (non-shared) images, B = 2, N = 32."""
+    for layer in LAYERS:
+        if layer[0] in ("D.c2", "D.c3", "D.c4", "G.t2", "G.t3", "G.t4", "G.t5"):
+            check(layer, 2, 32, "bf16", shared=False)
