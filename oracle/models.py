@@ -94,61 +94,101 @@ def mlp_cfg1_loss_grads(P, S, x, T):
 
 # ---------------------------------------------------------- PointNet ----
 
-def _stn_fwd(P, S, newS, x):
-    N, L, _ = x.shape
-    r = x.reshape(N * L, 3)
-    a1, k1 = _conv_bn_act(P, S, newS, r, "stn.c1", "stn.bn1", "relu")
-    a2, k2 = _conv_bn_act(P, S, newS, a1, "stn.c2", "stn.bn2", "relu")
-    a3, k3 = _conv_bn_act(P, S, newS, a2, "stn.c3", "stn.bn3", "relu")
-    g, idx = _max_pool("stn.max", a3.reshape(N, L, -1), k3["esc"])
-    f1, k4 = _conv_bn_act(P, S, newS, g, "stn.fc1", "stn.bn4", "relu")
-    f2, k5 = _conv_bn_act(P, S, newS, f1, "stn.fc2", "stn.bn5", "relu")
-    f3, f2s, W3s = _lin(P, f2, "stn.fc3")
-    T = f3.reshape(N, 3, 3) + np.eye(3)
-    return T, dict(k=(k1, k2, k3, k4, k5), idx=idx, f2=f2s, W3=W3s, L=L)
+def _stn_fwd(P, S, newS, x, pre="stn"):
+    """STN3d (pre "stn", x = points [N, L, 3]) or STNkd (pre "fstn", x = the
+    64-d point features [N, L, k]): conv k->64->128->1024 (BN, ReLU), max over
+    points, fc 1024->512->256 (BN, ReLU), fc 256->k*k, + I_k (reading R1)."""
+    N, L, k = x.shape
+    r = x.reshape(N * L, k)
+    a1, k1 = _conv_bn_act(P, S, newS, r, pre + ".c1", pre + ".bn1", "relu")
+    a2, k2 = _conv_bn_act(P, S, newS, a1, pre + ".c2", pre + ".bn2", "relu")
+    a3, k3 = _conv_bn_act(P, S, newS, a2, pre + ".c3", pre + ".bn3", "relu")
+    g, idx = _max_pool(pre + ".max", a3.reshape(N, L, -1), k3["esc"])
+    f1, k4 = _conv_bn_act(P, S, newS, g, pre + ".fc1", pre + ".bn4", "relu")
+    f2, k5 = _conv_bn_act(P, S, newS, f1, pre + ".fc2", pre + ".bn5", "relu")
+    f3, f2s, W3s = _lin(P, f2, pre + ".fc3")
+    T = f3.reshape(N, k, k) + np.eye(k)
+    return T, dict(k=(k1, k2, k3, k4, k5), idx=idx, f2=f2s, W3=W3s, L=L, pre=pre)
 
 
-def _stn_bwd(P, G, dT, c):
-    N = dT.shape[0]
-    df2, G["stn.fc3.W"], G["stn.fc3.b"] = _lin_bwd(dT.reshape(N, 9), c["f2"], c["W3"])
+def _stn_bwd(P, G, dT, c, need_dx=False):
+    N, k, _ = dT.shape
+    pre = c["pre"]
+    df2, G[pre + ".fc3.W"], G[pre + ".fc3.b"] = _lin_bwd(dT.reshape(N, k * k), c["f2"], c["W3"])
     k1, k2, k3, k4, k5 = c["k"]
     df1 = _conv_bn_act_bwd(P, G, df2, k5)
     dg = _conv_bn_act_bwd(P, G, df1, k4)
     da3 = Lr.max_over_points_bwd(dg, c["idx"], c["L"]).reshape(-1, dg.shape[1])
     da2 = _conv_bn_act_bwd(P, G, da3, k3)
     da1 = _conv_bn_act_bwd(P, G, da2, k2)
-    _conv_bn_act_bwd(P, G, da1, k1, need_dx=False)   # input points: no dgrad
+    return _conv_bn_act_bwd(P, G, da1, k1, need_dx=need_dx)   # STN3d: input points, no dgrad
 
 
-def _feat_fwd(P, S, newS, x):
+FT_REG_WEIGHT = 0.001      # feature-transform regularizer weight of the cited training script (reading R30)
+
+
+def feature_transform_reg(T):
+    """Regularizer of the 64 x 64 feature transform (reading R30):
+    l = mean_n ||T_n T_n^T - I||_F, and dl/dT_n = 2 A_n T_n / (N ||A_n||_F),
+    A_n = T_n T_n^T - I (symmetric)."""
+    N, k, _ = T.shape
+    A = np.matmul(T, T.transpose(0, 2, 1)) - np.eye(k)
+    f = np.sqrt(np.sum(A * A, axis=(1, 2)))
+    dT = 2.0 * np.matmul(A, T) / (N * np.maximum(f, 1e-300))[:, None, None]
+    return f.mean(), dT
+
+
+def _feat_fwd(P, S, newS, x, ft=False):
     N, L, _ = x.shape
     T, stn_c = _stn_fwd(P, S, newS, x)
     xt = Lr.transform_points(x, T)
     r = xt.reshape(N * L, 3)
     a1, k1 = _conv_bn_act(P, S, newS, r, "feat.c1", "feat.bn1", "relu")
+    fc = dict(T=T, stn=stn_c, x=x, L=L, ft=ft)
+    if ft:     # feature transform: x' = a1 T2 per cloud, T2 from STNkd(a1) (P:L981, reading R30)
+        T2, fstn_c = _stn_fwd(P, S, newS, a1.reshape(N, L, -1), "fstn")
+        a1t = Lr.transform_points(a1.reshape(N, L, -1), T2).reshape(N * L, -1)
+        fc.update(T2=T2, fstn=fstn_c, a1=a1)
+        a1 = a1t
     a2, k2 = _conv_bn_act(P, S, newS, a1, "feat.c2", "feat.bn2", "relu")
     z3, k3 = _conv_bn_act(P, S, newS, a2, "feat.c3", "feat.bn3", None)
     g, idx = _max_pool("feat.max", z3.reshape(N, L, -1), k3["esc"])
-    return g, a1, dict(T=T, stn=stn_c, x=x, k=(k1, k2, k3), idx=idx, L=L)
+    fc.update(k=(k1, k2, k3), idx=idx)
+    return g, a1, fc
 
 
 def _feat_bwd(P, G, dg, da1_extra, c):
     k1, k2, k3 = c["k"]
+    N, L = c["x"].shape[0], c["L"]
     dz3 = Lr.max_over_points_bwd(dg, c["idx"], c["L"]).reshape(-1, dg.shape[1])
     da2 = _conv_bn_act_bwd(P, G, dz3, k3)
     da1 = _conv_bn_act_bwd(P, G, da2, k2)
     if da1_extra is not None:
         da1 = da1 + da1_extra
+    if c["ft"]:          # back through x' = a1 T2 and STNkd(a1); + the regularizer's dT2
+        C1 = da1.shape[1]
+        da1_, dT2 = Lr.transform_points_bwd(da1.reshape(N, L, C1), c["a1"].reshape(N, L, C1), c["T2"])
+        dT2 = dT2 + FT_REG_WEIGHT * c["dT2_reg"]
+        da1 = da1_.reshape(N * L, C1) + _stn_bwd(P, G, dT2, c["fstn"], need_dx=True)
     dr = _conv_bn_act_bwd(P, G, da1, k1)
-    N, L = c["x"].shape[0], c["L"]
     _, dT = Lr.transform_points_bwd(dr.reshape(N, L, 3), c["x"], c["T"])
     _stn_bwd(P, G, dT, c["stn"])
 
 
-def pointnet_cls_loss_grads(P, S, x, labels, keep, p_drop):
-    """Forward + backward of PointNetCls for ONE model; keep = dropout keep mask [N, f2]."""
+def _ft_loss(fc):
+    """Adds the feature-transform regularizer term to the loss (and keeps its
+    gradient for the backward)."""
+    if not fc["ft"]:
+        return 0.0
+    reg, fc["dT2_reg"] = feature_transform_reg(fc["T2"])
+    return FT_REG_WEIGHT * reg
+
+
+def pointnet_cls_loss_grads(P, S, x, labels, keep, p_drop, ft=False):
+    """Forward + backward of PointNetCls for ONE model; keep = dropout keep mask
+    [N, f2]; ft: feature transform on (loss += 0.001 * regularizer)."""
     newS = {}
-    g, _, fc = _feat_fwd(P, S, newS, x)
+    g, _, fc = _feat_fwd(P, S, newS, x, ft)
     h1, k1 = _conv_bn_act(P, S, newS, g, "head.fc1", "head.bn1", "relu")
     y2, h1s, W2s = _lin(P, h1, "head.fc2")
     d2 = Lr.dropout(y2, keep, p_drop)
@@ -159,6 +199,7 @@ def pointnet_cls_loss_grads(P, S, x, labels, keep, p_drop):
     h2 = z2 * gate2
     logits, h2s, W3s = _lin(P, h2, "head.fc3")
     loss, dlogits = Lr.nll_mean(logits, labels)
+    loss = loss + _ft_loss(fc)
     G = {}
     dh2, G["head.fc3.W"], G["head.fc3.b"] = _lin_bwd(dlogits, h2s, W3s)
     dz2 = dh2 * gate2
@@ -170,11 +211,11 @@ def pointnet_cls_loss_grads(P, S, x, labels, keep, p_drop):
     return loss, G, newS, dict(logits=logits, T=fc["T"], g=g)
 
 
-def pointnet_seg_loss_grads(P, S, x, labels):
+def pointnet_seg_loss_grads(P, S, x, labels, ft=False):
     """Forward + backward of PointNetDenseCls for ONE model; labels [N, L]."""
     newS = {}
     N, L, _ = x.shape
-    g, pointfeat, fc = _feat_fwd(P, S, newS, x)
+    g, pointfeat, fc = _feat_fwd(P, S, newS, x, ft)
     C3 = g.shape[1]
     h0 = np.concatenate([np.repeat(g, L, axis=0), pointfeat], axis=1)   # [N*L, C3+C1]
     h1, k1 = _conv_bn_act(P, S, newS, h0, "head.c1", "head.bn1", "relu")
@@ -182,6 +223,7 @@ def pointnet_seg_loss_grads(P, S, x, labels):
     h3, k3 = _conv_bn_act(P, S, newS, h2, "head.c3", "head.bn3", "relu")
     logits, h3s, W4s = _lin(P, h3, "head.c4")
     loss, dlogits = Lr.nll_mean(logits, labels.reshape(-1))
+    loss = loss + _ft_loss(fc)
     G = {}
     dh3, G["head.c4.W"], G["head.c4.b"] = _lin_bwd(dlogits, h3s, W4s)
     dh2 = _conv_bn_act_bwd(P, G, dh3, k3)
@@ -322,7 +364,7 @@ def hp_of(hp, b):
     return {k: float(v[b]) for k, v in hp.items()}
 
 
-def train_step(arch, P, S, opt, batch, t, hp_b, b=0, dropout_seed=42, p_drop=0.3):
+def train_step(arch, P, S, opt, batch, t, hp_b, b=0, dropout_seed=42, p_drop=0.3, ft=False):
     """One serial training step of model b: forward, backward, Adam (t >= 1).
 
     Returns loss, grads (before the step), new params, new Adam state, new BN
@@ -334,10 +376,10 @@ def train_step(arch, P, S, opt, batch, t, hp_b, b=0, dropout_seed=42, p_drop=0.3
         x, labels = batch
         f2 = P["head.fc2.W"].shape[0]
         keep = dropout_keep_mask(dropout_seed, b, t, 0, x.shape[0] * f2, p_drop).reshape(x.shape[0], f2)
-        loss, G, newS, out = pointnet_cls_loss_grads(P, S, x, labels, keep, p_drop)
+        loss, G, newS, out = pointnet_cls_loss_grads(P, S, x, labels, keep, p_drop, ft)
         out["keep"] = keep
     elif arch == "pointnet_seg":
-        loss, G, newS, out = pointnet_seg_loss_grads(P, S, *batch)
+        loss, G, newS, out = pointnet_seg_loss_grads(P, S, *batch, ft=ft)
     else:
         raise ValueError(arch)
     newP, newOpt = adam_model(P, G, opt, t, hp_b)

@@ -151,7 +151,7 @@ POINTNET_WIDTHS = (64, 128, 1024, 512, 256)
 SEG_HEAD_WIDTHS = (512, 256, 128)
 
 
-def param_specs(arch, k=None, widths=None):
+def param_specs(arch, k=None, widths=None, ft=False):
     """Parameter list of an architecture (shapes only; Appendix A of SURVEY).
 
     `widths` = (c1, c2, c3, f1, f2) narrows PointNet for tiny finite-difference
@@ -171,6 +171,11 @@ def param_specs(arch, k=None, widths=None):
         # PointNetfeat
         s += _lin("feat.c1", 3, c1) + _lin("feat.c2", c1, c2) + _lin("feat.c3", c2, c3)
         s += _bn("feat.bn1", c1) + _bn("feat.bn2", c2) + _bn("feat.bn3", c3)
+        if ft:     # STNkd on the c1 features (feature transform, k = c1)
+            s += _lin("fstn.c1", c1, c1) + _lin("fstn.c2", c1, c2) + _lin("fstn.c3", c2, c3)
+            s += _lin("fstn.fc1", c3, f1) + _lin("fstn.fc2", f1, f2) + _lin("fstn.fc3", f2, c1 * c1)
+            s += _bn("fstn.bn1", c1) + _bn("fstn.bn2", c2) + _bn("fstn.bn3", c3)
+            s += _bn("fstn.bn4", f1) + _bn("fstn.bn5", f2)
         if arch == "pointnet_cls":
             k = 40 if k is None else k
             s += _lin("head.fc1", c3, f1) + _lin("head.fc2", f1, f2) + _lin("head.fc3", f2, k)
@@ -203,11 +208,11 @@ def param_specs(arch, k=None, widths=None):
     raise ValueError("unknown arch %r" % (arch,))
 
 
-def init_params(arch, seed, k=None, widths=None):
+def init_params(arch, seed, k=None, widths=None, ft=False):
     """Initial parameters of one model (seed = 1000 + b by convention)."""
     g = rng(seed, 8)
     out = {}
-    for name, shape, init in param_specs(arch, k, widths):
+    for name, shape, init in param_specs(arch, k, widths, ft):
         if init.startswith("u:"):
             bound = 1.0 / np.sqrt(int(init[2:]))
             v = g.uniform(-bound, bound, size=shape)

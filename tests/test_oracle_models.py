@@ -312,3 +312,81 @@ def test_decisions_max_ties_flagged_exactly():
     assert np.array_equal(d.sites["m"]["flag"], want)
     assert want[0, 1] and idx[0, 1] == 0                          # all-zero channel: tie, first index
     assert np.array_equal(idx, np.argmax(x, axis=1))
+
+
+# --------------------------------------------------- feature transform ----
+
+def test_feature_transform_reg_closed_forms():
+    """Reading R30: ||T T^T - I||_F is 0 for orthogonal T (rotations), and for
+    T = c I it is |c^2 - 1| sqrt(k) with gradient 2 c sign(c^2 - 1) I / (N sqrt(k))."""
+    k, N = 5, 3
+    Q, _ = np.linalg.qr(R.standard_normal((k, k)))
+    l, dT = M.feature_transform_reg(np.stack([Q] * N))
+    assert l < 1e-12
+    for c in (0.5, 1.7):
+        l, dT = M.feature_transform_reg(np.stack([c * np.eye(k)] * N))
+        assert l == pytest.approx(abs(c * c - 1) * np.sqrt(k), rel=1e-12)
+        assert np.allclose(dT, 2 * c * np.sign(c * c - 1) / (N * np.sqrt(k)) * np.eye(k)[None], rtol=1e-12)
+
+
+def test_pointnet_cls_feature_transform_fd_tiny():
+    P = synth.init_params("pointnet_cls", 1000, k=5, widths=TINY, ft=True)
+    assert "fstn.fc3.W" in P and P["fstn.fc3.W"].shape == (TINY[0] ** 2, TINY[4])
+    x, y = synth.points_cls(0, N=3, L=16, k=5)
+    keep = R.uniform(size=(3, 8)) > 0.3
+    lf = lambda: M.pointnet_cls_loss_grads(P, {}, x, y, keep, 0.3, ft=True)[0]
+    loss, G, _, _ = M.pointnet_cls_loss_grads(P, {}, x, y, keep, 0.3, ft=True)
+    assert set(G) == set(P)
+    fd_params(lf, P, G)
+
+
+def test_pointnet_seg_feature_transform_fd_tiny():
+    P = synth.init_params("pointnet_seg", 1000, k=6, widths=TINY, ft=True)
+    x, y = synth.points_seg(0, N=2, L=16, k=6)
+    lf = lambda: M.pointnet_seg_loss_grads(P, {}, x, y, ft=True)[0]
+    loss, G, _, _ = M.pointnet_seg_loss_grads(P, {}, x, y, ft=True)
+    assert set(G) == set(P)
+    fd_params(lf, P, G)
+
+
+def test_pointnet_cls_feature_transform_vs_torch_autograd():
+    """PointNetCls(feature_transform=True) of the cited implementation in
+    torch.nn.functional (STNkd, bmm, feature_transform_regularizer * 0.001),
+    fp64 autograd, vs the oracle's hand-written backward."""
+    W = (8, 16, 32, 16, 16)
+    Pn = synth.init_params("pointnet_cls", 1003, k=7, widths=W, ft=True)
+    x, y = synth.points_cls(2, N=4, L=20, k=7)
+    keep = R.uniform(size=(4, W[4])) > 0.3
+    P = {k: torch.tensor(v, requires_grad=True) for k, v in Pn.items()}
+    st = {}
+    conv = lambda h, n: F.conv1d(h, P[n + ".W"][:, :, None], P[n + ".b"])
+
+    def stn(h, pre, k):
+        h = F.relu(_tbn(conv(h, pre + ".c1"), P, pre + ".bn1", st, pre + "1"))
+        h = F.relu(_tbn(conv(h, pre + ".c2"), P, pre + ".bn2", st, pre + "2"))
+        h = F.relu(_tbn(conv(h, pre + ".c3"), P, pre + ".bn3", st, pre + "3"))
+        h = torch.max(h, 2)[0]
+        h = F.relu(_tbn(F.linear(h, P[pre + ".fc1.W"], P[pre + ".fc1.b"]), P, pre + ".bn4", st, pre + "4"))
+        h = F.relu(_tbn(F.linear(h, P[pre + ".fc2.W"], P[pre + ".fc2.b"]), P, pre + ".bn5", st, pre + "5"))
+        return F.linear(h, P[pre + ".fc3.W"], P[pre + ".fc3.b"]).view(-1, k, k) + torch.eye(k, dtype=torch.float64)
+
+    xt = torch.tensor(x).transpose(1, 2)
+    T = stn(xt, "stn", 3)
+    h = torch.bmm(xt.transpose(2, 1), T).transpose(2, 1)
+    h = F.relu(_tbn(conv(h, "feat.c1"), P, "feat.bn1", st, "f1"))
+    T2 = stn(h, "fstn", W[0])
+    h = torch.bmm(h.transpose(2, 1), T2).transpose(2, 1)
+    h = F.relu(_tbn(conv(h, "feat.c2"), P, "feat.bn2", st, "f2"))
+    g = torch.max(_tbn(conv(h, "feat.c3"), P, "feat.bn3", st, "f3"), 2)[0]
+    h = F.relu(_tbn(F.linear(g, P["head.fc1.W"], P["head.fc1.b"]), P, "head.bn1", st, "h1"))
+    h = F.linear(h, P["head.fc2.W"], P["head.fc2.b"]) * torch.tensor(keep.astype(float)) / 0.7
+    h = F.relu(_tbn(h, P, "head.bn2", st, "h2"))
+    logits = F.linear(h, P["head.fc3.W"], P["head.fc3.b"])
+    I = torch.eye(W[0], dtype=torch.float64)[None]
+    reg = torch.mean(torch.norm(torch.bmm(T2, T2.transpose(2, 1)) - I, dim=(1, 2)))
+    loss = F.nll_loss(F.log_softmax(logits, dim=1), torch.tensor(y)) + 0.001 * reg
+    loss.backward()
+    l0, G, _, _ = M.pointnet_cls_loss_grads(Pn, {}, x, y, keep, 0.3, ft=True)
+    assert l0 == pytest.approx(loss.item(), rel=1e-12)
+    for k in G:
+        assert np.allclose(G[k], P[k].grad.numpy(), rtol=1e-8, atol=1e-12), k
