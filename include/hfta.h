@@ -457,6 +457,29 @@ hfta_status hfta_fused_adadelta(int B, int64_t P, float* param, const float* gra
 hfta_status hfta_steplr(int B, const float* lr0, const float* gamma, const int32_t* period, int64_t epoch,
                         float* lr, hfta_stream stream);
 
+/* ------------------------------------------- PointNet feature transform -- */
+/*
+ * The STNkd feature transform ("Feature Transformation" of the
+ * PointNet tuning space; reading R30).  F3: fp32 [B][N][K*K] (the STNkd fc3
+ * output, model stride f_bstride), K <= 64.
+ * _make: Tt[b][n][j][i] = F3[b][n][i*K + j] + (i == j), dtype dt, i.e. the
+ *   TRANSPOSED transform (T + I)^T, the K-major weight operand with which the
+ *   per-cloud product x' = x (T + I) runs as hfta_fused_linear_fwd over B*N
+ *   models (X [L][K] per cloud, W = Tt, no bias).
+ * _reg: with T = F3 + I, A = T T^T - I, f = ||A||_F per (b, n):
+ *   dF3[b][n][i*K + j] = dTt[b][n][j][i] + weight * 2 (A T)[i][j] / (N f)
+ *   (dTt: fp32 [B][N][K][K], the weight gradient of that per-cloud Linear),
+ *   loss[b] += weight * (1/N) sum_n f (fixed order), and mean_loss (nullable)
+ *   = (1/B) sum_b loss[b].  Workspace: hfta_feature_transform_reg_workspace.
+ */
+hfta_status hfta_feature_transform_make(int B, int64_t N, int64_t K, hfta_dtype dt, const float* F3,
+                                        int64_t f_bstride, hfta_out Tt, hfta_stream stream);
+size_t hfta_feature_transform_reg_workspace(int B, int64_t N);
+hfta_status hfta_feature_transform_reg(int B, int64_t N, int64_t K, const float* F3, int64_t f_bstride,
+                                       const float* dTt, int64_t dt_bstride, float weight, float* dF3,
+                                       int64_t df_bstride, float* loss, float* mean_loss, void* ws,
+                                       size_t ws_bytes, hfta_stream stream);
+
 /* ------------------------------------------------------------- utility -- */
 /* Y = X1 + X2 elementwise over [B][rows][cols] (dtype dt): sums the two
  * gradient paths into a shared activation (PointNet-seg's point feature). */

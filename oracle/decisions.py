@@ -149,10 +149,11 @@ def max_index(name, x, scale=None):
     return used
 
 
-def store(x, what, name=None):
+def store(x, what, name=None, k=None):
     """Witness runs only: the rounding an implementation applies to a stored
-    operand ("act", "w", "out", "grad") of layer `name`; identity otherwise."""
+    operand ("act", "w", "out", "grad") of layer `name` (k: the contraction
+    length of an "out"); identity otherwise."""
     d = ACTIVE
     if d is None or d.store is None:
         return x
-    return d.store(x, what, name)
+    return d.store(x, what, name, k)

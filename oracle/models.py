@@ -46,7 +46,7 @@ def _bn_err_scale(y, c, gamma):
 def _lin(P, r, name):
     """Linear layer on the operands an implementation stores (identity here)."""
     rs, Ws = D.store(r, "act", name), D.store(P[name + ".W"], "w", name)
-    return D.store(Lr.linear_fwd(rs, Ws, P[name + ".b"]), "out", name), rs, Ws
+    return D.store(Lr.linear_fwd(rs, Ws, P[name + ".b"]), "out", name, rs.shape[1]), rs, Ws
 
 
 def _lin_bwd(dy, rs, Ws, need_dx=True):
@@ -243,7 +243,8 @@ D_LAYERS = [(2, 1), (2, 1), (2, 1), (2, 1), (1, 0)]     # c1..c5
 def _conv(P, h, name, s, p, transposed=False):
     hs, Ws = D.store(h, "act", name), D.store(P[name], "w", name)
     f = Lr.convT2d_fwd if transposed else Lr.conv2d_fwd
-    return D.store(f(hs, Ws, s, p), "out", name), hs, Ws
+    k = Ws.shape[0] * Ws.shape[2] * Ws.shape[3] if transposed else Ws.shape[1] * Ws.shape[2] * Ws.shape[3]
+    return D.store(f(hs, Ws, s, p), "out", name, k), hs, Ws
 
 
 def gen_fwd(P, S, newS, z, tag="G"):

@@ -23,7 +23,8 @@ from .net import FusedNet, _Acts, _in, _out, A_RELU, A_NONE
 # since sum(xhat) = 0), so the fused step writes exact zeros instead of
 # reducing a rounding-noise column sum.
 BN_FOLLOWED = {"stn.c1", "stn.c2", "stn.c3", "stn.fc1", "stn.fc2", "feat.c1", "feat.c2", "feat.c3",
-               "head.fc1", "head.c1", "head.c2", "head.c3"}
+               "head.fc1", "head.c1", "head.c2", "head.c3",
+               "fstn.c1", "fstn.c2", "fstn.c3", "fstn.fc1", "fstn.fc2"}
 
 
 class FusedPointNet(FusedNet):
@@ -32,7 +33,7 @@ class FusedPointNet(FusedNet):
     bn_followed = BN_FOLLOWED
 
     def __init__(self, B, param_specs, params, hp, task="cls", dtype="f32", N=32, L=2500, k=40,
-                 p_drop=0.3, dropout_seed=42, device="cuda"):
+                 p_drop=0.3, dropout_seed=42, device="cuda", feature_transform=False, ft_weight=0.001):
         assert task in ("cls", "seg")
         self._base_init(B, param_specs, params, hp, dtype, device)
         self.task, self.N, self.L, self.k = task, N, L, k
@@ -48,6 +49,9 @@ class FusedPointNet(FusedNet):
         # statistics from G = X^T X, BN apply in the GEMM epilogue, backward
         # without forming dY; the pre-BN y1 / y2 are never stored.
         self.fuse_bn = self.fuse_lbm and self.c1 in (64, 128) and self.c2 <= 128
+        # feature transform (reading R30): STNkd on the c1 features, x' = a1 T2 per cloud
+        self.ft, self.ft_weight = bool(feature_transform), float(ft_weight)
+        self.pf_key = "feat.a1t" if self.ft else "feat.a1"        # the point feature c2 / the seg head consume
         self._alloc()
 
     # ------------------------------------------------------------ buffers --
@@ -58,10 +62,11 @@ class FusedPointNet(FusedNet):
         f = _Acts(B, torch.float32, self.device)     # per-sample tensors: fp32 in both modes
         self.x_dt = torch.empty(R, 3, dtype=self.tdt, device=self.device)
         S = {}
-        for p in ("stn", "feat"):
+        for p in ("stn", "feat") + (("fstn",) if self.ft else ()):
+            kin = c1 if p == "fstn" else 3                              # input channels of the block's c1
             if self.fuse_bn:
                 S[p + ".a1"], S[p + ".a2"] = a(R, c1), a(R, c2)
-                S[p + ".G1"], S[p + ".s1"] = f(3, 3), f(1, 3)          # Gram / column sums of the layer inputs
+                S[p + ".G1"], S[p + ".s1"] = f(kin, kin), f(1, kin)    # Gram / column sums of the layer inputs
                 S[p + ".G2"], S[p + ".s2"] = f(c1, c1), f(1, c1)
             else:
                 S[p + ".y1"], S[p + ".a1"] = a(R, c1), a(R, c1)
@@ -77,6 +82,14 @@ class FusedPointNet(FusedNet):
         S["stn.f2"], S["stn.h5"] = f(N, f2), f(N, f2)
         S["stn.f3"] = f(N, 9)
         S["feat.xt"] = a(R, 3)
+        if self.ft:
+            S["fstn.f1"], S["fstn.h4"] = f(N, f1), f(N, f1)
+            S["fstn.f2"], S["fstn.h5"] = f(N, f2), f(N, f2)
+            S["fstn.f3"], S["d.ff3"] = f(N, c1 * c1), f(N, c1 * c1)
+            S["ft.Tt"] = a(N * c1, c1)                  # (T2 + I)^T per cloud: [B][N][c1][c1]
+            S["ft.dTt"] = f(N * c1, c1)
+            S["feat.a1t"] = a(R, c1)                    # x' = a1 T2
+            S["d.a1p"], S["d.a1q"] = a(R, c1), a(R, c1)
         if self.task == "cls":
             S["head.y1"], S["head.h1"] = f(N, f1), f(N, f1)
             S["head.y2"], S["head.d2"], S["head.h2"] = f(N, f2), f(N, f2), f(N, f2)
@@ -128,6 +141,13 @@ class FusedPointNet(FusedNet):
         if self.fuse_bn:
             ws.reserve(H.hfta_fused_linear_bn_workspace(B, R, c1, 3))
             ws.reserve(H.hfta_fused_linear_bn_workspace(B, R, c2, c1))
+            ws.reserve(H.hfta_fused_linear_bn_workspace(B, R, c1, c1))
+        if self.ft:
+            for dt in (self.dt, H.HFTA_F32):
+                ws.reserve(H.hfta_fused_linear_bwd_workspace(B * N, self.L, c1, c1, dt))
+                ws.reserve(H.hfta_fused_linear_bwd_workspace(B, N, c1 * c1, f2, dt))
+                ws.reserve(H.hfta_fused_linear_bwd_workspace(B, R, c1, c1, dt))
+            ws.reserve(H.hfta_feature_transform_reg_workspace(B, N))
         if self.task == "seg":
             for (M, Nn, K) in [(R, self.h1w, c1), (N, self.h1w, c3), (R, self.h2w, self.h1w), (R, self.h3w, self.h2w),
                                (R, self.k, self.h3w)]:
@@ -242,7 +262,13 @@ class FusedPointNet(FusedNet):
         H.hfta_transform_points_fwd(self.B, self.N, self.L, self.dt, H.tin(x, 0, 3), _in(S["stn.f3"]), 1,
                                     _out(S["feat.xt"]), s)
         self._lbn_fwd("feat", 1, _in(S["feat.xt"]), 3, s)
-        self._lbn_fwd("feat", 2, _in(S["feat.a1"]), self.c1, s)
+        if self.ft:
+            self._lbn_fwd("fstn", 1, _in(S["feat.a1"]), self.c1, s)
+            self._lbn_fwd("fstn", 2, _in(S["fstn.a1"]), self.c1, s)
+            self._block_fwd("fstn", A_RELU, s)
+            self._stn_head_fwd(s, "fstn")
+            self._ft_apply(s)
+        self._lbn_fwd("feat", 2, _in(S[self.pf_key]), self.c1, s)
         self._block_fwd("feat", A_NONE, s)
 
     def _stn_feat_bwd_fused(self, x, s):
@@ -251,9 +277,14 @@ class FusedPointNet(FusedNet):
         # feat: K10 bwd -> dZ2 (gated by relu'(a2)); c2 -> dZ1 (gated by relu'(a1), after the
         # seg head's gradient is added for seg); c1 -> d xt
         self._block_bwd("feat", A_NONE, s, dx_act=A_RELU)
-        self._lbn_bwd("feat", 2, S["d.c2a"], _in(S["feat.a1"]), self.c1, S["d.c1a"], A_NONE if seg else A_RELU, s)
-        if seg:      # the point feature a1 also feeds the seg head: add its gradient, then relu'
+        gate_now = not seg and not self.ft        # the c2 input is a1 itself (a ReLU output): gate in the GEMM
+        self._lbn_bwd("feat", 2, S["d.c2a"], _in(S[self.pf_key]), self.c1, S["d.c1a"], A_RELU if gate_now else A_NONE,
+                      s)
+        if seg:      # the point feature also feeds the seg head: add its gradient
             H.hfta_add(self.B, R, self.c1, self.dt, _in(S["d.c1a"]), _in(S["d.pf"]), _out(S["d.c1a"]), s)
+        if self.ft:  # back through x' = a1 T2 (+ regularizer) and STNkd(a1): d.c1a = d(a1), not yet gated
+            self._ft_bwd(s, fused=True)
+        if not gate_now:
             H.hfta_act_bwd(self.B, R, self.c1, self.dt, A_RELU, self.act_alpha, _in(S["feat.a1"]), _in(S["d.c1a"]),
                            _out(S["d.c1a"]), s)
         self._lbn_bwd("feat", 1, S["d.c1a"], _in(S["feat.xt"]), 3, S["d.xt"], A_NONE, s)
@@ -263,21 +294,60 @@ class FusedPointNet(FusedNet):
         self._lbn_bwd("stn", 2, S["d.c2a"], _in(S["stn.a1"]), self.c1, S["d.c1a"], A_RELU, s)
         self._lbn_bwd("stn", 1, S["d.c1a"], H.tin(self.x_dt, 0, 3), 3, None, A_NONE, s)
 
-    def _stn_head_fwd(self, s):
+    def _stn_head_fwd(self, s, p="stn"):
         S = self.S
-        self._lin_fwd(_in(S["stn.g"]), self.N, "stn.fc1", S["stn.f1"], s)
-        self._bn_fwd(S["stn.f1"], "stn.bn4", A_RELU, S["stn.h4"], s)
-        self._lin_fwd(_in(S["stn.h4"]), self.N, "stn.fc2", S["stn.f2"], s)
-        self._bn_fwd(S["stn.f2"], "stn.bn5", A_RELU, S["stn.h5"], s)
-        self._lin_fwd(_in(S["stn.h5"]), self.N, "stn.fc3", S["stn.f3"], s)
+        self._lin_fwd(_in(S[p + ".g"]), self.N, p + ".fc1", S[p + ".f1"], s)
+        self._bn_fwd(S[p + ".f1"], p + ".bn4", A_RELU, S[p + ".h4"], s)
+        self._lin_fwd(_in(S[p + ".h4"]), self.N, p + ".fc2", S[p + ".f2"], s)
+        self._bn_fwd(S[p + ".f2"], p + ".bn5", A_RELU, S[p + ".h5"], s)
+        self._lin_fwd(_in(S[p + ".h5"]), self.N, p + ".fc3", S[p + ".f3"], s)
 
-    def _stn_head_bwd(self, s):
+    def _stn_head_bwd(self, s, p="stn"):
+        """From d(f3) (S["d.f3"] / S["d.ff3"]) to the pooled feature's gradient S["d.g"]."""
         S, N = self.S, self.N
-        self._lin_bwd(S["d.f3"], _in(S["stn.h5"]), N, "stn.fc3", S["d.sf2a"], s)
-        self._bn_bwd(S["d.sf2a"], S["stn.f2"], "stn.bn5", A_RELU, S["d.sf2b"], s)
-        self._lin_bwd(S["d.sf2b"], _in(S["stn.h4"]), N, "stn.fc2", S["d.sf1a"], s)
-        self._bn_bwd(S["d.sf1a"], S["stn.f1"], "stn.bn4", A_RELU, S["d.sf1b"], s)
-        self._lin_bwd(S["d.sf1b"], _in(S["stn.g"]), N, "stn.fc1", S["d.g"], s)
+        self._lin_bwd(S["d.f3" if p == "stn" else "d.ff3"], _in(S[p + ".h5"]), N, p + ".fc3", S["d.sf2a"], s)
+        self._bn_bwd(S["d.sf2a"], S[p + ".f2"], p + ".bn5", A_RELU, S["d.sf2b"], s)
+        self._lin_bwd(S["d.sf2b"], _in(S[p + ".h4"]), N, p + ".fc2", S["d.sf1a"], s)
+        self._bn_bwd(S["d.sf1a"], S[p + ".f1"], p + ".bn4", A_RELU, S["d.sf1b"], s)
+        self._lin_bwd(S["d.sf1b"], _in(S[p + ".g"]), N, p + ".fc1", S["d.g"], s)
+
+    # ------------------------------------------------ feature transform --
+    def _ft_views(self):
+        """The per-cloud operands as B*N fused 'models': a1 / x' [B*N][L][c1], Tt [B*N][c1][c1]."""
+        S, L, c1 = self.S, self.L, self.c1
+        return (H.tin(S["feat.a1"], L * c1, c1), H.tin(S["ft.Tt"], c1 * c1, c1), H.tout(S["feat.a1t"], L * c1, c1))
+
+    def _ft_apply(self, s):
+        """T2 = STNkd fc3 + I (transposed, compute dtype) and x' = a1 T2 per cloud (reading R30)."""
+        S, N, c1 = self.S, self.N, self.c1
+        H.hfta_feature_transform_make(self.B, N, c1, self.dt, H.ptr(S["fstn.f3"]), N * c1 * c1,
+                                      H.tout(S["ft.Tt"], N * c1 * c1, c1), s)
+        a1, Tt, a1t = self._ft_views()
+        H.hfta_fused_linear_fwd(self.B * N, self.L, c1, c1, self.dt, a1, Tt, None, 0, 0, 0, a1t, s)
+
+    def _ft_bwd(self, s, fused):
+        """d.c1a holds d(x'); leaves d(a1) (ungated) in d.c1a: the transform's dgrad + STNkd's input
+        gradient; adds the regularizer to loss[b]."""
+        S, N, R, c1 = self.S, self.N, self.R, self.c1
+        a1, Tt, _ = self._ft_views()
+        H.hfta_fused_linear_bwd(self.B * N, self.L, c1, c1, self.dt, H.tin(S["d.c1a"], self.L * c1, c1), a1, Tt,
+                                H.tout(S["d.a1p"], self.L * c1, c1), H.ptr(S["ft.dTt"]), c1 * c1, c1, None, 0, 0,
+                                self.ws.ptr, self.ws.nbytes, s)
+        H.hfta_feature_transform_reg(self.B, N, c1, H.ptr(S["fstn.f3"]), N * c1 * c1, H.ptr(S["ft.dTt"]), N * c1 * c1,
+                                     self.ft_weight, H.ptr(S["d.ff3"]), N * c1 * c1, H.ptr(self.loss),
+                                     H.ptr(self.mean_loss), self.ws.ptr, self.ws.nbytes, s)
+        self._stn_head_bwd(s, "fstn")
+        if fused:
+            self._block_bwd("fstn", A_RELU, s, dx_act=A_RELU)
+            self._lbn_bwd("fstn", 2, S["d.c2a"], _in(S["fstn.a1"]), self.c1, S["d.a1q"], A_RELU, s)
+            self._lbn_bwd("fstn", 1, S["d.a1q"], _in(S["feat.a1"]), self.c1, S["d.c1a"], A_NONE, s)
+        else:
+            self._block_bwd("fstn", A_RELU, s)
+            self._bn_bwd(S["d.c2a"], S["fstn.y2"], "fstn.bn2", A_RELU, S["d.c2b"], s)
+            self._lin_bwd(S["d.c2b"], _in(S["fstn.a1"]), R, "fstn.c2", S["d.a1q"], s)
+            self._bn_bwd(S["d.a1q"], S["fstn.y1"], "fstn.bn1", A_RELU, S["d.c1b"], s)
+            self._lin_bwd(S["d.c1b"], _in(S["feat.a1"]), R, "fstn.c1", S["d.c1a"], s)
+        H.hfta_add(self.B, R, c1, self.dt, _in(S["d.c1a"]), _in(S["d.a1p"]), _out(S["d.c1a"]), s)
 
     def _stn_feat_fwd(self, x, s):
         S, R = self.S, self.R
@@ -298,7 +368,15 @@ class FusedPointNet(FusedNet):
                                     _out(S["feat.xt"]), s)
         self._lin_fwd(_in(S["feat.xt"]), R, "feat.c1", S["feat.y1"], s)
         self._bn_fwd(S["feat.y1"], "feat.bn1", A_RELU, S["feat.a1"], s)
-        self._lin_fwd(_in(S["feat.a1"]), R, "feat.c2", S["feat.y2"], s)
+        if self.ft:
+            self._lin_fwd(_in(S["feat.a1"]), R, "fstn.c1", S["fstn.y1"], s)
+            self._bn_fwd(S["fstn.y1"], "fstn.bn1", A_RELU, S["fstn.a1"], s)
+            self._lin_fwd(_in(S["fstn.a1"]), R, "fstn.c2", S["fstn.y2"], s)
+            self._bn_fwd(S["fstn.y2"], "fstn.bn2", A_RELU, S["fstn.a2"], s)
+            self._block_fwd("fstn", A_RELU, s)
+            self._stn_head_fwd(s, "fstn")
+            self._ft_apply(s)
+        self._lin_fwd(_in(S[self.pf_key]), R, "feat.c2", S["feat.y2"], s)
         self._bn_fwd(S["feat.y2"], "feat.bn2", A_RELU, S["feat.a2"], s)
         self._block_fwd("feat", A_NONE, s)
 
@@ -307,9 +385,11 @@ class FusedPointNet(FusedNet):
         # feat
         self._block_bwd("feat", A_NONE, s)
         self._bn_bwd(S["d.c2a"], S["feat.y2"], "feat.bn2", A_RELU, S["d.c2b"], s)
-        self._lin_bwd(S["d.c2b"], _in(S["feat.a1"]), R, "feat.c2", S["d.c1a"], s)
+        self._lin_bwd(S["d.c2b"], _in(S[self.pf_key]), R, "feat.c2", S["d.c1a"], s)
         if self.task == "seg":      # the point feature also feeds the seg head
             H.hfta_add(self.B, R, self.c1, self.dt, _in(S["d.c1a"]), _in(S["d.pf"]), _out(S["d.c1a"]), s)
+        if self.ft:
+            self._ft_bwd(s, fused=False)
         self._bn_bwd(S["d.c1a"], S["feat.y1"], "feat.bn1", A_RELU, S["d.c1b"], s)
         self._lin_bwd(S["d.c1b"], _in(S["feat.xt"]), R, "feat.c1", S["d.xt"], s)
         H.hfta_transform_points_bwd(self.B, N, self.L, self.dt, H.tin(x, 0, 3), _in(S["d.xt"]), _out(S["d.f3"]), s)
@@ -358,7 +438,7 @@ class FusedPointNet(FusedNet):
         wld = c3 + c1
         H.hfta_fused_linear_fwd(B, N, h1, c3, H.HFTA_F32, _in(S["feat.g"]), ar.w_in("head.c1.W", H.HFTA_F32, 0, wld),
                                 ar.fptr("p", "head.c1.b"), P, 0, 0, _out(S["seg.u"]), s)
-        H.hfta_fused_linear_fwd(B, R, h1, c1, self.dt, _in(S["feat.a1"]), ar.w_in("head.c1.W", self.dt, c3, wld),
+        H.hfta_fused_linear_fwd(B, R, h1, c1, self.dt, _in(S[self.pf_key]), ar.w_in("head.c1.W", self.dt, c3, wld),
                                 H.ptr(S["seg.u"]), N * h1, h1, L, _out(S["seg.y1"]), s)
         self._bn_fwd(S["seg.y1"], "head.bn1", A_RELU, S["seg.h1"], s)
         self._lin_fwd(_in(S["seg.h1"]), R, "head.c2", S["seg.y2"], s)
@@ -380,7 +460,7 @@ class FusedPointNet(FusedNet):
         self._bn_bwd(S["d.s1a"], S["seg.y1"], "head.bn1", A_RELU, S["d.s1b"], s)
         dy1 = S["d.s1b"]
         # point part: dWp = dy1^T pf, d pf = dy1 Wp (bias grad identically 0: BN follows)
-        H.hfta_fused_linear_bwd(B, R, h1, c1, self.dt, _in(dy1), _in(S["feat.a1"]),
+        H.hfta_fused_linear_bwd(B, R, h1, c1, self.dt, _in(dy1), _in(S[self.pf_key]),
                                 ar.w_in("head.c1.W", self.dt, c3, wld), _out(S["d.pf"]),
                                 ar.fptr("g", "head.c1.W", c3), P, wld, None, P, 0, self.ws.ptr, self.ws.nbytes, s)
         # per-sample part: S[n] = sum_l dy1[n*L+l]; dWg = S^T g; dg = S Wg

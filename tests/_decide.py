@@ -11,6 +11,8 @@ subgradient instead of a result a rounding-level decision flip moves.
 No method arithmetic here: decisions are booleans / indices read from the GPU
 buffers; all values come from the oracle.
 """
+import zlib
+
 import numpy as np
 import torch
 
@@ -23,7 +25,7 @@ from oracle import models as OM
 # per site from the bf16-storage witness -- WITNESS_SAFETY x the largest
 # change of the site's decision variable that bf16 rounding of the stored
 # operands causes in the oracle itself (at least BF16_FLOOR).
-MARGIN_F32 = 2.0 ** -11
+MARGIN_F32 = 2.0 ** -14       # floor of the fp32 margins (the witness calibrates them per site)
 # bf16 gradient gate per tensor: max(2e-2, WITNESS_GATE x the witness's
 # normwise change of that gradient).  The GPU rounds at a few points the
 # witness does not model (dZ stored in bf16 between kernels, the K10 M matrix
@@ -49,6 +51,13 @@ def pointnet_gpu_decisions(net, b):
     d["_stn.pooled_on"] = _h(S["stn.g"][b]) > 0           # ReLU gate of stn.bn3 at the argmax rows
     d["stn.bn4"] = _h(S["stn.h4"][b]) > 0
     d["stn.bn5"] = _h(S["stn.h5"][b]) > 0
+    if getattr(net, "ft", False):          # STNkd of the feature transform
+        for i in (1, 2):
+            d["fstn.bn%d" % i] = _h(S["fstn.a%d" % i][b]) > 0
+        d["fstn.max"] = S["fstn.amax"][b].cpu().numpy().astype(np.int64)
+        d["_fstn.pooled_on"] = _h(S["fstn.g"][b]) > 0
+        d["fstn.bn4"] = _h(S["fstn.h4"][b]) > 0
+        d["fstn.bn5"] = _h(S["fstn.h5"][b]) > 0
     if net.task == "cls":
         d["head.bn1"] = _h(S["head.h1"][b]) > 0
         d["head.bn2"] = _h(S["head.h2"][b]) > 0
@@ -63,6 +72,9 @@ def pointnet_gpu_values(net, b):
     S = net.S
     v = {"stn.bn1": S["stn.a1"][b], "stn.bn2": S["stn.a2"][b], "feat.bn1": S["feat.a1"][b],
          "feat.bn2": S["feat.a2"][b], "stn.bn4": S["stn.h4"][b], "stn.bn5": S["stn.h5"][b]}
+    if getattr(net, "ft", False):
+        v.update({"fstn.bn1": S["fstn.a1"][b], "fstn.bn2": S["fstn.a2"][b], "fstn.bn4": S["fstn.h4"][b],
+                  "fstn.bn5": S["fstn.h5"][b]})
     if net.task == "cls":
         v.update({"head.bn1": S["head.h1"][b], "head.bn2": S["head.h2"][b]})
     else:
@@ -89,16 +101,17 @@ def decision_errors(ctx, gpu_vals, margins):
     return out
 
 
-def witness_margins(own, wit):
-    """Per-site margins from the bf16-storage witness (same decisions): the
-    largest |change| of the decision variable over its error scale."""
+def witness_margins(own, wit, floor=None):
+    """Per-site margins from the witness (same decisions): WITNESS_SAFETY x
+    the largest |change| of the decision variable over its error scale."""
+    floor = BF16_FLOOR if floor is None else floor
     m = {}
     for site, v in own.sites.items():
         w = wit.sites[site]
         key = "z" if v["kind"] == "relu" else "x"
         sc = v["scale"] if v["kind"] == "relu" else v["scale"][:, None, :]
         err = float(np.max(np.abs(w[key] - v[key]) / sc))
-        m[site] = max(BF16_FLOOR, WITNESS_SAFETY * err)
+        m[site] = max(floor, WITNESS_SAFETY * err)
     return m
 
 
@@ -114,13 +127,14 @@ def build_override(own_ctx, gpu, margins, L=None, skip=()):
             continue
         own = v["own"]
         flag = Dm.flags(v, margins[site])
-        if site == "stn.bn3":
+        if site in ("stn.bn3", "fstn.bn3"):
             # only the argmax rows' gates are observable (and used by the backward)
+            pre = site.split(".")[0]
             ov = own.copy()
-            amax = gpu["stn.max"]
+            amax = gpu[pre + ".max"]
             N, C = amax.shape
             rows = np.arange(N)[:, None] * L + amax
-            ov[rows, np.arange(C)[None, :]] = gpu["_stn.pooled_on"]
+            ov[rows, np.arange(C)[None, :]] = gpu["_%s.pooled_on" % pre]
             g = ov
         elif site in gpu:
             g = np.asarray(gpu[site]).reshape(own.shape)
@@ -152,10 +166,24 @@ def bf16_store(out_layers=()):
     """Witness rounding at the bf16-AMP storage points: every contraction's
     inputs, weights and incoming gradients; its output only for the layers
     whose pre-activation the GPU path stores in bf16 (`out_layers`)."""
-    def f(x, what, name):
+    def f(x, what, name, k=None):
         if what == "out" and (name is None or not any(name.startswith(p) for p in out_layers)):
             return x
         return _rb(x)
+    return f
+
+
+def f32_store():
+    """fp32 witness: every stored operand rounded to fp32, and every
+    contraction output perturbed by relative noise of the size fp32
+    accumulation leaves (2^-24 sqrt(k), k the contraction length; seeded per
+    layer, so the witness is deterministic)."""
+    def f(x, what, name, k=None):
+        x = np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
+        if what == "out" and k:
+            g = np.random.default_rng(zlib.crc32(repr((name, x.shape)).encode()))
+            x = x * (1.0 + 2.0 ** -24 * np.sqrt(k) * g.standard_normal(x.shape))
+        return x
     return f
 
 
@@ -180,18 +208,19 @@ def oracle_with_decisions(arch, P, S, O, batch, t, hp_b, b, gpu, dtype, L=None, 
 def with_decisions(step, gpu, dtype, L=None, witness=False, out_layers=(), skip=()):
     """The three-pass flow above for any oracle step callable `step()`.
     Sites whose name starts with a prefix in `skip` keep the oracle's own
-    decisions and are not compared."""
+    decisions and are not compared.  The witness runs in both precisions
+    (bf16: storage rounding; fp32: storage rounding + accumulation-size
+    noise, reading R28) and calibrates the per-site margins and the
+    per-tensor gates."""
     d1 = Dm.Decisions()
     with Dm.use(d1):
         res1 = step()
-    res_w = None
-    if witness or dtype == "bf16":
-        own = {k: v["own"] for k, v in d1.sites.items()}
-        dw = Dm.Decisions(0.0, own, force=True, store=bf16_store(out_layers))
-        with Dm.use(dw):
-            res_w = step()
-        res_w["own"] = res1                 # the same decisions without the rounding
-    margins = witness_margins(d1, dw) if dtype == "bf16" else {k: MARGIN_F32 for k in d1.sites}
+    own = {k: v["own"] for k, v in d1.sites.items()}
+    dw = Dm.Decisions(0.0, own, force=True, store=bf16_store(out_layers) if dtype == "bf16" else f32_store())
+    with Dm.use(dw):
+        res_w = step()
+    res_w["own"] = res1                 # the same decisions without the rounding
+    margins = witness_margins(d1, dw, BF16_FLOOR if dtype == "bf16" else MARGIN_F32)
     override, report = build_override(d1, gpu, margins, L, skip)
     report["_ctx"] = d1
     report["_margins"] = margins
@@ -201,3 +230,10 @@ def with_decisions(step, gpu, dtype, L=None, witness=False, out_layers=(), skip=
     with Dm.use(d2):
         res = step()
     return res, report, res_w
+
+
+def gate(tol, wit, own, ref_shape_ok=True):
+    """Per-quantity gate of reading R28: max(north_star tolerance,
+    WITNESS_GATE x the witness's normwise change of that quantity)."""
+    from tests._cmp import relerr
+    return max(tol, WITNESS_GATE * relerr(wit, own))

@@ -87,7 +87,7 @@ def _gates(dtype, ref, wit, key):
     tol = TOL[dtype]
     g = {}
     for n, v in ref[key].items():
-        g[n] = tol if dtype == "f32" else max(tol, DE.WITNESS_GATE * relerr(wit[key][n], wit["own"][key][n]))
+        g[n] = DE.gate(tol, wit[key][n], wit["own"][key][n])
     return g
 
 
@@ -115,7 +115,7 @@ def _check(dtype, net, errs, res, hp, B, gate_g):
             assert abs(errs[i][b] - ref[k]) <= tol * abs(ref[k]), (b, k, errs[i][b], ref[k])
         GD, GG = net.D.grads(b), net.G.grads(b)
         for half, G, key, gate in (("D", GD, "GD", True), ("G", GG, "GG", gate_g)):
-            gt = _gates(dtype, ref, wit, key) if dtype == "bf16" else {n: tol for n in ref[key]}
+            gt = _gates(dtype, ref, wit, key)
             for n, r_ in ref[key].items():
                 e = relerr(G[n], r_)
                 worst.append((e / gt[n], e, gt[n], b, half + "." + n, gate))
@@ -131,12 +131,14 @@ def _check(dtype, net, errs, res, hp, B, gate_g):
                     v = _to_torch(n, arena.host_tensor("v", n)[b])
                     assert relerr(m, m_ref) <= gt[n] * 1.01 + 1e-6, (b, half, n, "exp_avg")
                     assert relerr(v, v_ref) <= 2 * gt[n] * 1.01 + 1e-6, (b, half, n, "exp_avg_sq")
-        for half, st in (("D", ref["SD"]), ("G", ref["SG"])):
+        for half, key in (("D", "SD"), ("G", "SG")):
             h = net.D if half == "D" else net.G
+            st, ws_, os_ = ref[key], wit[key], wit["own"][key]
             for name in h.bn:
                 rm, rv = (t[b].cpu().numpy() for t in h.running[name])
-                assert relerr(rm, st[name + ".rm"]) <= tol, (b, half, name, "running_mean")
-                assert relerr(rv, st[name + ".rv"]) <= tol, (b, half, name, "running_var")
+                for k2, got in ((".rm", rm), (".rv", rv)):
+                    g_ = DE.gate(tol, ws_[name + k2], os_[name + k2])
+                    assert relerr(got, st[name + k2]) <= g_, (b, half, name, k2, relerr(got, st[name + k2]), g_)
     worst.sort(reverse=True)
     print("\n[%s] worst gradient errors (err / gate, gated): %s" % (dtype, " ".join(
         "%s:%.2e/%.1e%s" % (n, e, g, "" if gd else "(ungated)") for _, e, g, b, n, gd in worst[:8])))
