@@ -130,6 +130,30 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+# -------------------------------------------------------- step roofline --
+
+def step_roofline(workload, dtype, value, pk, args):
+    """Whole-step fraction of roofline: the method's algorithmic
+    flops per model-sample (cls 4.1908, seg 15.0962 GFLOP,
+    DCGAN 2.2746 GFLOP) at the sustained bf16 peak give the compute ceiling;
+    the HBM ceiling of the deepest fusion schedule (S3, App. B5: 17.4 MB per
+    model-sample for PointNet bf16) is the bytes floor.  frac = achieved /
+    min(ceilings): the step's time vs the larger of its two lower bounds."""
+    gf = {"pointnet_cls": 4.1908, "pointnet_seg": 15.0962, "dcgan": 2.2746}[workload]
+    if workload == "pointnet_cls" and (args.N, args.L) != (32, 2500):
+        return None
+    peak_tf = pk["bf16_tflops_sustained"] if dtype == "bf16" else pk["bf16_tflops_sustained"] / 3.0
+    comp = peak_tf * 1e12 / (gf * 1e9)
+    hbm_mb = {"pointnet_cls": 17.4, "pointnet_seg": None, "dcgan": None}[workload]
+    hbm = pk["hbm_gbs"] * 1e9 / (hbm_mb * 1e6 * (1 if dtype == "bf16" else 2)) if hbm_mb else None
+    ceiling = min(c for c in (comp, hbm) if c)
+    return {"gflop_per_model_sample": gf, "compute_ceiling": comp, "hbm_ceiling_S3": hbm,
+            "achieved_tflops": value * gf * 1e9 / 1e12, "frac": value / ceiling, "unit": UNIT,
+            "peak": "sustained bf16 %.1f TF/s%s" % (pk["bf16_tflops_sustained"],
+                                                   "" if dtype == "bf16" else " / 3 (3-pass split fp32)"),
+            "note": "algorithmic flops of the method (fusion does no extra work, P:L729)"}
+
+
 # -------------------------------------------------------------------- ours --
 
 def build_net(args, rank, world, device):
@@ -180,8 +204,12 @@ def build_net(args, rank, world, device):
         Nd = args.N_dcgan
         gs = [(n, s) for n, s, _ in synth.param_specs("dcgan_g")]
         ds = [(n, s) for n, s, _ in synth.param_specs("dcgan_d")]
-        PG = [synth.init_params("dcgan_g", 1000 + base + b) for b in range(B)]
-        PD = [synth.init_params("dcgan_d", 2000 + base + b) for b in range(B)]
+        if args.fast_init:   # identical initial parameters, different hyper-parameters
+            PG = [synth.init_params("dcgan_g", 1000)] * B
+            PD = [synth.init_params("dcgan_d", 2000)] * B
+        else:
+            PG = [synth.init_params("dcgan_g", 1000 + base + b) for b in range(B)]
+            PD = [synth.init_params("dcgan_d", 2000 + base + b) for b in range(B)]
         hp = shard.slice_hparams(synth.hparams_dcgan(3, B * world), base, base + B)
         net = FusedDCGAN(B, gs, ds, PG, PD, hp, N=Nd, dtype=args.dtype, device=device)
         real = synth.images(0, N=Nd).transpose(0, 2, 3, 1).astype(np.float32)
@@ -276,7 +304,8 @@ def run_ours(args, rank, world, local_rank):
     mem_peak = torch.cuda.max_memory_allocated(device)
 
     # ---- roofline probe: CUDA events around the probed kernel in eager steps ----
-    probe_name = args.probe if args.workload in ("pointnet_cls", "pointnet_seg") else None
+    probe_name = args.probe or {"pointnet_cls": "feat.c3:fwd", "pointnet_seg": "head.c2:fwd",
+                                "dcgan": "D.c3:fwd"}[args.workload]
     probe_ms = []
     if probe_name:
         net.probe_arm(probe_name)
@@ -284,6 +313,8 @@ def run_ours(args, rank, world, local_rank):
             wl.step()
         torch.cuda.synchronize()
         probe_ms = net.probe_collect()
+        if args.workload == "dcgan":      # D runs 3 times per iteration: one launch per pass
+            probe_ms = probe_ms[:3 * 3]
 
     # ---- end to end through the public API: pinned host inputs in, losses out ----
     graph_e2e = None
@@ -328,6 +359,7 @@ def run_ours(args, rank, world, local_rank):
                         "d2h_bytes_per_step": int(wl.d2h)}}
         path = "tc" if args.dtype == "bf16" else "simt"
         roof = net.probe_roofline(probe_name, probe_ms, pk, path=path) if probe_name else None
+        line["step_roofline"] = step_roofline(args.workload, args.dtype, value, pk, args)
         try:   # DRAM traffic of the probed kernel from the committed ncu --set full capture
             key = probe_name + (":lbm" if getattr(net, "fuse_lbm", False) and ".c3:" in probe_name else "")
             tr = json.load(open(os.path.join(ROOT, "profiles", "traffic_r01.json")))[key]
@@ -374,7 +406,8 @@ def main():
     ap.add_argument("--k", type=int, default=40)
     ap.add_argument("--k-seg", type=int, default=50)
     ap.add_argument("--N-dcgan", type=int, default=128)
-    ap.add_argument("--probe", default="feat.c3:fwd")
+    ap.add_argument("--probe", default=None, help="layer:fwd|bwd timed for the roofline (default: the workload's "
+                    "dominant contraction)")
     ap.add_argument("--ref-samples", type=int, default=8)
     ap.add_argument("--fast-init", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -160,9 +160,55 @@ class FusedDCGAN:
         ld = shp[-1] if name.startswith("t") else int(np.prod(shp[1:]))
         return H.tin(src, ar.P, ld, ar.off[name])
 
+    # CUDA events around one named (de)convolution forward (bench roofline probe):
+    # name = "D.c3:fwd" etc.
+    _probe = None
+
+    def probe_arm(self, name):
+        self._probe, self._probe_ev = name, []
+
+    def probe_collect(self):
+        ms = [a.elapsed_time(b) for a, b in getattr(self, "_probe_ev", [])]
+        self._probe = None
+        return ms
+
+    def probe_roofline(self, name, ms, peaks, path="tc"):
+        """Implicit-GEMM (de)convolution: algorithmic flops 2 B M N K of the
+        layer (M output pixels, K = 16 C_in); tensor-bound (AI 338-819 for the
+        inner layers) against the sustained bf16 peak."""
+        layer = name.split(":")[0]
+        net, lname = layer.split(".")
+        i = int(lname[1:]) - 1
+        d = (self.ddesc if net == "D" else self.gdesc)[i]
+        if d.transposed:
+            Ho = (d.H - 1) * d.stride - 2 * d.pad + d.kh
+            flops = 2.0 * self.B * d.N * d.H * d.W * d.C_in * d.C_out * d.kh * d.kw
+        else:
+            Ho = (d.H + 2 * d.pad - d.kh) // d.stride + 1
+            flops = 2.0 * self.B * d.N * Ho * Ho * d.C_out * d.C_in * d.kh * d.kw
+        nbytes = self.B * 2 * (d.N * d.H * d.W * d.C_in + d.N * Ho * Ho * d.C_out + d.C_in * d.C_out * d.kh * d.kw)
+        t = float(np.mean(ms)) / 1e3 if ms else float("nan")
+        ach = flops / t / 1e12
+        pk = peaks["bf16_tflops_sustained"]
+        return {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
+                "kernel": name + " (implicit-GEMM tcgen05 conv, one launch)", "launches_timed": len(ms),
+                "ms_per_launch": t * 1e3, "algorithmic": {"flops": flops, "bytes": nbytes},
+                "peak_source": peaks["source"]}
+
     def _conv_fwd(self, half, name, desc, X, Y, s):
+        tag = ("G." if half is self.G else "D.") + name.split(".")[0] + ":fwd"
+        e0 = None
+        if self._probe == tag:
+            import torch
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.current_stream())
         H.hfta_fused_conv_fwd(self.B, desc, self.dt, X, self._win(half, name), self._out(Y), self.ws.ptr,
                               self.ws.nbytes, s)
+        if e0 is not None:
+            import torch
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(torch.cuda.current_stream())
+            self._probe_ev.append((e0, e1))
 
     def _conv_bwd(self, half, name, desc, dY, X, dX, s, wgrad=True, accumulate=0):
         ar = half.arena
