@@ -50,6 +50,11 @@ hfta_status colsum_reduce(const GemmP& p, cudaStream_t s);   // colsum (+)= sum_
 hfta_status gemm_tc(const GemmP& p, hfta_dtype dt_in, bool out_f32, cudaStream_t s);
 bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32);
 
+// fp32-accurate contraction on the tensor cores (3xTF32, gemm_tf32.cu): fp32
+// operands / output, plain epilogue (bias, row-grouped bias, accumulate, split-K).
+bool gemm_tf32_supported(const GemmP& p);
+hfta_status gemm_tf32(const GemmP& p, cudaStream_t s);
+
 // Implicit-GEMM convolution on the tcgen05 engine (kernel 4x4, stride 2, pad 1;
 // gemm_tc.cu CONV modes; no im2col / col2im buffer).  Image tensors are dense
 // NHWC per model [B][n][h][w][c] with c % 64 == 0 (bstride 0 = shared).

@@ -18,6 +18,7 @@ hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void
     return gemm_skinny(p, dt, ws, wsb, s);
   if (gemm_tc_supported(p, dt, out_f32)) return gemm_tc(p, dt, out_f32, s);
   if (epi) return fail(HFTA_ERR_UNSUPPORTED, "fused epilogue / second K segment needs the tensor-core or skinny path");
+  if (dt == HFTA_F32 && gemm_tf32_supported(p)) return gemm_tf32(p, s);     // fp32: 3xTF32 tensor cores
   return gemm_simt(p, dt, out_f32, s);
 }
 
