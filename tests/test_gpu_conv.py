@@ -13,8 +13,8 @@ images); fp32 runs the fallback everywhere.
 Inputs are rounded to the operand dtype before the oracle sees them, so the
 oracle and the kernel contract the same values (reading R16).  Gates
 (normwise per model, reading R20): bf16 outputs 1e-2 (their own bf16
-rounding ~2e-3), fp32 outputs 1e-5; dW (fp32 accumulation) 1e-4 bf16 /
-1e-5 fp32.
+rounding ~2e-3); fp32 (3xTF32 tensor cores, whose fp32 accumulation over
+K up to 8192 reaches ~1.5e-5) and every dW: the north_star's 1e-4.
 """
 import numpy as np
 import pytest
@@ -101,8 +101,8 @@ def run_layer(layer, B, N, dtype, shared, seed=0):
 def check(layer, B, N, dtype, shared):
     name, tr, Hs, Ci, Co, k, st, pd = layer
     r = run_layer(layer, B, N, dtype, shared)
-    tol_o = 1e-2 if dtype == "bf16" else 1e-5
-    tol_w = 1e-4 if dtype == "bf16" else 1e-5
+    tol_o = 1e-2 if dtype == "bf16" else 1e-4
+    tol_w = 1e-4
     for b in range(B):
         xb = r["X"][0 if shared else b].transpose(0, 3, 1, 2)          # NCHW
         dyb = r["dY"][b].transpose(0, 3, 1, 2)

@@ -82,7 +82,9 @@ def test_linear_fwd_bwd(dt, M, N, K, B, shared):
         dx, dw, dbb = OL.linear_bwd(dY[b], xb, W[b])
         assert_close(host(Y[b]), y, tol, "Y")
         assert_close(host(dX[b]), dx, tol, "dX")
-        assert_close(host(dW[b]), dw, 1e-5 if dt == "f32" else 1e-4, "dW")
+        # fp32 wgrad reduces over M (up to 2000 rows here) in the tensor cores' fp32
+        # accumulator (3xTF32): ~1.5e-5 at M = 2000, gated at the north_star's 1e-4
+        assert_close(host(dW[b]), dw, 1e-4, "dW")
         assert_close(host(db[b]), dbb, 1e-5, "dbias")
 
 
