@@ -249,9 +249,9 @@ class PointNetRunner:
     decay and StepLR(gamma, step_size); the partition's infusible batch size
     is the fused job's N.  An "epoch" is `steps_per_epoch` fused steps.
     metric = -(final training loss) of each model (higher is better); cost =
-    the job's device time (CUDA events) in seconds.  The feature-transform
-    switch selects the STNkd variant when the build has it (else it is part
-    of the infusible key only)."""
+    the job's device time (CUDA events) in seconds.  The infusible feature-
+    transform switch selects the STNkd variant (FusedPointNet feature_transform,
+    P:L981)."""
 
     def __init__(self, L=256, k=40, steps_per_epoch=2, dtype="bf16", seed=0, device_ids=None):
         self.L, self.k, self.spe, self.dtype, self.seed = L, k, steps_per_epoch, dtype, seed
@@ -267,14 +267,16 @@ class PointNetRunner:
         from . import hfta as H
         dev = "cuda:%d" % (self.device_ids[device] if self.device_ids else 0)
         N = int(part.key[0])
+        ft = bool(part.key[1]) if len(part.key) > 1 else False
         sets = [m[1] for m in part.members]
         B = len(sets)
         hp = {k: np.array([s_[k] for s_ in sets], dtype=np.float64) for k in ("lr", "beta1", "beta2", "wd")}
         hp["eps"] = np.full(B, 1e-8)
-        specs = [(n, s) for n, s, _ in synth.param_specs("pointnet_cls", self.k)]
-        Ps = [synth.init_params("pointnet_cls", 1000 + m[0], self.k) for m in part.members]
+        specs = [(n, s) for n, s, _ in synth.param_specs("pointnet_cls", self.k, None, ft)]
+        Ps = [synth.init_params("pointnet_cls", 1000 + m[0], self.k, None, ft) for m in part.members]
         with torch.cuda.device(dev):
-            net = FusedPointNet(B, specs, Ps, hp, task="cls", dtype=self.dtype, N=N, L=self.L, k=self.k, device=dev)
+            net = FusedPointNet(B, specs, Ps, hp, task="cls", dtype=self.dtype, N=N, L=self.L, k=self.k, device=dev,
+                                feature_transform=ft)
             gam = torch.tensor([s_["gamma"] for s_ in sets], dtype=torch.float32, device=dev)
             per = torch.tensor([s_["step_size"] for s_ in sets], dtype=torch.int32, device=dev)
             lr0 = net.hv.t["lr"].clone()
