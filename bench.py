@@ -6,10 +6,11 @@ Workload (BJ configs[1]): PointNet-cls, ModelNet40-shaped synthetic point
 clouds (batch N=32, L=2500 points, k=40 classes), B fused models with
 per-model hyper-parameters, bf16-AMP (per-point tensors bf16, per-sample
 tensors/statistics/optimizer fp32), one step = forward + backward + fused
-Adam over all B models.  `value` = B * N * steps / time (device-timed, inputs
+Adam over all B models.  Default B = the peak of the measured B sweep
+(tools/sweep.py, profiles/sweep_r02_*.jsonl): 256 models per GPU for cls.  `value` = B * N * steps / time (device-timed, inputs
 resident in HBM), summed over ranks (weak scaling: B models per GPU).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--B 64] [--dtype bf16|f32]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--B 256] [--dtype bf16|f32]
   python bench.py --impl reference ...   (the CPU oracle, bounded sample)
   torchrun --nproc-per-node N bench.py --gpus N ...
 
@@ -399,7 +400,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--B", type=int, default=64)
+    ap.add_argument("--B", type=int, default=None,
+                    help="models per GPU (default: the peak of the B sweep, profiles/sweep_r02_*.jsonl)")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--N", type=int, default=32)
     ap.add_argument("--L", type=int, default=2500)
@@ -415,6 +417,10 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of the captured step graph")
     ap.add_argument("--workload", default="pointnet_cls", choices=["pointnet_cls", "pointnet_seg", "dcgan"])
     args = ap.parse_args()
+    if args.B is None:      # peak of the measured B sweep (throughput flat within 1% beyond it)
+        args.B = {("pointnet_cls", "bf16"): 256, ("pointnet_seg", "bf16"): 96, ("dcgan", "bf16"): 96,
+                  ("pointnet_cls", "f32"): 64, ("pointnet_seg", "f32"): 64, ("dcgan", "f32"): 64}[(args.workload,
+                                                                                                 args.dtype)]
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
