@@ -189,9 +189,10 @@ class FusedDCGAN:
         nbytes = self.B * 2 * (d.N * d.H * d.W * d.C_in + d.N * Ho * Ho * d.C_out + d.C_in * d.C_out * d.kh * d.kw)
         t = float(np.mean(ms)) / 1e3 if ms else float("nan")
         ach = flops / t / 1e12
-        pk = peaks["bf16_tflops_sustained"]
+        pk = peaks["bf16_tflops_sustained"] / (1.0 if self.dt == H.HFTA_BF16 else 6.0)
+        kind = "implicit-GEMM tcgen05 conv" if self.dt == H.HFTA_BF16 else "patch matrix + 3xTF32 GEMM"
         return {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
-                "kernel": name + " (implicit-GEMM tcgen05 conv, one launch)", "launches_timed": len(ms),
+                "kernel": name + " (%s, one call)" % kind, "launches_timed": len(ms),
                 "ms_per_launch": t * 1e3, "algorithmic": {"flops": flops, "bytes": nbytes},
                 "peak_source": peaks["source"]}
 

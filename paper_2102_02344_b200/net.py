@@ -94,6 +94,20 @@ class FusedNet:
         else:   # dgrad reads dY, W, writes dX; wgrad reads dY, X, writes dW fp32
             nbytes = self.B * ((M * Nn + Nn * K + M * K) * s + (M * Nn + M * K) * s + Nn * K * 4)
         t = float(np.mean(ms)) / 1e3 if ms else float("nan")
+        if path == "tf32x3":  # fp32 on the tensor cores: 3 tf32 MMAs per product, tf32 dense = 1/2 of bf16
+            peak = peaks["bf16_tflops_sustained"] / 6.0
+            ach = flops / t / 1e12
+            ridge = peak * 1e12 / (peaks["hbm_gbs"] * 1e9)
+            if flops / nbytes < ridge:
+                ach_b = nbytes / t / 1e9
+                return {"bound": "hbm", "achieved": ach_b, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": ach_b / peaks["hbm_gbs"], "traffic": None, "kernel": name + " (3xTF32)",
+                        "launches_timed": len(ms), "ms_per_launch": t * 1e3,
+                        "algorithmic": {"flops": flops, "bytes": nbytes}, "peak_source": peaks["source"]}
+            return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "traffic": None, "kernel": name + " (3xTF32)", "launches_timed": len(ms), "ms_per_launch": t * 1e3,
+                    "algorithmic": {"flops": flops, "bytes": nbytes},
+                    "peak_source": "sustained bf16 / 6 (tf32 = 1/2 bf16 rate, 3 MMAs per product); " + peaks["source"]}
         if path == "simt":   # FFMA-bound SIMT kernel: 148 SM x 128 FMA/clk x 2 flop x max clock
             peak = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
             ach = flops / t / 1e12

@@ -291,12 +291,12 @@ def test_dropout_mask_bit_exact(dt):
     X = rounded(R.standard_normal((B, rows, cols)), tdt)
     Y = torch.empty(B, rows, cols, dtype=tdt, device=DEV)
     H.hfta_dropout_fwd(B, rows, cols, code, H.tin(dev(X, tdt), rows * cols, cols), H.tout(Y, rows * cols, cols), 42,
-                       5, None, 0, p, s())
+                       5, None, 0, p, 0, s())
     # the same mask when the step comes from a device counter (graph-capturable form): 4 + 1
     Y2 = torch.empty_like(Y)
     stepd = torch.tensor([4], dtype=torch.int64, device=DEV)
     H.hfta_dropout_fwd(B, rows, cols, code, H.tin(dev(X, tdt), rows * cols, cols), H.tout(Y2, rows * cols, cols), 42,
-                       1, H.ptr(stepd), 0, p, s())
+                       1, H.ptr(stepd), 0, p, 0, s())
     torch.cuda.synchronize()
     assert torch.equal(Y, Y2)
     torch.cuda.synchronize()
@@ -305,6 +305,26 @@ def test_dropout_mask_bit_exact(dt):
         got = host(Y[b])
         assert np.array_equal(got != 0, keep & (X[b] != 0))
         assert_close(got, OL.dropout(X[b], keep, np.float32(p)), 1e-6 if dt == "f32" else 1e-2, "dropout")
+
+
+def test_dropout_sharded_masks_equal_unsharded():
+    """A model-array shard (ranks own contiguous model blocks)
+    passes its first global model index: its masks equal the masks the same
+    models draw in an unsharded run and the oracle's for the global index."""
+    B, rows, cols, p = 6, 16, 100, 0.3
+    X = rounded(R.standard_normal((B, rows, cols)), torch.float32)
+    full = torch.empty(B, rows, cols, device=DEV)
+    H.hfta_dropout_fwd(B, rows, cols, 0, H.tin(dev(X), rows * cols, cols), H.tout(full, rows * cols, cols), 42,
+                       3, None, 0, p, 0, s())
+    for lo, hi in ((0, 2), (2, 4), (4, 6)):                 # 3 "ranks"
+        part = torch.empty(hi - lo, rows, cols, device=DEV)
+        H.hfta_dropout_fwd(hi - lo, rows, cols, 0, H.tin(dev(X[lo:hi]), rows * cols, cols),
+                           H.tout(part, rows * cols, cols), 42, 3, None, 0, p, lo, s())
+        torch.cuda.synchronize()
+        assert torch.equal(part, full[lo:hi])
+        for b in range(lo, hi):
+            keep = dropout_keep_mask(42, b, 3, 0, rows * cols, p).reshape(rows, cols)
+            assert np.array_equal(host(part[b - lo]) != 0, keep & (X[b] != 0))
 
 
 @pytest.mark.parametrize("K", [50, 40, 7])

@@ -28,6 +28,11 @@ def _worker(rank, world, port, B_total, q):
     # each rank's "losses" are a deterministic function of the global model index
     local = torch.tensor([1000.0 + b for b in range(lo, hi)], dtype=torch.float32)
     allv = shard.gather_losses(local, B_total, world)
+    # the double-buffered gatherer of the bench: two consecutive steps, each in global order
+    g = shard.LossGather(B_total, world, "cpu")
+    g1 = g.launch(local).clone()
+    g2 = g.launch(local + 1.0).clone()
+    assert np.array_equal(g1.numpy(), allv.numpy()) and np.array_equal(g2.numpy(), allv.numpy() + 1.0)
     t = torch.tensor([float(rank + 1)], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)                 # the bench's max-over-ranks timing
     q.put((rank, lo, hi, allv.numpy().tolist(), float(t.item())))
