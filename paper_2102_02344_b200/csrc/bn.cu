@@ -14,6 +14,7 @@ namespace hfta {
 namespace {
 
 constexpr int NT = 256;
+constexpr int FLUSH = 16;   // rows per fp32 partial run of the statistics reductions (then fp64)
 
 // Pre-activation z = a*x + c of a BN column, a = gamma*invstd,
 // c = beta - mean*a: ONE fp32 rounding order shared by every forward and
@@ -68,10 +69,10 @@ template <typename T, int VEC>
 __global__ void __launch_bounds__(NT) k_bn_stats(int64_t R, int64_t C, const T* __restrict__ X,
                                                  int64_t xbs, int64_t ld, Geo g,
                                                  double* __restrict__ p1, double* __restrict__ p2) {
-  // fp64 accumulation: a thread sums ~R / (chunks * rows per block) shifted
-  // values; in fp32 that sequential sum's error (~n u |x - shift|) reached
-  // 5e-5 of a channel's spread at R = 80 000 and moved the BN output z
-  // (reading R15c); fp64 adds are free in this HBM-bound pass
+  // fp64 accumulation of fp32 runs: a thread sums ~R / (chunks * rows per
+  // block) shifted values; one fp32 sequential sum's error (~n u |x - shift|)
+  // reached 5e-5 of a channel's spread at R = 80 000 and moved the BN output
+  // z (reading R15c); runs of FLUSH rows in fp32, flushed into fp64
   __shared__ double s1[NT * VEC], s2[NT * VEC];
   const int b = blockIdx.z, chunk = blockIdx.y;
   const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
@@ -85,6 +86,12 @@ __global__ void __launch_bounds__(NT) k_bn_stats(int64_t R, int64_t C, const T* 
     ld_vec<T, VEC>(Xb + c0, sh);
     const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
     const int64_t r1 = min(R, r0 + g.rows_per_chunk);
+    // fp32 partial sums over runs of FLUSH rows (error ~FLUSH u of a run), flushed into
+    // the fp64 accumulators: fp64 adds only every FLUSH rows (fp64 is a slow pipe)
+    float p1[VEC], p2[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) { p1[v] = 0.f; p2[v] = 0.f; }
+    int cnt = 0;
     for (int64_t r = r0 + rl; r < r1; r += UNR * g.rpb) {
       float x[UNR][VEC];
 #pragma unroll
@@ -95,12 +102,19 @@ __global__ void __launch_bounds__(NT) k_bn_stats(int64_t R, int64_t C, const T* 
         if (r + u * g.rpb < r1) {
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
-            const double d = (double)(x[u][v] - sh[v]);       // exact for |x - shift| within 2^24 ulps
-            a1[v] += d;
-            a2[v] = fma(d, d, a2[v]);
+            const float d = x[u][v] - sh[v];
+            p1[v] += d;
+            p2[v] = fmaf(d, d, p2[v]);
           }
         }
+      if (++cnt == FLUSH) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) { a1[v] += (double)p1[v]; a2[v] += (double)p2[v]; p1[v] = 0.f; p2[v] = 0.f; }
+        cnt = 0;
+      }
     }
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) { a1[v] += (double)p1[v]; a2[v] += (double)p2[v]; }
   }
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
@@ -206,6 +220,10 @@ __global__ void __launch_bounds__(NT, 3) k_bn_bwd_reduce(int64_t R, int64_t C, c
     const T* Db = dY + (int64_t)b * dbs;
     const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
     const int64_t r1 = min(R, r0 + g.rows_per_chunk);
+    float p1[VEC], p2[VEC];          // fp32 runs of FLUSH rows, flushed into fp64 (as k_bn_stats)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) { p1[v] = 0.f; p2[v] = 0.f; }
+    int cnt = 0;
     for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
       float x[VEC], d[VEC];
       ld_vec<T, VEC>(Xb + r * xld + c0, x);
@@ -213,10 +231,17 @@ __global__ void __launch_bounds__(NT, 3) k_bn_bwd_reduce(int64_t R, int64_t C, c
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         const float dz = d[v] * act_grad(fmaf(ka[v], x[v], kc[v]), act, alpha);
-        a1[v] += (double)dz;
-        a2[v] = fma((double)dz, (double)(x[v] - m[v]), a2[v]);
+        p1[v] += dz;
+        p2[v] = fmaf(dz, x[v] - m[v], p2[v]);
+      }
+      if (++cnt == FLUSH) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) { a1[v] += (double)p1[v]; a2[v] += (double)p2[v]; p1[v] = 0.f; p2[v] = 0.f; }
+        cnt = 0;
       }
     }
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) { a1[v] += (double)p1[v]; a2[v] += (double)p2[v]; }
   }
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
