@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(NT) k_bn_apply(int64_t R, int64_t C, const T* 
 // evaluates dx = A*act'(z)*dy + Bx*x + Cc with three per-column constants.
 // Few live per-column values keep these kernels at <= 80 registers (3 CTAs/SM).
 template <typename T, int VEC>
-__global__ void __launch_bounds__(NT, 3) k_bn_bwd_reduce(int64_t R, int64_t C, const T* __restrict__ dY, int64_t dbs,
+__global__ void __launch_bounds__(NT, 2) k_bn_bwd_reduce(int64_t R, int64_t C, const T* __restrict__ dY, int64_t dbs,
                                                          int64_t dld, const T* __restrict__ X, int64_t xbs, int64_t xld,
                                                          const float* __restrict__ gamma,
                                                          const float* __restrict__ beta, int64_t gbs,

@@ -33,6 +33,9 @@ constexpr int BK = 64;      // k per stage: 64 bf16 = 128 B = one swizzle row
 constexpr int NTHREADS = 576;
 constexpr int NEPI = 8;           // epilogue warps per group (= arrivals per tile)
 constexpr int NEPI_ALL = 16;
+// SWIZZLE_NONE core-matrix strides of the 8-channel image operands (bytes; tools/micro/nosw_8ch.cu)
+constexpr uint32_t NOSW_K_LBO = 2048, NOSW_K_SBO = 128;     // K-major: k-adjacent (taps), m-adjacent (8-row groups)
+constexpr uint32_t NOSW_MN_LBO = 128, NOSW_MN_SBO = 1024;   // MN-major: k-adjacent (8-row groups), mn-adjacent (taps)
 
 struct TcArgs {
   int B, splits, order;            // order 0: n fastest, 1: m fastest
@@ -121,7 +124,12 @@ __device__ __forceinline__ void tile_coords(uint32_t t, const TcArgs& p, int& mt
 //                           the epilogue interleaves row (n,i,j) into output pixel (n, 2i+ph, 2j+pw)
 //   3  Conv2d wgrad:        A = dY (MN-major), B(k = (n,oy,ox), n = (tap,ci)) gathered (stride 2)
 //   4  ConvT2d wgrad:       A(k = (n,i,j), m = (tap,co)) = dY[n][2i-1+kh][2j-1+kw][co] gathered, B = X (MN-major)
-template <bool A_MN, bool B_MN, int BN, int STAGES, bool OUT_F32, bool BRES, int EPI, int CONV = 0>
+// NARROW (CONV 1, 3, 4): the image operand has 8 channels (16-B rows: D's
+// input image, G's output image) -- one SWIZZLE_NONE box per kernel tap,
+// core-matrix layout: K-major A (mode 1) = 8 taps x 8 channels per k-block,
+// tap t's 128 x 16 B box at t * 2048; MN-major (mode 3's B, mode 4's A) = 16
+// taps x 8 channels, tap t's 64-row x 16 B box at t * 1024.
+template <bool A_MN, bool B_MN, int BN, int STAGES, bool OUT_F32, bool BRES, int EPI, int CONV = 0, bool NARROW = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
@@ -235,7 +243,20 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           mbar_expect_tx(&full[stage], (CSUM && p.ab_same) ? A_BYTES : LOAD_BYTES);
           (void)sb;
           const int k0 = (int)(kbeg + (int64_t)kb * BK);
-          if constexpr (CONV == 1) {                      // stride-2 gather of the input image
+          if constexpr (CONV == 1 && NARROW) {            // 8 taps of an 8-channel image per k-block
+#pragma unroll
+            for (int t8 = 0; t8 < 8; ++t8) {
+              const int tap = kb * 8 + t8;
+              tma_load_5d(sa + t8 * 2048, &tmA, &full[stage], 0, 2 * gx0 - 1 + (tap & 3), 2 * gy0 - 1 + (tap >> 2), gn0,
+                          ba);
+            }
+            if constexpr (B_MN) {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
+            } else {
+              tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
+            }
+          } else if constexpr (CONV == 1) {               // stride-2 gather of the input image
             const int tap = kb / p.cblk, cb = kb - tap * p.cblk;
             tma_load_5d(sa, &tmA, &full[stage], cb * 64, 2 * gx0 - 1 + (tap & 3), 2 * gy0 - 1 + (tap >> 2), gn0, ba);
             if constexpr (B_MN) {                         // ConvT dgrad: B(n = ci, k = (tap, co)) = Wt[tap][co][ci]
@@ -262,18 +283,32 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             tma_load_3d(sa + 8192, &tmA, &full[stage], m0 + 64, k0, ba);
             int gn, gy, gx;
             grid_pos((uint32_t)k0, p, gn, gy, gx);
+            if constexpr (NARROW) {                       // 16 taps x 8 channels = the whole 128-column tile
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) {
-              const int ncol = n0 + 64 * j, tap = ncol / p.cg, ci0 = ncol - tap * p.cg;
-              tma_load_5d(sb + j * 8192, &tmB, &full[stage], ci0, 2 * gx - 1 + (tap & 3), 2 * gy - 1 + (tap >> 2), gn, bb);
+              for (int tap = 0; tap < 16; ++tap)
+                tma_load_5d(sb + tap * 1024, &tmB, &full[stage], 0, 2 * gx - 1 + (tap & 3), 2 * gy - 1 + (tap >> 2), gn, bb);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j) {
+                const int ncol = n0 + 64 * j, tap = ncol / p.cg, ci0 = ncol - tap * p.cg;
+                tma_load_5d(sb + j * 8192, &tmB, &full[stage], ci0, 2 * gx - 1 + (tap & 3), 2 * gy - 1 + (tap >> 2), gn,
+                            bb);
+              }
             }
           } else if constexpr (CONV == 4) {               // A = stride-2 gather of dY per (tap, co) atom, X plain
             int gn, gy, gx;
             grid_pos((uint32_t)k0, p, gn, gy, gx);
+            if constexpr (NARROW) {                       // 16 taps x 8 channels = the whole 128-row tile
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const int mm = m0 + 64 * j, tap = mm / p.cg, co0 = mm - tap * p.cg;
-              tma_load_5d(sa + j * 8192, &tmA, &full[stage], co0, 2 * gx - 1 + (tap & 3), 2 * gy - 1 + (tap >> 2), gn, ba);
+              for (int tap = 0; tap < 16; ++tap)
+                tma_load_5d(sa + tap * 1024, &tmA, &full[stage], 0, 2 * gx - 1 + (tap & 3), 2 * gy - 1 + (tap >> 2), gn, ba);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int mm = m0 + 64 * j, tap = mm / p.cg, co0 = mm - tap * p.cg;
+                tma_load_5d(sa + j * 8192, &tmA, &full[stage], co0, 2 * gx - 1 + (tap & 3), 2 * gy - 1 + (tap >> 2), gn,
+                            ba);
+              }
             }
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
@@ -338,13 +373,23 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         {
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sb = BRES ? smem_u32(bres + kb * B_BYTES) : ((CSUM && p.ab_same) ? sa : sa + A_BYTES);
-          const uint64_t ad0 = A_MN ? smem_desc(sa, 8192, 1024) : smem_desc(sa, 16, 1024);
-          const uint64_t bd0 = B_MN ? smem_desc(sb, 8192, 1024) : smem_desc(sb, 16, 1024);
+          // NARROW image operands: SWIZZLE_NONE core matrices (K-major A of mode 1: 8-row groups
+          // 128 B apart, taps 2048 B apart; MN-major: 8-k groups 128 B apart, 8-column taps 1024 B apart)
+          constexpr bool NA = NARROW && (CONV == 1 || CONV == 4), NB = NARROW && CONV == 3;
+          const uint64_t ad0 = NA ? (CONV == 1 ? smem_desc_nosw(sa, NOSW_K_LBO, NOSW_K_SBO)
+                                               : smem_desc_nosw(sa, NOSW_MN_LBO, NOSW_MN_SBO))
+                                  : (A_MN ? smem_desc(sa, 8192, 1024) : smem_desc(sa, 16, 1024));
+          const uint64_t bd0 = NB ? smem_desc_nosw(sb, NOSW_MN_LBO, NOSW_MN_SBO)
+                                  : (B_MN ? smem_desc(sb, 8192, 1024) : smem_desc(sb, 16, 1024));
+          // per 16-element k step: SW128 K-major +32 B, SW128 MN-major +16 rows x 128 B,
+          // NARROW K-major +2 taps (4096 B), NARROW MN-major +16 rows x 16 B (256 B)
+          constexpr uint64_t AST = NA ? (CONV == 1 ? 256 : 16) : (A_MN ? 128 : 2);
+          constexpr uint64_t BST = NB ? 16 : (B_MN ? 128 : 2);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // K-major: +32 B per 16-element k step inside the 128-B swizzle row;
             // MN-major: +16 rows x 128 B (descriptor address unit: 16 B).
-            tc_mma_ss(d_tmem, ad0 + (uint64_t)(A_MN ? k * 128 : k * 2), bd0 + (uint64_t)(B_MN ? k * 128 : k * 2), idesc,
+            tc_mma_ss(d_tmem, ad0 + (uint64_t)k * AST, bd0 + (uint64_t)k * BST, idesc,
                       (kb | k) != 0 ? 1u : 0u);
           }
           tc_commit_w(&empty[stage]);                  // smem slot free once these MMAs retire
@@ -763,12 +808,13 @@ hfta_status img_map(CUtensorMap* m, const ConvTcP& p, int nb, int rows, int st) 
   const int64_t hw = (int64_t)p.img_h * p.img_w * p.img_c;
   const int64_t dims[5] = {p.img_c, p.img_w, p.img_h, p.img_n, nb};
   const int64_t str[5] = {1, p.img_c, (int64_t)p.img_w * p.img_c, hw, nb > 1 ? p.img_bs : (int64_t)p.img_n * hw};
-  const uint32_t box[5] = {64, (uint32_t)st * bw, (uint32_t)st * bh, bn, 1};
+  const bool narrow = p.img_c == 8;            // one 16-B row per position, SWIZZLE_NONE core matrices
+  const uint32_t box[5] = {narrow ? 8u : 64u, (uint32_t)st * bw, (uint32_t)st * bh, bn, 1};
   const uint32_t es[5] = {1, (uint32_t)st, (uint32_t)st, 1, 1};
-  return make_map_nd(m, p.img, 5, dims, str, box, es);
+  return make_map_nd(m, p.img, 5, dims, str, box, es, !narrow);
 }
 
-template <int CONV, bool A_MN, bool B_MN, int BN, bool OUT_F32>
+template <int CONV, bool A_MN, bool B_MN, int BN, bool OUT_F32, bool NARROW = false>
 hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   constexpr int STAGES = (BN == 256) ? 3 : 4;
   constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + (OUT_F32 ? 0 : NEPI_ALL * 4096) +
@@ -831,7 +877,7 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   a.cblk = cp.img_c / 64;
   a.cg = cp.img_c;   // 3: C_in per tap of B; 4: C_out (the gathered dY's channels) per tap of A
   a.y_c = (int)cp.N; a.y_h = cp.y_h; a.y_w = cp.y_w; a.y_bs = cp.c_bs;
-  auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, false, 0, CONV>;
+  auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, false, 0, CONV, NARROW>;
   ensure_smem(kern, SMEM);
   const int64_t total = (int64_t)a.tiles_m * a.tiles_n * a.splits * a.B;
   HFTA_REQUIRE(total < ((int64_t)1 << 31), HFTA_ERR_SHAPE, "conv_tc: %lld tiles exceed int32", (long long)total);
@@ -844,7 +890,9 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
 }  // namespace
 
 bool conv_tc_supported(const ConvTcP& p) {
-  if (p.M < 1 || p.N < 1 || p.K < 1 || p.img_c % 64 || !aligned16(p.img) || !aligned16(p.opd) || !aligned16(p.C))
+  const bool narrow = p.img_c == 8 && p.mode != 2;     // 8-channel image operand (SWIZZLE_NONE boxes)
+  if (p.M < 1 || p.N < 1 || p.K < 1 || (p.img_c % 64 && !narrow) || !aligned16(p.img) || !aligned16(p.opd) ||
+      !aligned16(p.C))
     return false;
   if ((p.img_bs * 2) % 16 || (p.opd_bs * 2) % 16 || (p.opd_ld * 2) % 16) return false;
   uint32_t bw, bh, bn;
@@ -854,14 +902,25 @@ bool conv_tc_supported(const ConvTcP& p) {
     case 1: return p.K == 16 * (int64_t)p.img_c && p.N % 16 == 0 && (p.c_ld * 2) % 16 == 0 && (p.c_bs * 2) % 16 == 0;
     case 2: return p.K == 4 * (int64_t)p.img_c && p.N % 8 == 0 && p.N <= 256 && p.y_h == 2 * p.grid_h &&
                    p.y_w == 2 * p.grid_w && (p.c_bs * 2) % 16 == 0;
-    case 3: return p.N == 16 * (int64_t)p.img_c && p.c_ld % 4 == 0;
-    case 4: return p.M == 16 * (int64_t)p.img_c && p.N % 16 == 0 && p.c_ld % 4 == 0;
+    case 3: return p.N == 16 * (int64_t)p.img_c && p.c_ld % 4 == 0;     // narrow: N = 128 (one tile)
+    case 4: return p.M == 16 * (int64_t)p.img_c && p.N % 16 == 0 && p.c_ld % 4 == 0;   // narrow: M = 128
     default: return false;
   }
 }
 
 hfta_status conv_tc(const ConvTcP& p, cudaStream_t s) {
   if (!conv_tc_supported(p)) return fail(HFTA_ERR_UNSUPPORTED, "conv_tc: configuration not supported");
+  if (p.img_c == 8) {        // 8-channel image operand
+    switch (p.mode) {
+      case 1:
+        if (p.w_mn) return p.N <= 64 ? launch_conv<1, false, true, 64, false, true>(p, s)
+                                     : launch_conv<1, false, true, 128, false, true>(p, s);
+        return p.N <= 64 ? launch_conv<1, false, false, 64, false, true>(p, s)
+                         : launch_conv<1, false, false, 128, false, true>(p, s);
+      case 3: return launch_conv<3, true, true, 128, true, true>(p, s);
+      default: return launch_conv<4, true, true, 128, true, true>(p, s);
+    }
+  }
   switch (p.mode) {
     case 1:
       if (p.w_mn) {

@@ -168,6 +168,16 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
+// SWIZZLE_NONE descriptor (core matrices of 8 rows x 16 B; the 8-channel
+// image operands of the implicit-GEMM convolutions)
+__device__ __forceinline__ uint64_t smem_desc_nosw(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;          // version (Blackwell); layout SWIZZLE_NONE = 0
+  return d;
+}
 
 // ------------------------------------------------------------ host side --
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -207,7 +217,7 @@ hfta_status make_map(CUtensorMap* m, const void* ptr, int64_t inner, int64_t row
 // elements along dim i delivers ceil(box[i] / es[i]) of them (measured,
 // tools/micro/tma_stride.cu), out-of-bounds coordinates (also negative) zero-fill.
 hfta_status make_map_nd(CUtensorMap* m, const void* ptr, int rank, const int64_t* dims, const int64_t* strides,
-                        const uint32_t* box, const uint32_t* es) {
+                        const uint32_t* box, const uint32_t* es, bool swizzle = true) {
   cuuint64_t d[5], st[4];
   cuuint32_t bx[5], e[5];
   for (int i = 0; i < rank; ++i) {
@@ -217,8 +227,8 @@ hfta_status make_map_nd(CUtensorMap* m, const void* ptr, int rank, const int64_t
     if (i > 0) st[i - 1] = (cuuint64_t)(strides[i] * 2);
   }
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), d, st, bx, e,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(HFTA_ERR_CUDA, "cuTensorMapEncodeTiled (%d-d) failed (%d): dims %lld %lld %lld %lld %lld", rank, (int)r,
                 (long long)dims[0], (long long)(rank > 1 ? dims[1] : 0), (long long)(rank > 2 ? dims[2] : 0),

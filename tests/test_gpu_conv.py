@@ -5,10 +5,10 @@ benched batch (N = 128 images of 64 x 64, BJ configs[3]), B in {1, 3}, shared
 input images (bstride 0, as D(real) sees them) and per-model ones.
 
 Paths covered: the implicit-GEMM tcgen05 modes (stride-2 TMA gather:
-D c2-c4 fwd and wgrad, G t2-t4 dgrad; sub-pixel phases: G t2-t5 fwd, D c1-c4
-dgrad; ConvT wgrad: G t2-t4), the dense-GEMM layers (G t1, D c5) and the
-patch-matrix fallback (D c1 fwd / wgrad, G t5 dgrad / wgrad: 8-channel
-images); fp32 runs the fallback everywhere.
+D c1-c4 fwd and wgrad, G t2-t5 dgrad; sub-pixel phases: G t2-t5 fwd, D c1-c4
+dgrad; ConvT wgrad: G t2-t5; the 8-channel images of D c1 / G t5 through
+SWIZZLE_NONE core-matrix boxes), the dense-GEMM layers (G t1, D c5); fp32 runs
+the patch-matrix path with 3xTF32 GEMMs.
 
 Inputs are rounded to the operand dtype before the oracle sees them, so the
 oracle and the kernel contract the same values (reading R16).  Gates
