@@ -142,15 +142,21 @@ hfta_status hfta_fused_linear_bwd(int B, int64_t M, int64_t N, int64_t K, hfta_d
  * dW fp32 in the same layout at dW + b*dW_bstride (accumulate != 0 adds: the
  * D(real) + D(fake) gradient accumulation of the DCGAN step).  dX.ptr NULL /
  * dW NULL skip that output.  No bias (the DCGAN convolutions have none).
- * Channel counts: TMA/tensor-core path when rows are 16-B multiples (pad C_in
- * 100 -> 104 for the generator input), SIMT otherwise.
+ * act (fwd): an activation of a layer without BatchNorm (D c1 LeakyReLU
+ * act_alpha, G t5 Tanh) applied to Y -- in the implicit-GEMM epilogue on the
+ * tensor-core path (its backward gates on the stored output: y > 0 <=> act(y) > 0).
+ * Paths: bf16 k4 s2 p1 with 8 or 64-multiple channels: implicit GEMM (TMA
+ * gathers / sub-pixel phases, no patch matrix); 1x1-input / whole-window
+ * layers: dense GEMMs; fp32: patch matrix + 3xTF32 GEMMs.  Images are dense
+ * NHWC per model (X.ld == C_in, Y.ld == C_out).
  */
 typedef struct {
   int N, H, W, C_in, C_out, kh, kw, stride, pad, transposed;
 } hfta_conv_desc;
 size_t hfta_fused_conv_workspace(int B, const hfta_conv_desc* desc, hfta_dtype dt);
 hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* desc, hfta_dtype dt, hfta_in X, hfta_in W,
-                                hfta_out Y, void* ws, size_t ws_bytes, hfta_stream stream);
+                                hfta_out Y, hfta_act act, float act_alpha, void* ws, size_t ws_bytes,
+                                hfta_stream stream);
 hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* desc, hfta_dtype dt, hfta_in dY, hfta_in X,
                                 hfta_in W, hfta_out dX, float* dW, int64_t dW_bstride, int accumulate,
                                 void* ws, size_t ws_bytes, hfta_stream stream);

@@ -14,7 +14,6 @@ namespace hfta {
 namespace {
 
 constexpr int NT = 256;
-constexpr int FLUSH = 16;   // rows per fp32 partial run of the statistics reductions (then fp64)
 
 // Pre-activation z = a*x + c of a BN column, a = gamma*invstd,
 // c = beta - mean*a: ONE fp32 rounding order shared by every forward and
@@ -48,6 +47,12 @@ bool vec_ok(const void* p, int64_t ld, int64_t bs, int64_t C, int vec) {
   return p == nullptr || (aligned16(p) && ld % vec == 0 && bs % vec == 0 && C % vec == 0);
 }
 
+// RUN: the most rows one thread sums sequentially in fp32 (the reductions'
+// per-thread runs; error ~RUN u of a run, then fixed-order fp64 combination
+// across threads and chunks -- reading R15c: a 2000-row fp32 run had moved
+// the BN output z by 5e-5 of a channel's spread)
+constexpr int RUN = 32;
+
 Geo make_geo(int B, int64_t R, int64_t C, int vec, int bps = 0) {
   Geo g;
   g.vec = vec;
@@ -58,6 +63,7 @@ Geo make_geo(int B, int64_t R, int64_t C, int vec, int bps = 0) {
   int64_t target = (int64_t)(bps > 0 ? bps : bn_blocks_per_sm()) * std::max(num_sms(), 148);
   int64_t chunks = std::max<int64_t>(1, target / ((int64_t)g.colgroups * B));
   chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, cdiv(R, (int64_t)g.rpb * 8)));
+  chunks = std::max<int64_t>(chunks, cdiv(R, (int64_t)g.rpb * RUN));        // runs of <= RUN rows per thread
   g.rows_per_chunk = cdiv(cdiv(R, chunks), g.rpb) * g.rpb;
   g.chunks = (int)cdiv(R, g.rows_per_chunk);
   return g;
@@ -66,55 +72,40 @@ Geo make_geo(int B, int64_t R, int64_t C, int vec, int bps = 0) {
 // Welford-free stable stats: per-thread fp32 sums of (x - shift) and (x - shift)^2
 // with shift = x[row 0] of the column; merged across row lanes in fixed order.
 template <typename T, int VEC>
-__global__ void __launch_bounds__(NT) k_bn_stats(int64_t R, int64_t C, const T* __restrict__ X,
+__global__ void __launch_bounds__(NT, 2) k_bn_stats(int64_t R, int64_t C, const T* __restrict__ X,
                                                  int64_t xbs, int64_t ld, Geo g,
                                                  double* __restrict__ p1, double* __restrict__ p2) {
-  // fp64 accumulation of fp32 runs: a thread sums ~R / (chunks * rows per
-  // block) shifted values; one fp32 sequential sum's error (~n u |x - shift|)
-  // reached 5e-5 of a channel's spread at R = 80 000 and moved the BN output
-  // z (reading R15c); runs of FLUSH rows in fp32, flushed into fp64
+  // each thread sums <= RUN rows in fp32 (4 rows' loads in flight), blocks
+  // combine their threads and chunks in fp64, fixed order (reading R15c)
   __shared__ double s1[NT * VEC], s2[NT * VEC];
   const int b = blockIdx.z, chunk = blockIdx.y;
   const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
   const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
   const T* Xb = X + (int64_t)b * xbs;
-  double a1[VEC], a2[VEC];
-  float sh[VEC];
+  float a1[VEC], a2[VEC], sh[VEC];
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) { a1[v] = 0.0; a2[v] = 0.0; sh[v] = 0.f; }
+  for (int v = 0; v < VEC; ++v) { a1[v] = 0.f; a2[v] = 0.f; sh[v] = 0.f; }
   if (c0 < C) {
     ld_vec<T, VEC>(Xb + c0, sh);
     const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
     const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-    // fp32 partial sums over runs of FLUSH rows (error ~FLUSH u of a run), flushed into
-    // the fp64 accumulators: fp64 adds only every FLUSH rows (fp64 is a slow pipe)
-    float p1[VEC], p2[VEC];
+    constexpr int U = 4;
+    for (int64_t r = r0 + rl; r < r1; r += U * g.rpb) {
+      float x[U][VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) { p1[v] = 0.f; p2[v] = 0.f; }
-    int cnt = 0;
-    for (int64_t r = r0 + rl; r < r1; r += UNR * g.rpb) {
-      float x[UNR][VEC];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u)
+      for (int u = 0; u < U; ++u)
         if (r + u * g.rpb < r1) ld_vec<T, VEC>(Xb + (r + u * g.rpb) * ld + c0, x[u]);
 #pragma unroll
-      for (int u = 0; u < UNR; ++u)
+      for (int u = 0; u < U; ++u)
         if (r + u * g.rpb < r1) {
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
             const float d = x[u][v] - sh[v];
-            p1[v] += d;
-            p2[v] = fmaf(d, d, p2[v]);
+            a1[v] += d;
+            a2[v] = fmaf(d, d, a2[v]);
           }
         }
-      if (++cnt == FLUSH) {
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) { a1[v] += (double)p1[v]; a2[v] += (double)p2[v]; p1[v] = 0.f; p2[v] = 0.f; }
-        cnt = 0;
-      }
     }
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) { a1[v] += (double)p1[v]; a2[v] += (double)p2[v]; }
   }
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
@@ -158,7 +149,7 @@ __global__ void k_bn_finalize(int B, int64_t R, int64_t C, const T* __restrict__
 }
 
 template <typename T, int VEC>
-__global__ void __launch_bounds__(NT) k_bn_apply(int64_t R, int64_t C, const T* __restrict__ X, int64_t xbs,
+__global__ void __launch_bounds__(NT, 2) k_bn_apply(int64_t R, int64_t C, const T* __restrict__ X, int64_t xbs,
                                                  int64_t xld, T* __restrict__ Y, int64_t ybs, int64_t yld,
                                                  const float* __restrict__ gamma, const float* __restrict__ beta,
                                                  int64_t gbs, const float* __restrict__ smean,
@@ -178,12 +169,19 @@ __global__ void __launch_bounds__(NT) k_bn_apply(int64_t R, int64_t C, const T* 
   T* Yb = Y + (int64_t)b * ybs + c0;
   const int r0 = (int)((int64_t)chunk * g.rows_per_chunk);
   const int r1 = (int)min(R, (int64_t)r0 + g.rows_per_chunk);
-  for (int r = r0 + rl; r < r1; r += g.rpb) {
-    float x[VEC];
-    ld_vec<T, VEC>(Xb + (int64_t)r * xld, x);
+  constexpr int U = 4;               // four rows' loads in flight per thread
+  for (int r = r0 + rl; r < r1; r += U * g.rpb) {
+    float x[U][VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) x[v] = act_fwd(fmaf(x[v], sc[v], sf[v]), act, alpha);
-    st_vec<T, VEC>(Yb + (int64_t)r * yld, x);
+    for (int u = 0; u < U; ++u)
+      if (r + u * g.rpb < r1) ld_vec<T, VEC>(Xb + (int64_t)(r + u * g.rpb) * xld, x[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (r + u * g.rpb < r1) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) x[u][v] = act_fwd(fmaf(x[u][v], sc[v], sf[v]), act, alpha);
+        st_vec<T, VEC>(Yb + (int64_t)(r + u * g.rpb) * yld, x[u]);
+      }
   }
 }
 
@@ -205,9 +203,9 @@ __global__ void __launch_bounds__(NT, 2) k_bn_bwd_reduce(int64_t R, int64_t C, c
   const int b = blockIdx.z, chunk = blockIdx.y;
   const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
   const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
-  double a1[VEC], a2[VEC];          // fp64 sums (as k_bn_stats): dbeta / dgamma can cancel
+  float a1[VEC], a2[VEC];          // <= RUN rows per thread in fp32, fp64 across threads / chunks
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) { a1[v] = 0.0; a2[v] = 0.0; }
+  for (int v = 0; v < VEC; ++v) { a1[v] = 0.f; a2[v] = 0.f; }
   if (c0 < C) {
     float ka[VEC], kc[VEC], m[VEC];
 #pragma unroll
@@ -220,28 +218,26 @@ __global__ void __launch_bounds__(NT, 2) k_bn_bwd_reduce(int64_t R, int64_t C, c
     const T* Db = dY + (int64_t)b * dbs;
     const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
     const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-    float p1[VEC], p2[VEC];          // fp32 runs of FLUSH rows, flushed into fp64 (as k_bn_stats)
+    constexpr int U = 2;             // two rows of both streams in flight
+    for (int64_t r = r0 + rl; r < r1; r += U * g.rpb) {
+      float x[U][VEC], d[U][VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) { p1[v] = 0.f; p2[v] = 0.f; }
-    int cnt = 0;
-    for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
-      float x[VEC], d[VEC];
-      ld_vec<T, VEC>(Xb + r * xld + c0, x);
-      ld_vec<T, VEC>(Db + r * dld + c0, d);
+      for (int u = 0; u < U; ++u)
+        if (r + u * g.rpb < r1) {
+          ld_vec<T, VEC>(Xb + (r + u * g.rpb) * xld + c0, x[u]);
+          ld_vec<T, VEC>(Db + (r + u * g.rpb) * dld + c0, d[u]);
+        }
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        const float dz = d[v] * act_grad(fmaf(ka[v], x[v], kc[v]), act, alpha);
-        p1[v] += dz;
-        p2[v] = fmaf(dz, x[v] - m[v], p2[v]);
-      }
-      if (++cnt == FLUSH) {
+      for (int u = 0; u < U; ++u)
+        if (r + u * g.rpb < r1) {
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) { a1[v] += (double)p1[v]; a2[v] += (double)p2[v]; p1[v] = 0.f; p2[v] = 0.f; }
-        cnt = 0;
-      }
+          for (int v = 0; v < VEC; ++v) {
+            const float dz = d[u][v] * act_grad(fmaf(ka[v], x[u][v], kc[v]), act, alpha);
+            a1[v] += dz;
+            a2[v] = fmaf(dz, x[u][v] - m[v], a2[v]);
+          }
+        }
     }
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) { a1[v] += (double)p1[v]; a2[v] += (double)p2[v]; }
   }
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
@@ -293,7 +289,7 @@ __global__ void k_bn_bwd_finalize(int B, int64_t R, int64_t C, int chunks, const
 }
 
 template <typename T, int VEC>
-__global__ void __launch_bounds__(NT, 3) k_bn_bwd_apply(int B, int64_t R, int64_t C, const T* __restrict__ dY,
+__global__ void __launch_bounds__(NT, 2) k_bn_bwd_apply(int B, int64_t R, int64_t C, const T* __restrict__ dY,
                                                         int64_t dbs, int64_t dld, const T* __restrict__ X, int64_t xbs,
                                                         int64_t xld, T* __restrict__ dX, int64_t obs, int64_t old,
                                                         int act, float alpha, Geo g, const float* __restrict__ coef) {
@@ -314,16 +310,25 @@ __global__ void __launch_bounds__(NT, 3) k_bn_bwd_apply(int B, int64_t R, int64_
   T* Ob = dX + (int64_t)b * obs;
   const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
   const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-  for (int64_t r = r0 + rl; r < r1; r += g.rpb) {
-    float x[VEC], d[VEC];
-    ld_vec<T, VEC>(Xb + r * xld + c0, x);
-    ld_vec<T, VEC>(Db + r * dld + c0, d);
+  constexpr int U = 2;               // two rows of both streams in flight
+  for (int64_t r = r0 + rl; r < r1; r += U * g.rpb) {
+    float x[U][VEC], d[U][VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      const float gd = d[v] * act_grad(fmaf(ka[v], x[v], kc[v]), act, alpha);
-      x[v] = fmaf(kA[v], gd, fmaf(kB[v], x[v], kC[v]));
-    }
-    st_vec<T, VEC>(Ob + r * old + c0, x);
+    for (int u = 0; u < U; ++u)
+      if (r + u * g.rpb < r1) {
+        ld_vec<T, VEC>(Xb + (r + u * g.rpb) * xld + c0, x[u]);
+        ld_vec<T, VEC>(Db + (r + u * g.rpb) * dld + c0, d[u]);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (r + u * g.rpb < r1) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          const float gd = d[u][v] * act_grad(fmaf(ka[v], x[u][v], kc[v]), act, alpha);
+          x[u][v] = fmaf(kA[v], gd, fmaf(kB[v], x[u][v], kC[v]));
+        }
+        st_vec<T, VEC>(Ob + (r + u * g.rpb) * old + c0, x[u]);
+      }
   }
 }
 

@@ -318,7 +318,7 @@ size_t hfta_fused_conv_workspace(int B, const hfta_conv_desc* d, hfta_dtype dt) 
 }
 
 hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* d, hfta_dtype dt, hfta_in X, hfta_in W, hfta_out Y,
-                                void* ws, size_t ws_bytes, hfta_stream stream) {
+                                hfta_act act, float act_alpha, void* ws, size_t ws_bytes, hfta_stream stream) {
   if (hfta_status st = check_init()) return st;
   HFTA_CHECK_B(B);
   Shape sh;
@@ -334,13 +334,25 @@ hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
                "conv_fwd: images must be dense NHWC (X.ld %lld vs C_in %d, Y.ld %lld vs C_out %d)", (long long)X.ld,
                d->C_in, (long long)Y.ld, d->C_out);
   const int64_t xe = img_elems(d->N, d->H, d->W, d->C_in), ye = img_elems(d->N, sh.Ho, sh.Wo, d->C_out);
-  if (dt == HFTA_BF16 && k4s2p1(d) && (X.bstride == 0 || X.bstride == xe) && (Y.bstride == ye || B == 1)) {
+  HFTA_REQUIRE(act == HFTA_ACT_NONE || act == HFTA_ACT_LEAKY_RELU || act == HFTA_ACT_TANH || act == HFTA_ACT_RELU,
+               HFTA_ERR_UNSUPPORTED, "conv_fwd: activation %d", (int)act);
+  if (dt == HFTA_BF16 && k4s2p1(d) && (X.bstride == 0 || X.bstride == xe) && (Y.bstride == ye || B == 1) &&
+      act != HFTA_ACT_RELU) {
     ConvTcP cp = fwd_cp(B, d, sh, X.ptr, X.bstride, W.ptr, W.bstride, W.ld, Y.ptr, Y.bstride);
+    cp.act = act; cp.act_alpha = act_alpha;      // fused into the epilogue
     if (conv_tc_supported(cp)) {
       if (hfta_status st = conv_tc(cp, s)) return st;
       return post_launch(s, "hfta_fused_conv_fwd");
     }
   }
+  // other paths: the activation as a separate in-place pass at the end
+  const auto finish = [&]() -> hfta_status {
+    if (act != HFTA_ACT_NONE)
+      if (hfta_status st = hfta_act_fwd(B, (int64_t)d->N * sh.Ho * sh.Wo, d->C_out, dt, act, act_alpha,
+                                        hfta_in{Y.ptr, Y.bstride, Y.ld}, Y, stream))
+        return st;
+    return post_launch(s, "hfta_fused_conv_fwd");
+  };
   if (dense_convT(d) || dense_conv(d)) {
     // t1: Y[n][(kh,kw,co)] = X[n] Wt^T ; c5: Y[n][co] = X[n][(h,w,ci)] W^T -- plain GEMMs in NHWC
     p.M = d->N; p.N = dense_convT(d) ? sh.Kc : d->C_out; p.K = dense_convT(d) ? d->C_in : sh.Kc;
@@ -349,7 +361,7 @@ hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
     p.C = Y.ptr; p.c_bs = Y.bstride; p.c_ld = p.N;
     p.k_chunk = p.K;
     if (hfta_status st = run_gemm(p, dt, false, s)) return st;
-    return post_launch(s, "hfta_fused_conv_fwd");
+    return finish();
   }
   HFTA_REQUIRE(col_bytes(B, d, dt, sh) > 0, HFTA_ERR_UNSUPPORTED, "conv_fwd: operands not eligible for the "
                "implicit-GEMM path (alignment / model strides) and no patch-matrix workspace for this configuration");
@@ -373,7 +385,7 @@ hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
     if (hfta_status st = run_gemm(p, dt, false, s)) return st;
     col2im(dt, sh.g, col, sh.Ms * sh.Kc, sh.Kc, Y.ptr, Y.bstride, B, s);
   }
-  return post_launch(s, "hfta_fused_conv_fwd");
+  return finish();
 }
 
 hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* d, hfta_dtype dt, hfta_in dY, hfta_in X, hfta_in W,

@@ -72,6 +72,7 @@ struct ConvTcP {
   void* C; int64_t c_bs, c_ld;   // 1: Y [B][M][N] bf16; 2: Y image (c_bs = model stride); 3, 4: dW fp32 (ld c_ld)
   int y_h, y_w;             // mode 2: output image size
   int accumulate; int splits; int64_t k_chunk; float* part;   // 3, 4: split-K over the reduction rows
+  int act; float act_alpha;        // 1, 2 (forward): activation applied in the epilogue (layers without BN)
 };
 bool conv_tc_supported(const ConvTcP& p);
 hfta_status conv_tc(const ConvTcP& p, cudaStream_t s);

@@ -411,7 +411,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const uint32_t sbias = smem_u32(sbias_all + ew * BN);
     const uint32_t sscale = smem_u32(sscale_all + ew * BN);
     constexpr int NSTEP = BN / 64;
-    const int my_steps = (NSTEP - half + 1) / 2;
+    // sub-pixel phase tiles 64 wide (direct stores, no TMA staging): the two warps
+    // of a lane quarter take one 32-column half each instead of idling one of them
+    constexpr bool SPLIT_COLS = CONV == 2 && NSTEP == 1;
+    const int my_steps = SPLIT_COLS ? 1 : (NSTEP - half + 1) / 2;
     const int acc = grp;                          // local tile parity = accumulator buffer
     uint32_t acc_phase = 0;
     int64_t cur_key = -1;
@@ -484,7 +487,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
 #pragma unroll 1
       for (int si = 0; si < my_steps; ++si) {
-        const int j = half + 2 * si;     // 64-column step, processed as two 32-column halves
+        const int j = SPLIT_COLS ? 0 : half + 2 * si;   // 64-column step, processed as two 32-column halves
         const int64_t n0 = (int64_t)nt * BN + j * 64;
         const bool last = si == my_steps - 1;
         uint8_t* buf = stage_out + ew * 4096;  // bf16 staging: this warp's 32 x 64 sub-tile
@@ -496,11 +499,13 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
+          if (SPLIT_COLS && hh != half) continue;        // warp-uniform
           uint32_t u[32];
-          const uint32_t ta = tmem_base + (uint32_t)(acc * ABUF + j * 64 + hh * 32) + ((uint32_t)(quarter * 32) << 16);
+          const uint32_t ta = tmem_base + (uint32_t)(acc * ABUF + (SPLIT_COLS ? 0 : j * 64) + hh * 32) +
+                              ((uint32_t)(quarter * 32) << 16);
           tmem_ld32_nowait(ta, u);
           tmem_wait_ld();
-          if (last && hh == 1) {         // this warp's last TMEM read of the tile: release the accumulator
+          if (last && (SPLIT_COLS || hh == 1)) {   // this warp's last TMEM read of the tile: release the accumulator
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -537,6 +542,15 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
               for (int q = 0; q < 32; ++q)
                 if (c0 + q < p.N) v[q] += brow[c0 + q];
+            }
+            if constexpr (CONV != 0) {           // activation of a layer without BN (D c1 LeakyReLU, G t5 Tanh)
+              if (p.act == HFTA_ACT_LEAKY_RELU) {
+#pragma unroll
+                for (int q = 0; q < 32; ++q) v[q] = v[q] > 0.f ? v[q] : p.act_alpha * v[q];
+              } else if (p.act == HFTA_ACT_TANH) {
+#pragma unroll
+                for (int q = 0; q < 32; ++q) v[q] = tanhf(v[q]);
+              }
             }
           }
           // gating values = this tile's A operand, still resident in smem: per
@@ -877,6 +891,7 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   a.cblk = cp.img_c / 64;
   a.cg = cp.img_c;   // 3: C_in per tap of B; 4: C_out (the gathered dY's channels) per tap of A
   a.y_c = (int)cp.N; a.y_h = cp.y_h; a.y_w = cp.y_w; a.y_bs = cp.c_bs;
+  a.act = (CONV == 1 || CONV == 2) ? cp.act : HFTA_ACT_NONE; a.act_alpha = cp.act_alpha;
   auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, false, 0, CONV, NARROW>;
   ensure_smem(kern, SMEM);
   const int64_t total = (int64_t)a.tiles_m * a.tiles_n * a.splits * a.B;

@@ -196,15 +196,15 @@ class FusedDCGAN:
                 "ms_per_launch": t * 1e3, "algorithmic": {"flops": flops, "bytes": nbytes},
                 "peak_source": peaks["source"]}
 
-    def _conv_fwd(self, half, name, desc, X, Y, s):
+    def _conv_fwd(self, half, name, desc, X, Y, s, act=H.ACT_NONE, alpha=0.0):
         tag = ("G." if half is self.G else "D.") + name.split(".")[0] + ":fwd"
         e0 = None
         if self._probe == tag:
             import torch
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record(torch.cuda.current_stream())
-        H.hfta_fused_conv_fwd(self.B, desc, self.dt, X, self._win(half, name), self._out(Y), self.ws.ptr,
-                              self.ws.nbytes, s)
+        H.hfta_fused_conv_fwd(self.B, desc, self.dt, X, self._win(half, name), self._out(Y), act, alpha,
+                              self.ws.ptr, self.ws.nbytes, s)
         if e0 is not None:
             import torch
             e1 = torch.cuda.Event(enable_timing=True)
@@ -248,8 +248,8 @@ class FusedDCGAN:
     # ---------------------------------------------------------- passes --
     def _D_forward(self, img_in, s):
         D = self.D
-        self._conv_fwd(D, "c1.W", self.ddesc[0], img_in, self.dy[0], s)
-        self._act(H.ACT_LEAKY_RELU, 0.2, self.dy[0], self.dh[0], s)
+        # c1 has no BN: LeakyReLU(0.2) applied in the convolution's epilogue (dh[0] = act(y))
+        self._conv_fwd(D, "c1.W", self.ddesc[0], img_in, self.dh[0], s, H.ACT_LEAKY_RELU, 0.2)
         for i in (1, 2, 3):
             self._conv_fwd(D, "c%d.W" % (i + 1), self.ddesc[i], self._in(self.dh[i - 1]), self.dy[i], s)
             self._bn_fwd(D, "bn%d" % (i + 1), self.dy[i], H.ACT_LEAKY_RELU, 0.2, self.dh[i], s)
@@ -264,19 +264,19 @@ class FusedDCGAN:
                          accumulate)
             self._conv_bwd(D, "c%d.W" % (i + 1), self.ddesc[i], self.ddy[i], self._in(self.dh[i - 1]),
                            self.ddh[i - 1], s, wgrad, accumulate)
-        self._act_bwd(H.ACT_LEAKY_RELU, 0.2, self.dy[0], self.ddh[0], self.ddy[0], s)
+        self._act_bwd(H.ACT_LEAKY_RELU, 0.2, self.dh[0], self.ddh[0], self.ddy[0], s)   # gate: act(y) > 0 <=> y > 0
         self._conv_bwd(D, "c1.W", self.ddesc[0], self.ddy[0], img_in, self.dimg if need_dimg else None, s, wgrad,
                        accumulate)
 
     def _G_forward(self, s):
         G = self.G
         x = H.tin(self.z, self.N * NZP, NZP)
-        for i in range(5):
+        for i in range(4):
             self._conv_fwd(G, "t%d.W" % (i + 1), self.gdesc[i], x, self.gy[i], s)
-            if i < 4:
-                self._bn_fwd(G, "bn%d" % (i + 1), self.gy[i], H.ACT_RELU, 0.0, self.gh[i], s)
-                x = self._in(self.gh[i])
-        self._act(H.ACT_TANH, 0.0, self.gy[4], self.fake, s)
+            self._bn_fwd(G, "bn%d" % (i + 1), self.gy[i], H.ACT_RELU, 0.0, self.gh[i], s)
+            x = self._in(self.gh[i])
+        # t5 has no BN: Tanh in the convolution's epilogue (fake = tanh(y))
+        self._conv_fwd(G, "t5.W", self.gdesc[4], x, self.fake, s, H.ACT_TANH, 0.0)
 
     def _G_backward(self, dfake, s):
         G = self.G

@@ -94,7 +94,8 @@ _SIGS = {
     "hfta_feature_transform_reg_workspace": (sz, [i32, i64]),
     "hfta_feature_transform_reg": (i32, [i32, i64, i64, vp, i64, vp, i64, f32, vp, i64, vp, vp, vp, sz, vp]),
     "hfta_fused_conv_workspace": (sz, [i32, C.POINTER(hfta_conv_desc), i32]),
-    "hfta_fused_conv_fwd": (i32, [i32, C.POINTER(hfta_conv_desc), i32, hfta_in, hfta_in, hfta_out, vp, sz, vp]),
+    "hfta_fused_conv_fwd": (i32, [i32, C.POINTER(hfta_conv_desc), i32, hfta_in, hfta_in, hfta_out, i32, f32, vp, sz,
+                                  vp]),
     "hfta_fused_conv_bwd": (i32, [i32, C.POINTER(hfta_conv_desc), i32, hfta_in, hfta_in, hfta_in, hfta_out, vp, i64,
                                   i32, vp, sz, vp]),
     "hfta_loss_bce_logits": (i32, [i32, i64, i32, hfta_in, f32, vp, vp, hfta_out, vp, sz, vp]),

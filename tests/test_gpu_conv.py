@@ -61,7 +61,7 @@ def host(t):
     return t.detach().float().cpu().numpy().astype(np.float64)
 
 
-def run_layer(layer, B, N, dtype, shared, seed=0):
+def run_layer(layer, B, N, dtype, shared, seed=0, act=0, alpha=0.0):
     name, tr, Hs, Ci, Co, k, st, pd = layer
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     code = 1 if dtype == "bf16" else 0
@@ -91,16 +91,16 @@ def run_layer(layer, B, N, dtype, shared, seed=0):
     xbs = 0 if shared else N * Hs * Hs * Ci
     wbs = int(np.prod(Wg.shape[1:]))
     H.hfta_fused_conv_fwd(B, d, code, H.tin(Xd, xbs, Ci), H.tin(Wd, wbs, wld), H.tout(Y, N * Ho * Ho * Co, Co),
-                          H.ptr(ws), ws.numel(), s())
+                          act, alpha, H.ptr(ws), ws.numel(), s())
     H.hfta_fused_conv_bwd(B, d, code, H.tin(dYd, N * Ho * Ho * Co, Co), H.tin(Xd, xbs, Ci), H.tin(Wd, wbs, wld),
                           H.tout(dX, N * Hs * Hs * Ci, Ci), H.ptr(dW), wbs, 1, H.ptr(ws), ws.numel(), s())
     torch.cuda.synchronize()
     return dict(X=X, Wt=Wt, dY=dY, dW0=dW0, Y=host(Y), dX=host(dX), dW=host(dW), Ho=Ho)
 
 
-def check(layer, B, N, dtype, shared):
+def check(layer, B, N, dtype, shared, act=0, alpha=0.0):
     name, tr, Hs, Ci, Co, k, st, pd = layer
-    r = run_layer(layer, B, N, dtype, shared)
+    r = run_layer(layer, B, N, dtype, shared, act=act, alpha=alpha)
     tol_o = 1e-2 if dtype == "bf16" else 1e-4
     tol_w = 1e-4
     for b in range(B):
@@ -115,6 +115,10 @@ def check(layer, B, N, dtype, shared):
             y = OL.conv2d_fwd(xb, Wt, st, pd)
             dx, dw = OL.conv2d_bwd(dyb, xb, Wt, st, pd)
             dw_g = dw.transpose(0, 2, 3, 1)                            # [Co][Ci][kh][kw] -> [Co][kh][kw][Ci]
+        if act == H.ACT_LEAKY_RELU:
+            y = OL.leaky_relu(y, alpha)
+        elif act == H.ACT_TANH:
+            y = OL.tanh(y)
         assert_close(r["Y"][b], y.transpose(0, 2, 3, 1), tol_o, "%s model %d Y" % (name, b))
         assert_close(r["dX"][b], dx.transpose(0, 2, 3, 1), tol_o, "%s model %d dX" % (name, b))
         assert_close(r["dW"][b], r["dW0"][b] + dw_g, tol_w, "%s model %d dW (accumulate)" % (name, b))
@@ -139,3 +143,12 @@ def test_conv_layer_bf16_per_model_inputs():
     for layer in LAYERS:
         if layer[0] in ("D.c2", "D.c3", "D.c4", "G.t2", "G.t3", "G.t4", "G.t5"):
             check(layer, 2, 32, "bf16", shared=False)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_conv_fused_activation(dtype):
+    """The activation of a layer without BN applied by hfta_fused_conv_fwd:
+    D c1 -> LeakyReLU(0.2), G t5 -> Tanh (in the implicit-GEMM epilogue in
+    bf16, a separate pass in fp32), N = 32, B = 2."""
+    check(LAYERS[0], 2, 32, dtype, shared=False, act=H.ACT_LEAKY_RELU, alpha=0.2)
+    check(LAYERS[9], 2, 32, dtype, shared=False, act=H.ACT_TANH, alpha=0.0)
