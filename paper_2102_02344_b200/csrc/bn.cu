@@ -51,9 +51,15 @@ bool vec_ok(const void* p, int64_t ld, int64_t bs, int64_t C, int vec) {
 // per-thread runs; error ~RUN u of a run, then fixed-order fp64 combination
 // across threads and chunks -- reading R15c: a 2000-row fp32 run had moved
 // the BN output z by 5e-5 of a channel's spread)
-constexpr int RUN = 32;
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+int bn_run() { static int v = env_int("HFTA_BN_RUN", 128); return v; }
 
-Geo make_geo(int B, int64_t R, int64_t C, int vec, int bps = 0) {
+// run > 0: chunks short enough that one thread sums <= run rows (reductions);
+// run == 0: apply passes (no reduction, chunks sized for parallelism only)
+Geo make_geo(int B, int64_t R, int64_t C, int vec, int bps = 0, int run = 0) {
   Geo g;
   g.vec = vec;
   g.tpr = (int)std::min<int64_t>(32, pow2ceil(cdiv(C, vec)));
@@ -63,7 +69,7 @@ Geo make_geo(int B, int64_t R, int64_t C, int vec, int bps = 0) {
   int64_t target = (int64_t)(bps > 0 ? bps : bn_blocks_per_sm()) * std::max(num_sms(), 148);
   int64_t chunks = std::max<int64_t>(1, target / ((int64_t)g.colgroups * B));
   chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, cdiv(R, (int64_t)g.rpb * 8)));
-  chunks = std::max<int64_t>(chunks, cdiv(R, (int64_t)g.rpb * RUN));        // runs of <= RUN rows per thread
+  if (run > 0) chunks = std::max<int64_t>(chunks, cdiv(R, (int64_t)g.rpb * run));   // runs of <= run rows per thread
   g.rows_per_chunk = cdiv(cdiv(R, chunks), g.rpb) * g.rpb;
   g.chunks = (int)cdiv(R, g.rows_per_chunk);
   return g;
@@ -71,8 +77,8 @@ Geo make_geo(int B, int64_t R, int64_t C, int vec, int bps = 0) {
 
 // Welford-free stable stats: per-thread fp32 sums of (x - shift) and (x - shift)^2
 // with shift = x[row 0] of the column; merged across row lanes in fixed order.
-template <typename T, int VEC>
-__global__ void __launch_bounds__(NT, 2) k_bn_stats(int64_t R, int64_t C, const T* __restrict__ X,
+template <typename T, int VEC, int U, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_bn_stats(int64_t R, int64_t C, const T* __restrict__ X,
                                                  int64_t xbs, int64_t ld, Geo g,
                                                  double* __restrict__ p1, double* __restrict__ p2) {
   // each thread sums <= RUN rows in fp32 (4 rows' loads in flight), blocks
@@ -89,7 +95,6 @@ __global__ void __launch_bounds__(NT, 2) k_bn_stats(int64_t R, int64_t C, const 
     ld_vec<T, VEC>(Xb + c0, sh);
     const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
     const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-    constexpr int U = 4;
     for (int64_t r = r0 + rl; r < r1; r += U * g.rpb) {
       float x[U][VEC];
 #pragma unroll
@@ -148,8 +153,8 @@ __global__ void k_bn_finalize(int B, int64_t R, int64_t C, const T* __restrict__
   if (rvar) rvar[i] = (float)((1.0 - momentum) * (double)rvar[i] + momentum * var * (double)R / (double)(R - 1));
 }
 
-template <typename T, int VEC>
-__global__ void __launch_bounds__(NT, 2) k_bn_apply(int64_t R, int64_t C, const T* __restrict__ X, int64_t xbs,
+template <typename T, int VEC, int U, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_bn_apply(int64_t R, int64_t C, const T* __restrict__ X, int64_t xbs,
                                                  int64_t xld, T* __restrict__ Y, int64_t ybs, int64_t yld,
                                                  const float* __restrict__ gamma, const float* __restrict__ beta,
                                                  int64_t gbs, const float* __restrict__ smean,
@@ -169,7 +174,6 @@ __global__ void __launch_bounds__(NT, 2) k_bn_apply(int64_t R, int64_t C, const 
   T* Yb = Y + (int64_t)b * ybs + c0;
   const int r0 = (int)((int64_t)chunk * g.rows_per_chunk);
   const int r1 = (int)min(R, (int64_t)r0 + g.rows_per_chunk);
-  constexpr int U = 4;               // four rows' loads in flight per thread
   for (int r = r0 + rl; r < r1; r += U * g.rpb) {
     float x[U][VEC];
 #pragma unroll
@@ -191,8 +195,8 @@ __global__ void __launch_bounds__(NT, 2) k_bn_apply(int64_t R, int64_t C, const 
 // sum dz*(x - mean) (shifted by the exact mean: no cancellation); the apply pass
 // evaluates dx = A*act'(z)*dy + Bx*x + Cc with three per-column constants.
 // Few live per-column values keep these kernels at <= 80 registers (3 CTAs/SM).
-template <typename T, int VEC>
-__global__ void __launch_bounds__(NT, 2) k_bn_bwd_reduce(int64_t R, int64_t C, const T* __restrict__ dY, int64_t dbs,
+template <typename T, int VEC, int U, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_bn_bwd_reduce(int64_t R, int64_t C, const T* __restrict__ dY, int64_t dbs,
                                                          int64_t dld, const T* __restrict__ X, int64_t xbs, int64_t xld,
                                                          const float* __restrict__ gamma,
                                                          const float* __restrict__ beta, int64_t gbs,
@@ -218,7 +222,6 @@ __global__ void __launch_bounds__(NT, 2) k_bn_bwd_reduce(int64_t R, int64_t C, c
     const T* Db = dY + (int64_t)b * dbs;
     const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
     const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-    constexpr int U = 2;             // two rows of both streams in flight
     for (int64_t r = r0 + rl; r < r1; r += U * g.rpb) {
       float x[U][VEC], d[U][VEC];
 #pragma unroll
@@ -288,8 +291,8 @@ __global__ void k_bn_bwd_finalize(int B, int64_t R, int64_t C, int chunks, const
   coef[4 * BC + i] = fc;
 }
 
-template <typename T, int VEC>
-__global__ void __launch_bounds__(NT, 2) k_bn_bwd_apply(int B, int64_t R, int64_t C, const T* __restrict__ dY,
+template <typename T, int VEC, int U, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_bn_bwd_apply(int B, int64_t R, int64_t C, const T* __restrict__ dY,
                                                         int64_t dbs, int64_t dld, const T* __restrict__ X, int64_t xbs,
                                                         int64_t xld, T* __restrict__ dX, int64_t obs, int64_t old,
                                                         int act, float alpha, Geo g, const float* __restrict__ coef) {
@@ -310,7 +313,6 @@ __global__ void __launch_bounds__(NT, 2) k_bn_bwd_apply(int B, int64_t R, int64_
   T* Ob = dX + (int64_t)b * obs;
   const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
   const int64_t r1 = min(R, r0 + g.rows_per_chunk);
-  constexpr int U = 2;               // two rows of both streams in flight
   for (int64_t r = r0 + rl; r < r1; r += U * g.rpb) {
     float x[U][VEC], d[U][VEC];
 #pragma unroll
@@ -330,6 +332,219 @@ __global__ void __launch_bounds__(NT, 2) k_bn_bwd_apply(int B, int64_t R, int64_
         st_vec<T, VEC>(Ob + (r + u * g.rpb) * old + c0, x[u]);
       }
   }
+}
+
+// ------------------------------------------- cp.async row pipelines ------
+// 16-B vectors (8 bf16 / 4 fp32 per thread): each thread streams its rows
+// rbeg, rbeg + step, ... through a private S-stage ring in shared memory
+// (LDGSTS, no registers held by loads in flight): S rows x NS streams x 16 B
+// per thread, S x NS x 4 KB per CTA.  Measured on the seg head shapes: the
+// register-staged loops above reach 2.8-3.9 TB/s on the reductions (one or
+// two rows in flight per thread).
+template <int NS, int S>
+struct Ring {
+  static constexpr uint32_t SLOT = NS * NT * 16;     // bytes per stage
+  static constexpr size_t BYTES = (size_t)S * SLOT;
+};
+
+template <typename T, int NS, int S, typename F>
+__device__ __forceinline__ void row_pipe(const T* g0, int64_t ld0, const T* g1, int64_t ld1, int64_t rbeg,
+                                         int64_t rend, int step, uint32_t ring, F&& f) {
+  constexpr uint32_t SLOT = Ring<NS, S>::SLOT;
+  const int n = rbeg < rend ? (int)((rend - rbeg + step - 1) / step) : 0;
+  const uint32_t tslot = ring + threadIdx.x * 16;
+  auto issue = [&](int k) {
+    const int64_t r = rbeg + (int64_t)k * step;
+    const uint32_t a = tslot + (uint32_t)(k % S) * SLOT;
+    cp_async16(a, g0 + r * ld0);
+    if constexpr (NS == 2) cp_async16(a + NT * 16, g1 + r * ld1);
+  };
+#pragma unroll
+  for (int k = 0; k < S - 1; ++k) {
+    if (k < n) issue(k);
+    cp_async_commit();
+  }
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) {
+    if (i + S - 1 < n) issue(i + S - 1);
+    cp_async_commit();
+    cp_async_wait<S - 1>();                          // row i's group has landed
+    const uint32_t a = tslot + (uint32_t)(i % S) * SLOT;
+    f(rbeg + (int64_t)i * step, a, a + NT * 16);
+  }
+  cp_async_wait<0>();
+}
+
+// fixed-order fp64 merge of the per-thread fp32 runs of a CTA (reuses the ring)
+template <int VEC>
+__device__ __forceinline__ void block_merge(double* s1, double* s2, const float (&a1)[VEC], const float (&a2)[VEC],
+                                            int rl, int lane, const Geo& g, int64_t C, int b, int chunk,
+                                            double* __restrict__ p1, double* __restrict__ p2) {
+  __syncthreads();                                   // every thread is done with its ring slots
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    s1[rl * g.cb + lane * VEC + v] = a1[v];
+    s2[rl * g.cb + lane * VEC + v] = a2[v];
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < g.cb; col += NT) {
+    int64_t c = (int64_t)blockIdx.x * g.cb + col;
+    if (c >= C) continue;
+    double t1 = 0.0, t2 = 0.0;
+    for (int r = 0; r < g.rpb; ++r) { t1 += s1[r * g.cb + col]; t2 += s2[r * g.cb + col]; }
+    int64_t o = ((int64_t)b * g.chunks + chunk) * C + c;
+    p1[o] = t1;
+    p2[o] = t2;
+  }
+}
+
+template <typename T, int VEC> constexpr size_t merge_bytes() { return 2 * (size_t)NT * VEC * sizeof(double); }
+template <typename T, int VEC, int NS, int S> constexpr size_t pipe_smem() {
+  return Ring<NS, S>::BYTES > merge_bytes<T, VEC>() ? Ring<NS, S>::BYTES : merge_bytes<T, VEC>();
+}
+
+template <typename T, int VEC, int S, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_bn_stats_p(int64_t R, int64_t C, const T* __restrict__ X, int64_t xbs,
+                                                        int64_t ld, Geo g, double* __restrict__ p1,
+                                                        double* __restrict__ p2) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int b = blockIdx.z, chunk = blockIdx.y;
+  const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
+  const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
+  const T* Xb = X + (int64_t)b * xbs + c0;
+  float a1[VEC], a2[VEC], sh[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) { a1[v] = 0.f; a2[v] = 0.f; sh[v] = 0.f; }
+  if (c0 < C) {
+    ld_vec<T, VEC>(Xb, sh);
+    const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
+    row_pipe<T, 1, S>(Xb, ld, Xb, ld, r0 + rl, min(R, r0 + g.rows_per_chunk), g.rpb, (uint32_t)__cvta_generic_to_shared(smem_raw),
+                      [&](int64_t, uint32_t sx, uint32_t) {
+                        float x[VEC];
+                        ld_vec_smem<T, VEC>(sx, x);
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) {
+                          const float d = x[v] - sh[v];
+                          a1[v] += d;
+                          a2[v] = fmaf(d, d, a2[v]);
+                        }
+                      });
+  }
+  double* s1 = reinterpret_cast<double*>(smem_raw);
+  block_merge<VEC>(s1, s1 + NT * VEC, a1, a2, rl, lane, g, C, b, chunk, p1, p2);
+}
+
+template <typename T, int VEC, int S, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_bn_apply_p(int64_t R, int64_t C, const T* __restrict__ X, int64_t xbs,
+                                                        int64_t xld, T* __restrict__ Y, int64_t ybs, int64_t yld,
+                                                        const float* __restrict__ gamma,
+                                                        const float* __restrict__ beta, int64_t gbs,
+                                                        const float* __restrict__ smean,
+                                                        const float* __restrict__ sinv, int act, float alpha, Geo g) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int b = blockIdx.z, chunk = blockIdx.y;
+  const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
+  const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
+  if (c0 >= C) return;
+  float sc[VEC], sf[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    float m = smean[(int64_t)b * C + c0 + v], is = sinv[(int64_t)b * C + c0 + v];
+    float ga = gamma[(int64_t)b * gbs + c0 + v], be = beta[(int64_t)b * gbs + c0 + v];
+    bn_affine(ga, be, m, is, sc[v], sf[v]);
+  }
+  const T* Xb = X + (int64_t)b * xbs + c0;
+  T* Yb = Y + (int64_t)b * ybs + c0;
+  const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
+  row_pipe<T, 1, S>(Xb, xld, Xb, xld, r0 + rl, min(R, r0 + g.rows_per_chunk), g.rpb, (uint32_t)__cvta_generic_to_shared(smem_raw),
+                    [&](int64_t r, uint32_t sx, uint32_t) {
+                      float x[VEC];
+                      ld_vec_smem<T, VEC>(sx, x);
+#pragma unroll
+                      for (int v = 0; v < VEC; ++v) x[v] = act_fwd(fmaf(x[v], sc[v], sf[v]), act, alpha);
+                      st_vec<T, VEC>(Yb + r * yld, x);
+                    });
+}
+
+template <typename T, int VEC, int S, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_bn_bwd_reduce_p(int64_t R, int64_t C, const T* __restrict__ dY,
+                                                             int64_t dbs, int64_t dld, const T* __restrict__ X,
+                                                             int64_t xbs, int64_t xld,
+                                                             const float* __restrict__ gamma,
+                                                             const float* __restrict__ beta, int64_t gbs,
+                                                             const float* __restrict__ smean,
+                                                             const float* __restrict__ sinv, int act, float alpha,
+                                                             Geo g, double* __restrict__ p1, double* __restrict__ p2) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int b = blockIdx.z, chunk = blockIdx.y;
+  const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
+  const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
+  float a1[VEC], a2[VEC];            // fp32 runs of <= run rows per thread, fp64 across threads / chunks
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) { a1[v] = 0.f; a2[v] = 0.f; }
+  if (c0 < C) {
+    float ka[VEC], kc[VEC], m[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      m[v] = smean[(int64_t)b * C + c0 + v];
+      bn_affine(gamma[(int64_t)b * gbs + c0 + v], beta[(int64_t)b * gbs + c0 + v], m[v],
+                sinv[(int64_t)b * C + c0 + v], ka[v], kc[v]);
+    }
+    const T* Xb = X + (int64_t)b * xbs + c0;
+    const T* Db = dY + (int64_t)b * dbs + c0;
+    const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
+    row_pipe<T, 2, S>(Xb, xld, Db, dld, r0 + rl, min(R, r0 + g.rows_per_chunk), g.rpb, (uint32_t)__cvta_generic_to_shared(smem_raw),
+                      [&](int64_t, uint32_t sx, uint32_t sd) {
+                        float x[VEC], d[VEC];
+                        ld_vec_smem<T, VEC>(sx, x);
+                        ld_vec_smem<T, VEC>(sd, d);
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) {
+                          const float dz = d[v] * act_grad(fmaf(ka[v], x[v], kc[v]), act, alpha);
+                          a1[v] += dz;
+                          a2[v] = fmaf(dz, x[v] - m[v], a2[v]);
+                        }
+                      });
+  }
+  double* s1 = reinterpret_cast<double*>(smem_raw);
+  block_merge<VEC>(s1, s1 + NT * VEC, a1, a2, rl, lane, g, C, b, chunk, p1, p2);
+}
+
+template <typename T, int VEC, int S, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_bn_bwd_apply_p(int B, int64_t R, int64_t C, const T* __restrict__ dY,
+                                                            int64_t dbs, int64_t dld, const T* __restrict__ X,
+                                                            int64_t xbs, int64_t xld, T* __restrict__ dX, int64_t obs,
+                                                            int64_t old, int act, float alpha, Geo g,
+                                                            const float* __restrict__ coef) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int b = blockIdx.z, chunk = blockIdx.y;
+  const int lane = threadIdx.x % g.tpr, rl = threadIdx.x / g.tpr;
+  const int64_t c0 = (int64_t)blockIdx.x * g.cb + (int64_t)lane * VEC;
+  if (c0 >= C) return;
+  const int64_t BC = (int64_t)B * C;
+  float kA[VEC], kB[VEC], kC[VEC], ka[VEC], kc[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    int64_t i = (int64_t)b * C + c0 + v;
+    kA[v] = coef[i]; kB[v] = coef[BC + i]; kC[v] = coef[2 * BC + i];
+    ka[v] = coef[3 * BC + i]; kc[v] = coef[4 * BC + i];
+  }
+  const T* Xb = X + (int64_t)b * xbs + c0;
+  const T* Db = dY + (int64_t)b * dbs + c0;
+  T* Ob = dX + (int64_t)b * obs + c0;
+  const int64_t r0 = (int64_t)chunk * g.rows_per_chunk;
+  row_pipe<T, 2, S>(Xb, xld, Db, dld, r0 + rl, min(R, r0 + g.rows_per_chunk), g.rpb, (uint32_t)__cvta_generic_to_shared(smem_raw),
+                    [&](int64_t r, uint32_t sx, uint32_t sd) {
+                      float x[VEC], d[VEC];
+                      ld_vec_smem<T, VEC>(sx, x);
+                      ld_vec_smem<T, VEC>(sd, d);
+#pragma unroll
+                      for (int v = 0; v < VEC; ++v) {
+                        const float gd = d[v] * act_grad(fmaf(ka[v], x[v], kc[v]), act, alpha);
+                        x[v] = fmaf(kA[v], gd, fmaf(kB[v], x[v], kC[v]));
+                      }
+                      st_vec<T, VEC>(Ob + r * old, x);
+                    });
 }
 
 // --------------------------------------------------- BN + act + max (K8a) --
@@ -506,12 +721,34 @@ int pick_vec(hfta_dtype dt, int64_t C, std::initializer_list<std::tuple<const vo
   return vec;
 }
 
-constexpr int BWD_BPS = 32;   // backward passes read 2 tensors: more row chunks in flight (measured)
+// backward passes read 2 tensors: more row chunks in flight (measured)
+int bn_bwd_bps() { static int v = env_int("HFTA_BN_BWD_BPS", 32); return v; }
+int bn_s1() { static int v = env_int("HFTA_BN_S1", 16); return v; }   // ring stages, one-stream kernels
+int bn_s2() { static int v = env_int("HFTA_BN_S2", 8); return v; }    // ring stages, two-stream kernels
+
+template <typename K_, typename... A>
+void launch_pipe(K_* kern, size_t smem, dim3 grid, cudaStream_t s, A... args) {
+  ensure_smem(kern, smem);
+  kern<<<grid, NT, smem, s>>>(args...);
+}
+// one-stream kernels (stats, apply) at S1 in {8, 16}; two-stream (bwd reduce / apply) at S2 in {4, 8}
+#define LAUNCH_P1(T, KERNEL, GRID, ...)                                                        \
+  do {                                                                                        \
+    constexpr int V_ = 16 / (int)sizeof(T);                                                   \
+    if (bn_s1() <= 8) launch_pipe(KERNEL<T, V_, 8, 4>, pipe_smem<T, V_, 1, 8>(), GRID, s, __VA_ARGS__);   \
+    else launch_pipe(KERNEL<T, V_, 16, 3>, pipe_smem<T, V_, 1, 16>(), GRID, s, __VA_ARGS__);             \
+  } while (0)
+#define LAUNCH_P2(T, KERNEL, GRID, ...)                                                        \
+  do {                                                                                        \
+    constexpr int V_ = 16 / (int)sizeof(T);                                                   \
+    if (bn_s2() <= 4) launch_pipe(KERNEL<T, V_, 4, 3>, pipe_smem<T, V_, 2, 4>(), GRID, s, __VA_ARGS__);   \
+    else launch_pipe(KERNEL<T, V_, 8, 3>, pipe_smem<T, V_, 2, 8>(), GRID, s, __VA_ARGS__);               \
+  } while (0)
 
 size_t bn_parts_bytes(int B, int64_t R, int64_t C) {
   int ch = 1;
   for (int vec : {1, 4, 8})
-    for (int bps : {0, BWD_BPS}) ch = std::max(ch, make_geo(B, R, C, vec, bps).chunks);
+    for (int bps : {0, bn_bwd_bps()}) ch = std::max(ch, make_geo(B, R, C, vec, bps, bn_run()).chunks);
   return align_up(2 * (size_t)B * ch * C * sizeof(double), 256);
 }
 
@@ -526,6 +763,9 @@ using namespace hfta;
     else if (vec == 4) KERNEL<T, 4><<<GRID, NT, 0, s>>>(__VA_ARGS__);                          \
     else KERNEL<T, 8><<<GRID, NT, 0, s>>>(__VA_ARGS__);                                        \
   } while (0)
+
+// the register-staged kernels serve unaligned / odd-width tensors (VEC = 1)
+#define LAUNCH_V1(T, KERNEL, GRID, ...) KERNEL<T, 1, 1, 3><<<GRID, NT, 0, s>>>(__VA_ARGS__)
 
 #define DT_DISPATCH(dt, ...)                                                                   \
   do {                                                                                        \
@@ -556,18 +796,26 @@ hfta_status hfta_fused_bn_fwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_i
   HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "bn_fwd: workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = (cudaStream_t)stream;
   int vec = pick_vec(dt, C, {{X.ptr, X.ld, X.bstride}, {Y.ptr, Y.ld, Y.bstride}});
-  Geo g = make_geo(B, R, C, vec);
+  Geo g = make_geo(B, R, C, vec, 0, bn_run());
+  Geo ga = make_geo(B, R, C, vec);
   double* p1 = reinterpret_cast<double*>(ws);
   double* p2 = p1 + (size_t)B * g.chunks * C;
-  dim3 grid(g.colgroups, g.chunks, B);
-  DT_DISPATCH(dt, {
-    LAUNCH_VEC(T, vec, k_bn_stats, grid, R, C, (const T*)X.ptr, X.bstride, X.ld, g, p1, p2);
+  dim3 grid(g.colgroups, g.chunks, B), grida(ga.colgroups, ga.chunks, B);
+    DT_DISPATCH(dt, {
+    if (vec > 1) LAUNCH_P1(T, k_bn_stats_p, grid, R, C, (const T*)X.ptr, X.bstride, X.ld, g, p1, p2);
+    else LAUNCH_V1(T, k_bn_stats, grid, R, C, (const T*)X.ptr, X.bstride, X.ld, g, p1, p2);
     k_bn_finalize<T><<<(unsigned)cdiv((int64_t)B * C, 256), 256, 0, s>>>(
         B, R, C, (const T*)X.ptr, X.bstride, g.chunks, p1, p2, eps, momentum, running_mean, running_var,
         save_mean, save_invstd);
     if (Y.ptr)
-      LAUNCH_VEC(T, vec, k_bn_apply, grid, R, C, (const T*)X.ptr, X.bstride, X.ld, (T*)Y.ptr, Y.bstride, Y.ld,
-                 gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, g);
+    {
+      if (vec > 1)
+        LAUNCH_P1(T, k_bn_apply_p, grida, R, C, (const T*)X.ptr, X.bstride, X.ld, (T*)Y.ptr, Y.bstride, Y.ld,
+                  gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, ga);
+      else
+        LAUNCH_V1(T, k_bn_apply, grida, R, C, (const T*)X.ptr, X.bstride, X.ld, (T*)Y.ptr, Y.bstride, Y.ld,
+                  gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, ga);
+    }
   });
   count_launches(Y.ptr ? 3 : 2);
   return post_launch(s, "hfta_fused_bn_fwd");
@@ -588,19 +836,24 @@ hfta_status hfta_fused_bn_bwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_i
   HFTA_REQUIRE(ws && ws_bytes >= need, HFTA_ERR_WORKSPACE, "bn_bwd: workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = (cudaStream_t)stream;
   int vec = pick_vec(dt, C, {{X.ptr, X.ld, X.bstride}, {dY.ptr, dY.ld, dY.bstride}, {dX.ptr, dX.ld, dX.bstride}});
-  Geo g = make_geo(B, R, C, vec, BWD_BPS);
+  Geo g = make_geo(B, R, C, vec, bn_bwd_bps(), bn_run());
+  Geo ga = make_geo(B, R, C, vec, bn_bwd_bps());
   double* p1 = reinterpret_cast<double*>(ws);
   double* p2 = p1 + (size_t)B * g.chunks * C;
   size_t parts_bytes = bn_parts_bytes(B, R, C);
   float* coef = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + parts_bytes);
-  dim3 grid(g.colgroups, g.chunks, B);
-  DT_DISPATCH(dt, {
-    LAUNCH_VEC(T, vec, k_bn_bwd_reduce, grid, R, C, (const T*)dY.ptr, dY.bstride, dY.ld, (const T*)X.ptr,
+  dim3 grid(g.colgroups, g.chunks, B), grida(ga.colgroups, ga.chunks, B);
+    DT_DISPATCH(dt, {
+    if (vec > 1) LAUNCH_P2(T, k_bn_bwd_reduce_p, grid, R, C, (const T*)dY.ptr, dY.bstride, dY.ld, (const T*)X.ptr,
+               X.bstride, X.ld, gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, g, p1, p2);
+    else LAUNCH_V1(T, k_bn_bwd_reduce, grid, R, C, (const T*)dY.ptr, dY.bstride, dY.ld, (const T*)X.ptr,
                X.bstride, X.ld, gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, g, p1, p2);
     k_bn_bwd_finalize<<<(unsigned)cdiv((int64_t)B * C, 256), 256, 0, s>>>(
         B, R, C, g.chunks, p1, p2, gamma, beta, gb_bstride, save_mean, save_invstd, dgamma, dbeta, accumulate, coef);
-    LAUNCH_VEC(T, vec, k_bn_bwd_apply, grid, B, R, C, (const T*)dY.ptr, dY.bstride, dY.ld, (const T*)X.ptr,
-               X.bstride, X.ld, (T*)dX.ptr, dX.bstride, dX.ld, (int)act, act_alpha, g, coef);
+    if (vec > 1) LAUNCH_P2(T, k_bn_bwd_apply_p, grida, B, R, C, (const T*)dY.ptr, dY.bstride, dY.ld, (const T*)X.ptr,
+              X.bstride, X.ld, (T*)dX.ptr, dX.bstride, dX.ld, (int)act, act_alpha, ga, coef);
+    else LAUNCH_V1(T, k_bn_bwd_apply, grida, B, R, C, (const T*)dY.ptr, dY.bstride, dY.ld, (const T*)X.ptr,
+              X.bstride, X.ld, (T*)dX.ptr, dX.bstride, dX.ld, (int)act, act_alpha, ga, coef);
   });
   count_launches(3);
   return post_launch(s, "hfta_fused_bn_bwd");

@@ -110,6 +110,27 @@ __device__ __forceinline__ void st_vec(T* p, const float (&v)[VEC]) {
   }
 }
 
+// ---- cp.async (LDGSTS) row pipelines: loads in flight without registers --
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// 16 B of shared memory (8 bf16 or 4 fp32) -> VEC floats
+template <typename T, int VEC>
+__device__ __forceinline__ void ld_vec_smem(uint32_t saddr, float (&v)[VEC]) {
+  static_assert(VEC * sizeof(T) == 16, "16-byte vectors only");
+  uint4 u;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "r"(saddr));
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    unpack_bf2(u.x, v[0], v[1]); unpack_bf2(u.y, v[2], v[3]); unpack_bf2(u.z, v[4], v[5]); unpack_bf2(u.w, v[6], v[7]);
+  } else {
+    v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y); v[2] = __uint_as_float(u.z); v[3] = __uint_as_float(u.w);
+  }
+}
+
 __device__ __forceinline__ float act_fwd(float z, int act, float alpha) {
   if (act == HFTA_ACT_RELU) return z > 0.f ? z : 0.f;
   if (act == HFTA_ACT_LEAKY_RELU) return z > 0.f ? z : alpha * z;
