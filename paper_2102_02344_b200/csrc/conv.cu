@@ -269,6 +269,32 @@ size_t col_bytes(int B, const hfta_conv_desc* d, hfta_dtype dt, const Shape& sh)
   return (f && g && w) ? 0 : align_up((size_t)B * sh.Ms * sh.Kc * dsize(dt), 256);
 }
 
+// Mode 5 (phase-merged sub-pixel GEMM) for a mode-2 contraction with 8
+// output channels (G t5 fwd, D c1 dgrad): the 4 phases x 8 channels fill one
+// 32-wide tile instead of four 8-of-64-wide ones.  Its weight operand is
+// rebuilt per call into the workspace.
+bool merged_phases(const ConvTcP& cp) { return cp.mode == 2 && cp.w_cn == 8 && cp.w_ca % 64 == 0; }
+size_t merged_w_bytes(int B, const ConvTcP& cp) {
+  return merged_phases(cp) ? align_up((size_t)(cp.opd_bs == 0 ? 1 : B) * 32 * 9 * cp.w_ca * 2, 256) : 0;
+}
+ConvTcP as_merged(const ConvTcP& cp, void* wp) {
+  ConvTcP m = cp;
+  m.mode = 5; m.N = 32; m.K = 9 * (int64_t)cp.w_ca;
+  m.opd = wp; m.opd_ld = m.K; m.opd_bs = cp.opd_bs == 0 ? 0 : 32 * m.K;
+  return m;
+}
+// run a mode-2 contraction, merged when eligible (wp: >= merged_w_bytes of workspace)
+hfta_status run_phases(const ConvTcP& cp, void* wp, size_t wpb, cudaStream_t s) {
+  if (merged_phases(cp) && wp && wpb >= merged_w_bytes(cp.B, cp)) {
+    ConvTcP m = as_merged(cp, wp);
+    if (conv_tc_supported(m)) {
+      if (hfta_status st = conv_subpixel_weights(cp.B, cp.w_ca, cp.w_mn, cp.opd, cp.opd_bs, wp, s)) return st;
+      return conv_tc(m, s);
+    }
+  }
+  return conv_tc(cp, s);
+}
+
 // split-K partials of a tensor-core conv wgrad (modes 3, 4)
 size_t conv_wgrad_part(int B, int64_t rows, int64_t M, int64_t N) {
   int sp; int64_t ch;
@@ -314,6 +340,14 @@ size_t hfta_fused_conv_workspace(int B, const hfta_conv_desc* d, hfta_dtype dt) 
   size_t lin = std::max(hfta_fused_linear_bwd_workspace(B, M, sh.Co, sh.Kc, dt),
                         hfta_fused_linear_bwd_workspace(B, M, sh.Kc, sh.Ci, dt));
   lin = std::max(lin, std::max(conv_wgrad_part(B, M, sh.Co, sh.Kc), conv_wgrad_part(B, M, sh.Kc, sh.Ci)));
+  if (dt == HFTA_BF16 && k4s2p1(d)) {          // phase-merged weights (fwd of a ConvT, dgrad of a Conv)
+    char* a = reinterpret_cast<char*>(256);
+    const int64_t xe = img_elems(d->N, d->H, d->W, d->C_in), ye = img_elems(d->N, sh.Ho, sh.Wo, d->C_out);
+    const int64_t we = (int64_t)d->kh * d->kw * d->C_in * d->C_out;
+    const int64_t wld = sh.transposed ? d->C_in : (int64_t)d->kh * d->kw * d->C_in;
+    lin = std::max(lin, merged_w_bytes(B, fwd_cp(B, d, sh, a, xe, a, we, wld, a, ye)));
+    lin = std::max(lin, merged_w_bytes(B, dgrad_cp(B, d, sh, a, ye, a, we, wld, a, xe)));
+  }
   return col + align_up(lin, 256);
 }
 
@@ -341,7 +375,8 @@ hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
     ConvTcP cp = fwd_cp(B, d, sh, X.ptr, X.bstride, W.ptr, W.bstride, W.ld, Y.ptr, Y.bstride);
     cp.act = act; cp.act_alpha = act_alpha;      // fused into the epilogue
     if (conv_tc_supported(cp)) {
-      if (hfta_status st = conv_tc(cp, s)) return st;
+      const size_t colb = col_bytes(B, d, dt, sh);
+      if (hfta_status st = run_phases(cp, col + colb, ws_bytes - colb, s)) return st;
       return post_launch(s, "hfta_fused_conv_fwd");
     }
   }
@@ -430,7 +465,7 @@ hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
   if (tc && need_dX) {
     ConvTcP cp = dgrad_cp(B, d, sh, dY.ptr, dY.bstride, W.ptr, W.bstride, W.ld, dX.ptr, dX.bstride);
     if (conv_tc_supported(cp)) {
-      if (hfta_status st = conv_tc(cp, s)) return st;
+      if (hfta_status st = run_phases(cp, lws, lwsb, s)) return st;     // after the wgrad's use of lws
       need_dX = false;
     }
   }

@@ -60,7 +60,8 @@ hfta_status gemm_tf32(const GemmP& p, cudaStream_t s);
 // NHWC per model [B][n][h][w][c] with c % 64 == 0 (bstride 0 = shared).
 struct ConvTcP {
   int mode;                 // 1 Conv2d fwd / ConvT2d dgrad, 2 sub-pixel phases (ConvT2d fwd / Conv2d dgrad),
-                            // 3 Conv2d wgrad, 4 ConvT2d wgrad
+                            // 3 Conv2d wgrad, 4 ConvT2d wgrad, 5 merged sub-pixel phases for 8 output
+                            // channels (opd = the [32][9 x C] phase-merged weights of conv_subpixel_weights)
   int B;
   int64_t M, N, K;          // GEMM extents (mode 2: per phase)
   const void* img; int64_t img_bs; int img_n, img_h, img_w, img_c;   // the gathered / shifted image operand
@@ -75,6 +76,9 @@ struct ConvTcP {
   int act; float act_alpha;        // 1, 2 (forward): activation applied in the epilogue (layers without BN)
 };
 bool conv_tc_supported(const ConvTcP& p);
+// mode 5 operand: Wp[b][(ph,pw,co)][(dy,dx,ca)] (32 x 9 Ca, K-major bf16) from mode-2 weights
+// (w_mn: Conv2d W [Ca][16][8], else ConvT2d Wt [16][8][Ca]); zeros where phase (ph,pw) does not use tap (dy,dx)
+hfta_status conv_subpixel_weights(int B, int ca, int w_mn, const void* W, int64_t w_bs, void* Wp, cudaStream_t s);
 hfta_status conv_tc(const ConvTcP& p, cudaStream_t s);
 
 // Dispatch: skinny -> tcgen05 -> SIMT (EPI features: skinny / tcgen05 only).

@@ -124,6 +124,10 @@ __device__ __forceinline__ void tile_coords(uint32_t t, const TcArgs& p, int& mt
 //                           the epilogue interleaves row (n,i,j) into output pixel (n, 2i+ph, 2j+pw)
 //   3  Conv2d wgrad:        A = dY (MN-major), B(k = (n,oy,ox), n = (tap,ci)) gathered (stride 2)
 //   4  ConvT2d wgrad:       A(k = (n,i,j), m = (tap,co)) = dY[n][2i-1+kh][2j-1+kw][co] gathered, B = X (MN-major)
+//   5  mode 2 for 8 output channels, the 4 phases merged into N = 32 columns (ph, pw, co):
+//                           A(m = (n,i,j), k = (dy,dx,c)) = X[n][i+dy][j+dx][c], dy, dx in {-1,0,1} (9 shifted
+//                           boxes), B = the phase-merged weights (zeros where a phase skips a tap); each
+//                           row's 32 columns are 4 output pixels x 8 channels (four 16-B stores)
 // NARROW (CONV 1, 3, 4): the image operand has 8 channels (16-B rows: D's
 // input image, G's output image) -- one SWIZZLE_NONE box per kernel tap,
 // core-matrix layout: K-major A (mode 1) = 8 taps x 8 channels per k-block,
@@ -224,7 +228,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int ba = p.a_shared ? 0 : b, bb = p.b_shared ? 0 : b;
         const int m0 = mt * BM, n0 = nt * BN;
         int gn0 = 0, gy0 = 0, gx0 = 0;            // CONV 1, 2: grid position of the tile's first row
-        if constexpr (CONV == 1 || CONV == 2) grid_pos((uint32_t)m0, p, gn0, gy0, gx0);
+        if constexpr (CONV == 1 || CONV == 2 || CONV == 5) grid_pos((uint32_t)m0, p, gn0, gy0, gx0);
         if constexpr (BRES) {
           const int64_t key = (int64_t)bb * p.tiles_n + nt;
           if (key != bkey) {                       // new (model, n-tile): reload the resident B
@@ -278,6 +282,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             } else {
               tma_load_4d(sb, &tmB, &full[stage], cb * 64, n0, tap, bb);
             }
+          } else if constexpr (CONV == 5) {               // shifted box (dy, dx) of 9, phase-merged weights
+            const int t9 = kb / p.cblk, cb = kb - t9 * p.cblk;
+            tma_load_5d(sa, &tmA, &full[stage], cb * 64, gx0 + t9 % 3 - 1, gy0 + t9 / 3 - 1, gn0, ba);
+            tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
           } else if constexpr (CONV == 3) {               // dY plain, B = stride-2 gather of X per (tap, ci) atom
             tma_load_3d(sa, &tmA, &full[stage], m0, k0, ba);
             tma_load_3d(sa + 8192, &tmA, &full[stage], m0 + 64, k0, ba);
@@ -414,7 +422,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     // sub-pixel phase tiles 64 wide (direct stores, no TMA staging): the two warps
     // of a lane quarter take one 32-column half each instead of idling one of them
     constexpr bool SPLIT_COLS = CONV == 2 && NSTEP == 1;
-    const int my_steps = SPLIT_COLS ? 1 : (NSTEP - half + 1) / 2;
+    constexpr bool ONE_HALF = BN == 32;           // one 32-column half: the first warp of each quarter
+    const int my_steps = ONE_HALF ? (half == 0 ? 1 : 0) : (SPLIT_COLS ? 1 : (NSTEP - half + 1) / 2);
     const int acc = grp;                          // local tile parity = accumulator buffer
     uint32_t acc_phase = 0;
     int64_t cur_key = -1;
@@ -493,19 +502,19 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         uint8_t* buf = stage_out + ew * 4096;  // bf16 staging: this warp's 32 x 64 sub-tile
         const uint32_t rowaddr = smem_u32(buf) + lane * 128;
         const uint32_t sw = (uint32_t)(lane & 7);
-        if (!OUT_F32 && CONV != 2 && n0 < p.N) {   // the previous store of this warp (a tile ago) has read its staging
+        if (!OUT_F32 && CONV != 2 && CONV != 5 && n0 < p.N) {   // the previous store of this warp (a tile ago) has read its staging
           if (lane == 0) tma_store_wait_read<0>();
           __syncwarp();
         }
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
-          if (SPLIT_COLS && hh != half) continue;        // warp-uniform
+          if ((SPLIT_COLS && hh != half) || (ONE_HALF && hh != 0)) continue;   // warp-uniform
           uint32_t u[32];
           const uint32_t ta = tmem_base + (uint32_t)(acc * ABUF + (SPLIT_COLS ? 0 : j * 64) + hh * 32) +
                               ((uint32_t)(quarter * 32) << 16);
           tmem_ld32_nowait(ta, u);
           tmem_wait_ld();
-          if (last && (SPLIT_COLS || hh == 1)) {   // this warp's last TMEM read of the tile: release the accumulator
+          if (last && (SPLIT_COLS || ONE_HALF || hh == 1)) {   // this warp's last TMEM read of the tile: release it
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -541,9 +550,19 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 add_f32x2(v[4 * q + 2], v[4 * q + 3], t4.z, t4.w);
               }
             } else if (brow) {
+              const float* br = brow + c0;
+              if (c0 + 32 <= p.N && (reinterpret_cast<uintptr_t>(br) & 15) == 0) {
 #pragma unroll
-              for (int q = 0; q < 32; ++q)
-                if (c0 + q < p.N) v[q] += brow[c0 + q];
+                for (int q = 0; q < 8; ++q) {   // rows of one sample share the bias row: L1 broadcast
+                  const float4 t4 = __ldg(reinterpret_cast<const float4*>(br) + q);
+                  add_f32x2(v[4 * q], v[4 * q + 1], t4.x, t4.y);
+                  add_f32x2(v[4 * q + 2], v[4 * q + 3], t4.z, t4.w);
+                }
+              } else {
+#pragma unroll
+                for (int q = 0; q < 32; ++q)
+                  if (c0 + q < p.N) v[q] += br[q];
+              }
             }
             if constexpr (CONV != 0) {           // activation of a layer without BN (D c1 LeakyReLU, G t5 Tanh)
               if (p.act == HFTA_ACT_LEAKY_RELU) {
@@ -618,6 +637,22 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
                 for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
                 dst[q] = w4;
+              }
+            }
+          } else if constexpr (CONV == 5) {
+            // merged phases: column 8 q + c of row (n, i, j) -> pixel (n, 2i + (q >> 1), 2j + (q & 1)), channel c
+            if (row_ok) {
+              int gn, gy, gx;
+              grid_pos((uint32_t)m, p, gn, gy, gx);
+              __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(p.C) + (int64_t)b * p.y_bs;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int64_t pix = ((int64_t)gn * p.y_h + 2 * gy + (q >> 1)) * p.y_w + 2 * gx + (q & 1);
+                uint4 w4;
+                __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+                *reinterpret_cast<uint4*>(yb + pix * 8) = w4;
               }
             }
           } else if constexpr (!OUT_F32) {
@@ -833,7 +868,7 @@ hfta_status img_map(CUtensorMap* m, const ConvTcP& p, int nb, int rows, int st) 
 
 template <int CONV, bool A_MN, bool B_MN, int BN, bool OUT_F32, bool NARROW = false>
 hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
-  constexpr int STAGES = (BN == 256) ? 3 : 4;
+  constexpr int STAGES = (BN == 256) ? 3 : (BN == 32 ? 7 : 4);
   constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + (OUT_F32 ? 0 : NEPI_ALL * 4096) +
                           NEPI_ALL * BN * 4 + ((A_MN && B_MN && OUT_F32) ? (size_t)STAGES * 8192 : 0);
   static_assert(SMEM <= 232448, "shared memory budget");
@@ -860,6 +895,9 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
         st = make_map_nd(&tb, cp.opd, 4, dims, str, box, es);
       }
     }
+  } else if (CONV == 5) {
+    st = img_map(&ta, cp, nbi, BM, 1);
+    if (!st) st = make_map(&tb, cp.opd, cp.K, cp.N, cp.opd_ld, cp.opd_bs, nbo, BK, BN);
   } else if (CONV == 3) {
     st = make_map(&ta, cp.opd, cp.M, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, BK);
     if (!st) st = img_map(&tb, cp, nbi, BK, 2);
@@ -883,7 +921,7 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   a.B = cp.B; a.M = cp.M; a.N = cp.N; a.K = cp.K;
   a.splits = CONV == 2 ? 4 : (CONV == 1 ? 1 : std::max(cp.splits, 1));     // mode 2: the 4 phases
   a.k_chunk = (CONV == 1 || CONV == 2 || cp.k_chunk <= 0) ? cp.K : cp.k_chunk;
-  a.a_shared = (CONV == 1 || CONV == 2 || CONV == 4) ? (nbi == 1 && cp.B > 1) : (nbo == 1 && cp.B > 1);
+  a.a_shared = (CONV == 1 || CONV == 2 || CONV == 4 || CONV == 5) ? (nbi == 1 && cp.B > 1) : (nbo == 1 && cp.B > 1);
   a.b_shared = (CONV == 3) ? (nbi == 1 && cp.B > 1) : (nbo == 1 && cp.B > 1);
   a.C = cp.C; a.c_bs = cp.c_bs; a.c_ld = cp.c_ld;
   a.accumulate = cp.accumulate; a.part = cp.part;
@@ -893,8 +931,8 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   a.gw = cp.grid_w; a.gh = cp.grid_h; a.ghw = cp.grid_w * cp.grid_h;
   a.cblk = cp.img_c / 64;
   a.cg = cp.img_c;   // 3: C_in per tap of B; 4: C_out (the gathered dY's channels) per tap of A
-  a.y_c = (int)cp.N; a.y_h = cp.y_h; a.y_w = cp.y_w; a.y_bs = cp.c_bs;
-  a.act = (CONV == 1 || CONV == 2) ? cp.act : HFTA_ACT_NONE; a.act_alpha = cp.act_alpha;
+  a.y_c = CONV == 5 ? 8 : (int)cp.N; a.y_h = cp.y_h; a.y_w = cp.y_w; a.y_bs = cp.c_bs;
+  a.act = (CONV == 1 || CONV == 2 || CONV == 5) ? cp.act : HFTA_ACT_NONE; a.act_alpha = cp.act_alpha;
   auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, false, 0, CONV, NARROW>;
   ensure_smem(kern, SMEM);
   const int64_t total = (int64_t)a.tiles_m * a.tiles_n * a.splits * a.B;
@@ -908,18 +946,20 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
 }  // namespace
 
 bool conv_tc_supported(const ConvTcP& p) {
-  const bool narrow = p.img_c == 8 && p.mode != 2;     // 8-channel image operand (SWIZZLE_NONE boxes)
+  const bool narrow = p.img_c == 8 && p.mode != 2 && p.mode != 5;   // 8-channel image operand (SWIZZLE_NONE boxes)
   if (p.M < 1 || p.N < 1 || p.K < 1 || (p.img_c % 64 && !narrow) || !aligned16(p.img) || !aligned16(p.opd) ||
       !aligned16(p.C))
     return false;
   if ((p.img_bs * 2) % 16 || (p.opd_bs * 2) % 16 || (p.opd_ld * 2) % 16) return false;
   uint32_t bw, bh, bn;
-  const int rows = (p.mode == 1 || p.mode == 2) ? BM : BK;
+  const int rows = (p.mode == 1 || p.mode == 2 || p.mode == 5) ? BM : BK;
   if (!grid_box(p.grid_w, p.grid_h, p.img_n, rows, bw, bh, bn)) return false;
   switch (p.mode) {
     case 1: return p.K == 16 * (int64_t)p.img_c && p.N % 16 == 0 && (p.c_ld * 2) % 16 == 0 && (p.c_bs * 2) % 16 == 0;
     case 2: return p.K == 4 * (int64_t)p.img_c && p.N % 8 == 0 && p.N <= 256 && p.y_h == 2 * p.grid_h &&
                    p.y_w == 2 * p.grid_w && (p.c_bs * 2) % 16 == 0;
+    case 5: return p.K == 9 * (int64_t)p.img_c && p.N == 32 && p.y_h == 2 * p.grid_h && p.y_w == 2 * p.grid_w &&
+                   (p.c_bs * 2) % 16 == 0 && (p.opd_ld * 2) % 16 == 0;
     case 3: return p.N == 16 * (int64_t)p.img_c && p.c_ld % 4 == 0;     // narrow: N = 128 (one tile)
     case 4: return p.M == 16 * (int64_t)p.img_c && p.N % 16 == 0 && p.c_ld % 4 == 0;   // narrow: M = 128
     default: return false;
@@ -958,9 +998,45 @@ hfta_status conv_tc(const ConvTcP& p, cudaStream_t s) {
       if (p.N <= 64) return launch_conv<2, false, false, 64, false>(p, s);
       if (p.N <= 128) return launch_conv<2, false, false, 128, false>(p, s);
       return launch_conv<2, false, false, 256, false>(p, s);
+    case 5: return launch_conv<5, false, false, 32, false>(p, s);
     case 3: return launch_conv<3, true, true, 128, true>(p, s);
     default: return launch_conv<4, true, true, 128, true>(p, s);
   }
+}
+
+// ---- mode 5 operand: the phase-merged weights ----
+// kernel row / column of phase `par` for input offset `off` (phase_tap's inverse), -1: unused
+__device__ __forceinline__ int phase_k(int par, int off) {
+  return par ? (off == 1 ? 0 : (off == 0 ? 2 : -1)) : (off == 0 ? 1 : (off == -1 ? 3 : -1));
+}
+
+__global__ void k_subpixel_w(int nb, int ca, int w_mn, const __nv_bfloat16* __restrict__ W, int64_t w_bs,
+                             __nv_bfloat16* __restrict__ Wp) {
+  const int64_t per = 32 * 9 * (int64_t)ca;
+  const int64_t total = per * nb;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / per);
+    const int64_t r = i - b * per;
+    const int n = (int)(r / (9 * ca)), k = (int)(r - (int64_t)n * 9 * ca);
+    const int t9 = k / ca, c = k - t9 * ca, phase = n >> 3, co = n & 7;
+    const int kh = phase_k(phase >> 1, t9 / 3 - 1), kw = phase_k(phase & 1, t9 % 3 - 1);
+    __nv_bfloat16 v = __float2bfloat16_rn(0.f);
+    if (kh >= 0 && kw >= 0) {
+      const int tap = kh * 4 + kw;
+      const __nv_bfloat16* wb = W + (int64_t)b * w_bs;
+      v = w_mn ? wb[((int64_t)c * 16 + tap) * 8 + co] : wb[((int64_t)tap * 8 + co) * ca + c];
+    }
+    Wp[i] = v;
+  }
+}
+
+hfta_status conv_subpixel_weights(int B, int ca, int w_mn, const void* W, int64_t w_bs, void* Wp, cudaStream_t s) {
+  const int nb = w_bs == 0 ? 1 : B;
+  const int64_t total = (int64_t)nb * 32 * 9 * ca;
+  k_subpixel_w<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 4 * 148), 256, 0, s>>>(
+      nb, ca, w_mn, reinterpret_cast<const __nv_bfloat16*>(W), w_bs, reinterpret_cast<__nv_bfloat16*>(Wp));
+  count_launches(1);
+  return HFTA_OK;
 }
 
 bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32) {
