@@ -23,7 +23,7 @@
 #include "gemm.cuh"
 
 namespace hfta {
-void wgrad_split_rows(int B, int64_t rows, int64_t N, int64_t K, int* splits, int64_t* chunk);
+void wgrad_split_rows(int B, int64_t rows, int64_t N, int64_t K, int* splits, int64_t* chunk, int bn = 128);
 hfta_status colsum_impl(int B, int64_t rows, int64_t C, int64_t group, hfta_dtype dt, hfta_in X, float* S,
                         int64_t S_bstride, int accumulate, void* ws, size_t ws_bytes, cudaStream_t s);
 size_t colsum_ws(int B, int64_t rows, int64_t C, int64_t group);
@@ -297,15 +297,19 @@ hfta_status run_phases(const ConvTcP& cp, void* wp, size_t wpb, cudaStream_t s) 
 
 // split-K partials of a tensor-core conv wgrad (modes 3, 4)
 size_t conv_wgrad_part(int B, int64_t rows, int64_t M, int64_t N) {
-  int sp; int64_t ch;
-  wgrad_split_rows(B, rows, M, N, &sp, &ch);
-  return sp > 1 ? (size_t)sp * B * M * N * sizeof(float) : 0;
+  size_t r = 0;
+  for (int bn : {128, 256}) {            // either tile width conv_wgrad_bn picks
+    int sp; int64_t ch;
+    wgrad_split_rows(B, rows, M, N, &sp, &ch, bn);
+    r = std::max(r, sp > 1 ? (size_t)sp * B * M * N * sizeof(float) : (size_t)0);
+  }
+  return r;
 }
 
 hfta_status conv_wgrad_tc(ConvTcP& cp, int64_t rows, float* dW, int64_t dW_bstride, int64_t ld, int accumulate,
                           char* lws, size_t lwsb, cudaStream_t s) {
   int sp; int64_t ch;
-  wgrad_split_rows(cp.B, rows, cp.M, cp.N, &sp, &ch);
+  wgrad_split_rows(cp.B, rows, cp.M, cp.N, &sp, &ch, conv_wgrad_bn(cp));
   cp.K = rows; cp.splits = sp; cp.k_chunk = ch;
   cp.C = dW; cp.c_bs = dW_bstride; cp.c_ld = ld; cp.accumulate = accumulate;
   cp.part = nullptr;

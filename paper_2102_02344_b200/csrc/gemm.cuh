@@ -80,6 +80,8 @@ bool conv_tc_supported(const ConvTcP& p);
 // (w_mn: Conv2d W [Ca][16][8], else ConvT2d Wt [16][8][Ca]); zeros where phase (ph,pw) does not use tap (dy,dx)
 hfta_status conv_subpixel_weights(int B, int ca, int w_mn, const void* W, int64_t w_bs, void* Wp, cudaStream_t s);
 hfta_status conv_tc(const ConvTcP& p, cudaStream_t s);
+// tile width along N of the wgrad modes (3, 4) conv_tc launches for p (split-K policy input)
+int conv_wgrad_bn(const ConvTcP& p);
 
 // Dispatch: skinny -> tcgen05 -> SIMT (EPI features: skinny / tcgen05 only).
 hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void* ws = nullptr, size_t wsb = 0);

@@ -142,7 +142,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   // atom of ones after its BN columns, and MMAs of column-sum tiles use
   // N = BN + 16: accumulator columns BN..BN+15 then hold sum_k A(m, k) (the
   // fused dbias / Gram column sums) at no extra MMA instruction.
-  constexpr bool CSUM = A_MN && B_MN && OUT_F32;
+  constexpr bool CSUM = A_MN && B_MN && OUT_F32 && CONV == 0;
   constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB
   constexpr uint32_t B_LOAD = BN * BK * 2;    // bytes of B loaded per stage
   constexpr uint32_t B_BYTES = B_LOAD + (CSUM ? 8192 : 0);
@@ -870,7 +870,7 @@ template <int CONV, bool A_MN, bool B_MN, int BN, bool OUT_F32, bool NARROW = fa
 hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   constexpr int STAGES = (BN == 256) ? 3 : (BN == 32 ? 7 : 4);
   constexpr size_t SMEM = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + (OUT_F32 ? 0 : NEPI_ALL * 4096) +
-                          NEPI_ALL * BN * 4 + ((A_MN && B_MN && OUT_F32) ? (size_t)STAGES * 8192 : 0);
+                          NEPI_ALL * BN * 4;
   static_assert(SMEM <= 232448, "shared memory budget");
   if (hfta_status st = get_encode()) return st;
   CUtensorMap ta, tb, tc_;
@@ -999,9 +999,19 @@ hfta_status conv_tc(const ConvTcP& p, cudaStream_t s) {
       if (p.N <= 128) return launch_conv<2, false, false, 128, false>(p, s);
       return launch_conv<2, false, false, 256, false>(p, s);
     case 5: return launch_conv<5, false, false, 32, false>(p, s);
-    case 3: return launch_conv<3, true, true, 128, true>(p, s);
-    default: return launch_conv<4, true, true, 128, true>(p, s);
+    // wgrads: both operands stream per k-block, so 256-wide tiles (48 KB of
+    // operands per 512 MMA cycles instead of 32 KB per 256) keep the tensor
+    // pipe fed from L2
+    case 3: return conv_wgrad_bn(p) == 256 ? launch_conv<3, true, true, 256, true>(p, s)
+                                           : launch_conv<3, true, true, 128, true>(p, s);
+    default: return conv_wgrad_bn(p) == 256 ? launch_conv<4, true, true, 256, true>(p, s)
+                                            : launch_conv<4, true, true, 128, true>(p, s);
   }
+}
+
+int conv_wgrad_bn(const ConvTcP& p) {
+  if (p.img_c == 8) return 128;                    // narrow: one 128-wide tile
+  return (p.mode == 3 ? p.N % 256 == 0 : p.N >= 256) ? 256 : 128;
 }
 
 // ---- mode 5 operand: the phase-merged weights ----

@@ -25,13 +25,13 @@ hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void
 namespace {
 // split-K policy of the weight-gradient contraction (reduction over M rows).
 struct Split { int splits; int64_t chunk; };
-Split wgrad_split(int B, int64_t M, int64_t N, int64_t K) {
+Split wgrad_split(int B, int64_t M, int64_t N, int64_t K, int bn = 128) {
   // Split the reduction over M so the persistent grid's last wave is full:
   // the busiest CTA streams ceil(tiles / SMs) tiles, each (M/s) rows of
   // (N + K) bf16 plus an N x K fp32 partial written and re-read by the
   // reduction; pick the split count s minimising that.
   const int64_t sms = std::max(num_sms(), 1);
-  const int64_t tiles = cdiv(N, 128) * cdiv(K, 128) * (int64_t)B;
+  const int64_t tiles = cdiv(N, 128) * cdiv(K, bn) * (int64_t)B;   // bn: the tile width along K
   const int64_t maxs = std::max<int64_t>(1, M / 1024);
   int64_t best_s = 1;
   double best = -1.0;
@@ -48,8 +48,8 @@ Split wgrad_split(int B, int64_t M, int64_t N, int64_t K) {
 }  // namespace
 
 // the same policy for callers outside this file (implicit-GEMM conv wgrad)
-void wgrad_split_rows(int B, int64_t rows, int64_t N, int64_t K, int* splits, int64_t* chunk) {
-  Split sp = wgrad_split(B, rows, N, K);
+void wgrad_split_rows(int B, int64_t rows, int64_t N, int64_t K, int* splits, int64_t* chunk, int bn) {
+  Split sp = wgrad_split(B, rows, N, K, bn);
   *splits = sp.splits;
   *chunk = sp.chunk;
 }
