@@ -284,3 +284,56 @@ def convT2d_bwd(dy, x, W, s, p, need_dx=True):
             if need_dx:
                 dx += np.tensordot(g, W[:, :, ky, kx], axes=([1], [1])).transpose(0, 3, 1, 2)
     return dx, dW
+
+
+# ------------------------------------------------------ pooling (NEXT-4) ----
+# App. B rows MaxPool2d and AdaptiveAvgPool2d: the fused
+# operator pools each of the B x C channels independently, i.e. the serial
+# operator per model.  PyTorch semantics: padding takes no part in the max
+# (padded positions are -inf), the first window tap wins exact ties (reading
+# R32), the output size is floor((H + 2p - k) / s) + 1.
+
+def maxpool2d_windows(x, k, s, p):
+    """x [N, C, H, W] -> windows [N, Ho, Wo, k*k, C], tap t = ky*k + kx, -inf outside."""
+    N, C, H, W = x.shape
+    Ho, Wo = _out(H, k, s, p), _out(W, k, s, p)
+    xp = np.full((N, C, H + 2 * p, W + 2 * p), -np.inf)
+    xp[:, :, p:p + H, p:p + W] = x
+    win = np.empty((N, Ho, Wo, k * k, C))
+    for ky in range(k):
+        for kx in range(k):
+            win[:, :, :, ky * k + kx, :] = xp[:, :, ky:ky + s * (Ho - 1) + 1:s,
+                                              kx:kx + s * (Wo - 1) + 1:s].transpose(0, 2, 3, 1)
+    return win
+
+
+def maxpool2d_fwd(x, k, s, p, idx=None):
+    """y [N, C, Ho, Wo] = max over each window; idx [N, Ho, Wo, C] the tap
+    (first on ties) -- or the given idx (a decision taken elsewhere)."""
+    win = maxpool2d_windows(x, k, s, p)
+    if idx is None:
+        idx = np.argmax(win, axis=3)
+    y = np.take_along_axis(win, idx[:, :, :, None, :], axis=3)[:, :, :, 0, :]
+    return y.transpose(0, 3, 1, 2), idx
+
+
+def maxpool2d_bwd(dy, idx, x_shape, k, s, p):
+    """dx: each output gradient routed to the input pixel of its window's argmax."""
+    N, C, H, W = x_shape
+    _, _, Ho, Wo = dy.shape
+    dxp = np.zeros((N, C, H + 2 * p, W + 2 * p))
+    n, oy, ox, c = np.meshgrid(np.arange(N), np.arange(Ho), np.arange(Wo), np.arange(C), indexing="ij")
+    iy = oy * s + idx // k
+    ix = ox * s + idx % k
+    np.add.at(dxp, (n, c, iy, ix), dy.transpose(0, 2, 3, 1))
+    return dxp[:, :, p:p + H, p:p + W]
+
+
+def avgpool_global_fwd(x):
+    """AdaptiveAvgPool2d((1, 1)): y [N, C] = mean over H, W."""
+    return x.mean(axis=(2, 3))
+
+
+def avgpool_global_bwd(dy, x_shape):
+    N, C, H, W = x_shape
+    return np.broadcast_to(dy[:, :, None, None] / (H * W), x_shape).copy()

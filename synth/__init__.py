@@ -93,6 +93,13 @@ def noise(seed, b, step, N=128, nz=100):
     return f32(rng(seed, 4, b, step).standard_normal((N, nz)))
 
 
+def cifar(seed=0, N=128, k=10, H=32, W=32):
+    """CIFAR-10-shaped batch (ResNet-18 family, NEXT-4): images NCHW ~ N(0,1)
+    (the normalised-pixel range) and labels uniform in [0, k)."""
+    g = rng(seed, 9)
+    return f32(g.standard_normal((N, 3, H, W))), g.integers(0, k, size=N).astype(np.int64)
+
+
 def mlp_cfg1_batch(seed=0, N=2, L=128, C_out=64):
     """BJ cfg1: shared points [N*L, 3] ~ U(-1,1) and target [N*L, C_out] ~ N(0,1)."""
     g = rng(seed, 5)
@@ -127,6 +134,15 @@ def hparams_dcgan(seed, B):
                 beta2=f32(np.full(B, 0.999)),
                 eps=f32(np.full(B, 1e-8)),
                 wd=f32(np.zeros(B)))
+
+
+def hparams_resnet(seed, B):
+    """Per-model Adadelta vectors (ranges: reading R33)."""
+    g = rng(seed, 10)
+    return dict(lr=f32(10.0 ** g.uniform(-1.0, 0.5, size=B)),
+                rho=f32(g.uniform(0.8, 0.95, size=B)),
+                eps=f32(np.full(B, 1e-6)),
+                wd=f32(g.uniform(0.0, 1e-3, size=B)))
 
 
 # ------------------------------------------------------------ parameters ----
@@ -205,6 +221,21 @@ def param_specs(arch, k=None, widths=None, ft=False):
             if 1 <= i <= 3:
                 s += _bn("bn%d" % (i + 1), ch[i + 1], gan=True)
         return s
+    if arch == "resnet18":
+        k = 10 if k is None else k
+        w = (64, 128, 256, 512) if widths is None else widths
+        s = [("conv1.W", (w[0], 3, 7, 7), "u:%d" % (3 * 49))] + _bn("bn1", w[0])
+        cin = w[0]
+        for si, c in enumerate(w):
+            for b in range(2):
+                stride = 2 if (si > 0 and b == 0) else 1
+                n = "l%d.%d" % (si + 1, b)
+                s += [(n + ".conv1.W", (c, cin, 3, 3), "u:%d" % (9 * cin))] + _bn(n + ".bn1", c)
+                s += [(n + ".conv2.W", (c, c, 3, 3), "u:%d" % (9 * c))] + _bn(n + ".bn2", c)
+                if stride != 1 or cin != c:
+                    s += [(n + ".down.W", (c, cin, 1, 1), "u:%d" % cin)] + _bn(n + ".dbn", c)
+                cin = c
+        return s + _lin("fc", w[-1], k)
     raise ValueError("unknown arch %r" % (arch,))
 
 
