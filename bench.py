@@ -140,12 +140,13 @@ def step_roofline(workload, dtype, value, pk, args):
     the HBM ceiling of the deepest fusion schedule (S3, App. B5: 17.4 MB per
     model-sample for PointNet bf16) is the bytes floor.  frac = achieved /
     min(ceilings): the step's time vs the larger of its two lower bounds."""
-    gf = {"pointnet_cls": 4.1908, "pointnet_seg": 15.0962, "dcgan": 2.2746}[workload]
+    gf = {"pointnet_cls": 4.1908, "pointnet_seg": 15.0962, "dcgan": 2.2746,
+          "resnet18": getattr(args, "resnet_gflop", None)}[workload]
     if workload == "pointnet_cls" and (args.N, args.L) != (32, 2500):
         return None
     peak_tf = pk["bf16_tflops_sustained"] if dtype == "bf16" else pk["bf16_tflops_sustained"] / 6.0
     comp = peak_tf * 1e12 / (gf * 1e9)
-    hbm_mb = {"pointnet_cls": 17.4, "pointnet_seg": None, "dcgan": None}[workload]
+    hbm_mb = {"pointnet_cls": 17.4}.get(workload)
     hbm = pk["hbm_gbs"] * 1e9 / (hbm_mb * 1e6 * (1 if dtype == "bf16" else 2)) if hbm_mb else None
     ceiling = min(c for c in (comp, hbm) if c)
     return {"gflop_per_model_sample": gf, "compute_ceiling": comp, "hbm_ceiling_S3": hbm,
@@ -201,6 +202,35 @@ def build_net(args, rank, world, device):
         w.x_host, w.y_host = x, y
         w.desc = "%s (BJ configs[%d]), N=%d clouds x %d points, k=%d" % (arch, 1 if task == "cls" else 2, args.N,
                                                                        args.L, k)
+    elif args.workload == "resnet18":
+        from paper_2102_02344_b200.resnet import FusedResNet18
+        Nr = args.N_resnet
+        specs = synth.param_specs("resnet18")
+        if args.fast_init:
+            Ps = [synth.init_params("resnet18", 1000)] * B
+        else:
+            Ps = [synth.init_params("resnet18", 1000 + base + b) for b in range(B)]
+        hp = shard.slice_hparams(synth.hparams_resnet(3, B * world), base, base + B)
+        net = FusedResNet18(B, specs, Ps, hp, N=Nr, dtype=args.dtype, device=device)
+        x, y = synth.cifar(0, N=Nr)
+        xh = torch.from_numpy(np.ascontiguousarray(x.transpose(0, 2, 3, 1))).pin_memory()
+        yh = torch.from_numpy(y.astype(np.int32)).pin_memory()
+        xd, yd = torch.empty_like(xh, device=device), torch.empty_like(yh, device=device)
+        xd.copy_(xh)
+        yd.copy_(yh)
+        net.set_inputs(xd, yd)
+        lh = torch.empty(B, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            yd.copy_(yh, non_blocking=True)
+            net.set_inputs(xd, yd)
+            lh.copy_(net.step(), non_blocking=True)
+        w.net, w.step, w.e2e_step, w.loss = net, net.step, e2e_step, lambda: net.loss
+        w.samples = Nr
+        w.h2d, w.d2h = xh.numel() * 4 + yh.numel() * 4, B * 4
+        args.resnet_gflop = net.flops_per_sample() / 1e9
+        w.desc = "resnet18 (NEXT-4; torchvision BasicBlock, 10 classes), N=%d CIFAR-shaped 32x32 images, Adadelta" % Nr
     else:
         from paper_2102_02344_b200.dcgan import FusedDCGAN
         Nd = args.N_dcgan
@@ -311,7 +341,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- roofline probe: CUDA events around the probed kernel in eager steps ----
     probe_name = args.probe or {"pointnet_cls": "feat.c3:fwd", "pointnet_seg": "head.c2:fwd",
-                                "dcgan": "D.c3:fwd"}[args.workload]
+                                "dcgan": "D.c3:fwd", "resnet18": "l1.1.conv1:fwd"}[args.workload]
     probe_ms = []
     if probe_name:
         net.probe_arm(probe_name)
@@ -413,6 +443,7 @@ def main():
     ap.add_argument("--k", type=int, default=40)
     ap.add_argument("--k-seg", type=int, default=50)
     ap.add_argument("--N-dcgan", type=int, default=128)
+    ap.add_argument("--N-resnet", type=int, default=128, help="ResNet-18 batch (P:L937: 128)")
     ap.add_argument("--probe", default=None, help="layer:fwd|bwd timed for the roofline (default: the workload's "
                     "dominant contraction)")
     ap.add_argument("--ref-samples", type=int, default=8)
@@ -420,11 +451,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-serial", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of the captured step graph")
-    ap.add_argument("--workload", default="pointnet_cls", choices=["pointnet_cls", "pointnet_seg", "dcgan"])
+    ap.add_argument("--workload", default="pointnet_cls", choices=["pointnet_cls", "pointnet_seg", "dcgan", "resnet18"])
     args = ap.parse_args()
     if args.B is None:      # peak of the measured B sweep (throughput flat within 1% beyond it)
         args.B = {("pointnet_cls", "bf16"): 256, ("pointnet_seg", "bf16"): 96, ("dcgan", "bf16"): 96,
-                  ("pointnet_cls", "f32"): 64, ("pointnet_seg", "f32"): 64, ("dcgan", "f32"): 64}[(args.workload,
+                  ("pointnet_cls", "f32"): 64, ("pointnet_seg", "f32"): 64, ("dcgan", "f32"): 64,
+                  ("resnet18", "bf16"): 64, ("resnet18", "f32"): 32}[(args.workload,
                                                                                                  args.dtype)]
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -488,6 +488,36 @@ hfta_status hfta_feature_transform_reg(int B, int64_t N, int64_t K, const float*
                                        int64_t df_bstride, float* loss, float* mean_loss, void* ws,
                                        size_t ws_bytes, hfta_stream stream);
 
+/* ------------------------------------------ pooling (ResNet-18, NEXT-4) -- */
+/*
+ * Fused MaxPool2d (App. B row MaxPool2d): every (model b,
+ * channel c) pooled on its own.  X [B][N][H][W][C] dense NHWC per model
+ * (X.ld = C, X.bstride elements per model, 0 = shared); Y [B][N][Ho][Wo][C]
+ * with Ho = (H + 2 pad - k) / stride + 1; argmax uint8 [B][N][Ho][Wo][C]
+ * (model stride am_bstride) = the winning tap ky * k + kx.  Padded positions
+ * take no part (PyTorch: -inf padding, requires 2 pad <= k); the first tap
+ * in (ky, kx) order wins exact ties (reading R32).  k <= 15.
+ * _bwd: dX[n][iy][ix][c] = sum of dY over the windows whose argmax is
+ * (iy, ix) -- a gather in ascending (oy, ox) order (deterministic); dX is
+ * overwritten.  Errors: HFTA_ERR_SHAPE (bad geometry, ld != C),
+ * HFTA_ERR_INVALID_VALUE (null pointers).
+ */
+hfta_status hfta_maxpool2d_fwd(int B, int N, int H, int W, int C, int k, int stride, int pad, hfta_dtype dt,
+                               hfta_in X, hfta_out Y, uint8_t* argmax, int64_t am_bstride, hfta_stream stream);
+hfta_status hfta_maxpool2d_bwd(int B, int N, int H, int W, int C, int k, int stride, int pad, hfta_dtype dt,
+                               hfta_in dY, const uint8_t* argmax, int64_t am_bstride, hfta_out dX,
+                               hfta_stream stream);
+/*
+ * Fused AdaptiveAvgPool2d((1, 1)) (App. B row AdaptiveAvgPool2d,
+ * P:L1289-1290): Y[b][n][c] = (1/HW) sum_q X[b][n][q][c] over the HW pixels
+ * of image n (fp32 sum in pixel order); _bwd: dX[b][n][q][c] = dY[b][n][c] / HW.
+ * Layouts dense ([N][HW][C] and [N][C], ld = C).
+ */
+hfta_status hfta_avgpool2d_fwd(int B, int64_t N, int64_t HW, int64_t C, hfta_dtype dt, hfta_in X, hfta_out Y,
+                               hfta_stream stream);
+hfta_status hfta_avgpool2d_bwd(int B, int64_t N, int64_t HW, int64_t C, hfta_dtype dt, hfta_in dY, hfta_out dX,
+                               hfta_stream stream);
+
 /* ------------------------------------------------------------- utility -- */
 /* Y = X1 + X2 elementwise over [B][rows][cols] (dtype dt): sums the two
  * gradient paths into a shared activation (PointNet-seg's point feature). */

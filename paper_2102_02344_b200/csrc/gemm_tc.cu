@@ -1073,7 +1073,7 @@ bool gemm_tc_supported(const GemmP& p, hfta_dtype dt_in, bool out_f32) {
   // bounds, which TMA zero-fills (the A side only feeds rows the epilogue
   // clips; the B side stays at multiples of 16).
 
-  if (!p.b_kmajor && (p.N % 16)) return false;
+  if (!p.b_kmajor && (p.N % 8)) return false;     // 16-B rows; the box tail past N is zero-filled
   return true;
 }
 

@@ -104,6 +104,10 @@ _SIGS = {
     "hfta_fused_sgd": (i32, [i32, i64, vp, vp, vp, i64, vp, vp, vp, vp, i32, vp, vp, i64, vp]),
     "hfta_fused_adadelta": (i32, [i32, i64, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, i64, vp]),
     "hfta_steplr": (i32, [i32, vp, vp, vp, i64, vp, vp]),
+    "hfta_maxpool2d_fwd": (i32, [i32, i32, i32, i32, i32, i32, i32, i32, i32, hfta_in, hfta_out, vp, i64, vp]),
+    "hfta_maxpool2d_bwd": (i32, [i32, i32, i32, i32, i32, i32, i32, i32, i32, hfta_in, vp, i64, hfta_out, vp]),
+    "hfta_avgpool2d_fwd": (i32, [i32, i64, i64, i64, i32, hfta_in, hfta_out, vp]),
+    "hfta_avgpool2d_bwd": (i32, [i32, i64, i64, i64, i32, hfta_in, hfta_out, vp]),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -110,7 +110,8 @@ def witness_margins(own, wit, floor=None):
         w = wit.sites[site]
         key = "z" if v["kind"] == "relu" else "x"
         sc = v["scale"] if v["kind"] == "relu" else v["scale"][:, None, :]
-        err = float(np.max(np.abs(w[key] - v[key]) / sc))
+        fin = np.isfinite(w[key]) & np.isfinite(v[key])      # -inf: padded max-pool window taps
+        err = float(np.max(np.abs(np.where(fin, w[key] - v[key], 0.0)) / sc))
         m[site] = max(floor, WITNESS_SAFETY * err)
     return m
 
