@@ -179,6 +179,11 @@ hfta_status make_shape(const hfta_conv_desc* d, Shape* sh) {
 }
 
 bool k4s2p1(const hfta_conv_desc* d) { return d->kh == 4 && d->kw == 4 && d->stride == 2 && d->pad == 1; }
+// Conv2d (not transposed) the gather modes take: square kernel, stride 1 or 2
+bool gather_conv(const hfta_conv_desc* d) {
+  return !d->transposed && d->kh == d->kw && (d->stride == 1 || d->stride == 2) && d->kh <= 15;
+}
+bool tc_geometry(const hfta_conv_desc* d) { return k4s2p1(d) || gather_conv(d); }
 
 // 1x1 input, stride 1, pad 0 (ConvT) / window = whole input, pad 0 (Conv): a dense GEMM in NHWC
 bool dense_convT(const hfta_conv_desc* d) { return d->transposed && d->H == 1 && d->W == 1 && d->stride == 1 && d->pad == 0; }
@@ -200,8 +205,10 @@ ConvTcP fwd_cp(int B, const hfta_conv_desc* d, const Shape& sh, const void* X, i
   ConvTcP cp = img_op(B, X, x_bs, d->N, d->H, d->W, d->C_in);
   cp.opd = W; cp.opd_bs = w_bs;
   const int64_t ye = img_elems(d->N, sh.Ho, sh.Wo, d->C_out);
-  if (!sh.transposed) {          // stride-2 gather of X
-    cp.mode = 1; cp.M = (int64_t)d->N * sh.Ho * sh.Wo; cp.N = d->C_out; cp.K = 16 * (int64_t)d->C_in;
+  if (!sh.transposed) {          // strided gather of X
+    cp.mode = 1; cp.M = (int64_t)d->N * sh.Ho * sh.Wo; cp.N = d->C_out;
+    cp.K = (int64_t)d->kh * d->kw * d->C_in;
+    cp.ks = d->kh; cp.cs = d->stride; cp.cpad = d->pad;
     cp.grid_w = (int)sh.Wo; cp.grid_h = (int)sh.Ho; cp.opd_ld = w_ld;
     cp.C = Y; cp.c_bs = y_bs; cp.c_ld = d->C_out;
   } else {                       // 4 sub-pixel phases of X against the ConvT taps
@@ -214,9 +221,10 @@ ConvTcP fwd_cp(int B, const hfta_conv_desc* d, const Shape& sh, const void* X, i
 ConvTcP wgrad_cp(int B, const hfta_conv_desc* d, const Shape& sh, const void* dY, int64_t dy_bs, const void* X,
                  int64_t x_bs) {
   ConvTcP cp;
-  if (!sh.transposed) {          // dW[co][(kh,kw,ci)] = sum_(n,oy,ox) dY (x) stride-2 gather of X
+  if (!sh.transposed) {          // dW[co][(kh,kw,ci)] = sum_(n,oy,ox) dY (x) strided gather of X
     cp = img_op(B, X, x_bs, d->N, d->H, d->W, d->C_in);
-    cp.mode = 3; cp.M = d->C_out; cp.N = 16 * (int64_t)d->C_in;
+    cp.mode = 3; cp.M = d->C_out; cp.N = (int64_t)d->kh * d->kw * d->C_in;
+    cp.ks = d->kh; cp.cs = d->stride; cp.cpad = d->pad;
     cp.grid_w = (int)sh.Wo; cp.grid_h = (int)sh.Ho;
     cp.opd = dY; cp.opd_bs = dy_bs; cp.opd_ld = d->C_out;
     cp.K = (int64_t)d->N * sh.Ho * sh.Wo;
@@ -234,7 +242,17 @@ ConvTcP dgrad_cp(int B, const hfta_conv_desc* d, const Shape& sh, const void* dY
   ConvTcP cp = img_op(B, dY, dy_bs, d->N, (int)sh.Ho, (int)sh.Wo, d->C_out);
   cp.opd = W; cp.opd_bs = w_bs;
   const int64_t xe = img_elems(d->N, d->H, d->W, d->C_in);
-  if (!sh.transposed) {          // 4 sub-pixel phases of dY against the (adjoint) Conv taps
+  if (!sh.transposed && d->stride == 1) {
+    // stride 1: dX = Conv2d(dY, W flipped and transposed) with pad k-1-p -- the
+    // gather mode over dY, B read from W [Co][taps][Ci] at the flipped tap
+    cp.mode = 1; cp.M = (int64_t)d->N * d->H * d->W; cp.N = d->C_in; cp.K = (int64_t)d->kh * d->kw * d->C_out;
+    cp.ks = d->kh; cp.cs = 1; cp.cpad = d->kh - 1 - d->pad;
+    cp.w_mn = 1; cp.wflip = 1; cp.w_cn = d->C_in; cp.w_ca = d->C_out;
+    cp.grid_w = d->W; cp.grid_h = d->H; cp.opd_ld = w_ld;
+    cp.C = dX; cp.c_bs = B > 1 ? dx_bs : xe; cp.c_ld = d->C_in;
+  } else if (!sh.transposed && !k4s2p1(d)) {
+    cp.mode = 0;                 // other strided Conv2d dgrads: the patch-matrix path
+  } else if (!sh.transposed) {   // 4 sub-pixel phases of dY against the (adjoint) Conv taps
     cp.mode = 2; cp.M = (int64_t)d->N * sh.Ho * sh.Wo; cp.N = d->C_in; cp.K = 4 * (int64_t)d->C_out;
     cp.grid_w = (int)sh.Wo; cp.grid_h = (int)sh.Ho; cp.w_mn = 1; cp.w_cn = d->C_in; cp.w_ca = d->C_out;
     cp.C = dX; cp.c_bs = B > 1 ? dx_bs : xe; cp.y_h = d->H; cp.y_w = d->W;
@@ -250,7 +268,7 @@ ConvTcP dgrad_cp(int B, const hfta_conv_desc* d, const Shape& sh, const void* dY
 // aligned, model-major operands (the runtime re-checks the real pointers).
 void plan(int B, const hfta_conv_desc* d, hfta_dtype dt, const Shape& sh, bool& f, bool& g, bool& w) {
   f = g = w = false;
-  if (dt != HFTA_BF16 || !k4s2p1(d)) return;
+  if (dt != HFTA_BF16 || !tc_geometry(d)) return;
   char* a = reinterpret_cast<char*>(256);       // any 16-B aligned address: only eligibility is evaluated
   const int64_t xe = img_elems(d->N, d->H, d->W, d->C_in), ye = img_elems(d->N, sh.Ho, sh.Wo, d->C_out);
   const int64_t we = (int64_t)d->kh * d->kw * d->C_in * d->C_out;
@@ -374,7 +392,7 @@ hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
   const int64_t xe = img_elems(d->N, d->H, d->W, d->C_in), ye = img_elems(d->N, sh.Ho, sh.Wo, d->C_out);
   HFTA_REQUIRE(act == HFTA_ACT_NONE || act == HFTA_ACT_LEAKY_RELU || act == HFTA_ACT_TANH || act == HFTA_ACT_RELU,
                HFTA_ERR_UNSUPPORTED, "conv_fwd: activation %d", (int)act);
-  if (dt == HFTA_BF16 && k4s2p1(d) && (X.bstride == 0 || X.bstride == xe) && (Y.bstride == ye || B == 1) &&
+  if (dt == HFTA_BF16 && tc_geometry(d) && (X.bstride == 0 || X.bstride == xe) && (Y.bstride == ye || B == 1) &&
       act != HFTA_ACT_RELU) {
     ConvTcP cp = fwd_cp(B, d, sh, X.ptr, X.bstride, W.ptr, W.bstride, W.ld, Y.ptr, Y.bstride);
     cp.act = act; cp.act_alpha = act_alpha;      // fused into the epilogue
@@ -456,7 +474,7 @@ hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
       return st;
     return post_launch(s, "hfta_fused_conv_bwd");
   }
-  const bool tc = dt == HFTA_BF16 && k4s2p1(d) && (X.bstride == 0 || X.bstride == xe) &&
+  const bool tc = dt == HFTA_BF16 && tc_geometry(d) && (X.bstride == 0 || X.bstride == xe) &&
                   (dY.bstride == ye || B == 1) && (!dX.ptr || dX.bstride == xe || B == 1);
   bool need_dW = dW != nullptr, need_dX = dX.ptr != nullptr;
   if (tc && need_dW) {

@@ -60,7 +60,21 @@ struct TcArgs {
   int cblk;                          // CONV 1, 2: 64-channel blocks per tap of the image operand
   int cg;                            // CONV 3: channels per tap of B (C_in); CONV 4: rows per tap of A (C_out)
   int y_c, y_h, y_w; int64_t y_bs;   // CONV 2: output image [B][n][y_h][y_w][y_c] the phases interleave into
+  // CONV 1, 3, 4 gather geometry: kernel ks x ks, stride cs, pad cp (DCGAN: 4, 2, 1); taps = ks * ks
+  int ks, cs, cp, taps;
+  int wflip;                         // CONV 1 with B MN-major: B is the 4-D weight view {Cn, taps, Ca} read at
+                                     // tap taps-1-t (the stride-1 Conv2d dgrad: flipped, transposed W)
 };
+
+// Image coordinate of kernel tap `tap` (row-major ky * ks + kx) for output grid position g
+// (gather modes): x = cs * g - cp + kx.  Taps past the kernel (a partial last k-block of an
+// 8-channel image) read tap 0: their weight rows are zero (TMA zero-fill past K).
+__device__ __forceinline__ void tap_xy(const TcArgs& p, int tap, int gx, int gy, int& x, int& y) {
+  if (tap >= p.taps) tap = 0;
+  const int ky = tap / p.ks, kx = tap - ky * p.ks;
+  x = p.cs * gx - p.cp + kx;
+  y = p.cs * gy - p.cp + ky;
+}
 
 // Row index r of a dense NHWC grid (gw x gh per image) -> (image, row, col), 32-bit.
 __device__ __forceinline__ void grid_pos(uint32_t r, const TcArgs& p, int& n, int& y, int& x) {
@@ -250,9 +264,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           if constexpr (CONV == 1 && NARROW) {            // 8 taps of an 8-channel image per k-block
 #pragma unroll
             for (int t8 = 0; t8 < 8; ++t8) {
-              const int tap = kb * 8 + t8;
-              tma_load_5d(sa + t8 * 2048, &tmA, &full[stage], 0, 2 * gx0 - 1 + (tap & 3), 2 * gy0 - 1 + (tap >> 2), gn0,
-                          ba);
+              int x, y;
+              tap_xy(p, kb * 8 + t8, gx0, gy0, x, y);
+              tma_load_5d(sa + t8 * 2048, &tmA, &full[stage], 0, x, y, gn0, ba);
             }
             if constexpr (B_MN) {
 #pragma unroll
@@ -260,12 +274,20 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             } else {
               tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
             }
-          } else if constexpr (CONV == 1) {               // stride-2 gather of the input image
+          } else if constexpr (CONV == 1) {               // strided gather of the input image
             const int tap = kb / p.cblk, cb = kb - tap * p.cblk;
-            tma_load_5d(sa, &tmA, &full[stage], cb * 64, 2 * gx0 - 1 + (tap & 3), 2 * gy0 - 1 + (tap >> 2), gn0, ba);
-            if constexpr (B_MN) {                         // ConvT dgrad: B(n = ci, k = (tap, co)) = Wt[tap][co][ci]
+            int x, y;
+            tap_xy(p, tap, gx0, gy0, x, y);
+            tma_load_5d(sa, &tmA, &full[stage], cb * 64, x, y, gn0, ba);
+            if constexpr (B_MN) {
+              if (p.wflip) {                              // Conv dgrad (stride 1): B(n = ci, k = (t, co)) = W[co][T-1-t][ci]
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
+                for (int j = 0; j < BN / 64; ++j)
+                  tma_load_4d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, p.taps - 1 - tap, cb * 64, bb);
+              } else {                                    // ConvT dgrad: B(n = ci, k = (tap, co)) = Wt[tap][co][ci]
+#pragma unroll
+                for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
+              }
             } else {
               tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
             }
@@ -291,31 +313,39 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             tma_load_3d(sa + 8192, &tmA, &full[stage], m0 + 64, k0, ba);
             int gn, gy, gx;
             grid_pos((uint32_t)k0, p, gn, gy, gx);
-            if constexpr (NARROW) {                       // 16 taps x 8 channels = the whole 128-column tile
+            if constexpr (NARROW) {                       // 16 taps x 8 channels = one 128-column tile
 #pragma unroll
-              for (int tap = 0; tap < 16; ++tap)
-                tma_load_5d(sb + tap * 1024, &tmB, &full[stage], 0, 2 * gx - 1 + (tap & 3), 2 * gy - 1 + (tap >> 2), gn, bb);
+              for (int t = 0; t < 16; ++t) {
+                int x, y;
+                tap_xy(p, n0 / 8 + t, gx, gy, x, y);
+                tma_load_5d(sb + t * 1024, &tmB, &full[stage], 0, x, y, gn, bb);
+              }
             } else {
 #pragma unroll
               for (int j = 0; j < BN / 64; ++j) {
                 const int ncol = n0 + 64 * j, tap = ncol / p.cg, ci0 = ncol - tap * p.cg;
-                tma_load_5d(sb + j * 8192, &tmB, &full[stage], ci0, 2 * gx - 1 + (tap & 3), 2 * gy - 1 + (tap >> 2), gn,
-                            bb);
+                int x, y;
+                tap_xy(p, tap, gx, gy, x, y);
+                tma_load_5d(sb + j * 8192, &tmB, &full[stage], ci0, x, y, gn, bb);
               }
             }
           } else if constexpr (CONV == 4) {               // A = stride-2 gather of dY per (tap, co) atom, X plain
             int gn, gy, gx;
             grid_pos((uint32_t)k0, p, gn, gy, gx);
-            if constexpr (NARROW) {                       // 16 taps x 8 channels = the whole 128-row tile
+            if constexpr (NARROW) {                       // 16 taps x 8 channels = one 128-row tile
 #pragma unroll
-              for (int tap = 0; tap < 16; ++tap)
-                tma_load_5d(sa + tap * 1024, &tmA, &full[stage], 0, 2 * gx - 1 + (tap & 3), 2 * gy - 1 + (tap >> 2), gn, ba);
+              for (int t = 0; t < 16; ++t) {
+                int x, y;
+                tap_xy(p, m0 / 8 + t, gx, gy, x, y);
+                tma_load_5d(sa + t * 1024, &tmA, &full[stage], 0, x, y, gn, ba);
+              }
             } else {
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
                 const int mm = m0 + 64 * j, tap = mm / p.cg, co0 = mm - tap * p.cg;
-                tma_load_5d(sa + j * 8192, &tmA, &full[stage], co0, 2 * gx - 1 + (tap & 3), 2 * gy - 1 + (tap >> 2), gn,
-                            ba);
+                int x, y;
+                tap_xy(p, tap, gx, gy, x, y);
+                tma_load_5d(sa + j * 8192, &tmA, &full[stage], co0, x, y, gn, ba);
               }
             }
 #pragma unroll
@@ -877,10 +907,18 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   const int nbi = cp.img_bs == 0 ? 1 : cp.B;
   const int nbo = cp.opd_bs == 0 ? 1 : cp.B;
   hfta_status st = HFTA_OK;
+  const int ks = cp.ks > 0 ? cp.ks : 4, cs = cp.ks > 0 ? cp.cs : 2, cpd = cp.ks > 0 ? cp.cpad : 1;
   if (CONV == 1) {
-    st = img_map(&ta, cp, nbi, BM, 2);
-    if (!st) st = B_MN ? make_map(&tb, cp.opd, cp.N, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, BK)
-                       : make_map(&tb, cp.opd, cp.K, cp.N, cp.opd_ld, cp.opd_bs, nbo, BK, BN);
+    st = img_map(&ta, cp, nbi, BM, cs);
+    if (!st && B_MN && cp.wflip) {   // W [Ca][taps][Cn] as {Cn, taps, Ca, B}: one tap's 64 x 64 MN-major atom
+      const int64_t cn = cp.w_cn, ca = cp.w_ca, T = (int64_t)ks * ks, wbs = nbo > 1 ? cp.opd_bs : T * cn * ca;
+      const int64_t dims[4] = {cn, T, ca, nbo}, str[4] = {1, cn, T * cn, wbs};
+      const uint32_t box[4] = {64, 1, 64, 1}, es[4] = {1, 1, 1, 1};
+      st = make_map_nd(&tb, cp.opd, 4, dims, str, box, es);
+    } else if (!st) {
+      st = B_MN ? make_map(&tb, cp.opd, cp.N, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, BK)
+                : make_map(&tb, cp.opd, cp.K, cp.N, cp.opd_ld, cp.opd_bs, nbo, BK, BN);
+    }
   } else if (CONV == 2) {
     st = img_map(&ta, cp, nbi, BM, 1);
     if (!st) {
@@ -900,9 +938,9 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
     if (!st) st = make_map(&tb, cp.opd, cp.K, cp.N, cp.opd_ld, cp.opd_bs, nbo, BK, BN);
   } else if (CONV == 3) {
     st = make_map(&ta, cp.opd, cp.M, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, BK);
-    if (!st) st = img_map(&tb, cp, nbi, BK, 2);
+    if (!st) st = img_map(&tb, cp, nbi, BK, cs);
   } else {
-    st = img_map(&ta, cp, nbi, BK, 2);
+    st = img_map(&ta, cp, nbi, BK, cs);
     if (!st) st = make_map(&tb, cp.opd, cp.N, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, BK);
   }
   if (st) return st;
@@ -933,6 +971,7 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   a.cg = cp.img_c;   // 3: C_in per tap of B; 4: C_out (the gathered dY's channels) per tap of A
   a.y_c = CONV == 5 ? 8 : (int)cp.N; a.y_h = cp.y_h; a.y_w = cp.y_w; a.y_bs = cp.c_bs;
   a.act = (CONV == 1 || CONV == 2 || CONV == 5) ? cp.act : HFTA_ACT_NONE; a.act_alpha = cp.act_alpha;
+  a.ks = ks; a.cs = cs; a.cp = cpd; a.taps = ks * ks; a.wflip = cp.wflip;
   auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, false, 0, CONV, NARROW>;
   ensure_smem(kern, SMEM);
   const int64_t total = (int64_t)a.tiles_m * a.tiles_n * a.splits * a.B;
@@ -954,13 +993,17 @@ bool conv_tc_supported(const ConvTcP& p) {
   uint32_t bw, bh, bn;
   const int rows = (p.mode == 1 || p.mode == 2 || p.mode == 5) ? BM : BK;
   if (!grid_box(p.grid_w, p.grid_h, p.img_n, rows, bw, bh, bn)) return false;
+  const int64_t taps = p.ks > 0 ? (int64_t)p.ks * p.ks : 16;
+  if (p.ks > 0 && (p.cs < 1 || p.cs > 2 || p.cpad < 0 || p.ks > 15 || (p.mode != 1 && p.mode != 3))) return false;
+  if (p.wflip && (p.mode != 1 || !p.w_mn || p.cs != 1 || p.w_cn % 64 || p.w_ca % 64)) return false;
   switch (p.mode) {
-    case 1: return p.K == 16 * (int64_t)p.img_c && p.N % 16 == 0 && (p.c_ld * 2) % 16 == 0 && (p.c_bs * 2) % 16 == 0;
+    case 1: return p.K == taps * (int64_t)p.img_c && p.N % 16 == 0 && (p.c_ld * 2) % 16 == 0 &&
+                   (p.c_bs * 2) % 16 == 0;
     case 2: return p.K == 4 * (int64_t)p.img_c && p.N % 8 == 0 && p.N <= 256 && p.y_h == 2 * p.grid_h &&
                    p.y_w == 2 * p.grid_w && (p.c_bs * 2) % 16 == 0;
     case 5: return p.K == 9 * (int64_t)p.img_c && p.N == 32 && p.y_h == 2 * p.grid_h && p.y_w == 2 * p.grid_w &&
                    (p.c_bs * 2) % 16 == 0 && (p.opd_ld * 2) % 16 == 0;
-    case 3: return p.N == 16 * (int64_t)p.img_c && p.c_ld % 4 == 0;     // narrow: N = 128 (one tile)
+    case 3: return p.N == taps * (int64_t)p.img_c && p.c_ld % 4 == 0;   // narrow: 16 taps per 128-wide tile
     case 4: return p.M == 16 * (int64_t)p.img_c && p.N % 16 == 0 && p.c_ld % 4 == 0;   // narrow: M = 128
     default: return false;
   }

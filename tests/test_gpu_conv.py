@@ -152,3 +152,26 @@ def test_conv_fused_activation(dtype):
     bf16, a separate pass in fp32), N = 32, B = 2."""
     check(LAYERS[0], 2, 32, dtype, shared=False, act=H.ACT_LEAKY_RELU, alpha=0.2)
     check(LAYERS[9], 2, 32, dtype, shared=False, act=H.ACT_TANH, alpha=0.0)
+
+
+# ResNet-18 family (NEXT-4) layers at the bench's batch (N = 128 images of
+# 32 x 32): the general gather modes (kernel 7 / 3 / 1, stride 1 / 2, pad 3 /
+# 1 / 0), the flipped-weight stride-1 dgrad, the patch-matrix dgrads of the
+# strided 3x3 / 1x1 layers, the 8-channel stem.
+RESNET = [("R.stem", 0, 32, 8, 64, 7, 2, 3),
+          ("R.l1", 0, 8, 64, 64, 3, 1, 1),
+          ("R.l2a", 0, 8, 64, 128, 3, 2, 1),
+          ("R.l2d", 0, 8, 64, 128, 1, 2, 0),
+          ("R.l3", 0, 2, 256, 256, 3, 1, 1),
+          ("R.l4", 0, 1, 512, 512, 3, 1, 1)]
+
+
+@pytest.mark.parametrize("layer", RESNET, ids=[l[0] for l in RESNET])
+@pytest.mark.parametrize("B", [1, 3])
+def test_resnet_conv_bf16(layer, B):
+    check(layer, B, 128, "bf16", shared=(B == 3 and layer[0] == "R.stem"))
+
+
+@pytest.mark.parametrize("layer", RESNET, ids=[l[0] for l in RESNET])
+def test_resnet_conv_f32(layer):
+    check(layer, 2, 8, "f32", shared=False)
