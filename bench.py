@@ -456,7 +456,7 @@ def main():
     if args.B is None:      # peak of the measured B sweep (throughput flat within 1% beyond it)
         args.B = {("pointnet_cls", "bf16"): 256, ("pointnet_seg", "bf16"): 96, ("dcgan", "bf16"): 96,
                   ("pointnet_cls", "f32"): 64, ("pointnet_seg", "f32"): 64, ("dcgan", "f32"): 64,
-                  ("resnet18", "bf16"): 64, ("resnet18", "f32"): 32}[(args.workload,
+                  ("resnet18", "bf16"): 256, ("resnet18", "f32"): 128}[(args.workload,
                                                                                                  args.dtype)]
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

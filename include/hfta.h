@@ -160,6 +160,18 @@ hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* desc, hfta_dtype dt
 hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* desc, hfta_dtype dt, hfta_in dY, hfta_in X,
                                 hfta_in W, hfta_out dX, float* dW, int64_t dW_bstride, int accumulate,
                                 void* ws, size_t ws_bytes, hfta_stream stream);
+/*
+ * As hfta_fused_conv_bwd, and dX additionally multiplied by the backward of
+ * the activation that consumed X: dX *= act'(gate) with gate the activation's
+ * output (or input: same sign) in dX's layout, act in {NONE, ReLU (0),
+ * LeakyReLU (dX_alpha)} -- e.g. D c2's dgrad through D c1's LeakyReLU(0.2).
+ * Fused into the sub-pixel dgrad epilogue (bf16 k4 s2 p1, dense gate with
+ * the dX model stride); other paths apply it as one pass after the dgrad.
+ */
+hfta_status hfta_fused_conv_bwd_gated(int B, const hfta_conv_desc* desc, hfta_dtype dt, hfta_in dY, hfta_in X,
+                                      hfta_in W, hfta_out dX, float* dW, int64_t dW_bstride, int accumulate,
+                                      hfta_act dX_act, float dX_alpha, hfta_in dX_gate, void* ws, size_t ws_bytes,
+                                      hfta_stream stream);
 
 /* ------------------------------------------------------- fused BatchNorm -- */
 /*

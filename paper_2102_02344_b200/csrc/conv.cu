@@ -302,14 +302,18 @@ ConvTcP as_merged(const ConvTcP& cp, void* wp) {
   return m;
 }
 // run a mode-2 contraction, merged when eligible (wp: >= merged_w_bytes of workspace)
-hfta_status run_phases(const ConvTcP& cp, void* wp, size_t wpb, cudaStream_t s) {
+// *gated: whether the kernel applied cp.gate (mode 2 only; the merged mode does not)
+hfta_status run_phases(const ConvTcP& cp, void* wp, size_t wpb, cudaStream_t s, bool* gated = nullptr) {
+  if (gated) *gated = false;
   if (merged_phases(cp) && wp && wpb >= merged_w_bytes(cp.B, cp)) {
     ConvTcP m = as_merged(cp, wp);
+    m.gate = nullptr;
     if (conv_tc_supported(m)) {
       if (hfta_status st = conv_subpixel_weights(cp.B, cp.w_ca, cp.w_mn, cp.opd, cp.opd_bs, wp, s)) return st;
       return conv_tc(m, s);
     }
   }
+  if (gated) *gated = cp.mode == 2 && cp.gate != nullptr;
   return conv_tc(cp, s);
 }
 
@@ -448,7 +452,29 @@ hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
 hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* d, hfta_dtype dt, hfta_in dY, hfta_in X, hfta_in W,
                                 hfta_out dX, float* dW, int64_t dW_bstride, int accumulate, void* ws, size_t ws_bytes,
                                 hfta_stream stream) {
+  return hfta_fused_conv_bwd_gated(B, d, dt, dY, X, W, dX, dW, dW_bstride, accumulate, HFTA_ACT_NONE, 0.f,
+                                   hfta_in{nullptr, 0, 1}, ws, ws_bytes, stream);
+}
+
+hfta_status hfta_fused_conv_bwd_gated(int B, const hfta_conv_desc* d, hfta_dtype dt, hfta_in dY, hfta_in X,
+                                      hfta_in W, hfta_out dX, float* dW, int64_t dW_bstride, int accumulate,
+                                      hfta_act dX_act, float dX_alpha, hfta_in dX_gate, void* ws, size_t ws_bytes,
+                                      hfta_stream stream) {
   if (hfta_status st = check_init()) return st;
+  HFTA_REQUIRE(dX_act == HFTA_ACT_NONE || dX_act == HFTA_ACT_RELU || dX_act == HFTA_ACT_LEAKY_RELU,
+               HFTA_ERR_UNSUPPORTED, "conv_bwd: dX activation %d (ReLU / LeakyReLU gates only)", (int)dX_act);
+  HFTA_REQUIRE(dX_act == HFTA_ACT_NONE || (dX.ptr && dX_gate.ptr && dX_gate.ld == d->C_in), HFTA_ERR_INVALID_VALUE,
+               "conv_bwd: a dX activation needs dX and a dense gate tensor (ld == C_in)");
+  // the activation backward of the layer that consumed X, applied to dX: in the
+  // sub-pixel dgrad epilogue when that path runs, else as one pass at the end
+  bool gate_done = dX_act == HFTA_ACT_NONE;
+  const auto finish = [&]() -> hfta_status {
+    if (!gate_done)
+      if (hfta_status st = hfta_act_bwd(B, (int64_t)d->N * d->H * d->W, d->C_in, dt, dX_act, dX_alpha, dX_gate,
+                                        hfta_in{dX.ptr, dX.bstride, dX.ld}, dX, stream))
+        return st;
+    return post_launch((cudaStream_t)stream, "hfta_fused_conv_bwd");
+  };
   HFTA_CHECK_B(B);
   Shape sh;
   if (hfta_status st = make_shape(d, &sh)) return st;
@@ -472,7 +498,7 @@ hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
                                                dX.ptr ? hfta_out{dX.ptr, dX.bstride, Kg} : hfta_out{nullptr, 0, 1}, dW,
                                                dW_bstride, Kg, nullptr, 0, accumulate, lws, lwsb, stream))
       return st;
-    return post_launch(s, "hfta_fused_conv_bwd");
+    return finish();
   }
   const bool tc = dt == HFTA_BF16 && tc_geometry(d) && (X.bstride == 0 || X.bstride == xe) &&
                   (dY.bstride == ye || B == 1) && (!dX.ptr || dX.bstride == xe || B == 1);
@@ -486,12 +512,18 @@ hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
   }
   if (tc && need_dX) {
     ConvTcP cp = dgrad_cp(B, d, sh, dY.ptr, dY.bstride, W.ptr, W.bstride, W.ld, dX.ptr, dX.bstride);
+    if (!gate_done && dX_gate.bstride == xe) {
+      cp.gate = dX_gate.ptr; cp.gate_bs = dX_gate.bstride;
+      cp.gate_alpha = dX_act == HFTA_ACT_LEAKY_RELU ? dX_alpha : 0.f;
+    }
     if (conv_tc_supported(cp)) {
-      if (hfta_status st = run_phases(cp, lws, lwsb, s)) return st;     // after the wgrad's use of lws
+      bool gated = false;
+      if (hfta_status st = run_phases(cp, lws, lwsb, s, &gated)) return st;     // after the wgrad's use of lws
+      gate_done = gate_done || gated;
       need_dX = false;
     }
   }
-  if (!need_dW && !need_dX) return post_launch(s, "hfta_fused_conv_bwd");
+  if (!need_dW && !need_dX) return finish();
   HFTA_REQUIRE(colb > 0, HFTA_ERR_UNSUPPORTED, "conv_bwd: operands not eligible for the implicit-GEMM path "
                "(alignment / model strides) and no patch-matrix workspace for this configuration");
   if (!need_dW) dW = nullptr;
@@ -537,7 +569,7 @@ hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
       if (hfta_status st = run_gemm(p, dt, false, s)) return st;
     }
   }
-  return post_launch(s, "hfta_fused_conv_bwd");
+  return finish();
 }
 
 }  // extern "C"

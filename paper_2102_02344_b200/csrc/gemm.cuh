@@ -76,6 +76,7 @@ struct ConvTcP {
   int act; float act_alpha;        // 1, 2 (forward): activation applied in the epilogue (layers without BN)
   int ks, cs, cpad;         // modes 1, 3, 4: kernel size, stride, pad of the gather (0 = DCGAN's 4, 2, 1)
   int wflip;                // mode 1, w_mn: B = W [Ca][taps][Cn] read flipped (stride-1 Conv2d dgrad)
+  const void* gate; int64_t gate_bs; float gate_alpha;   // mode 2: output *= (gate > 0 ? 1 : gate_alpha)
 };
 bool conv_tc_supported(const ConvTcP& p);
 // mode 5 operand: Wp[b][(ph,pw,co)][(dy,dx,ca)] (32 x 9 Ca, K-major bf16) from mode-2 weights

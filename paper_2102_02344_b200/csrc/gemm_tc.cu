@@ -659,9 +659,24 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               const int64_t pix = ((int64_t)gn * p.y_h + 2 * gy + (split >> 1)) * p.y_w + 2 * gx + (split & 1);
               uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C) + (int64_t)b * p.y_bs +
                                                     pix * p.y_c + c0);
+              // gated dgrad (the next layer's activation backward, e.g. D c1's LeakyReLU):
+              // v *= act'(gate) with the gate tensor in the output's layout
+              const uint4* gsrc = p.mask ? reinterpret_cast<const uint4*>(p.mask + (int64_t)b * p.mask_bs +
+                                                                           pix * p.y_c + c0) : nullptr;
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 if (c0 + 8 * q >= p.N) break;
+                if (gsrc) {
+                  const uint4 g4 = __ldg(gsrc + q);
+                  const uint32_t gw[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    float g0, g1;
+                    unpack_bf2(gw[e], g0, g1);
+                    v[8 * q + 2 * e] *= g0 > 0.f ? 1.f : p.mask_alpha;
+                    v[8 * q + 2 * e + 1] *= g1 > 0.f ? 1.f : p.mask_alpha;
+                  }
+                }
                 uint4 w4;
                 __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
 #pragma unroll
@@ -972,6 +987,10 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   a.y_c = CONV == 5 ? 8 : (int)cp.N; a.y_h = cp.y_h; a.y_w = cp.y_w; a.y_bs = cp.c_bs;
   a.act = (CONV == 1 || CONV == 2 || CONV == 5) ? cp.act : HFTA_ACT_NONE; a.act_alpha = cp.act_alpha;
   a.ks = ks; a.cs = cs; a.cp = cpd; a.taps = ks * ks; a.wflip = cp.wflip;
+  if (CONV == 2 && cp.gate) {        // gated dgrad: ReLU' (alpha 0) / LeakyReLU' (alpha) of the gate tensor
+    a.mask = reinterpret_cast<const __nv_bfloat16*>(cp.gate); a.mask_bs = cp.gate_bs;
+    a.mask_alpha = cp.gate_alpha;
+  }
   auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, false, 0, CONV, NARROW>;
   ensure_smem(kern, SMEM);
   const int64_t total = (int64_t)a.tiles_m * a.tiles_n * a.splits * a.B;

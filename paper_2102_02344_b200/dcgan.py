@@ -211,12 +211,16 @@ class FusedDCGAN:
             e1.record(torch.cuda.current_stream())
             self._probe_ev.append((e0, e1))
 
-    def _conv_bwd(self, half, name, desc, dY, X, dX, s, wgrad=True, accumulate=0):
+    def _conv_bwd(self, half, name, desc, dY, X, dX, s, wgrad=True, accumulate=0, gate=None):
+        """gate: (act, alpha, tensor) -- dX *= act'(tensor), the backward of the
+        activation that consumed X (fused into the dgrad epilogue)."""
         ar = half.arena
-        H.hfta_fused_conv_bwd(self.B, desc, self.dt, self._in(dY), X, self._win(half, name),
-                              self._out(dX) if dX is not None else H.hfta_out(None, 0, 1),
-                              ar.fptr("g", name) if wgrad else None, ar.P, accumulate, self.ws.ptr,
-                              self.ws.nbytes, s)
+        act, alpha, g = gate if gate is not None else (H.ACT_NONE, 0.0, None)
+        H.hfta_fused_conv_bwd_gated(self.B, desc, self.dt, self._in(dY), X, self._win(half, name),
+                                    self._out(dX) if dX is not None else H.hfta_out(None, 0, 1),
+                                    ar.fptr("g", name) if wgrad else None, ar.P, accumulate, act, alpha,
+                                    self._in(g) if g is not None else H.hfta_in(None, 0, 1), self.ws.ptr,
+                                    self.ws.nbytes, s)
 
     def _bn_fwd(self, half, name, X, act, alpha, Y, s):
         R, C = X[0].numel() // X.shape[-1], X.shape[-1]
@@ -262,9 +266,12 @@ class FusedDCGAN:
         for i in (3, 2, 1):
             self._bn_bwd(D, "bn%d" % (i + 1), self.ddh[i], self.dy[i], H.ACT_LEAKY_RELU, 0.2, self.ddy[i], s, wgrad,
                          accumulate)
-            self._conv_bwd(D, "c%d.W" % (i + 1), self.ddesc[i], self.ddy[i], self._in(self.dh[i - 1]),
-                           self.ddh[i - 1], s, wgrad, accumulate)
-        self._act_bwd(H.ACT_LEAKY_RELU, 0.2, self.dh[0], self.ddh[0], self.ddy[0], s)   # gate: act(y) > 0 <=> y > 0
+            if i > 1:
+                self._conv_bwd(D, "c%d.W" % (i + 1), self.ddesc[i], self.ddy[i], self._in(self.dh[i - 1]),
+                               self.ddh[i - 1], s, wgrad, accumulate)
+            else:       # c2's dgrad through c1's LeakyReLU (gate: act(y) > 0 <=> y > 0), one epilogue
+                self._conv_bwd(D, "c2.W", self.ddesc[1], self.ddy[1], self._in(self.dh[0]), self.ddy[0], s, wgrad,
+                               accumulate, gate=(H.ACT_LEAKY_RELU, 0.2, self.dh[0]))
         self._conv_bwd(D, "c1.W", self.ddesc[0], self.ddy[0], img_in, self.dimg if need_dimg else None, s, wgrad,
                        accumulate)
 

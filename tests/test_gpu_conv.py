@@ -175,3 +175,36 @@ def test_resnet_conv_bf16(layer, B):
 @pytest.mark.parametrize("layer", RESNET, ids=[l[0] for l in RESNET])
 def test_resnet_conv_f32(layer):
     check(layer, 2, 8, "f32", shared=False)
+
+
+@pytest.mark.parametrize("layer,act,alpha", [(LAYERS[1], "leaky", 0.2), (RESNET[1], "relu", 0.0),
+                                             (LAYERS[2], "relu", 0.0)], ids=["D.c2-leaky", "R.l1-relu", "D.c3-relu"])
+def test_conv_bwd_gated(layer, act, alpha):
+    """hfta_fused_conv_bwd_gated: dX *= act'(gate) -- fused into the sub-pixel
+    dgrad epilogue (D c2 / c3), a separate pass on the other paths (R.l1)."""
+    name, tr, Hs, Ci, Co, k, st, pd = layer
+    B, N = 2, 32
+    code = H.ACT_LEAKY_RELU if act == "leaky" else H.ACT_RELU
+    rng = np.random.default_rng(11)
+    Ho = (Hs + 2 * pd - k) // st + 1
+    X = rnd(rng.standard_normal((B, N, Hs, Hs, Ci)), torch.bfloat16)
+    Wg = rnd(rng.standard_normal((B, Co, k, k, Ci)) / np.sqrt(k * k * Ci), torch.bfloat16)
+    dY = rnd(rng.standard_normal((B, N, Ho, Ho, Co)), torch.bfloat16)
+    G = rnd(rng.standard_normal((B, N, Hs, Hs, Ci)), torch.bfloat16)
+    d = H.hfta_conv_desc()
+    d.N, d.H, d.W, d.C_in, d.C_out, d.kh, d.kw, d.stride, d.pad, d.transposed = N, Hs, Hs, Ci, Co, k, k, st, pd, tr
+    dev = lambda a: torch.tensor(a).to(torch.bfloat16).to(DEV).contiguous()
+    Xd, Wd, dYd, Gd = dev(X), dev(Wg), dev(dY), dev(G)
+    dX = torch.empty(B, N, Hs, Hs, Ci, dtype=torch.bfloat16, device=DEV)
+    ws = torch.empty(max(H.hfta_fused_conv_workspace(B, d, 1), 256), dtype=torch.uint8, device=DEV)
+    xe = N * Hs * Hs * Ci
+    wbs = int(np.prod(Wg.shape[1:]))
+    H.hfta_fused_conv_bwd_gated(B, d, 1, H.tin(dYd, N * Ho * Ho * Co, Co), H.tin(Xd, xe, Ci),
+                                H.tin(Wd, wbs, k * k * Ci), H.tout(dX, xe, Ci), None, wbs, 0, code, alpha,
+                                H.tin(Gd, xe, Ci), H.ptr(ws), ws.numel(), s())
+    torch.cuda.synchronize()
+    for b in range(B):
+        dx, _ = OL.conv2d_bwd(dY[b].transpose(0, 3, 1, 2), X[b].transpose(0, 3, 1, 2), Wg[b].transpose(0, 3, 1, 2),
+                              st, pd)
+        ref = dx.transpose(0, 2, 3, 1) * np.where(G[b] > 0, 1.0, alpha)
+        assert_close(host(dX)[b], ref, 1e-2, "%s gated dX model %d" % (name, b))

@@ -50,17 +50,18 @@ def point(args, B, device):
         torch.cuda.synchronize()
         vals.append(B * wl.samples * args.steps / (e0.elapsed_time(e1) / 1e3))
     mem = torch.cuda.max_memory_allocated(device)
+    samples = wl.samples
     del g, wl
     gc.collect()
     torch.cuda.empty_cache()
     return dict(B=B, value=sum(vals) / len(vals), min=min(vals), max=max(vals), repeats=len(vals),
-                ms_per_step=B * (args.N if args.workload != "dcgan" else args.N_dcgan) * 1e3 / (sum(vals) / len(vals)),
+                ms_per_step=B * samples * 1e3 / (sum(vals) / len(vals)),
                 peak_mem_gb=mem / 1e9)
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", default="pointnet_cls", choices=["pointnet_cls", "pointnet_seg", "dcgan"])
+    ap.add_argument("--workload", default="pointnet_cls", choices=["pointnet_cls", "pointnet_seg", "dcgan", "resnet18"])
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
@@ -71,6 +72,7 @@ def main():
     ap.add_argument("--k", type=int, default=40)
     ap.add_argument("--k-seg", type=int, default=50)
     ap.add_argument("--N-dcgan", type=int, default=128)
+    ap.add_argument("--N-resnet", type=int, default=128)
     ap.add_argument("--max-seconds", type=float, default=900.0)
     args = ap.parse_args()
     import torch
