@@ -62,6 +62,7 @@ struct TcArgs {
   int y_c, y_h, y_w; int64_t y_bs;   // CONV 2: output image [B][n][y_h][y_w][y_c] the phases interleave into
   // CONV 1, 3, 4 gather geometry: kernel ks x ks, stride cs, pad cp (DCGAN: 4, 2, 1); taps = ks * ks
   int ks, cs, cp, taps;
+  uint8_t tkx[64], tky[64];          // tap -> (kx, ky) (row-major; entries past `taps` = tap 0): no division
   int wflip;                         // CONV 1 with B MN-major: B is the 4-D weight view {Cn, taps, Ca} read at
                                      // tap taps-1-t (the stride-1 Conv2d dgrad: flipped, transposed W)
 };
@@ -70,10 +71,13 @@ struct TcArgs {
 // (gather modes): x = cs * g - cp + kx.  Taps past the kernel (a partial last k-block of an
 // 8-channel image) read tap 0: their weight rows are zero (TMA zero-fill past K).
 __device__ __forceinline__ void tap_xy(const TcArgs& p, int tap, int gx, int gy, int& x, int& y) {
-  if (tap >= p.taps) tap = 0;
-  const int ky = tap / p.ks, kx = tap - ky * p.ks;
-  x = p.cs * gx - p.cp + kx;
-  y = p.cs * gy - p.cp + ky;
+  if (p.ks == 4 && p.cs == 2 && p.cp == 1) {      // k4 s2 p1 (DCGAN): shifts, no table reads
+    x = 2 * gx - 1 + (tap & 3);
+    y = 2 * gy - 1 + (tap >> 2);
+    return;
+  }
+  x = p.cs * gx - p.cp + p.tkx[tap & 63];
+  y = p.cs * gy - p.cp + p.tky[tap & 63];
 }
 
 // Row index r of a dense NHWC grid (gw x gh per image) -> (image, row, col), 32-bit.
@@ -987,6 +991,10 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   a.y_c = CONV == 5 ? 8 : (int)cp.N; a.y_h = cp.y_h; a.y_w = cp.y_w; a.y_bs = cp.c_bs;
   a.act = (CONV == 1 || CONV == 2 || CONV == 5) ? cp.act : HFTA_ACT_NONE; a.act_alpha = cp.act_alpha;
   a.ks = ks; a.cs = cs; a.cp = cpd; a.taps = ks * ks; a.wflip = cp.wflip;
+  for (int t = 0; t < 64; ++t) {
+    const int tt = t < a.taps ? t : 0;
+    a.tkx[t] = (uint8_t)(tt % ks); a.tky[t] = (uint8_t)(tt / ks);
+  }
   if (CONV == 2 && cp.gate) {        // gated dgrad: ReLU' (alpha 0) / LeakyReLU' (alpha) of the gate tensor
     a.mask = reinterpret_cast<const __nv_bfloat16*>(cp.gate); a.mask_bs = cp.gate_bs;
     a.mask_alpha = cp.gate_alpha;
@@ -1013,7 +1021,7 @@ bool conv_tc_supported(const ConvTcP& p) {
   const int rows = (p.mode == 1 || p.mode == 2 || p.mode == 5) ? BM : BK;
   if (!grid_box(p.grid_w, p.grid_h, p.img_n, rows, bw, bh, bn)) return false;
   const int64_t taps = p.ks > 0 ? (int64_t)p.ks * p.ks : 16;
-  if (p.ks > 0 && (p.cs < 1 || p.cs > 2 || p.cpad < 0 || p.ks > 15 || (p.mode != 1 && p.mode != 3))) return false;
+  if (p.ks > 0 && (p.cs < 1 || p.cs > 2 || p.cpad < 0 || p.ks > 8 || (p.mode != 1 && p.mode != 3))) return false;
   if (p.wflip && (p.mode != 1 || !p.w_mn || p.cs != 1 || p.w_cn % 64 || p.w_ca % 64)) return false;
   switch (p.mode) {
     case 1: return p.K == taps * (int64_t)p.img_c && p.N % 16 == 0 && (p.c_ld * 2) % 16 == 0 &&
