@@ -364,15 +364,20 @@ hfta_status hfta_transform_points_bwd(int B, int64_t N, int64_t L, hfta_dtype dt
  * *step_ptr + step, read at kernel time -- so a captured CUDA graph of the
  * training step draws a fresh mask on every replay.  b in the counter is the
  * GLOBAL model index model_offset + (local b): a model-array shard draws the
- * masks its models draw in an unsharded run (the rank's first model index).
+ * masks its models draw in an unsharded run (the rank's first model index);
+ * model_ids (device int32 [B], nullable) overrides it with explicit per-model
+ * ids (an HFHT partition of non-contiguous hyper-parameter sets draws each
+ * set's own masks, whatever partition it lands in).
  * X/Y [B][rows][cols] dtype dt.  bwd: same mask applied to dY.
  */
 hfta_status hfta_dropout_fwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in X,
                              hfta_out Y, uint64_t seed, int64_t step, const int64_t* step_ptr,
-                             int32_t layer, float p, int32_t model_offset, hfta_stream stream);
+                             int32_t layer, float p, int32_t model_offset, const int32_t* model_ids,
+                             hfta_stream stream);
 hfta_status hfta_dropout_bwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in dY,
                              hfta_out dX, uint64_t seed, int64_t step, const int64_t* step_ptr,
-                             int32_t layer, float p, int32_t model_offset, hfta_stream stream);
+                             int32_t layer, float p, int32_t model_offset, const int32_t* model_ids,
+                             hfta_stream stream);
 /*
  * Segmented column sums: S[b][g][c] = sum_{r in group g} X[b][r][c] with
  * groups of `group` consecutive rows (group = rows: plain column sum).

@@ -83,13 +83,14 @@ template <typename T>
 __global__ void k_dropout(int64_t rows, int64_t cols, const T* __restrict__ X, int64_t xbs, int64_t xld,
                           T* __restrict__ Y, int64_t ybs, int64_t yld, uint32_t k0, uint32_t k1, uint32_t step_arg,
                           const int64_t* __restrict__ step_ptr, uint32_t layer, uint32_t thr, float scale,
-                          uint32_t model_offset) {
+                          uint32_t model_offset, const int32_t* __restrict__ model_ids) {
   const int b = blockIdx.y;
+  const uint32_t gid = model_ids ? (uint32_t)model_ids[b] : model_offset + (uint32_t)b;   // global model index
   const uint32_t step = step_ptr ? (uint32_t)(*step_ptr + (int64_t)step_arg) : step_arg;   // device counter: graphs
   const int64_t n = rows * cols;
   const int64_t groups = (n + 3) / 4;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < groups; q += (int64_t)gridDim.x * blockDim.x) {
-    U4 w = philox4x32_10(U4{(uint32_t)q, model_offset + (uint32_t)b, step, layer}, k0, k1);   // global model index
+    U4 w = philox4x32_10(U4{(uint32_t)q, gid, step, layer}, k0, k1);
     uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -322,7 +323,8 @@ hfta_status hfta_transform_points_bwd(int B, int64_t N, int64_t L, hfta_dtype dt
 
 static hfta_status dropout_common(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in X, hfta_out Y,
                                   uint64_t seed, int64_t step, const int64_t* step_ptr, int32_t layer, float p,
-                                  int32_t model_offset, hfta_stream stream, const char* what) {
+                                  int32_t model_offset, const int32_t* model_ids, hfta_stream stream,
+                                  const char* what) {
   if (hfta_status st = check_init()) return st;
   HFTA_CHECK_B(B);
   HFTA_REQUIRE(rows >= 1 && cols >= 1 && X.ptr && Y.ptr, HFTA_ERR_INVALID_VALUE, "%s: bad args", what);
@@ -338,26 +340,27 @@ static hfta_status dropout_common(int B, int64_t rows, int64_t cols, hfta_dtype 
   if (dt == HFTA_F32)
     k_dropout<float><<<grid, 256, 0, s>>>(rows, cols, (const float*)X.ptr, X.bstride, X.ld, (float*)Y.ptr, Y.bstride,
                                          Y.ld, k0, k1, (uint32_t)step, step_ptr, (uint32_t)layer, thr, scale,
-                                         (uint32_t)model_offset);
+                                         (uint32_t)model_offset, model_ids);
   else
     k_dropout<__nv_bfloat16><<<grid, 256, 0, s>>>(rows, cols, (const __nv_bfloat16*)X.ptr, X.bstride, X.ld,
                                                  (__nv_bfloat16*)Y.ptr, Y.bstride, Y.ld, k0, k1, (uint32_t)step,
-                                                 step_ptr, (uint32_t)layer, thr, scale, (uint32_t)model_offset);
+                                                 step_ptr, (uint32_t)layer, thr, scale, (uint32_t)model_offset,
+                                                 model_ids);
   count_launches(1);
   return post_launch(s, what);
 }
 
 hfta_status hfta_dropout_fwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in X, hfta_out Y, uint64_t seed,
                              int64_t step, const int64_t* step_ptr, int32_t layer, float p, int32_t model_offset,
-                             hfta_stream stream) {
-  return dropout_common(B, rows, cols, dt, X, Y, seed, step, step_ptr, layer, p, model_offset, stream,
+                             const int32_t* model_ids, hfta_stream stream) {
+  return dropout_common(B, rows, cols, dt, X, Y, seed, step, step_ptr, layer, p, model_offset, model_ids, stream,
                         "hfta_dropout_fwd");
 }
 
 hfta_status hfta_dropout_bwd(int B, int64_t rows, int64_t cols, hfta_dtype dt, hfta_in dY, hfta_out dX,
                              uint64_t seed, int64_t step, const int64_t* step_ptr, int32_t layer, float p,
-                             int32_t model_offset, hfta_stream stream) {
-  return dropout_common(B, rows, cols, dt, dY, dX, seed, step, step_ptr, layer, p, model_offset, stream,
+                             int32_t model_offset, const int32_t* model_ids, hfta_stream stream) {
+  return dropout_common(B, rows, cols, dt, dY, dX, seed, step, step_ptr, layer, p, model_offset, model_ids, stream,
                         "hfta_dropout_bwd");
 }
 

@@ -275,8 +275,9 @@ class PointNetRunner:
         specs = [(n, s) for n, s, _ in synth.param_specs("pointnet_cls", self.k, None, ft)]
         Ps = [synth.init_params("pointnet_cls", 1000 + m[0], self.k, None, ft) for m in part.members]
         with torch.cuda.device(dev):
+            # each set's dropout masks keyed by its own id: results independent of the partitioning
             net = FusedPointNet(B, specs, Ps, hp, task="cls", dtype=self.dtype, N=N, L=self.L, k=self.k, device=dev,
-                                feature_transform=ft)
+                                feature_transform=ft, model_ids=[m[0] for m in part.members])
             gam = torch.tensor([s_["gamma"] for s_ in sets], dtype=torch.float32, device=dev)
             per = torch.tensor([s_["step_size"] for s_ in sets], dtype=torch.int32, device=dev)
             lr0 = net.hv.t["lr"].clone()

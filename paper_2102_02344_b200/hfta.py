@@ -79,8 +79,10 @@ _SIGS = {
                                        vp, vp, hfta_out, i32, f32, vp, i64, i64, vp, i64, vp, vp, i32, vp, sz, vp]),
     "hfta_transform_points_fwd": (i32, [i32, i64, i64, i32, hfta_in, hfta_in, i32, hfta_out, vp]),
     "hfta_transform_points_bwd": (i32, [i32, i64, i64, i32, hfta_in, hfta_in, hfta_out, vp]),
-    "hfta_dropout_fwd": (i32, [i32, i64, i64, i32, hfta_in, hfta_out, u64, i64, vp, C.c_int32, f32, C.c_int32, vp]),
-    "hfta_dropout_bwd": (i32, [i32, i64, i64, i32, hfta_in, hfta_out, u64, i64, vp, C.c_int32, f32, C.c_int32, vp]),
+    "hfta_dropout_fwd": (i32, [i32, i64, i64, i32, hfta_in, hfta_out, u64, i64, vp, C.c_int32, f32, C.c_int32, vp,
+                               vp]),
+    "hfta_dropout_bwd": (i32, [i32, i64, i64, i32, hfta_in, hfta_out, u64, i64, vp, C.c_int32, f32, C.c_int32, vp,
+                               vp]),
     "hfta_colsum_workspace": (sz, [i32, i64, i64, i64]),
     "hfta_colsum": (i32, [i32, i64, i64, i64, i32, hfta_in, vp, i64, i32, vp, sz, vp]),
     "hfta_loss_workspace": (sz, [i32, i64]),

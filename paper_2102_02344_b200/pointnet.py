@@ -33,13 +33,17 @@ class FusedPointNet(FusedNet):
     bn_followed = BN_FOLLOWED
 
     def __init__(self, B, param_specs, params, hp, task="cls", dtype="f32", N=32, L=2500, k=40,
-                 p_drop=0.3, dropout_seed=42, device="cuda", feature_transform=False, ft_weight=0.001, model_offset=0):
+                 p_drop=0.3, dropout_seed=42, device="cuda", feature_transform=False, ft_weight=0.001, model_offset=0,
+                 model_ids=None):
         assert task in ("cls", "seg")
         self._base_init(B, param_specs, params, hp, dtype, device)
         self.task, self.N, self.L, self.k = task, N, L, k
         self.R = N * L
         self.p_drop, self.dropout_seed = p_drop, dropout_seed
         self.model_offset = int(model_offset)     # global index of model 0 (model-array sharding: dropout masks)
+        # explicit per-model dropout ids (HFHT partitions of non-contiguous sets), else model_offset + b
+        self.model_ids = (torch.tensor(np.asarray(model_ids, dtype=np.int32), device=device)
+                          if model_ids is not None else None)
         sh = self.arena.shape
         self.c1, self.c2, self.c3 = sh["stn.c1.W"][0], sh["stn.c2.W"][0], sh["stn.c3.W"][0]
         self.f1, self.f2 = sh["stn.fc1.W"][0], sh["stn.fc2.W"][0]
@@ -417,7 +421,7 @@ class FusedPointNet(FusedNet):
         # the Philox step comes from the device step counter (+1: it is advanced by the
         # optimizer at the end of the step), so a captured CUDA graph replays correctly
         H.hfta_dropout_fwd(self.B, N, self.f2, H.HFTA_F32, _in(S["head.y2"]), _out(S["head.d2"]), self.dropout_seed,
-                           1, H.ptr(self.hv.step), 0, self.p_drop, self.model_offset, s)
+                           1, H.ptr(self.hv.step), 0, self.p_drop, self.model_offset, H.ptr(self.model_ids), s)
         self._bn_fwd(S["head.d2"], "head.bn2", A_RELU, S["head.h2"], s)
         self._lin_fwd(_in(S["head.h2"]), N, "head.fc3", S["head.logits"], s)
         H.hfta_loss_nll(self.B, N, self.k, H.HFTA_F32, _in(S["head.logits"]), H.ptr(self.labels), 0, H.ptr(self.loss),
@@ -425,7 +429,7 @@ class FusedPointNet(FusedNet):
         self._lin_bwd(S["d.logits"], _in(S["head.h2"]), N, "head.fc3", S["d.f2a"], s)
         self._bn_bwd(S["d.f2a"], S["head.d2"], "head.bn2", A_RELU, S["d.f2b"], s)
         H.hfta_dropout_bwd(self.B, N, self.f2, H.HFTA_F32, _in(S["d.f2b"]), _out(S["d.f2a"]), self.dropout_seed,
-                           1, H.ptr(self.hv.step), 0, self.p_drop, self.model_offset, s)
+                           1, H.ptr(self.hv.step), 0, self.p_drop, self.model_offset, H.ptr(self.model_ids), s)
         self._lin_bwd(S["d.f2a"], _in(S["head.h1"]), N, "head.fc2", S["d.f1a"], s)
         self._bn_bwd(S["d.f1a"], S["head.y1"], "head.bn1", A_RELU, S["d.f1b"], s)
         self._lin_bwd(S["d.f1b"], _in(S["feat.g"]), N, "head.fc1", S["d.g"], s)

@@ -291,12 +291,12 @@ def test_dropout_mask_bit_exact(dt):
     X = rounded(R.standard_normal((B, rows, cols)), tdt)
     Y = torch.empty(B, rows, cols, dtype=tdt, device=DEV)
     H.hfta_dropout_fwd(B, rows, cols, code, H.tin(dev(X, tdt), rows * cols, cols), H.tout(Y, rows * cols, cols), 42,
-                       5, None, 0, p, 0, s())
+                       5, None, 0, p, 0, None, s())
     # the same mask when the step comes from a device counter (graph-capturable form): 4 + 1
     Y2 = torch.empty_like(Y)
     stepd = torch.tensor([4], dtype=torch.int64, device=DEV)
     H.hfta_dropout_fwd(B, rows, cols, code, H.tin(dev(X, tdt), rows * cols, cols), H.tout(Y2, rows * cols, cols), 42,
-                       1, H.ptr(stepd), 0, p, 0, s())
+                       1, H.ptr(stepd), 0, p, 0, None, s())
     torch.cuda.synchronize()
     assert torch.equal(Y, Y2)
     torch.cuda.synchronize()
@@ -315,16 +315,32 @@ def test_dropout_sharded_masks_equal_unsharded():
     X = rounded(R.standard_normal((B, rows, cols)), torch.float32)
     full = torch.empty(B, rows, cols, device=DEV)
     H.hfta_dropout_fwd(B, rows, cols, 0, H.tin(dev(X), rows * cols, cols), H.tout(full, rows * cols, cols), 42,
-                       3, None, 0, p, 0, s())
+                       3, None, 0, p, 0, None, s())
     for lo, hi in ((0, 2), (2, 4), (4, 6)):                 # 3 "ranks"
         part = torch.empty(hi - lo, rows, cols, device=DEV)
         H.hfta_dropout_fwd(hi - lo, rows, cols, 0, H.tin(dev(X[lo:hi]), rows * cols, cols),
-                           H.tout(part, rows * cols, cols), 42, 3, None, 0, p, lo, s())
+                           H.tout(part, rows * cols, cols), 42, 3, None, 0, p, lo, None, s())
         torch.cuda.synchronize()
         assert torch.equal(part, full[lo:hi])
         for b in range(lo, hi):
             keep = dropout_keep_mask(42, b, 3, 0, rows * cols, p).reshape(rows, cols)
             assert np.array_equal(host(part[b - lo]) != 0, keep & (X[b] != 0))
+
+
+def test_dropout_explicit_model_ids():
+    """Per-model ids (an HFHT partition of non-contiguous hyper-parameter
+    sets): model b draws the mask of id[b]."""
+    B, rows, cols, p = 3, 8, 64, 0.3
+    ids = [7, 2, 11]
+    X = rounded(R.standard_normal((B, rows, cols)), torch.float32)
+    Y = torch.empty(B, rows, cols, device=DEV)
+    idd = torch.tensor(ids, dtype=torch.int32, device=DEV)
+    H.hfta_dropout_fwd(B, rows, cols, 0, H.tin(dev(X), rows * cols, cols), H.tout(Y, rows * cols, cols), 42,
+                       2, None, 0, p, 0, H.ptr(idd), s())
+    torch.cuda.synchronize()
+    for b in range(B):
+        keep = dropout_keep_mask(42, ids[b], 2, 0, rows * cols, p).reshape(rows, cols)
+        assert np.array_equal(host(Y[b]) != 0, keep & (X[b] != 0))
 
 
 @pytest.mark.parametrize("K", [50, 40, 7])
