@@ -398,7 +398,7 @@ def run_ours(args, rank, world, local_rank):
         line["step_roofline"] = step_roofline(args.workload, args.dtype, value, pk, args)
         try:   # DRAM traffic of the probed kernel from the committed ncu --set full capture
             key = probe_name + (":lbm" if getattr(net, "fuse_lbm", False) and ".c3:" in probe_name else "")
-            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic_r01.json")))[key]
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic_r02.json")))[key]
             if path == "tc":
                 roof["traffic"] = tr["dram_bytes_per_model"] * B
                 roof["traffic_source"] = tr["source"]
