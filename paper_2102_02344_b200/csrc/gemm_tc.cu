@@ -964,7 +964,7 @@ hfta_status img_map(CUtensorMap* m, const ConvTcP& p, int nb, int rows, int st) 
 // CTA-pair multicast of the shared B tile in the conv modes (opt-in: env HFTA_CONV_PAIRS=1)
 bool conv_pairs_enabled() {
   static const bool on = [] {
-    const char* e = getenv("HFTA_CONV_PAIRS");    // measured: no gain (the small-N tiles are MMA-issue bound)
+    const char* e = getenv("HFTA_CONV_PAIRS");    // measured: no gain (not the shared operand)
     return e && e[0] == '1';
   }();
   return on;
