@@ -129,19 +129,39 @@ __global__ void __launch_bounds__(NT, MINB) k_bn_stats(int64_t R, int64_t C, con
   }
 }
 
+// Chunk partials -> per-(model, channel) sums: block = (32 channels, model b),
+// 8 warps take chunks w, w + 8, ... (lane = channel: coalesced), then warp 0
+// adds the 8 warp sums in order (fixed order: deterministic).
+__device__ __forceinline__ bool chunk_sums(int64_t C, int chunks, const double* __restrict__ p1,
+                                           const double* __restrict__ p2, double& s1, double& s2) {
+  __shared__ double r1[8][32], r2[8][32];
+  const int b = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  double a1 = 0.0, a2 = 0.0;
+  if (c < C)
+    for (int k = w; k < chunks; k += 8) {
+      a1 += p1[((int64_t)b * chunks + k) * C + c];
+      a2 += p2[((int64_t)b * chunks + k) * C + c];
+    }
+  r1[w][lane] = a1;
+  r2[w][lane] = a2;
+  __syncthreads();
+  if (w != 0 || c >= C) return false;
+  s1 = 0.0; s2 = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) { s1 += r1[q][lane]; s2 += r2[q][lane]; }
+  return true;
+}
+
 template <typename T>
 __global__ void k_bn_finalize(int B, int64_t R, int64_t C, const T* __restrict__ X, int64_t xbs, int chunks,
                               const double* __restrict__ p1, const double* __restrict__ p2, float eps,
                               float momentum, float* __restrict__ rmean, float* __restrict__ rvar,
                               float* __restrict__ smean, float* __restrict__ sinv) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)B * C) return;
-  int64_t b = i / C, c = i % C;
-  double s1 = 0.0, s2 = 0.0;
-  for (int k = 0; k < chunks; ++k) {
-    s1 += p1[(b * chunks + k) * C + c];
-    s2 += p2[(b * chunks + k) * C + c];
-  }
+  double s1, s2;
+  if (!chunk_sums(C, chunks, p1, p2, s1, s2)) return;
+  const int64_t b = blockIdx.y, c = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
+  const int64_t i = b * C + c;
   double shift = (double)ldf(X + b * xbs + c);
   double md = s1 / (double)R;
   double var = s2 / (double)R - md * md;
@@ -268,14 +288,10 @@ __global__ void k_bn_bwd_finalize(int B, int64_t R, int64_t C, int chunks, const
                                   const float* __restrict__ beta, int64_t gbs, const float* __restrict__ smean,
                                   const float* __restrict__ sinv, float* __restrict__ dgamma,
                                   float* __restrict__ dbeta, int accumulate, float* __restrict__ coef) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)B * C) return;
-  int64_t b = i / C, c = i % C;
-  double s1 = 0.0, s2 = 0.0;
-  for (int k = 0; k < chunks; ++k) {
-    s1 += p1[(b * chunks + k) * C + c];
-    s2 += p2[(b * chunks + k) * C + c];
-  }
+  double s1, s2;
+  if (!chunk_sums(C, chunks, p1, p2, s1, s2)) return;
+  const int64_t b = blockIdx.y, c = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
+  const int64_t i = b * C + c;
   const double is = sinv[i], m = smean[i], ga = gamma[b * gbs + c], be = beta[b * gbs + c];
   const double db = s1, dg = s2 * is;
   if (dbeta) dbeta[b * gbs + c] = accumulate ? dbeta[b * gbs + c] + (float)db : (float)db;
@@ -804,7 +820,7 @@ hfta_status hfta_fused_bn_fwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_i
     DT_DISPATCH(dt, {
     if (vec > 1) LAUNCH_P1(T, k_bn_stats_p, grid, R, C, (const T*)X.ptr, X.bstride, X.ld, g, p1, p2);
     else LAUNCH_V1(T, k_bn_stats, grid, R, C, (const T*)X.ptr, X.bstride, X.ld, g, p1, p2);
-    k_bn_finalize<T><<<(unsigned)cdiv((int64_t)B * C, 256), 256, 0, s>>>(
+    k_bn_finalize<T><<<dim3((unsigned)cdiv(C, 32), (unsigned)B), 256, 0, s>>>(
         B, R, C, (const T*)X.ptr, X.bstride, g.chunks, p1, p2, eps, momentum, running_mean, running_var,
         save_mean, save_invstd);
     if (Y.ptr)
@@ -848,7 +864,7 @@ hfta_status hfta_fused_bn_bwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_i
                X.bstride, X.ld, gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, g, p1, p2);
     else LAUNCH_V1(T, k_bn_bwd_reduce, grid, R, C, (const T*)dY.ptr, dY.bstride, dY.ld, (const T*)X.ptr,
                X.bstride, X.ld, gamma, beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, g, p1, p2);
-    k_bn_bwd_finalize<<<(unsigned)cdiv((int64_t)B * C, 256), 256, 0, s>>>(
+    k_bn_bwd_finalize<<<dim3((unsigned)cdiv(C, 32), (unsigned)B), 256, 0, s>>>(
         B, R, C, g.chunks, p1, p2, gamma, beta, gb_bstride, save_mean, save_invstd, dgamma, dbeta, accumulate, coef);
     if (vec > 1) LAUNCH_P2(T, k_bn_bwd_apply_p, grida, B, R, C, (const T*)dY.ptr, dY.bstride, dY.ld, (const T*)X.ptr,
               X.bstride, X.ld, (T*)dX.ptr, dX.bstride, dX.ld, (int)act, act_alpha, ga, coef);
