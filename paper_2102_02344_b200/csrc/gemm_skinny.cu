@@ -392,6 +392,79 @@ __global__ void k_gemv_fwd(GemmP p) {
   }
 }
 
+// gemv fwd with 16-B vectors (bf16, K % 8 == 0, aligned rows): lane l reads
+// A[m][8 l + 256 i ..] and B[n][..] as uint4 -- a warp moves 512 B per step.
+template <int NMAX>
+__global__ void k_gemv_fwd_v8(GemmP p) {
+  const int b = blockIdx.y;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+  const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(p.A) + (int64_t)b * p.a_bs;
+  const __nv_bfloat16* Bw = reinterpret_cast<const __nv_bfloat16*>(p.Bm) + (int64_t)b * p.b_bs;
+  __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(p.C) + (int64_t)b * p.c_bs;
+  for (int64_t m = warp; m < p.M; m += nwarps) {
+    float acc[NMAX];
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) acc[n] = 0.f;
+    const uint4* ar = reinterpret_cast<const uint4*>(A + m * p.a_ld);
+    for (int64_t q = lane; q < p.K / 8; q += 32) {
+      float a[8];
+      ld_vec<__nv_bfloat16, 8>(reinterpret_cast<const __nv_bfloat16*>(ar + q), a);
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) {
+        if (n >= p.N) break;
+        float w[8];
+        ld_vec<__nv_bfloat16, 8>(Bw + n * p.b_ld + q * 8, w);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[n] = fmaf(a[e], w[e], acc[n]);
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[n] += __shfl_xor_sync(0xffffffffu, acc[n], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n) {
+        if (n >= p.N) break;
+        float v = acc[n];
+        if (p.bias) v += p.bias[(int64_t)b * p.bias_bs + (p.bias_div > 0 ? (m / p.bias_div) * p.bias_ld : 0) + n];
+        stf(C + m * p.c_ld + n, v);
+      }
+    }
+  }
+}
+
+// outer-product-like small K with B MN-major ([K][N], n contiguous), bf16,
+// N % 8 == 0: thread = (row m, 8 consecutive n), 16-B loads / stores.
+__global__ void k_smallk_v8(GemmP p) {
+  const int b = blockIdx.y;
+  const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(p.A) + (int64_t)b * p.a_bs;
+  const __nv_bfloat16* Bw = reinterpret_cast<const __nv_bfloat16*>(p.Bm) + (int64_t)b * p.b_bs;
+  __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(p.C) + (int64_t)b * p.c_bs;
+  const int64_t nv = p.N / 8, tot = p.M * nv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / nv, n0 = (i - m * nv) * 8;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    for (int64_t k = 0; k < p.K; ++k) {
+      const float a = ldf(A + m * p.a_ld + k);
+      float w[8];
+      ld_vec<__nv_bfloat16, 8>(Bw + k * p.b_ld + n0, w);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = fmaf(a, w[e], acc[e]);
+    }
+    if (p.bias) {
+      const float* br = p.bias + (int64_t)b * p.bias_bs + (p.bias_div > 0 ? (m / p.bias_div) * p.bias_ld : 0) + n0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += br[e];
+    }
+    st_vec<__nv_bfloat16, 8>(C + m * p.c_ld + n0, acc);
+  }
+}
+
 // any majorness, reduction K <= 8: C[m][n] = sum_k A(m,k) B(n,k); thread per output element.
 template <typename T, bool AK, bool BKM>
 __global__ void k_smallk(GemmP p) {
@@ -491,13 +564,23 @@ hfta_status gemm_skinny(const GemmP& p, hfta_dtype dt, void* ws, size_t ws_bytes
     }
     if (gemv_fwd_ok(p)) {
       dim3 grid((unsigned)std::min<int64_t>(cdiv(p.M, 8), 1024), p.B);
-      if (bf) k_gemv_fwd<__nv_bfloat16><<<grid, 256, 0, s>>>(p);
+      const bool v8 = bf && p.K % 8 == 0 && p.a_ld % 8 == 0 && p.b_ld % 8 == 0 && p.a_bs % 8 == 0 &&
+                      p.b_bs % 8 == 0 && aligned16(p.A) && aligned16(p.Bm);
+      if (v8) k_gemv_fwd_v8<KMAX><<<grid, 256, 0, s>>>(p);
+      else if (bf) k_gemv_fwd<__nv_bfloat16><<<grid, 256, 0, s>>>(p);
       else k_gemv_fwd<float><<<grid, 256, 0, s>>>(p);
       count_launches(1);
       return post_launch(s, "gemm_gemv_fwd");
     }
     if (smallk_ok(p)) {
       dim3 grid((unsigned)std::min<int64_t>(cdiv(p.M * p.N, 256), 8192), p.B);
+      if (bf && !p.b_kmajor && p.N % 8 == 0 && p.b_ld % 8 == 0 && p.b_bs % 8 == 0 && p.c_ld % 8 == 0 &&
+          p.c_bs % 8 == 0 && aligned16(p.Bm) && aligned16(p.C)) {
+        dim3 g8((unsigned)std::min<int64_t>(cdiv(p.M * p.N / 8, 256), 8192), p.B);
+        k_smallk_v8<<<g8, 256, 0, s>>>(p);
+        count_launches(1);
+        return post_launch(s, "gemm_smallk");
+      }
 #define SK(AK, BK) (bf ? (void)k_smallk<__nv_bfloat16, AK, BK><<<grid, 256, 0, s>>>(p) : (void)k_smallk<float, AK, BK><<<grid, 256, 0, s>>>(p))
       if (p.a_kmajor && p.b_kmajor) SK(true, true);
       else if (p.a_kmajor) SK(true, false);
