@@ -65,9 +65,6 @@ struct TcArgs {
   uint8_t tkx[64], tky[64];          // tap -> (kx, ky) (row-major; entries past `taps` = tap 0): no division
   int wflip;                         // CONV 1 with B MN-major: B is the 4-D weight view {Cn, taps, Ca} read at
                                      // tap taps-1-t (the stride-1 Conv2d dgrad: flipped, transposed W)
-  // CTA pairs (conv modes): cl = 2 launches clusters of 2 CTAs that take the two m-tiles of a
-  // pair (same model, n-tile, split: the same B tile); each loads half of B and multicasts it
-  int cl, tiles_mp;                  // cluster size (1, 2), m-tile pairs
 };
 
 // Image coordinate of kernel tap `tap` (row-major ky * ks + kx) for output grid position g
@@ -111,11 +108,9 @@ __device__ __forceinline__ void add_f32x2(float& a, float& b, float c, float d) 
 
 // Tile t -> (m-tile, n-tile, split, model) in 32-bit arithmetic (tile counts
 // fit easily; the int64 divisions cost ~150 instructions per tile per warp)
-__device__ __forceinline__ void tile_coords(uint32_t t, const TcArgs& p, int& mt, int& nt, int& split, int& b,
-                                            int rank = 0) {
+__device__ __forceinline__ void tile_coords(uint32_t t, const TcArgs& p, int& mt, int& nt, int& split, int& b) {
   uint32_t r = t;
-  const uint32_t tn = (uint32_t)p.tiles_n, sp = (uint32_t)p.splits;
-  const uint32_t tm = (uint32_t)(p.cl == 2 ? p.tiles_mp : p.tiles_m);
+  const uint32_t tn = (uint32_t)p.tiles_n, tm = (uint32_t)p.tiles_m, sp = (uint32_t)p.splits;
   if (p.order == 0) {
     if (tn == 1) nt = 0; else { nt = (int)(r % tn); r /= tn; }
     mt = (int)(r % tm); r /= tm;
@@ -124,7 +119,6 @@ __device__ __forceinline__ void tile_coords(uint32_t t, const TcArgs& p, int& mt
     if (tn == 1) nt = 0; else { nt = (int)(r % tn); r /= tn; }
   }
   if (sp == 1) { split = 0; b = (int)r; } else { split = (int)(r % sp); b = (int)(r / sp); }
-  if (p.cl == 2) mt = 2 * mt + rank;     // the pair's m-tiles (2 mt' + 1 may be past tiles_m: computed, not stored)
 }
 
 // BRES ("B resident", forward layers with K <= 128): the B operand (the
@@ -202,8 +196,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      // + epilogue arrivals (gating from A); a CTA pair: both MMA warps release a stage
-      mbar_init(&empty[s], (EPI == 2 && p.mask_kb >= 0) ? 1 + NEPI : (p.cl == 2 ? 2 : 1));
+      mbar_init(&empty[s], (EPI == 2 && p.mask_kb >= 0) ? 1 + NEPI : 1);   // + epilogue arrivals (gating from A)
     }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], NEPI); }
     mbar_init(bfull, 1);
@@ -228,16 +221,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   }
   tc_fence_before();
   __syncthreads();
-  if (p.cl == 2) cluster_sync_all();            // the peer's barriers exist before any multicast reaches them
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int rank = p.cl == 2 ? (int)cluster_rank() : 0;
-  const int64_t tiles_mn = (int64_t)(p.cl == 2 ? p.tiles_mp : p.tiles_m) * p.tiles_n;
+  const int64_t tiles_mn = (int64_t)p.tiles_m * p.tiles_n;
   const int64_t total = tiles_mn * p.splits * p.B;
-  const int cl = p.cl == 2 ? 2 : 1;
-  const int64_t tfirst = blockIdx.x / cl, tstep = gridDim.x / cl;
-  const uint16_t MC = 3;                        // multicast mask of a pair
 
   if (warp == 0) {
     // ============================ TMA producer ============================
@@ -248,9 +236,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       uint32_t phase = 0;
       int64_t bkey = -1;
       uint32_t epoch = 0;
-      for (int64_t t = tfirst; t < total; t += tstep) {
+      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
         int mt, nt, split, b;
-        tile_coords((uint32_t)t, p, mt, nt, split, b, rank);
+        tile_coords((uint32_t)t, p, mt, nt, split, b);
         const int64_t kbeg = CONV == 2 ? 0 : (int64_t)split * p.k_chunk;
         const int64_t kend = CONV == 2 ? p.K : min(p.K, kbeg + p.k_chunk);
         const int nkb1 = (int)((kend - kbeg + BK - 1) / BK);
@@ -286,13 +274,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
             if constexpr (B_MN) {
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j) {
-                if (p.cl == 2) tma_load_3d_mc(sb + j * 8192 + rank * 4096, &tmB, &full[stage], n0 + 64 * j, k0 + 32 * rank, bb, MC);
-                else tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
-              }
+              for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
             } else {
-              if (p.cl == 2) tma_load_3d_mc(sb + rank * (BN / 2) * 128, &tmB, &full[stage], k0, n0 + rank * (BN / 2), bb, MC);
-              else tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
+              tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
             }
           } else if constexpr (CONV == 1) {               // strided gather of the input image
             const int tap = kb / p.cblk, cb = kb - tap * p.cblk;
@@ -302,23 +286,14 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             if constexpr (B_MN) {
               if (p.wflip) {                              // Conv dgrad (stride 1): B(n = ci, k = (t, co)) = W[co][T-1-t][ci]
 #pragma unroll
-                for (int j = 0; j < BN / 64; ++j) {
-                  if (p.cl == 2)
-                    tma_load_4d_mc(sb + j * 8192 + rank * 4096, &tmB, &full[stage], n0 + 64 * j, p.taps - 1 - tap,
-                                   cb * 64 + 32 * rank, bb, MC);
-                  else tma_load_4d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, p.taps - 1 - tap, cb * 64, bb);
-                }
+                for (int j = 0; j < BN / 64; ++j)
+                  tma_load_4d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, p.taps - 1 - tap, cb * 64, bb);
               } else {                                    // ConvT dgrad: B(n = ci, k = (tap, co)) = Wt[tap][co][ci]
 #pragma unroll
-                for (int j = 0; j < BN / 64; ++j) {
-                  if (p.cl == 2)
-                    tma_load_3d_mc(sb + j * 8192 + rank * 4096, &tmB, &full[stage], n0 + 64 * j, k0 + 32 * rank, bb, MC);
-                  else tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
-                }
+                for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
               }
             } else {
-              if (p.cl == 2) tma_load_3d_mc(sb + rank * (BN / 2) * 128, &tmB, &full[stage], k0, n0 + rank * (BN / 2), bb, MC);
-              else tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
+              tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
             }
           } else if constexpr (CONV == 2) {               // sub-pixel phase `split`, tap t of 4
             const int t4 = kb / p.cblk, cb = kb - t4 * p.cblk;
@@ -329,21 +304,14 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             const int tap = kh * 4 + kw;
             if constexpr (B_MN) {
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j) {
-                if (p.cl == 2)
-                  tma_load_4d_mc(sb + j * 8192 + rank * 4096, &tmB, &full[stage], n0 + 64 * j, tap, cb * 64 + 32 * rank, bb, MC);
-                else tma_load_4d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, tap, cb * 64, bb);
-              }
+              for (int j = 0; j < BN / 64; ++j) tma_load_4d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, tap, cb * 64, bb);
             } else {
-              if (p.cl == 2)
-                tma_load_4d_mc(sb + rank * (BN / 2) * 128, &tmB, &full[stage], cb * 64, n0 + rank * (BN / 2), tap, bb, MC);
-              else tma_load_4d(sb, &tmB, &full[stage], cb * 64, n0, tap, bb);
+              tma_load_4d(sb, &tmB, &full[stage], cb * 64, n0, tap, bb);
             }
           } else if constexpr (CONV == 5) {               // shifted box (dy, dx) of 9, phase-merged weights
             const int t9 = kb / p.cblk, cb = kb - t9 * p.cblk;
             tma_load_5d(sa, &tmA, &full[stage], cb * 64, gx0 + t9 % 3 - 1, gy0 + t9 / 3 - 1, gn0, ba);
-            if (p.cl == 2) tma_load_3d_mc(sb + rank * (BN / 2) * 128, &tmB, &full[stage], k0, n0 + rank * (BN / 2), bb, MC);
-            else tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
+            tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
           } else if constexpr (CONV == 3) {               // dY plain, B = stride-2 gather of X per (tap, ci) atom
             tma_load_3d(sa, &tmA, &full[stage], m0, k0, ba);
             tma_load_3d(sa + 8192, &tmA, &full[stage], m0 + 64, k0, ba);
@@ -354,11 +322,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               for (int t = 0; t < 16; ++t) {
                 int x, y;
                 tap_xy(p, n0 / 8 + t, gx, gy, x, y);
-                if (p.cl == 2) {
-                  if ((t & 1) == rank) tma_load_5d_mc(sb + t * 1024, &tmB, &full[stage], 0, x, y, gn, bb, MC);
-                } else {
-                  tma_load_5d(sb + t * 1024, &tmB, &full[stage], 0, x, y, gn, bb);
-                }
+                tma_load_5d(sb + t * 1024, &tmB, &full[stage], 0, x, y, gn, bb);
               }
             } else {
 #pragma unroll
@@ -366,11 +330,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 const int ncol = n0 + 64 * j, tap = ncol / p.cg, ci0 = ncol - tap * p.cg;
                 int x, y;
                 tap_xy(p, tap, gx, gy, x, y);
-                if (p.cl == 2) {       // atoms split between the pair (BN >= 128)
-                  if ((j & 1) == rank) tma_load_5d_mc(sb + j * 8192, &tmB, &full[stage], ci0, x, y, gn, bb, MC);
-                } else {
-                  tma_load_5d(sb + j * 8192, &tmB, &full[stage], ci0, x, y, gn, bb);
-                }
+                tma_load_5d(sb + j * 8192, &tmB, &full[stage], ci0, x, y, gn, bb);
               }
             }
           } else if constexpr (CONV == 4) {               // A = stride-2 gather of dY per (tap, co) atom, X plain
@@ -393,11 +353,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               }
             }
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) {
-              if (p.cl == 2)
-                tma_load_3d_mc(sb + j * 8192 + rank * 4096, &tmB, &full[stage], n0 + 64 * j, k0 + 32 * rank, bb, MC);
-              else tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
-            }
+            for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
           } else if (EPI == 2 && kb >= nkb1) {            // second K segment (K-major A2, B2)
             const int k2 = (kb - nkb1) * BK;
             tma_load_3d(sa, &tmA2, &full[stage], k2, m0, b);
@@ -430,9 +386,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     uint32_t acc_phase = 0;
     int64_t bkey = -1;
     uint32_t epoch = 0;
-    for (int64_t t = tfirst; t < total; t += tstep) {
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
       int mt_, nt_, split, b_;
-      tile_coords((uint32_t)t, p, mt_, nt_, split, b_, rank);
+      tile_coords((uint32_t)t, p, mt_, nt_, split, b_);
       (void)mt_;
       if constexpr (BRES) {
         const int bb_ = p.b_shared ? 0 : b_;
@@ -478,8 +434,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             tc_mma_ss(d_tmem, ad0 + (uint64_t)k * AST, bd0 + (uint64_t)k * BST, idesc,
                       (kb | k) != 0 ? 1u : 0u);
           }
-          if (p.cl == 2) tc_commit_mc(&empty[stage], MC);   // both CTAs' slots (the pair shares B)
-          else tc_commit_w(&empty[stage]);             // smem slot free once these MMAs retire
+          tc_commit_w(&empty[stage]);                  // smem slot free once these MMAs retire
           if (kb == nkb - 1) tc_commit_w(&tfull[acc]);   // accumulator ready
         }
         __syncwarp();
@@ -489,7 +444,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       __syncwarp();
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-  } else if (warp >= 2 && warp < 2 + NEPI_ALL) {
+  } else {
     // ============================== epilogue ==============================
     const int ew = warp - 2;                      // 0 .. NEPI_ALL-1
     const int grp = ew / NEPI;                    // this warp's group takes tiles of local parity grp
@@ -509,9 +464,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     int estage = 0;                               // stage counter mirrored from the producer (mask_kb >= 0)
     const bool mask_smem = EPI == 2 && p.mask_kb >= 0;
     int64_t li = 0;                               // local tile ordinal
-    for (int64_t t = tfirst; t < total; t += tstep, ++li) {
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++li) {
       int mt, nt, split, b;
-      tile_coords((uint32_t)t, p, mt, nt, split, b, rank);
+      tile_coords((uint32_t)t, p, mt, nt, split, b);
       int tile_nkb = 0;
       if (mask_smem) {
         const int64_t kbeg_ = (int64_t)split * p.k_chunk, kend_ = min(p.K, kbeg_ + p.k_chunk);
@@ -804,7 +759,6 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   if (warp >= 2 && lane == 0) tma_store_wait_read<0>();
   tc_fence_before();
   __syncthreads();
-  if (p.cl == 2) cluster_sync_all();            // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
@@ -961,15 +915,6 @@ hfta_status img_map(CUtensorMap* m, const ConvTcP& p, int nb, int rows, int st) 
   return make_map_nd(m, p.img, 5, dims, str, box, es, !narrow);
 }
 
-// CTA-pair multicast of the shared B tile in the conv modes (opt-in: env HFTA_CONV_PAIRS=1)
-bool conv_pairs_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("HFTA_CONV_PAIRS");    // measured: no gain (not the shared operand)
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 template <int CONV, bool A_MN, bool B_MN, int BN, bool OUT_F32, bool NARROW = false>
 hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   constexpr int STAGES = (BN == 256) ? 3 : (BN == 32 ? 7 : 4);
@@ -982,26 +927,16 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   const int nbo = cp.opd_bs == 0 ? 1 : cp.B;
   hfta_status st = HFTA_OK;
   const int ks = cp.ks > 0 ? cp.ks : 4, cs = cp.ks > 0 ? cp.cs : 2, cpd = cp.ks > 0 ? cp.cpad : 1;
-  // CTA pairs sharing the B tile (each CTA loads half of it and multicasts): the
-  // m-tiles of a pair take the same model / n-tile / split.  Modes 3, 4 pair only
-  // with an even m-tile count (their odd partner would be a wasted tile).
-  const int tiles_m = (int)cdiv(cp.M, BM);
-  int cl = 1;
-  if (conv_pairs_enabled() && tiles_m >= 2 && num_sms() >= 2 &&
-      (CONV == 1 || CONV == 2 || CONV == 5 || tiles_m % 2 == 0))
-    cl = 2;
-  const uint32_t kh = cl == 2 ? 32 : 64;                  // k rows of an MN-major B box (half an atom when paired)
-  const uint32_t nb = cl == 2 ? BN / 2 : BN;              // n rows of a K-major B box
   if (CONV == 1) {
     st = img_map(&ta, cp, nbi, BM, cs);
     if (!st && B_MN && cp.wflip) {   // W [Ca][taps][Cn] as {Cn, taps, Ca, B}: one tap's 64 x 64 MN-major atom
       const int64_t cn = cp.w_cn, ca = cp.w_ca, T = (int64_t)ks * ks, wbs = nbo > 1 ? cp.opd_bs : T * cn * ca;
       const int64_t dims[4] = {cn, T, ca, nbo}, str[4] = {1, cn, T * cn, wbs};
-      const uint32_t box[4] = {64, 1, kh, 1}, es[4] = {1, 1, 1, 1};
+      const uint32_t box[4] = {64, 1, 64, 1}, es[4] = {1, 1, 1, 1};
       st = make_map_nd(&tb, cp.opd, 4, dims, str, box, es);
     } else if (!st) {
-      st = B_MN ? make_map(&tb, cp.opd, cp.N, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, kh)
-                : make_map(&tb, cp.opd, cp.K, cp.N, cp.opd_ld, cp.opd_bs, nbo, BK, nb);
+      st = B_MN ? make_map(&tb, cp.opd, cp.N, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, BK)
+                : make_map(&tb, cp.opd, cp.K, cp.N, cp.opd_ld, cp.opd_bs, nbo, BK, BN);
     }
   } else if (CONV == 2) {
     st = img_map(&ta, cp, nbi, BM, 1);
@@ -1009,23 +944,23 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
       const int64_t cn = cp.w_cn, ca = cp.w_ca, wbs = nbo > 1 ? cp.opd_bs : 16 * cn * ca;
       if (B_MN) {        // Conv2d weights W [Ca][16][Cn] (n = ci contiguous, k = co)
         const int64_t dims[4] = {cn, 16, ca, nbo}, str[4] = {1, cn, 16 * cn, wbs};
-        const uint32_t box[4] = {64, 1, kh, 1}, es[4] = {1, 1, 1, 1};
+        const uint32_t box[4] = {64, 1, 64, 1}, es[4] = {1, 1, 1, 1};
         st = make_map_nd(&tb, cp.opd, 4, dims, str, box, es);
       } else {           // ConvT2d weights Wt [16][Cn][Ca] (rows n = co, k = ci contiguous)
         const int64_t dims[4] = {ca, cn, 16, nbo}, str[4] = {1, ca, cn * ca, wbs};
-        const uint32_t box[4] = {64, nb, 1, 1}, es[4] = {1, 1, 1, 1};
+        const uint32_t box[4] = {64, (uint32_t)BN, 1, 1}, es[4] = {1, 1, 1, 1};
         st = make_map_nd(&tb, cp.opd, 4, dims, str, box, es);
       }
     }
   } else if (CONV == 5) {
     st = img_map(&ta, cp, nbi, BM, 1);
-    if (!st) st = make_map(&tb, cp.opd, cp.K, cp.N, cp.opd_ld, cp.opd_bs, nbo, BK, nb);
+    if (!st) st = make_map(&tb, cp.opd, cp.K, cp.N, cp.opd_ld, cp.opd_bs, nbo, BK, BN);
   } else if (CONV == 3) {
     st = make_map(&ta, cp.opd, cp.M, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, BK);
     if (!st) st = img_map(&tb, cp, nbi, BK, cs);
   } else {
     st = img_map(&ta, cp, nbi, BK, cs);
-    if (!st) st = make_map(&tb, cp.opd, cp.N, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, kh);
+    if (!st) st = make_map(&tb, cp.opd, cp.N, cp.K, cp.opd_ld, cp.opd_bs, nbo, 64, BK);
   }
   if (st) return st;
   tc_ = tb;
@@ -1047,8 +982,7 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   a.b_shared = (CONV == 3) ? (nbi == 1 && cp.B > 1) : (nbo == 1 && cp.B > 1);
   a.C = cp.C; a.c_bs = cp.c_bs; a.c_ld = cp.c_ld;
   a.accumulate = cp.accumulate; a.part = cp.part;
-  a.tiles_m = tiles_m; a.tiles_n = (int)cdiv(cp.N, BN);
-  a.cl = cl; a.tiles_mp = (tiles_m + 1) / 2;
+  a.tiles_m = (int)cdiv(cp.M, BM); a.tiles_n = (int)cdiv(cp.N, BN);
   a.order = (A_MN && B_MN) ? 1 : 0;
   a.mask_kb = -1;
   a.gw = cp.grid_w; a.gh = cp.grid_h; a.ghw = cp.grid_w * cp.grid_h;
@@ -1067,26 +1001,10 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   }
   auto kern = k_gemm_tc<A_MN, B_MN, BN, STAGES, OUT_F32, false, 0, CONV, NARROW>;
   ensure_smem(kern, SMEM);
-  const int64_t total = (int64_t)(cl == 2 ? a.tiles_mp : a.tiles_m) * a.tiles_n * a.splits * a.B;
-  HFTA_REQUIRE(total * cl < ((int64_t)1 << 31), HFTA_ERR_SHAPE, "conv_tc: %lld tiles exceed int32", (long long)total);
-  if (cl == 1) {
-    const int grid = (int)std::min<int64_t>(total, num_sms());
-    kern<<<grid, NTHREADS, SMEM, s>>>(ta, tb, tc_, ta, tb, a);
-  } else {                  // persistent clusters of 2 CTAs (one pair of SMs each)
-    const int grid = 2 * (int)std::min<int64_t>(total, num_sms() / 2);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid, 1, 1);
-    cfg.blockDim = dim3(NTHREADS, 1, 1);
-    cfg.dynamicSmemBytes = SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc_, ta, tb, a);
-    if (e != cudaSuccess) return fail(HFTA_ERR_CUDA, "conv_tc: cluster launch failed: %s", cudaGetErrorString(e));
-  }
+  const int64_t total = (int64_t)a.tiles_m * a.tiles_n * a.splits * a.B;
+  HFTA_REQUIRE(total < ((int64_t)1 << 31), HFTA_ERR_SHAPE, "conv_tc: %lld tiles exceed int32", (long long)total);
+  const int grid = (int)std::min<int64_t>(total, num_sms());
+  kern<<<grid, NTHREADS, SMEM, s>>>(ta, tb, tc_, ta, tb, a);
   count_launches(1);
   return post_launch(s, "conv_tc");
 }
