@@ -229,7 +229,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
   if (warp == 0) {
     // ============================ TMA producer ============================
-    if (lane == 0) {
+    // the whole warp runs the loop (warp-uniform values in uniform registers);
+    // one elected lane issues each TMA / expect_tx
+    {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
       int stage = 0;
@@ -251,18 +253,49 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const int64_t key = (int64_t)bb * p.tiles_n + nt;
           if (key != bkey) {                       // new (model, n-tile): reload the resident B
             if (bkey >= 0) { mbar_wait(bempty, (epoch - 1) & 1); }
-            mbar_expect_tx(bfull, (uint32_t)nkb * B_BYTES);
+            mbar_expect_tx_w(bfull, (uint32_t)nkb * B_BYTES);
             for (int kb = 0; kb < nkb; ++kb)
-              tma_load_3d(bres + kb * B_BYTES, &tmB, bfull, (int)(kbeg + (int64_t)kb * BK), n0, bb);
+              tma_load_3d_w(bres + kb * B_BYTES, &tmB, bfull, (int)(kbeg + (int64_t)kb * BK), n0, bb);
             bkey = key;
             ++epoch;
           }
         }
+        // per-k-block address math without divisions (the producer thread's
+        // instruction count bounds the small-N tiles): k-block kb = (tap ktap,
+        // channel block kcb), advanced incrementally; a tap's image offsets are
+        // recomputed only when the tap changes, per-tile invariants hoisted
+        int ktap = 0, kcb = 0, tx = 0, ty = 0, ttap = 0;
+        bool new_tap = true;
+        int jtap[BN / 64 > 0 ? BN / 64 : 1], jci[BN / 64 > 0 ? BN / 64 : 1];
+        if constexpr (CONV == 3 && !NARROW) {
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) {
+            const int ncol = n0 + 64 * j;
+            jtap[j] = ncol / p.cg;
+            jci[j] = ncol - jtap[j] * p.cg;
+          }
+        }
+        (void)jtap; (void)jci; (void)tx; (void)ty; (void)ttap; (void)new_tap;
         for (int kb = 0; kb < nkb; ++kb) {
+          if constexpr (CONV == 1 || CONV == 2 || CONV == 5) {
+            if (new_tap) {
+              if constexpr (CONV == 1) {
+                tap_xy(p, ktap, gx0, gy0, tx, ty);
+              } else if constexpr (CONV == 2) {
+                int kh, oh, kw, ow;
+                phase_tap(split >> 1, ktap >> 1, kh, oh);
+                phase_tap(split & 1, ktap & 1, kw, ow);
+                tx = gx0 + ow; ty = gy0 + oh; ttap = kh * 4 + kw;
+              } else {
+                tx = gx0 + ktap % 3 - 1; ty = gy0 + ktap / 3 - 1;
+              }
+              new_tap = false;
+            }
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(&full[stage], (CSUM && p.ab_same) ? A_BYTES : LOAD_BYTES);
+          mbar_expect_tx_w(&full[stage], (CSUM && p.ab_same) ? A_BYTES : LOAD_BYTES);
           (void)sb;
           const int k0 = (int)(kbeg + (int64_t)kb * BK);
           if constexpr (CONV == 1 && NARROW) {            // 8 taps of an 8-channel image per k-block
@@ -270,51 +303,44 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             for (int t8 = 0; t8 < 8; ++t8) {
               int x, y;
               tap_xy(p, kb * 8 + t8, gx0, gy0, x, y);
-              tma_load_5d(sa + t8 * 2048, &tmA, &full[stage], 0, x, y, gn0, ba);
+              tma_load_5d_w(sa + t8 * 2048, &tmA, &full[stage], 0, x, y, gn0, ba);
             }
             if constexpr (B_MN) {
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
+              for (int j = 0; j < BN / 64; ++j) tma_load_3d_w(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
             } else {
-              tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
+              tma_load_3d_w(sb, &tmB, &full[stage], k0, n0, bb);
             }
           } else if constexpr (CONV == 1) {               // strided gather of the input image
-            const int tap = kb / p.cblk, cb = kb - tap * p.cblk;
-            int x, y;
-            tap_xy(p, tap, gx0, gy0, x, y);
-            tma_load_5d(sa, &tmA, &full[stage], cb * 64, x, y, gn0, ba);
+            const int tap = ktap, cb = kcb;
+            tma_load_5d_w(sa, &tmA, &full[stage], cb * 64, tx, ty, gn0, ba);
             if constexpr (B_MN) {
               if (p.wflip) {                              // Conv dgrad (stride 1): B(n = ci, k = (t, co)) = W[co][T-1-t][ci]
 #pragma unroll
                 for (int j = 0; j < BN / 64; ++j)
-                  tma_load_4d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, p.taps - 1 - tap, cb * 64, bb);
+                  tma_load_4d_w(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, p.taps - 1 - tap, cb * 64, bb);
               } else {                                    // ConvT dgrad: B(n = ci, k = (tap, co)) = Wt[tap][co][ci]
 #pragma unroll
-                for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
+                for (int j = 0; j < BN / 64; ++j) tma_load_3d_w(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
               }
             } else {
-              tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
+              tma_load_3d_w(sb, &tmB, &full[stage], k0, n0, bb);
             }
           } else if constexpr (CONV == 2) {               // sub-pixel phase `split`, tap t of 4
-            const int t4 = kb / p.cblk, cb = kb - t4 * p.cblk;
-            int kh, oh, kw, ow;
-            phase_tap(split >> 1, t4 >> 1, kh, oh);
-            phase_tap(split & 1, t4 & 1, kw, ow);
-            tma_load_5d(sa, &tmA, &full[stage], cb * 64, gx0 + ow, gy0 + oh, gn0, ba);
-            const int tap = kh * 4 + kw;
+            const int cb = kcb, tap = ttap;
+            tma_load_5d_w(sa, &tmA, &full[stage], cb * 64, tx, ty, gn0, ba);
             if constexpr (B_MN) {
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j) tma_load_4d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, tap, cb * 64, bb);
+              for (int j = 0; j < BN / 64; ++j) tma_load_4d_w(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, tap, cb * 64, bb);
             } else {
-              tma_load_4d(sb, &tmB, &full[stage], cb * 64, n0, tap, bb);
+              tma_load_4d_w(sb, &tmB, &full[stage], cb * 64, n0, tap, bb);
             }
           } else if constexpr (CONV == 5) {               // shifted box (dy, dx) of 9, phase-merged weights
-            const int t9 = kb / p.cblk, cb = kb - t9 * p.cblk;
-            tma_load_5d(sa, &tmA, &full[stage], cb * 64, gx0 + t9 % 3 - 1, gy0 + t9 / 3 - 1, gn0, ba);
-            tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
+            tma_load_5d_w(sa, &tmA, &full[stage], kcb * 64, tx, ty, gn0, ba);
+            tma_load_3d_w(sb, &tmB, &full[stage], k0, n0, bb);
           } else if constexpr (CONV == 3) {               // dY plain, B = stride-2 gather of X per (tap, ci) atom
-            tma_load_3d(sa, &tmA, &full[stage], m0, k0, ba);
-            tma_load_3d(sa + 8192, &tmA, &full[stage], m0 + 64, k0, ba);
+            tma_load_3d_w(sa, &tmA, &full[stage], m0, k0, ba);
+            tma_load_3d_w(sa + 8192, &tmA, &full[stage], m0 + 64, k0, ba);
             int gn, gy, gx;
             grid_pos((uint32_t)k0, p, gn, gy, gx);
             if constexpr (NARROW) {                       // 16 taps x 8 channels = one 128-column tile
@@ -322,15 +348,14 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               for (int t = 0; t < 16; ++t) {
                 int x, y;
                 tap_xy(p, n0 / 8 + t, gx, gy, x, y);
-                tma_load_5d(sb + t * 1024, &tmB, &full[stage], 0, x, y, gn, bb);
+                tma_load_5d_w(sb + t * 1024, &tmB, &full[stage], 0, x, y, gn, bb);
               }
             } else {
 #pragma unroll
               for (int j = 0; j < BN / 64; ++j) {
-                const int ncol = n0 + 64 * j, tap = ncol / p.cg, ci0 = ncol - tap * p.cg;
                 int x, y;
-                tap_xy(p, tap, gx, gy, x, y);
-                tma_load_5d(sb + j * 8192, &tmB, &full[stage], ci0, x, y, gn, bb);
+                tap_xy(p, jtap[j], gx, gy, x, y);
+                tma_load_5d_w(sb + j * 8192, &tmB, &full[stage], jci[j], x, y, gn, bb);
               }
             }
           } else if constexpr (CONV == 4) {               // A = stride-2 gather of dY per (tap, co) atom, X plain
@@ -341,7 +366,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               for (int t = 0; t < 16; ++t) {
                 int x, y;
                 tap_xy(p, m0 / 8 + t, gx, gy, x, y);
-                tma_load_5d(sa + t * 1024, &tmA, &full[stage], 0, x, y, gn, ba);
+                tma_load_5d_w(sa + t * 1024, &tmA, &full[stage], 0, x, y, gn, ba);
               }
             } else {
 #pragma unroll
@@ -349,32 +374,33 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 const int mm = m0 + 64 * j, tap = mm / p.cg, co0 = mm - tap * p.cg;
                 int x, y;
                 tap_xy(p, tap, gx, gy, x, y);
-                tma_load_5d(sa + j * 8192, &tmA, &full[stage], co0, x, y, gn, ba);
+                tma_load_5d_w(sa + j * 8192, &tmA, &full[stage], co0, x, y, gn, ba);
               }
             }
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
+            for (int j = 0; j < BN / 64; ++j) tma_load_3d_w(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
           } else if (EPI == 2 && kb >= nkb1) {            // second K segment (K-major A2, B2)
             const int k2 = (kb - nkb1) * BK;
-            tma_load_3d(sa, &tmA2, &full[stage], k2, m0, b);
-            if constexpr (!BRES) tma_load_3d(sb, &tmB2, &full[stage], k2, n0, b);
+            tma_load_3d_w(sa, &tmA2, &full[stage], k2, m0, b);
+            if constexpr (!BRES) tma_load_3d_w(sb, &tmB2, &full[stage], k2, n0, b);
           } else if (A_MN) {
-            tma_load_3d(sa, &tmA, &full[stage], m0, k0, ba);
-            tma_load_3d(sa + 8192, &tmA, &full[stage], m0 + 64, k0, ba);
+            tma_load_3d_w(sa, &tmA, &full[stage], m0, k0, ba);
+            tma_load_3d_w(sa + 8192, &tmA, &full[stage], m0 + 64, k0, ba);
           } else {
-            tma_load_3d(sa, &tmA, &full[stage], k0, m0, ba);
+            tma_load_3d_w(sa, &tmA, &full[stage], k0, m0, ba);
           }
           if (CONV != 0 || (EPI == 2 && kb >= nkb1)) {
           } else if (CSUM && p.ab_same) {                 // Gram: the A tile is also B
           } else if constexpr (!BRES) {
             if (B_MN) {
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
+              for (int j = 0; j < BN / 64; ++j) tma_load_3d_w(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0, bb);
             } else {
-              tma_load_3d(sb, &tmB, &full[stage], k0, n0, bb);
+              tma_load_3d_w(sb, &tmB, &full[stage], k0, n0, bb);
             }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++kcb == p.cblk) { kcb = 0; ++ktap; new_tap = true; }
         }
       }
     }
