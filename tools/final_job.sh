@@ -3,7 +3,7 @@
 # reference arm, ncu launch lists with tensor-pipe activity and DRAM bytes.
 # Outputs: gpurun_out/final3/.
 set -x
-O=gpurun_out/final4
+O=gpurun_out/final5
 mkdir -p $O
 python bench.py > $O/bench_cls_bf16.json 2> $O/bench_cls_bf16.err
 python bench.py --no-serial --no-cpu-baseline > $O/bench_cls_bf16_b.json 2> $O/bench_cls_bf16_b.err
