@@ -24,6 +24,8 @@ ACT_NONE, ACT_RELU, ACT_LEAKY_RELU, ACT_TANH, ACT_SIGMOID = 0, 1, 2, 3, 4
 STATUS = {0: "HFTA_OK", 1: "HFTA_ERR_INVALID_VALUE", 2: "HFTA_ERR_SHAPE", 3: "HFTA_ERR_ALIGNMENT",
           4: "HFTA_ERR_UNSUPPORTED", 5: "HFTA_ERR_ARCH", 6: "HFTA_ERR_WORKSPACE", 7: "HFTA_ERR_CUDA",
           8: "HFTA_ERR_NOT_INITIALIZED"}
+(HFTA_ERR_INVALID_VALUE, HFTA_ERR_SHAPE, HFTA_ERR_ALIGNMENT, HFTA_ERR_UNSUPPORTED, HFTA_ERR_ARCH, HFTA_ERR_WORKSPACE,
+ HFTA_ERR_CUDA, HFTA_ERR_NOT_INITIALIZED) = range(1, 9)
 
 
 class HftaError(RuntimeError):

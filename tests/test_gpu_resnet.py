@@ -185,3 +185,33 @@ def test_resnet18_step_narrow_b3(dtype):
     """Narrow widths (the fused operators at other channel counts), B = 3."""
     net, loss, res, hp = run_resnet(dtype, B=3, N=6, widths=(16, 32, 32, 64), seed=1)
     _check(dtype, net, loss, res, 3)
+
+
+def test_pool_and_gated_conv_errors():
+    """Validation before any launch: bad pooling geometry, non-dense layouts,
+    a dgrad gate with an activation other than ReLU / LeakyReLU."""
+    import paper_2102_02344_b200.hfta as H
+    st = torch.cuda.current_stream().cuda_stream
+    X = torch.zeros(1, 2, 8, 8, 16, dtype=torch.bfloat16, device="cuda")
+    Y = torch.zeros(1, 2, 4, 4, 16, dtype=torch.bfloat16, device="cuda")
+    am = torch.zeros(1, 2, 4, 4, 16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(H.HftaError) as e:          # pad > k / 2
+        H.hfta_maxpool2d_fwd(1, 2, 8, 8, 16, 3, 2, 2, H.HFTA_BF16, H.tin(X, X[0].numel(), 16),
+                             H.tout(Y, Y[0].numel(), 16), H.ptr(am), am[0].numel(), st)
+    assert e.value.code == H.HFTA_ERR_SHAPE
+    with pytest.raises(H.HftaError) as e:          # ld != C (not dense NHWC)
+        H.hfta_maxpool2d_fwd(1, 2, 8, 8, 16, 3, 2, 1, H.HFTA_BF16, H.tin(X, X[0].numel(), 32),
+                             H.tout(Y, Y[0].numel(), 16), H.ptr(am), am[0].numel(), st)
+    assert e.value.code == H.HFTA_ERR_SHAPE
+    with pytest.raises(H.HftaError) as e:          # B = 0
+        H.hfta_avgpool2d_fwd(0, 2, 64, 16, H.HFTA_BF16, H.tin(X, 0, 16), H.tout(Y, 16, 16), st)
+    assert e.value.code == H.HFTA_ERR_INVALID_VALUE
+    d = H.hfta_conv_desc()
+    d.N, d.H, d.W, d.C_in, d.C_out, d.kh, d.kw, d.stride, d.pad, d.transposed = 2, 8, 8, 64, 64, 3, 3, 1, 1, 0
+    Xc = torch.zeros(1, 2, 8, 8, 64, dtype=torch.bfloat16, device="cuda")
+    Wc = torch.zeros(1, 64, 3, 3, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(H.HftaError) as e:          # Tanh is not a gate activation
+        H.hfta_fused_conv_bwd_gated(1, d, H.HFTA_BF16, H.tin(Xc, Xc[0].numel(), 64), H.tin(Xc, Xc[0].numel(), 64),
+                                    H.tin(Wc, Wc[0].numel(), 576), H.tout(Xc, Xc[0].numel(), 64), None, 0, 0,
+                                    H.ACT_TANH, 0.0, H.tin(Xc, Xc[0].numel(), 64), None, 0, st)
+    assert e.value.code == H.HFTA_ERR_UNSUPPORTED
