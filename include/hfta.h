@@ -173,6 +173,19 @@ hfta_status hfta_fused_conv_bwd_gated(int B, const hfta_conv_desc* desc, hfta_dt
                                       hfta_act dX_act, float dX_alpha, hfta_in dX_gate, void* ws, size_t ws_bytes,
                                       hfta_stream stream);
 
+/*
+ * hfta_fused_linear_fwd on the bf16 tensor-core path (X, W bf16, Y bf16; not
+ * the skinny shapes) that also writes the BatchNorm statistics of the STORED
+ * Y from its epilogue (the §8(b) `bn_partials`): colstat fp32
+ * [B][ceil(M/32)][2][N], block k = rows 32k..32k+31, [0] = sum, [1] = sum of
+ * squares (fp32 over <= 32 rows).  Size: hfta_linear_colstat_size.  Returns
+ * HFTA_ERR_UNSUPPORTED where the shape does not take that path.
+ */
+size_t hfta_linear_colstat_size(int B, int64_t M, int64_t N);
+hfta_status hfta_fused_linear_fwd_stats(int B, int64_t M, int64_t N, int64_t K, hfta_in X, hfta_in W,
+                                        const float* bias, int64_t bias_bstride, int64_t bias_ld,
+                                        int64_t bias_row_div, hfta_out Y, float* colstat, hfta_stream stream);
+
 /* ------------------------------------------------------- fused BatchNorm -- */
 /*
  * Fused BatchNorm1d/2d (App. B rows P:L1274-1278): statistics per (model b,
@@ -201,6 +214,18 @@ hfta_status hfta_fused_bn_fwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_i
  *   dX = gamma*invstd/R * (R*dz - dbeta - xhat*dgamma).
  * dgamma/dbeta fp32 at [b*gb_bstride + c] (accumulate != 0 adds).
  */
+/*
+ * hfta_fused_bn_fwd with the statistics taken from colstat (written by
+ * hfta_fused_linear_fwd_stats for the same X, R rows): per (b, c) the block
+ * sums are merged in a fixed order in fp64, mean = S1/R, biased variance =
+ * S2/R - mean^2 (clamped at 0), running statistics and save_mean /
+ * save_invstd as hfta_fused_bn_fwd; then the same apply (+ act) into Y.
+ */
+hfta_status hfta_fused_bn_fwd_colstat(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_in X, const float* gamma,
+                                      const float* beta, int64_t gb_bstride, float* running_mean, float* running_var,
+                                      float momentum, float eps, hfta_act act, float act_alpha, hfta_out Y,
+                                      float* save_mean, float* save_invstd, const float* colstat,
+                                      hfta_stream stream);
 hfta_status hfta_fused_bn_bwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_in dY, hfta_in X,
                               const float* gamma, const float* beta, int64_t gb_bstride,
                               const float* save_mean, const float* save_invstd,

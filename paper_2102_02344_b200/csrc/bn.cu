@@ -173,6 +173,40 @@ __global__ void k_bn_finalize(int B, int64_t R, int64_t C, const T* __restrict__
   if (rvar) rvar[i] = (float)((1.0 - momentum) * (double)rvar[i] + momentum * var * (double)R / (double)(R - 1));
 }
 
+// Statistics from the producing GEMM's epilogue partials (hfta_fused_linear_fwd_stats):
+// colstat[b][blk][0|1][c] = sum / sum of squares of 32 stored rows; fixed-order fp64 merge
+// (8 warps take blocks w, w + 8, ..., then warp 0 adds the 8 warp sums in order).
+__global__ void k_bn_finalize_colstat(int B, int64_t R, int64_t C, int64_t nblk, const float* __restrict__ cs,
+                                      float eps, float momentum, float* __restrict__ rmean,
+                                      float* __restrict__ rvar, float* __restrict__ smean,
+                                      float* __restrict__ sinv) {
+  __shared__ double r1[8][32], r2[8][32];
+  const int b = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  double a1 = 0.0, a2 = 0.0;
+  if (c < C)
+    for (int64_t k = w; k < nblk; k += 8) {
+      const float* q = cs + (((int64_t)b * nblk + k) * 2) * C + c;
+      a1 += (double)q[0];
+      a2 += (double)q[C];
+    }
+  r1[w][lane] = a1;
+  r2[w][lane] = a2;
+  __syncthreads();
+  if (w != 0 || c >= C) return;
+  double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) { s1 += r1[q][lane]; s2 += r2[q][lane]; }
+  const int64_t i = (int64_t)b * C + c;
+  const double mean = s1 / (double)R;
+  double var = s2 / (double)R - mean * mean;
+  if (var < 0.0) var = 0.0;
+  smean[i] = (float)mean;
+  sinv[i] = (float)(1.0 / sqrt(var + (double)eps));
+  if (rmean) rmean[i] = (float)((1.0 - momentum) * (double)rmean[i] + momentum * mean);
+  if (rvar) rvar[i] = (float)((1.0 - momentum) * (double)rvar[i] + momentum * var * (double)R / (double)(R - 1));
+}
+
 template <typename T, int VEC, int U, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_bn_apply(int64_t R, int64_t C, const T* __restrict__ X, int64_t xbs,
                                                  int64_t xld, T* __restrict__ Y, int64_t ybs, int64_t yld,
@@ -835,6 +869,36 @@ hfta_status hfta_fused_bn_fwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_i
   });
   count_launches(Y.ptr ? 3 : 2);
   return post_launch(s, "hfta_fused_bn_fwd");
+}
+
+hfta_status hfta_fused_bn_fwd_colstat(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_in X, const float* gamma,
+                                      const float* beta, int64_t gb_bstride, float* running_mean, float* running_var,
+                                      float momentum, float eps, hfta_act act, float act_alpha, hfta_out Y,
+                                      float* save_mean, float* save_invstd, const float* colstat,
+                                      hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(R >= 2 && C >= 1, HFTA_ERR_SHAPE, "bn_fwd_colstat: R=%lld (needs >= 2), C=%lld", (long long)R,
+               (long long)C);
+  HFTA_REQUIRE(X.ptr && Y.ptr && gamma && beta && save_mean && save_invstd && colstat, HFTA_ERR_INVALID_VALUE,
+               "bn_fwd_colstat: X, Y, gamma, beta, save_mean, save_invstd, colstat are required");
+  HFTA_REQUIRE(X.ld >= C && Y.ld >= C && (Y.bstride > 0 || B == 1), HFTA_ERR_SHAPE, "bn_fwd_colstat: strides");
+  cudaStream_t s = (cudaStream_t)stream;
+  k_bn_finalize_colstat<<<dim3((unsigned)cdiv(C, 32), (unsigned)B), 256, 0, s>>>(
+      B, R, C, cdiv(R, 32), colstat, eps, momentum, running_mean, running_var, save_mean, save_invstd);
+  const int vec = pick_vec(dt, C, {{X.ptr, X.ld, X.bstride}, {Y.ptr, Y.ld, Y.bstride}});
+  Geo ga = make_geo(B, R, C, vec);
+  dim3 grida(ga.colgroups, ga.chunks, B);
+  DT_DISPATCH(dt, {
+    if (vec > 1)
+      LAUNCH_P1(T, k_bn_apply_p, grida, R, C, (const T*)X.ptr, X.bstride, X.ld, (T*)Y.ptr, Y.bstride, Y.ld, gamma,
+                beta, gb_bstride, save_mean, save_invstd, (int)act, act_alpha, ga);
+    else
+      LAUNCH_V1(T, k_bn_apply, grida, R, C, (const T*)X.ptr, X.bstride, X.ld, (T*)Y.ptr, Y.bstride, Y.ld, gamma, beta,
+                gb_bstride, save_mean, save_invstd, (int)act, act_alpha, ga);
+  });
+  count_launches(2);
+  return post_launch(s, "hfta_fused_bn_fwd_colstat");
 }
 
 hfta_status hfta_fused_bn_bwd(int B, int64_t R, int64_t C, hfta_dtype dt, hfta_in dY, hfta_in X,

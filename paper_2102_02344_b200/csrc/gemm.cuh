@@ -38,6 +38,10 @@ struct GemmP {
   // constant ones operand (MN-major A, fp32-output tcgen05 path only)
   float* colsum; int64_t colsum_bs; int colsum_acc;   // colsum_acc: add into colsum
   float* colsum_part;                                 // [splits][B][M] when splits > 1
+  // BatchNorm statistics of the bf16 OUTPUT C (tcgen05 path, plain epilogue):
+  // colstat[b][blk][0|1][n] = sum / sum of squares of the stored C[b][32 blk ..
+  // 32 blk + 31][n] (32-row blocks, fp32)
+  float* colstat; int64_t colstat_bs;
 };
 
 // dt_in: operand dtype; out_f32: C is fp32 (else dt_in).

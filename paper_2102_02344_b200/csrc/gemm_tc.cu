@@ -54,6 +54,7 @@ struct TcArgs {
   int mask_kb;                       // >= 0: the gating tensor is the A tile of k-blocks mask_kb..:
                                      // read from the resident smem stage (released by the epilogue)
   float* colsum; int64_t colsum_bs; int colsum_acc; float* colsum_part;   // fused column sums of A
+  float* colstat; int64_t colstat_bs;  // BN statistics of the stored bf16 C per 32-row block (see gemm.cuh)
   int ab_same;                       // Gram X^T X (A == B, one 128-wide tile): B is read from the A stage
   // implicit-GEMM convolution geometry (CONV > 0; kernel 4x4, stride 2, pad 1)
   int gw, gh, ghw;                   // the image grid the GEMM rows (CONV 1, 2) / reduction rows (3, 4) enumerate
@@ -744,6 +745,29 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               }
               st_shared_v4(rowaddr + (((uint32_t)(hh * 4 + q) ^ sw) << 4), w4);
             }
+            if (CONV == 0 && EPI == 0 && p.colstat) {
+              // BN statistics of the values as stored: lane l sums column hh*32 + l over the
+              // warp's 32 staged rows (row r, chunk q at q ^ (r & 7); 2-B reads, conflict-free)
+              __syncwarp();
+              const int64_t row0 = (int64_t)mt * BM + quarter * 32;
+              const int nrow = (int)min((int64_t)32, p.M - row0);
+              const int64_t col = c0 + lane;
+              if (nrow > 0 && col < p.N) {
+                const uint32_t base = smem_u32(buf) + (uint32_t)((lane & 7) * 2);
+                const uint32_t qc = (uint32_t)(hh * 4 + (lane >> 3));
+                float s1 = 0.f, s2 = 0.f;
+                for (int r = 0; r < nrow; ++r) {
+                  unsigned short u;
+                  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(u) : "r"(base + r * 128 + ((qc ^ (uint32_t)(r & 7)) << 4)));
+                  const float x = __uint_as_float((uint32_t)u << 16);
+                  s1 += x;
+                  s2 = fmaf(x, x, s2);
+                }
+                float* cs = p.colstat + (int64_t)b * p.colstat_bs + (row0 / 32) * 2 * p.N + col;
+                cs[0] = s1;
+                cs[p.N] = s2;
+              }
+            }
             if (hh == 1) {
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
               __syncwarp();
@@ -842,6 +866,7 @@ hfta_status launch_tc(const GemmP& p, cudaStream_t s) {
   a.mask_act = p.mask_act; a.mask_alpha = p.mask_alpha;
   a.K2 = EPI == 2 ? p.K2 : 0;
   a.colsum = p.colsum; a.colsum_bs = p.colsum_bs; a.colsum_acc = p.colsum_acc; a.colsum_part = p.colsum_part;
+  a.colstat = OUT_F32 ? nullptr : p.colstat; a.colstat_bs = p.colstat_bs;
   a.mask_kb = -1;
   // Gram X^T X of one 128-wide tile: load the tile once, use it as both operands
   a.ab_same = (A_MN && B_MN && OUT_F32 && BN == 128 && p.A == p.Bm && p.a_ld == p.b_ld && p.a_bs == p.b_bs &&

@@ -107,6 +107,38 @@ hfta_status hfta_fused_linear_fwd(int B, int64_t M, int64_t N, int64_t K, hfta_d
   return run_gemm(p, mixed ? HFTA_BF16 : dt, mixed, (cudaStream_t)stream);
 }
 
+size_t hfta_linear_colstat_size(int B, int64_t M, int64_t N) {
+  if (B < 1 || M < 1 || N < 1) return 0;
+  return (size_t)B * cdiv(M, 32) * 2 * N * sizeof(float);
+}
+
+hfta_status hfta_fused_linear_fwd_stats(int B, int64_t M, int64_t N, int64_t K, hfta_in X, hfta_in W,
+                                        const float* bias, int64_t bias_bstride, int64_t bias_ld,
+                                        int64_t bias_row_div, hfta_out Y, float* colstat, hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_CHECK_B(B);
+  HFTA_REQUIRE(M >= 1 && N >= 1 && K >= 1 && colstat, HFTA_ERR_INVALID_VALUE,
+               "linear_fwd_stats: M,N,K = %lld,%lld,%lld, colstat %p", (long long)M, (long long)N, (long long)K,
+               (void*)colstat);
+  if (hfta_status st = check_in(X, "X", B)) return st;
+  if (hfta_status st = check_in(W, "W", B)) return st;
+  if (hfta_status st = check_out(Y, "Y", B)) return st;
+  HFTA_REQUIRE(X.ld >= K && W.ld >= K && Y.ld >= N, HFTA_ERR_SHAPE, "linear_fwd_stats: ld < extent");
+  GemmP p{};
+  p.B = B; p.M = M; p.N = N; p.K = K;
+  p.A = X.ptr; p.a_bs = X.bstride; p.a_ld = X.ld; p.a_kmajor = 1;
+  p.Bm = W.ptr; p.b_bs = W.bstride; p.b_ld = W.ld; p.b_kmajor = 1;
+  p.C = Y.ptr; p.c_bs = Y.bstride; p.c_ld = Y.ld;
+  p.bias = bias; p.bias_bs = bias_bstride; p.bias_ld = bias_ld;
+  p.bias_div = (bias_ld > 0 && bias_row_div > 0) ? bias_row_div : 0;
+  p.splits = 1; p.k_chunk = cdiv(K, 16) * 16;
+  p.colstat = colstat; p.colstat_bs = cdiv(M, 32) * 2 * N;
+  HFTA_REQUIRE(!skinny_fwd_ok(p) && gemm_tc_supported(p, HFTA_BF16, false), HFTA_ERR_UNSUPPORTED,
+               "linear_fwd_stats: the statistics ride on the bf16 tensor-core epilogue (K %lld, N %lld not eligible)",
+               (long long)K, (long long)N);
+  return gemm_tc(p, HFTA_BF16, false, (cudaStream_t)stream);
+}
+
 size_t hfta_fused_linear_bwd_workspace(int B, int64_t M, int64_t N, int64_t K, hfta_dtype dt) {
   if (B < 1 || M < 1 || N < 1 || K < 1) return 0;
   Split sp = wgrad_split(B, M, N, K);

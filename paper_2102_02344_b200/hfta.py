@@ -58,6 +58,10 @@ _SIGS = {
     "hfta_fused_linear_bwd_workspace": (sz, [i32, i64, i64, i64, i32]),
     "hfta_fused_linear_bwd": (i32, [i32, i64, i64, i64, i32, hfta_in, hfta_in, hfta_in, hfta_out, vp, i64, i64, vp,
                                     i64, i32, vp, sz, vp]),
+    "hfta_linear_colstat_size": (sz, [i32, i64, i64]),
+    "hfta_fused_linear_fwd_stats": (i32, [i32, i64, i64, i64, hfta_in, hfta_in, vp, i64, i64, i64, hfta_out, vp, vp]),
+    "hfta_fused_bn_fwd_colstat": (i32, [i32, i64, i64, i32, hfta_in, vp, vp, i64, vp, vp, f32, f32, i32, f32, hfta_out,
+                                        vp, vp, vp, vp]),
     "hfta_fused_bn_workspace": (sz, [i32, i64, i64]),
     "hfta_fused_bn_fwd": (i32, [i32, i64, i64, i32, hfta_in, vp, vp, i64, vp, vp, f32, f32, i32, f32, hfta_out, vp,
                                 vp, vp, sz, vp]),

@@ -192,6 +192,15 @@ class FusedNet:
                             act, self.act_alpha, _out(Y) if Y is not None else H.tout(None, 0, 1), H.ptr(sm), H.ptr(si),
                             self.ws.ptr, self.ws.nbytes, s)
 
+    def _bn_fwd_colstat(self, X, name, act, Y, colstat, s):
+        """BN forward whose statistics come from the producing GEMM's epilogue."""
+        R, C = X.shape[1], X.shape[2]
+        rm, rv = self.running[name]
+        sm, si = self.saved[name]
+        H.hfta_fused_bn_fwd_colstat(self.B, R, C, self._dt(X), _in(X), self.arena.fptr("p", name + ".g"),
+                                    self.arena.fptr("p", name + ".beta"), self.arena.P, H.ptr(rm), H.ptr(rv), 0.1,
+                                    1e-5, act, self.act_alpha, _out(Y), H.ptr(sm), H.ptr(si), colstat, s)
+
     def _bn_bwd(self, dY, X, name, act, dX, s):
         R, C = X.shape[1], X.shape[2]
         sm, si = self.saved[name]

@@ -10,6 +10,8 @@ model-major [B][rows][C] with C contiguous (rows = N*L points).
 
 Per-model results are unfused with `params(b)` / `arena.host_tensor`.
 """
+import os
+
 import numpy as np
 import torch
 
@@ -109,6 +111,10 @@ class FusedPointNet(FusedNet):
             kpad = (self.k + 15) // 16 * 16          # logits ld: 16-element aligned rows
             S["seg.u"] = f(N, h1)                   # g Wg^T + b: per-sample bias table of the split weight
             S["seg.y1"], S["seg.h1"] = a(R, h1), a(R, h1)
+            # BN statistics from the head GEMMs' epilogues (bf16; HFTA_SEG_COLSTAT=0 disables)
+            self._colstat = (torch.empty(H.hfta_linear_colstat_size(B, R, max(h1, h2, h3)) // 4, dtype=torch.float32,
+                                         device=self.device)
+                             if self.dt == H.HFTA_BF16 and os.environ.get("HFTA_SEG_COLSTAT", "1") != "0" else None)
             S["seg.y2"], S["seg.h2"] = a(R, h2), a(R, h2)
             S["seg.y3"], S["seg.h3"] = a(R, h3), a(R, h3)
             S["seg.logits"], S["d.logits"] = a(R, kpad), a(R, kpad)
@@ -446,13 +452,30 @@ class FusedPointNet(FusedNet):
         wld = c3 + c1
         H.hfta_fused_linear_fwd(B, N, h1, c3, H.HFTA_F32, _in(S["feat.g"]), ar.w_in("head.c1.W", H.HFTA_F32, 0, wld),
                                 ar.fptr("p", "head.c1.b"), P, 0, 0, _out(S["seg.u"]), s)
-        H.hfta_fused_linear_fwd(B, R, h1, c1, self.dt, _in(S[self.pf_key]), ar.w_in("head.c1.W", self.dt, c3, wld),
-                                H.ptr(S["seg.u"]), N * h1, h1, L, _out(S["seg.y1"]), s)
-        self._bn_fwd(S["seg.y1"], "head.bn1", A_RELU, S["seg.h1"], s)
-        self._lin_fwd(_in(S["seg.h1"]), R, "head.c2", S["seg.y2"], s)
-        self._bn_fwd(S["seg.y2"], "head.bn2", A_RELU, S["seg.h2"], s)
-        self._lin_fwd(_in(S["seg.h2"]), R, "head.c3", S["seg.y3"], s)
-        self._bn_fwd(S["seg.y3"], "head.bn3", A_RELU, S["seg.h3"], s)
+        if self._colstat is not None:
+            # bf16: each head GEMM's epilogue writes the BN statistics of the y it stores
+            # (hfta_fused_linear_fwd_stats), so BN skips its statistics pass over y
+            cs = H.ptr(self._colstat)
+            H.hfta_fused_linear_fwd_stats(B, R, h1, c1, _in(S[self.pf_key]), ar.w_in("head.c1.W", self.dt, c3, wld),
+                                          H.ptr(S["seg.u"]), N * h1, h1, L, _out(S["seg.y1"]), cs, s)
+            self._bn_fwd_colstat(S["seg.y1"], "head.bn1", A_RELU, S["seg.h1"], cs, s)
+            for src, name, y, bn, h in (("seg.h1", "head.c2", "seg.y2", "head.bn2", "seg.h2"),
+                                        ("seg.h2", "head.c3", "seg.y3", "head.bn3", "seg.h3")):
+                Nn, K = ar.shape[name + ".W"]
+                e0 = self._pbegin(name + ":fwd", s)
+                H.hfta_fused_linear_fwd_stats(B, R, Nn, K, _in(S[src]), ar.w_in(name + ".W", self.dt),
+                                              ar.fptr("p", name + ".b"), P, 0, 0, _out(S[y]), cs, s)
+                self._pend(e0)
+                self._bn_fwd_colstat(S[y], bn, A_RELU, S[h], cs, s)
+        else:
+            H.hfta_fused_linear_fwd(B, R, h1, c1, self.dt, _in(S[self.pf_key]),
+                                    ar.w_in("head.c1.W", self.dt, c3, wld), H.ptr(S["seg.u"]), N * h1, h1, L,
+                                    _out(S["seg.y1"]), s)
+            self._bn_fwd(S["seg.y1"], "head.bn1", A_RELU, S["seg.h1"], s)
+            self._lin_fwd(_in(S["seg.h1"]), R, "head.c2", S["seg.y2"], s)
+            self._bn_fwd(S["seg.y2"], "head.bn2", A_RELU, S["seg.h2"], s)
+            self._lin_fwd(_in(S["seg.h2"]), R, "head.c3", S["seg.y3"], s)
+            self._bn_fwd(S["seg.y3"], "head.bn3", A_RELU, S["seg.h3"], s)
         lg, dl = S["seg.logits"], S["d.logits"]
         kp = lg.shape[2]
         H.hfta_fused_linear_fwd(B, R, self.k, self.h3w, self.dt, _in(S["seg.h3"]), ar.w_in("head.c4.W", self.dt),

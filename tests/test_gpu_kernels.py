@@ -514,3 +514,56 @@ def test_fused_adadelta_and_steplr():
         ref = [steplr(float(np.float32(0.1)), float(np.float32(0.5)), 10, ep),
                steplr(float(np.float32(1e-3)), float(np.float32(0.9)), 3, ep)]
         assert np.allclose(host(out), ref, rtol=1e-6)
+
+
+@pytest.mark.parametrize("M,N,K,B", [(5000, 256, 512, 2), (777, 128, 64, 3), (80, 512, 128, 1)])
+def test_linear_fwd_stats_and_bn_from_colstat(M, N, K, B):
+    """hfta_fused_linear_fwd_stats writes the same Y as hfta_fused_linear_fwd
+    plus per-32-row column sums / sums of squares of the STORED bf16 Y; BN
+    forward from those partials matches BN forward with its own statistics
+    pass (mean / invstd 1e-5, outputs within one bf16 rounding)."""
+    code, tdt = DT["bf16"]
+    X = rounded(R.standard_normal((B, M, K)), tdt)
+    W = rounded(R.standard_normal((B, N, K)) / np.sqrt(K), tdt)
+    bias = torch.tensor(R.standard_normal((B, N)), dtype=torch.float32, device=DEV)
+    Xd, Wd = dev(X, tdt), dev(W, tdt)
+    Y1 = torch.empty(B, M, N, dtype=tdt, device=DEV)
+    Y2 = torch.empty_like(Y1)
+    cs = torch.empty(H.hfta_linear_colstat_size(B, M, N) // 4, dtype=torch.float32, device=DEV)
+    H.hfta_fused_linear_fwd(B, M, N, K, code, H.tin(Xd, M * K, K), H.tin(Wd, N * K, K), H.ptr(bias), N, 0, 0,
+                            H.tout(Y1, M * N, N), s())
+    H.hfta_fused_linear_fwd_stats(B, M, N, K, H.tin(Xd, M * K, K), H.tin(Wd, N * K, K), H.ptr(bias), N, 0, 0,
+                                  H.tout(Y2, M * N, N), H.ptr(cs), s())
+    torch.cuda.synchronize()
+    assert torch.equal(Y1, Y2)
+    y = host(Y2)
+    nblk = (M + 31) // 32
+    c = cs.view(B, nblk, 2, N).double().cpu().numpy()
+    for b in range(B):
+        for k in (0, nblk // 2, nblk - 1):
+            rows = y[b, 32 * k:min(M, 32 * k + 32)]
+            np.testing.assert_allclose(c[b, k, 0], rows.sum(0), rtol=1e-5, atol=1e-4)
+            np.testing.assert_allclose(c[b, k, 1], (rows * rows).sum(0), rtol=1e-5, atol=1e-4)
+    g = torch.tensor(R.uniform(0.5, 1.5, (B, N)), dtype=torch.float32, device=DEV)
+    be = torch.tensor(R.uniform(-0.5, 0.5, (B, N)), dtype=torch.float32, device=DEV)
+    outs = []
+    for use_cs in (False, True):
+        rm, rv = torch.zeros(B, N, device=DEV), torch.ones(B, N, device=DEV)
+        sm, si = torch.empty(B, N, device=DEV), torch.empty(B, N, device=DEV)
+        Z = torch.empty_like(Y2)
+        if use_cs:
+            H.hfta_fused_bn_fwd_colstat(B, M, N, code, H.tin(Y2, M * N, N), H.ptr(g), H.ptr(be), N, H.ptr(rm),
+                                        H.ptr(rv), 0.1, 1e-5, 1, 0.0, H.tout(Z, M * N, N), H.ptr(sm), H.ptr(si),
+                                        H.ptr(cs), s())
+        else:
+            ws = torch.empty(H.hfta_fused_bn_workspace(B, M, N), dtype=torch.uint8, device=DEV)
+            H.hfta_fused_bn_fwd(B, M, N, code, H.tin(Y2, M * N, N), H.ptr(g), H.ptr(be), N, H.ptr(rm), H.ptr(rv),
+                                0.1, 1e-5, 1, 0.0, H.tout(Z, M * N, N), H.ptr(sm), H.ptr(si), H.ptr(ws), ws.numel(),
+                                s())
+        torch.cuda.synchronize()
+        outs.append((host(Z), host(sm), host(si), host(rm), host(rv)))
+    (z0, m0, i0, rm0, rv0), (z1, m1, i1, rm1, rv1) = outs
+    assert_close(m1, m0, 1e-5, "mean")
+    assert_close(i1, i0, 1e-5, "invstd")
+    assert_close(rv1, rv0, 1e-5, "running var")
+    assert_close(z1, z0, 4e-3, "BN output")
