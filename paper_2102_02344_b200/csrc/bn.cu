@@ -802,7 +802,39 @@ size_t bn_parts_bytes(int B, int64_t R, int64_t C) {
   return align_up(2 * (size_t)B * ch * C * sizeof(double), 256);
 }
 
+// fallback of the epilogue statistics: thread = (model b, 32-row block, column)
+template <typename T>
+__global__ void k_colstat_rows(int B, int64_t M, int64_t N, const T* __restrict__ Y, int64_t ybs, int64_t yld,
+                               float* __restrict__ cs) {
+  const int64_t nblk = (M + 31) / 32;
+  const int64_t total = (int64_t)B * nblk * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = i % N, k = (i / N) % nblk, b = i / (N * nblk);
+    const T* y = Y + b * ybs + 32 * k * yld + n;
+    const int rows = (int)min((int64_t)32, M - 32 * k);
+    float s1 = 0.f, s2 = 0.f;
+    for (int r = 0; r < rows; ++r) {
+      const float x = ldf(y + r * yld);
+      s1 += x;
+      s2 = fmaf(x, x, s2);
+    }
+    float* o = cs + ((b * nblk + k) * 2) * N + n;
+    o[0] = s1;
+    o[N] = s2;
+  }
+}
+
 }  // namespace
+
+hfta_status colstat_rows(int B, int64_t M, int64_t N, hfta_dtype dt, hfta_in Y, float* colstat, cudaStream_t s) {
+  const int64_t total = (int64_t)B * ((M + 31) / 32) * N;
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 256), 148 * 16);
+  if (dt == HFTA_F32) k_colstat_rows<float><<<grid, 256, 0, s>>>(B, M, N, (const float*)Y.ptr, Y.bstride, Y.ld, colstat);
+  else k_colstat_rows<__nv_bfloat16><<<grid, 256, 0, s>>>(B, M, N, (const __nv_bfloat16*)Y.ptr, Y.bstride, Y.ld,
+                                                         colstat);
+  count_launches(1);
+  return HFTA_OK;
+}
 }  // namespace hfta
 
 using namespace hfta;

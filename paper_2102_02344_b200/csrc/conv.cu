@@ -377,8 +377,25 @@ size_t hfta_fused_conv_workspace(int B, const hfta_conv_desc* d, hfta_dtype dt) 
   return col + align_up(lin, 256);
 }
 
+static hfta_status conv_fwd_impl(int B, const hfta_conv_desc* d, hfta_dtype dt, hfta_in X, hfta_in W, hfta_out Y,
+                                 hfta_act act, float act_alpha, float* colstat, void* ws, size_t ws_bytes,
+                                 hfta_stream stream);
+
 hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* d, hfta_dtype dt, hfta_in X, hfta_in W, hfta_out Y,
                                 hfta_act act, float act_alpha, void* ws, size_t ws_bytes, hfta_stream stream) {
+  return conv_fwd_impl(B, d, dt, X, W, Y, act, act_alpha, nullptr, ws, ws_bytes, stream);
+}
+
+hfta_status hfta_fused_conv_fwd_stats(int B, const hfta_conv_desc* d, hfta_dtype dt, hfta_in X, hfta_in W,
+                                      hfta_out Y, float* colstat, void* ws, size_t ws_bytes, hfta_stream stream) {
+  if (hfta_status st = check_init()) return st;
+  HFTA_REQUIRE(colstat, HFTA_ERR_INVALID_VALUE, "conv_fwd_stats: colstat is required");
+  return conv_fwd_impl(B, d, dt, X, W, Y, HFTA_ACT_NONE, 0.f, colstat, ws, ws_bytes, stream);
+}
+
+static hfta_status conv_fwd_impl(int B, const hfta_conv_desc* d, hfta_dtype dt, hfta_in X, hfta_in W, hfta_out Y,
+                                 hfta_act act, float act_alpha, float* colstat, void* ws, size_t ws_bytes,
+                                 hfta_stream stream) {
   if (hfta_status st = check_init()) return st;
   HFTA_CHECK_B(B);
   Shape sh;
@@ -402,7 +419,12 @@ hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
     cp.act = act; cp.act_alpha = act_alpha;      // fused into the epilogue
     if (conv_tc_supported(cp)) {
       const size_t colb = col_bytes(B, d, dt, sh);
+      if (cp.mode == 1) cp.colstat = colstat;     // statistics from the TMA-store epilogue
       if (hfta_status st = run_phases(cp, col + colb, ws_bytes - colb, s)) return st;
+      if (colstat && cp.mode != 1)
+        if (hfta_status st = colstat_rows(B, (int64_t)d->N * sh.Ho * sh.Wo, d->C_out, dt,
+                                          hfta_in{Y.ptr, Y.bstride, Y.ld}, colstat, s))
+          return st;
       return post_launch(s, "hfta_fused_conv_fwd");
     }
   }
@@ -411,6 +433,10 @@ hfta_status hfta_fused_conv_fwd(int B, const hfta_conv_desc* d, hfta_dtype dt, h
     if (act != HFTA_ACT_NONE)
       if (hfta_status st = hfta_act_fwd(B, (int64_t)d->N * sh.Ho * sh.Wo, d->C_out, dt, act, act_alpha,
                                         hfta_in{Y.ptr, Y.bstride, Y.ld}, Y, stream))
+        return st;
+    if (colstat)          // statistics of the stored Y (the paths without the epilogue statistics)
+      if (hfta_status st = colstat_rows(B, (int64_t)d->N * sh.Ho * sh.Wo, d->C_out, dt,
+                                        hfta_in{Y.ptr, Y.bstride, Y.ld}, colstat, s))
         return st;
     return post_launch(s, "hfta_fused_conv_fwd");
   };

@@ -78,6 +78,7 @@ struct ConvTcP {
   int y_h, y_w;             // mode 2: output image size
   int accumulate; int splits; int64_t k_chunk; float* part;   // 3, 4: split-K over the reduction rows
   int act; float act_alpha;        // 1, 2 (forward): activation applied in the epilogue (layers without BN)
+  float* colstat;                   // mode 1: BN statistics of the stored Y per 32-row block (gemm.cuh GemmP)
   int ks, cs, cpad;         // modes 1, 3, 4: kernel size, stride, pad of the gather (0 = DCGAN's 4, 2, 1)
   int wflip;                // mode 1, w_mn: B = W [Ca][taps][Cn] read flipped (stride-1 Conv2d dgrad)
   const void* gate; int64_t gate_bs; float gate_alpha;   // mode 2: output *= (gate > 0 ? 1 : gate_alpha)
@@ -89,6 +90,10 @@ hfta_status conv_subpixel_weights(int B, int ca, int w_mn, const void* W, int64_
 hfta_status conv_tc(const ConvTcP& p, cudaStream_t s);
 // tile width along N of the wgrad modes (3, 4) conv_tc launches for p (split-K policy input)
 int conv_wgrad_bn(const ConvTcP& p);
+
+// colstat[b][blk][0|1][n] of a stored [B][M][N] activation (ld N, model stride
+// Y.bstride), 32-row blocks: the fallback of the epilogue statistics (bn.cu).
+hfta_status colstat_rows(int B, int64_t M, int64_t N, hfta_dtype dt, hfta_in Y, float* colstat, cudaStream_t s);
 
 // Dispatch: skinny -> tcgen05 -> SIMT (EPI features: skinny / tcgen05 only).
 hfta_status run_gemm(GemmP& p, hfta_dtype dt, bool out_f32, cudaStream_t s, void* ws = nullptr, size_t wsb = 0);

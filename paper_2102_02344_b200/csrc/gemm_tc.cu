@@ -745,7 +745,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               }
               st_shared_v4(rowaddr + (((uint32_t)(hh * 4 + q) ^ sw) << 4), w4);
             }
-            if (CONV == 0 && EPI == 0 && p.colstat) {
+            if ((CONV == 0 || CONV == 1) && EPI == 0 && p.colstat) {
               // BN statistics of the values as stored: lane l sums column hh*32 + l over the
               // warp's 32 staged rows (row r, chunk q at q ^ (r & 7); 2-B reads, conflict-free)
               __syncwarp();
@@ -1042,6 +1042,7 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   a.y_c = CONV == 5 ? 8 : (int)cp.N; a.y_h = cp.y_h; a.y_w = cp.y_w; a.y_bs = cp.c_bs;
   a.act = (CONV == 1 || CONV == 2 || CONV == 5) ? cp.act : HFTA_ACT_NONE; a.act_alpha = cp.act_alpha;
   a.ks = ks; a.cs = cs; a.cp = cpd; a.taps = ks * ks; a.wflip = cp.wflip;
+  if (CONV == 1 && !OUT_F32) { a.colstat = cp.colstat; a.colstat_bs = cdiv(cp.M, 32) * 2 * cp.N; }
   for (int t = 0; t < 64; ++t) {
     const int tt = t < a.taps ? t : 0;
     a.tkx[t] = (uint8_t)(tt % ks); a.tky[t] = (uint8_t)(tt / ks);

@@ -142,6 +142,11 @@ class FusedDCGAN:
         ws.reserve(H.hfta_loss_workspace(B, N))
         ws.alloc()
         self.ws = ws
+        # bf16: D's BN statistics come from the conv epilogues (HFTA_COLSTAT=0 disables)
+        import os
+        self.colstat = (torch.empty(max(H.hfta_linear_colstat_size(B, N * dsz[i + 1] ** 2, dch[i + 1])
+                                        for i in (1, 2, 3)) // 4, dtype=torch.float32, device=dev)
+                        if self.dt == H.HFTA_BF16 and os.environ.get("HFTA_COLSTAT", "1") != "0" else None)
 
     # -------------------------------------------------------- wrappers --
     @staticmethod
@@ -250,13 +255,38 @@ class FusedDCGAN:
         H.hfta_act_bwd(self.B, rows, XY.shape[-1], self.dt, act, alpha, self._in(XY), self._in(dY), self._out(dX), s)
 
     # ---------------------------------------------------------- passes --
+    def _bn_fwd_colstat(self, half, name, X, act, alpha, Y, s):
+        R, C = X[0].numel() // X.shape[-1], X.shape[-1]
+        rm, rv = half.running[name]
+        sm, si = half.saved[name]
+        ar = half.arena
+        H.hfta_fused_bn_fwd_colstat(self.B, R, C, self.dt, self._in(X), ar.fptr("p", name + ".g"),
+                                    ar.fptr("p", name + ".beta"), ar.P, H.ptr(rm), H.ptr(rv), 0.1, 1e-5, act, alpha,
+                                    self._out(Y), H.ptr(sm), H.ptr(si), H.ptr(self.colstat), s)
+
     def _D_forward(self, img_in, s):
         D = self.D
         # c1 has no BN: LeakyReLU(0.2) applied in the convolution's epilogue (dh[0] = act(y))
         self._conv_fwd(D, "c1.W", self.ddesc[0], img_in, self.dh[0], s, H.ACT_LEAKY_RELU, 0.2)
         for i in (1, 2, 3):
-            self._conv_fwd(D, "c%d.W" % (i + 1), self.ddesc[i], self._in(self.dh[i - 1]), self.dy[i], s)
-            self._bn_fwd(D, "bn%d" % (i + 1), self.dy[i], H.ACT_LEAKY_RELU, 0.2, self.dh[i], s)
+            name = "c%d.W" % (i + 1)
+            if self.colstat is not None:    # BN statistics from the implicit-GEMM conv's epilogue
+                tag = "D." + name.split(".")[0] + ":fwd"
+                e0 = None
+                if self._probe == tag:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(torch.cuda.current_stream())
+                H.hfta_fused_conv_fwd_stats(self.B, self.ddesc[i], self.dt, self._in(self.dh[i - 1]),
+                                            self._win(D, name), self._out(self.dy[i]), H.ptr(self.colstat),
+                                            self.ws.ptr, self.ws.nbytes, s)
+                if e0 is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(torch.cuda.current_stream())
+                    self._probe_ev.append((e0, e1))
+                self._bn_fwd_colstat(D, "bn%d" % (i + 1), self.dy[i], H.ACT_LEAKY_RELU, 0.2, self.dh[i], s)
+            else:
+                self._conv_fwd(D, name, self.ddesc[i], self._in(self.dh[i - 1]), self.dy[i], s)
+                self._bn_fwd(D, "bn%d" % (i + 1), self.dy[i], H.ACT_LEAKY_RELU, 0.2, self.dh[i], s)
         self._conv_fwd(D, "c5.W", self.ddesc[4], self._in(self.dh[3]), self.dy[4], s)
 
     def _D_backward(self, dlogit, img_in, s, wgrad, accumulate, need_dimg):

@@ -106,6 +106,8 @@ _SIGS = {
                                   vp]),
     "hfta_fused_conv_bwd": (i32, [i32, C.POINTER(hfta_conv_desc), i32, hfta_in, hfta_in, hfta_in, hfta_out, vp, i64,
                                   i32, vp, sz, vp]),
+    "hfta_fused_conv_fwd_stats": (i32, [i32, C.POINTER(hfta_conv_desc), i32, hfta_in, hfta_in, hfta_out, vp, vp, sz,
+                                        vp]),
     "hfta_fused_conv_bwd_gated": (i32, [i32, C.POINTER(hfta_conv_desc), i32, hfta_in, hfta_in, hfta_in, hfta_out, vp,
                                         i64, i32, i32, f32, hfta_in, vp, sz, vp]),
     "hfta_loss_bce_logits": (i32, [i32, i64, i32, hfta_in, f32, vp, vp, hfta_out, vp, sz, vp]),

@@ -135,6 +135,12 @@ class FusedResNet18:
         ws.reserve(H.hfta_fused_linear_bwd_workspace(B, N, self.k, C, self.dt))
         ws.alloc()
         self.ws = ws
+        # bf16: every BN's statistics come from its conv's epilogue (HFTA_COLSTAT=0 disables)
+        import os
+        sizes = [H.hfta_linear_colstat_size(B, N * s1 * s1, w0)] + \
+                [H.hfta_linear_colstat_size(B, N * blk["hout"] ** 2, blk["cout"]) for blk in self.blocks]
+        self.colstat = (torch.empty(max(sizes) // 4, dtype=torch.float32, device=dev)
+                        if self.dt == H.HFTA_BF16 and os.environ.get("HFTA_COLSTAT", "1") != "0" else None)
 
     # -------------------------------------------------------- wrappers --
     @staticmethod
@@ -217,6 +223,30 @@ class FusedResNet18:
                               self._out(dX) if dX is not None else H.hfta_out(None, 0, 1),
                               self.arena.fptr("g", name), self.arena.P, 0, self.ws.ptr, self.ws.nbytes, s)
 
+    def _conv_bn_fwd(self, cname, desc, X, y, bname, act, out, s):
+        """conv -> BN (-> act): with the bf16 path the BN statistics come from the
+        conv's epilogue (hfta_fused_conv_fwd_stats -> hfta_fused_bn_fwd_colstat)."""
+        if self.colstat is None:
+            self._conv_fwd(cname, desc, X, y, s)
+            self._bn_fwd(bname, y, act, out, s)
+            return
+        e0 = None
+        if self._probe == cname[:-2] + ":fwd":
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.current_stream())
+        H.hfta_fused_conv_fwd_stats(self.B, desc, self.dt, X, self._win(cname), self._out(y), H.ptr(self.colstat),
+                                    self.ws.ptr, self.ws.nbytes, s)
+        if e0 is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(torch.cuda.current_stream())
+            self._probe_ev.append((e0, e1))
+        rm, rv = self.running[bname]
+        sm, si = self.saved[bname]
+        ar = self.arena
+        H.hfta_fused_bn_fwd_colstat(self.B, self._rows(y), y.shape[-1], self.dt, self._in(y), ar.fptr("p", bname + ".g"),
+                                    ar.fptr("p", bname + ".beta"), ar.P, H.ptr(rm), H.ptr(rv), 0.1, 1e-5, act, 0.0,
+                                    self._out(out), H.ptr(sm), H.ptr(si), H.ptr(self.colstat), s)
+
     def _bn_fwd(self, name, X, act, Y, s):
         rm, rv = self.running[name]
         sm, si = self.saved[name]
@@ -241,20 +271,18 @@ class FusedResNet18:
         st = self.stem
         w0 = self.widths[0]
         img = H.tin(self.img, 0, NCP)                       # shared by all models
-        self._conv_fwd("conv1.W", st["desc"], img, st["y"], s)
-        self._bn_fwd("bn1", st["y"], H.ACT_RELU, st["a"], s)
+        self._conv_bn_fwd("conv1.W", st["desc"], img, st["y"], "bn1", H.ACT_RELU, st["a"], s)
         H.hfta_maxpool2d_fwd(self.B, self.N, st["hw"], st["hw"], w0, 3, 2, 1, self.dt, self._in(st["a"]),
                              self._out(self.h0), H.ptr(st["am"]), st["am"][0].numel(), s)
         h = self.h0
         for blk in self.blocks:
             n = blk["name"]
-            self._conv_fwd(n + ".conv1.W", blk["d1"], self._in(h), blk["y1"], s)
-            self._bn_fwd(n + ".bn1", blk["y1"], H.ACT_RELU, blk["a1"], s)
-            self._conv_fwd(n + ".conv2.W", blk["d2"], self._in(blk["a1"]), blk["y2"], s)
-            self._bn_fwd(n + ".bn2", blk["y2"], H.ACT_NONE, blk["z2"], s)
+            self._conv_bn_fwd(n + ".conv1.W", blk["d1"], self._in(h), blk["y1"], n + ".bn1", H.ACT_RELU, blk["a1"], s)
+            self._conv_bn_fwd(n + ".conv2.W", blk["d2"], self._in(blk["a1"]), blk["y2"], n + ".bn2", H.ACT_NONE,
+                              blk["z2"], s)
             if blk["down"]:
-                self._conv_fwd(n + ".down.W", blk["dd"], self._in(h), blk["yd"], s)
-                self._bn_fwd(n + ".dbn", blk["yd"], H.ACT_NONE, blk["zd"], s)
+                self._conv_bn_fwd(n + ".down.W", blk["dd"], self._in(h), blk["yd"], n + ".dbn", H.ACT_NONE,
+                                  blk["zd"], s)
                 sc = blk["zd"]
             else:
                 sc = h

@@ -208,3 +208,43 @@ def test_conv_bwd_gated(layer, act, alpha):
                               st, pd)
         ref = dx.transpose(0, 2, 3, 1) * np.where(G[b] > 0, 1.0, alpha)
         assert_close(host(dX)[b], ref, 1e-2, "%s gated dX model %d" % (name, b))
+
+
+@pytest.mark.parametrize("layer", [LAYERS[2], RESNET[2], RESNET[1], LAYERS[7], RESNET[0]],
+                         ids=["D.c3", "R.l2a", "R.l1", "G.t3-fallback", "R.stem-narrow"])
+def test_conv_fwd_stats(layer):
+    """hfta_fused_conv_fwd_stats: the same Y as hfta_fused_conv_fwd and the
+    per-32-row column sums / sums of squares of the stored Y (from the
+    implicit-GEMM epilogue, or one pass over Y on the other paths)."""
+    name, tr, Hs, Ci, Co, k, st, pd = layer
+    B, N = 2, 32
+    rng = np.random.default_rng(5)
+    Ho = (Hs - 1) * st - 2 * pd + k if tr else (Hs + 2 * pd - k) // st + 1
+    X = rnd(rng.standard_normal((B, N, Hs, Hs, Ci)), torch.bfloat16)
+    shp = (B, k, k, Co, Ci) if tr else (B, Co, k, k, Ci)
+    Wg = rnd(rng.standard_normal(shp) / np.sqrt(k * k * Ci), torch.bfloat16)
+    d = H.hfta_conv_desc()
+    d.N, d.H, d.W, d.C_in, d.C_out, d.kh, d.kw, d.stride, d.pad, d.transposed = N, Hs, Hs, Ci, Co, k, k, st, pd, tr
+    dev = lambda a: torch.tensor(a).to(torch.bfloat16).to(DEV).contiguous()
+    Xd, Wd = dev(X), dev(Wg)
+    Y1 = torch.empty(B, N, Ho, Ho, Co, dtype=torch.bfloat16, device=DEV)
+    Y2 = torch.empty_like(Y1)
+    ws = torch.empty(max(H.hfta_fused_conv_workspace(B, d, 1), 256), dtype=torch.uint8, device=DEV)
+    R = N * Ho * Ho
+    cs = torch.empty(H.hfta_linear_colstat_size(B, R, Co) // 4, dtype=torch.float32, device=DEV)
+    wbs, wld = int(np.prod(Wg.shape[1:])), (Ci if tr else k * k * Ci)
+    xe = N * Hs * Hs * Ci
+    H.hfta_fused_conv_fwd(B, d, 1, H.tin(Xd, xe, Ci), H.tin(Wd, wbs, wld), H.tout(Y1, R * Co, Co), 0, 0.0,
+                          H.ptr(ws), ws.numel(), s())
+    H.hfta_fused_conv_fwd_stats(B, d, 1, H.tin(Xd, xe, Ci), H.tin(Wd, wbs, wld), H.tout(Y2, R * Co, Co), H.ptr(cs),
+                                H.ptr(ws), ws.numel(), s())
+    torch.cuda.synchronize()
+    assert torch.equal(Y1, Y2)
+    y = host(Y2).reshape(B, R, Co)
+    nblk = (R + 31) // 32
+    c = cs.view(B, nblk, 2, Co).double().cpu().numpy()
+    for b in range(B):
+        for kb in (0, nblk // 3, nblk - 1):
+            rows = y[b, 32 * kb:min(R, 32 * kb + 32)]
+            np.testing.assert_allclose(c[b, kb, 0], rows.sum(0), rtol=1e-5, atol=1e-4)
+            np.testing.assert_allclose(c[b, kb, 1], (rows * rows).sum(0), rtol=1e-5, atol=1e-4)
