@@ -164,9 +164,10 @@ hfta_status hfta_fused_conv_bwd(int B, const hfta_conv_desc* desc, hfta_dtype dt
  * hfta_fused_conv_fwd (no activation) that also writes the BatchNorm
  * statistics of the stored Y, colstat [B][ceil(R/32)][2][C_out] with
  * R = N*Ho*Wo (layout of hfta_fused_linear_fwd_stats; size
- * hfta_linear_colstat_size(B, R, C_out)): from the TMA-store epilogue on the
- * implicit-GEMM Conv2d path, from one pass over Y elsewhere.  Feed to
- * hfta_fused_bn_fwd_colstat.
+ * hfta_linear_colstat_size(B, R, C_out)): from the implicit-GEMM epilogues
+ * (Conv2d: block k = output rows 32k..32k+31; ConvT2d sub-pixel phases: the
+ * blocks partition the rows phase by phase), from one pass over Y elsewhere.
+ * Feed to hfta_fused_bn_fwd_colstat (which only needs the block totals).
  */
 hfta_status hfta_fused_conv_fwd_stats(int B, const hfta_conv_desc* desc, hfta_dtype dt, hfta_in X, hfta_in W,
                                       hfta_out Y, float* colstat, void* ws, size_t ws_bytes, hfta_stream stream);

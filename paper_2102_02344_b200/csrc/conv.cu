@@ -419,9 +419,12 @@ static hfta_status conv_fwd_impl(int B, const hfta_conv_desc* d, hfta_dtype dt, 
     cp.act = act; cp.act_alpha = act_alpha;      // fused into the epilogue
     if (conv_tc_supported(cp)) {
       const size_t colb = col_bytes(B, d, dt, sh);
-      if (cp.mode == 1) cp.colstat = colstat;     // statistics from the TMA-store epilogue
+      // statistics from the epilogue: Conv2d (TMA store) and the sub-pixel phases (4 phases x M/32
+      // blocks = the output's 32-row blocks when M % 32 == 0; not the merged 8-channel mode)
+      const bool epi_stats = cp.mode == 1 || (cp.mode == 2 && cp.M % 32 == 0 && !merged_phases(cp));
+      if (epi_stats) cp.colstat = colstat;
       if (hfta_status st = run_phases(cp, col + colb, ws_bytes - colb, s)) return st;
-      if (colstat && cp.mode != 1)
+      if (colstat && !epi_stats)
         if (hfta_status st = colstat_rows(B, (int64_t)d->N * sh.Ho * sh.Wo, d->C_out, dt,
                                           hfta_in{Y.ptr, Y.bstride, Y.ld}, colstat, s))
           return st;

@@ -715,6 +715,41 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 dst[q] = w4;
               }
             }
+            if (p.colstat) {
+              // BN statistics of the stored values (G's ConvT forward): the warp stages its 32
+              // rows' bf16 (row = lane) and lane l sums column c0 + l; block index = (phase,
+              // 32-row block of the phase grid), so the 4 phases cover the whole output
+              const uint32_t srow = smem_u32(buf) + (uint32_t)lane * 128;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                uint4 w4 = make_uint4(0u, 0u, 0u, 0u);
+                __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+                st_shared_v4(srow + (((uint32_t)q ^ (uint32_t)(lane & 7)) << 4), w4);
+              }
+              __syncwarp();
+              const int64_t row0 = (int64_t)mt * BM + quarter * 32;
+              const int nrow = (int)min((int64_t)32, p.M - row0);
+              const int64_t col = c0 + lane;
+              if (nrow > 0 && col < p.N) {
+                const uint32_t base = smem_u32(buf) + (uint32_t)((lane & 7) * 2);
+                const uint32_t qc = (uint32_t)(lane >> 3);
+                float s1 = 0.f, s2 = 0.f;
+                for (int r = 0; r < nrow; ++r) {
+                  unsigned short u;
+                  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(u) : "r"(base + r * 128 + ((qc ^ (uint32_t)(r & 7)) << 4)));
+                  const float x = __uint_as_float((uint32_t)u << 16);
+                  s1 += x;
+                  s2 = fmaf(x, x, s2);
+                }
+                const int64_t nblk = (p.M + 31) / 32;
+                float* cs = p.colstat + (int64_t)b * p.colstat_bs + ((int64_t)split * nblk + row0 / 32) * 2 * p.N + col;
+                cs[0] = s1;
+                cs[p.N] = s2;
+              }
+              __syncwarp();
+            }
           } else if constexpr (CONV == 5) {
             // merged phases: column 8 q + c of row (n, i, j) -> pixel (n, 2i + (q >> 1), 2j + (q & 1)), channel c
             if (row_ok) {
@@ -1042,7 +1077,10 @@ hfta_status launch_conv(const ConvTcP& cp, cudaStream_t s) {
   a.y_c = CONV == 5 ? 8 : (int)cp.N; a.y_h = cp.y_h; a.y_w = cp.y_w; a.y_bs = cp.c_bs;
   a.act = (CONV == 1 || CONV == 2 || CONV == 5) ? cp.act : HFTA_ACT_NONE; a.act_alpha = cp.act_alpha;
   a.ks = ks; a.cs = cs; a.cp = cpd; a.taps = ks * ks; a.wflip = cp.wflip;
-  if (CONV == 1 && !OUT_F32) { a.colstat = cp.colstat; a.colstat_bs = cdiv(cp.M, 32) * 2 * cp.N; }
+  if ((CONV == 1 || CONV == 2) && !OUT_F32) {
+    a.colstat = cp.colstat;
+    a.colstat_bs = (CONV == 2 ? 4 : 1) * cdiv(cp.M, 32) * 2 * cp.N;   // mode 2: 4 phases of M/32 blocks
+  }
   for (int t = 0; t < 64; ++t) {
     const int tt = t < a.taps ? t : 0;
     a.tkx[t] = (uint8_t)(tt % ks); a.tky[t] = (uint8_t)(tt / ks);

@@ -144,8 +144,10 @@ class FusedDCGAN:
         self.ws = ws
         # bf16: D's BN statistics come from the conv epilogues (HFTA_COLSTAT=0 disables)
         import os
-        self.colstat = (torch.empty(max(H.hfta_linear_colstat_size(B, N * dsz[i + 1] ** 2, dch[i + 1])
-                                        for i in (1, 2, 3)) // 4, dtype=torch.float32, device=dev)
+        self.colstat = (torch.empty(max([H.hfta_linear_colstat_size(B, N * dsz[i + 1] ** 2, dch[i + 1])
+                                         for i in (1, 2, 3)] +
+                                        [H.hfta_linear_colstat_size(B, N * gsz[i + 1] ** 2, gch[i + 1])
+                                         for i in range(4)]) // 4, dtype=torch.float32, device=dev)
                         if self.dt == H.HFTA_BF16 and os.environ.get("HFTA_COLSTAT", "1") != "0" else None)
 
     # -------------------------------------------------------- wrappers --
@@ -309,8 +311,14 @@ class FusedDCGAN:
         G = self.G
         x = H.tin(self.z, self.N * NZP, NZP)
         for i in range(4):
-            self._conv_fwd(G, "t%d.W" % (i + 1), self.gdesc[i], x, self.gy[i], s)
-            self._bn_fwd(G, "bn%d" % (i + 1), self.gy[i], H.ACT_RELU, 0.0, self.gh[i], s)
+            if self.colstat is not None:    # BN statistics from the sub-pixel epilogue (t1: one pass over y)
+                H.hfta_fused_conv_fwd_stats(self.B, self.gdesc[i], self.dt, x, self._win(G, "t%d.W" % (i + 1)),
+                                            self._out(self.gy[i]), H.ptr(self.colstat), self.ws.ptr, self.ws.nbytes,
+                                            s)
+                self._bn_fwd_colstat(G, "bn%d" % (i + 1), self.gy[i], H.ACT_RELU, 0.0, self.gh[i], s)
+            else:
+                self._conv_fwd(G, "t%d.W" % (i + 1), self.gdesc[i], x, self.gy[i], s)
+                self._bn_fwd(G, "bn%d" % (i + 1), self.gy[i], H.ACT_RELU, 0.0, self.gh[i], s)
             x = self._in(self.gh[i])
         # t5 has no BN: Tanh in the convolution's epilogue (fake = tanh(y))
         self._conv_fwd(G, "t5.W", self.gdesc[4], x, self.fake, s, H.ACT_TANH, 0.0)
