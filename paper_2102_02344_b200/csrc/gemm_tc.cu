@@ -122,6 +122,36 @@ __device__ __forceinline__ void tile_coords(uint32_t t, const TcArgs& p, int& mt
   if (sp == 1) { split = 0; b = (int)r; } else { split = (int)(r % sp); b = (int)(r / sp); }
 }
 
+// BN statistics of one staged 32-row block, lane = column: rows r at base + 128 r,
+// 16-B chunk qc ^ (r & 7) (SWIZZLE_128B staging); full blocks unrolled with 4
+// independent accumulator pairs (the loop-carried add chain was the epilogue's
+// critical path), ragged blocks (and the sub-pixel epilogue: register budget) row by row
+template <bool UNROLL>
+__device__ __forceinline__ void colstat_sum(uint32_t base, uint32_t qc, int nrow, float& s1, float& s2) {
+  if (UNROLL && nrow == 32) {
+    float a1[4] = {0.f, 0.f, 0.f, 0.f}, a2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      unsigned short u;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(u) : "r"(base + r * 128 + ((qc ^ (uint32_t)(r & 7)) << 4)));
+      const float x = __uint_as_float((uint32_t)u << 16);
+      a1[r & 3] += x;
+      a2[r & 3] = fmaf(x, x, a2[r & 3]);
+    }
+    s1 = (a1[0] + a1[1]) + (a1[2] + a1[3]);
+    s2 = (a2[0] + a2[1]) + (a2[2] + a2[3]);
+    return;
+  }
+  s1 = 0.f; s2 = 0.f;
+  for (int r = 0; r < nrow; ++r) {
+    unsigned short u;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(u) : "r"(base + r * 128 + ((qc ^ (uint32_t)(r & 7)) << 4)));
+    const float x = __uint_as_float((uint32_t)u << 16);
+    s1 += x;
+    s2 = fmaf(x, x, s2);
+  }
+}
+
 // BRES ("B resident", forward layers with K <= 128): the B operand (the
 // weight slice of one model / n-tile, <= 2 k-blocks) stays in shared memory
 // while the CTA sweeps consecutive m-tiles of the same (model, n-tile) --
@@ -508,22 +538,31 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       // per-(model, n-tile) bias / scale slices: reloaded only when the key
       // changes (BRES schedules sweep many m-tiles per key), loaded into
       // registers BEFORE the accumulator wait so the latency overlaps the MMAs
-      const bool vbias = p.bias && p.bias_div == 0;
-      const int64_t key = (int64_t)b * p.tiles_n + nt;
+      // row-grouped bias table (seg head g.c1: one row per cloud of bias_div rows): when this
+      // warp's 32 rows share one table row, that row is staged like a vector bias
+      int64_t tgrp = -1;
+      if (CONV == 0 && !OUT_F32 && p.bias && p.bias_div > 0) {
+        const int64_t w0 = (int64_t)mt * BM + quarter * 32;
+        const int64_t glo = w0 / p.bias_div, ghi = min(w0 + 31, p.M - 1) / p.bias_div;
+        if (glo == ghi) tgrp = glo;
+      }
+      const bool vbias = p.bias && (p.bias_div == 0 || tgrp >= 0);
+      const float* bsrc = p.bias ? p.bias + (int64_t)b * p.bias_bs + (tgrp >= 0 ? tgrp * p.bias_ld : 0) : nullptr;
+      const int64_t key = ((tgrp + 1) * p.B + b) * p.tiles_n + nt;
       const bool reload = key != cur_key;
       float bpre[BN / 32], spre[BN / 32];
       if (reload) {
 #pragma unroll
         for (int jj = 0; jj < BN / 32; ++jj) {
           const int64_t n = (int64_t)nt * BN + jj * 32 + lane;
-          bpre[jj] = (vbias && n < p.N) ? p.bias[(int64_t)b * p.bias_bs + n] : 0.f;
+          bpre[jj] = (vbias && n < p.N) ? bsrc[n] : 0.f;
           spre[jj] = (EPI == 1 && n < p.N) ? p.scale[(int64_t)b * p.scale_bs + n] : 0.f;
         }
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const float* brow = nullptr;       // per-row bias table (row-grouped bias only)
-      if (p.bias && p.bias_div > 0 && row_ok)
+      const float* brow = nullptr;       // per-row bias table (row-grouped bias, rows of 2 groups)
+      if (p.bias && p.bias_div > 0 && tgrp < 0 && row_ok)
         brow = p.bias + (int64_t)b * p.bias_bs + (m / p.bias_div) * p.bias_ld;
       if (reload) {                      // this warp's smem copies (broadcast reads later)
 #pragma unroll
@@ -735,14 +774,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               if (nrow > 0 && col < p.N) {
                 const uint32_t base = smem_u32(buf) + (uint32_t)((lane & 7) * 2);
                 const uint32_t qc = (uint32_t)(lane >> 3);
-                float s1 = 0.f, s2 = 0.f;
-                for (int r = 0; r < nrow; ++r) {
-                  unsigned short u;
-                  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(u) : "r"(base + r * 128 + ((qc ^ (uint32_t)(r & 7)) << 4)));
-                  const float x = __uint_as_float((uint32_t)u << 16);
-                  s1 += x;
-                  s2 = fmaf(x, x, s2);
-                }
+                float s1, s2;
+                colstat_sum<CONV != 2>(base, qc, nrow, s1, s2);
                 const int64_t nblk = (p.M + 31) / 32;
                 float* cs = p.colstat + (int64_t)b * p.colstat_bs + ((int64_t)split * nblk + row0 / 32) * 2 * p.N + col;
                 cs[0] = s1;
@@ -790,14 +823,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               if (nrow > 0 && col < p.N) {
                 const uint32_t base = smem_u32(buf) + (uint32_t)((lane & 7) * 2);
                 const uint32_t qc = (uint32_t)(hh * 4 + (lane >> 3));
-                float s1 = 0.f, s2 = 0.f;
-                for (int r = 0; r < nrow; ++r) {
-                  unsigned short u;
-                  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(u) : "r"(base + r * 128 + ((qc ^ (uint32_t)(r & 7)) << 4)));
-                  const float x = __uint_as_float((uint32_t)u << 16);
-                  s1 += x;
-                  s2 = fmaf(x, x, s2);
-                }
+                float s1, s2;
+                colstat_sum<true>(base, qc, nrow, s1, s2);
                 float* cs = p.colstat + (int64_t)b * p.colstat_bs + (row0 / 32) * 2 * p.N + col;
                 cs[0] = s1;
                 cs[p.N] = s2;
