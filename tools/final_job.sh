@@ -1,9 +1,9 @@
 # Round-2 final measurement job (one gpurun call): the bench line of every
 # workload (twice for the headline workloads: box-to-box spread), the
 # reference arm, ncu launch lists with tensor-pipe activity and DRAM bytes.
-# Outputs: gpurun_out/final6/.
+# Outputs: gpurun_out/final7/.
 set -x
-O=gpurun_out/final6
+O=gpurun_out/final7
 mkdir -p $O
 python bench.py > $O/bench_cls_bf16.json 2> $O/bench_cls_bf16.err
 python bench.py --no-serial --no-cpu-baseline > $O/bench_cls_bf16_b.json 2> $O/bench_cls_bf16_b.err
