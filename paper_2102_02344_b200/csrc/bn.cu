@@ -56,6 +56,9 @@ int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 int bn_run() { static int v = env_int("HFTA_BN_RUN", 128); return v; }
+// fewest rows one thread streams per chunk (small-R layers: blocks long enough
+// to amortise their setup and the partial merge)
+int bn_min_rows() { static int v = std::max(1, env_int("HFTA_BN_MINROWS", 8)); return v; }
 
 // run > 0: chunks short enough that one thread sums <= run rows (reductions);
 // run == 0: apply passes (no reduction, chunks sized for parallelism only)
@@ -68,7 +71,7 @@ Geo make_geo(int B, int64_t R, int64_t C, int vec, int bps = 0, int run = 0) {
   g.colgroups = (int)cdiv(C, g.cb);
   int64_t target = (int64_t)(bps > 0 ? bps : bn_blocks_per_sm()) * std::max(num_sms(), 148);
   int64_t chunks = std::max<int64_t>(1, target / ((int64_t)g.colgroups * B));
-  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, cdiv(R, (int64_t)g.rpb * 8)));
+  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, cdiv(R, (int64_t)g.rpb * bn_min_rows())));
   if (run > 0) chunks = std::max<int64_t>(chunks, cdiv(R, (int64_t)g.rpb * run));   // runs of <= run rows per thread
   g.rows_per_chunk = cdiv(cdiv(R, chunks), g.rpb) * g.rpb;
   g.chunks = (int)cdiv(R, g.rows_per_chunk);
