@@ -454,10 +454,11 @@ def main():
     ap.add_argument("--workload", default="pointnet_cls", choices=["pointnet_cls", "pointnet_seg", "dcgan", "resnet18"])
     args = ap.parse_args()
     if args.B is None:      # peak of the measured B sweep (throughput flat within 1% beyond it)
-        args.B = {("pointnet_cls", "bf16"): 256, ("pointnet_seg", "bf16"): 96, ("dcgan", "bf16"): 96,
+        # (final sweeps profiles/sweep_r02c_*.jsonl: seg flat 58-59k from B = 32 to 192,
+        # DCGAN 213k from 128, ResNet-18 705k at 512)
+        args.B = {("pointnet_cls", "bf16"): 256, ("pointnet_seg", "bf16"): 96, ("dcgan", "bf16"): 128,
                   ("pointnet_cls", "f32"): 64, ("pointnet_seg", "f32"): 64, ("dcgan", "f32"): 64,
-                  ("resnet18", "bf16"): 256, ("resnet18", "f32"): 128}[(args.workload,
-                                                                                                 args.dtype)]
+                  ("resnet18", "bf16"): 512, ("resnet18", "f32"): 128}[(args.workload, args.dtype)]
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
